@@ -1,0 +1,182 @@
+/* C-ABI of the B200-native Mixtera hot path (libmxb200.so).
+ *
+ * Plain pointers and sizes only: no torch or Python types cross this
+ * boundary. "device" arguments are CUDA device pointers on the current
+ * device, "host" arguments are ordinary host memory, `stream` is a
+ * cudaStream_t (NULL = legacy default stream). Every function returns an int
+ * status (MX_OK = 0, MX_EXHAUSTED = 1, negative = error); the message of the
+ * last error on the calling thread is mx_last_error().
+ *
+ * The reference (mixplane, pure Python) has no FFI: its seams are the Python
+ * duck types called from server.py. Each entry point below replaces one of
+ * them (reference file:line in brackets); INTEGRATION.md shows the ctypes
+ * binding a maintainer adds on the reference side.
+ *
+ * Error codes map to the reference's exception types (errors.py:4-45):
+ *   MX_ERR_QUERY -> QueryError, MX_ERR_INDEX -> IndexBuildError,
+ *   MX_ERR_MIXTURE -> MixtureError, MX_ERR_FEEDBACK -> FeedbackError,
+ *   MX_ERR_DATA -> DataReadError, MX_ERR_INVALID -> ValueError.
+ */
+#ifndef MIXTERA_B200_H
+#define MIXTERA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MX_OK 0
+#define MX_EXHAUSTED 1
+#define MX_ERR_CUDA (-1)
+#define MX_ERR_INVALID (-2)
+#define MX_ERR_QUERY (-3)
+#define MX_ERR_INDEX (-4)
+#define MX_ERR_MIXTURE (-5)
+#define MX_ERR_FEEDBACK (-6)
+#define MX_ERR_DATA (-7)
+#define MX_ERR_UNSUPPORTED (-8)
+
+#define MX_MAX_PROPS 16
+
+typedef struct mx_index mx_index;
+typedef struct mx_gen mx_gen;
+
+/* Last error message of the calling thread ("" when none). */
+const char* mx_last_error(void);
+/* ABI version; bumps on any signature change. */
+int mx_abi_version(void);
+
+/* ------------------------------------------------------------------ stage 1
+ * Columnar catalog + filter, encoded by the host (codec.py):
+ *   columns[p]   device int32[n_samples], property p in NAME order (-1 = null),
+ *                files concatenated in ascending file-id order;
+ *   lut          host uint32, property p occupies [lut_offsets[p], lut_offsets[p+1]):
+ *                entry (code+1) = packed-key contribution | 0x80000000 if the
+ *                code fails the conjunctive filter (catalog.py:459-511);
+ *   field_shift/field_width: bit position of property p's value-rank field;
+ *   key strings: piece (key_string_base[p] + rank - 1) is
+ *                escape(prop) ":" escape(v1) "," ... (mixtures.py:118-121).
+ */
+typedef struct mx_catalog_desc {
+  int32_t n_props;
+  const int32_t* const* columns;
+  const uint32_t* lut;
+  const int32_t* lut_offsets;
+  int64_t n_samples;
+  int32_t n_files;
+  const int64_t* file_offsets; /* device int64[n_files+1] */
+  const int32_t* file_ds;      /* host int32[n_files] */
+  const int64_t* file_ids;     /* host int64[n_files], ascending */
+  uint32_t key_bits;
+  uint32_t rank_mask;
+  const uint32_t* field_shift; /* host [n_props] */
+  const uint32_t* field_width; /* host [n_props] */
+  const uint8_t* key_strings;
+  const int64_t* key_string_offsets; /* host [n_pieces+1] */
+  const int32_t* key_string_base;    /* host [n_props] */
+} mx_catalog_desc;
+
+/* Fused filter + interval detection + index build
+ * [MetadataCatalog.filter_intervals catalog.py:549-605 + build_index
+ *  index.py:88-115, called from server.py:112-115]. Errors: MX_ERR_QUERY for
+ * an un-keyable (all-null) sample or an empty catalog. An empty result is a
+ * valid index with 0 keys (the server raises "matches no samples"). */
+int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out);
+int mx_index_free(mx_index* index);
+int mx_index_sizes(const mx_index* index, int64_t* n_keys, int64_t* n_blocks,
+                   int64_t* n_intervals, int64_t* n_samples);
+/* Realized component keys in MixtureKey.sort_key order [ChunkerIndex
+ * component_keys/key_sample_counts index.py:59-73]: host outputs [n_keys]. */
+int mx_index_export_keys(const mx_index* index, uint32_t* packed, int64_t* samples);
+/* Flat interval table in (key, dataset, file, start) order
+ * [ChunkerIndex._index index.py:50-55]: host outputs [n_intervals]. */
+int mx_index_export_intervals(const mx_index* index, uint32_t* key_rank, int32_t* ds,
+                              int64_t* file_id, uint32_t* start, uint32_t* end);
+
+/* ------------------------------------------------------------------ stage 2
+ * Generator = per-key RangeCursor layouts + seeded component order
+ * [ChunkGenerator.__init__ chunks.py:136-146, RangeCursor index.py:126-147].
+ * cursor_prefix = stable-hash message prefix for (job_seed, "cursor"),
+ * chunk_prefix  = prefix for (job_seed, "chunk") (seeding.py:18-33);
+ * order_seed    = derive_seed(job_seed, "component-order"). */
+int mx_gen_create(mx_index* index, const uint8_t* cursor_prefix, int32_t cursor_prefix_len,
+                  const uint8_t* chunk_prefix, int32_t chunk_prefix_len, uint64_t order_seed,
+                  void* stream, mx_gen** out);
+int mx_gen_free(mx_gen* gen);
+
+/* Mixture in force for the next plan [MixtureSpec mixtures.py:187-252].
+ * allow: host uint32 [n_mkeys][allow_words]; bit (allow_base[p] + r) of mixture
+ * key m says whether a component holding value-rank r (0 = null) of property p
+ * matches m on p (mixtures.py:100-109). weights: host double [n_mkeys] in
+ * MixtureKey.sort_key order. */
+typedef struct mx_mixture_desc {
+  int32_t n_mkeys;
+  const uint32_t* allow;
+  int32_t allow_words;
+  const int32_t* allow_base; /* host [n_props] */
+  const double* weights;
+  int64_t chunk_size;
+  int32_t strict;
+} mx_mixture_desc;
+
+/* Plan and emit up to max_chunks chunks under `mix`, exactly the sequence
+ * max_chunks calls of ChunkGenerator.generate(spec) would return
+ * [chunks.py:194-230, redistribute_best_effort :109-130, apportion
+ * mixtures.py:158-184]. n_out = chunks emitted; MX_EXHAUSTED when the plan
+ * ended with generate() returning None (report via mx_gen_report). */
+int mx_gen_plan(mx_gen* gen, const mx_mixture_desc* mix, int64_t max_chunks, int64_t* n_out);
+/* Same for generate_arbitrary(chunk_size) [chunks.py:232-253]. */
+int mx_gen_plan_arbitrary(mx_gen* gen, int64_t chunk_size, int64_t max_chunks, int64_t* n_out);
+/* Sizes of the last plan's result. */
+int mx_gen_result_sizes(const mx_gen* gen, int64_t* n_chunks, int64_t* n_ranges);
+/* Copy the last plan's chunks to host: chunk_offsets [n_chunks+1] (into the
+ * range arrays), chunk_ids / seeds [n_chunks], ranges [n_ranges] sorted per
+ * chunk by (mixture key, file, start), merged (chunks.py:169-192). `mkey` is
+ * the mixture-key index (or the component rank for arbitrary chunks). */
+int mx_gen_result_copy(const mx_gen* gen, int64_t* chunk_offsets, int64_t* chunk_ids, uint64_t* seeds,
+                       uint32_t* mkey, int32_t* ds, int64_t* file_id, uint32_t* start, uint32_t* end);
+/* Device views of the same result (valid until the next plan/free). */
+int mx_gen_result_device(const mx_gen* gen, const int64_t** chunk_offsets, const uint64_t** seeds,
+                         const uint32_t** mkey, const uint32_t** file_index, const uint32_t** start,
+                         const uint32_t** end);
+/* Shortfall report of the last generate() that returned None: host [n_mkeys]. */
+int mx_gen_report(const mx_gen* gen, int64_t* remaining);
+int mx_gen_next_chunk_id(const mx_gen* gen, int64_t* next_id);
+int mx_gen_set_next_chunk_id(mx_gen* gen, int64_t next_id);
+/* Cursor checkpoint form {pos, offset} per component rank
+ * [RangeCursor.state_dict/load_state index.py:180-189]: host [n_keys]. */
+int mx_gen_get_cursors(const mx_gen* gen, int64_t* pos, int64_t* offset);
+int mx_gen_set_cursors(mx_gen* gen, const int64_t* pos, const int64_t* offset);
+/* Component order as component ranks: host [n_keys]. */
+int mx_gen_component_order(const mx_gen* gen, uint32_t* order);
+/* RangeCursor._ranges of one component: host outputs sized by n_ranges. */
+int mx_gen_cursor_ranges(const mx_gen* gen, uint32_t comp, int64_t* n_ranges, int32_t* ds,
+                         int64_t* file_id, uint32_t* start, uint32_t* end, int64_t capacity);
+
+/* ------------------------------------------------------------------ stage 3
+ * Per-domain loss reduction [per_domain_loss client.py:582-598]: device
+ * f32 losses[n], int32 tags[n] in [0, n_domains) -> device f64 sums, int64
+ * counts [n_domains] (overwritten). MX_ERR_DATA on a tag out of range. */
+int mx_domain_loss(const float* losses, const int32_t* tags, int64_t n, int32_t n_domains,
+                   double* sums, int64_t* counts, void* stream);
+/* Batched power-law fit [fit_power_law ado.py:121-168]: domain d's points
+ * are [point_offsets[d], point_offsets[d+1]) of n[] / loss[] (device f64);
+ * geom: device f64[49] = numpy.geomspace(1e-6, 1, 49). out_law: device f64
+ * [n_domains][4] = (epsilon, beta, alpha, fallback). */
+int mx_fit_power_law(int32_t n_domains, const int64_t* point_offsets, const double* n,
+                     const double* loss, const double* geom, double* out_law, void* stream);
+/* ADO mixture update [AdoState.compute_pi/_floored ado.py:273-319]. Device
+ * f64 state vectors of length k: mu, credit, law (k x 4, NaN row = no law),
+ * pi_bar (in/out), pi (out). shared_n = _shared_n(t). Writes pi; advances
+ * pi_bar with count *pi_bar_count (device int64, incremented). */
+int mx_ado_pi(int32_t k, const double* mu, const double* credit, const double* law,
+              double shared_n, double p_min, double smoothing, double* pi_bar,
+              int64_t* pi_bar_count, double* pi, void* stream);
+/* credit <- (1 - rate) * credit + rate * pi [AdoState.record_step ado.py:241-243]. */
+int mx_ado_credit(int32_t k, double rate, const double* pi, double* credit, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MIXTERA_B200_H */

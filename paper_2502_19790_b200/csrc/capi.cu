@@ -1,0 +1,399 @@
+// C-ABI entry points (include/mixtera_b200.h): argument checks, handle
+// ownership, error strings, host<->device copies of small results.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "mixtera_internal.cuh"
+
+namespace mx {
+int domain_loss(const float* losses, const int32_t* tags, long long n, int K, double* sums, long long* counts,
+                cudaStream_t s);
+int fit_power_law(int D, const long long* off, const double* n, const double* loss, const double* geom, double* out,
+                  cudaStream_t s);
+int ado_pi(int k, const double* mu, const double* credit, const double* law, double n, double p_min, double smoothing,
+           double* pi_bar, long long* cnt, double* pi, cudaStream_t s);
+int ado_credit(int k, double rate, const double* pi, double* credit, cudaStream_t s);
+}  // namespace mx
+
+static thread_local std::string g_err;
+
+int mx_fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int mx_fail_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  return mx_fail(MX_ERR_CUDA, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e), cudaGetErrorString(e), what,
+                 file, line);
+}
+
+#define MX_CHECK_ARG(cond, msg)                          \
+  do {                                                   \
+    if (!(cond)) return mx_fail(MX_ERR_INVALID, "%s", msg); \
+  } while (0)
+
+using namespace mx;
+
+extern "C" {
+
+const char* mx_last_error(void) { return g_err.c_str(); }
+int mx_abi_version(void) { return 1; }
+
+int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out) {
+  MX_CHECK_ARG(desc && out, "null argument");
+  g_err.clear();
+  cudaStream_t s = (cudaStream_t)stream;
+  mx_index* ix = new mx_index();
+  ix->d.stream = s;
+  IndexData& d = ix->d;
+  d.n_props = desc->n_props;
+  for (int p = 0; p < desc->n_props && p < MX_MAX_PROPS; ++p) {
+    d.field_shift[p] = desc->field_shift[p];
+    d.field_width[p] = desc->field_width[p];
+    d.str_base[p] = desc->key_string_base[p];
+  }
+  int rc = MX_OK;
+  // key strings for device BLAKE2b
+  {
+    int n_pieces = 0;
+    for (int p = 0; p < desc->n_props && p < MX_MAX_PROPS; ++p) {
+      int card = (desc->lut_offsets[p + 1] - desc->lut_offsets[p]) - 1;
+      n_pieces = std::max(n_pieces, desc->key_string_base[p] + card);
+    }
+    const long long nbytes = desc->key_string_offsets[n_pieces];
+    cudaError_t e = d.str_off.alloc(n_pieces + 1, s);
+    if (e == cudaSuccess) e = d.str_bytes.alloc(nbytes > 0 ? nbytes : 1, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(d.str_off.p, desc->key_string_offsets, sizeof(long long) * (n_pieces + 1),
+                          cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && nbytes > 0)
+      e = cudaMemcpyAsync(d.str_bytes.p, desc->key_strings, nbytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) rc = mx_fail_cuda(e, "key strings", __FILE__, __LINE__);
+  }
+  if (rc == MX_OK) rc = stage1_build(desc, s, &d);
+  if (rc < 0) {
+    delete ix;
+    return rc;
+  }
+  *out = ix;
+  return MX_OK;
+}
+
+int mx_index_free(mx_index* index) {
+  if (!index) return MX_OK;
+  cudaStream_t s = index->d.stream;
+  delete index;
+  cudaStreamSynchronize(s);
+  return MX_OK;
+}
+
+int mx_index_sizes(const mx_index* index, int64_t* n_keys, int64_t* n_blocks, int64_t* n_intervals,
+                   int64_t* n_samples) {
+  MX_CHECK_ARG(index, "null index");
+  const IndexData& d = index->d;
+  if (n_keys) *n_keys = d.n_keys;
+  if (n_blocks) *n_blocks = d.n_blocks;
+  if (n_intervals) *n_intervals = d.n_intervals;
+  if (n_samples) {
+    unsigned long long t = 0;
+    if (d.n_intervals > 0) {
+      cudaError_t e = cudaMemcpy(&t, d.iv_cum.p + d.n_intervals, sizeof(t), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return mx_fail_cuda(e, "sizes", __FILE__, __LINE__);
+    }
+    *n_samples = (int64_t)t;
+  }
+  return MX_OK;
+}
+
+int mx_index_export_keys(const mx_index* index, uint32_t* packed, int64_t* samples) {
+  MX_CHECK_ARG(index, "null index");
+  const IndexData& d = index->d;
+  const long long K = d.n_keys;
+  if (K == 0) return MX_OK;
+  std::vector<u32> kbf(K + 1), bf(d.n_blocks + 1);
+  std::vector<unsigned long long> cum(d.n_intervals + 1);
+  cudaError_t e = cudaMemcpy(kbf.data(), d.key_blk_first.p, sizeof(u32) * (K + 1), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(bf.data(), d.blk_first.p, sizeof(u32) * (d.n_blocks + 1), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(cum.data(), d.iv_cum.p, sizeof(u64) * (d.n_intervals + 1), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && packed) e = cudaMemcpy(packed, d.key_packed.p, sizeof(u32) * K, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "export keys", __FILE__, __LINE__);
+  if (samples)
+    for (long long k = 0; k < K; ++k) samples[k] = (int64_t)(cum[bf[kbf[k + 1]]] - cum[bf[kbf[k]]]);
+  return MX_OK;
+}
+
+int mx_index_export_intervals(const mx_index* index, uint32_t* key_rank, int32_t* ds, int64_t* file_id,
+                              uint32_t* start, uint32_t* end) {
+  MX_CHECK_ARG(index, "null index");
+  const IndexData& d = index->d;
+  const long long I = d.n_intervals;
+  if (I == 0) return MX_OK;
+  std::vector<u32> f(I), bk(d.n_blocks), bf(d.n_blocks + 1);
+  cudaError_t e = cudaMemcpy(f.data(), d.iv_file.p, sizeof(u32) * I, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && start) e = cudaMemcpy(start, d.iv_start.p, sizeof(u32) * I, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && end) e = cudaMemcpy(end, d.iv_end.p, sizeof(u32) * I, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(bk.data(), d.blk_key.p, sizeof(u32) * d.n_blocks, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(bf.data(), d.blk_first.p, sizeof(u32) * (d.n_blocks + 1), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "export intervals", __FILE__, __LINE__);
+  for (long long b = 0; b < d.n_blocks; ++b)
+    for (u32 i = bf[b]; i < bf[b + 1]; ++i)
+      if (key_rank) key_rank[i] = bk[b];
+  for (long long i = 0; i < I; ++i) {
+    if (ds) ds[i] = d.h_file_ds[f[i]];
+    if (file_id) file_id[i] = d.h_file_ids[f[i]];
+  }
+  return MX_OK;
+}
+
+int mx_gen_create(mx_index* index, const uint8_t* cursor_prefix, int32_t cursor_prefix_len, const uint8_t* chunk_prefix,
+                  int32_t chunk_prefix_len, uint64_t order_seed, void* stream, mx_gen** out) {
+  MX_CHECK_ARG(index && out, "null argument");
+  g_err.clear();
+  cudaStream_t s = (cudaStream_t)stream;
+  mx_gen* g = new mx_gen();
+  int rc = MX_OK;
+  cudaError_t e = g->d.chunk_prefix.alloc(chunk_prefix_len > 0 ? chunk_prefix_len : 1, s);
+  if (e == cudaSuccess && chunk_prefix_len > 0)
+    e = cudaMemcpyAsync(g->d.chunk_prefix.p, chunk_prefix, chunk_prefix_len, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) rc = mx_fail_cuda(e, "chunk prefix", __FILE__, __LINE__);
+  g->d.chunk_prefix_len = chunk_prefix_len;
+  if (rc == MX_OK) rc = cursor_build(&index->d, cursor_prefix, cursor_prefix_len, order_seed, s, &g->d);
+  if (rc < 0) {
+    delete g;
+    return rc;
+  }
+  *out = g;
+  return MX_OK;
+}
+
+int mx_gen_free(mx_gen* gen) {
+  if (!gen) return MX_OK;
+  cudaStream_t s = gen->d.stream;
+  delete gen;
+  cudaStreamSynchronize(s);
+  return MX_OK;
+}
+
+int mx_gen_plan(mx_gen* gen, const mx_mixture_desc* mix, int64_t max_chunks, int64_t* n_out) {
+  MX_CHECK_ARG(gen && mix && n_out, "null argument");
+  MX_CHECK_ARG(max_chunks >= 1, "max_chunks must be >= 1");
+  g_err.clear();
+  long long n = 0;
+  int rc = plan_mixture(&gen->d, mix, max_chunks, &n);
+  *n_out = n;
+  return rc;
+}
+
+int mx_gen_plan_arbitrary(mx_gen* gen, int64_t chunk_size, int64_t max_chunks, int64_t* n_out) {
+  MX_CHECK_ARG(gen && n_out, "null argument");
+  MX_CHECK_ARG(max_chunks >= 1, "max_chunks must be >= 1");
+  g_err.clear();
+  long long n = 0;
+  int rc = plan_arbitrary(&gen->d, chunk_size, max_chunks, &n);
+  *n_out = n;
+  return rc;
+}
+
+int mx_gen_result_sizes(const mx_gen* gen, int64_t* n_chunks, int64_t* n_ranges) {
+  MX_CHECK_ARG(gen, "null generator");
+  if (n_chunks) *n_chunks = gen->d.res_chunks;
+  if (n_ranges) *n_ranges = gen->d.res_ranges;
+  return MX_OK;
+}
+
+int mx_gen_result_copy(const mx_gen* gen, int64_t* chunk_offsets, int64_t* chunk_ids, uint64_t* seeds, uint32_t* mkey,
+                       int32_t* ds, int64_t* file_id, uint32_t* start, uint32_t* end) {
+  MX_CHECK_ARG(gen, "null generator");
+  const GenData& g = gen->d;
+  const long long C = g.res_chunks, R = g.res_ranges;
+  cudaStream_t s = g.stream;
+  cudaError_t e = cudaSuccess;
+  if (chunk_offsets) e = cudaMemcpyAsync(chunk_offsets, g.res_off.p, sizeof(long long) * (C + 1), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && chunk_ids && C)
+    e = cudaMemcpyAsync(chunk_ids, g.res_id.p, sizeof(long long) * C, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && seeds && C) e = cudaMemcpyAsync(seeds, (const void*)g.res_seed.p, sizeof(u64) * C, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && mkey && R) e = cudaMemcpyAsync(mkey, g.res_mkey.p, sizeof(u32) * R, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && start && R) e = cudaMemcpyAsync(start, g.res_start.p, sizeof(u32) * R, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && end && R) e = cudaMemcpyAsync(end, g.res_end.p, sizeof(u32) * R, cudaMemcpyDeviceToHost, s);
+  std::vector<u32> f;
+  if (e == cudaSuccess && R && (ds || file_id)) {
+    f.resize(R);
+    e = cudaMemcpyAsync(f.data(), g.res_file.p, sizeof(u32) * R, cudaMemcpyDeviceToHost, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "result copy", __FILE__, __LINE__);
+  if (!f.empty())
+    for (long long i = 0; i < R; ++i) {
+      if (ds) ds[i] = g.ix->h_file_ds[f[i]];
+      if (file_id) file_id[i] = g.ix->h_file_ids[f[i]];
+    }
+  return MX_OK;
+}
+
+int mx_gen_result_device(const mx_gen* gen, const int64_t** chunk_offsets, const uint64_t** seeds,
+                         const uint32_t** mkey, const uint32_t** file_index, const uint32_t** start,
+                         const uint32_t** end) {
+  MX_CHECK_ARG(gen, "null generator");
+  const GenData& g = gen->d;
+  if (chunk_offsets) *chunk_offsets = reinterpret_cast<const int64_t*>(g.res_off.p);
+  if (seeds) *seeds = reinterpret_cast<const uint64_t*>(g.res_seed.p);
+  if (mkey) *mkey = g.res_mkey.p;
+  if (file_index) *file_index = g.res_file.p;
+  if (start) *start = g.res_start.p;
+  if (end) *end = g.res_end.p;
+  return MX_OK;
+}
+
+int mx_gen_report(const mx_gen* gen, int64_t* remaining) {
+  MX_CHECK_ARG(gen && remaining, "null argument");
+  for (size_t i = 0; i < gen->d.report.size(); ++i) remaining[i] = gen->d.report[i];
+  return MX_OK;
+}
+
+int mx_gen_next_chunk_id(const mx_gen* gen, int64_t* next_id) {
+  MX_CHECK_ARG(gen && next_id, "null argument");
+  *next_id = gen->d.next_chunk_id;
+  return MX_OK;
+}
+
+int mx_gen_set_next_chunk_id(mx_gen* gen, int64_t next_id) {
+  MX_CHECK_ARG(gen && next_id >= 0, "bad argument");
+  gen->d.next_chunk_id = next_id;
+  return MX_OK;
+}
+
+// consumed <-> {pos, offset}: pos = #cursor ranges fully consumed
+static int cursor_tables(const GenData& g, std::vector<u32>& kbf, std::vector<u32>& bf,
+                         std::vector<unsigned long long>& ccum) {
+  const IndexData& d = *g.ix;
+  kbf.resize(d.n_keys + 1);
+  bf.resize(d.n_blocks + 1);
+  ccum.resize(d.n_intervals + 1);
+  cudaError_t e = cudaMemcpy(kbf.data(), d.key_blk_first.p, sizeof(u32) * kbf.size(), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(bf.data(), d.blk_first.p, sizeof(u32) * bf.size(), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && d.n_intervals)
+    e = cudaMemcpy(ccum.data(), g.ccum.p, sizeof(u64) * ccum.size(), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "cursor tables", __FILE__, __LINE__);
+  return MX_OK;
+}
+
+int mx_gen_get_cursors(const mx_gen* gen, int64_t* pos, int64_t* offset) {
+  MX_CHECK_ARG(gen && pos && offset, "null argument");
+  const GenData& g = gen->d;
+  const long long K = g.K;
+  if (K == 0) return MX_OK;
+  std::vector<u32> kbf, bf;
+  std::vector<unsigned long long> ccum, used(K);
+  int rc = cursor_tables(g, kbf, bf, ccum);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpy(used.data(), g.consumed.p, sizeof(u64) * K, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "cursors", __FILE__, __LINE__);
+  for (long long k = 0; k < K; ++k) {
+    const long long ib = bf[kbf[k]], ie = bf[kbf[k + 1]];
+    const unsigned long long base = ccum[ib];
+    // number of ranges whose end <= used
+    long long lo = ib, hi = ie;
+    while (lo < hi) {
+      long long mid = (lo + hi) / 2;
+      if (ccum[mid + 1] - base <= used[k]) lo = mid + 1; else hi = mid;
+    }
+    pos[k] = lo - ib;
+    offset[k] = (int64_t)(used[k] - (ccum[lo] - base));
+  }
+  return MX_OK;
+}
+
+int mx_gen_set_cursors(mx_gen* gen, const int64_t* pos, const int64_t* offset) {
+  MX_CHECK_ARG(gen && pos && offset, "null argument");
+  GenData& g = gen->d;
+  const long long K = g.K;
+  if (K == 0) return MX_OK;
+  std::vector<u32> kbf, bf;
+  std::vector<unsigned long long> ccum, used(K);
+  int rc = cursor_tables(g, kbf, bf, ccum);
+  if (rc) return rc;
+  for (long long k = 0; k < K; ++k) {
+    const long long ib = bf[kbf[k]], ie = bf[kbf[k + 1]];
+    if (pos[k] < 0 || pos[k] > ie - ib || offset[k] < 0)
+      return mx_fail(MX_ERR_INVALID, "cursor state out of range for component %lld", k);
+    used[k] = ccum[ib + pos[k]] - ccum[ib] + (unsigned long long)offset[k];
+    if (used[k] > ccum[ie] - ccum[ib]) return mx_fail(MX_ERR_INVALID, "cursor offset beyond component %lld", k);
+  }
+  cudaError_t e = cudaMemcpy(g.consumed.p, used.data(), sizeof(u64) * K, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "set cursors", __FILE__, __LINE__);
+  return MX_OK;
+}
+
+int mx_gen_component_order(const mx_gen* gen, uint32_t* order) {
+  MX_CHECK_ARG(gen && order, "null argument");
+  memcpy(order, gen->d.h_comp_order.data(), sizeof(u32) * gen->d.K);
+  return MX_OK;
+}
+
+int mx_gen_cursor_ranges(const mx_gen* gen, uint32_t comp, int64_t* n_ranges, int32_t* ds, int64_t* file_id,
+                         uint32_t* start, uint32_t* end, int64_t capacity) {
+  MX_CHECK_ARG(gen && n_ranges, "null argument");
+  const GenData& g = gen->d;
+  const IndexData& d = *g.ix;
+  if ((long long)comp >= g.K) return mx_fail(MX_ERR_INVALID, "component %u out of range", comp);
+  u32 kb[2], ib, ie;
+  cudaError_t e = cudaMemcpy(kb, d.key_blk_first.p + comp, sizeof(u32) * 2, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&ib, d.blk_first.p + kb[0], sizeof(u32), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&ie, d.blk_first.p + kb[1], sizeof(u32), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "cursor ranges", __FILE__, __LINE__);
+  const long long n = ie - ib;
+  *n_ranges = n;
+  if (!ds && !file_id && !start && !end) return MX_OK;
+  if (capacity < n) return mx_fail(MX_ERR_INVALID, "capacity %lld < %lld ranges", (long long)capacity, n);
+  std::vector<u32> civ(n), f(d.n_intervals), s0(d.n_intervals), e0(d.n_intervals);
+  e = cudaMemcpy(civ.data(), g.civ.p + ib, sizeof(u32) * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(f.data(), d.iv_file.p, sizeof(u32) * d.n_intervals, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(s0.data(), d.iv_start.p, sizeof(u32) * d.n_intervals, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(e0.data(), d.iv_end.p, sizeof(u32) * d.n_intervals, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "cursor ranges", __FILE__, __LINE__);
+  for (long long i = 0; i < n; ++i) {
+    u32 iv = civ[i];
+    if (ds) ds[i] = d.h_file_ds[f[iv]];
+    if (file_id) file_id[i] = d.h_file_ids[f[iv]];
+    if (start) start[i] = s0[iv];
+    if (end) end[i] = e0[iv];
+  }
+  return MX_OK;
+}
+
+int mx_domain_loss(const float* losses, const int32_t* tags, int64_t n, int32_t n_domains, double* sums,
+                   int64_t* counts, void* stream) {
+  MX_CHECK_ARG(n >= 0, "negative length");
+  MX_CHECK_ARG(sums && counts, "null output");
+  g_err.clear();
+  return domain_loss(losses, tags, n, n_domains, sums, reinterpret_cast<long long*>(counts), (cudaStream_t)stream);
+}
+
+int mx_fit_power_law(int32_t n_domains, const int64_t* point_offsets, const double* n, const double* loss,
+                     const double* geom, double* out_law, void* stream) {
+  g_err.clear();
+  return fit_power_law(n_domains, reinterpret_cast<const long long*>(point_offsets), n, loss, geom, out_law,
+                       (cudaStream_t)stream);
+}
+
+int mx_ado_pi(int32_t k, const double* mu, const double* credit, const double* law, double shared_n, double p_min,
+              double smoothing, double* pi_bar, int64_t* pi_bar_count, double* pi, void* stream) {
+  g_err.clear();
+  return ado_pi(k, mu, credit, law, shared_n, p_min, smoothing, pi_bar, reinterpret_cast<long long*>(pi_bar_count), pi,
+                (cudaStream_t)stream);
+}
+
+int mx_ado_credit(int32_t k, double rate, const double* pi, double* credit, void* stream) {
+  g_err.clear();
+  return ado_credit(k, rate, pi, credit, (cudaStream_t)stream);
+}
+
+}  // extern "C"

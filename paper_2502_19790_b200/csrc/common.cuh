@@ -1,0 +1,116 @@
+// Shared device utilities for the sm_100a Mixtera hot path.
+//
+// * warp primitives (inclusive scans, sums),
+// * decoupled look-back for single-pass device-wide prefix sums (stage-1
+//   run compaction and the index scans),
+// * streaming 128-bit loads that bypass L1 (column tiles are touched once),
+// * an error channel: kernels report typed failures through a small device
+//   struct the host reads after the launch sequence (mapped to the
+//   reference's exception types by capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define MX_FULL 0xffffffffu
+
+namespace mx {
+
+typedef unsigned long long u64;
+typedef uint32_t u32;
+
+__device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ int ld_stream(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ u64 ld_acquire(const u64* p) {
+  u64 r;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+  return r;
+}
+
+__device__ __forceinline__ void st_release(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T o = __shfl_up_sync(MX_FULL, v, d);
+    if (lane >= d) v += o;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(MX_FULL, v, d);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back (single pass scan). One 64-bit status word per tile:
+// bits 63..62 = flag (0 = not ready, 1 = tile aggregate, 2 = inclusive
+// prefix), bits 61..0 = value. Tiles take ids from an atomic counter so every
+// predecessor of a tile has already been scheduled (forward progress).
+// ---------------------------------------------------------------------------
+constexpr u64 LB_AGG = 1ull << 62;
+constexpr u64 LB_PREFIX = 2ull << 62;
+constexpr u64 LB_VALUE = (1ull << 62) - 1;
+
+// Called by ALL lanes of ONE warp. Returns the exclusive prefix of `tile`.
+__device__ __forceinline__ u64 lookback_exclusive(u64* status, int tile, u64 aggregate) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_release(status, LB_PREFIX | aggregate);
+    return 0;
+  }
+  if (lane == 0) st_release(status + tile, LB_AGG | aggregate);
+  u64 excl = 0;
+  int base = tile - 1;
+  while (true) {
+    const int idx = base - lane;
+    u64 w = idx >= 0 ? ld_acquire(status + idx) : LB_PREFIX;
+    const u64 flag = w & ~LB_VALUE;
+    if (__any_sync(MX_FULL, flag == 0)) continue;  // a predecessor is still running
+    const u32 pm = __ballot_sync(MX_FULL, flag == LB_PREFIX);
+    const int first = pm ? __ffs(pm) - 1 : 32;
+    u64 v = lane <= first ? (w & LB_VALUE) : 0;
+    excl += warp_sum(v);
+    if (pm) break;
+    base -= 32;
+  }
+  if (lane == 0) st_release(status + tile, LB_PREFIX | (excl + aggregate));
+  return excl;
+}
+
+// Device-side error record (first failure wins per field).
+struct DevError {
+  u64 null_key_sample;  // min global sample index of an un-keyable run (~0 = none)
+  u32 overlap;          // non-zero: overlapping/empty interval detected
+  u32 pad;
+};
+
+}  // namespace mx
+
+#define MX_CUDA_TRY(expr)                                   \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return ::mx_fail_cuda(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+int mx_fail_cuda(cudaError_t e, const char* what, const char* file, int line);
+int mx_fail(int code, const char* fmt, ...);

@@ -1,0 +1,276 @@
+// Generator setup: RangeCursor layouts + component order, on device.
+//
+// Reference: RangeCursor.__init__ (index.py:126-147) -- per component key,
+//   rng = Random(derive_seed(seed, "cursor", key.canonical_string()))
+//   shuffle the sorted dataset ids, then each dataset's sorted file ids (same
+//   rng), concatenate each file's intervals ascending;
+// ChunkGenerator.__init__ (chunks.py:139-141) -- component keys in sort order
+//   shuffled by Random(derive_seed(seed, "component-order")).
+//
+// Kernels: key_seed_kernel (device BLAKE2b of each key's canonical string),
+// cursor_shuffle_kernel (one warp per key; MT19937 state and the key's block
+// list staged in shared memory, the sequential Fisher-Yates run by one lane),
+// cursor_intervals_kernel (expand shuffled blocks to interval ids, warp scan),
+// cum_len_kernel (u64 look-back scan of lengths in cursor order),
+// component_order_kernel (one shuffle of K ranks).
+#include "blake2b.cuh"
+#include "common.cuh"
+#include "mixtera_internal.cuh"
+#include "mt19937.cuh"
+
+namespace mx {
+
+struct KeyStrView {
+  const u32* key_packed;
+  int n_props;
+  u32 shift[MX_MAX_PROPS];
+  u32 width[MX_MAX_PROPS];
+  int32_t base[MX_MAX_PROPS];
+  const uint8_t* bytes;
+  const long long* off;
+};
+
+__global__ void key_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix, int prefix_len, u64* seeds) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const u32 packed = v.key_packed[k];
+  long long len = 0;
+  int present = 0;
+  for (int p = 0; p < v.n_props; ++p) {
+    u32 r = (packed >> v.shift[p]) & ((1u << v.width[p]) - 1u);
+    if (r) {
+      long long pc = v.base[p] + r - 1;
+      len += v.off[pc + 1] - v.off[pc] + (present ? 1 : 0);
+      ++present;
+    }
+  }
+  Blake2b b;
+  b.init();
+  b.bytes(prefix, prefix_len);
+  b.len8((u64)len);
+  present = 0;
+  for (int p = 0; p < v.n_props; ++p) {
+    u32 r = (packed >> v.shift[p]) & ((1u << v.width[p]) - 1u);
+    if (r) {
+      if (present) b.byte(';');
+      long long pc = v.base[p] + r - 1;
+      b.bytes(v.bytes + v.off[pc], v.off[pc + 1] - v.off[pc]);
+      ++present;
+    }
+  }
+  seeds[k] = b.seed63();
+}
+
+constexpr int CS_WARPS = 4;
+constexpr int CS_LCAP = 2048;
+
+__global__ void __launch_bounds__(CS_WARPS * 32)
+cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file, const int32_t* file_ds,
+                      const u64* seeds, u32* grp, u32* gid, u32* cur_blk) {
+  __shared__ u32 s_mt[CS_WARPS][MT_N];
+  __shared__ u32 s_list[CS_WARPS][CS_LCAP];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long k = blockIdx.x * (long long)CS_WARPS + w; k < K; k += (long long)gridDim.x * CS_WARPS) {
+    const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
+    const int nb = (int)(b1 - b0);
+    const bool in_smem = nb <= CS_LCAP;
+    u32* work = in_smem ? s_list[w] : cur_blk + b0;
+    if (lane == 0) {
+      MT mt;
+      mt.s = s_mt[w];
+      mt.seed_u64(seeds[k]);
+      // dataset groups (blocks are file-sorted and ds is nondecreasing in file order)
+      int G = 0;
+      int prev = -1;
+      for (int b = 0; b < nb; ++b) {
+        int ds = file_ds[blk_file[b0 + b]];
+        if (b == 0 || ds != prev) {
+          grp[b0 + G] = (u32)b;
+          gid[b0 + G] = (u32)G;
+          ++G;
+        }
+        prev = ds;
+      }
+      mt.shuffle(gid + b0, G);
+      int pos = 0;
+      for (int g = 0; g < G; ++g) {
+        const u32 gi = gid[b0 + g];
+        const int s = (int)grp[b0 + gi];
+        const int e = gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
+        for (int b = s; b < e; ++b) work[pos + b - s] = b0 + (u32)b;
+        mt.shuffle(work + pos, e - s);
+        pos += e - s;
+      }
+    }
+    __syncwarp();
+    if (in_smem)
+      for (int i = lane; i < nb; i += 32) cur_blk[b0 + i] = s_list[w][i];
+    __syncwarp();
+  }
+}
+
+// civ: interval ids in cursor order; key k keeps its sorted-order index range
+__global__ void __launch_bounds__(256)
+cursor_intervals_kernel(long long K, const u32* key_blk_first, const u32* blk_first, const u32* cur_blk, u32* civ) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  for (long long k = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5); k < K; k += warps) {
+    const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
+    u32 out = blk_first[b0];
+    for (u32 pos = b0; pos < b1; pos += 32) {
+      const u32 my = pos + lane;
+      u32 blk = 0, cnt = 0;
+      if (my < b1) {
+        blk = cur_blk[my];
+        cnt = blk_first[blk + 1] - blk_first[blk];
+      }
+      u32 inc = warp_incl_scan(cnt);
+      u32 dst = out + inc - cnt;
+      for (u32 t = 0; t < cnt; ++t) civ[dst + t] = blk_first[blk] + t;
+      out += __shfl_sync(MX_FULL, inc, 31);
+    }
+  }
+}
+
+constexpr int CL_THREADS = 256;
+constexpr int CL_ITEMS = 8;
+constexpr int CL_TILE = CL_THREADS * CL_ITEMS;
+
+// cum[j+1] = sum of lengths of intervals perm[0..j] (perm = civ)
+__global__ void __launch_bounds__(CL_THREADS)
+cum_len_kernel(const u32* perm, const u32* start, const u32* end, long long n, u64* status, u32* tile_ctr, u64* cum) {
+  __shared__ u64 s_w[CL_THREADS / 32 + 1];
+  __shared__ int s_tile;
+  __shared__ u64 s_excl;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const long long b = (long long)tile * CL_TILE + threadIdx.x * CL_ITEMS;
+  u64 v[CL_ITEMS], sum = 0;
+#pragma unroll
+  for (int q = 0; q < CL_ITEMS; ++q) {
+    long long i = b + q;
+    u64 l = 0;
+    if (i < n) {
+      u32 iv = perm[i];
+      l = end[iv] - start[iv];
+    }
+    v[q] = l;
+    sum += l;
+  }
+  u64 inc = warp_incl_scan(sum);
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    u64 x = lane < CL_THREADS / 32 ? s_w[lane] : 0;
+    u64 xi = warp_incl_scan(x);
+    if (lane < CL_THREADS / 32) s_w[lane] = xi - x;
+    u64 tot = __shfl_sync(MX_FULL, xi, 31);
+    u64 t = lookback_exclusive(status, tile, tot);
+    if (lane == 0) s_excl = t;
+  }
+  __syncthreads();
+  u64 run = s_excl + s_w[warp] + inc - sum;
+  if (tile == 0 && threadIdx.x == 0) cum[0] = 0;
+#pragma unroll
+  for (int q = 0; q < CL_ITEMS; ++q) {
+    long long i = b + q;
+    run += v[q];
+    if (i < n) cum[i + 1] = run;
+  }
+}
+
+__global__ void comp_total_kernel(long long K, const u32* key_blk_first, const u32* blk_first, const u64* iv_cum,
+                                  u64* total) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  total[k] = iv_cum[blk_first[key_blk_first[k + 1]]] - iv_cum[blk_first[key_blk_first[k]]];
+}
+
+constexpr int CO_SMEM = 8192;
+
+__global__ void component_order_kernel(long long K, u64 seed, u32* order) {
+  __shared__ u32 s_mt[MT_N];
+  __shared__ u32 s_ord[CO_SMEM];
+  if (threadIdx.x != 0) return;
+  MT mt;
+  mt.s = s_mt;
+  mt.seed_u64(seed);
+  u32* x = K <= CO_SMEM ? s_ord : order;
+  for (long long i = 0; i < K; ++i) x[i] = (u32)i;
+  mt.shuffle(x, (int)K);
+  if (x != order)
+    for (long long i = 0; i < K; ++i) order[i] = x[i];
+}
+
+int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, unsigned long long order_seed,
+                 cudaStream_t s, GenData* g) {
+  g->ix = ix;
+  g->stream = s;
+  const long long K = ix->n_keys, B = ix->n_blocks, I = ix->n_intervals;
+  g->K = K;
+  MX_CUDA_TRY(g->consumed.alloc(K > 0 ? K : 1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(g->consumed.p, 0, sizeof(u64) * (K > 0 ? K : 1), s));
+  if (K == 0) return MX_OK;
+  DevBuf<uint8_t> pre;
+  DevBuf<u64> seeds;
+  MX_CUDA_TRY(pre.alloc(prefix_len > 0 ? prefix_len : 1, s));
+  if (prefix_len > 0)
+    MX_CUDA_TRY(cudaMemcpyAsync(pre.p, cursor_prefix, prefix_len, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(seeds.alloc(K, s));
+  KeyStrView v{};
+  v.key_packed = ix->key_packed.p;
+  v.n_props = ix->n_props;
+  for (int p = 0; p < ix->n_props; ++p) {
+    v.shift[p] = ix->field_shift[p];
+    v.width[p] = ix->field_width[p];
+    v.base[p] = ix->str_base[p];
+  }
+  v.bytes = ix->str_bytes.p;
+  v.off = ix->str_off.p;
+  key_seed_kernel<<<(unsigned)((K + 127) / 128), 128, 0, s>>>(v, K, pre.p, prefix_len, seeds.p);
+  DevBuf<u32> grp, gid;
+  MX_CUDA_TRY(grp.alloc(B, s));
+  MX_CUDA_TRY(gid.alloc(B, s));
+  MX_CUDA_TRY(g->cur_blk.alloc(B, s));
+  {
+    long long blocks = (K + CS_WARPS - 1) / CS_WARPS;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    cursor_shuffle_kernel<<<(unsigned)blocks, CS_WARPS * 32, 0, s>>>(K, ix->key_blk_first.p, ix->blk_file.p,
+                                                                   ix->file_ds.p, seeds.p, grp.p, gid.p,
+                                                                   g->cur_blk.p);
+  }
+  MX_CUDA_TRY(g->civ.alloc(I, s));
+  {
+    long long blocks = (K + 7) / 8;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    cursor_intervals_kernel<<<(unsigned)blocks, 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
+                                                            g->cur_blk.p, g->civ.p);
+  }
+  MX_CUDA_TRY(g->ccum.alloc(I + 1, s));
+  {
+    const int tiles = (int)((I + CL_TILE - 1) / CL_TILE);
+    DevBuf<u64> st;
+    DevBuf<u32> ctr;
+    MX_CUDA_TRY(st.alloc(tiles, s));
+    MX_CUDA_TRY(ctr.alloc(1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(st.p, 0, sizeof(u64) * tiles, s));
+    MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32), s));
+    cum_len_kernel<<<tiles, CL_THREADS, 0, s>>>(g->civ.p, ix->iv_start.p, ix->iv_end.p, I, st.p, ctr.p, g->ccum.p);
+  }
+  MX_CUDA_TRY(g->comp_total.alloc(K, s));
+  comp_total_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
+                                                               ix->iv_cum.p, g->comp_total.p);
+  MX_CUDA_TRY(g->comp_order.alloc(K, s));
+  component_order_kernel<<<1, 32, 0, s>>>(K, order_seed, g->comp_order.p);
+  MX_CUDA_TRY(cudaGetLastError());
+  g->h_comp_order.resize(K);
+  g->h_comp_total.resize(K);
+  MX_CUDA_TRY(cudaMemcpyAsync(g->h_comp_order.data(), g->comp_order.p, sizeof(u32) * K, cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(g->h_comp_total.data(), g->comp_total.p, sizeof(u64) * K, cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  return MX_OK;
+}
+
+}  // namespace mx

@@ -1,0 +1,117 @@
+// Internal data structures behind the opaque C-ABI handles.
+//
+// HBM layout of an index (I = intervals, B = (key, file) blocks, K = keys):
+//   iv_key/iv_file/iv_start/iv_end  u32[I]   sorted by (packed key, file, start)
+//   iv_cum                          u64[I+1] cumulative samples in that order
+//   blk_first u32[B+1], blk_file u32[B], blk_key u32[B]   (key, file) blocks
+//   key_blk_first u32[K+1], key_packed u32[K]             keys in sort_key order
+// A generator adds the RangeCursor layout:
+//   cur_blk u32[B]   blocks of each key in shuffled cursor order
+//   civ     u32[I]   interval ids in cursor order (key k owns the same index
+//                    range [blk_first[key_blk_first[k]], ...) as in iv_*)
+//   ccum    u64[I+1] cumulative samples in cursor order
+//   consumed u64[K]  per-component samples already handed out
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/mixtera_b200.h"
+#include "common.cuh"
+
+#define MX_SMEM_LUT_MAX 12288
+
+namespace mx {
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  long long n = 0;
+  cudaStream_t s = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  cudaError_t alloc(long long count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    if (count <= 0) return cudaSuccess;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (size_t)count, stream);
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  void take(DevBuf& o) {
+    release();
+    p = o.p; n = o.n; s = o.s;
+    o.p = nullptr; o.n = 0;
+  }
+};
+
+struct IndexData {
+  cudaStream_t stream = 0;
+  long long n_samples_total = 0;
+  int n_files = 0;
+  u32 key_bits = 0;
+  long long n_intervals = 0, n_keys = 0, n_blocks = 0;
+  DevBuf<u32> iv_key, iv_file, iv_start, iv_end;
+  DevBuf<u64> iv_cum;
+  DevBuf<u32> blk_first, blk_file, blk_key;
+  DevBuf<u32> key_blk_first, key_packed;
+  DevBuf<int32_t> file_ds;
+  std::vector<int32_t> h_file_ds;
+  std::vector<int64_t> h_file_ids;
+  // key codec (canonical strings for cursor seeds)
+  int n_props = 0;
+  u32 field_shift[MX_MAX_PROPS] = {};
+  u32 field_width[MX_MAX_PROPS] = {};
+  int32_t str_base[MX_MAX_PROPS] = {};
+  DevBuf<uint8_t> str_bytes;
+  DevBuf<long long> str_off;
+};
+
+struct GenData {
+  IndexData* ix = nullptr;
+  cudaStream_t stream = 0;
+  long long K = 0;
+  DevBuf<u32> comp_order;  // component ranks in seeded order
+  std::vector<u32> h_comp_order;
+  DevBuf<u32> cur_blk;
+  DevBuf<u32> civ;
+  DevBuf<u64> ccum;
+  DevBuf<u64> comp_total;
+  std::vector<unsigned long long> h_comp_total;
+  DevBuf<u64> consumed;
+  DevBuf<uint8_t> chunk_prefix;
+  int chunk_prefix_len = 0;
+  long long next_chunk_id = 0;
+  // last plan result
+  long long res_chunks = 0, res_ranges = 0;
+  DevBuf<long long> res_off;
+  DevBuf<long long> res_id;
+  DevBuf<u64> res_seed;
+  DevBuf<u32> res_mkey, res_file, res_start, res_end;
+  std::vector<long long> report;
+  int last_mkeys = 0;
+};
+
+int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out);
+int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, unsigned long long order_seed,
+                 cudaStream_t s, GenData* g);
+int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, long long* n_out);
+int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long long* n_out);
+
+}  // namespace mx
+
+struct mx_index {
+  mx::IndexData d;
+};
+struct mx_gen {
+  mx::GenData d;
+};

@@ -1,0 +1,689 @@
+// Stage 1 -- ChunkerIndex construction on sm_100a.
+//
+// Replaces MetadataCatalog.filter_intervals (catalog.py:549-605) +
+// build_index (index.py:88-115) with three device passes:
+//
+//  1. scan_runs_kernel: ONE streaming pass over the int32 code columns.
+//     Per sample: code -> (packed key contribution | filter-fail bit) via a
+//     shared-memory LUT, sum over properties = order-preserving packed key
+//     (codec.py explains the layout), run boundaries from neighbour compares
+//     (__shfl_up/down across lanes, shared memory across warps, direct halo
+//     loads across tiles), file boundaries from the tile's file-start list.
+//     Run starts are compacted with a warp byte-packed scan + block scan +
+//     decoupled look-back, and written as SoA interval records
+//     (key, file, start, end) in (file, start) order.
+//  2. an LSD radix sort of the records by packed key (8-bit digits, stable
+//     warp-multisplit ranking) -> (key, file, start) order. The packed key is
+//     order-preserving, so this IS MixtureKey.sort_key order (index.py:50-55
+//     component_keys()).
+//  3. two look-back scans: key/block boundary flags -> dense key ranks and
+//     (key, file) block ids; interval lengths -> u64 cumulative samples.
+//
+// Algorithmic bytes: B1 = N*sum(w_p) + 16*I + 8*B_kf + 16*K.
+#include "common.cuh"
+#include "mixtera_internal.cuh"
+
+namespace mx {
+
+// ---------------------------------------------------------------- pass 1
+constexpr int S1_THREADS = 256;
+constexpr int S1_SEGS = 4;                      // int4 segments per thread
+constexpr int S1_WARP = 32 * 4 * S1_SEGS;       // 512 samples per warp
+constexpr int S1_TILE = (S1_THREADS / 32) * S1_WARP;  // 4096 samples per tile
+constexpr int S1_FILE_CAP = 512;                // file starts cached per tile
+constexpr u32 FAIL = 0x80000000u;
+
+struct S1Args {
+  const int32_t* cols[MX_MAX_PROPS];
+  int lut_off[MX_MAX_PROPS + 1];
+  int n_props;
+  const u32* lut;  // device copy of the concatenated LUT
+  long long n;
+  const long long* file_off;
+  int n_files;
+  u32 rank_mask;
+  u32* rec_key;
+  u32* rec_file;
+  u32* rec_start;
+  u32* rec_end;
+  u64* status;
+  u32* tile_ctr;
+  u64* n_runs;
+  DevError* err;
+};
+
+template <bool SMEM_LUT>
+__device__ __forceinline__ u32 lut_get(const u32* s_lut, const u32* g_lut, int idx) {
+  return SMEM_LUT ? s_lut[idx] : __ldg(g_lut + idx);
+}
+
+// Status word of one sample: packed key, bit 31 set when it fails the filter
+// or lies outside [0, n).
+template <bool SMEM_LUT>
+__device__ u32 sample_status(const S1Args& a, const u32* s_lut, long long i) {
+  if (i < 0 || i >= a.n) return FAIL;
+  u32 key = 0, any = 0;
+  for (int p = 0; p < a.n_props; ++p) {
+    int c = a.cols[p][i];
+    u32 e = lut_get<SMEM_LUT>(s_lut, a.lut, a.lut_off[p] + c + 1);
+    key += e & ~FAIL;
+    any |= e;
+  }
+  return (any & FAIL) | key;
+}
+
+__device__ __forceinline__ int upper_bound_ll(const long long* v, int n, long long x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (v[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <bool SMEM_LUT>
+__global__ void __launch_bounds__(S1_THREADS)
+scan_runs_kernel(S1Args a) {
+  extern __shared__ u32 s_lut[];
+  __shared__ long long s_fstart[S1_FILE_CAP];
+  __shared__ int s_fa, s_nf, s_overflow, s_tile;
+  __shared__ long long s_fbase;
+  __shared__ u32 s_warp_first[S1_THREADS / 32], s_warp_last[S1_THREADS / 32];
+  __shared__ u32 s_warp_tot[S1_THREADS / 32];
+  __shared__ u64 s_tile_excl;
+  __shared__ u32 s_halo_prev, s_halo_next;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (SMEM_LUT) {
+    for (int i = tid; i < a.lut_off[a.n_props]; i += S1_THREADS) s_lut[i] = a.lut[i];
+  }
+  if (tid == 0) s_tile = atomicAdd(a.tile_ctr, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const long long t0 = (long long)tile * S1_TILE;
+
+  // file starts inside (t0, t0 + TILE]
+  if (tid == 0) {
+    int fa = upper_bound_ll(a.file_off, a.n_files + 1, t0) - 1;
+    if (fa >= a.n_files) fa = a.n_files - 1;
+    s_fa = fa;
+    s_fbase = a.file_off[fa];
+    s_halo_prev = sample_status<SMEM_LUT>(a, s_lut, t0 - 1);
+    s_halo_next = sample_status<SMEM_LUT>(a, s_lut, t0 + S1_TILE);
+  }
+  __syncthreads();
+  const int fa = s_fa;
+  for (int k = tid; k < S1_FILE_CAP; k += S1_THREADS) {
+    int f = fa + 1 + k;
+    s_fstart[k] = f <= a.n_files ? a.file_off[f] : (1ll << 62);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int m = upper_bound_ll(s_fstart, S1_FILE_CAP, t0 + S1_TILE);
+    s_nf = m;
+    s_overflow = (m == S1_FILE_CAP) ? 1 : 0;
+  }
+  __syncthreads();
+  const int nf = s_nf;
+  const bool overflow = s_overflow;
+
+  // ---- load codes (coalesced int4 per lane per segment) and build status
+  const long long wbase = t0 + (long long)warp * S1_WARP;
+  u32 st[S1_SEGS][4];
+#pragma unroll
+  for (int j = 0; j < S1_SEGS; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st[j][q] = 0;
+  u32 anyf[S1_SEGS][4];
+#pragma unroll
+  for (int j = 0; j < S1_SEGS; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) anyf[j][q] = 0;
+  const bool full = wbase + S1_WARP <= a.n;
+  for (int p = 0; p < a.n_props; ++p) {
+    const int32_t* col = a.cols[p];
+    const int lo = a.lut_off[p] + 1;
+    if (full) {
+      int4 v[S1_SEGS];
+#pragma unroll
+      for (int j = 0; j < S1_SEGS; ++j)
+        v[j] = ld_stream_v4(reinterpret_cast<const int4*>(col + wbase + 128 * j + 4 * lane));
+#pragma unroll
+      for (int j = 0; j < S1_SEGS; ++j) {
+        u32 e0 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v[j].x);
+        u32 e1 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v[j].y);
+        u32 e2 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v[j].z);
+        u32 e3 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v[j].w);
+        st[j][0] += e0 & ~FAIL; anyf[j][0] |= e0;
+        st[j][1] += e1 & ~FAIL; anyf[j][1] |= e1;
+        st[j][2] += e2 & ~FAIL; anyf[j][2] |= e2;
+        st[j][3] += e3 & ~FAIL; anyf[j][3] |= e3;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < S1_SEGS; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          long long i = wbase + 128 * j + 4 * lane + q;
+          if (i < a.n) {
+            u32 e = lut_get<SMEM_LUT>(s_lut, a.lut, lo + col[i]);
+            st[j][q] += e & ~FAIL;
+            anyf[j][q] |= e;
+          }
+        }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < S1_SEGS; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      long long i = wbase + 128 * j + 4 * lane + q;
+      st[j][q] = (i < a.n) ? ((anyf[j][q] & FAIL) | st[j][q]) : FAIL;
+    }
+
+  // ---- neighbours across warps
+  if (lane == 0) s_warp_first[warp] = st[0][0];
+  if (lane == 31) s_warp_last[warp] = st[S1_SEGS - 1][3];
+  __syncthreads();
+  const u32 warp_prev = warp == 0 ? s_halo_prev : s_warp_last[warp - 1];
+  const u32 warp_next = warp == S1_THREADS / 32 - 1 ? s_halo_next : s_warp_first[warp + 1];
+
+  // ---- file membership per sample
+  auto fstart_of = [&](int f) -> long long {
+    if (overflow) return a.file_off[f];
+    return f == fa ? s_fbase : s_fstart[f - fa - 1];
+  };
+  auto file_of = [&](long long i) -> int {
+    if (overflow) {
+      int f = upper_bound_ll(a.file_off, a.n_files + 1, i) - 1;
+      return f;
+    }
+    return fa + upper_bound_ll(s_fstart, nf, i);
+  };
+
+  u32 starts[S1_SEGS], ends[S1_SEGS];
+  int fidx[S1_SEGS][4];
+#pragma unroll
+  for (int j = 0; j < S1_SEGS; ++j) {
+    u32 prev_last = __shfl_up_sync(MX_FULL, st[j][3], 1);
+    u32 next_first = __shfl_down_sync(MX_FULL, st[j][0], 1);
+    u32 seg_prev = __shfl_sync(MX_FULL, st[j > 0 ? j - 1 : 0][3], 31);
+    u32 seg_next = __shfl_sync(MX_FULL, st[j < S1_SEGS - 1 ? j + 1 : 0][0], 0);
+    if (lane == 0) prev_last = j == 0 ? warp_prev : seg_prev;
+    if (lane == 31) next_first = j == S1_SEGS - 1 ? warp_next : seg_next;
+    const long long i0 = wbase + 128 * j + 4 * lane;
+    int f = file_of(i0);
+    u32 sm = 0, em = 0;
+    bool fs_cur = (i0 < a.n) && fstart_of(f) == i0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long i = i0 + q;
+      fidx[j][q] = f;
+      const u32 cur = st[j][q];
+      const u32 prv = q == 0 ? prev_last : st[j][q - 1];
+      const u32 nxt = q == 3 ? next_first : st[j][q + 1];
+      // does sample i+1 start a new file?
+      bool fs_next;
+      int fn = f;
+      if (overflow) {
+        fn = (i + 1 < a.n) ? file_of(i + 1) : f;
+        fs_next = (i + 1 < a.n) && fstart_of(fn) == i + 1;
+      } else {
+        int k = f - fa;  // index into s_fstart of the next file start
+        fs_next = k < nf && s_fstart[k] == i + 1;
+        if (fs_next) fn = f + 1;
+        // skip empty files (duplicate offsets)
+        while (fs_next && fn - fa < nf && s_fstart[fn - fa] == i + 1) ++fn;
+      }
+      const bool pass = !(cur & FAIL);
+      const bool start = pass && (fs_cur || (prv & FAIL) || prv != cur);
+      const bool end = pass && (fs_next || (nxt & FAIL) || nxt != cur);
+      sm |= (u32)start << q;
+      em |= (u32)end << q;
+      fs_cur = fs_next;
+      f = fn;
+    }
+    starts[j] = sm;
+    ends[j] = em;
+  }
+
+  // ---- compaction: byte-packed per-segment counts, warp scan, block scan
+  u32 pack = 0;
+#pragma unroll
+  for (int j = 0; j < S1_SEGS; ++j) pack |= (u32)__popc(starts[j]) << (8 * j);
+  const u32 incl = warp_incl_scan(pack);
+  const u32 excl = incl - pack;
+  const u32 wtot = __shfl_sync(MX_FULL, incl, 31);
+  u32 seg_base[S1_SEGS];
+  u32 acc = 0;
+#pragma unroll
+  for (int j = 0; j < S1_SEGS; ++j) {
+    seg_base[j] = acc + ((excl >> (8 * j)) & 0xff);
+    acc += (wtot >> (8 * j)) & 0xff;
+  }
+  if (lane == 0) s_warp_tot[warp] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    u32 v = lane < S1_THREADS / 32 ? s_warp_tot[lane] : 0;
+    u32 inc = warp_incl_scan(v);
+    u32 tile_agg = __shfl_sync(MX_FULL, inc, 31);
+    if (lane < S1_THREADS / 32) s_warp_tot[lane] = inc - v;
+    u64 tex = lookback_exclusive(a.status, tile, tile_agg);
+    if (lane == 0) {
+      s_tile_excl = tex;
+      if ((long long)(tile + 1) * S1_TILE >= a.n) *a.n_runs = tex + tile_agg;
+    }
+  }
+  __syncthreads();
+  const u64 base = s_tile_excl + s_warp_tot[warp];
+
+  // ---- emit records
+#pragma unroll
+  for (int j = 0; j < S1_SEGS; ++j) {
+    u64 run = base + seg_base[j];  // number of run starts before this thread's segment j
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long i = wbase + 128 * j + 4 * lane + q;
+      if ((starts[j] >> q) & 1) {
+        const u32 key = st[j][q];
+        a.rec_key[run] = key;
+        a.rec_file[run] = (u32)fidx[j][q];
+        a.rec_start[run] = (u32)(i - fstart_of(fidx[j][q]));
+        if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)i);
+        ++run;
+      }
+      if ((ends[j] >> q) & 1) a.rec_end[run - 1] = (u32)(i + 1 - fstart_of(fidx[j][q]));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- radix sort
+constexpr int RS_THREADS = 256;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096, warp-striped
+constexpr int RS_WARPS = RS_THREADS / 32;
+
+__global__ void __launch_bounds__(RS_THREADS)
+radix_upsweep(const u32* keys, long long n, int shift, u32* hist, int ntiles) {
+  __shared__ u32 h[256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  h[tid] = 0;
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * RS_TILE + warp * (32 * RS_ITEMS);
+#pragma unroll 4
+  for (int k = 0; k < RS_ITEMS; ++k) {
+    long long i = base + k * 32 + lane;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  hist[(long long)tid * ntiles + blockIdx.x] = h[tid];
+}
+
+// one CTA per digit: exclusive scan of its row across tiles, row total out
+__global__ void __launch_bounds__(256)
+radix_rowscan(u32* hist, int ntiles, u32* digit_tot) {
+  __shared__ u32 s_w[8];
+  __shared__ u32 s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  u32* row = hist + (long long)blockIdx.x * ntiles;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int b = 0; b < ntiles; b += 256 * 4) {
+    u32 v[4], s = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int i = b + tid * 4 + q;
+      v[q] = i < ntiles ? row[i] : 0;
+      s += v[q];
+    }
+    u32 inc = warp_incl_scan(s);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      u32 x = lane < 8 ? s_w[lane] : 0;
+      u32 xi = warp_incl_scan(x);
+      if (lane < 8) s_w[lane] = xi - x;
+    }
+    __syncthreads();
+    u32 run = s_carry + s_w[warp] + inc - s;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int i = b + tid * 4 + q;
+      if (i < ntiles) row[i] = run;
+      run += v[q];
+    }
+    __syncthreads();
+    if (tid == 255) s_carry = run;
+    __syncthreads();
+  }
+  if (tid == 0) digit_tot[blockIdx.x] = s_carry;
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+radix_downsweep(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2in,
+                u32* kout, u32* p0out, u32* p1out, u32* p2out,
+                long long n, int shift, const u32* hist, const u32* digit_tot, int ntiles) {
+  __shared__ u32 s_base[256];
+  __shared__ u32 s_wcnt[RS_WARPS][256];
+  __shared__ u32 s_w[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {  // digit bases = exclusive scan of digit totals + this tile's row prefix
+    u32 x = digit_tot[tid];
+    u32 inc = warp_incl_scan(x);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      u32 y = lane < 8 ? s_w[lane] : 0;
+      u32 yi = warp_incl_scan(y);
+      if (lane < 8) s_w[lane] = yi - y;
+    }
+    __syncthreads();
+    s_base[tid] = s_w[warp] + inc - x + hist[(long long)tid * ntiles + blockIdx.x];
+  }
+#pragma unroll
+  for (int w = 0; w < RS_WARPS; ++w) s_wcnt[w][tid] = 0;
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * RS_TILE + warp * (32 * RS_ITEMS);
+  u32 key[RS_ITEMS];
+  u32 rank[RS_ITEMS];
+#pragma unroll
+  for (int k = 0; k < RS_ITEMS; ++k) {
+    long long i = base + k * 32 + lane;
+    bool ok = i < n;
+    key[k] = ok ? kin[i] : 0;
+    u32 d = (key[k] >> shift) & 0xff;
+    u32 peers = __match_any_sync(MX_FULL, ok ? d : 0x100u);
+    u32 before = __popc(peers & ((1u << lane) - 1));
+    u32 cur = s_wcnt[warp][d & 0xff];
+    __syncwarp();
+    rank[k] = cur + before;
+    if (ok && before == 0) s_wcnt[warp][d] = cur + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {  // per digit: exclusive scan over warps
+    u32 run = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+      u32 c = s_wcnt[w][tid];
+      s_wcnt[w][tid] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < RS_ITEMS; ++k) {
+    long long i = base + k * 32 + lane;
+    if (i < n) {
+      u32 d = (key[k] >> shift) & 0xff;
+      u32 dst = s_base[d] + s_wcnt[warp][d] + rank[k];
+      kout[dst] = key[k];
+      p0out[dst] = p0in[i];
+      p1out[dst] = p1in[i];
+      p2out[dst] = p2in[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- finalize
+constexpr int SC_THREADS = 256;
+constexpr int SC_ITEMS = 8;
+constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
+
+// Block-wide exclusive scan helper for u64 (returns exclusive, writes total).
+__device__ __forceinline__ u64 block_excl_u64(u64 v, u64* s_w, u64* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u64 inc = warp_incl_scan(v);
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    u64 x = lane < SC_THREADS / 32 ? s_w[lane] : 0;
+    u64 xi = warp_incl_scan(x);
+    if (lane < SC_THREADS / 32) s_w[lane] = xi - x;
+    if (lane == 31) s_w[SC_THREADS / 32] = xi;
+  }
+  __syncthreads();
+  *total = s_w[SC_THREADS / 32];
+  return s_w[warp] + inc - v;
+}
+
+// Boundary flags -> key ranks / block ids; writes the block + key tables.
+// Packed value: (key changes << 32) | block changes.
+__global__ void __launch_bounds__(SC_THREADS)
+index_bounds_kernel(const u32* key, const u32* file, long long n, u64* status, u32* tile_ctr,
+                    u32* blk_first, u32* blk_file, u32* blk_key,
+                    u32* key_blk_first, u32* key_packed, u64* totals) {
+  __shared__ u64 s_w[SC_THREADS / 32 + 1];
+  __shared__ int s_tile;
+  __shared__ u64 s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const long long b = (long long)tile * SC_TILE + threadIdx.x * SC_ITEMS;
+  u64 v[SC_ITEMS];
+  u64 sum = 0;
+#pragma unroll
+  for (int q = 0; q < SC_ITEMS; ++q) {
+    long long i = b + q;
+    u64 f = 0;
+    if (i < n) {
+      bool kc = i == 0 || key[i] != key[i - 1];
+      bool bc = kc || file[i] != file[i - 1];
+      f = ((u64)kc << 32) | (u64)bc;
+    }
+    v[q] = f;
+    sum += f;
+  }
+  u64 tot;
+  u64 ex = block_excl_u64(sum, s_w, &tot);
+  if (threadIdx.x < 32) {
+    u64 t = lookback_exclusive(status, tile, tot);
+    if (threadIdx.x == 0) {
+      s_excl = t;
+      if ((long long)(tile + 1) * SC_TILE >= n) *totals = t + tot;
+    }
+  }
+  __syncthreads();
+  u64 run = s_excl + ex;
+#pragma unroll
+  for (int q = 0; q < SC_ITEMS; ++q) {
+    long long i = b + q;
+    run += v[q];
+    if (i < n && (v[q] & 1)) {
+      u32 k = (u32)(run >> 32) - 1, blk = (u32)run - 1;
+      blk_first[blk] = (u32)i;
+      blk_file[blk] = file[i];
+      blk_key[blk] = k;
+      if (v[q] >> 32) {
+        key_blk_first[k] = blk;
+        key_packed[k] = key[i];
+      }
+    }
+  }
+}
+
+// u64 inclusive scan of interval lengths -> cum[i + 1]; cum[0] = 0.
+__global__ void __launch_bounds__(SC_THREADS)
+interval_cum_kernel(const u32* start, const u32* end, long long n, u64* status, u32* tile_ctr,
+                    u64* cum, DevError* err) {
+  __shared__ u64 s_w[SC_THREADS / 32 + 1];
+  __shared__ int s_tile;
+  __shared__ u64 s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const long long b = (long long)tile * SC_TILE + threadIdx.x * SC_ITEMS;
+  u64 v[SC_ITEMS];
+  u64 sum = 0;
+#pragma unroll
+  for (int q = 0; q < SC_ITEMS; ++q) {
+    long long i = b + q;
+    u64 l = 0;
+    if (i < n) {
+      u32 s = start[i], e = end[i];
+      if (e <= s) atomicOr(&err->overlap, 1u);
+      l = e > s ? e - s : 0;
+    }
+    v[q] = l;
+    sum += l;
+  }
+  u64 tot;
+  u64 ex = block_excl_u64(sum, s_w, &tot);
+  if (threadIdx.x < 32) {
+    u64 t = lookback_exclusive(status, tile, tot);
+    if (threadIdx.x == 0) s_excl = t;
+  }
+  __syncthreads();
+  u64 run = s_excl + ex;
+  if (b == 0 && threadIdx.x == 0) cum[0] = 0;
+#pragma unroll
+  for (int q = 0; q < SC_ITEMS; ++q) {
+    long long i = b + q;
+    run += v[q];
+    if (i < n) cum[i + 1] = run;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
+  if (d->n_props < 1 || d->n_props > MX_MAX_PROPS)
+    return mx_fail(MX_ERR_UNSUPPORTED, "n_props=%d outside [1, %d]", d->n_props, MX_MAX_PROPS);
+  if (d->key_bits > 31)
+    return mx_fail(MX_ERR_UNSUPPORTED, "packed key needs %u bits (> 31)", d->key_bits);
+  if (d->n_files < 1) return mx_fail(MX_ERR_QUERY, "catalog is empty");
+  IndexData& ix = *out;
+  ix.n_samples_total = d->n_samples;
+  ix.n_files = d->n_files;
+  ix.key_bits = d->key_bits;
+  const long long n = d->n_samples;
+  S1Args a{};
+  a.n_props = d->n_props;
+  for (int p = 0; p < d->n_props; ++p) a.cols[p] = d->columns[p];
+  for (int p = 0; p <= d->n_props; ++p) a.lut_off[p] = d->lut_offsets[p];
+  const int lut_total = d->lut_offsets[d->n_props];
+  DevBuf<u32> lut;
+  MX_CUDA_TRY(lut.alloc(lut_total, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(lut.p, d->lut, sizeof(u32) * lut_total, cudaMemcpyHostToDevice, s));
+  a.lut = lut.p;
+  a.n = n;
+  a.file_off = reinterpret_cast<const long long*>(d->file_offsets);
+  a.n_files = d->n_files;
+  a.rank_mask = d->rank_mask;
+  // file table copies (ds and ids are needed for exports and cursors)
+  MX_CUDA_TRY(ix.file_ds.alloc(d->n_files, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(ix.file_ds.p, d->file_ds, sizeof(int32_t) * d->n_files, cudaMemcpyHostToDevice, s));
+  ix.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
+  ix.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
+
+  const int ntiles = (int)((n + S1_TILE - 1) / S1_TILE);
+  DevBuf<u32> rk, rf, rs, re;
+  DevBuf<u64> status, scratch64;
+  DevBuf<u32> ctr;
+  DevBuf<DevError> err;
+  const long long cap = n > 0 ? n : 1;  // worst case: every sample its own run
+  MX_CUDA_TRY(rk.alloc(cap, s));
+  MX_CUDA_TRY(rf.alloc(cap, s));
+  MX_CUDA_TRY(rs.alloc(cap, s));
+  MX_CUDA_TRY(re.alloc(cap, s));
+  MX_CUDA_TRY(status.alloc(ntiles > 0 ? ntiles : 1, s));
+  MX_CUDA_TRY(scratch64.alloc(4, s));
+  MX_CUDA_TRY(ctr.alloc(4, s));
+  MX_CUDA_TRY(err.alloc(1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(status.p, 0, sizeof(u64) * (ntiles > 0 ? ntiles : 1), s));
+  MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32) * 4, s));
+  MX_CUDA_TRY(cudaMemsetAsync(scratch64.p, 0, sizeof(u64) * 4, s));
+  MX_CUDA_TRY(cudaMemsetAsync(err.p, 0xff, sizeof(u64), s));
+  MX_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(err.p) + 8, 0, 8, s));
+  a.rec_key = rk.p; a.rec_file = rf.p; a.rec_start = rs.p; a.rec_end = re.p;
+  a.status = status.p; a.tile_ctr = ctr.p; a.n_runs = scratch64.p; a.err = err.p;
+  if (ntiles > 0) {
+    const bool smem = lut_total <= MX_SMEM_LUT_MAX;
+    if (smem) {
+      scan_runs_kernel<true><<<ntiles, S1_THREADS, sizeof(u32) * lut_total, s>>>(a);
+    } else {
+      scan_runs_kernel<false><<<ntiles, S1_THREADS, 0, s>>>(a);
+    }
+    MX_CUDA_TRY(cudaGetLastError());
+  }
+  u64 h_runs = 0;
+  DevError h_err;
+  MX_CUDA_TRY(cudaMemcpyAsync(&h_runs, scratch64.p, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(&h_err, err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_err.null_key_sample != ~0ull) {
+    const long long g = (long long)h_err.null_key_sample;
+    std::vector<long long> off(d->n_files + 1);
+    MX_CUDA_TRY(cudaMemcpy(off.data(), d->file_offsets, sizeof(long long) * off.size(), cudaMemcpyDeviceToHost));
+    int f = (int)(std::upper_bound(off.begin(), off.end(), g) - off.begin()) - 1;
+    return mx_fail(MX_ERR_QUERY,
+                   "sample %lld of file %lld has no non-null properties; it cannot be keyed into a mixture",
+                   g - off[f], (long long)d->file_ids[f]);
+  }
+  const long long I = (long long)h_runs;
+  ix.n_intervals = I;
+  if (I == 0) {
+    ix.n_keys = 0;
+    ix.n_blocks = 0;
+    return MX_OK;
+  }
+  // ---- radix sort by packed key
+  const int passes = (d->key_bits + 7) / 8;
+  const int rtiles = (int)((I + RS_TILE - 1) / RS_TILE);
+  DevBuf<u32> k2, f2, s2, e2, hist, dtot;
+  MX_CUDA_TRY(k2.alloc(I, s));
+  MX_CUDA_TRY(f2.alloc(I, s));
+  MX_CUDA_TRY(s2.alloc(I, s));
+  MX_CUDA_TRY(e2.alloc(I, s));
+  MX_CUDA_TRY(hist.alloc((long long)256 * rtiles, s));
+  MX_CUDA_TRY(dtot.alloc(256, s));
+  u32 *ka = rk.p, *fa_ = rf.p, *sa = rs.p, *ea = re.p;
+  u32 *kb = k2.p, *fb = f2.p, *sb = s2.p, *eb = e2.p;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int shift = 8 * pass;
+    radix_upsweep<<<rtiles, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles);
+    radix_rowscan<<<256, 256, 0, s>>>(hist.p, rtiles, dtot.p);
+    radix_downsweep<<<rtiles, RS_THREADS, 0, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p, dtot.p, rtiles);
+    MX_CUDA_TRY(cudaGetLastError());
+    std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);
+  }
+  // sorted arrays now in (ka, fa_, sa, ea); keep them
+  if (ka == rk.p) {
+    ix.iv_key.take(rk); ix.iv_file.take(rf); ix.iv_start.take(rs); ix.iv_end.take(re);
+  } else {
+    ix.iv_key.take(k2); ix.iv_file.take(f2); ix.iv_start.take(s2); ix.iv_end.take(e2);
+  }
+  // ---- boundaries and cumulative lengths
+  const int stiles = (int)((I + SC_TILE - 1) / SC_TILE);
+  DevBuf<u64> st2;
+  MX_CUDA_TRY(st2.alloc(stiles, s));
+  MX_CUDA_TRY(ix.blk_first.alloc(I + 1, s));
+  MX_CUDA_TRY(ix.blk_file.alloc(I, s));
+  MX_CUDA_TRY(ix.blk_key.alloc(I, s));
+  MX_CUDA_TRY(ix.key_blk_first.alloc(I + 1, s));
+  MX_CUDA_TRY(ix.key_packed.alloc(I, s));
+  MX_CUDA_TRY(ix.iv_cum.alloc(I + 1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(st2.p, 0, sizeof(u64) * stiles, s));
+  MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32) * 4, s));
+  index_bounds_kernel<<<stiles, SC_THREADS, 0, s>>>(ix.iv_key.p, ix.iv_file.p, I, st2.p, ctr.p,
+                                                    ix.blk_first.p, ix.blk_file.p, ix.blk_key.p,
+                                                    ix.key_blk_first.p, ix.key_packed.p, scratch64.p + 1);
+  MX_CUDA_TRY(cudaMemsetAsync(st2.p, 0, sizeof(u64) * stiles, s));
+  interval_cum_kernel<<<stiles, SC_THREADS, 0, s>>>(ix.iv_start.p, ix.iv_end.p, I, st2.p, ctr.p + 1,
+                                                    ix.iv_cum.p, err.p);
+  MX_CUDA_TRY(cudaGetLastError());
+  u64 tot = 0;
+  MX_CUDA_TRY(cudaMemcpyAsync(&tot, scratch64.p + 1, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(&h_err, err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_err.overlap) return mx_fail(MX_ERR_INDEX, "empty or overlapping interval in index build");
+  ix.n_keys = (long long)(tot >> 32);
+  ix.n_blocks = (long long)(tot & 0xffffffffull);
+  // sentinels
+  const u32 sI = (u32)I, sB = (u32)ix.n_blocks;
+  MX_CUDA_TRY(cudaMemcpyAsync(ix.blk_first.p + ix.n_blocks, &sI, sizeof(u32), cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(ix.key_blk_first.p + ix.n_keys, &sB, sizeof(u32), cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  return MX_OK;
+}
+
+}  // namespace mx

@@ -1,0 +1,1059 @@
+// Stage 2 -- chunk generation on sm_100a.
+//
+// Reference: ChunkGenerator.generate (chunks.py:194-230), _take_for_key
+// (:150-167), redistribute_best_effort (:109-130), apportion
+// (mixtures.py:158-184), _normalize/_finish (chunks.py:169-192),
+// generate_arbitrary (:232-253).
+//
+// The reference walks Python cursor objects range by range. Here a chunk is
+// decided at COUNT level first and only then cut:
+//
+//  * match_*_kernel   -- mixture key x component key matching from per-
+//                        property value-rank bitsets (mixtures.py:100-109);
+//                        per mixture key the matching components in seeded
+//                        component order (L_m).
+//  * plan_kernel      -- ONE thread replays Algorithm 1 on integers: passes
+//                        over mixture keys, depletion, strict stop, best-effort
+//                        redistribution with a bit-exact apportion (Neumaier
+//                        sum, int(share + 1e-9), (-frac, key rank) order).
+//                        When no component is shared between mixture keys
+//                        (the common case), each mixture key draws from its
+//                        own stream S_m = concat of its components' cursor
+//                        streams, and a chunk's outcome depends only on which
+//                        keys are depleted. One simulated chunk then repeats
+//                        verbatim for floor(avail_m / took_m) chunks: the plan
+//                        is a handful of PHASES (base, stride per key) instead
+//                        of one replay per chunk. Shared components fall back
+//                        to an exact per-chunk replay at component level.
+//  * emit_*_kernels   -- fully parallel over (chunk, term): binary search of
+//                        the stream offset in segment prefix sums, then in the
+//                        cursor-order interval prefix sums (ccum), cut the
+//                        intervals; per-chunk sort by (mixture key, file,
+//                        start) + adjacent merge in shared memory; compaction
+//                        into a CSR; device BLAKE2b chunk seeds.
+//
+// Algorithmic bytes: B2 = sum over chunks of
+// (16 * intervals touched + 20 * ranges emitted) + 8 per chunk seed.
+#include "blake2b.cuh"
+#include "common.cuh"
+#include "mixtera_internal.cuh"
+
+namespace mx {
+
+// ------------------------------------------------------------------ matching
+struct MatchArgs {
+  int Km;
+  long long K;
+  const u32* comp_order;  // [K] component ranks in seeded order
+  const u32* key_packed;  // [K]
+  int n_props;
+  u32 shift[MX_MAX_PROPS];
+  u32 width[MX_MAX_PROPS];
+  int allow_base[MX_MAX_PROPS];
+  int allow_words;
+  const u32* allow;  // [Km][allow_words]
+};
+
+__device__ __forceinline__ bool mkey_matches(const MatchArgs& a, int m, u32 packed) {
+  const u32* al = a.allow + (long long)m * a.allow_words;
+  for (int p = 0; p < a.n_props; ++p) {
+    u32 r = (packed >> a.shift[p]) & ((1u << a.width[p]) - 1u);
+    u32 bit = (u32)a.allow_base[p] + r;
+    if (!((al[bit >> 5] >> (bit & 31)) & 1u)) return false;
+  }
+  return true;
+}
+
+// one CTA per mixture key: count matches, and the per-component hit counts
+__global__ void match_count_kernel(MatchArgs a, u32* L_cnt, u32* comp_hits) {
+  __shared__ u32 s_cnt;
+  const int m = blockIdx.x;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  u32 c = 0;
+  for (long long pos = threadIdx.x; pos < a.K; pos += blockDim.x) {
+    u32 comp = a.comp_order[pos];
+    if (mkey_matches(a, m, a.key_packed[comp])) {
+      ++c;
+      atomicAdd(comp_hits + comp, 1u);
+    }
+  }
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) L_cnt[m] = s_cnt;
+}
+
+// one CTA per mixture key: ordered compaction of matching components
+__global__ void __launch_bounds__(256) match_fill_kernel(MatchArgs a, const u32* L_off, u32* L) {
+  __shared__ u32 s_w[8];
+  __shared__ u32 s_base;
+  const int m = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_base = L_off[m];
+  __syncthreads();
+  for (long long b = 0; b < a.K; b += 256) {
+    long long pos = b + threadIdx.x;
+    u32 comp = pos < a.K ? a.comp_order[pos] : 0;
+    u32 f = (pos < a.K && mkey_matches(a, m, a.key_packed[comp])) ? 1u : 0u;
+    u32 inc = warp_incl_scan(f);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      u32 x = lane < 8 ? s_w[lane] : 0;
+      u32 xi = warp_incl_scan(x);
+      if (lane < 8) s_w[lane] = xi - x;
+    }
+    __syncthreads();
+    if (f) L[s_base + s_w[warp] + inc - 1] = comp;
+    __syncthreads();
+    if (threadIdx.x == 255) s_base += s_w[7] + inc;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ streams
+// A stream is a list of segments (component, absolute start offset, length).
+//   mode 0 (disjoint mixture): stream m = L_m components, [consumed, total)
+//   mode 1 (shared components): stream c = component c, [0, total)
+//   mode 2 (arbitrary): stream 0 = all components in order, [consumed, total)
+__global__ void build_segments_kernel(int mode, int n_streams, const u32* s_off, const u32* list,
+                                      const u64* comp_total, const u64* consumed, u32* seg_comp, u64* seg_lo,
+                                      u64* seg_pre) {
+  // one thread per stream, sequential prefix (segments per stream are few or
+  // the stream count is small)
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_streams) return;
+  u32 b = s_off[s], e = s_off[s + 1];
+  u64 run = 0;
+  for (u32 i = b; i < e; ++i) {
+    u32 c = mode == 1 ? (u32)s : list[i];
+    u64 lo = mode == 1 ? 0 : consumed[c];
+    u64 len = comp_total[c] - lo;
+    seg_comp[i] = c;
+    seg_lo[i] = lo;
+    seg_pre[i + s] = run;  // seg_pre has (segments + streams) entries: stream s uses [b + s, e + s]
+    run += len;
+  }
+  seg_pre[e + s] = run;
+}
+
+// consumed[c] after a plan: lo + clamp(pos_s - pre_i, 0, len_i)
+__global__ void commit_segments_kernel(int n_streams, const u32* s_off, const u32* seg_comp, const u64* seg_lo,
+                                       const u64* seg_pre, const u64* pos, u64* consumed) {
+  int s = blockIdx.x;
+  if (s >= n_streams) return;
+  u32 b = s_off[s], e = s_off[s + 1];
+  u64 p = pos[s];
+  for (u32 i = b + threadIdx.x; i < e; i += blockDim.x) {
+    u64 pre = seg_pre[i + s], nxt = seg_pre[i + 1 + s];
+    u64 used = p <= pre ? 0 : (p >= nxt ? nxt - pre : p - pre);
+    consumed[seg_comp[i]] = seg_lo[i] + used;
+  }
+}
+
+// ------------------------------------------------------------------ planner
+struct Term {
+  u32 m;       // mixture key index (ignored in arbitrary mode)
+  u32 stream;  // stream id
+  u64 base;    // stream offset of chunk 0 of the phase
+  u64 len;     // samples per chunk
+  u64 stride;  // base advance per chunk
+};
+
+struct Phase {
+  long long chunk_begin;  // relative to the plan
+  long long n_chunks;
+  long long term_begin;
+  long long n_terms;
+};
+
+struct PlanArgs {
+  int mode;
+  int Km;
+  long long C;
+  int strict;
+  long long max_chunks;
+  const double* w;
+  // mode 0 / 2: stream lengths
+  const u64* seg_pre;
+  const u32* s_off;
+  // mode 1
+  const u32* L_off;
+  const u32* L;
+  const u64* comp_total;
+  u64* consumed;
+  u32* front;
+  // scratch [Km]
+  long long* counts;
+  long long* rem;
+  long long* found;
+  long long* took;
+  unsigned char* dead;
+  unsigned char* newly;
+  u64* pos;  // per stream, relative
+  int* ap_idx;
+  double* ap_frac;
+  long long* ap_base;
+  // out
+  Phase* phases;
+  long long cap_phases;
+  Term* terms;
+  long long cap_terms;
+  long long* out;  // [0]=chunks [1]=phases [2]=terms [3]=exhausted
+  long long* report;
+};
+
+// CPython 3.12 builtin sum over floats (Neumaier), keys in index order
+__device__ double neumaier(const double* w, const unsigned char* skip, int n) {
+  double s = 0.0, c = 0.0;
+  for (int i = 0; i < n; ++i) {
+    if (skip && skip[i]) continue;
+    double x = w[i];
+    double t = s + x;
+    if (fabs(s) >= fabs(x)) c += (s - t) + x;
+    else c += (x - t) + s;
+    s = t;
+  }
+  return c != 0.0 ? s + c : s;
+}
+
+__device__ __forceinline__ bool frac_before(double fa, int a, double fb, int b) {
+  // order by (-frac, key index)
+  if (fa != fb) return fa > fb;
+  return a < b;
+}
+
+// heap sort of idx[0..n) by frac_before (ascending in that order)
+__device__ void heap_sort(int* idx, const double* fr, int n) {
+  auto less = [&](int x, int y) { return frac_before(fr[x], x, fr[y], y); };
+  auto sift = [&](int root, int end) {
+    while (true) {
+      int child = 2 * root + 1;
+      if (child >= end) return;
+      if (child + 1 < end && less(idx[child], idx[child + 1])) ++child;
+      if (less(idx[root], idx[child])) {
+        int t = idx[root]; idx[root] = idx[child]; idx[child] = t;
+        root = child;
+      } else {
+        return;
+      }
+    }
+  };
+  for (int s = n / 2 - 1; s >= 0; --s) sift(s, n);
+  for (int e = n - 1; e > 0; --e) {
+    int t = idx[0]; idx[0] = idx[e]; idx[e] = t;
+    sift(0, e);
+  }
+}
+
+// apportion(weights restricted to keys with !skip[i], total): adds the counts
+// into out[] (out[i] += count_i). Returns false when wsum <= 0.
+__device__ bool apportion_add(const PlanArgs& a, const unsigned char* skip, long long total, long long* out) {
+  const int n = a.Km;
+  double wsum = neumaier(a.w, skip, n);
+  if (!(wsum > 0.0)) return false;
+  const double tot = (double)total;
+  long long assigned = 0;
+  int cnt = 0;
+  for (int i = 0; i < n; ++i) {
+    if (skip && skip[i]) continue;
+    double share = a.w[i] / wsum * tot;
+    long long base = (long long)(share + 1e-9);
+    double fr = share - (double)base;
+    a.ap_frac[i] = fr > 0.0 ? fr : 0.0;
+    a.ap_base[i] = base;
+    assigned += base;
+    a.ap_idx[cnt++] = i;
+  }
+  long long left = total - assigned;
+  if (left > 0) {
+    if (cnt <= 32) {  // insertion sort
+      for (int x = 1; x < cnt; ++x) {
+        int v = a.ap_idx[x];
+        int y = x - 1;
+        while (y >= 0 && frac_before(a.ap_frac[v], v, a.ap_frac[a.ap_idx[y]], a.ap_idx[y])) {
+          a.ap_idx[y + 1] = a.ap_idx[y];
+          --y;
+        }
+        a.ap_idx[y + 1] = v;
+      }
+    } else {
+      heap_sort(a.ap_idx, a.ap_frac, cnt);
+    }
+    for (long long t = 0; t < left && t < cnt; ++t) a.ap_base[a.ap_idx[t]] += 1;
+  }
+  for (int x = 0; x < cnt; ++x) out[a.ap_idx[x]] += a.ap_base[a.ap_idx[x]];
+  return true;
+}
+
+// take up to `need` from mixture key m (mode 1: component frontiers)
+__device__ long long take_shared(PlanArgs& a, int m, long long need, long long* n_terms) {
+  long long got = 0;
+  u32 b = a.L_off[m], e = a.L_off[m + 1];
+  for (u32 i = b + a.front[m]; i < e && need > 0; ++i) {
+    u32 c = a.L[i];
+    u64 used = a.consumed[c], tot = a.comp_total[c];
+    if (used >= tot) {
+      if (i == b + a.front[m]) a.front[m] += 1;
+      continue;
+    }
+    long long t = (long long)(tot - used) < need ? (long long)(tot - used) : need;
+    if (*n_terms < a.cap_terms) {
+      Term& tm = a.terms[*n_terms];
+      tm.m = (u32)m;
+      tm.stream = c;
+      tm.base = used;
+      tm.len = (u64)t;
+      tm.stride = 0;
+    }
+    *n_terms += 1;
+    a.consumed[c] = used + (u64)t;
+    got += t;
+    need -= t;
+  }
+  return got;
+}
+
+// Simulate one generate() call. Returns 1 = chunk, 0 = None (exhausted).
+__device__ int simulate_chunk(PlanArgs& a, long long* n_terms) {
+  const int Km = a.Km;
+  for (int m = 0; m < Km; ++m) {
+    a.rem[m] = a.counts[m];
+    a.dead[m] = 0;
+    a.took[m] = 0;
+  }
+  while (true) {
+    bool anypos = false;
+    for (int m = 0; m < Km; ++m) anypos |= a.rem[m] > 0;
+    if (!anypos) break;
+    for (int m = 0; m < Km; ++m) {
+      a.found[m] = -1;
+      if (a.rem[m] <= 0) continue;
+      long long g;
+      if (a.mode == 1) {
+        g = take_shared(a, m, a.rem[m], n_terms);
+      } else {
+        u64 len = a.seg_pre[a.s_off[m + 1] + m + 1 - 1];  // end of stream m
+        long long avail = (long long)(len - a.pos[m]) - a.took[m];
+        g = a.rem[m] < avail ? a.rem[m] : avail;
+      }
+      a.took[m] += g;
+      a.rem[m] -= g;
+      a.found[m] = g;
+    }
+    bool any_new = false;
+    for (int m = 0; m < Km; ++m) {
+      a.newly[m] = (a.found[m] == 0 && a.rem[m] > 0) ? 1 : 0;
+      any_new |= a.newly[m];
+    }
+    if (!any_new) continue;
+    if (a.strict) {
+      for (int m = 0; m < Km; ++m) a.report[m] = a.rem[m];
+      return 0;
+    }
+    for (int m = 0; m < Km; ++m) {
+      if (!a.newly[m]) continue;
+      a.dead[m] = 1;
+      bool alive = false;
+      for (int x = 0; x < Km; ++x) alive |= !a.dead[x];
+      if (!alive) {
+        for (int x = 0; x < Km; ++x) a.report[x] = a.rem[x];
+        return 0;
+      }
+      if (a.rem[m] > 0) apportion_add(a, a.dead, a.rem[m], a.rem);
+      a.rem[m] = 0;
+    }
+  }
+  return 1;
+}
+
+__global__ void plan_kernel(PlanArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int Km = a.Km;
+  for (int m = 0; m < Km; ++m) a.counts[m] = 0;
+  apportion_add(a, nullptr, a.C, a.counts);
+  long long chunks = 0, n_ph = 0, n_terms = 0, exhausted = 0;
+  for (int m = 0; m < Km; ++m) a.pos[m] = 0;
+  while (chunks < a.max_chunks) {
+    if (n_ph >= a.cap_phases) break;
+    if (a.mode == 1) {
+      if (a.cap_terms - n_terms < (long long)Km + a.C) break;
+      long long t0 = n_terms;
+      int ok = simulate_chunk(a, &n_terms);
+      if (!ok) {
+        n_terms = t0;
+        exhausted = 1;
+        break;
+      }
+      Phase& ph = a.phases[n_ph++];
+      ph.chunk_begin = chunks;
+      ph.n_chunks = 1;
+      ph.term_begin = t0;
+      ph.n_terms = n_terms - t0;
+      chunks += 1;
+      continue;
+    }
+    if (a.cap_terms - n_terms < (long long)Km) break;
+    int ok = simulate_chunk(a, &n_terms);
+    if (!ok) {
+      for (int m = 0; m < Km; ++m) a.pos[m] += (u64)a.took[m];
+      exhausted = 1;
+      break;
+    }
+    // repetition count: every key with took > 0 can serve floor(avail / took) chunks
+    long long rep = a.max_chunks - chunks;
+    for (int m = 0; m < Km; ++m) {
+      if (a.took[m] <= 0) continue;
+      u64 len = a.seg_pre[a.s_off[m + 1] + m];
+      long long avail = (long long)(len - a.pos[m]);
+      long long r = avail / a.took[m];
+      if (r < rep) rep = r;
+    }
+    if (rep < 1) rep = 1;
+    Phase& ph = a.phases[n_ph++];
+    ph.chunk_begin = chunks;
+    ph.n_chunks = rep;
+    ph.term_begin = n_terms;
+    long long nt = 0;
+    for (int m = 0; m < Km; ++m) {
+      if (a.took[m] <= 0) continue;
+      Term& tm = a.terms[n_terms + nt++];
+      tm.m = (u32)m;
+      tm.stream = (u32)m;
+      tm.base = a.pos[m];
+      tm.len = (u64)a.took[m];
+      tm.stride = (u64)a.took[m];
+      a.pos[m] += (u64)a.took[m] * (u64)rep;
+    }
+    ph.n_terms = nt;
+    n_terms += nt;
+    chunks += rep;
+  }
+  a.out[0] = chunks;
+  a.out[1] = n_ph;
+  a.out[2] = n_terms;
+  a.out[3] = exhausted;
+}
+
+// arbitrary mode: one stream, chunk k = [k*C, (k+1)*C) clipped
+__global__ void plan_arbitrary_kernel(const u64* seg_pre, long long nseg, long long C, long long max_chunks,
+                                      Phase* phases, Term* terms, long long* out, u64* pos) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  u64 total = seg_pre[nseg];
+  const long long n_avail = (long long)((total + (u64)C - 1) / (u64)C);
+  long long n = n_avail < max_chunks ? n_avail : max_chunks;
+  const long long exhausted = n_avail < max_chunks ? 1 : 0;  // one more call would return None
+  long long full = (long long)(total / (u64)C);
+  if (full > n) full = n;
+  long long np = 0, nt = 0;
+  if (full > 0) {
+    phases[np] = Phase{0, full, nt, 1};
+    terms[nt] = Term{0, 0, 0, (u64)C, (u64)C};
+    ++np; ++nt;
+  }
+  if (n > full) {  // short tail chunk
+    u64 b = (u64)full * (u64)C;
+    phases[np] = Phase{full, 1, nt, 1};
+    terms[nt] = Term{0, 0, b, total - b, 0};
+    ++np; ++nt;
+  }
+  u64 used = (u64)full * (u64)C;
+  if (n > full) used = total;
+  pos[0] = used;
+  out[0] = n;
+  out[1] = np;
+  out[2] = nt;
+  out[3] = exhausted;
+}
+
+// ------------------------------------------------------------------ emission
+struct EmitArgs {
+  const Phase* phases;
+  long long n_phases;
+  const Term* terms;
+  const u64* pair_pre;  // [n_phases+1] pair prefix
+  // streams
+  const u32* s_off;
+  const u32* seg_comp;
+  const u64* seg_lo;
+  const u64* seg_pre;
+  int arbitrary;
+  // cursor layout
+  const u32* key_blk_first;
+  const u32* blk_first;
+  const u32* civ;
+  const u64* ccum;
+  const u32* iv_start;
+  const u32* iv_end;
+  const u32* iv_file;
+};
+
+__device__ __forceinline__ long long ub_u64(const u64* v, long long lo, long long hi, u64 x) {
+  // first index in [lo, hi) with v[idx] > x
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if (v[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int phase_of_pair(const EmitArgs& a, u64 pair) {
+  long long lo = 0, hi = a.n_phases;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if (a.pair_pre[mid + 1] <= pair) lo = mid + 1; else hi = mid;
+  }
+  return (int)lo;
+}
+
+// Walk the stream range of one (chunk, term) pair. WRITE=false: count pieces.
+template <bool WRITE>
+__device__ u64 walk_pair(const EmitArgs& a, u64 pair, long long* chunk_out, u32* pm, u32* pf, u32* ps, u32* pe,
+                         u64 out_base) {
+  const int p = phase_of_pair(a, pair);
+  const Phase ph = a.phases[p];
+  const u64 local = pair - a.pair_pre[p];
+  const long long kr = (long long)(local / (u64)ph.n_terms);
+  const Term tm = a.terms[ph.term_begin + (long long)(local % (u64)ph.n_terms)];
+  if (chunk_out) *chunk_out = ph.chunk_begin + kr;
+  const u32 s = tm.stream;
+  const long long sb = a.s_off[s], se = a.s_off[s + 1];
+  const u64* pre = a.seg_pre + s;  // stream s prefix lives at seg_pre[i + s]
+  u64 x = tm.base + (u64)kr * tm.stride;
+  u64 y = x + tm.len;
+  const u64 send = pre[se];
+  if (y > send) y = send;
+  u64 n = 0;
+  if (x >= y) return 0;
+  long long i = ub_u64(pre, sb, se, x) - 1;  // segment containing x
+  while (x < y) {
+    const u32 c = a.seg_comp[i];
+    const u64 seg_start = pre[i], seg_end = pre[i + 1];
+    const u64 lo_abs = a.seg_lo[i] + (x - seg_start);
+    const u64 hi_abs = a.seg_lo[i] + ((y < seg_end ? y : seg_end) - seg_start);
+    // component c occupies civ/ccum range [ib, ie)
+    const long long ib = a.blk_first[a.key_blk_first[c]];
+    const long long ie = a.blk_first[a.key_blk_first[c + 1]];
+    const u64 cb = a.ccum[ib];
+    long long j = ub_u64(a.ccum, ib, ie, cb + lo_abs) - 1;
+    const long long j1 = ub_u64(a.ccum, ib, ie, cb + hi_abs - 1) - 1;
+    if (!WRITE) {
+      n += (u64)(j1 - j + 1);
+    } else {
+      for (; j <= j1; ++j) {
+        const u32 iv = a.civ[j];
+        const u64 off = a.ccum[j] - cb;
+        const u64 len = a.ccum[j + 1] - a.ccum[j];
+        const u64 from = lo_abs > off ? lo_abs : off;
+        const u64 to = hi_abs < off + len ? hi_abs : off + len;
+        const u64 o = out_base + n++;
+        pm[o] = a.arbitrary ? c : tm.m;
+        pf[o] = a.iv_file[iv];
+        ps[o] = a.iv_start[iv] + (u32)(from - off);
+        pe[o] = a.iv_start[iv] + (u32)(to - off);
+      }
+    }
+    x = seg_end < y ? seg_end : y;
+    ++i;
+  }
+  return n;
+}
+
+__global__ void emit_count_kernel(EmitArgs a, u64 n_pairs, u64* pair_cnt) {
+  u64 pr = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  if (pr >= n_pairs) return;
+  pair_cnt[pr] = walk_pair<false>(a, pr, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
+}
+
+__global__ void emit_write_kernel(EmitArgs a, u64 n_pairs, const u64* pair_off, u32* pm, u32* pf, u32* ps, u32* pe) {
+  u64 pr = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  if (pr >= n_pairs) return;
+  walk_pair<true>(a, pr, nullptr, pm, pf, ps, pe, pair_off[pr]);
+}
+
+// first pair of every chunk (+ sentinel) -> piece range per chunk
+__global__ void chunk_pieces_kernel(EmitArgs a, long long n_chunks, const u64* pair_off, u64 n_pairs,
+                                    u64* chunk_piece_off) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k > n_chunks) return;
+  if (k == n_chunks) {
+    chunk_piece_off[k] = pair_off[n_pairs];
+    return;
+  }
+  long long lo = 0, hi = a.n_phases;
+  while (lo < hi) {  // last phase with chunk_begin <= k
+    long long mid = (lo + hi) >> 1;
+    if (a.phases[mid].chunk_begin <= k) lo = mid + 1; else hi = mid;
+  }
+  const int p = (int)lo - 1;
+  const Phase ph = a.phases[p];
+  u64 first = a.pair_pre[p] + (u64)(k - ph.chunk_begin) * (u64)ph.n_terms;
+  chunk_piece_off[k] = pair_off[first];
+}
+
+// ---- per-chunk sort (mixture key, file, start) + merge of adjacent ranges
+__device__ __forceinline__ bool piece_less(uint4 x, uint4 y) {
+  if (x.x != y.x) return x.x < y.x;
+  if (x.y != y.y) return x.y < y.y;
+  return x.z < y.z;
+}
+
+// sorts s[0..n) (n <= cap, padded to a power of two with max sentinels),
+// then merges in place; returns merged count. Called by `nt` threads.
+__device__ u32 sort_merge(uint4* s, u32 n, int tid, int nt, u32* s_flags) {
+  u32 np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  for (u32 i = n + tid; i < np2; i += nt) s[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+  __syncthreads();
+  for (u32 k = 2; k <= np2; k <<= 1) {
+    for (u32 j = k >> 1; j > 0; j >>= 1) {
+      for (u32 i = tid; i < np2; i += nt) {
+        u32 l = i ^ j;
+        if (l > i) {
+          uint4 a = s[i], b = s[l];
+          bool up = (i & k) == 0;
+          if (piece_less(b, a) == up) {
+            s[i] = b;
+            s[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // heads: not (same key, same file, contiguous)
+  for (u32 i = tid; i < n; i += nt) {
+    bool head = i == 0 || !(s[i].x == s[i - 1].x && s[i].y == s[i - 1].y && s[i].z == s[i - 1].w);
+    s_flags[i] = head ? 1u : 0u;
+  }
+  __syncthreads();
+  // sequential prefix by thread 0 is fine for the small per-chunk counts
+  __shared__ u32 s_m;
+  if (tid == 0) {
+    u32 run = 0;
+    for (u32 i = 0; i < n; ++i) {
+      run += s_flags[i];
+      s_flags[i] = run;  // inclusive head count
+    }
+    s_m = run;
+  }
+  __syncthreads();
+  // compaction into the front of a second half is unsafe in place; stage ends
+  uint4 mine[8];
+  int cnt = 0;
+  for (u32 i = tid; i < n; i += nt) {
+    bool last = (i + 1 == n) || (s_flags[i + 1] != s_flags[i]);
+    if (last && cnt < 8) mine[cnt++] = make_uint4(i, s_flags[i] - 1, s[i].w, 0);
+  }
+  __syncthreads();
+  // heads: write (m, f, start) to slot; ends: patch end
+  uint4 heads[8];
+  int hc = 0;
+  for (u32 i = tid; i < n; i += nt) {
+    bool head = (i == 0) || (s_flags[i] != s_flags[i - 1]);
+    if (head && hc < 8) heads[hc++] = make_uint4(s_flags[i] - 1, s[i].x, s[i].y, s[i].z);
+  }
+  __syncthreads();
+  for (int h = 0; h < hc; ++h) s[heads[h].x] = make_uint4(heads[h].y, heads[h].z, heads[h].w, 0);
+  __syncthreads();
+  for (int h = 0; h < cnt; ++h) s[mine[h].y].w = mine[h].z;
+  __syncthreads();
+  return s_m;
+}
+
+constexpr int NM_THREADS = 256;
+constexpr int NM_CAP = 2048;
+
+__global__ void __launch_bounds__(NM_THREADS)
+normalize_kernel(long long n_chunks, const u64* chunk_piece_off, u32* pm, u32* pf, u32* ps, u32* pe,
+                 u64* merged_cnt, u32* too_big) {
+  __shared__ uint4 s[NM_CAP];
+  __shared__ u32 s_flags[NM_CAP];
+  for (long long k = blockIdx.x; k < n_chunks; k += gridDim.x) {
+    const u64 o0 = chunk_piece_off[k], o1 = chunk_piece_off[k + 1];
+    const u32 n = (u32)(o1 - o0);
+    if (n > NM_CAP) {
+      if (threadIdx.x == 0) atomicMax(too_big, n);
+      continue;
+    }
+    for (u32 i = threadIdx.x; i < n; i += NM_THREADS) s[i] = make_uint4(pm[o0 + i], pf[o0 + i], ps[o0 + i], pe[o0 + i]);
+    __syncthreads();
+    u32 m = n ? sort_merge(s, n, threadIdx.x, NM_THREADS, s_flags) : 0;
+    for (u32 i = threadIdx.x; i < m; i += NM_THREADS) {
+      pm[o0 + i] = s[i].x;
+      pf[o0 + i] = s[i].y;
+      ps[o0 + i] = s[i].z;
+      pe[o0 + i] = s[i].w;
+    }
+    if (threadIdx.x == 0) merged_cnt[k] = m;
+    __syncthreads();
+  }
+}
+
+// exclusive scan of merged counts -> res_off (single CTA, loops)
+__global__ void offsets_kernel(long long n, const u64* cnt, long long* off) {
+  __shared__ u64 s_w[32];
+  __shared__ u64 s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (long long b = 0; b < n; b += blockDim.x) {
+    long long i = b + threadIdx.x;
+    u64 v = i < n ? cnt[i] : 0;
+    u64 inc = warp_incl_scan(v);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      u64 x = lane < nw ? s_w[lane] : 0;
+      u64 xi = warp_incl_scan(x);
+      if (lane < nw) s_w[lane] = xi - x;
+    }
+    __syncthreads();
+    u64 ex = s_carry + s_w[warp] + inc - v;
+    if (i < n) off[i] = (long long)ex;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = ex + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[n] = (long long)s_carry;
+}
+
+__global__ void compact_kernel(long long n_chunks, const u64* chunk_piece_off, const long long* res_off, const u32* pm,
+                               const u32* pf, const u32* ps, const u32* pe, u32* rm, u32* rf, u32* rs, u32* re) {
+  for (long long k = blockIdx.x; k < n_chunks; k += gridDim.x) {
+    const u64 src = chunk_piece_off[k];
+    const long long dst = res_off[k], n = res_off[k + 1] - res_off[k];
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+      rm[dst + i] = pm[src + i];
+      rf[dst + i] = pf[src + i];
+      rs[dst + i] = ps[src + i];
+      re[dst + i] = pe[src + i];
+    }
+  }
+}
+
+// chunk seeds: derive_seed(job_seed, "chunk", chunk_id)  (chunks.py:188)
+__global__ void chunk_seed_kernel(long long n, long long first_id, const uint8_t* prefix, int prefix_len, u64* seeds,
+                                  long long* ids) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  uint8_t dec[20];
+  const long long id = first_id + k;
+  int dl = u64_to_dec((u64)id, dec);
+  Blake2b b;
+  b.init();
+  b.bytes(prefix, prefix_len);
+  b.len8((u64)dl);
+  b.bytes(dec, dl);
+  seeds[k] = b.seed63();
+  ids[k] = id;
+}
+
+// pair prefix over phases (single CTA)
+__global__ void pair_prefix_kernel(const Phase* ph, long long n, u64* pre) {
+  if (threadIdx.x != 0) return;
+  u64 run = 0;
+  for (long long p = 0; p < n; ++p) {
+    pre[p] = run;
+    run += (u64)ph[p].n_chunks * (u64)ph[p].n_terms;
+  }
+  pre[n] = run;
+}
+
+// ------------------------------------------------------------------ host
+struct PlanWork {
+  int mode = 0;
+  int n_streams = 0;
+  DevBuf<u32> s_off, seg_comp;
+  DevBuf<u64> seg_lo, seg_pre;
+};
+
+static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, const DevBuf<Term>& terms,
+                long long n_chunks, long long n_phases, cudaStream_t s) {
+  IndexData* ix = g->ix;
+  g->res_chunks = n_chunks;
+  g->res_ranges = 0;
+  MX_CUDA_TRY(g->res_off.alloc(n_chunks + 1, s));
+  MX_CUDA_TRY(g->res_seed.alloc(n_chunks > 0 ? n_chunks : 1, s));
+  MX_CUDA_TRY(g->res_id.alloc(n_chunks > 0 ? n_chunks : 1, s));
+  if (n_chunks == 0) {
+    const long long z = 0;
+    MX_CUDA_TRY(cudaMemcpyAsync(g->res_off.p, &z, sizeof(z), cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(cudaStreamSynchronize(s));
+    return MX_OK;
+  }
+  DevBuf<u64> pair_pre;
+  MX_CUDA_TRY(pair_pre.alloc(n_phases + 1, s));
+  pair_prefix_kernel<<<1, 32, 0, s>>>(phases.p, n_phases, pair_pre.p);
+  u64 n_pairs = 0;
+  MX_CUDA_TRY(cudaMemcpyAsync(&n_pairs, pair_pre.p + n_phases, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  EmitArgs a{};
+  a.phases = phases.p;
+  a.n_phases = n_phases;
+  a.terms = terms.p;
+  a.pair_pre = pair_pre.p;
+  a.s_off = w.s_off.p;
+  a.seg_comp = w.seg_comp.p;
+  a.seg_lo = w.seg_lo.p;
+  a.seg_pre = w.seg_pre.p;
+  a.arbitrary = w.mode == 2;
+  a.key_blk_first = ix->key_blk_first.p;
+  a.blk_first = ix->blk_first.p;
+  a.civ = g->civ.p;
+  a.ccum = g->ccum.p;
+  a.iv_start = ix->iv_start.p;
+  a.iv_end = ix->iv_end.p;
+  a.iv_file = ix->iv_file.p;
+  DevBuf<u64> pair_off;
+  MX_CUDA_TRY(pair_off.alloc(n_pairs + 1, s));
+  const unsigned pb = (unsigned)((n_pairs + 255) / 256);
+  emit_count_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p);
+  // exclusive scan of counts in place (+ total at [n_pairs])
+  {
+    DevBuf<long long> tmp;
+    MX_CUDA_TRY(tmp.alloc(n_pairs + 1, s));
+    offsets_kernel<<<1, 1024, 0, s>>>((long long)n_pairs, pair_off.p, tmp.p);
+    MX_CUDA_TRY(cudaMemcpyAsync(pair_off.p, tmp.p, sizeof(u64) * (n_pairs + 1), cudaMemcpyDeviceToDevice, s));
+  }
+  u64 n_pieces = 0;
+  MX_CUDA_TRY(cudaMemcpyAsync(&n_pieces, pair_off.p + n_pairs, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  DevBuf<u32> pm, pf, ps, pe;
+  const long long cap = n_pieces > 0 ? (long long)n_pieces : 1;
+  MX_CUDA_TRY(pm.alloc(cap, s));
+  MX_CUDA_TRY(pf.alloc(cap, s));
+  MX_CUDA_TRY(ps.alloc(cap, s));
+  MX_CUDA_TRY(pe.alloc(cap, s));
+  emit_write_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p);
+  DevBuf<u64> cpo, mcnt;
+  DevBuf<u32> big;
+  MX_CUDA_TRY(cpo.alloc(n_chunks + 1, s));
+  MX_CUDA_TRY(mcnt.alloc(n_chunks, s));
+  MX_CUDA_TRY(big.alloc(1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(big.p, 0, sizeof(u32), s));
+  chunk_pieces_kernel<<<(unsigned)((n_chunks + 256) / 256), 256, 0, s>>>(a, n_chunks, pair_off.p, n_pairs, cpo.p);
+  {
+    long long grid = n_chunks < 148 * 8 ? n_chunks : 148 * 8;
+    normalize_kernel<<<(unsigned)grid, NM_THREADS, 0, s>>>(n_chunks, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p, big.p);
+  }
+  offsets_kernel<<<1, 1024, 0, s>>>(n_chunks, mcnt.p, g->res_off.p);
+  u32 h_big = 0;
+  long long total = 0;
+  MX_CUDA_TRY(cudaMemcpyAsync(&h_big, big.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(&total, g->res_off.p + n_chunks, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_big) return mx_fail(MX_ERR_UNSUPPORTED, "a chunk has %u ranges before merging (> %d supported)", h_big, NM_CAP);
+  g->res_ranges = total;
+  const long long rc = total > 0 ? total : 1;
+  MX_CUDA_TRY(g->res_mkey.alloc(rc, s));
+  MX_CUDA_TRY(g->res_file.alloc(rc, s));
+  MX_CUDA_TRY(g->res_start.alloc(rc, s));
+  MX_CUDA_TRY(g->res_end.alloc(rc, s));
+  {
+    long long grid = n_chunks < 148 * 8 ? n_chunks : 148 * 8;
+    compact_kernel<<<(unsigned)grid, 128, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
+                                                  g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p);
+  }
+  chunk_seed_kernel<<<(unsigned)((n_chunks + 127) / 128), 128, 0, s>>>(n_chunks, g->next_chunk_id, g->chunk_prefix.p,
+                                                                      g->chunk_prefix_len, g->res_seed.p, g->res_id.p);
+  MX_CUDA_TRY(cudaGetLastError());
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  g->next_chunk_id += n_chunks;
+  return MX_OK;
+}
+
+int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, long long* n_out) {
+  cudaStream_t s = g->stream;
+  IndexData* ix = g->ix;
+  const int Km = mix->n_mkeys;
+  const long long K = g->K;
+  *n_out = 0;
+  if (Km < 1) return mx_fail(MX_ERR_MIXTURE, "mixture has no keys");
+  if (mix->chunk_size < 1) return mx_fail(MX_ERR_MIXTURE, "chunk_size must be positive");
+  if (mix->strict && mix->chunk_size < Km)
+    return mx_fail(MX_ERR_MIXTURE, "chunk size %lld below the number of mixture keys (%d)", (long long)mix->chunk_size, Km);
+  g->report.assign(Km, 0);
+  g->last_mkeys = Km;
+  // ---- matching
+  MatchArgs ma{};
+  ma.Km = Km;
+  ma.K = K;
+  ma.comp_order = g->comp_order.p;
+  ma.key_packed = ix->key_packed.p;
+  ma.n_props = ix->n_props;
+  for (int p = 0; p < ix->n_props; ++p) {
+    ma.shift[p] = ix->field_shift[p];
+    ma.width[p] = ix->field_width[p];
+    ma.allow_base[p] = mix->allow_base[p];
+  }
+  ma.allow_words = mix->allow_words;
+  DevBuf<u32> allow, L_cnt, hits;
+  DevBuf<double> wts;
+  MX_CUDA_TRY(allow.alloc((long long)Km * mix->allow_words, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(allow.p, mix->allow, sizeof(u32) * Km * mix->allow_words, cudaMemcpyHostToDevice, s));
+  ma.allow = allow.p;
+  MX_CUDA_TRY(wts.alloc(Km, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(wts.p, mix->weights, sizeof(double) * Km, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(L_cnt.alloc(Km, s));
+  MX_CUDA_TRY(hits.alloc(K > 0 ? K : 1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(hits.p, 0, sizeof(u32) * (K > 0 ? K : 1), s));
+  if (K > 0) match_count_kernel<<<Km, 256, 0, s>>>(ma, L_cnt.p, hits.p);
+  std::vector<u32> h_cnt(Km), h_hits(K > 0 ? K : 1, 0);
+  MX_CUDA_TRY(cudaMemcpyAsync(h_cnt.data(), L_cnt.p, sizeof(u32) * Km, cudaMemcpyDeviceToHost, s));
+  if (K > 0) MX_CUDA_TRY(cudaMemcpyAsync(h_hits.data(), hits.p, sizeof(u32) * K, cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<u32> h_off(Km + 1, 0);
+  for (int m = 0; m < Km; ++m) h_off[m + 1] = h_off[m] + h_cnt[m];
+  bool shared = false;
+  for (long long c = 0; c < K; ++c) shared |= h_hits[c] > 1;
+  DevBuf<u32> L_off, L;
+  MX_CUDA_TRY(L_off.alloc(Km + 1, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(L_off.p, h_off.data(), sizeof(u32) * (Km + 1), cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(L.alloc(h_off[Km] > 0 ? h_off[Km] : 1, s));
+  if (K > 0) match_fill_kernel<<<Km, 256, 0, s>>>(ma, L_off.p, L.p);
+  // ---- streams
+  PlanWork w;
+  w.mode = shared ? 1 : 0;
+  if (w.mode == 0) {
+    w.n_streams = Km;
+    MX_CUDA_TRY(w.s_off.alloc(Km + 1, s));
+    MX_CUDA_TRY(cudaMemcpyAsync(w.s_off.p, L_off.p, sizeof(u32) * (Km + 1), cudaMemcpyDeviceToDevice, s));
+    const long long nseg = h_off[Km];
+    MX_CUDA_TRY(w.seg_comp.alloc(nseg > 0 ? nseg : 1, s));
+    MX_CUDA_TRY(w.seg_lo.alloc(nseg > 0 ? nseg : 1, s));
+    MX_CUDA_TRY(w.seg_pre.alloc(nseg + Km, s));
+    build_segments_kernel<<<(Km + 127) / 128, 128, 0, s>>>(0, Km, w.s_off.p, L.p, g->comp_total.p, g->consumed.p,
+                                                          w.seg_comp.p, w.seg_lo.p, w.seg_pre.p);
+  } else {
+    w.n_streams = (int)K;
+    std::vector<u32> so(K + 1);
+    for (long long c = 0; c <= K; ++c) so[c] = (u32)c;
+    MX_CUDA_TRY(w.s_off.alloc(K + 1, s));
+    MX_CUDA_TRY(cudaMemcpyAsync(w.s_off.p, so.data(), sizeof(u32) * (K + 1), cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(w.seg_comp.alloc(K, s));
+    MX_CUDA_TRY(w.seg_lo.alloc(K, s));
+    MX_CUDA_TRY(w.seg_pre.alloc(2 * K, s));
+    build_segments_kernel<<<(unsigned)((K + 127) / 128), 128, 0, s>>>(1, (int)K, w.s_off.p, nullptr, g->comp_total.p,
+                                                                      g->consumed.p, w.seg_comp.p, w.seg_lo.p,
+                                                                      w.seg_pre.p);
+    MX_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  // ---- plan
+  long long cap_phases, cap_terms;
+  if (w.mode == 1) {
+    cap_phases = max_chunks < (1 << 20) ? max_chunks : (1 << 20);
+    cap_terms = cap_phases * 4 + (long long)Km + mix->chunk_size + 64;
+  } else {
+    cap_phases = 4 * (long long)Km + 64;
+    if (cap_phases > max_chunks + 1) cap_phases = max_chunks + 1;
+    cap_terms = cap_phases * (long long)Km;
+    const long long term_budget = 1ll << 24;  // 512 MB of terms; the plan resumes on the next call
+    if (cap_terms > term_budget) cap_terms = term_budget > Km ? term_budget : Km;
+  }
+  DevBuf<Phase> phases;
+  DevBuf<Term> terms;
+  DevBuf<long long> scratch_ll, out, report;
+  DevBuf<unsigned char> flags;
+  DevBuf<u64> pos;
+  DevBuf<int> ap_idx;
+  DevBuf<double> ap_frac;
+  DevBuf<u32> front;
+  MX_CUDA_TRY(phases.alloc(cap_phases, s));
+  MX_CUDA_TRY(terms.alloc(cap_terms, s));
+  MX_CUDA_TRY(scratch_ll.alloc(5LL * Km, s));
+  MX_CUDA_TRY(out.alloc(4, s));
+  MX_CUDA_TRY(report.alloc(Km, s));
+  MX_CUDA_TRY(flags.alloc(2LL * Km, s));
+  MX_CUDA_TRY(pos.alloc(Km, s));
+  MX_CUDA_TRY(ap_idx.alloc(Km, s));
+  MX_CUDA_TRY(ap_frac.alloc(Km, s));
+  MX_CUDA_TRY(front.alloc(Km, s));
+  MX_CUDA_TRY(cudaMemsetAsync(front.p, 0, sizeof(u32) * Km, s));
+  MX_CUDA_TRY(cudaMemsetAsync(report.p, 0, sizeof(long long) * Km, s));
+  PlanArgs pa{};
+  pa.mode = w.mode;
+  pa.Km = Km;
+  pa.C = mix->chunk_size;
+  pa.strict = mix->strict;
+  pa.max_chunks = max_chunks;
+  pa.w = wts.p;
+  pa.seg_pre = w.seg_pre.p;
+  pa.s_off = w.s_off.p;
+  pa.L_off = L_off.p;
+  pa.L = L.p;
+  pa.comp_total = g->comp_total.p;
+  pa.consumed = g->consumed.p;
+  pa.front = front.p;
+  pa.counts = scratch_ll.p;
+  pa.rem = scratch_ll.p + Km;
+  pa.found = scratch_ll.p + 2 * Km;
+  pa.took = scratch_ll.p + 3 * Km;
+  pa.ap_base = scratch_ll.p + 4 * Km;
+  pa.dead = flags.p;
+  pa.newly = flags.p + Km;
+  pa.pos = pos.p;
+  pa.ap_idx = ap_idx.p;
+  pa.ap_frac = ap_frac.p;
+  pa.phases = phases.p;
+  pa.cap_phases = cap_phases;
+  pa.terms = terms.p;
+  pa.cap_terms = cap_terms;
+  pa.out = out.p;
+  pa.report = report.p;
+  plan_kernel<<<1, 32, 0, s>>>(pa);
+  long long h_out[4];
+  MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(g->report.data(), report.p, sizeof(long long) * Km, cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  if (w.mode == 0)
+    commit_segments_kernel<<<Km, 128, 0, s>>>(Km, w.s_off.p, w.seg_comp.p, w.seg_lo.p, w.seg_pre.p, pos.p,
+                                              g->consumed.p);
+  int rc = emit(g, w, phases, terms, h_out[0], h_out[1], s);
+  if (rc != MX_OK) return rc;
+  *n_out = h_out[0];
+  return h_out[3] ? MX_EXHAUSTED : MX_OK;
+}
+
+int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long long* n_out) {
+  cudaStream_t s = g->stream;
+  const long long K = g->K;
+  *n_out = 0;
+  if (chunk_size < 1) return mx_fail(MX_ERR_MIXTURE, "chunk_size must be positive");
+  g->last_mkeys = 0;
+  g->report.clear();
+  PlanWork w;
+  w.mode = 2;
+  w.n_streams = 1;
+  if (K == 0) {
+    int rc = emit(g, w, DevBuf<Phase>(), DevBuf<Term>(), 0, 0, s);
+    return rc != MX_OK ? rc : MX_EXHAUSTED;
+  }
+  std::vector<u32> so = {0u, (u32)K};
+  MX_CUDA_TRY(w.s_off.alloc(2, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(w.s_off.p, so.data(), sizeof(u32) * 2, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(w.seg_comp.alloc(K, s));
+  MX_CUDA_TRY(w.seg_lo.alloc(K, s));
+  MX_CUDA_TRY(w.seg_pre.alloc(K + 1, s));
+  build_segments_kernel<<<1, 32, 0, s>>>(2, 1, w.s_off.p, g->comp_order.p, g->comp_total.p, g->consumed.p,
+                                         w.seg_comp.p, w.seg_lo.p, w.seg_pre.p);
+  DevBuf<Phase> phases;
+  DevBuf<Term> terms;
+  DevBuf<long long> out;
+  DevBuf<u64> pos;
+  MX_CUDA_TRY(phases.alloc(2, s));
+  MX_CUDA_TRY(terms.alloc(2, s));
+  MX_CUDA_TRY(out.alloc(4, s));
+  MX_CUDA_TRY(pos.alloc(1, s));
+  plan_arbitrary_kernel<<<1, 32, 0, s>>>(w.seg_pre.p, K, chunk_size, max_chunks, phases.p, terms.p, out.p, pos.p);
+  long long h_out[4];
+  MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  commit_segments_kernel<<<1, 128, 0, s>>>(1, w.s_off.p, w.seg_comp.p, w.seg_lo.p, w.seg_pre.p, pos.p, g->consumed.p);
+  int rc = emit(g, w, phases, terms, h_out[0], h_out[1], s);
+  if (rc != MX_OK) return rc;
+  *n_out = h_out[0];
+  return h_out[3] ? MX_EXHAUSTED : MX_OK;
+}
+
+}  // namespace mx

@@ -1,0 +1,216 @@
+"""Device-resident catalog and ChunkerIndex (stage 1 behind the reference API).
+
+``build_index_from_catalog(catalog, predicates)`` is the drop-in for the
+reference's ``build_index(catalog.filter_intervals(predicates))``
+(``server.py:112-115``): one CUDA pipeline (``csrc/stage1.cu``) from the int32
+code columns in HBM to the key-major interval table, never materialising
+Python ``IntervalRow`` objects. ``ChunkerIndex`` exposes the reference's
+duck type (``index.py:50-85``) by decoding device tables lazily.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from .catalog import ColumnarCatalog, FilterPredicate
+from .codec import KeyCodec
+from .errors import QueryError
+from .mixtures import MixtureKey, sorted_keys
+
+
+class DeviceCatalog:
+    """A ``ColumnarCatalog`` uploaded to HBM (columns in property-name order)."""
+
+    def __init__(self, host: ColumnarCatalog, columns=None, nullable=None, device=None):
+        import torch
+
+        self.host = host
+        self.device = torch.device(device or "cuda")
+        props = sorted(host.vocab)
+        if columns is None:
+            columns = {p: torch.from_numpy(host.columns[p]).to(self.device) for p in props}
+        self.columns = {p: columns[p].contiguous() for p in props}
+        if nullable is None:
+            nullable = {p: bool((self.columns[p] < 0).any().item()) for p in props}
+        self.nullable = nullable
+        self.codec = KeyCodec.build(host.vocab, nullable)
+        self.file_offsets = torch.from_numpy(np.asarray(host.file_offsets, dtype=np.int64)).to(self.device)
+        ds = np.asarray(host.file_ds)
+        if len(ds) > 1 and np.any(np.diff(ds) < 0):
+            raise ValueError("dataset ids must be nondecreasing in file-id order (registration order)")
+        self.file_ds = np.ascontiguousarray(ds, dtype=np.int32)
+        self.file_ids = np.ascontiguousarray(host.file_ids, dtype=np.int64)
+        self._strings = self.codec.key_strings()
+
+    @staticmethod
+    def from_reference(cat, device=None) -> "DeviceCatalog":
+        return DeviceCatalog(ColumnarCatalog.from_reference(cat), device=device)
+
+    @property
+    def n_samples(self) -> int:
+        return self.host.n_samples
+
+    def descriptor(self, preds: list[FilterPredicate]):
+        """C struct for mx_index_build; returns (desc, keepalive)."""
+        codec = self.codec
+        lut, lut_off = codec.luts(self.host, preds)
+        cols = (C.c_void_p * len(codec.props))(*[self.columns[p].data_ptr() for p in codec.props])
+        blob, soff, sbase = self._strings
+        keep = dict(
+            lut=np.ascontiguousarray(lut), lut_off=np.ascontiguousarray(lut_off), cols=cols,
+            shift=np.array(codec.shift, dtype=np.uint32), width=np.array(codec.width, dtype=np.uint32),
+            blob=np.frombuffer(blob, dtype=np.uint8).copy() if blob else np.zeros(1, np.uint8),
+            soff=soff, sbase=sbase,
+        )
+        P = C.POINTER
+        d = _lib.CatalogDesc()
+        d.n_props = len(codec.props)
+        d.columns = C.cast(cols, P(C.c_void_p))
+        d.lut = keep["lut"].ctypes.data_as(P(C.c_uint32))
+        d.lut_offsets = keep["lut_off"].ctypes.data_as(P(C.c_int32))
+        d.n_samples = self.host.n_samples
+        d.n_files = self.host.n_files
+        d.file_offsets = self.file_offsets.data_ptr()
+        d.file_ds = self.file_ds.ctypes.data_as(P(C.c_int32))
+        d.file_ids = self.file_ids.ctypes.data_as(P(C.c_int64))
+        d.key_bits = codec.key_bits
+        d.rank_mask = codec.rank_mask
+        d.field_shift = keep["shift"].ctypes.data_as(P(C.c_uint32))
+        d.field_width = keep["width"].ctypes.data_as(P(C.c_uint32))
+        d.key_strings = keep["blob"].ctypes.data_as(P(C.c_uint8))
+        d.key_string_offsets = keep["soff"].ctypes.data_as(P(C.c_int64))
+        d.key_string_base = keep["sbase"].ctypes.data_as(P(C.c_int32))
+        return d, keep
+
+
+class ChunkerIndex:
+    """Immutable device index; same duck type as the reference ``ChunkerIndex``."""
+
+    def __init__(self, handle: int, catalog: DeviceCatalog, stream=None):
+        self._h = C.c_void_p(handle)
+        self.catalog = catalog
+        self.codec = catalog.codec
+        self.stream = stream
+        L = _lib.lib()
+        k, b, i, n = (C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64())
+        _lib.check(L.mx_index_sizes(self._h, C.byref(k), C.byref(b), C.byref(i), C.byref(n)))
+        self.n_keys, self.n_blocks, self.n_intervals, self.n_samples = k.value, b.value, i.value, n.value
+        self._keys = None
+        self._nested = None
+        self._counts = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib._handle is not None:
+            _lib._handle.mx_index_free(h)
+            self._h = None
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    # ---------------------------------------------------------- exports
+    def packed_keys(self) -> tuple[np.ndarray, np.ndarray]:
+        packed = np.zeros(self.n_keys, dtype=np.uint32)
+        samples = np.zeros(self.n_keys, dtype=np.int64)
+        if self.n_keys:
+            _lib.check(_lib.lib().mx_index_export_keys(self._h, _lib.ptr(packed), _lib.ptr(samples)))
+        return packed, samples
+
+    def interval_table(self) -> dict[str, np.ndarray]:
+        """Flat (key rank, ds, file id, start, end) in index order."""
+        n = self.n_intervals
+        out = dict(key=np.zeros(n, np.uint32), ds=np.zeros(n, np.int32), fid=np.zeros(n, np.int64),
+                   start=np.zeros(n, np.uint32), end=np.zeros(n, np.uint32))
+        if n:
+            _lib.check(_lib.lib().mx_index_export_intervals(
+                self._h, *(_lib.ptr(out[x]) for x in ("key", "ds", "fid", "start", "end"))))
+        return out
+
+    def table(self) -> list[tuple]:
+        """[(key canonical string, ds, fid, start, end)] -- the parity form."""
+        keys = self.component_keys()
+        ks = [k.canonical_string() for k in keys]
+        t = self.interval_table()
+        return [(ks[r], int(d), int(f), int(a), int(b))
+                for r, d, f, a, b in zip(t["key"], t["ds"], t["fid"], t["start"], t["end"])]
+
+    # ---------------------------------------------------------- reference duck type
+    def component_keys(self) -> list[MixtureKey]:
+        if self._keys is None:
+            packed, samples = self.packed_keys()
+            self._keys = [self.codec.decode(int(p)) for p in packed]
+            self._counts = samples
+        return list(self._keys)
+
+    def _nested_index(self):
+        if self._nested is None:
+            keys = self.component_keys()
+            t = self.interval_table()
+            nested: dict = {}
+            for r, d, f, a, b in zip(t["key"].tolist(), t["ds"].tolist(), t["fid"].tolist(),
+                                     t["start"].tolist(), t["end"].tolist()):
+                nested.setdefault(keys[r], {}).setdefault(d, {}).setdefault(f, []).append((a, b))
+            self._nested = nested
+        return self._nested
+
+    @property
+    def _index(self):
+        return self._nested_index()
+
+    def entries(self, key: MixtureKey):
+        return self._nested_index().get(key, {})
+
+    def matching_keys(self, mixture_key: MixtureKey) -> list[MixtureKey]:
+        return [k for k in self.component_keys() if mixture_key.matches(k)]
+
+    def key_sample_counts(self) -> dict[MixtureKey, int]:
+        keys = self.component_keys()
+        return {k: int(n) for k, n in zip(keys, self._counts)}
+
+    def total_samples(self) -> int:
+        return int(self.n_samples)
+
+    def __contains__(self, key) -> bool:
+        return key in set(self.component_keys())
+
+    def __eq__(self, other) -> bool:
+        mine = self._nested_index()
+        theirs = getattr(other, "_index", None)
+        if theirs is None:
+            return False
+        if isinstance(other, ChunkerIndex):
+            return self.table() == other.table()
+        conv = {MixtureKey(tuple(getattr(k, "entries", k))): v for k, v in theirs.items()}
+        return mine == conv
+
+    __hash__ = None
+
+
+def build_index_from_catalog(catalog, predicates: Sequence = (), stream=None) -> ChunkerIndex:
+    """Fused filter + intervals + index on the GPU.
+
+    ``catalog`` is a ``DeviceCatalog``, a ``ColumnarCatalog`` (uploaded), or a
+    reference ``MetadataCatalog`` (adapted then uploaded). Errors follow the
+    reference: unknown property / empty catalog / un-keyable sample ->
+    ``QueryError``.
+    """
+    if not isinstance(catalog, DeviceCatalog):
+        if not isinstance(catalog, ColumnarCatalog):
+            if not getattr(catalog, "_files", None):
+                raise QueryError("catalog is empty")
+            catalog = ColumnarCatalog.from_reference(catalog)
+        catalog = DeviceCatalog(catalog)
+    if catalog.host.n_files == 0:
+        raise QueryError("catalog is empty")
+    preds = catalog.host.validated(predicates)
+    desc, keep = catalog.descriptor(preds)
+    L = _lib.lib()
+    out = C.c_void_p()
+    _lib.check(L.mx_index_build(C.byref(desc), C.c_void_p(_lib.stream_ptr(stream)), C.byref(out)))
+    del keep
+    return ChunkerIndex(out.value, catalog, stream)
