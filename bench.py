@@ -1,0 +1,317 @@
+"""Benchmark of the Mixtera hot path on B200 (contract: one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], SURVEY.md §8d cfg 2): 100M samples in
+10,000 files, 5 int32 property columns (cards 4,5,5,4,5 -> 2,000 component
+keys), run layout R=64, static multi-property best-effort mixture, chunk 1024,
+job seed 42. Synthetic metadata (seeded run table expanded on the device);
+2 GB of columns > 126 MB L2, so no L2 flush is needed between steps.
+
+One STEP = the whole job on the device: stage 1 (filter + key pack + runs +
+grouping into the ChunkerIndex) + RangeCursor layout + emission of EVERY chunk
+of the job (planner + cut + normalise + CSR + seeds). value = samples/s
+(N / step time); chunks/s is reported beside it. `e2e` runs the same step
+through the public API from PINNED HOST columns (H2D inside the timed region)
+and copies the full chunk CSR back (D2H inside). The roofline line is for the
+dominant kernel (scan_runs, stage 1's streaming pass), timed with CUDA events
+recorded by the library on the launching stream.
+
+--impl reference times the CPU oracle port (oracle/oracle.py, a numpy/stdlib
+restatement of the reference's own algorithm) on a bounded slice of the same
+workload on the host cores. Under torchrun with N > 1 every rank indexes its
+own 100M-sample file shard (weak scaling) and the step time is the max over
+ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "samples indexed/sec + chunks/sec (1/2/4/8 B200) vs host-CPU ref; % HBM roofline"
+UNIT = "samples/s"
+CFG = dict(workload="cfg2: 100M samples, 10k files, 5 props (4,5,5,4,5) -> 2000 keys, R=64, "
+                    "static 4-key best-effort mixture, chunk 1024, seed 42",
+           n_samples=100_000_000, n_files=10_000, props=5, run_mean=64, chunk_size=1024, job_seed=42,
+           l2="inputs (2 GB of columns) exceed the 126 MB L2; no flush needed")
+REF_SAMPLE = 4_000_000  # --impl reference: samples per step (bounded CPU slice)
+CPU_SAMPLE = 10_000_000  # cpu_baseline leg of our arm
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], 0.0, set()
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for n, v in zip(names, r[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(rank: int, scale: float):
+    from paper_2502_19790_b200 import synth
+
+    n = int(CFG["n_samples"] * scale)
+    f = max(1, int(CFG["n_files"] * scale))
+    rt = synth.make_runs(n, f, synth.CFG2_PROPS, CFG["run_mean"], seed=2 + 1000 * rank)
+    return rt
+
+
+def device_columns(rt, device):
+    import torch
+
+    lens = torch.from_numpy(rt.run_lengths()).to(device)
+    return {p: torch.repeat_interleave(torch.from_numpy(c).to(device), lens) for p, c in rt.run_codes.items()}
+
+
+def run_step(meta, cols, spec, stream=None):
+    """One job on the device: index + cursor layout + every chunk. Returns
+    (index, batch) so callers can read sizes."""
+    from paper_2502_19790_b200 import ChunkGenerator, DeviceCatalog, build_index_from_catalog
+
+    dcat = DeviceCatalog(meta, columns=cols, nullable={p: False for p in cols})
+    idx = build_index_from_catalog(dcat, [], stream=stream)
+    gen = ChunkGenerator(idx, CFG["job_seed"], stream=stream)
+    batch = gen.plan_batch(spec, 1 << 40)
+    return idx, gen, batch
+
+
+def cpu_port(n_samples: int, rank: int = 0):
+    """Oracle port on a bounded slice of the workload (host cores, 1 thread)."""
+    from oracle import oracle as orc
+    from paper_2502_19790_b200 import synth
+
+    f = max(1, n_samples // (CFG["n_samples"] // CFG["n_files"]))
+    cc = synth.expand_numpy(synth.make_runs(n_samples, f, synth.CFG2_PROPS, CFG["run_mean"], seed=2))
+    spec = synth.cfg2_mixture(CFG["chunk_size"])
+    w = {orc.as_key(k): v for k, v in spec.weights.items()}
+    t0 = time.perf_counter()
+    idx = orc.build_index(cc, [])
+    gen = orc.OracleGenerator(idx, CFG["job_seed"])
+    chunks = 0
+    while gen.generate(w, spec.chunk_size, spec.strict) is not None:
+        chunks += 1
+    dt = time.perf_counter() - t0
+    return dt, chunks
+
+
+def reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_port(REF_SAMPLE)
+    times, chunks = [], 0
+    for _ in range(args.steps):
+        dt, chunks = cpu_port(REF_SAMPLE)
+        times.append(dt)
+    t = sum(times) / len(times)
+    v = REF_SAMPLE / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": dict(CFG, workload=CFG["workload"] + f" (CPU slice: first {REF_SAMPLE:,} samples)"),
+        "chunks_per_s": chunks / t,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{REF_SAMPLE:,} samples of the cfg2 layout per step (oracle/oracle.py, "
+                                   "numpy + CPython stdlib, single thread like the GIL-bound reference)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def our_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_19790_b200 import _lib, synth
+    from paper_2502_19790_b200.catalog import ColumnarCatalog
+
+    rank, world, local = env_rank()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(device)
+    L = _lib.lib()
+    rt = make_workload(rank, args.scale)
+    meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
+    cols = device_columns(rt, device)
+    spec = synth.cfg2_mixture(CFG["chunk_size"])
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        idx, gen, batch = run_step(meta, cols, spec)
+        del idx, gen, batch
+    barrier()
+    # ---------------------------------------------------------------- timed
+    L.mx_profile_reset()
+    L.mx_profile_enable(1)
+    clocks = Clocks(device.index)
+    launches0 = L.mx_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    n_chunks = n_ranges = n_iv = 0
+    for _ in range(args.steps):
+        idx, gen, batch = run_step(meta, cols, spec)
+        n_chunks, n_ranges, n_iv = batch.n_chunks, batch.n_ranges, idx.n_intervals
+        n_keys, n_blocks = idx.n_keys, idx.n_blocks
+        del idx, gen, batch
+    ev1.record(stream)
+    barrier()
+    launches = (L.mx_launch_count() - launches0) / args.steps
+    clk = clocks.stop()
+    L.mx_profile_enable(0)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    phases = {p: _lib.profile_read(p) for p in ("scan_runs", "radix_sort", "index_scans", "cursor_layout",
+                                                 "cursor_shuffle", "plan", "emit")}
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    n = rt.n_samples
+    # ------------------------------------------------------------ e2e (host buffers)
+    pinned = {p: c.cpu().pin_memory() for p, c in cols.items()}
+    del cols
+    torch.cuda.empty_cache()
+    h2d = sum(x.numel() * 4 for x in pinned.values())
+
+    def e2e_step():
+        dcols = {p: x.to(device, non_blocking=True) for p, x in pinned.items()}
+        idx, gen, batch = run_step(meta, dcols, spec)
+        h = batch.to_host()
+        return sum(v.nbytes for k, v in h.items() if k in ("off", "ids", "seeds")) + 16 * batch.n_ranges
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    d2h = 0
+    for _ in range(args.steps):
+        d2h = e2e_step()
+    e1.record(stream)
+    barrier()
+    ems = e0.elapsed_time(e1) / args.steps
+    te = torch.tensor([ems], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    ems = float(te.item())
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    # ------------------------------------------------------------ roofline
+    peak, peak_kind = peaks()
+    scan_ms, scan_n = phases["scan_runs"]
+    scan_avg = scan_ms / max(scan_n, 1)
+    scan_bytes = n * 4 * len(rt.run_codes) + 16 * n_iv
+    achieved = scan_bytes / (scan_avg * 1e-3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "scan_runs_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": world * n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": dict(CFG, parallelism=f"file-sharded x{world}" if world > 1 else "single GPU"),
+        "chunks_per_s": world * n_chunks / (ms_max * 1e-3),
+        "job": {"samples": n, "intervals": n_iv, "keys": n_keys, "blocks": n_blocks, "chunks": n_chunks,
+                "ranges": n_ranges},
+        "phases_ms": {p: round(v[0] / max(v[1], 1), 4) for p, v in phases.items()},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "scan_runs_kernel",
+                     "bytes_per_launch": scan_bytes, "peak_kind": peak_kind,
+                     "note": "algorithmic bytes = N*4*P column reads + 16 B per interval record"},
+        "e2e": {"value": world * n / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems},
+        "gpu_launches": int(launches * args.steps),
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        dt, chunks = cpu_port(CPU_SAMPLE)
+        line["cpu_baseline"] = {"value": CPU_SAMPLE / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                                "chunks_per_s": chunks / dt,
+                                "sample": f"first {CPU_SAMPLE:,} samples ({CPU_SAMPLE // 10_000} files) of the cfg2 "
+                                          "layout through oracle/oracle.py (numpy + CPython stdlib, 1 thread)"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0, help="fraction of the cfg2 size (debug only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        our_arm(args)
+
+
+if __name__ == "__main__":
+    main()

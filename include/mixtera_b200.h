@@ -46,6 +46,14 @@ typedef struct mx_gen mx_gen;
 const char* mx_last_error(void);
 /* ABI version; bumps on any signature change. */
 int mx_abi_version(void);
+/* Kernels this library has launched since it was loaded (all streams). */
+int64_t mx_launch_count(void);
+/* Per-phase CUDA-event timing on the launching stream: phases are
+ * "scan_runs" (the stage-1 streaming kernel alone), "radix_sort",
+ * "index_scans", "cursor_layout", "cursor_shuffle", "plan", "emit". */
+int mx_profile_enable(int on);
+int mx_profile_reset(void);
+int mx_profile_read(const char* phase, double* total_ms, int64_t* count);
 
 /* ------------------------------------------------------------------ stage 1
  * Columnar catalog + filter, encoded by the host (codec.py):

@@ -77,6 +77,10 @@ class MixtureDesc(C.Structure):
 _SIGS = {
     "mx_last_error": (C.c_char_p, []),
     "mx_abi_version": (C.c_int, []),
+    "mx_launch_count": (i64, []),
+    "mx_profile_enable": (C.c_int, [C.c_int]),
+    "mx_profile_reset": (C.c_int, []),
+    "mx_profile_read": (C.c_int, [C.c_char_p, P(dbl), P(i64)]),
     "mx_index_build": (C.c_int, [P(CatalogDesc), vp, P(vp)]),
     "mx_index_free": (C.c_int, [vp]),
     "mx_index_sizes": (C.c_int, [vp, P(i64), P(i64), P(i64), P(i64)]),
@@ -142,6 +146,12 @@ def check(rc: int) -> int:
         return rc
     msg = _handle.mx_last_error().decode("utf-8", "replace") if _handle else "error"
     raise _ERRORS.get(rc, DeviceError)(msg)
+
+
+def profile_read(phase: str) -> tuple[float, int]:
+    ms, n = dbl(), i64()
+    check(lib().mx_profile_read(phase.encode(), C.byref(ms), C.byref(n)))
+    return ms.value, n.value
 
 
 def stream_ptr(stream=None) -> int:

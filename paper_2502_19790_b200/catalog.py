@@ -90,6 +90,8 @@ class ColumnarCatalog:
     file_paths: dict[int, str] = field(default_factory=dict)
 
     def __post_init__(self):
+        if getattr(self, "_meta_only", False):
+            return
         self.file_ids = np.asarray(self.file_ids, dtype=np.int64)
         self.file_ds = np.asarray(self.file_ds, dtype=np.int32)
         self.file_offsets = np.asarray(self.file_offsets, dtype=np.int64)
@@ -158,6 +160,25 @@ class ColumnarCatalog:
                         hit[c + 1] = True
             ok &= hit if pred.positive else ~hit
         return ok
+
+    @staticmethod
+    def meta_only(vocab, file_sizes, file_ds=None, file_ids=None, multiple=None) -> "ColumnarCatalog":
+        """Catalog metadata without host columns (the columns live only in HBM,
+        e.g. expanded on the device by bench.py)."""
+        sizes = np.asarray(file_sizes, dtype=np.int64)
+        offsets = np.zeros(len(sizes) + 1, dtype=np.int64)
+        np.cumsum(sizes, out=offsets[1:])
+        obj = ColumnarCatalog.__new__(ColumnarCatalog)
+        obj._meta_only = True
+        obj.columns = {p: None for p in vocab}
+        obj.vocab = {k: list(v) for k, v in vocab.items()}
+        obj.multiple = {p: bool((multiple or {}).get(p, False)) for p in vocab}
+        obj.file_ids = np.arange(1, len(sizes) + 1, dtype=np.int64) if file_ids is None else np.asarray(file_ids, np.int64)
+        obj.file_ds = np.zeros(len(sizes), np.int32) if file_ds is None else np.asarray(file_ds, np.int32)
+        obj.file_offsets = offsets
+        obj.dataset_names = [f"ds{i}" for i in range(int(obj.file_ds.max()) + 1 if len(sizes) else 0)]
+        obj.file_paths = {}
+        return obj
 
     # ------------------------------------------------------------ adapters
     @staticmethod

@@ -20,6 +20,79 @@ int ado_credit(int k, double rate, const double* pi, double* credit, cudaStream_
 
 static thread_local std::string g_err;
 
+// ---------------------------------------------------------------- accounting
+#include <atomic>
+#include <map>
+#include <mutex>
+
+static std::atomic<long long> g_launches{0};
+static std::atomic<int> g_profile{0};
+static std::mutex g_prof_mu;
+struct PhaseAcc {
+  double ms = 0;
+  long long count = 0;
+};
+static std::map<std::string, PhaseAcc> g_prof;
+struct PendingPhase {
+  std::string name;
+  cudaEvent_t a, b;
+};
+static std::vector<PendingPhase> g_pending;
+
+void mx_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Keep memory freed with cudaFreeAsync cached in the device's default pool
+// (the default release threshold of 0 hands it back to the driver at every
+// synchronisation, which makes each job re-map gigabytes of HBM).
+static void keep_pool_warm() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> g(mu);
+  for (int d : done)
+    if (d == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(dev);
+}
+
+MxPhase::MxPhase(const char* n, cudaStream_t s) : name(n), stream(s), start(nullptr) {
+  if (!g_profile.load()) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, s);
+  start = e;
+}
+
+MxPhase::~MxPhase() {
+  if (!start) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, stream);
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_pending.push_back(PendingPhase{name, (cudaEvent_t)start, e});
+}
+
+static void collect_phases() {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& p : g_pending) {
+    float ms = 0;
+    cudaEventSynchronize(p.b);
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      PhaseAcc& acc = g_prof[p.name];
+      acc.ms += ms;
+      acc.count += 1;
+    }
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  g_pending.clear();
+}
+
 int mx_fail(int code, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
@@ -45,11 +118,37 @@ using namespace mx;
 extern "C" {
 
 const char* mx_last_error(void) { return g_err.c_str(); }
+
+int64_t mx_launch_count(void) { return g_launches.load(); }
+
+int mx_profile_enable(int on) {
+  collect_phases();
+  g_profile.store(on ? 1 : 0);
+  return MX_OK;
+}
+
+int mx_profile_reset(void) {
+  collect_phases();
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof.clear();
+  return MX_OK;
+}
+
+int mx_profile_read(const char* phase, double* total_ms, int64_t* count) {
+  MX_CHECK_ARG(phase, "null phase");
+  collect_phases();
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  auto it = g_prof.find(phase);
+  if (total_ms) *total_ms = it == g_prof.end() ? 0.0 : it->second.ms;
+  if (count) *count = it == g_prof.end() ? 0 : it->second.count;
+  return MX_OK;
+}
 int mx_abi_version(void) { return 1; }
 
 int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out) {
   MX_CHECK_ARG(desc && out, "null argument");
   g_err.clear();
+  keep_pool_warm();
   cudaStream_t s = (cudaStream_t)stream;
   mx_index* ix = new mx_index();
   ix->d.stream = s;
@@ -157,6 +256,7 @@ int mx_gen_create(mx_index* index, const uint8_t* cursor_prefix, int32_t cursor_
                   int32_t chunk_prefix_len, uint64_t order_seed, void* stream, mx_gen** out) {
   MX_CHECK_ARG(index && out, "null argument");
   g_err.clear();
+  keep_pool_warm();
   cudaStream_t s = (cudaStream_t)stream;
   mx_gen* g = new mx_gen();
   int rc = MX_OK;

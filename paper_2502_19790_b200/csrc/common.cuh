@@ -114,3 +114,15 @@ struct DevError {
 
 int mx_fail_cuda(cudaError_t e, const char* what, const char* file, int line);
 int mx_fail(int code, const char* fmt, ...);
+
+// Launch accounting and per-phase CUDA-event timing (capi.cu). A phase timer
+// records events on the launching stream when profiling is enabled
+// (mx_profile_enable); totals are read back with mx_profile_read.
+void mx_count_launch();
+struct MxPhase {
+  const char* name;
+  cudaStream_t stream;
+  void* start;
+  MxPhase(const char* n, cudaStream_t s);
+  ~MxPhase();
+};

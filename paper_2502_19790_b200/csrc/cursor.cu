@@ -213,6 +213,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   MX_CUDA_TRY(g->consumed.alloc(K > 0 ? K : 1, s));
   MX_CUDA_TRY(cudaMemsetAsync(g->consumed.p, 0, sizeof(u64) * (K > 0 ? K : 1), s));
   if (K == 0) return MX_OK;
+  MxPhase ph("cursor_layout", s);
   DevBuf<uint8_t> pre;
   DevBuf<u64> seeds;
   MX_CUDA_TRY(pre.alloc(prefix_len > 0 ? prefix_len : 1, s));
@@ -230,16 +231,19 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   v.bytes = ix->str_bytes.p;
   v.off = ix->str_off.p;
   key_seed_kernel<<<(unsigned)((K + 127) / 128), 128, 0, s>>>(v, K, pre.p, prefix_len, seeds.p);
+  mx_count_launch();
   DevBuf<u32> grp, gid;
   MX_CUDA_TRY(grp.alloc(B, s));
   MX_CUDA_TRY(gid.alloc(B, s));
   MX_CUDA_TRY(g->cur_blk.alloc(B, s));
   {
+    MxPhase ph2("cursor_shuffle", s);
     long long blocks = (K + CS_WARPS - 1) / CS_WARPS;
     if (blocks > 148 * 16) blocks = 148 * 16;
     cursor_shuffle_kernel<<<(unsigned)blocks, CS_WARPS * 32, 0, s>>>(K, ix->key_blk_first.p, ix->blk_file.p,
                                                                    ix->file_ds.p, seeds.p, grp.p, gid.p,
                                                                    g->cur_blk.p);
+    mx_count_launch();
   }
   MX_CUDA_TRY(g->civ.alloc(I, s));
   {
@@ -247,6 +251,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     if (blocks > 148 * 8) blocks = 148 * 8;
     cursor_intervals_kernel<<<(unsigned)blocks, 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
                                                             g->cur_blk.p, g->civ.p);
+    mx_count_launch();
   }
   MX_CUDA_TRY(g->ccum.alloc(I + 1, s));
   {
@@ -258,12 +263,15 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     MX_CUDA_TRY(cudaMemsetAsync(st.p, 0, sizeof(u64) * tiles, s));
     MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32), s));
     cum_len_kernel<<<tiles, CL_THREADS, 0, s>>>(g->civ.p, ix->iv_start.p, ix->iv_end.p, I, st.p, ctr.p, g->ccum.p);
+    mx_count_launch();
   }
   MX_CUDA_TRY(g->comp_total.alloc(K, s));
   comp_total_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
                                                                ix->iv_cum.p, g->comp_total.p);
+  mx_count_launch();
   MX_CUDA_TRY(g->comp_order.alloc(K, s));
   component_order_kernel<<<1, 32, 0, s>>>(K, order_seed, g->comp_order.p);
+  mx_count_launch();
   MX_CUDA_TRY(cudaGetLastError());
   g->h_comp_order.resize(K);
   g->h_comp_total.resize(K);

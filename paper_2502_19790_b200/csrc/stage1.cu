@@ -20,6 +20,8 @@
 //     (key, file) block ids; interval lengths -> u64 cumulative samples.
 //
 // Algorithmic bytes: B1 = N*sum(w_p) + 16*I + 8*B_kf + 16*K.
+#include <memory>
+
 #include "common.cuh"
 #include "mixtera_internal.cuh"
 
@@ -597,11 +599,14 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   a.rec_key = rk.p; a.rec_file = rf.p; a.rec_start = rs.p; a.rec_end = re.p;
   a.status = status.p; a.tile_ctr = ctr.p; a.n_runs = scratch64.p; a.err = err.p;
   if (ntiles > 0) {
+    MxPhase ph("scan_runs", s);
     const bool smem = lut_total <= MX_SMEM_LUT_MAX;
     if (smem) {
       scan_runs_kernel<true><<<ntiles, S1_THREADS, sizeof(u32) * lut_total, s>>>(a);
+      mx_count_launch();
     } else {
       scan_runs_kernel<false><<<ntiles, S1_THREADS, 0, s>>>(a);
+      mx_count_launch();
     }
     MX_CUDA_TRY(cudaGetLastError());
   }
@@ -638,14 +643,19 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(dtot.alloc(256, s));
   u32 *ka = rk.p, *fa_ = rf.p, *sa = rs.p, *ea = re.p;
   u32 *kb = k2.p, *fb = f2.p, *sb = s2.p, *eb = e2.p;
+  std::unique_ptr<MxPhase> ph_sort(new MxPhase("radix_sort", s));
   for (int pass = 0; pass < passes; ++pass) {
     const int shift = 8 * pass;
     radix_upsweep<<<rtiles, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles);
+    mx_count_launch();
     radix_rowscan<<<256, 256, 0, s>>>(hist.p, rtiles, dtot.p);
+    mx_count_launch();
     radix_downsweep<<<rtiles, RS_THREADS, 0, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p, dtot.p, rtiles);
+    mx_count_launch();
     MX_CUDA_TRY(cudaGetLastError());
     std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);
   }
+  ph_sort.reset();
   // sorted arrays now in (ka, fa_, sa, ea); keep them
   if (ka == rk.p) {
     ix.iv_key.take(rk); ix.iv_file.take(rf); ix.iv_start.take(rs); ix.iv_end.take(re);
@@ -664,12 +674,16 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(ix.iv_cum.alloc(I + 1, s));
   MX_CUDA_TRY(cudaMemsetAsync(st2.p, 0, sizeof(u64) * stiles, s));
   MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32) * 4, s));
+  std::unique_ptr<MxPhase> ph_scan(new MxPhase("index_scans", s));
   index_bounds_kernel<<<stiles, SC_THREADS, 0, s>>>(ix.iv_key.p, ix.iv_file.p, I, st2.p, ctr.p,
                                                     ix.blk_first.p, ix.blk_file.p, ix.blk_key.p,
                                                     ix.key_blk_first.p, ix.key_packed.p, scratch64.p + 1);
+  mx_count_launch();
   MX_CUDA_TRY(cudaMemsetAsync(st2.p, 0, sizeof(u64) * stiles, s));
   interval_cum_kernel<<<stiles, SC_THREADS, 0, s>>>(ix.iv_start.p, ix.iv_end.p, I, st2.p, ctr.p + 1,
                                                     ix.iv_cum.p, err.p);
+  mx_count_launch();
+  ph_scan.reset();
   MX_CUDA_TRY(cudaGetLastError());
   u64 tot = 0;
   MX_CUDA_TRY(cudaMemcpyAsync(&tot, scratch64.p + 1, sizeof(u64), cudaMemcpyDeviceToHost, s));

@@ -34,6 +34,8 @@
 //
 // Algorithmic bytes: B2 = sum over chunks of
 // (16 * intervals touched + 20 * ranges emitted) + 8 per chunk seed.
+#include <memory>
+
 #include "blake2b.cuh"
 #include "common.cuh"
 #include "mixtera_internal.cuh"
@@ -771,6 +773,7 @@ struct PlanWork {
 static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, const DevBuf<Term>& terms,
                 long long n_chunks, long long n_phases, cudaStream_t s) {
   IndexData* ix = g->ix;
+  MxPhase ph("emit", s);
   g->res_chunks = n_chunks;
   g->res_ranges = 0;
   MX_CUDA_TRY(g->res_off.alloc(n_chunks + 1, s));
@@ -785,6 +788,7 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
   DevBuf<u64> pair_pre;
   MX_CUDA_TRY(pair_pre.alloc(n_phases + 1, s));
   pair_prefix_kernel<<<1, 32, 0, s>>>(phases.p, n_phases, pair_pre.p);
+  mx_count_launch();
   u64 n_pairs = 0;
   MX_CUDA_TRY(cudaMemcpyAsync(&n_pairs, pair_pre.p + n_phases, sizeof(u64), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
@@ -809,11 +813,13 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
   MX_CUDA_TRY(pair_off.alloc(n_pairs + 1, s));
   const unsigned pb = (unsigned)((n_pairs + 255) / 256);
   emit_count_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p);
+  mx_count_launch();
   // exclusive scan of counts in place (+ total at [n_pairs])
   {
     DevBuf<long long> tmp;
     MX_CUDA_TRY(tmp.alloc(n_pairs + 1, s));
     offsets_kernel<<<1, 1024, 0, s>>>((long long)n_pairs, pair_off.p, tmp.p);
+    mx_count_launch();
     MX_CUDA_TRY(cudaMemcpyAsync(pair_off.p, tmp.p, sizeof(u64) * (n_pairs + 1), cudaMemcpyDeviceToDevice, s));
   }
   u64 n_pieces = 0;
@@ -826,6 +832,7 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
   MX_CUDA_TRY(ps.alloc(cap, s));
   MX_CUDA_TRY(pe.alloc(cap, s));
   emit_write_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p);
+  mx_count_launch();
   DevBuf<u64> cpo, mcnt;
   DevBuf<u32> big;
   MX_CUDA_TRY(cpo.alloc(n_chunks + 1, s));
@@ -833,11 +840,14 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
   MX_CUDA_TRY(big.alloc(1, s));
   MX_CUDA_TRY(cudaMemsetAsync(big.p, 0, sizeof(u32), s));
   chunk_pieces_kernel<<<(unsigned)((n_chunks + 256) / 256), 256, 0, s>>>(a, n_chunks, pair_off.p, n_pairs, cpo.p);
+  mx_count_launch();
   {
     long long grid = n_chunks < 148 * 8 ? n_chunks : 148 * 8;
     normalize_kernel<<<(unsigned)grid, NM_THREADS, 0, s>>>(n_chunks, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p, big.p);
+    mx_count_launch();
   }
   offsets_kernel<<<1, 1024, 0, s>>>(n_chunks, mcnt.p, g->res_off.p);
+  mx_count_launch();
   u32 h_big = 0;
   long long total = 0;
   MX_CUDA_TRY(cudaMemcpyAsync(&h_big, big.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -854,9 +864,11 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
     long long grid = n_chunks < 148 * 8 ? n_chunks : 148 * 8;
     compact_kernel<<<(unsigned)grid, 128, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
                                                   g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p);
+    mx_count_launch();
   }
   chunk_seed_kernel<<<(unsigned)((n_chunks + 127) / 128), 128, 0, s>>>(n_chunks, g->next_chunk_id, g->chunk_prefix.p,
                                                                       g->chunk_prefix_len, g->res_seed.p, g->res_id.p);
+  mx_count_launch();
   MX_CUDA_TRY(cudaGetLastError());
   MX_CUDA_TRY(cudaStreamSynchronize(s));
   g->next_chunk_id += n_chunks;
@@ -875,6 +887,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     return mx_fail(MX_ERR_MIXTURE, "chunk size %lld below the number of mixture keys (%d)", (long long)mix->chunk_size, Km);
   g->report.assign(Km, 0);
   g->last_mkeys = Km;
+  std::unique_ptr<MxPhase> ph_plan(new MxPhase("plan", s));
   // ---- matching
   MatchArgs ma{};
   ma.Km = Km;
@@ -898,7 +911,10 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   MX_CUDA_TRY(L_cnt.alloc(Km, s));
   MX_CUDA_TRY(hits.alloc(K > 0 ? K : 1, s));
   MX_CUDA_TRY(cudaMemsetAsync(hits.p, 0, sizeof(u32) * (K > 0 ? K : 1), s));
-  if (K > 0) match_count_kernel<<<Km, 256, 0, s>>>(ma, L_cnt.p, hits.p);
+  if (K > 0) {
+    match_count_kernel<<<Km, 256, 0, s>>>(ma, L_cnt.p, hits.p);
+    mx_count_launch();
+  }
   std::vector<u32> h_cnt(Km), h_hits(K > 0 ? K : 1, 0);
   MX_CUDA_TRY(cudaMemcpyAsync(h_cnt.data(), L_cnt.p, sizeof(u32) * Km, cudaMemcpyDeviceToHost, s));
   if (K > 0) MX_CUDA_TRY(cudaMemcpyAsync(h_hits.data(), hits.p, sizeof(u32) * K, cudaMemcpyDeviceToHost, s));
@@ -911,7 +927,10 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   MX_CUDA_TRY(L_off.alloc(Km + 1, s));
   MX_CUDA_TRY(cudaMemcpyAsync(L_off.p, h_off.data(), sizeof(u32) * (Km + 1), cudaMemcpyHostToDevice, s));
   MX_CUDA_TRY(L.alloc(h_off[Km] > 0 ? h_off[Km] : 1, s));
-  if (K > 0) match_fill_kernel<<<Km, 256, 0, s>>>(ma, L_off.p, L.p);
+  if (K > 0) {
+    match_fill_kernel<<<Km, 256, 0, s>>>(ma, L_off.p, L.p);
+    mx_count_launch();
+  }
   // ---- streams
   PlanWork w;
   w.mode = shared ? 1 : 0;
@@ -925,6 +944,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     MX_CUDA_TRY(w.seg_pre.alloc(nseg + Km, s));
     build_segments_kernel<<<(Km + 127) / 128, 128, 0, s>>>(0, Km, w.s_off.p, L.p, g->comp_total.p, g->consumed.p,
                                                           w.seg_comp.p, w.seg_lo.p, w.seg_pre.p);
+    mx_count_launch();
   } else {
     w.n_streams = (int)K;
     std::vector<u32> so(K + 1);
@@ -937,6 +957,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     build_segments_kernel<<<(unsigned)((K + 127) / 128), 128, 0, s>>>(1, (int)K, w.s_off.p, nullptr, g->comp_total.p,
                                                                       g->consumed.p, w.seg_comp.p, w.seg_lo.p,
                                                                       w.seg_pre.p);
+    mx_count_launch();
     MX_CUDA_TRY(cudaStreamSynchronize(s));
   }
   // ---- plan
@@ -1002,13 +1023,17 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   pa.out = out.p;
   pa.report = report.p;
   plan_kernel<<<1, 32, 0, s>>>(pa);
+  mx_count_launch();
   long long h_out[4];
   MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaMemcpyAsync(g->report.data(), report.p, sizeof(long long) * Km, cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
-  if (w.mode == 0)
+  ph_plan.reset();
+  if (w.mode == 0) {
     commit_segments_kernel<<<Km, 128, 0, s>>>(Km, w.s_off.p, w.seg_comp.p, w.seg_lo.p, w.seg_pre.p, pos.p,
                                               g->consumed.p);
+    mx_count_launch();
+  }
   int rc = emit(g, w, phases, terms, h_out[0], h_out[1], s);
   if (rc != MX_OK) return rc;
   *n_out = h_out[0];
@@ -1037,6 +1062,7 @@ int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long 
   MX_CUDA_TRY(w.seg_pre.alloc(K + 1, s));
   build_segments_kernel<<<1, 32, 0, s>>>(2, 1, w.s_off.p, g->comp_order.p, g->comp_total.p, g->consumed.p,
                                          w.seg_comp.p, w.seg_lo.p, w.seg_pre.p);
+  mx_count_launch();
   DevBuf<Phase> phases;
   DevBuf<Term> terms;
   DevBuf<long long> out;
@@ -1046,10 +1072,12 @@ int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long 
   MX_CUDA_TRY(out.alloc(4, s));
   MX_CUDA_TRY(pos.alloc(1, s));
   plan_arbitrary_kernel<<<1, 32, 0, s>>>(w.seg_pre.p, K, chunk_size, max_chunks, phases.p, terms.p, out.p, pos.p);
+  mx_count_launch();
   long long h_out[4];
   MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
   commit_segments_kernel<<<1, 128, 0, s>>>(1, w.s_off.p, w.seg_comp.p, w.seg_lo.p, w.seg_pre.p, pos.p, g->consumed.p);
+  mx_count_launch();
   int rc = emit(g, w, phases, terms, h_out[0], h_out[1], s);
   if (rc != MX_OK) return rc;
   *n_out = h_out[0];

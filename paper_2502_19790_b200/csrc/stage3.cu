@@ -372,7 +372,9 @@ int domain_loss(const float* losses, const int32_t* tags, long long n, int K, do
   MX_CUDA_TRY(bad.alloc(1, s));
   MX_CUDA_TRY(cudaMemsetAsync(bad.p, 0, sizeof(u32), s));
   domain_loss_kernel<<<blocks, DL_THREADS, 0, s>>>(losses, tags, n, K, per_block, ps.p, pc.p, bad.p);
+  mx_count_launch();
   domain_loss_final<<<(K + 127) / 128, 128, 0, s>>>(ps.p, pc.p, blocks, K, sums, counts);
+  mx_count_launch();
   u32 h_bad = 0;
   MX_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
@@ -392,6 +394,7 @@ int fit_power_law(int D, const long long* off, const double* n, const double* lo
   const size_t smem = sizeof(double) * 3 * (size_t)maxp;
   MX_CUDA_TRY(cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   fit_kernel<<<D, FIT_THREADS, smem, s>>>(off, n, loss, geom, out, (int)maxp);
+  mx_count_launch();
   MX_CUDA_TRY(cudaGetLastError());
   return MX_OK;
 }
@@ -400,12 +403,14 @@ int ado_pi(int k, const double* mu, const double* credit, const double* law, dou
            double* pi_bar, long long* cnt, double* pi, cudaStream_t s) {
   if (k < 1 || k > PI_MAXK) return mx_fail(MX_ERR_UNSUPPORTED, "domains=%d outside [1, %d]", k, PI_MAXK);
   pi_kernel<<<1, 32, 0, s>>>(k, mu, credit, law, n, p_min, smoothing, pi_bar, cnt, pi);
+  mx_count_launch();
   MX_CUDA_TRY(cudaGetLastError());
   return MX_OK;
 }
 
 int ado_credit(int k, double rate, const double* pi, double* credit, cudaStream_t s) {
   credit_kernel<<<(k + 127) / 128, 128, 0, s>>>(k, rate, pi, credit);
+  mx_count_launch();
   MX_CUDA_TRY(cudaGetLastError());
   return MX_OK;
 }
