@@ -75,29 +75,45 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
     const int nb = (int)(b1 - b0);
     const bool in_smem = nb <= CS_LCAP;
     u32* work = in_smem ? s_list[w] : cur_blk + b0;
+    // dataset groups (blocks are file-sorted and ds is nondecreasing in file
+    // order): one group when first and last block share a dataset, else a
+    // warp-parallel scan of dataset changes
+    const bool one_ds = nb == 0 || file_ds[blk_file[b0]] == file_ds[blk_file[b1 - 1]];
+    int G = 1;
+    if (!one_ds) {
+      G = 0;
+      for (int b = 0; b < nb; b += 32) {
+        const int i = b + lane;
+        bool head = false;
+        if (i < nb) head = i == 0 || file_ds[blk_file[b0 + i]] != file_ds[blk_file[b0 + i - 1]];
+        const u32 hm = __ballot_sync(MX_FULL, head);
+        if (head) {
+          const int gi = G + __popc(hm & ((1u << lane) - 1));
+          grp[b0 + gi] = (u32)i;
+          gid[b0 + gi] = (u32)gi;
+        }
+        G += __popc(hm);
+      }
+    } else {
+      if (lane == 0) {
+        grp[b0] = 0;
+        gid[b0] = 0;
+      }
+      for (int i = lane; i < nb; i += 32) work[i] = b0 + (u32)i;
+    }
+    __syncwarp();
     if (lane == 0) {
       MT mt;
       mt.s = s_mt[w];
       mt.seed_u64(seeds[k]);
-      // dataset groups (blocks are file-sorted and ds is nondecreasing in file order)
-      int G = 0;
-      int prev = -1;
-      for (int b = 0; b < nb; ++b) {
-        int ds = file_ds[blk_file[b0 + b]];
-        if (b == 0 || ds != prev) {
-          grp[b0 + G] = (u32)b;
-          gid[b0 + G] = (u32)G;
-          ++G;
-        }
-        prev = ds;
-      }
       mt.shuffle(gid + b0, G);
       int pos = 0;
       for (int g = 0; g < G; ++g) {
         const u32 gi = gid[b0 + g];
         const int s = (int)grp[b0 + gi];
         const int e = gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
-        for (int b = s; b < e; ++b) work[pos + b - s] = b0 + (u32)b;
+        if (G > 1)  // single group: filled by the whole warp below
+          for (int b = s; b < e; ++b) work[pos + b - s] = b0 + (u32)b;
         mt.shuffle(work + pos, e - s);
         pos += e - s;
       }
@@ -214,6 +230,21 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   MX_CUDA_TRY(cudaMemsetAsync(g->consumed.p, 0, sizeof(u64) * (K > 0 ? K : 1), s));
   if (K == 0) return MX_OK;
   MxPhase ph("cursor_layout", s);
+  // the component-order shuffle (one sequential Fisher-Yates over K ranks)
+  // runs on a side stream, overlapped with the per-key cursor shuffles
+  static thread_local cudaStream_t side = nullptr;
+  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (!side) {
+    MX_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    MX_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    MX_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  MX_CUDA_TRY(g->comp_order.alloc(K, s));
+  MX_CUDA_TRY(cudaEventRecord(ev_fork, s));
+  MX_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
+  component_order_kernel<<<1, 32, 0, side>>>(K, order_seed, g->comp_order.p);
+  mx_count_launch();
+  MX_CUDA_TRY(cudaEventRecord(ev_join, side));
   DevBuf<uint8_t> pre;
   DevBuf<u64> seeds;
   MX_CUDA_TRY(pre.alloc(prefix_len > 0 ? prefix_len : 1, s));
@@ -269,9 +300,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   comp_total_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
                                                                ix->iv_cum.p, g->comp_total.p);
   mx_count_launch();
-  MX_CUDA_TRY(g->comp_order.alloc(K, s));
-  component_order_kernel<<<1, 32, 0, s>>>(K, order_seed, g->comp_order.p);
-  mx_count_launch();
+  MX_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
   MX_CUDA_TRY(cudaGetLastError());
   g->h_comp_order.resize(K);
   g->h_comp_total.resize(K);

@@ -20,6 +20,9 @@
 //     (key, file) block ids; interval lengths -> u64 cumulative samples.
 //
 // Algorithmic bytes: B1 = N*sum(w_p) + 16*I + 8*B_kf + 16*K.
+#include <stdlib.h>
+#include <string.h>
+
 #include <memory>
 
 #include "common.cuh"
@@ -52,6 +55,11 @@ struct S1Args {
   u32* tile_ctr;
   u64* n_runs;
   DevError* err;
+  const u32* lut_sum;    // LUT with the fail flag as a count at bit `fail_shift` (sum-only keying)
+  u32 fail_limit;        // 1 << fail_shift: a sample passes iff its sum is below
+  u32* tile_cnt;         // slot mode: runs started in each tile
+  u32* tile_open;        // slot mode: tile's last run ends in a later tile
+  long long* tile_head;  // slot mode: 0 none, -1 run passes through, >0 end+1 of the continuing run
 };
 
 template <bool SMEM_LUT>
@@ -299,23 +307,32 @@ scan_runs_kernel(S1Args a) {
   }
 }
 
+}  // namespace mx
+
+#include "scan_tma.cuh"
+
+namespace mx {
+
 // ---------------------------------------------------------------- radix sort
 constexpr int RS_THREADS = 256;
-constexpr int RS_ITEMS = 16;
+constexpr int RS_ITEMS = 4;  // small tiles: enough CTAs for ~1M-record sorts
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096, warp-striped
 constexpr int RS_WARPS = RS_THREADS / 32;
 
 __global__ void __launch_bounds__(RS_THREADS)
-radix_upsweep(const u32* keys, long long n, int shift, u32* hist, int ntiles) {
+radix_upsweep(const u32* keys, long long n, int shift, u32* hist, int ntiles, const u32* seg_cnt) {
+  // seg_cnt != null: tile b's elements are the first seg_cnt[b] slots of
+  // [b*RS_TILE, (b+1)*RS_TILE) (stage-1 slot output); else dense [0, n)
   __shared__ u32 h[256];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   h[tid] = 0;
   __syncthreads();
+  const long long lim = seg_cnt ? (long long)blockIdx.x * RS_TILE + seg_cnt[blockIdx.x] : n;
   const long long base = (long long)blockIdx.x * RS_TILE + warp * (32 * RS_ITEMS);
 #pragma unroll 4
   for (int k = 0; k < RS_ITEMS; ++k) {
     long long i = base + k * 32 + lane;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
+    if (i < lim) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
   }
   __syncthreads();
   hist[(long long)tid * ntiles + blockIdx.x] = h[tid];
@@ -364,8 +381,10 @@ radix_rowscan(u32* hist, int ntiles, u32* digit_tot) {
 __global__ void __launch_bounds__(RS_THREADS)
 radix_downsweep(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2in,
                 u32* kout, u32* p0out, u32* p1out, u32* p2out,
-                long long n, int shift, const u32* hist, const u32* digit_tot, int ntiles) {
+                long long n, int shift, const u32* hist, const u32* digit_tot, int ntiles,
+                const u32* seg_cnt) {
   __shared__ u32 s_base[256];
+  const long long lim = seg_cnt ? (long long)blockIdx.x * RS_TILE + seg_cnt[blockIdx.x] : n;
   __shared__ u32 s_wcnt[RS_WARPS][256];
   __shared__ u32 s_w[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -391,7 +410,7 @@ radix_downsweep(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2i
 #pragma unroll
   for (int k = 0; k < RS_ITEMS; ++k) {
     long long i = base + k * 32 + lane;
-    bool ok = i < n;
+    bool ok = i < lim;
     key[k] = ok ? kin[i] : 0;
     u32 d = (key[k] >> shift) & 0xff;
     u32 peers = __match_any_sync(MX_FULL, ok ? d : 0x100u);
@@ -416,7 +435,7 @@ radix_downsweep(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2i
 #pragma unroll
   for (int k = 0; k < RS_ITEMS; ++k) {
     long long i = base + k * 32 + lane;
-    if (i < n) {
+    if (i < lim) {
       u32 d = (key[k] >> shift) & 0xff;
       u32 dst = s_base[d] + s_wcnt[warp][d] + rank[k];
       kout[dst] = key[k];
@@ -547,6 +566,30 @@ interval_cum_kernel(const u32* start, const u32* end, long long n, u64* status, 
 }
 
 // ---------------------------------------------------------------- host side
+template <int SEGS, int PC>
+static void launch_direct(const S1Args& a, const TileMeta* m, long long ntiles, bool smem_lut, int lut_total,
+                          cudaStream_t s) {
+  if (smem_lut) {
+    scan_direct_kernel<SEGS, PC, true><<<(unsigned)ntiles, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m, ntiles);
+  } else {
+    scan_direct_kernel<SEGS, 0, false><<<(unsigned)ntiles, S1_THREADS, 0, s>>>(a, m, ntiles);
+  }
+}
+
+template <int SEGS>
+static void dispatch_direct(const S1Args& a, const TileMeta* m, long long ntiles, bool smem_lut, int lut_total,
+                            cudaStream_t s) {
+  switch (smem_lut && a.lut_sum ? a.n_props : 0) {
+    case 1: launch_direct<SEGS, 1>(a, m, ntiles, true, lut_total, s); break;
+    case 2: launch_direct<SEGS, 2>(a, m, ntiles, true, lut_total, s); break;
+    case 3: launch_direct<SEGS, 3>(a, m, ntiles, true, lut_total, s); break;
+    case 4: launch_direct<SEGS, 4>(a, m, ntiles, true, lut_total, s); break;
+    case 5: launch_direct<SEGS, 5>(a, m, ntiles, true, lut_total, s); break;
+    case 6: launch_direct<SEGS, 6>(a, m, ntiles, true, lut_total, s); break;
+    default: launch_direct<SEGS, 0>(a, m, ntiles, smem_lut, lut_total, s); break;
+  }
+}
+
 int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   if (d->n_props < 1 || d->n_props > MX_MAX_PROPS)
     return mx_fail(MX_ERR_UNSUPPORTED, "n_props=%d outside [1, %d]", d->n_props, MX_MAX_PROPS);
@@ -567,6 +610,21 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(lut.alloc(lut_total, s));
   MX_CUDA_TRY(cudaMemcpyAsync(lut.p, d->lut, sizeof(u32) * lut_total, cudaMemcpyHostToDevice, s));
   a.lut = lut.p;
+  // sum-keying LUT: fail flag as a count above the key bits (needs key_bits +
+  // bitlen(P) <= 31), see scan_direct_kernel
+  DevBuf<u32> lut_sum;
+  int pbits = 0;
+  while ((1 << pbits) <= d->n_props) ++pbits;
+  const bool sum_ok = d->key_bits + pbits <= 31;
+  if (sum_ok) {
+    std::vector<u32> ls(lut_total);
+    for (int i = 0; i < lut_total; ++i)
+      ls[i] = (d->lut[i] & ~FAIL) + ((d->lut[i] >> 31) << d->key_bits);
+    MX_CUDA_TRY(lut_sum.alloc(lut_total, s));
+    MX_CUDA_TRY(cudaMemcpyAsync(lut_sum.p, ls.data(), sizeof(u32) * lut_total, cudaMemcpyHostToDevice, s));
+    a.lut_sum = lut_sum.p;
+    a.fail_limit = 1u << d->key_bits;
+  }
   a.n = n;
   a.file_off = reinterpret_cast<const long long*>(d->file_offsets);
   a.n_files = d->n_files;
@@ -577,12 +635,56 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   ix.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
   ix.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
 
-  const int ntiles = (int)((n + S1_TILE - 1) / S1_TILE);
+  // ---- tile geometry of the TMA-staged persistent scan (scan_tma.cuh):
+  // as many 16-sample-per-thread tiles as let two CTAs per SM keep a ring of
+  // >= 2 column tiles each in shared memory.
+  const bool smem_lut = lut_total <= MX_SMEM_LUT_MAX;
+  // MX_SCAN = direct (default) | tma | v1 selects the stage-1 pass variant
+  const char* scan_env = getenv("MX_SCAN");
+  const bool use_v1 = scan_env && !strcmp(scan_env, "v1");
+  const bool use_tma = scan_env && !strcmp(scan_env, "tma");
+  const int direct_segs = 4;  // slot mode: scan tile == radix tile (4096)
+  const bool slot_mode = !use_v1 && !use_tma;
+  int dev = 0, n_sm = 148;
+  MX_CUDA_TRY(cudaGetDevice(&dev));
+  MX_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  const int lut_bytes = smem_lut ? (lut_total * 4 + 127) / 128 * 128 : 0;
+  const int P = d->n_props;
+  int segs = 1, stages = 2;
+  {
+    const int budget = 100 * 1024;
+    const int cand[3] = {4, 2, 1};
+    for (int c = 0; c < 3; ++c) {
+      const int stage_bytes = P * 1024 * cand[c] * 4 + (int)sizeof(TileMeta);
+      if (lut_bytes + 2 * stage_bytes <= budget) {
+        segs = cand[c];
+        stages = std::min(TMA_MAX_STAGES, (budget - lut_bytes) / stage_bytes);
+        break;
+      }
+    }
+  }
+  const int tile_len = use_v1 ? S1_TILE : (use_tma ? 1024 * segs : 1024 * direct_segs);
+  const int ntiles = (int)((n + tile_len - 1) / tile_len);
+  bool aligned = true;
+  for (int p = 0; p < P; ++p) aligned &= (reinterpret_cast<uintptr_t>(d->columns[p]) % 16) == 0;
+  const long long nstaged = aligned ? n / tile_len : 0;
+  DevBuf<TileMeta> tmeta;
   DevBuf<u32> rk, rf, rs, re;
   DevBuf<u64> status, scratch64;
   DevBuf<u32> ctr;
   DevBuf<DevError> err;
-  const long long cap = n > 0 ? n : 1;  // worst case: every sample its own run
+  // worst case every sample is its own run; slot mode addresses whole tiles
+  const long long cap = std::max<long long>(1, slot_mode ? (long long)ntiles * tile_len : n);
+  DevBuf<u32> t_cnt, t_open;
+  DevBuf<long long> t_head;
+  if (slot_mode && ntiles > 0) {
+    MX_CUDA_TRY(t_cnt.alloc(ntiles, s));
+    MX_CUDA_TRY(t_open.alloc(ntiles, s));
+    MX_CUDA_TRY(t_head.alloc(ntiles, s));
+    a.tile_cnt = t_cnt.p;
+    a.tile_open = t_open.p;
+    a.tile_head = t_head.p;
+  }
   MX_CUDA_TRY(rk.alloc(cap, s));
   MX_CUDA_TRY(rf.alloc(cap, s));
   MX_CUDA_TRY(rs.alloc(cap, s));
@@ -598,10 +700,9 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(err.p) + 8, 0, 8, s));
   a.rec_key = rk.p; a.rec_file = rf.p; a.rec_start = rs.p; a.rec_end = re.p;
   a.status = status.p; a.tile_ctr = ctr.p; a.n_runs = scratch64.p; a.err = err.p;
-  if (ntiles > 0) {
+  if (ntiles > 0 && use_v1) {
     MxPhase ph("scan_runs", s);
-    const bool smem = lut_total <= MX_SMEM_LUT_MAX;
-    if (smem) {
+    if (smem_lut) {
       scan_runs_kernel<true><<<ntiles, S1_THREADS, sizeof(u32) * lut_total, s>>>(a);
       mx_count_launch();
     } else {
@@ -609,6 +710,40 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
       mx_count_launch();
     }
     MX_CUDA_TRY(cudaGetLastError());
+  } else if (ntiles > 0 && !use_tma) {
+    MX_CUDA_TRY(tmeta.alloc(ntiles, s));
+    tile_meta_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(a, tile_len, ntiles, tmeta.p);
+    mx_count_launch();
+    {
+      MxPhase ph("scan_runs", s);
+      dispatch_direct<direct_segs>(a, tmeta.p, ntiles, smem_lut, lut_total, s);
+      mx_count_launch();
+    }
+    slot_fixup_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(ntiles, tile_len, t_cnt.p, t_open.p, t_head.p, rf.p,
+                                                          a.file_off, re.p, scratch64.p);
+    mx_count_launch();
+    MX_CUDA_TRY(cudaGetLastError());
+  } else if (ntiles > 0) {
+    MX_CUDA_TRY(tmeta.alloc(ntiles, s));
+    tile_meta_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(a, tile_len, ntiles, tmeta.p);
+    mx_count_launch();
+    const size_t dyn = lut_bytes + (size_t)stages * P * tile_len * 4 + (size_t)stages * sizeof(TileMeta);
+    auto launch = [&](auto kernel) -> int {
+      MX_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+      int occ = 1;
+      MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, S1_THREADS, dyn));
+      const long long grid = std::min<long long>(ntiles, (long long)n_sm * std::max(occ, 1));
+      MxPhase ph("scan_runs", s);
+      kernel<<<(unsigned)grid, S1_THREADS, dyn, s>>>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes);
+      mx_count_launch();
+      MX_CUDA_TRY(cudaGetLastError());
+      return MX_OK;
+    };
+    int rc = MX_OK;
+    if (segs == 4) rc = smem_lut ? launch(scan_tma_kernel<4, true>) : launch(scan_tma_kernel<4, false>);
+    else if (segs == 2) rc = smem_lut ? launch(scan_tma_kernel<2, true>) : launch(scan_tma_kernel<2, false>);
+    else rc = smem_lut ? launch(scan_tma_kernel<1, true>) : launch(scan_tma_kernel<1, false>);
+    if (rc != MX_OK) return rc;
   }
   u64 h_runs = 0;
   DevError h_err;
@@ -639,18 +774,31 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(f2.alloc(I, s));
   MX_CUDA_TRY(s2.alloc(I, s));
   MX_CUDA_TRY(e2.alloc(I, s));
-  MX_CUDA_TRY(hist.alloc((long long)256 * rtiles, s));
+  MX_CUDA_TRY(hist.alloc((long long)256 * std::max(rtiles, slot_mode ? ntiles : 0), s));
   MX_CUDA_TRY(dtot.alloc(256, s));
   u32 *ka = rk.p, *fa_ = rf.p, *sa = rs.p, *ea = re.p;
   u32 *kb = k2.p, *fb = f2.p, *sb = s2.p, *eb = e2.p;
   std::unique_ptr<MxPhase> ph_sort(new MxPhase("radix_sort", s));
+  if (slot_mode) {  // per-tile slots -> dense records (order preserved)
+    DevBuf<u64> toff;
+    MX_CUDA_TRY(toff.alloc(ntiles + 1, s));
+    tile_offsets_kernel<<<1, 1024, 0, s>>>(ntiles, t_cnt.p, toff.p);
+    mx_count_launch();
+    slot_compact_kernel<<<std::min(ntiles, n_sm * 16), 256, 0, s>>>(ntiles, tile_len, t_cnt.p, toff.p, rk.p, rf.p,
+                                                                     rs.p, re.p, k2.p, f2.p, s2.p, e2.p);
+    mx_count_launch();
+    std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);
+  }
   for (int pass = 0; pass < passes; ++pass) {
     const int shift = 8 * pass;
-    radix_upsweep<<<rtiles, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles);
+    const u32* seg = nullptr;
+    const int tiles = rtiles;
+    radix_upsweep<<<tiles, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, tiles, seg);
     mx_count_launch();
-    radix_rowscan<<<256, 256, 0, s>>>(hist.p, rtiles, dtot.p);
+    radix_rowscan<<<256, 256, 0, s>>>(hist.p, tiles, dtot.p);
     mx_count_launch();
-    radix_downsweep<<<rtiles, RS_THREADS, 0, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p, dtot.p, rtiles);
+    radix_downsweep<<<tiles, RS_THREADS, 0, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p, dtot.p, tiles,
+                                                 seg);
     mx_count_launch();
     MX_CUDA_TRY(cudaGetLastError());
     std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);

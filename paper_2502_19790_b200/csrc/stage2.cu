@@ -121,22 +121,29 @@ __global__ void __launch_bounds__(256) match_fill_kernel(MatchArgs a, const u32*
 __global__ void build_segments_kernel(int mode, int n_streams, const u32* s_off, const u32* list,
                                       const u64* comp_total, const u64* consumed, u32* seg_comp, u64* seg_lo,
                                       u64* seg_pre) {
-  // one thread per stream, sequential prefix (segments per stream are few or
-  // the stream count is small)
-  int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n_streams) return;
-  u32 b = s_off[s], e = s_off[s + 1];
-  u64 run = 0;
-  for (u32 i = b; i < e; ++i) {
-    u32 c = mode == 1 ? (u32)s : list[i];
-    u64 lo = mode == 1 ? 0 : consumed[c];
-    u64 len = comp_total[c] - lo;
-    seg_comp[i] = c;
-    seg_lo[i] = lo;
-    seg_pre[i + s] = run;  // seg_pre has (segments + streams) entries: stream s uses [b + s, e + s]
-    run += len;
+  // one warp per stream, 32 segments per step with a warp scan.
+  // seg_pre has (segments + streams) entries: stream s uses [b + s, e + s].
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long s = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); s < n_streams; s += warps) {
+    const u32 b = s_off[s], e = s_off[s + 1];
+    u64 run = 0;
+    for (u32 i0 = b; i0 < e; i0 += 32) {
+      const u32 i = i0 + lane;
+      u64 len = 0;
+      if (i < e) {
+        const u32 c = mode == 1 ? (u32)s : list[i];
+        const u64 lo = mode == 1 ? 0 : consumed[c];
+        len = comp_total[c] - lo;
+        seg_comp[i] = c;
+        seg_lo[i] = lo;
+      }
+      const u64 inc = warp_incl_scan(len);
+      if (i < e) seg_pre[i + s] = run + inc - len;
+      run += __shfl_sync(MX_FULL, inc, 31);
+    }
+    if (lane == 0) seg_pre[e + s] = run;
   }
-  seg_pre[e + s] = run;
 }
 
 // consumed[c] after a plan: lo + clamp(pos_s - pre_i, 0, len_i)
@@ -369,9 +376,35 @@ __device__ int simulate_chunk(PlanArgs& a, long long* n_terms) {
   return 1;
 }
 
+constexpr int PLAN_SMEM_KM = 256;
+
 __global__ void plan_kernel(PlanArgs a) {
+  // The planner is one sequential thread: keep its per-key state in shared
+  // memory when it fits (each access is then ~30 cycles instead of an L2 trip).
+  __shared__ long long s_ll[5][PLAN_SMEM_KM];
+  __shared__ unsigned char s_flags[2][PLAN_SMEM_KM];
+  __shared__ u64 s_pos[PLAN_SMEM_KM];
+  __shared__ int s_idx[PLAN_SMEM_KM];
+  __shared__ double s_frac[PLAN_SMEM_KM], s_w[PLAN_SMEM_KM];
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int Km = a.Km;
+  u64* pos_out = a.pos;
+  long long* report_out = a.report;
+  if (Km <= PLAN_SMEM_KM && a.mode != 1) {
+    for (int m = 0; m < Km; ++m) s_w[m] = a.w[m];
+    a.w = s_w;
+    a.counts = s_ll[0];
+    a.rem = s_ll[1];
+    a.found = s_ll[2];
+    a.took = s_ll[3];
+    a.ap_base = s_ll[4];
+    a.dead = s_flags[0];
+    a.newly = s_flags[1];
+    a.pos = s_pos;
+    a.ap_idx = s_idx;
+    a.ap_frac = s_frac;
+    a.report = s_ll[4];  // written only when the plan stops; ap_base is dead then
+  }
   for (int m = 0; m < Km; ++m) a.counts[m] = 0;
   apportion_add(a, nullptr, a.C, a.counts);
   long long chunks = 0, n_ph = 0, n_terms = 0, exhausted = 0;
@@ -430,6 +463,11 @@ __global__ void plan_kernel(PlanArgs a) {
     ph.n_terms = nt;
     n_terms += nt;
     chunks += rep;
+  }
+  if (a.pos != pos_out) {
+    for (int m = 0; m < Km; ++m) pos_out[m] = a.pos[m];
+    if (exhausted)
+      for (int m = 0; m < Km; ++m) report_out[m] = a.report[m];
   }
   a.out[0] = chunks;
   a.out[1] = n_ph;
@@ -623,21 +661,35 @@ __device__ u32 sort_merge(uint4* s, u32 n, int tid, int nt, u32* s_flags) {
       __syncthreads();
     }
   }
-  // heads: not (same key, same file, contiguous)
-  for (u32 i = tid; i < n; i += nt) {
-    bool head = i == 0 || !(s[i].x == s[i - 1].x && s[i].y == s[i - 1].y && s[i].z == s[i - 1].w);
-    s_flags[i] = head ? 1u : 0u;
-  }
-  __syncthreads();
-  // sequential prefix by thread 0 is fine for the small per-chunk counts
+  // heads: not (same key, same file, contiguous); inclusive head count by a
+  // blocked block-wide scan (each thread owns a contiguous run of elements)
   __shared__ u32 s_m;
-  if (tid == 0) {
-    u32 run = 0;
-    for (u32 i = 0; i < n; ++i) {
+  __shared__ u32 s_wsum[32];
+  {
+    const u32 per = (n + nt - 1) / nt;
+    const u32 b = tid * per, e = b + per < n ? b + per : n;
+    u32 cnt = 0;
+    for (u32 i = b; i < e; ++i) {
+      const bool head = i == 0 || !(s[i].x == s[i - 1].x && s[i].y == s[i - 1].y && s[i].z == s[i - 1].w);
+      s_flags[i] = head ? 1u : 0u;
+      cnt += head;
+    }
+    const int lane = tid & 31, warp = tid >> 5;
+    const u32 inc = warp_incl_scan(cnt);
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const u32 x = lane < nt / 32 ? s_wsum[lane] : 0;
+      const u32 xi = warp_incl_scan(x);
+      if (lane < nt / 32) s_wsum[lane] = xi - x;
+      if (lane == 31) s_m = xi;
+    }
+    __syncthreads();
+    u32 run = s_wsum[warp] + inc - cnt;
+    for (u32 i = b; i < e; ++i) {
       run += s_flags[i];
       s_flags[i] = run;  // inclusive head count
     }
-    s_m = run;
   }
   __syncthreads();
   // compaction into the front of a second half is unsafe in place; stage ends
@@ -667,11 +719,13 @@ constexpr int NM_THREADS = 256;
 constexpr int NM_CAP = 2048;
 
 __global__ void __launch_bounds__(NM_THREADS)
-normalize_kernel(long long n_chunks, const u64* chunk_piece_off, u32* pm, u32* pf, u32* ps, u32* pe,
-                 u64* merged_cnt, u32* too_big) {
+normalize_kernel(const u32* big_list, const u32* big_cnt, const u64* chunk_piece_off, u32* pm, u32* pf, u32* ps,
+                 u32* pe, u64* merged_cnt, u32* too_big) {
   __shared__ uint4 s[NM_CAP];
   __shared__ u32 s_flags[NM_CAP];
-  for (long long k = blockIdx.x; k < n_chunks; k += gridDim.x) {
+  const u32 nbig = *big_cnt;
+  for (u32 x = blockIdx.x; x < nbig; x += gridDim.x) {
+    const u32 k = big_list[x];
     const u64 o0 = chunk_piece_off[k], o1 = chunk_piece_off[k + 1];
     const u32 n = (u32)(o1 - o0);
     if (n > NM_CAP) {
@@ -689,6 +743,140 @@ normalize_kernel(long long n_chunks, const u64* chunk_piece_off, u32* pm, u32* p
     }
     if (threadIdx.x == 0) merged_cnt[k] = m;
     __syncthreads();
+  }
+}
+
+// Chunks of <= 32 pieces (the common case): one warp per chunk, bitonic sort
+// of (mixture key, file, start) across lanes with shuffles, merge by ballot.
+__global__ void __launch_bounds__(256)
+normalize_warp_kernel(long long n_chunks, const u64* chunk_piece_off, u32* pm, u32* pf, u32* ps, u32* pe,
+                      u64* merged_cnt, u32* big_list, u32* big_cnt) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long k = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n_chunks; k += warps) {
+    const u64 o0 = chunk_piece_off[k];
+    const u32 n = (u32)(chunk_piece_off[k + 1] - o0);
+    if (n > 32) {  // left to normalize_kernel
+      if (lane == 0) big_list[atomicAdd(big_cnt, 1u)] = (u32)k;
+      continue;
+    }
+    const bool ok = (u32)lane < n;
+    // sort key: hi = (mkey, file), lo = start; padding sorts last
+    unsigned long long hi = ok ? ((unsigned long long)pm[o0 + lane] << 32) | pf[o0 + lane] : ~0ull;
+    u32 lo = ok ? ps[o0 + lane] : ~0u;
+    u32 en = ok ? pe[o0 + lane] : ~0u;
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const unsigned long long ohi = __shfl_xor_sync(MX_FULL, hi, j);
+        const u32 olo = __shfl_xor_sync(MX_FULL, lo, j);
+        const u32 oen = __shfl_xor_sync(MX_FULL, en, j);
+        const bool other_less = ohi < hi || (ohi == hi && olo < lo);
+        const bool lower = (lane & j) == 0;      // this lane keeps the smaller of the pair?
+        const bool up = (lane & kk) == 0;        // ascending sub-sequence
+        const bool take = (lower == up) ? other_less : !other_less && !(ohi == hi && olo == lo);
+        if (take) {
+          hi = ohi;
+          lo = olo;
+          en = oen;
+        }
+      }
+    }
+    // merge: head unless same (key, file) and contiguous with the previous piece
+    const unsigned long long phi = __shfl_up_sync(MX_FULL, hi, 1);
+    const u32 pen = __shfl_up_sync(MX_FULL, en, 1);
+    const bool head = ok && (lane == 0 || !(phi == hi && pen == lo));
+    const u32 heads = __ballot_sync(MX_FULL, head);
+    const u32 slot = __popc(heads & ((2u << lane) - 1u)) - 1u;  // run index of this piece
+    const u32 nxt_head = __shfl_down_sync(MX_FULL, (u32)head, 1);
+    const bool last = ok && ((u32)lane == n - 1 || nxt_head);
+    if (head) {
+      pm[o0 + slot] = (u32)(hi >> 32);
+      pf[o0 + slot] = (u32)hi;
+      ps[o0 + slot] = lo;
+    }
+    __syncwarp();
+    if (last) pe[o0 + slot] = en;
+    if (lane == 0) merged_cnt[k] = __popc(heads);
+  }
+}
+
+// Exclusive scan (decoupled look-back) of u64 counts; out[n] = total.
+template <typename OUT>
+__global__ void __launch_bounds__(256)
+excl_scan_kernel(const u64* in, long long n, OUT* out, u64* status, u32* tile_ctr) {
+  constexpr int ITEMS = 8, TILE = 256 * ITEMS;
+  __shared__ u64 s_w[9];
+  __shared__ int s_tile;
+  __shared__ u64 s_excl;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const long long b = (long long)tile * TILE + threadIdx.x * ITEMS;
+  u64 v[ITEMS], sum = 0;
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    v[q] = b + q < n ? in[b + q] : 0;
+    sum += v[q];
+  }
+  const u64 inc = warp_incl_scan(sum);
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const u64 x = lane < 8 ? s_w[lane] : 0;
+    const u64 xi = warp_incl_scan(x);
+    if (lane < 8) s_w[lane] = xi - x;
+    const u64 tot = __shfl_sync(MX_FULL, xi, 31);
+    const u64 t = lookback_exclusive(status, tile, tot);
+    if (lane == 0) {
+      s_excl = t;
+      if ((long long)(tile + 1) * TILE >= n) out[n] = (OUT)(t + tot);
+    }
+  }
+  __syncthreads();
+  u64 run = s_excl + s_w[warp] + inc - sum;
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
+    if (b + q < n) out[b + q] = (OUT)run;
+    run += v[q];
+  }
+}
+
+template <typename OUT>
+static int excl_scan(const u64* in, long long n, OUT* out, cudaStream_t s) {
+  const long long tiles = (n + 2047) / 2048;
+  if (tiles == 0) {
+    MX_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(OUT), s));
+    return MX_OK;
+  }
+  DevBuf<u64> st;
+  DevBuf<u32> ctr;
+  MX_CUDA_TRY(st.alloc(tiles, s));
+  MX_CUDA_TRY(ctr.alloc(1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(st.p, 0, sizeof(u64) * tiles, s));
+  MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32), s));
+  excl_scan_kernel<OUT><<<(unsigned)tiles, 256, 0, s>>>(in, n, out, st.p, ctr.p);
+  mx_count_launch();
+  MX_CUDA_TRY(cudaGetLastError());
+  return MX_OK;
+}
+
+// Dense copy of each chunk's merged ranges (one warp per chunk).
+__global__ void compact_warp_kernel(long long n_chunks, const u64* chunk_piece_off, const long long* res_off,
+                                    const u32* pm, const u32* pf, const u32* ps, const u32* pe, u32* rm, u32* rf,
+                                    u32* rs, u32* re) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long k = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n_chunks; k += warps) {
+    const u64 src = chunk_piece_off[k];
+    const long long dst = res_off[k], n = res_off[k + 1] - dst;
+    for (long long i = threadIdx.x & 31; i < n; i += 32) {
+      rm[dst + i] = pm[src + i];
+      rf[dst + i] = pf[src + i];
+      rs[dst + i] = ps[src + i];
+      re[dst + i] = pe[src + i];
+    }
   }
 }
 
@@ -814,14 +1002,9 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
   const unsigned pb = (unsigned)((n_pairs + 255) / 256);
   emit_count_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p);
   mx_count_launch();
-  // exclusive scan of counts in place (+ total at [n_pairs])
-  {
-    DevBuf<long long> tmp;
-    MX_CUDA_TRY(tmp.alloc(n_pairs + 1, s));
-    offsets_kernel<<<1, 1024, 0, s>>>((long long)n_pairs, pair_off.p, tmp.p);
-    mx_count_launch();
-    MX_CUDA_TRY(cudaMemcpyAsync(pair_off.p, tmp.p, sizeof(u64) * (n_pairs + 1), cudaMemcpyDeviceToDevice, s));
-  }
+  // exclusive scan of counts in place (each element is read and written by
+  // the same thread; the total lands in [n_pairs])
+  if (int rc = excl_scan<u64>(pair_off.p, (long long)n_pairs, pair_off.p, s)) return rc;
   u64 n_pieces = 0;
   MX_CUDA_TRY(cudaMemcpyAsync(&n_pieces, pair_off.p + n_pairs, sizeof(u64), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
@@ -842,12 +1025,20 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
   chunk_pieces_kernel<<<(unsigned)((n_chunks + 256) / 256), 256, 0, s>>>(a, n_chunks, pair_off.p, n_pairs, cpo.p);
   mx_count_launch();
   {
-    long long grid = n_chunks < 148 * 8 ? n_chunks : 148 * 8;
-    normalize_kernel<<<(unsigned)grid, NM_THREADS, 0, s>>>(n_chunks, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p, big.p);
+    DevBuf<u32> blist, bcnt;
+    MX_CUDA_TRY(blist.alloc(n_chunks, s));
+    MX_CUDA_TRY(bcnt.alloc(1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(bcnt.p, 0, sizeof(u32), s));
+    const long long wgrid = std::min<long long>((n_chunks + 7) / 8, 148 * 16);
+    normalize_warp_kernel<<<(unsigned)wgrid, 256, 0, s>>>(n_chunks, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p, blist.p,
+                                                          bcnt.p);
+    mx_count_launch();
+    long long grid = n_chunks < 148 * 4 ? n_chunks : 148 * 4;
+    normalize_kernel<<<(unsigned)grid, NM_THREADS, 0, s>>>(blist.p, bcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p,
+                                                           big.p);
     mx_count_launch();
   }
-  offsets_kernel<<<1, 1024, 0, s>>>(n_chunks, mcnt.p, g->res_off.p);
-  mx_count_launch();
+  if (int rc = excl_scan<long long>(mcnt.p, n_chunks, g->res_off.p, s)) return rc;
   u32 h_big = 0;
   long long total = 0;
   MX_CUDA_TRY(cudaMemcpyAsync(&h_big, big.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
@@ -861,9 +1052,9 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
   MX_CUDA_TRY(g->res_start.alloc(rc, s));
   MX_CUDA_TRY(g->res_end.alloc(rc, s));
   {
-    long long grid = n_chunks < 148 * 8 ? n_chunks : 148 * 8;
-    compact_kernel<<<(unsigned)grid, 128, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
-                                                  g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p);
+    const long long grid = std::min<long long>((n_chunks + 7) / 8, 148 * 16);
+    compact_warp_kernel<<<(unsigned)grid, 256, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
+                                                       g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p);
     mx_count_launch();
   }
   chunk_seed_kernel<<<(unsigned)((n_chunks + 127) / 128), 128, 0, s>>>(n_chunks, g->next_chunk_id, g->chunk_prefix.p,
@@ -942,7 +1133,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     MX_CUDA_TRY(w.seg_comp.alloc(nseg > 0 ? nseg : 1, s));
     MX_CUDA_TRY(w.seg_lo.alloc(nseg > 0 ? nseg : 1, s));
     MX_CUDA_TRY(w.seg_pre.alloc(nseg + Km, s));
-    build_segments_kernel<<<(Km + 127) / 128, 128, 0, s>>>(0, Km, w.s_off.p, L.p, g->comp_total.p, g->consumed.p,
+    build_segments_kernel<<<(Km + 3) / 4, 128, 0, s>>>(0, Km, w.s_off.p, L.p, g->comp_total.p, g->consumed.p,
                                                           w.seg_comp.p, w.seg_lo.p, w.seg_pre.p);
     mx_count_launch();
   } else {
@@ -954,7 +1145,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     MX_CUDA_TRY(w.seg_comp.alloc(K, s));
     MX_CUDA_TRY(w.seg_lo.alloc(K, s));
     MX_CUDA_TRY(w.seg_pre.alloc(2 * K, s));
-    build_segments_kernel<<<(unsigned)((K + 127) / 128), 128, 0, s>>>(1, (int)K, w.s_off.p, nullptr, g->comp_total.p,
+    build_segments_kernel<<<(unsigned)std::min<long long>((K + 3) / 4, 148 * 16), 128, 0, s>>>(1, (int)K, w.s_off.p, nullptr, g->comp_total.p,
                                                                       g->consumed.p, w.seg_comp.p, w.seg_lo.p,
                                                                       w.seg_pre.p);
     mx_count_launch();
