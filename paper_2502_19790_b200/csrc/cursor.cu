@@ -62,12 +62,13 @@ __global__ void key_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix
 }
 
 constexpr int CS_WARPS = 4;
-constexpr int CS_LCAP = 2048;
+constexpr int CS_LCAP = 1536;
 
 __global__ void __launch_bounds__(CS_WARPS * 32)
 cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file, const int32_t* file_ds,
-                      const u64* seeds, u32* grp, u32* gid, u32* cur_blk) {
+                      const u64* seeds, const u32* mt_base, u32* grp, u32* gid, u32* cur_blk) {
   __shared__ u32 s_mt[CS_WARPS][MT_N];
+  __shared__ u32 s_out[CS_WARPS][MT_N];
   __shared__ u32 s_list[CS_WARPS][CS_LCAP];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (long long k = blockIdx.x * (long long)CS_WARPS + w; k < K; k += (long long)gridDim.x * CS_WARPS) {
@@ -102,21 +103,20 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
       for (int i = lane; i < nb; i += 32) work[i] = b0 + (u32)i;
     }
     __syncwarp();
-    if (lane == 0) {
-      MT mt;
-      mt.s = s_mt[w];
-      mt.seed_u64(seeds[k]);
-      mt.shuffle(gid + b0, G);
-      int pos = 0;
-      for (int g = 0; g < G; ++g) {
-        const u32 gi = gid[b0 + g];
-        const int s = (int)grp[b0 + gi];
-        const int e = gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
-        if (G > 1)  // single group: filled by the whole warp below
-          for (int b = s; b < e; ++b) work[pos + b - s] = b0 + (u32)b;
-        mt.shuffle(work + pos, e - s);
-        pos += e - s;
+    WarpMT mt{s_mt[w], s_out[w], MT_N};
+    mt.seed(mt_base, seeds[k]);
+    mt.shuffle(gid + b0, G);  // dataset order (one stream for the whole key)
+    int pos = 0;
+    for (int g = 0; g < G; ++g) {
+      const u32 gi = gid[b0 + g];
+      const int s = (int)grp[b0 + gi];
+      const int e = gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
+      if (G > 1) {  // single group: already filled above
+        for (int b = s + lane; b < e; b += 32) work[pos + b - s] = b0 + (u32)b;
+        __syncwarp();
       }
+      mt.shuffle(work + pos, e - s);  // file order within the dataset
+      pos += e - s;
     }
     __syncwarp();
     if (in_smem)
@@ -206,18 +206,18 @@ __global__ void comp_total_kernel(long long K, const u32* key_blk_first, const u
 
 constexpr int CO_SMEM = 8192;
 
-__global__ void component_order_kernel(long long K, u64 seed, u32* order) {
-  __shared__ u32 s_mt[MT_N];
+// one warp: shuffle of the K component ranks (chunks.py:139-141)
+__global__ void __launch_bounds__(32) component_order_kernel(long long K, u64 seed, const u32* mt_base, u32* order) {
+  __shared__ u32 s_mt[MT_N], s_out[MT_N];
   __shared__ u32 s_ord[CO_SMEM];
-  if (threadIdx.x != 0) return;
-  MT mt;
-  mt.s = s_mt;
-  mt.seed_u64(seed);
+  const int lane = threadIdx.x;
   u32* x = K <= CO_SMEM ? s_ord : order;
-  for (long long i = 0; i < K; ++i) x[i] = (u32)i;
+  for (long long i = lane; i < K; i += 32) x[i] = (u32)i;
+  WarpMT mt{s_mt, s_out, MT_N};
+  mt.seed(mt_base, seed);
   mt.shuffle(x, (int)K);
   if (x != order)
-    for (long long i = 0; i < K; ++i) order[i] = x[i];
+    for (long long i = lane; i < K; i += 32) order[i] = x[i];
 }
 
 int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, unsigned long long order_seed,
@@ -239,10 +239,15 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     MX_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     MX_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   }
+  static thread_local uint32_t h_base[MT_N];
+  if (h_base[0] != 19650218u) mt_base_table(h_base);
+  DevBuf<u32> mt_base;
+  MX_CUDA_TRY(mt_base.alloc(MT_N, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(mt_base.p, h_base, sizeof(h_base), cudaMemcpyHostToDevice, s));
   MX_CUDA_TRY(g->comp_order.alloc(K, s));
   MX_CUDA_TRY(cudaEventRecord(ev_fork, s));
   MX_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
-  component_order_kernel<<<1, 32, 0, side>>>(K, order_seed, g->comp_order.p);
+  component_order_kernel<<<1, 32, 0, side>>>(K, order_seed, mt_base.p, g->comp_order.p);
   mx_count_launch();
   MX_CUDA_TRY(cudaEventRecord(ev_join, side));
   DevBuf<uint8_t> pre;
@@ -272,8 +277,8 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     long long blocks = (K + CS_WARPS - 1) / CS_WARPS;
     if (blocks > 148 * 16) blocks = 148 * 16;
     cursor_shuffle_kernel<<<(unsigned)blocks, CS_WARPS * 32, 0, s>>>(K, ix->key_blk_first.p, ix->blk_file.p,
-                                                                   ix->file_ds.p, seeds.p, grp.p, gid.p,
-                                                                   g->cur_blk.p);
+                                                                   ix->file_ds.p, seeds.p, mt_base.p, grp.p,
+                                                                   gid.p, g->cur_blk.p);
     mx_count_launch();
   }
   MX_CUDA_TRY(g->civ.alloc(I, s));

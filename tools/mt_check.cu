@@ -1,0 +1,59 @@
+// Debug harness: scalar MT vs WarpMT shuffles must agree bit for bit.
+// nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -o /tmp/mt_check tools/mt_check.cu
+#include <cstdio>
+#include <vector>
+
+#include "../paper_2502_19790_b200/csrc/mt19937.cuh"
+
+using namespace mx;
+
+__global__ void ref_kernel(const unsigned long long* seeds, int n, uint32_t* out) {
+  __shared__ uint32_t st[MT_N];
+  if (threadIdx.x != 0) return;
+  MT mt;
+  mt.s = st;
+  mt.seed_u64(seeds[blockIdx.x]);
+  uint32_t* x = out + (long long)blockIdx.x * n;
+  for (int i = 0; i < n; ++i) x[i] = i;
+  mt.shuffle(x, n);
+}
+
+__global__ void warp_kernel(const unsigned long long* seeds, int n, const uint32_t* base, uint32_t* out) {
+  __shared__ uint32_t st[4][MT_N], buf[4][MT_N];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 4 + w;
+  uint32_t* x = out + (long long)b * n;
+  for (int i = lane; i < n; i += 32) x[i] = i;
+  __syncwarp();
+  WarpMT mt{st[w], buf[w], MT_N};
+  mt.seed(base, seeds[b]);
+  mt.shuffle(x, 1);
+  mt.shuffle(x, n);
+}
+
+int main() {
+  const int B = 64;
+  for (int n : {2, 3, 20, 700, 2000}) {
+    std::vector<unsigned long long> seeds(B);
+    for (int i = 0; i < B; ++i) seeds[i] = 0x9e3779b97f4a7c15ull * (i + 1) >> 1;
+    unsigned long long* ds;
+    uint32_t *o1, *o2, *base;
+    cudaMalloc(&ds, 8 * B);
+    cudaMalloc(&o1, 4ll * B * n);
+    cudaMalloc(&o2, 4ll * B * n);
+    cudaMalloc(&base, 4 * MT_N);
+    uint32_t hb[MT_N];
+    mt_base_table(hb);
+    cudaMemcpy(base, hb, sizeof(hb), cudaMemcpyHostToDevice);
+    cudaMemcpy(ds, seeds.data(), 8 * B, cudaMemcpyHostToDevice);
+    ref_kernel<<<B, 32>>>(ds, n, o1);
+    warp_kernel<<<B / 4, 128>>>(ds, n, base, o2);
+    std::vector<uint32_t> h1(B * n), h2(B * n);
+    cudaMemcpy(h1.data(), o1, 4ll * B * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h2.data(), o2, 4ll * B * n, cudaMemcpyDeviceToHost);
+    int bad = 0;
+    for (int i = 0; i < B * n; ++i) bad += h1[i] != h2[i];
+    printf("n=%d mismatches=%d err=%s first=%u/%u\n", n, bad, cudaGetErrorString(cudaGetLastError()), h1[0], h2[0]);
+  }
+  return 0;
+}
