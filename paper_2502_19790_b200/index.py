@@ -178,6 +178,9 @@ class ChunkerIndex:
     def __contains__(self, key) -> bool:
         return key in set(self.component_keys())
 
+    def __len__(self) -> int:  # an empty index is falsy, like an empty row list
+        return int(self.n_intervals)
+
     def __eq__(self, other) -> bool:
         mine = self._nested_index()
         theirs = getattr(other, "_index", None)
