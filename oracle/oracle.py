@@ -224,15 +224,26 @@ class OracleIndex:
         lo, hi = self.key_bounds[r], self.key_bounds[r + 1]
         ds, fid = self.ds[lo:hi], self.fid[lo:hi]
         rng = random.Random(seed_of(seed, "cursor", key_string(self.keys[r])))
-        datasets = sorted(set(ds.tolist()))
+        # rows are sorted by (ds, fid, start): group boundaries by run starts
+        brk = np.ones(len(fid), dtype=bool)
+        brk[1:] = (fid[1:] != fid[:-1]) | (ds[1:] != ds[:-1])
+        heads = np.flatnonzero(brk)
+        tails = np.append(heads[1:], len(fid))
+        by_ds: dict = {}
+        for h, t in zip(heads.tolist(), tails.tolist()):
+            by_ds.setdefault(int(ds[h]), []).append((int(fid[h]), h, t))
+        datasets = sorted(by_ds)
         rng.shuffle(datasets)
         out = []
+        s, e = self.start[lo:hi].tolist(), self.end[lo:hi].tolist()
         for d in datasets:
-            files = sorted(set(fid[ds == d].tolist()))
-            rng.shuffle(files)
-            for f in files:
-                sel = np.flatnonzero((ds == d) & (fid == f)) + lo
-                out.extend((d, f, int(self.start[i]), int(self.end[i])) for i in sel)
+            files = sorted(by_ds[d])
+            order = [f for f, _, _ in files]
+            rng.shuffle(order)
+            span = {f: (h, t) for f, h, t in files}
+            for f in order:
+                h, t = span[f]
+                out.extend((d, f, s[i], e[i]) for i in range(h, t))
         return out
 
 
