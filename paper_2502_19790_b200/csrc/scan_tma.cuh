@@ -1,15 +1,17 @@
-// Stage-1 streaming pass, persistent + TMA-staged (included by stage1.cu).
+// Stage-1 streaming pass (included by stage1.cu).
 //
-// Each CTA owns a ring of `stages` shared-memory slots. A slot holds one tile
-// of every code column plus the tile's precomputed metadata, filled by
-// cp.async.bulk (TMA bulk copies, SASS UBLKCP) completing on an mbarrier, so
-// the next tiles' HBM reads are in flight while the current tile is keyed,
-// run-detected and compacted. Tiles are claimed from an atomic counter in
-// increasing order, which keeps the decoupled look-back deadlock-free (every
-// predecessor of a claimed tile is owned by a running CTA that reaches it
-// first). Per-tile file bookkeeping (first file, file starts inside the tile,
-// neighbour-sample statuses) is computed up front by tile_meta_kernel, one
-// thread per tile, so no thread serialises on global binary searches.
+// Two launch shapes share one tile body (`finish_tile`):
+//  * scan_direct_kernel -- one CTA per 4096-sample tile; every 128-bit column
+//    load of a thread is issued up front; thousands of independent CTAs keep
+//    HBM busy through occupancy.
+//  * scan_pipe_kernel   -- persistent CTAs, each owning a ring of shared-memory
+//    slots filled by cp.async.bulk (TMA bulk copies, SASS UBLKCP) completing
+//    on mbarriers, so the next tiles' column bytes stream in while the current
+//    tile is keyed.
+// Both write each tile's runs into the tile's own slot region (tile-local
+// scan, no inter-tile dependency); run ends that fall into a later tile are
+// patched by slot_fixup_kernel and slot_compact_kernel densifies the records.
+// Per-tile file bookkeeping comes precomputed from tile_meta_kernel.
 #pragma once
 
 namespace mx {
@@ -72,248 +74,175 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, 
 constexpr int TMA_MAX_STAGES = 4;
 constexpr int TMA_FILE_CAP = 256;
 
-template <int SEGS, bool SMEM_LUT>
-__global__ void __launch_bounds__(S1_THREADS)
-scan_tma_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles, long long nstaged, int stages,
-                int lut_bytes) {
-  constexpr int WT = 32 * 4 * SEGS;             // samples per warp
-  constexpr int TILE = (S1_THREADS / 32) * WT;  // samples per tile
-  extern __shared__ __align__(128) unsigned char dyn[];
-  u32* s_lut = reinterpret_cast<u32*>(dyn);
-  int32_t* s_codes = reinterpret_cast<int32_t*>(dyn + lut_bytes);  // [stages][P][TILE]
-  TileMeta* s_meta = reinterpret_cast<TileMeta*>(s_codes + (long long)stages * a.n_props * TILE);
-  __shared__ __align__(8) u64 s_bar[TMA_MAX_STAGES];
-  __shared__ long long s_tile[TMA_MAX_STAGES];
-  __shared__ long long s_fstart[TMA_FILE_CAP];
-  __shared__ u32 s_warp_first[S1_THREADS / 32], s_warp_last[S1_THREADS / 32], s_warp_tot[S1_THREADS / 32];
-  __shared__ u64 s_tile_excl;
+struct TileScratch {  // per-CTA shared scratch of one tile
+  long long fstart[TMA_FILE_CAP];
+  u32 warp_first[S1_THREADS / 32], warp_last[S1_THREADS / 32], warp_tot[S1_THREADS / 32];
+  u32 last_open;
+};
 
+// Finalise statuses st[j][q] (packed key, FAIL bit) of this thread's samples
+// wbase + 128j + 4lane + q: run boundaries, tile-local compaction, records
+// into the tile's slot region [tile*TILE, ...).
+template <int SEGS>
+__device__ __forceinline__ void finish_tile(const S1Args& a, const TileMeta& m, long long tile, long long wbase,
+                                            u32 (&st)[SEGS][4], TileScratch& sc) {
+  constexpr int TILE = (S1_THREADS / 32) * 32 * 4 * SEGS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int P = a.n_props;
-  if (SMEM_LUT)
-    for (int i = tid; i < a.lut_off[P]; i += S1_THREADS) s_lut[i] = a.lut[i];
-
-  auto issue = [&](int s) {  // thread 0: claim the next tile into slot s
-    const long long t = (long long)atomicAdd(a.tile_ctr, 1u);
-    s_tile[s] = t;
-    if (t < nstaged) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_tx(&s_bar[s], (u32)(P * TILE * 4 + sizeof(TileMeta)));
-      for (int p = 0; p < P; ++p)
-        bulk_g2s(s_codes + ((long long)s * P + p) * TILE, a.cols[p] + t * TILE, TILE * 4, &s_bar[s]);
-      bulk_g2s(&s_meta[s], meta + t, sizeof(TileMeta), &s_bar[s]);
-    }
+  const int nf = m.nf;
+  const bool overflow = nf > TMA_FILE_CAP;
+  if (nf > 0 && !overflow)
+    for (int k = tid; k < nf; k += S1_THREADS) sc.fstart[k] = a.file_off[m.fa + 1 + k];
+  if (lane == 0) sc.warp_first[warp] = st[0][0];
+  if (lane == 31) sc.warp_last[warp] = st[SEGS - 1][3];
+  __syncthreads();
+  const u32 warp_prev = warp == 0 ? m.prev_status : sc.warp_last[warp - 1];
+  const u32 warp_next = warp == S1_THREADS / 32 - 1 ? m.next_status : sc.warp_first[warp + 1];
+  auto fstart_of = [&](int f) -> long long {
+    if (overflow) return a.file_off[f];
+    return f == m.fa ? m.fbase : sc.fstart[f - m.fa - 1];
   };
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < stages; ++s) issue(s);
+  // run boundaries: a run starts on a filter pass after a fail, a key change
+  // or a file start; it ends before a fail, a key change or a file start
+  u32 starts[SEGS], ends[SEGS];
+  int fidx[SEGS][4];
+#pragma unroll
+  for (int j = 0; j < SEGS; ++j) {
+    u32 prev_last = __shfl_up_sync(MX_FULL, st[j][3], 1);
+    u32 next_first = __shfl_down_sync(MX_FULL, st[j][0], 1);
+    const u32 seg_prev = __shfl_sync(MX_FULL, st[j > 0 ? j - 1 : 0][3], 31);
+    const u32 seg_next = __shfl_sync(MX_FULL, st[j < SEGS - 1 ? j + 1 : 0][0], 0);
+    if (lane == 0) prev_last = j == 0 ? warp_prev : seg_prev;
+    if (lane == 31) next_first = j == SEGS - 1 ? warp_next : seg_next;
+    const long long i0 = wbase + 128 * j + 4 * lane;
+    u32 sm = 0, em = 0;
+    if (nf == 0) {  // fast path: the whole tile lies in file m.fa
+      const bool fs0 = (i0 == m.fbase);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        fidx[j][q] = m.fa;
+        const u32 cur = st[j][q];
+        const u32 prv = q == 0 ? prev_last : st[j][q - 1];
+        const u32 nxt = q == 3 ? next_first : st[j][q + 1];
+        const bool pass = !(cur & FAIL);
+        sm |= (u32)(pass && ((q == 0 && fs0) || (prv & FAIL) || prv != cur)) << q;
+        em |= (u32)(pass && ((nxt & FAIL) || nxt != cur)) << q;
+      }
+    } else {
+      int f = overflow ? upper_bound_ll(a.file_off, a.n_files + 1, i0) - 1 : m.fa + upper_bound_ll(sc.fstart, nf, i0);
+      bool fs_cur = (i0 < a.n) && fstart_of(f) == i0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const long long i = i0 + q;
+        fidx[j][q] = f;
+        int fn = f;
+        bool fs_next;
+        if (overflow) {
+          fn = (i + 1 < a.n) ? upper_bound_ll(a.file_off, a.n_files + 1, i + 1) - 1 : f;
+          fs_next = (i + 1 < a.n) && a.file_off[fn] == i + 1;
+        } else {
+          const int k = f - m.fa;
+          fs_next = k < nf && sc.fstart[k] == i + 1;
+          if (fs_next) fn = f + 1;
+          while (fs_next && fn - m.fa < nf && sc.fstart[fn - m.fa] == i + 1) ++fn;  // empty files
+        }
+        const u32 cur = st[j][q];
+        const u32 prv = q == 0 ? prev_last : st[j][q - 1];
+        const u32 nxt = q == 3 ? next_first : st[j][q + 1];
+        const bool pass = !(cur & FAIL);
+        sm |= (u32)(pass && (fs_cur || (prv & FAIL) || prv != cur)) << q;
+        em |= (u32)(pass && (fs_next || (nxt & FAIL) || nxt != cur)) << q;
+        fs_cur = fs_next;
+        f = fn;
+      }
+    }
+    starts[j] = sm;
+    ends[j] = em;
+  }
+  // tile-local compaction: byte-packed per-segment counts, warp + block scan
+  u32 pack = 0;
+#pragma unroll
+  for (int j = 0; j < SEGS; ++j) pack |= (u32)__popc(starts[j]) << (8 * j);
+  const u32 incl = warp_incl_scan(pack);
+  const u32 excl = incl - pack;
+  const u32 wtot = __shfl_sync(MX_FULL, incl, 31);
+  u32 seg_base[SEGS];
+  u32 acc = 0;
+#pragma unroll
+  for (int j = 0; j < SEGS; ++j) {
+    seg_base[j] = acc + ((excl >> (8 * j)) & 0xff);
+    acc += (wtot >> (8 * j)) & 0xff;
+  }
+  if (lane == 0) sc.warp_tot[warp] = acc;
+  if (warp == S1_THREADS / 32 - 1 && lane == 31)  // holder of the tile's last sample
+    sc.last_open = (!(st[SEGS - 1][3] & FAIL) && !((ends[SEGS - 1] >> 3) & 1)) ? 1u : 0u;
+  __syncthreads();
+  if (warp == 0) {
+    const u32 x = lane < S1_THREADS / 32 ? sc.warp_tot[lane] : 0;
+    const u32 inc = warp_incl_scan(x);
+    if (lane < S1_THREADS / 32) sc.warp_tot[lane] = inc - x;
+    if (lane == 31) {
+      a.tile_cnt[tile] = inc;
+      a.tile_open[tile] = (inc > 0 && sc.last_open) ? 1u : 0u;  // last run ends in a later tile
+    }
+  }
+  if (tid == 0) {  // does the tile start inside a run begun in an earlier tile?
+    const u32 first = st[0][0];
+    a.tile_head[tile] = (!(first & FAIL) && !(starts[0] & 1)) ? -1 : 0;
   }
   __syncthreads();
-
-  for (int it = 0;; ++it) {
-    const int s = it % stages;
-    const long long tile = s_tile[s];
-    if (tile >= ntiles) break;
-    const bool staged = tile < nstaged;
-    if (staged) mbar_wait(&s_bar[s], (u32)((it / stages) & 1));
-    const TileMeta m = staged ? s_meta[s] : meta[tile];
-    const long long t0 = tile * TILE;
-    const long long wbase = t0 + (long long)warp * WT;
-
-    // ---- statuses (packed key | fail) of this thread's 4*SEGS samples
-    u32 st[SEGS][4], anyf[SEGS][4];
+  const u64 tbase = (u64)tile * TILE;
+  const u64 base = tbase + sc.warp_tot[warp];
 #pragma unroll
-    for (int j = 0; j < SEGS; ++j)
+  for (int j = 0; j < SEGS; ++j) {
+    if (!(starts[j] | ends[j])) continue;
+    u64 run = base + seg_base[j];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) st[j][q] = anyf[j][q] = 0;
-    for (int p = 0; p < P; ++p) {
-      const int lo = a.lut_off[p] + 1;
-      if (staged) {
-        const int32_t* c = s_codes + ((long long)s * P + p) * TILE + warp * WT + 4 * lane;
-#pragma unroll
-        for (int j = 0; j < SEGS; ++j) {
-          const int4 v = *reinterpret_cast<const int4*>(c + 128 * j);
-          const u32 e0 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v.x);
-          const u32 e1 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v.y);
-          const u32 e2 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v.z);
-          const u32 e3 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v.w);
-          st[j][0] += e0 & ~FAIL; anyf[j][0] |= e0;
-          st[j][1] += e1 & ~FAIL; anyf[j][1] |= e1;
-          st[j][2] += e2 & ~FAIL; anyf[j][2] |= e2;
-          st[j][3] += e3 & ~FAIL; anyf[j][3] |= e3;
-        }
-      } else {
-        const int32_t* col = a.cols[p];
-#pragma unroll
-        for (int j = 0; j < SEGS; ++j)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const long long i = wbase + 128 * j + 4 * lane + q;
-            if (i < a.n) {
-              const u32 e = lut_get<SMEM_LUT>(s_lut, a.lut, lo + col[i]);
-              st[j][q] += e & ~FAIL;
-              anyf[j][q] |= e;
-            }
-          }
+    for (int q = 0; q < 4; ++q) {
+      const long long i = wbase + 128 * j + 4 * lane + q;
+      if ((starts[j] >> q) & 1) {
+        const u32 key = st[j][q];
+        a.rec_key[run] = key;
+        a.rec_file[run] = (u32)fidx[j][q];
+        a.rec_start[run] = (u32)(i - fstart_of(fidx[j][q]));
+        if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)i);
+        ++run;
+      }
+      if ((ends[j] >> q) & 1) {
+        if (run > tbase) a.rec_end[run - 1] = (u32)(i + 1 - fstart_of(fidx[j][q]));
+        else a.tile_head[tile] = i + 1;  // end of the run continuing from before
       }
     }
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const long long i = wbase + 128 * j + 4 * lane + q;
-        st[j][q] = (i < a.n) ? ((anyf[j][q] & FAIL) | st[j][q]) : FAIL;
-      }
-    if (lane == 0) s_warp_first[warp] = st[0][0];
-    if (lane == 31) s_warp_last[warp] = st[SEGS - 1][3];
-    // file starts inside the tile (rare: only tiles that cross a file boundary)
-    const int nf = m.nf;
-    const bool overflow = nf > TMA_FILE_CAP;
-    if (nf > 0 && !overflow)
-      for (int k = tid; k < nf; k += S1_THREADS) s_fstart[k] = a.file_off[m.fa + 1 + k];
-    __syncthreads();
-    const u32 warp_prev = warp == 0 ? m.prev_status : s_warp_last[warp - 1];
-    const u32 warp_next = warp == S1_THREADS / 32 - 1 ? m.next_status : s_warp_first[warp + 1];
-
-    auto fstart_of = [&](int f) -> long long {
-      if (overflow) return a.file_off[f];
-      return f == m.fa ? m.fbase : s_fstart[f - m.fa - 1];
-    };
-
-    u32 starts[SEGS], ends[SEGS];
-    int fidx[SEGS][4];
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j) {
-      u32 prev_last = __shfl_up_sync(MX_FULL, st[j][3], 1);
-      u32 next_first = __shfl_down_sync(MX_FULL, st[j][0], 1);
-      const u32 seg_prev = __shfl_sync(MX_FULL, st[j > 0 ? j - 1 : 0][3], 31);
-      const u32 seg_next = __shfl_sync(MX_FULL, st[j < SEGS - 1 ? j + 1 : 0][0], 0);
-      if (lane == 0) prev_last = j == 0 ? warp_prev : seg_prev;
-      if (lane == 31) next_first = j == SEGS - 1 ? warp_next : seg_next;
-      const long long i0 = wbase + 128 * j + 4 * lane;
-      u32 sm = 0, em = 0;
-      if (nf == 0) {  // fast path: the whole tile lies in file m.fa
-        const bool fs0 = (i0 == m.fbase);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          fidx[j][q] = m.fa;
-          const u32 cur = st[j][q];
-          const u32 prv = q == 0 ? prev_last : st[j][q - 1];
-          const u32 nxt = q == 3 ? next_first : st[j][q + 1];
-          const bool pass = !(cur & FAIL);
-          const bool start = pass && ((q == 0 && fs0) || (prv & FAIL) || prv != cur);
-          const bool end = pass && ((nxt & FAIL) || nxt != cur);
-          sm |= (u32)start << q;
-          em |= (u32)end << q;
-        }
-      } else {
-        int f = overflow ? upper_bound_ll(a.file_off, a.n_files + 1, i0) - 1
-                         : m.fa + upper_bound_ll(s_fstart, nf, i0);
-        bool fs_cur = (i0 < a.n) && fstart_of(f) == i0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const long long i = i0 + q;
-          fidx[j][q] = f;
-          int fn = f;
-          bool fs_next;
-          if (overflow) {
-            fn = (i + 1 < a.n) ? upper_bound_ll(a.file_off, a.n_files + 1, i + 1) - 1 : f;
-            fs_next = (i + 1 < a.n) && a.file_off[fn] == i + 1;
-          } else {
-            const int k = f - m.fa;
-            fs_next = k < nf && s_fstart[k] == i + 1;
-            if (fs_next) fn = f + 1;
-            while (fs_next && fn - m.fa < nf && s_fstart[fn - m.fa] == i + 1) ++fn;
-          }
-          const u32 cur = st[j][q];
-          const u32 prv = q == 0 ? prev_last : st[j][q - 1];
-          const u32 nxt = q == 3 ? next_first : st[j][q + 1];
-          const bool pass = !(cur & FAIL);
-          const bool start = pass && (fs_cur || (prv & FAIL) || prv != cur);
-          const bool end = pass && (fs_next || (nxt & FAIL) || nxt != cur);
-          sm |= (u32)start << q;
-          em |= (u32)end << q;
-          fs_cur = fs_next;
-          f = fn;
-        }
-      }
-      starts[j] = sm;
-      ends[j] = em;
-    }
-
-    // ---- compaction: byte-packed per-segment counts, warp + block scan, look-back
-    u32 pack = 0;
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j) pack |= (u32)__popc(starts[j]) << (8 * j);
-    const u32 incl = warp_incl_scan(pack);
-    const u32 excl = incl - pack;
-    const u32 wtot = __shfl_sync(MX_FULL, incl, 31);
-    u32 seg_base[SEGS];
-    u32 acc = 0;
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j) {
-      seg_base[j] = acc + ((excl >> (8 * j)) & 0xff);
-      acc += (wtot >> (8 * j)) & 0xff;
-    }
-    if (lane == 0) s_warp_tot[warp] = acc;
-    __syncthreads();
-    if (warp == 0) {
-      const u32 v = lane < S1_THREADS / 32 ? s_warp_tot[lane] : 0;
-      const u32 inc = warp_incl_scan(v);
-      const u32 tile_agg = __shfl_sync(MX_FULL, inc, 31);
-      if (lane < S1_THREADS / 32) s_warp_tot[lane] = inc - v;
-      const u64 tex = lookback_exclusive(a.status, (int)tile, tile_agg);
-      if (lane == 0) {
-        s_tile_excl = tex;
-        if (tile == ntiles - 1) *a.n_runs = tex + tile_agg;
-      }
-    }
-    __syncthreads();
-    const u64 base = s_tile_excl + s_warp_tot[warp];
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j) {
-      if (!(starts[j] | ends[j])) continue;
-      u64 run = base + seg_base[j];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const long long i = wbase + 128 * j + 4 * lane + q;
-        if ((starts[j] >> q) & 1) {
-          const u32 key = st[j][q];
-          a.rec_key[run] = key;
-          a.rec_file[run] = (u32)fidx[j][q];
-          a.rec_start[run] = (u32)(i - fstart_of(fidx[j][q]));
-          if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)i);
-          ++run;
-        }
-        if ((ends[j] >> q) & 1) a.rec_end[run - 1] = (u32)(i + 1 - fstart_of(fidx[j][q]));
-      }
-    }
-    __syncthreads();  // slot s and the per-tile scratch are free again
-    if (tid == 0) issue(s);
-    __syncthreads();
   }
 }
 
+template <bool SUMF, int SEGS>
+__device__ __forceinline__ void normalise_status(const S1Args& a, long long wbase, u32 (&st)[SEGS][4],
+                                                 const u32 (&anyf)[SEGS][4]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < SEGS; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long i = wbase + 128 * j + 4 * lane + q;
+      if (SUMF) st[j][q] = (i < a.n && st[j][q] < a.fail_limit) ? st[j][q] : FAIL;
+      else st[j][q] = (i < a.n) ? ((anyf[j][q] & FAIL) | st[j][q]) : FAIL;
+    }
+}
+
 // ---------------------------------------------------------------------------
-// Non-persistent variant: one CTA per tile (thousands of independent CTAs keep
-// HBM busy through occupancy instead of a per-CTA pipeline), tile id =
-// blockIdx.x (CTAs are dispatched in index order, which the look-back relies
-// on, as in CUB's single-pass scan), per-tile metadata from tile_meta_kernel,
-// all column loads of a thread issued before any dependent work (PC = number
-// of properties at compile time; 0 = runtime loop).
+// One CTA per tile. PC = number of properties at compile time (0 = runtime
+// loop, then the fail flag is OR-ed instead of counted).
 template <int SEGS, int PC, bool SMEM_LUT>
 __global__ void __launch_bounds__(S1_THREADS, 2)
-scan_direct_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles) {
+scan_direct_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles, long long tile_base) {
   constexpr int WT = 32 * 4 * SEGS;
   constexpr int TILE = (S1_THREADS / 32) * WT;
+  constexpr bool SUMF = PC > 0;
   extern __shared__ __align__(16) u32 s_lut[];
-  __shared__ long long s_fstart[TMA_FILE_CAP];
-  __shared__ u32 s_warp_first[S1_THREADS / 32], s_warp_last[S1_THREADS / 32], s_warp_tot[S1_THREADS / 32];
-  __shared__ u64 s_tile_excl;
+  __shared__ TileScratch sc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int P = PC > 0 ? PC : a.n_props;
-  const long long tile = blockIdx.x;
+  const long long tile = tile_base + blockIdx.x;
   const long long t0 = tile * TILE;
   const long long wbase = t0 + (long long)warp * WT;
   const bool full = t0 + TILE <= a.n;
@@ -330,16 +259,11 @@ scan_direct_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles
   // 2. LUT to shared memory + tile metadata (overlaps the loads in flight).
   //    With PC > 0 the LUT carries the filter-fail flag as a COUNT above the
   //    key bits, so keying a sample is P lookups + P adds and one compare.
-  constexpr bool SUMF = PC > 0;
   if (SMEM_LUT) {
     const u32* src = SUMF ? a.lut_sum : a.lut;
     for (int i = tid; i < a.lut_off[P]; i += S1_THREADS) s_lut[i] = src[i];
   }
   const TileMeta m = meta[tile];
-  const int nf = m.nf;
-  const bool overflow = nf > TMA_FILE_CAP;
-  if (nf > 0 && !overflow)
-    for (int k = tid; k < nf; k += S1_THREADS) s_fstart[k] = a.file_off[m.fa + 1 + k];
   __syncthreads();
   // 3. statuses
   u32 st[SEGS][4], anyf[SEGS][4];
@@ -388,26 +312,92 @@ scan_direct_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles
       }
     }
   }
+  normalise_status<SUMF, SEGS>(a, wbase, st, anyf);
+  finish_tile<SEGS>(a, m, tile, wbase, st, sc);
+}
+
+// ---------------------------------------------------------------------------
+// Full-tile fast path (the hot kernel at cfg2): tiles [0, nfull) are complete,
+// the property count is a template constant, and everything before emission
+// runs on 32-bit tile-local sample indices. File starts inside a tile (a tile
+// spans at most a few files at realistic file sizes) are handled branch-light
+// for up to 4 boundaries; tiles with more fall back to finish_tile.
+constexpr int FAST_MAX_FS = 4;
+
+template <int PC>
+__global__ void __launch_bounds__(S1_THREADS, 2)
+scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
+  constexpr int SEGS = 4;
+  constexpr int WT = 32 * 4 * SEGS;
+  constexpr int TILE = (S1_THREADS / 32) * WT;
+  extern __shared__ __align__(16) u32 s_lut[];
+  __shared__ TileScratch sc;
+  __shared__ int s_fs[FAST_MAX_FS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long tile = blockIdx.x;
+  const long long t0 = tile * TILE;
+  const int lw = warp * WT + 4 * lane;  // tile-local index of this thread's sample (j=0, q=0)
+  int4 v[PC][SEGS];
+#pragma unroll
+  for (int p = 0; p < PC; ++p) {
+    const int32_t* col = a.cols[p] + t0 + lw;
+#pragma unroll
+    for (int j = 0; j < SEGS; ++j) v[p][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + 128 * j));
+  }
+  for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
+  const TileMeta m = meta[tile];
+  if (tid < FAST_MAX_FS) s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - t0) : 1 << 30;
+  __syncthreads();
+  if (m.nf > FAST_MAX_FS) {  // many tiny files: generic tile body
+    u32 st[SEGS][4], none[SEGS][4];
+#pragma unroll
+    for (int j = 0; j < SEGS; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) st[j][q] = none[j][q] = 0;
+#pragma unroll
+    for (int p = 0; p < PC; ++p) {
+      const u32* L = s_lut + a.lut_off[p] + 1;
+#pragma unroll
+      for (int j = 0; j < SEGS; ++j) {
+        st[j][0] += L[v[p][j].x]; st[j][1] += L[v[p][j].y];
+        st[j][2] += L[v[p][j].z]; st[j][3] += L[v[p][j].w];
+      }
+    }
+    normalise_status<true, SEGS>(a, t0 + warp * WT, st, none);
+    finish_tile<SEGS>(a, m, tile, t0 + warp * WT, st, sc);
+    return;
+  }
+  // statuses: key sum, FAIL when a filter-fail count reached the key bits
+  u32 st[SEGS][4];
 #pragma unroll
   for (int j = 0; j < SEGS; ++j)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const long long i = wbase + 128 * j + 4 * lane + q;
-      if (SUMF) st[j][q] = (i < a.n && st[j][q] < a.fail_limit) ? st[j][q] : FAIL;
-      else st[j][q] = (i < a.n) ? ((anyf[j][q] & FAIL) | st[j][q]) : FAIL;
+    for (int q = 0; q < 4; ++q) st[j][q] = 0;
+#pragma unroll
+  for (int p = 0; p < PC; ++p) {
+    const u32* L = s_lut + a.lut_off[p] + 1;
+#pragma unroll
+    for (int j = 0; j < SEGS; ++j) {
+      st[j][0] += L[v[p][j].x]; st[j][1] += L[v[p][j].y];
+      st[j][2] += L[v[p][j].z]; st[j][3] += L[v[p][j].w];
     }
-  if (lane == 0) s_warp_first[warp] = st[0][0];
-  if (lane == 31) s_warp_last[warp] = st[SEGS - 1][3];
+  }
+  const u32 lim = a.fail_limit;
+#pragma unroll
+  for (int j = 0; j < SEGS; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st[j][q] = st[j][q] < lim ? st[j][q] : FAIL;
+  if (lane == 0) sc.warp_first[warp] = st[0][0];
+  if (lane == 31) sc.warp_last[warp] = st[SEGS - 1][3];
   __syncthreads();
-  const u32 warp_prev = warp == 0 ? m.prev_status : s_warp_last[warp - 1];
-  const u32 warp_next = warp == S1_THREADS / 32 - 1 ? m.next_status : s_warp_first[warp + 1];
-  auto fstart_of = [&](int f) -> long long {
-    if (overflow) return a.file_off[f];
-    return f == m.fa ? m.fbase : s_fstart[f - m.fa - 1];
-  };
-  // 4. run boundaries
-  u32 starts[SEGS], ends[SEGS];
-  int fidx[SEGS][4];
+  const u32 warp_prev = warp == 0 ? m.prev_status : sc.warp_last[warp - 1];
+  const u32 warp_next = warp == S1_THREADS / 32 - 1 ? m.next_status : sc.warp_first[warp + 1];
+  const int fb0 = (int)(m.fbase - t0);  // <= 0: start of the file holding sample 0
+  const int nf = m.nf;
+  int fs[FAST_MAX_FS];
+#pragma unroll
+  for (int k = 0; k < FAST_MAX_FS; ++k) fs[k] = s_fs[k];  // local file starts in (0, TILE], padded
+  u32 starts[SEGS], ends[SEGS], fsel[SEGS];  // fsel: 3 bits per sample = file offset in the tile
 #pragma unroll
   for (int j = 0; j < SEGS; ++j) {
     u32 prev_last = __shfl_up_sync(MX_FULL, st[j][3], 1);
@@ -416,54 +406,34 @@ scan_direct_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles
     const u32 seg_next = __shfl_sync(MX_FULL, st[j < SEGS - 1 ? j + 1 : 0][0], 0);
     if (lane == 0) prev_last = j == 0 ? warp_prev : seg_prev;
     if (lane == 31) next_first = j == SEGS - 1 ? warp_next : seg_next;
-    const long long i0 = wbase + 128 * j + 4 * lane;
+    const int li0 = lw + 128 * j;
+    // file-start bits of samples li0..li0+4 (bit 4 = the next thread's first)
+    u32 fsb = (li0 == fb0) ? 1u : 0u;
+    u32 sel = 0;
+    if (nf) {
+#pragma unroll
+      for (int k = 0; k < FAST_MAX_FS; ++k) {
+        const int d = fs[k] - li0;  // file start k relative to this thread's first sample
+        if (d >= 0 && d <= 4) fsb |= 1u << d;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sel += (u32)(d <= q) << (3 * q);  // files started at or before sample q
+      }
+    }
+    fsel[j] = sel;
     u32 sm = 0, em = 0;
-    if (nf == 0) {
-      const bool fs0 = (i0 == m.fbase);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        fidx[j][q] = m.fa;
-        const u32 cur = st[j][q];
-        const u32 prv = q == 0 ? prev_last : st[j][q - 1];
-        const u32 nxt = q == 3 ? next_first : st[j][q + 1];
-        const bool pass = !(cur & FAIL);
-        sm |= (u32)(pass && ((q == 0 && fs0) || (prv & FAIL) || prv != cur)) << q;
-        em |= (u32)(pass && ((nxt & FAIL) || nxt != cur)) << q;
-      }
-    } else {
-      int f = overflow ? upper_bound_ll(a.file_off, a.n_files + 1, i0) - 1 : m.fa + upper_bound_ll(s_fstart, nf, i0);
-      bool fs_cur = (i0 < a.n) && fstart_of(f) == i0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const long long i = i0 + q;
-        fidx[j][q] = f;
-        int fn = f;
-        bool fs_next;
-        if (overflow) {
-          fn = (i + 1 < a.n) ? upper_bound_ll(a.file_off, a.n_files + 1, i + 1) - 1 : f;
-          fs_next = (i + 1 < a.n) && a.file_off[fn] == i + 1;
-        } else {
-          const int k = f - m.fa;
-          fs_next = k < nf && s_fstart[k] == i + 1;
-          if (fs_next) fn = f + 1;
-          while (fs_next && fn - m.fa < nf && s_fstart[fn - m.fa] == i + 1) ++fn;
-        }
-        const u32 cur = st[j][q];
-        const u32 prv = q == 0 ? prev_last : st[j][q - 1];
-        const u32 nxt = q == 3 ? next_first : st[j][q + 1];
-        const bool pass = !(cur & FAIL);
-        sm |= (u32)(pass && (fs_cur || (prv & FAIL) || prv != cur)) << q;
-        em |= (u32)(pass && (fs_next || (nxt & FAIL) || nxt != cur)) << q;
-        fs_cur = fs_next;
-        f = fn;
-      }
+    for (int q = 0; q < 4; ++q) {
+      const u32 cur = st[j][q];
+      const u32 prv = q == 0 ? prev_last : st[j][q - 1];
+      const u32 nxt = q == 3 ? next_first : st[j][q + 1];
+      const bool pass = !(cur & FAIL);
+      sm |= (u32)(pass && (((fsb >> q) & 1) || (prv & FAIL) || prv != cur)) << q;
+      em |= (u32)(pass && (((fsb >> (q + 1)) & 1) || (nxt & FAIL) || nxt != cur)) << q;
     }
     starts[j] = sm;
     ends[j] = em;
   }
-  // 5. tile-local compaction into this tile's slot region [tile*TILE, ...):
-  //    no inter-tile dependency. Run ends that fall in a later tile are
-  //    patched by slot_fixup_kernel; the first radix pass compacts the slots.
+  // tile-local compaction (same slot layout as finish_tile)
   u32 pack = 0;
 #pragma unroll
   for (int j = 0; j < SEGS; ++j) pack |= (u32)__popc(starts[j]) << (8 * j);
@@ -477,47 +447,145 @@ scan_direct_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles
     seg_base[j] = acc + ((excl >> (8 * j)) & 0xff);
     acc += (wtot >> (8 * j)) & 0xff;
   }
-  __shared__ u32 s_last_open;
-  if (lane == 0) s_warp_tot[warp] = acc;
-  if (warp == S1_THREADS / 32 - 1 && lane == 31)  // holder of the tile's last sample
-    s_last_open = (!(st[SEGS - 1][3] & FAIL) && !((ends[SEGS - 1] >> 3) & 1)) ? 1u : 0u;
+  if (lane == 0) sc.warp_tot[warp] = acc;
+  if (warp == S1_THREADS / 32 - 1 && lane == 31)
+    sc.last_open = (!(st[SEGS - 1][3] & FAIL) && !((ends[SEGS - 1] >> 3) & 1)) ? 1u : 0u;
   __syncthreads();
   if (warp == 0) {
-    const u32 x = lane < S1_THREADS / 32 ? s_warp_tot[lane] : 0;
+    const u32 x = lane < S1_THREADS / 32 ? sc.warp_tot[lane] : 0;
     const u32 inc = warp_incl_scan(x);
-    if (lane < S1_THREADS / 32) s_warp_tot[lane] = inc - x;
+    if (lane < S1_THREADS / 32) sc.warp_tot[lane] = inc - x;
     if (lane == 31) {
       a.tile_cnt[tile] = inc;
-      a.tile_open[tile] = (inc > 0 && s_last_open) ? 1u : 0u;  // last run ends in a later tile
+      a.tile_open[tile] = (inc > 0 && sc.last_open) ? 1u : 0u;
     }
   }
-  if (tid == 0) {  // does the tile start inside a run begun in an earlier tile?
-    const u32 first = st[0][0];
-    a.tile_head[tile] = (!(first & FAIL) && !(starts[0] & 1)) ? -1 : 0;
-  }
+  if (tid == 0) a.tile_head[tile] = (!(st[0][0] & FAIL) && !(starts[0] & 1)) ? -1 : 0;
   __syncthreads();
   const u64 tbase = (u64)tile * TILE;
-  const u64 base = tbase + s_warp_tot[warp];
+  const u64 base = tbase + sc.warp_tot[warp];
 #pragma unroll
   for (int j = 0; j < SEGS; ++j) {
     if (!(starts[j] | ends[j])) continue;
     u64 run = base + seg_base[j];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const long long i = wbase + 128 * j + 4 * lane + q;
+      const int li = lw + 128 * j + q;
+      const int fo = (fsel[j] >> (3 * q)) & 7;  // file = m.fa + fo
+      const long long fstart = fo == 0 ? m.fbase : t0 + s_fs[fo - 1];
       if ((starts[j] >> q) & 1) {
         const u32 key = st[j][q];
         a.rec_key[run] = key;
-        a.rec_file[run] = (u32)fidx[j][q];
-        a.rec_start[run] = (u32)(i - fstart_of(fidx[j][q]));
-        if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)i);
+        a.rec_file[run] = (u32)(m.fa + fo);
+        a.rec_start[run] = (u32)(t0 + li - fstart);
+        if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)(t0 + li));
         ++run;
       }
       if ((ends[j] >> q) & 1) {
-        if (run > tbase) a.rec_end[run - 1] = (u32)(i + 1 - fstart_of(fidx[j][q]));
-        else a.tile_head[tile] = i + 1;  // end of the run continuing from before
+        if (run > tbase) a.rec_end[run - 1] = (u32)(t0 + li + 1 - fstart);
+        else a.tile_head[tile] = t0 + li + 1;
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent CTAs with a TMA ring (cp.async.bulk + mbarrier). Tiles are
+// claimed in increasing order from an atomic counter; slot s of the ring holds
+// every column's tile plus the tile's metadata. Requires the shared-memory LUT
+// and 16-byte aligned columns; the (partial) last tile is read directly.
+template <int SEGS, int PC>
+__global__ void __launch_bounds__(S1_THREADS, 2)
+scan_pipe_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles, long long nstaged, int stages,
+                 int lut_bytes) {
+  constexpr int WT = 32 * 4 * SEGS;
+  constexpr int TILE = (S1_THREADS / 32) * WT;
+  constexpr bool SUMF = PC > 0;
+  extern __shared__ __align__(128) unsigned char dyn[];
+  u32* s_lut = reinterpret_cast<u32*>(dyn);
+  const int P = PC > 0 ? PC : a.n_props;
+  int32_t* s_codes = reinterpret_cast<int32_t*>(dyn + lut_bytes);  // [stages][P][TILE]
+  TileMeta* s_meta = reinterpret_cast<TileMeta*>(s_codes + (long long)stages * P * TILE);
+  __shared__ __align__(8) u64 s_bar[TMA_MAX_STAGES];
+  __shared__ long long s_tile[TMA_MAX_STAGES];
+  __shared__ TileScratch sc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    const u32* src = SUMF ? a.lut_sum : a.lut;
+    for (int i = tid; i < a.lut_off[P]; i += S1_THREADS) s_lut[i] = src[i];
+  }
+  auto issue = [&](int s) {  // thread 0: claim the next tile into slot s
+    const long long t = (long long)atomicAdd(a.tile_ctr, 1u);
+    s_tile[s] = t;
+    if (t < nstaged) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_tx(&s_bar[s], (u32)(P * TILE * 4 + sizeof(TileMeta)));
+      for (int p = 0; p < P; ++p)
+        bulk_g2s(s_codes + ((long long)s * P + p) * TILE, a.cols[p] + t * TILE, TILE * 4, &s_bar[s]);
+      bulk_g2s(&s_meta[s], meta + t, sizeof(TileMeta), &s_bar[s]);
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < stages; ++s) issue(s);
+  }
+  __syncthreads();
+  for (int it = 0;; ++it) {
+    const int s = it % stages;
+    const long long tile = s_tile[s];
+    if (tile >= ntiles) break;
+    const bool staged = tile < nstaged;
+    if (staged) mbar_wait(&s_bar[s], (u32)((it / stages) & 1));
+    const TileMeta m = staged ? s_meta[s] : meta[tile];
+    const long long wbase = tile * TILE + (long long)warp * WT;
+    u32 st[SEGS][4], anyf[SEGS][4];
+#pragma unroll
+    for (int j = 0; j < SEGS; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) st[j][q] = anyf[j][q] = 0;
+    for (int p = 0; p < P; ++p) {
+      const int lo = a.lut_off[p] + 1;
+      if (staged) {
+        const int32_t* c = s_codes + ((long long)s * P + p) * TILE + warp * WT + 4 * lane;
+#pragma unroll
+        for (int j = 0; j < SEGS; ++j) {
+          const int4 v = *reinterpret_cast<const int4*>(c + 128 * j);
+          const u32 e[4] = {s_lut[lo + v.x], s_lut[lo + v.y], s_lut[lo + v.z], s_lut[lo + v.w]};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (SUMF) {
+              st[j][q] += e[q];
+            } else {
+              st[j][q] += e[q] & ~FAIL;
+              anyf[j][q] |= e[q];
+            }
+          }
+        }
+      } else {
+        const int32_t* col = a.cols[p];
+#pragma unroll
+        for (int j = 0; j < SEGS; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const long long i = wbase + 128 * j + 4 * lane + q;
+            if (i < a.n) {
+              const u32 e = s_lut[lo + col[i]];
+              if (SUMF) {
+                st[j][q] += e;
+              } else {
+                st[j][q] += e & ~FAIL;
+                anyf[j][q] |= e;
+              }
+            }
+          }
+      }
+    }
+    normalise_status<SUMF, SEGS>(a, wbase, st, anyf);
+    finish_tile<SEGS>(a, m, tile, wbase, st, sc);
+    __syncthreads();  // slot s and the tile scratch are free again
+    if (tid == 0) issue(s);
+    __syncthreads();
   }
 }
 

@@ -567,27 +567,65 @@ interval_cum_kernel(const u32* start, const u32* end, long long n, u64* status, 
 
 // ---------------------------------------------------------------- host side
 template <int SEGS, int PC>
-static void launch_direct(const S1Args& a, const TileMeta* m, long long ntiles, bool smem_lut, int lut_total,
-                          cudaStream_t s) {
-  if (smem_lut) {
-    scan_direct_kernel<SEGS, PC, true><<<(unsigned)ntiles, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m, ntiles);
-  } else {
-    scan_direct_kernel<SEGS, 0, false><<<(unsigned)ntiles, S1_THREADS, 0, s>>>(a, m, ntiles);
-  }
+static int launch_pipe(const S1Args& a, const TileMeta* m, long long ntiles, long long nstaged, int stages,
+                       int lut_bytes, int n_sm, cudaStream_t s) {
+  auto kernel = scan_pipe_kernel<SEGS, PC>;
+  const size_t dyn = lut_bytes + (size_t)stages * a.n_props * (32 * 4 * SEGS * (S1_THREADS / 32)) * 4 +
+                     (size_t)stages * sizeof(TileMeta);
+  MX_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  int occ = 1;
+  MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, S1_THREADS, dyn));
+  const long long grid = std::min<long long>(ntiles, (long long)n_sm * std::max(occ, 1));
+  kernel<<<(unsigned)grid, S1_THREADS, dyn, s>>>(a, m, ntiles, nstaged, stages, lut_bytes);
+  return MX_OK;
 }
 
 template <int SEGS>
-static void dispatch_direct(const S1Args& a, const TileMeta* m, long long ntiles, bool smem_lut, int lut_total,
-                            cudaStream_t s) {
-  switch (smem_lut && a.lut_sum ? a.n_props : 0) {
-    case 1: launch_direct<SEGS, 1>(a, m, ntiles, true, lut_total, s); break;
-    case 2: launch_direct<SEGS, 2>(a, m, ntiles, true, lut_total, s); break;
-    case 3: launch_direct<SEGS, 3>(a, m, ntiles, true, lut_total, s); break;
-    case 4: launch_direct<SEGS, 4>(a, m, ntiles, true, lut_total, s); break;
-    case 5: launch_direct<SEGS, 5>(a, m, ntiles, true, lut_total, s); break;
-    case 6: launch_direct<SEGS, 6>(a, m, ntiles, true, lut_total, s); break;
-    default: launch_direct<SEGS, 0>(a, m, ntiles, smem_lut, lut_total, s); break;
+static int dispatch_pipe(const S1Args& a, const TileMeta* m, long long ntiles, long long nstaged, int stages,
+                         int lut_bytes, int n_sm, cudaStream_t s) {
+  switch (a.lut_sum ? a.n_props : 0) {
+    case 2: return launch_pipe<SEGS, 2>(a, m, ntiles, nstaged, stages, lut_bytes, n_sm, s);
+    case 3: return launch_pipe<SEGS, 3>(a, m, ntiles, nstaged, stages, lut_bytes, n_sm, s);
+    case 5: return launch_pipe<SEGS, 5>(a, m, ntiles, nstaged, stages, lut_bytes, n_sm, s);
+    default: return launch_pipe<SEGS, 0>(a, m, ntiles, nstaged, stages, lut_bytes, n_sm, s);
   }
+}
+
+template <int SEGS, int PC>
+static void launch_direct(const S1Args& a, const TileMeta* m, long long ntiles, bool smem_lut, int lut_total,
+                          cudaStream_t s, long long first = 0) {
+  if (ntiles - first <= 0) return;
+  const unsigned grid = (unsigned)(ntiles - first);
+  if (smem_lut) {
+    scan_direct_kernel<SEGS, PC, true><<<grid, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m, ntiles, first);
+  } else {
+    scan_direct_kernel<SEGS, 0, false><<<grid, S1_THREADS, 0, s>>>(a, m, ntiles, first);
+  }
+}
+
+template <int PC>
+static void launch_fast(const S1Args& a, const TileMeta* m, long long nfull, int lut_total, cudaStream_t s) {
+  if (nfull > 0) scan_fast_kernel<PC><<<(unsigned)nfull, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m);
+}
+
+// full tiles through scan_fast_kernel when it applies, the rest generically
+template <int SEGS>
+static void dispatch_direct(const S1Args& a, const TileMeta* m, long long ntiles, bool smem_lut, int lut_total,
+                            cudaStream_t s, long long nfull_aligned) {
+  const int pc = smem_lut && a.lut_sum ? a.n_props : 0;
+  long long done = 0;
+  if (SEGS == 4 && nfull_aligned > 0 && pc >= 1 && pc <= 6) {
+    switch (pc) {
+      case 1: launch_fast<1>(a, m, nfull_aligned, lut_total, s); break;
+      case 2: launch_fast<2>(a, m, nfull_aligned, lut_total, s); break;
+      case 3: launch_fast<3>(a, m, nfull_aligned, lut_total, s); break;
+      case 4: launch_fast<4>(a, m, nfull_aligned, lut_total, s); break;
+      case 5: launch_fast<5>(a, m, nfull_aligned, lut_total, s); break;
+      default: launch_fast<6>(a, m, nfull_aligned, lut_total, s); break;
+    }
+    done = nfull_aligned;
+  }
+  launch_direct<SEGS, 0>(a, m, ntiles, smem_lut, lut_total, s, done);
 }
 
 int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
@@ -635,35 +673,39 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   ix.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
   ix.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
 
-  // ---- tile geometry of the TMA-staged persistent scan (scan_tma.cuh):
-  // as many 16-sample-per-thread tiles as let two CTAs per SM keep a ring of
-  // >= 2 column tiles each in shared memory.
+  // ---- stage-1 pass variant (MX_SCAN = direct (default) | pipe | v1):
+  //  direct: one CTA per 4096-sample tile, slot output (scan_direct_kernel)
+  //  pipe:   persistent CTAs + TMA ring, slot output (scan_pipe_kernel)
+  //  v1:     one CTA per tile, decoupled look-back output (scan_runs_kernel)
   const bool smem_lut = lut_total <= MX_SMEM_LUT_MAX;
-  // MX_SCAN = direct (default) | tma | v1 selects the stage-1 pass variant
   const char* scan_env = getenv("MX_SCAN");
   const bool use_v1 = scan_env && !strcmp(scan_env, "v1");
-  const bool use_tma = scan_env && !strcmp(scan_env, "tma");
-  const int direct_segs = 4;  // slot mode: scan tile == radix tile (4096)
-  const bool slot_mode = !use_v1 && !use_tma;
-  int dev = 0, n_sm = 148;
+  const bool use_pipe = scan_env && (!strcmp(scan_env, "pipe") || !strcmp(scan_env, "tma")) && smem_lut;
+  const bool slot_mode = !use_v1;
+  int dev = 0, n_sm = 148, smem_optin = 0;
   MX_CUDA_TRY(cudaGetDevice(&dev));
   MX_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  MX_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int lut_bytes = smem_lut ? (lut_total * 4 + 127) / 128 * 128 : 0;
   const int P = d->n_props;
-  int segs = 1, stages = 2;
+  // pipe geometry: the widest tile whose ring of >= 2 slots fits, then as
+  // many slots (<= 4) as fit in ~200 KB
+  int pipe_segs = 1, stages = 2;
   {
-    const int budget = 100 * 1024;
+    const char* kb = getenv("MX_PIPE_KB");  // per-CTA ring budget (2 CTAs/SM by default)
+    const int budget = std::min(smem_optin - 8 * 1024, (kb ? atoi(kb) : 100) * 1024);
     const int cand[3] = {4, 2, 1};
     for (int c = 0; c < 3; ++c) {
       const int stage_bytes = P * 1024 * cand[c] * 4 + (int)sizeof(TileMeta);
       if (lut_bytes + 2 * stage_bytes <= budget) {
-        segs = cand[c];
+        pipe_segs = cand[c];
         stages = std::min(TMA_MAX_STAGES, (budget - lut_bytes) / stage_bytes);
         break;
       }
     }
   }
-  const int tile_len = use_v1 ? S1_TILE : (use_tma ? 1024 * segs : 1024 * direct_segs);
+  constexpr int direct_segs = 4;
+  const int tile_len = use_v1 ? S1_TILE : (use_pipe ? 1024 * pipe_segs : 1024 * direct_segs);
   const int ntiles = (int)((n + tile_len - 1) / tile_len);
   bool aligned = true;
   for (int p = 0; p < P; ++p) aligned &= (reinterpret_cast<uintptr_t>(d->columns[p]) % 16) == 0;
@@ -710,40 +752,28 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
       mx_count_launch();
     }
     MX_CUDA_TRY(cudaGetLastError());
-  } else if (ntiles > 0 && !use_tma) {
+  } else if (ntiles > 0) {
     MX_CUDA_TRY(tmeta.alloc(ntiles, s));
     tile_meta_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(a, tile_len, ntiles, tmeta.p);
     mx_count_launch();
     {
       MxPhase ph("scan_runs", s);
-      dispatch_direct<direct_segs>(a, tmeta.p, ntiles, smem_lut, lut_total, s);
+      int rc = MX_OK;
+      if (use_pipe) {
+        if (pipe_segs == 4) rc = dispatch_pipe<4>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes, n_sm, s);
+        else if (pipe_segs == 2) rc = dispatch_pipe<2>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes, n_sm, s);
+        else rc = dispatch_pipe<1>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes, n_sm, s);
+      } else {
+        dispatch_direct<direct_segs>(a, tmeta.p, ntiles, smem_lut, lut_total, s,
+                                     getenv("MX_SCAN_NOFAST") ? 0 : nstaged);
+      }
       mx_count_launch();
+      if (rc != MX_OK) return rc;
     }
     slot_fixup_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(ntiles, tile_len, t_cnt.p, t_open.p, t_head.p, rf.p,
                                                           a.file_off, re.p, scratch64.p);
     mx_count_launch();
     MX_CUDA_TRY(cudaGetLastError());
-  } else if (ntiles > 0) {
-    MX_CUDA_TRY(tmeta.alloc(ntiles, s));
-    tile_meta_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(a, tile_len, ntiles, tmeta.p);
-    mx_count_launch();
-    const size_t dyn = lut_bytes + (size_t)stages * P * tile_len * 4 + (size_t)stages * sizeof(TileMeta);
-    auto launch = [&](auto kernel) -> int {
-      MX_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-      int occ = 1;
-      MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, S1_THREADS, dyn));
-      const long long grid = std::min<long long>(ntiles, (long long)n_sm * std::max(occ, 1));
-      MxPhase ph("scan_runs", s);
-      kernel<<<(unsigned)grid, S1_THREADS, dyn, s>>>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes);
-      mx_count_launch();
-      MX_CUDA_TRY(cudaGetLastError());
-      return MX_OK;
-    };
-    int rc = MX_OK;
-    if (segs == 4) rc = smem_lut ? launch(scan_tma_kernel<4, true>) : launch(scan_tma_kernel<4, false>);
-    else if (segs == 2) rc = smem_lut ? launch(scan_tma_kernel<2, true>) : launch(scan_tma_kernel<2, false>);
-    else rc = smem_lut ? launch(scan_tma_kernel<1, true>) : launch(scan_tma_kernel<1, false>);
-    if (rc != MX_OK) return rc;
   }
   u64 h_runs = 0;
   DevError h_err;
