@@ -233,16 +233,13 @@ __device__ __forceinline__ void normalise_status(const S1Args& a, long long wbas
 // One CTA per tile. PC = number of properties at compile time (0 = runtime
 // loop, then the fail flag is OR-ed instead of counted).
 template <int SEGS, int PC, bool SMEM_LUT>
-__global__ void __launch_bounds__(S1_THREADS, 2)
-scan_direct_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles, long long tile_base) {
+__device__ __forceinline__ void direct_tile(const S1Args& a, const TileMeta* __restrict__ meta, long long tile,
+                                            u32* s_lut, TileScratch& sc) {
   constexpr int WT = 32 * 4 * SEGS;
   constexpr int TILE = (S1_THREADS / 32) * WT;
   constexpr bool SUMF = PC > 0;
-  extern __shared__ __align__(16) u32 s_lut[];
-  __shared__ TileScratch sc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int P = PC > 0 ? PC : a.n_props;
-  const long long tile = tile_base + blockIdx.x;
   const long long t0 = tile * TILE;
   const long long wbase = t0 + (long long)warp * WT;
   const bool full = t0 + TILE <= a.n;
@@ -316,6 +313,26 @@ scan_direct_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles
   finish_tile<SEGS>(a, m, tile, wbase, st, sc);
 }
 
+template <int SEGS, int PC, bool SMEM_LUT>
+__global__ void __launch_bounds__(S1_THREADS, 2)
+scan_direct_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles, long long tile_base) {
+  extern __shared__ __align__(16) u32 s_lut[];
+  __shared__ TileScratch sc;
+  direct_tile<SEGS, PC, SMEM_LUT>(a, meta, tile_base + blockIdx.x, s_lut, sc);
+}
+
+// tiles deferred by scan_fast_kernel (more file starts than it handles)
+template <int SEGS, bool SMEM_LUT>
+__global__ void __launch_bounds__(S1_THREADS, 2) scan_list_kernel(S1Args a, const TileMeta* __restrict__ meta) {
+  extern __shared__ __align__(16) u32 s_lut[];
+  __shared__ TileScratch sc;
+  const u32 n = *a.defer_cnt;
+  for (u32 x = blockIdx.x; x < n; x += gridDim.x) {
+    direct_tile<SEGS, 0, SMEM_LUT>(a, meta, a.defer_list[x], s_lut, sc);
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Full-tile fast path (the hot kernel at cfg2): tiles [0, nfull) are complete,
 // the property count is a template constant, and everything before emission
@@ -346,27 +363,12 @@ scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
   }
   for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
   const TileMeta m = meta[tile];
-  if (tid < FAST_MAX_FS) s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - t0) : 1 << 30;
-  __syncthreads();
-  if (m.nf > FAST_MAX_FS) {  // many tiny files: generic tile body
-    u32 st[SEGS][4], none[SEGS][4];
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) st[j][q] = none[j][q] = 0;
-#pragma unroll
-    for (int p = 0; p < PC; ++p) {
-      const u32* L = s_lut + a.lut_off[p] + 1;
-#pragma unroll
-      for (int j = 0; j < SEGS; ++j) {
-        st[j][0] += L[v[p][j].x]; st[j][1] += L[v[p][j].y];
-        st[j][2] += L[v[p][j].z]; st[j][3] += L[v[p][j].w];
-      }
-    }
-    normalise_status<true, SEGS>(a, t0 + warp * WT, st, none);
-    finish_tile<SEGS>(a, m, tile, t0 + warp * WT, st, sc);
+  if (m.nf > FAST_MAX_FS) {  // many tiny files: deferred to scan_list_kernel
+    if (tid == 0) a.defer_list[atomicAdd(a.defer_cnt, 1u)] = (u32)tile;
     return;
   }
+  if (tid < FAST_MAX_FS) s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - t0) : 1 << 30;
+  __syncthreads();
   // statuses: key sum, FAIL when a filter-fail count reached the key bits
   u32 st[SEGS][4];
 #pragma unroll

@@ -60,6 +60,8 @@ struct S1Args {
   u32* tile_cnt;         // slot mode: runs started in each tile
   u32* tile_open;        // slot mode: tile's last run ends in a later tile
   long long* tile_head;  // slot mode: 0 none, -1 run passes through, >0 end+1 of the continuing run
+  u32* defer_list;       // tiles scan_fast_kernel leaves to scan_list_kernel
+  u32* defer_cnt;
 };
 
 template <bool SMEM_LUT>
@@ -624,6 +626,9 @@ static void dispatch_direct(const S1Args& a, const TileMeta* m, long long ntiles
       default: launch_fast<6>(a, m, nfull_aligned, lut_total, s); break;
     }
     done = nfull_aligned;
+    // tiles the fast kernel deferred (more file starts than it handles)
+    const long long grid = std::min<long long>(nfull_aligned, 148 * 4);
+    scan_list_kernel<SEGS, true><<<(unsigned)grid, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m);
   }
   launch_direct<SEGS, 0>(a, m, ntiles, smem_lut, lut_total, s, done);
 }
@@ -717,15 +722,19 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   DevBuf<DevError> err;
   // worst case every sample is its own run; slot mode addresses whole tiles
   const long long cap = std::max<long long>(1, slot_mode ? (long long)ntiles * tile_len : n);
-  DevBuf<u32> t_cnt, t_open;
+  DevBuf<u32> t_cnt, t_open, defer;
   DevBuf<long long> t_head;
   if (slot_mode && ntiles > 0) {
     MX_CUDA_TRY(t_cnt.alloc(ntiles, s));
     MX_CUDA_TRY(t_open.alloc(ntiles, s));
     MX_CUDA_TRY(t_head.alloc(ntiles, s));
+    MX_CUDA_TRY(defer.alloc(ntiles + 1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(defer.p + ntiles, 0, sizeof(u32), s));
     a.tile_cnt = t_cnt.p;
     a.tile_open = t_open.p;
     a.tile_head = t_head.p;
+    a.defer_list = defer.p;
+    a.defer_cnt = defer.p + ntiles;
   }
   MX_CUDA_TRY(rk.alloc(cap, s));
   MX_CUDA_TRY(rf.alloc(cap, s));
