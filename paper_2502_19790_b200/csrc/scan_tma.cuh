@@ -341,49 +341,17 @@ __global__ void __launch_bounds__(S1_THREADS, 2) scan_list_kernel(S1Args a, cons
 // for up to 4 boundaries; tiles with more fall back to finish_tile.
 constexpr int FAST_MAX_FS = 4;
 
-template <int PC>
-__global__ void __launch_bounds__(S1_THREADS, 2)
-scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
+// Tile body of the fast path, given the raw key sums st[j][q] of this thread's
+// samples (tile-local index warp*512 + 128j + 4lane + q). s_fs: the tile's
+// file starts (local, padded with 1<<30), visible to the CTA.
+__device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, long long tile, u32 (&st)[4][4],
+                                          TileScratch& sc, const int* s_fs) {
   constexpr int SEGS = 4;
   constexpr int WT = 32 * 4 * SEGS;
   constexpr int TILE = (S1_THREADS / 32) * WT;
-  extern __shared__ __align__(16) u32 s_lut[];
-  __shared__ TileScratch sc;
-  __shared__ int s_fs[FAST_MAX_FS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long tile = blockIdx.x;
   const long long t0 = tile * TILE;
   const int lw = warp * WT + 4 * lane;  // tile-local index of this thread's sample (j=0, q=0)
-  int4 v[PC][SEGS];
-#pragma unroll
-  for (int p = 0; p < PC; ++p) {
-    const int32_t* col = a.cols[p] + t0 + lw;
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j) v[p][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + 128 * j));
-  }
-  for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
-  const TileMeta m = meta[tile];
-  if (m.nf > FAST_MAX_FS) {  // many tiny files: deferred to scan_list_kernel
-    if (tid == 0) a.defer_list[atomicAdd(a.defer_cnt, 1u)] = (u32)tile;
-    return;
-  }
-  if (tid < FAST_MAX_FS) s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - t0) : 1 << 30;
-  __syncthreads();
-  // statuses: key sum, FAIL when a filter-fail count reached the key bits
-  u32 st[SEGS][4];
-#pragma unroll
-  for (int j = 0; j < SEGS; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) st[j][q] = 0;
-#pragma unroll
-  for (int p = 0; p < PC; ++p) {
-    const u32* L = s_lut + a.lut_off[p] + 1;
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j) {
-      st[j][0] += L[v[p][j].x]; st[j][1] += L[v[p][j].y];
-      st[j][2] += L[v[p][j].z]; st[j][3] += L[v[p][j].w];
-    }
-  }
   const u32 lim = a.fail_limit;
 #pragma unroll
   for (int j = 0; j < SEGS; ++j)
@@ -463,31 +431,149 @@ scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
     }
   }
   if (tid == 0) a.tile_head[tile] = (!(st[0][0] & FAIL) && !(starts[0] & 1)) ? -1 : 0;
+  __shared__ u32 s_off[FAST_MAX_FS + 1];  // local sample -> in-file sample offset per file of the tile
+  if (tid <= FAST_MAX_FS) s_off[tid] = tid == 0 ? (u32)(t0 - m.fbase) : (u32)(-s_fs[tid - 1]);
   __syncthreads();
+  // records, all in 32-bit tile-local slot indices
   const u64 tbase = (u64)tile * TILE;
-  const u64 base = tbase + sc.warp_tot[warp];
+  u32* __restrict__ rk = a.rec_key + tbase;
+  u32* __restrict__ rf = a.rec_file + tbase;
+  u32* __restrict__ rs = a.rec_start + tbase;
+  u32* __restrict__ re = a.rec_end + tbase;
+  const u32 wb = sc.warp_tot[warp];
 #pragma unroll
   for (int j = 0; j < SEGS; ++j) {
     if (!(starts[j] | ends[j])) continue;
-    u64 run = base + seg_base[j];
+    u32 run = wb + seg_base[j];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int li = lw + 128 * j + q;
-      const int fo = (fsel[j] >> (3 * q)) & 7;  // file = m.fa + fo
-      const long long fstart = fo == 0 ? m.fbase : t0 + s_fs[fo - 1];
+      const u32 li = (u32)(lw + 128 * j + q);
+      const u32 fo = (fsel[j] >> (3 * q)) & 7;  // file = m.fa + fo
       if ((starts[j] >> q) & 1) {
         const u32 key = st[j][q];
-        a.rec_key[run] = key;
-        a.rec_file[run] = (u32)(m.fa + fo);
-        a.rec_start[run] = (u32)(t0 + li - fstart);
+        rk[run] = key;
+        rf[run] = (u32)m.fa + fo;
+        rs[run] = li + s_off[fo];
         if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)(t0 + li));
         ++run;
       }
       if ((ends[j] >> q) & 1) {
-        if (run > tbase) a.rec_end[run - 1] = (u32)(t0 + li + 1 - fstart);
+        if (run > 0) re[run - 1] = li + 1 + s_off[fo];
         else a.tile_head[tile] = t0 + li + 1;
       }
     }
+  }
+}
+
+template <int PC>
+__device__ __forceinline__ void lut_sums(const u32* s_lut, const S1Args& a, const int4 (&v)[PC][4], u32 (&st)[4][4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st[j][q] = 0;
+#pragma unroll
+  for (int p = 0; p < PC; ++p) {
+    const u32* L = s_lut + a.lut_off[p] + 1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      st[j][0] += L[v[p][j].x]; st[j][1] += L[v[p][j].y];
+      st[j][2] += L[v[p][j].z]; st[j][3] += L[v[p][j].w];
+    }
+  }
+}
+
+// one CTA per full tile, loads in registers
+template <int PC>
+__global__ void __launch_bounds__(S1_THREADS, 2)
+scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
+  constexpr int TILE = S1_THREADS * 16;
+  extern __shared__ __align__(16) u32 s_lut[];
+  __shared__ TileScratch sc;
+  __shared__ int s_fs[FAST_MAX_FS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long tile = blockIdx.x;
+  const long long t0 = tile * TILE;
+  const int lw = warp * 512 + 4 * lane;
+  int4 v[PC][4];
+#pragma unroll
+  for (int p = 0; p < PC; ++p) {
+    const int32_t* col = a.cols[p] + t0 + lw;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[p][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + 128 * j));
+  }
+  for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
+  const TileMeta m = meta[tile];
+  if (m.nf > FAST_MAX_FS) {  // many tiny files: deferred to scan_list_kernel
+    if (tid == 0) a.defer_list[atomicAdd(a.defer_cnt, 1u)] = (u32)tile;
+    return;
+  }
+  if (tid < FAST_MAX_FS) s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - t0) : 1 << 30;
+  __syncthreads();
+  u32 st[4][4];
+  lut_sums<PC>(s_lut, a, v, st);
+  fast_tile(a, m, tile, st, sc, s_fs);
+}
+
+// persistent CTAs, every full tile's columns + metadata streamed into a ring
+// of shared-memory slots by cp.async.bulk (TMA); same tile body
+template <int PC>
+__global__ void __launch_bounds__(S1_THREADS, 1)
+scan_fast_pipe_kernel(S1Args a, const TileMeta* __restrict__ meta, long long nfull, int stages, int lut_bytes) {
+  constexpr int TILE = S1_THREADS * 16;
+  extern __shared__ __align__(128) unsigned char dyn[];
+  u32* s_lut = reinterpret_cast<u32*>(dyn);
+  int32_t* s_codes = reinterpret_cast<int32_t*>(dyn + lut_bytes);  // [stages][PC][TILE]
+  TileMeta* s_meta = reinterpret_cast<TileMeta*>(s_codes + (long long)stages * PC * TILE);
+  __shared__ __align__(8) u64 s_bar[TMA_MAX_STAGES];
+  __shared__ long long s_tile[TMA_MAX_STAGES];
+  __shared__ TileScratch sc;
+  __shared__ int s_fs[FAST_MAX_FS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
+  auto issue = [&](int s) {  // thread 0: claim the next full tile into slot s
+    const long long t = (long long)atomicAdd(a.tile_ctr, 1u);
+    s_tile[s] = t;
+    if (t < nfull) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_tx(&s_bar[s], (u32)(PC * TILE * 4 + sizeof(TileMeta)));
+#pragma unroll
+      for (int p = 0; p < PC; ++p)
+        bulk_g2s(s_codes + ((long long)s * PC + p) * TILE, a.cols[p] + t * TILE, TILE * 4, &s_bar[s]);
+      bulk_g2s(&s_meta[s], meta + t, sizeof(TileMeta), &s_bar[s]);
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < stages; ++s) issue(s);
+  }
+  __syncthreads();
+  const int lw = warp * 512 + 4 * lane;
+  for (int it = 0;; ++it) {
+    const int s = it % stages;
+    const long long tile = s_tile[s];
+    if (tile >= nfull) break;
+    mbar_wait(&s_bar[s], (u32)((it / stages) & 1));
+    const TileMeta m = s_meta[s];
+    if (m.nf > FAST_MAX_FS) {
+      if (tid == 0) a.defer_list[atomicAdd(a.defer_cnt, 1u)] = (u32)tile;
+    } else {
+      int4 v[PC][4];
+      const int32_t* c = s_codes + (long long)s * PC * TILE + lw;
+#pragma unroll
+      for (int p = 0; p < PC; ++p)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[p][j] = *reinterpret_cast<const int4*>(c + p * TILE + 128 * j);
+      if (tid < FAST_MAX_FS)
+        s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - tile * TILE) : 1 << 30;
+      u32 st[4][4];
+      lut_sums<PC>(s_lut, a, v, st);
+      __syncthreads();  // s_fs
+      fast_tile(a, m, tile, st, sc, s_fs);
+    }
+    __syncthreads();  // slot s and the tile scratch are free again
+    if (tid == 0) issue(s);
+    __syncthreads();
   }
 }
 

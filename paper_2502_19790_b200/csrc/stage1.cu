@@ -607,7 +607,23 @@ static void launch_direct(const S1Args& a, const TileMeta* m, long long ntiles, 
 
 template <int PC>
 static void launch_fast(const S1Args& a, const TileMeta* m, long long nfull, int lut_total, cudaStream_t s) {
-  if (nfull > 0) scan_fast_kernel<PC><<<(unsigned)nfull, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m);
+  if (nfull <= 0) return;
+  const char* env = getenv("MX_SCAN");
+  if (env && !strcmp(env, "fastpipe")) {  // persistent + TMA ring variant
+    int dev = 0, n_sm = 148, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int lut_bytes = (lut_total * 4 + 127) / 128 * 128;
+    const int stage = PC * S1_THREADS * 16 * 4 + (int)sizeof(TileMeta);
+    const int stages = std::min(TMA_MAX_STAGES, (optin - 16 * 1024 - lut_bytes) / stage);
+    const size_t dyn = lut_bytes + (size_t)stages * stage;
+    auto kernel = scan_fast_pipe_kernel<PC>;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    kernel<<<(unsigned)std::min<long long>(nfull, n_sm), S1_THREADS, dyn, s>>>(a, m, nfull, stages, lut_bytes);
+    return;
+  }
+  scan_fast_kernel<PC><<<(unsigned)nfull, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m);
 }
 
 // full tiles through scan_fast_kernel when it applies, the rest generically
