@@ -150,6 +150,10 @@ int mx_gen_result_device(const mx_gen* gen, const int64_t** chunk_offsets, const
                          const uint32_t** end);
 /* Shortfall report of the last generate() that returned None: host [n_mkeys]. */
 int mx_gen_report(const mx_gen* gen, int64_t* remaining);
+/* Remember / restore the cursor state and next chunk id on the device (used
+ * to rewind a look-ahead plan to the last chunk handed to the caller). */
+int mx_gen_mark(mx_gen* gen);
+int mx_gen_reset_to_mark(mx_gen* gen);
 int mx_gen_next_chunk_id(const mx_gen* gen, int64_t* next_id);
 int mx_gen_set_next_chunk_id(mx_gen* gen, int64_t next_id);
 /* Cursor checkpoint form {pos, offset} per component rank

@@ -94,6 +94,8 @@ _SIGS = {
     "mx_gen_result_copy": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "mx_gen_result_device": (C.c_int, [vp, P(vp), P(vp), P(vp), P(vp), P(vp), P(vp)]),
     "mx_gen_report": (C.c_int, [vp, vp]),
+    "mx_gen_mark": (C.c_int, [vp]),
+    "mx_gen_reset_to_mark": (C.c_int, [vp]),
     "mx_gen_next_chunk_id": (C.c_int, [vp, P(i64)]),
     "mx_gen_set_next_chunk_id": (C.c_int, [vp, i64]),
     "mx_gen_get_cursors": (C.c_int, [vp, vp, vp]),

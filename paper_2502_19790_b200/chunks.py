@@ -216,7 +216,12 @@ class ChunkGenerator:
     # ---------------------------------------------------------- planning
     def _mixture_desc(self, spec: MixtureSpec):
         mkeys = spec.keys()
-        allow, base, words = self.index.codec.allow_table(mkeys)
+        sig = tuple(k.entries for k in mkeys)
+        cached = getattr(self, "_allow_cache", None)
+        if cached is None or cached[0] != sig:  # ADO re-plans with new weights, same keys
+            cached = (sig, *self.index.codec.allow_table(mkeys))
+            self._allow_cache = cached
+        _, allow, base, words = cached
         w = np.array([spec.weights[k] for k in mkeys], dtype=np.float64)
         keep = (np.ascontiguousarray(allow), np.ascontiguousarray(base), w)
         d = _lib.MixtureDesc()
@@ -284,9 +289,7 @@ class ChunkGenerator:
         self._batch = None
         if b is None or (self._served >= b.n_chunks and not b.exhausted):
             return
-        pos, off = self._batch_start_state
-        self._set_cursor_state(pos, off)
-        _lib.check(_lib.lib().mx_gen_set_next_chunk_id(self._h, self._batch_start_id))
+        _lib.check(_lib.lib().mx_gen_reset_to_mark(self._h))  # cursors + chunk id at the batch start
         if self._served > 0:
             self._plan(b.spec, self._served, b.arbitrary_size)
 
@@ -311,8 +314,7 @@ class ChunkGenerator:
         else:
             self._rewind()
             self._look_ahead = 1
-        self._batch_start_state = self._cursor_state()
-        self._batch_start_id = self._next_id
+        _lib.check(_lib.lib().mx_gen_mark(self._h))  # device-side snapshot for a later rewind
         n, exhausted, (mkeys, report) = self._plan(spec, self._look_ahead, arbitrary_size)
         batch = self._result(spec, mkeys, arbitrary_size)
         batch.exhausted, batch.report = exhausted, report

@@ -316,6 +316,28 @@ int mx_gen_result_copy(const mx_gen* gen, int64_t* chunk_offsets, int64_t* chunk
   const long long C = g.res_chunks, R = g.res_ranges;
   cudaStream_t s = g.stream;
   cudaError_t e = cudaSuccess;
+  if (g.h_small_valid == C && C > 0 && g.h_small) {  // small plan: served from the pinned mirror
+    const unsigned char* b = g.h_small + 32;
+    const long long cap = g.h_small_cap, slots = g.h_small_slots;
+    if (chunk_offsets) memcpy(chunk_offsets, b, sizeof(long long) * (C + 1));
+    b += sizeof(long long) * (cap + 1);
+    if (seeds) memcpy(seeds, b, sizeof(u64) * C);
+    b += sizeof(u64) * cap;
+    if (chunk_ids) memcpy(chunk_ids, b, sizeof(long long) * C);
+    b += sizeof(long long) * cap;
+    const u32* hm = reinterpret_cast<const u32*>(b);
+    const u32* hf = hm + slots;
+    const u32* hs = hf + slots;
+    const u32* he = hs + slots;
+    if (mkey) memcpy(mkey, hm, sizeof(u32) * R);
+    if (start) memcpy(start, hs, sizeof(u32) * R);
+    if (end) memcpy(end, he, sizeof(u32) * R);
+    for (long long i = 0; i < R; ++i) {
+      if (ds) ds[i] = g.ix->h_file_ds[hf[i]];
+      if (file_id) file_id[i] = g.ix->h_file_ids[hf[i]];
+    }
+    return MX_OK;
+  }
   if (chunk_offsets) e = cudaMemcpyAsync(chunk_offsets, g.res_off.p, sizeof(long long) * (C + 1), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && chunk_ids && C)
     e = cudaMemcpyAsync(chunk_ids, g.res_id.p, sizeof(long long) * C, cudaMemcpyDeviceToHost, s);
@@ -355,6 +377,31 @@ int mx_gen_result_device(const mx_gen* gen, const int64_t** chunk_offsets, const
 int mx_gen_report(const mx_gen* gen, int64_t* remaining) {
   MX_CHECK_ARG(gen && remaining, "null argument");
   for (size_t i = 0; i < gen->d.report.size(); ++i) remaining[i] = gen->d.report[i];
+  return MX_OK;
+}
+
+int mx_gen_mark(mx_gen* gen) {
+  MX_CHECK_ARG(gen, "null generator");
+  GenData& g = gen->d;
+  const long long K = g.K > 0 ? g.K : 1;
+  if (g.mark_consumed.n != K) {
+    cudaError_t e = g.mark_consumed.alloc(K, g.stream);
+    if (e != cudaSuccess) return mx_fail_cuda(e, "mark", __FILE__, __LINE__);
+  }
+  cudaError_t e = cudaMemcpyAsync(g.mark_consumed.p, g.consumed.p, sizeof(u64) * K, cudaMemcpyDeviceToDevice, g.stream);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "mark", __FILE__, __LINE__);
+  g.mark_next_id = g.next_chunk_id;
+  return MX_OK;
+}
+
+int mx_gen_reset_to_mark(mx_gen* gen) {
+  MX_CHECK_ARG(gen, "null generator");
+  GenData& g = gen->d;
+  if (!g.mark_consumed.p) return mx_fail(MX_ERR_INVALID, "no mark set");
+  cudaError_t e = cudaMemcpyAsync(g.consumed.p, g.mark_consumed.p, sizeof(u64) * g.mark_consumed.n,
+                                  cudaMemcpyDeviceToDevice, g.stream);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "reset", __FILE__, __LINE__);
+  g.next_chunk_id = g.mark_next_id;
   return MX_OK;
 }
 

@@ -42,6 +42,10 @@ struct DevBuf {
     if (count <= 0) return cudaSuccess;
     return cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (size_t)count, stream);
   }
+  cudaError_t reserve(long long count, cudaStream_t stream) {  // grow-only
+    if (p && n >= count) return cudaSuccess;
+    return alloc(count, stream);
+  }
   void release() {
     if (p) cudaFreeAsync(p, s);
     p = nullptr;
@@ -99,6 +103,36 @@ struct GenData {
   DevBuf<u32> res_mkey, res_file, res_start, res_end;
   std::vector<long long> report;
   int last_mkeys = 0;
+  // mark / reset of the cursor state (look-ahead rewinds without host copies)
+  DevBuf<u64> mark_consumed;
+  long long mark_next_id = 0;
+  // matching cache: the last mixture's allow bitsets -> per-key component lists
+  std::vector<u32> match_allow;
+  std::vector<int> match_base;
+  int match_words = 0;
+  bool match_shared = false;
+  std::vector<u32> match_off;  // host copy of L_off
+  DevBuf<u32> match_L_off, match_L;
+  // grow-only scratch for per-call planning (small plans allocate nothing)
+  DevBuf<unsigned char> ws[24];
+  template <typename T>
+  cudaError_t scratch(int slot, long long n, T** out) {
+    const long long bytes = (long long)sizeof(T) * (n > 0 ? n : 1);
+    if (ws[slot].n < bytes) {
+      cudaError_t e = ws[slot].alloc(bytes + bytes / 2, stream);
+      if (e != cudaSuccess) return e;
+    }
+    *out = reinterpret_cast<T*>(ws[slot].p);
+    return cudaSuccess;
+  }
+  // pinned host mirror of a small plan's result (one D2H per call)
+  unsigned char* h_small = nullptr;
+  long long h_small_bytes = 0;
+  long long h_small_valid = 0;  // chunk count the mirror holds (0 = use device result)
+  long long h_small_cap = 0, h_small_slots = 0;  // layout of the mirror
+  ~GenData() {
+    if (h_small) cudaFreeHost(h_small);
+  }
 };
 
 int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out);

@@ -546,16 +546,11 @@ __device__ __forceinline__ int phase_of_pair(const EmitArgs& a, u64 pair) {
   return (int)lo;
 }
 
-// Walk the stream range of one (chunk, term) pair. WRITE=false: count pieces.
-template <bool WRITE>
-__device__ u64 walk_pair(const EmitArgs& a, u64 pair, long long* chunk_out, u32* pm, u32* pf, u32* ps, u32* pe,
-                         u64 out_base) {
-  const int p = phase_of_pair(a, pair);
-  const Phase ph = a.phases[p];
-  const u64 local = pair - a.pair_pre[p];
-  const long long kr = (long long)(local / (u64)ph.n_terms);
-  const Term tm = a.terms[ph.term_begin + (long long)(local % (u64)ph.n_terms)];
-  if (chunk_out) *chunk_out = ph.chunk_begin + kr;
+// Walk the stream range of term `tm` for the kr-th chunk of its phase: the
+// intervals (in cursor order) it cuts. WRITE=false: count pieces; WRITE=true:
+// sink(i, mixture key, file index, start, end) for the i-th piece.
+template <bool WRITE, typename Sink>
+__device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink sink) {
   const u32 s = tm.stream;
   const long long sb = a.s_off[s], se = a.s_off[s + 1];
   const u64* pre = a.seg_pre + s;  // stream s prefix lives at seg_pre[i + s]
@@ -571,7 +566,6 @@ __device__ u64 walk_pair(const EmitArgs& a, u64 pair, long long* chunk_out, u32*
     const u64 seg_start = pre[i], seg_end = pre[i + 1];
     const u64 lo_abs = a.seg_lo[i] + (x - seg_start);
     const u64 hi_abs = a.seg_lo[i] + ((y < seg_end ? y : seg_end) - seg_start);
-    // component c occupies civ/ccum range [ib, ie)
     const long long ib = a.blk_first[a.key_blk_first[c]];
     const long long ie = a.blk_first[a.key_blk_first[c + 1]];
     const u64 cb = a.ccum[ib];
@@ -586,17 +580,35 @@ __device__ u64 walk_pair(const EmitArgs& a, u64 pair, long long* chunk_out, u32*
         const u64 len = a.ccum[j + 1] - a.ccum[j];
         const u64 from = lo_abs > off ? lo_abs : off;
         const u64 to = hi_abs < off + len ? hi_abs : off + len;
-        const u64 o = out_base + n++;
-        pm[o] = a.arbitrary ? c : tm.m;
-        pf[o] = a.iv_file[iv];
-        ps[o] = a.iv_start[iv] + (u32)(from - off);
-        pe[o] = a.iv_start[iv] + (u32)(to - off);
+        sink(n++, a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
+             a.iv_start[iv] + (u32)(to - off));
       }
     }
     x = seg_end < y ? seg_end : y;
     ++i;
   }
   return n;
+}
+
+// Walk the stream range of one (chunk, term) pair. WRITE=false: count pieces.
+template <bool WRITE>
+__device__ u64 walk_pair(const EmitArgs& a, u64 pair, long long* chunk_out, u32* pm, u32* pf, u32* ps, u32* pe,
+                         u64 out_base) {
+  const int p = phase_of_pair(a, pair);
+  const Phase ph = a.phases[p];
+  const u64 local = pair - a.pair_pre[p];
+  const long long kr = (long long)(local / (u64)ph.n_terms);
+  const Term tm = a.terms[ph.term_begin + (long long)(local % (u64)ph.n_terms)];
+  if (chunk_out) *chunk_out = ph.chunk_begin + kr;
+  if (WRITE) {
+    return walk_term<true>(a, tm, kr, [&](u64 i, u32 m, u32 f, u32 s0, u32 e0) {
+      pm[out_base + i] = m;
+      pf[out_base + i] = f;
+      ps[out_base + i] = s0;
+      pe[out_base + i] = e0;
+    });
+  }
+  return walk_term<false>(a, tm, kr, [](u64, u32, u32, u32, u32) {});
 }
 
 __global__ void emit_count_kernel(EmitArgs a, u64 n_pairs, u64* pair_cnt) {
@@ -950,23 +962,140 @@ __global__ void pair_prefix_kernel(const Phase* ph, long long n, u64* pre) {
   pre[n] = run;
 }
 
+// ------------------------------------------------------------------ small plans
+// A plan of a few chunks (ADO: one chunk per call) is emitted by two kernels
+// and one host sync: one CTA per chunk cuts all its terms into shared memory,
+// sorts + merges there and writes into a per-chunk slot; a finalising CTA
+// turns the slots into the CSR and derives the chunk seeds. Counts stay on
+// the device (plan_out), so nothing waits on the host in between.
+constexpr int SMALL_MAX_CHUNKS = 16;
+
+__global__ void __launch_bounds__(NM_THREADS)
+emit_small_kernel(EmitArgs a, const long long* plan_out, u32* gm, u32* gf, u32* gs, u32* ge, u64* cnt,
+                  u32* overflow) {
+  __shared__ uint4 s[NM_CAP];
+  __shared__ u32 s_flags[NM_CAP];
+  __shared__ u32 s_w[NM_THREADS / 32];
+  __shared__ u32 s_tot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long k = blockIdx.x;
+  if (k >= plan_out[0]) {
+    if (tid == 0) cnt[k] = 0;
+    return;
+  }
+  long long lo = 0, hi = plan_out[1];
+  while (lo < hi) {  // last phase with chunk_begin <= k
+    const long long mid = (lo + hi) >> 1;
+    if (a.phases[mid].chunk_begin <= k) lo = mid + 1; else hi = mid;
+  }
+  const Phase ph = a.phases[lo - 1];
+  const long long kr = k - ph.chunk_begin;
+  u32 run = 0;
+  for (long long tb = 0; tb < ph.n_terms; tb += NM_THREADS) {
+    const long long t = tb + tid;
+    Term tm{};
+    u32 c = 0;
+    if (t < ph.n_terms) {
+      tm = a.terms[ph.term_begin + t];
+      c = (u32)walk_term<false>(a, tm, kr, [](u64, u32, u32, u32, u32) {});
+    }
+    const u32 inc = warp_incl_scan(c);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const u32 x = lane < NM_THREADS / 32 ? s_w[lane] : 0;
+      const u32 xi = warp_incl_scan(x);
+      if (lane < NM_THREADS / 32) s_w[lane] = xi - x;
+      if (lane == 31) s_tot = xi;
+    }
+    __syncthreads();
+    const u32 base = run + s_w[warp] + inc - c, tot = s_tot;
+    if (run + tot > NM_CAP) {
+      if (tid == 0) atomicMax(overflow, run + tot);
+      return;
+    }
+    if (c)
+      walk_term<true>(a, tm, kr, [&](u64 i, u32 m, u32 f, u32 s0, u32 e0) { s[base + i] = make_uint4(m, f, s0, e0); });
+    run += tot;
+    __syncthreads();
+  }
+  const u32 m = run ? sort_merge(s, run, tid, NM_THREADS, s_flags) : 0;
+  const long long o = k * NM_CAP;
+  for (u32 i = tid; i < m; i += NM_THREADS) {
+    gm[o + i] = s[i].x;
+    gf[o + i] = s[i].y;
+    gs[o + i] = s[i].z;
+    ge[o + i] = s[i].w;
+  }
+  if (tid == 0) cnt[k] = m;
+}
+
+__global__ void __launch_bounds__(256)
+finalize_small_kernel(const long long* plan_out, const u64* cnt, const u32* gm, const u32* gf, const u32* gs,
+                      const u32* ge, u32* rm, u32* rf, u32* rs, u32* re, long long* res_off, u64* seeds, long long* ids,
+                      long long first_id, const uint8_t* prefix, int prefix_len, long long* header) {
+  __shared__ long long s_off[SMALL_MAX_CHUNKS + 1];
+  const long long n = plan_out[0];
+  if (threadIdx.x == 0) {
+    long long r = 0;
+    for (long long k = 0; k < n; ++k) {
+      s_off[k] = r;
+      r += (long long)cnt[k];
+    }
+    s_off[n] = r;
+    header[0] = n;
+    header[1] = r;
+    header[2] = plan_out[3];
+  }
+  __syncthreads();
+  for (long long k = 0; k <= n; k += 1)
+    if (threadIdx.x == 0) res_off[k] = s_off[k];
+  for (long long k = 0; k < n; ++k) {
+    const long long src = k * NM_CAP, dst = s_off[k], c = s_off[k + 1] - dst;
+    for (long long i = threadIdx.x; i < c; i += blockDim.x) {
+      rm[dst + i] = gm[src + i];
+      rf[dst + i] = gf[src + i];
+      rs[dst + i] = gs[src + i];
+      re[dst + i] = ge[src + i];
+    }
+  }
+  if (threadIdx.x < n) {  // derive_seed(job_seed, "chunk", id)  (chunks.py:188)
+    uint8_t dec[20];
+    const long long id = first_id + threadIdx.x;
+    const int dl = u64_to_dec((u64)id, dec);
+    Blake2b b;
+    b.init();
+    b.bytes(prefix, prefix_len);
+    b.len8((u64)dl);
+    b.bytes(dec, dl);
+    seeds[threadIdx.x] = b.seed63();
+    ids[threadIdx.x] = id;
+  }
+}
+
 // ------------------------------------------------------------------ host
-struct PlanWork {
+struct PlanWork {  // stream segment tables (generator scratch slots)
   int mode = 0;
   int n_streams = 0;
-  DevBuf<u32> s_off, seg_comp;
-  DevBuf<u64> seg_lo, seg_pre;
+  u32* s_off = nullptr;
+  u32* seg_comp = nullptr;
+  u64* seg_lo = nullptr;
+  u64* seg_pre = nullptr;
 };
 
-static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, const DevBuf<Term>& terms,
+enum ScratchSlot { S_WTS, S_SOFF, S_SEGC, S_SEGLO, S_SEGPRE, S_PHASES, S_TERMS, S_LL, S_OUT, S_REPORT, S_FLAGS,
+                   S_POS, S_APIDX, S_APFRAC, S_FRONT, S_GM, S_GF, S_GS, S_GE, S_OVF, S_CNT, S_HDR };
+
+static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Term* terms,
                 long long n_chunks, long long n_phases, cudaStream_t s) {
   IndexData* ix = g->ix;
   MxPhase ph("emit", s);
+  g->h_small_valid = 0;
   g->res_chunks = n_chunks;
   g->res_ranges = 0;
-  MX_CUDA_TRY(g->res_off.alloc(n_chunks + 1, s));
-  MX_CUDA_TRY(g->res_seed.alloc(n_chunks > 0 ? n_chunks : 1, s));
-  MX_CUDA_TRY(g->res_id.alloc(n_chunks > 0 ? n_chunks : 1, s));
+  MX_CUDA_TRY(g->res_off.reserve(n_chunks + 1, s));
+  MX_CUDA_TRY(g->res_seed.reserve(n_chunks > 0 ? n_chunks : 1, s));
+  MX_CUDA_TRY(g->res_id.reserve(n_chunks > 0 ? n_chunks : 1, s));
   if (n_chunks == 0) {
     const long long z = 0;
     MX_CUDA_TRY(cudaMemcpyAsync(g->res_off.p, &z, sizeof(z), cudaMemcpyHostToDevice, s));
@@ -975,20 +1104,20 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
   }
   DevBuf<u64> pair_pre;
   MX_CUDA_TRY(pair_pre.alloc(n_phases + 1, s));
-  pair_prefix_kernel<<<1, 32, 0, s>>>(phases.p, n_phases, pair_pre.p);
+  pair_prefix_kernel<<<1, 32, 0, s>>>(phases, n_phases, pair_pre.p);
   mx_count_launch();
   u64 n_pairs = 0;
   MX_CUDA_TRY(cudaMemcpyAsync(&n_pairs, pair_pre.p + n_phases, sizeof(u64), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
   EmitArgs a{};
-  a.phases = phases.p;
+  a.phases = phases;
   a.n_phases = n_phases;
-  a.terms = terms.p;
+  a.terms = terms;
   a.pair_pre = pair_pre.p;
-  a.s_off = w.s_off.p;
-  a.seg_comp = w.seg_comp.p;
-  a.seg_lo = w.seg_lo.p;
-  a.seg_pre = w.seg_pre.p;
+  a.s_off = w.s_off;
+  a.seg_comp = w.seg_comp;
+  a.seg_lo = w.seg_lo;
+  a.seg_pre = w.seg_pre;
   a.arbitrary = w.mode == 2;
   a.key_blk_first = ix->key_blk_first.p;
   a.blk_first = ix->blk_first.p;
@@ -1047,10 +1176,10 @@ static int emit(GenData* g, const PlanWork& w, const DevBuf<Phase>& phases, cons
   if (h_big) return mx_fail(MX_ERR_UNSUPPORTED, "a chunk has %u ranges before merging (> %d supported)", h_big, NM_CAP);
   g->res_ranges = total;
   const long long rc = total > 0 ? total : 1;
-  MX_CUDA_TRY(g->res_mkey.alloc(rc, s));
-  MX_CUDA_TRY(g->res_file.alloc(rc, s));
-  MX_CUDA_TRY(g->res_start.alloc(rc, s));
-  MX_CUDA_TRY(g->res_end.alloc(rc, s));
+  MX_CUDA_TRY(g->res_mkey.reserve(rc, s));
+  MX_CUDA_TRY(g->res_file.reserve(rc, s));
+  MX_CUDA_TRY(g->res_start.reserve(rc, s));
+  MX_CUDA_TRY(g->res_end.reserve(rc, s));
   {
     const long long grid = std::min<long long>((n_chunks + 7) / 8, 148 * 16);
     compact_warp_kernel<<<(unsigned)grid, 256, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
@@ -1092,62 +1221,78 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     ma.allow_base[p] = mix->allow_base[p];
   }
   ma.allow_words = mix->allow_words;
-  DevBuf<u32> allow, L_cnt, hits;
-  DevBuf<double> wts;
-  MX_CUDA_TRY(allow.alloc((long long)Km * mix->allow_words, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(allow.p, mix->allow, sizeof(u32) * Km * mix->allow_words, cudaMemcpyHostToDevice, s));
-  ma.allow = allow.p;
-  MX_CUDA_TRY(wts.alloc(Km, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(wts.p, mix->weights, sizeof(double) * Km, cudaMemcpyHostToDevice, s));
-  MX_CUDA_TRY(L_cnt.alloc(Km, s));
-  MX_CUDA_TRY(hits.alloc(K > 0 ? K : 1, s));
-  MX_CUDA_TRY(cudaMemsetAsync(hits.p, 0, sizeof(u32) * (K > 0 ? K : 1), s));
-  if (K > 0) {
-    match_count_kernel<<<Km, 256, 0, s>>>(ma, L_cnt.p, hits.p);
-    mx_count_launch();
+  double* wts_p = nullptr;
+  MX_CUDA_TRY(g->scratch(S_WTS, Km, &wts_p));
+  MX_CUDA_TRY(cudaMemcpyAsync(wts_p, mix->weights, sizeof(double) * Km, cudaMemcpyHostToDevice, s));
+  // matching depends only on the mixture KEYS (not the weights): reuse the
+  // previous plan's per-key component lists when the keys are unchanged
+  // (ADO re-plans every chunk with new weights over the same domains)
+  const size_t n_allow = (size_t)Km * mix->allow_words;
+  const bool cached = g->match_words == mix->allow_words && g->match_allow.size() == n_allow &&
+                      (int)g->match_base.size() == ix->n_props &&
+                      std::equal(g->match_base.begin(), g->match_base.end(), mix->allow_base) &&
+                      std::equal(g->match_allow.begin(), g->match_allow.end(), mix->allow);
+  if (!cached) {
+    DevBuf<u32> allow, L_cnt, hits;
+    MX_CUDA_TRY(allow.alloc((long long)n_allow, s));
+    MX_CUDA_TRY(cudaMemcpyAsync(allow.p, mix->allow, sizeof(u32) * n_allow, cudaMemcpyHostToDevice, s));
+    ma.allow = allow.p;
+    MX_CUDA_TRY(L_cnt.alloc(Km, s));
+    MX_CUDA_TRY(hits.alloc(K > 0 ? K : 1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(hits.p, 0, sizeof(u32) * (K > 0 ? K : 1), s));
+    if (K > 0) {
+      match_count_kernel<<<Km, 256, 0, s>>>(ma, L_cnt.p, hits.p);
+      mx_count_launch();
+    }
+    std::vector<u32> h_cnt(Km), h_hits(K > 0 ? K : 1, 0);
+    MX_CUDA_TRY(cudaMemcpyAsync(h_cnt.data(), L_cnt.p, sizeof(u32) * Km, cudaMemcpyDeviceToHost, s));
+    if (K > 0) MX_CUDA_TRY(cudaMemcpyAsync(h_hits.data(), hits.p, sizeof(u32) * K, cudaMemcpyDeviceToHost, s));
+    MX_CUDA_TRY(cudaStreamSynchronize(s));
+    g->match_off.assign(Km + 1, 0);
+    for (int m = 0; m < Km; ++m) g->match_off[m + 1] = g->match_off[m] + h_cnt[m];
+    g->match_shared = false;
+    for (long long c = 0; c < K; ++c) g->match_shared |= h_hits[c] > 1;
+    MX_CUDA_TRY(g->match_L_off.alloc(Km + 1, s));
+    MX_CUDA_TRY(cudaMemcpyAsync(g->match_L_off.p, g->match_off.data(), sizeof(u32) * (Km + 1), cudaMemcpyHostToDevice,
+                                s));
+    MX_CUDA_TRY(g->match_L.alloc(g->match_off[Km] > 0 ? g->match_off[Km] : 1, s));
+    if (K > 0) {
+      match_fill_kernel<<<Km, 256, 0, s>>>(ma, g->match_L_off.p, g->match_L.p);
+      mx_count_launch();
+    }
+    g->match_allow.assign(mix->allow, mix->allow + n_allow);
+    g->match_base.assign(mix->allow_base, mix->allow_base + ix->n_props);
+    g->match_words = mix->allow_words;
   }
-  std::vector<u32> h_cnt(Km), h_hits(K > 0 ? K : 1, 0);
-  MX_CUDA_TRY(cudaMemcpyAsync(h_cnt.data(), L_cnt.p, sizeof(u32) * Km, cudaMemcpyDeviceToHost, s));
-  if (K > 0) MX_CUDA_TRY(cudaMemcpyAsync(h_hits.data(), hits.p, sizeof(u32) * K, cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
-  std::vector<u32> h_off(Km + 1, 0);
-  for (int m = 0; m < Km; ++m) h_off[m + 1] = h_off[m] + h_cnt[m];
-  bool shared = false;
-  for (long long c = 0; c < K; ++c) shared |= h_hits[c] > 1;
-  DevBuf<u32> L_off, L;
-  MX_CUDA_TRY(L_off.alloc(Km + 1, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(L_off.p, h_off.data(), sizeof(u32) * (Km + 1), cudaMemcpyHostToDevice, s));
-  MX_CUDA_TRY(L.alloc(h_off[Km] > 0 ? h_off[Km] : 1, s));
-  if (K > 0) {
-    match_fill_kernel<<<Km, 256, 0, s>>>(ma, L_off.p, L.p);
-    mx_count_launch();
-  }
+  const std::vector<u32>& h_off = g->match_off;
+  const bool shared = g->match_shared;
+  const DevBuf<u32>& L_off = g->match_L_off;
+  const DevBuf<u32>& L = g->match_L;
   // ---- streams
   PlanWork w;
   w.mode = shared ? 1 : 0;
   if (w.mode == 0) {
     w.n_streams = Km;
-    MX_CUDA_TRY(w.s_off.alloc(Km + 1, s));
-    MX_CUDA_TRY(cudaMemcpyAsync(w.s_off.p, L_off.p, sizeof(u32) * (Km + 1), cudaMemcpyDeviceToDevice, s));
+    w.s_off = L_off.p;
     const long long nseg = h_off[Km];
-    MX_CUDA_TRY(w.seg_comp.alloc(nseg > 0 ? nseg : 1, s));
-    MX_CUDA_TRY(w.seg_lo.alloc(nseg > 0 ? nseg : 1, s));
-    MX_CUDA_TRY(w.seg_pre.alloc(nseg + Km, s));
-    build_segments_kernel<<<(Km + 3) / 4, 128, 0, s>>>(0, Km, w.s_off.p, L.p, g->comp_total.p, g->consumed.p,
-                                                          w.seg_comp.p, w.seg_lo.p, w.seg_pre.p);
+    MX_CUDA_TRY(g->scratch(S_SEGC, nseg, &w.seg_comp));
+    MX_CUDA_TRY(g->scratch(S_SEGLO, nseg, &w.seg_lo));
+    MX_CUDA_TRY(g->scratch(S_SEGPRE, nseg + Km, &w.seg_pre));
+    build_segments_kernel<<<(Km + 3) / 4, 128, 0, s>>>(0, Km, w.s_off, L.p, g->comp_total.p, g->consumed.p,
+                                                          w.seg_comp, w.seg_lo, w.seg_pre);
     mx_count_launch();
   } else {
     w.n_streams = (int)K;
     std::vector<u32> so(K + 1);
     for (long long c = 0; c <= K; ++c) so[c] = (u32)c;
-    MX_CUDA_TRY(w.s_off.alloc(K + 1, s));
-    MX_CUDA_TRY(cudaMemcpyAsync(w.s_off.p, so.data(), sizeof(u32) * (K + 1), cudaMemcpyHostToDevice, s));
-    MX_CUDA_TRY(w.seg_comp.alloc(K, s));
-    MX_CUDA_TRY(w.seg_lo.alloc(K, s));
-    MX_CUDA_TRY(w.seg_pre.alloc(2 * K, s));
-    build_segments_kernel<<<(unsigned)std::min<long long>((K + 3) / 4, 148 * 16), 128, 0, s>>>(1, (int)K, w.s_off.p, nullptr, g->comp_total.p,
-                                                                      g->consumed.p, w.seg_comp.p, w.seg_lo.p,
-                                                                      w.seg_pre.p);
+    MX_CUDA_TRY(g->scratch(S_SOFF, K + 1, &w.s_off));
+    MX_CUDA_TRY(cudaMemcpyAsync(w.s_off, so.data(), sizeof(u32) * (K + 1), cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(g->scratch(S_SEGC, K, &w.seg_comp));
+    MX_CUDA_TRY(g->scratch(S_SEGLO, K, &w.seg_lo));
+    MX_CUDA_TRY(g->scratch(S_SEGPRE, 2 * K, &w.seg_pre));
+    build_segments_kernel<<<(unsigned)std::min<long long>((K + 3) / 4, 148 * 16), 128, 0, s>>>(1, (int)K, w.s_off, nullptr, g->comp_total.p,
+                                                                      g->consumed.p, w.seg_comp, w.seg_lo,
+                                                                      w.seg_pre);
     mx_count_launch();
     MX_CUDA_TRY(cudaStreamSynchronize(s));
   }
@@ -1163,24 +1308,24 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     const long long term_budget = 1ll << 24;  // 512 MB of terms; the plan resumes on the next call
     if (cap_terms > term_budget) cap_terms = term_budget > Km ? term_budget : Km;
   }
-  DevBuf<Phase> phases;
-  DevBuf<Term> terms;
-  DevBuf<long long> scratch_ll, out, report;
-  DevBuf<unsigned char> flags;
-  DevBuf<u64> pos;
-  DevBuf<int> ap_idx;
-  DevBuf<double> ap_frac;
-  DevBuf<u32> front;
-  MX_CUDA_TRY(phases.alloc(cap_phases, s));
-  MX_CUDA_TRY(terms.alloc(cap_terms, s));
-  MX_CUDA_TRY(scratch_ll.alloc(5LL * Km, s));
-  MX_CUDA_TRY(out.alloc(4, s));
-  MX_CUDA_TRY(report.alloc(Km, s));
-  MX_CUDA_TRY(flags.alloc(2LL * Km, s));
-  MX_CUDA_TRY(pos.alloc(Km, s));
-  MX_CUDA_TRY(ap_idx.alloc(Km, s));
-  MX_CUDA_TRY(ap_frac.alloc(Km, s));
-  MX_CUDA_TRY(front.alloc(Km, s));
+  struct { Phase* p; } phases;
+  struct { Term* p; } terms;
+  struct { long long* p; } scratch_ll, out, report;
+  struct { unsigned char* p; } flags;
+  struct { u64* p; } pos;
+  struct { int* p; } ap_idx;
+  struct { double* p; } ap_frac;
+  struct { u32* p; } front;
+  MX_CUDA_TRY(g->scratch(S_PHASES, cap_phases, &phases.p));
+  MX_CUDA_TRY(g->scratch(S_TERMS, cap_terms, &terms.p));
+  MX_CUDA_TRY(g->scratch(S_LL, 5LL * Km, &scratch_ll.p));
+  MX_CUDA_TRY(g->scratch(S_OUT, 4, &out.p));
+  MX_CUDA_TRY(g->scratch(S_REPORT, Km, &report.p));
+  MX_CUDA_TRY(g->scratch(S_FLAGS, 2LL * Km, &flags.p));
+  MX_CUDA_TRY(g->scratch(S_POS, Km, &pos.p));
+  MX_CUDA_TRY(g->scratch(S_APIDX, Km, &ap_idx.p));
+  MX_CUDA_TRY(g->scratch(S_APFRAC, Km, &ap_frac.p));
+  MX_CUDA_TRY(g->scratch(S_FRONT, Km, &front.p));
   MX_CUDA_TRY(cudaMemsetAsync(front.p, 0, sizeof(u32) * Km, s));
   MX_CUDA_TRY(cudaMemsetAsync(report.p, 0, sizeof(long long) * Km, s));
   PlanArgs pa{};
@@ -1189,9 +1334,9 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   pa.C = mix->chunk_size;
   pa.strict = mix->strict;
   pa.max_chunks = max_chunks;
-  pa.w = wts.p;
-  pa.seg_pre = w.seg_pre.p;
-  pa.s_off = w.s_off.p;
+  pa.w = wts_p;
+  pa.seg_pre = w.seg_pre;
+  pa.s_off = w.s_off;
   pa.L_off = L_off.p;
   pa.L = L.p;
   pa.comp_total = g->comp_total.p;
@@ -1215,17 +1360,106 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   pa.report = report.p;
   plan_kernel<<<1, 32, 0, s>>>(pa);
   mx_count_launch();
+  if (max_chunks <= SMALL_MAX_CHUNKS && mix->chunk_size <= NM_CAP) {
+    // small plan: emission driven by device-side counts, one host sync
+    if (w.mode == 0) {
+      commit_segments_kernel<<<Km, 128, 0, s>>>(Km, w.s_off, w.seg_comp, w.seg_lo, w.seg_pre, pos.p,
+                                                g->consumed.p);
+      mx_count_launch();
+    }
+    EmitArgs a{};
+    a.phases = phases.p;
+    a.terms = terms.p;
+    a.s_off = w.s_off;
+    a.seg_comp = w.seg_comp;
+    a.seg_lo = w.seg_lo;
+    a.seg_pre = w.seg_pre;
+    a.arbitrary = 0;
+    a.key_blk_first = ix->key_blk_first.p;
+    a.blk_first = ix->blk_first.p;
+    a.civ = g->civ.p;
+    a.ccum = g->ccum.p;
+    a.iv_start = ix->iv_start.p;
+    a.iv_end = ix->iv_end.p;
+    a.iv_file = ix->iv_file.p;
+    const long long slots = max_chunks * NM_CAP;
+    struct { u32* p; } gm, gf, gs, ge, ovf;
+    struct { u64* p; } cnt;
+    struct { long long* p; } header;
+    MX_CUDA_TRY(g->scratch(S_GM, slots, &gm.p));
+    MX_CUDA_TRY(g->scratch(S_GF, slots, &gf.p));
+    MX_CUDA_TRY(g->scratch(S_GS, slots, &gs.p));
+    MX_CUDA_TRY(g->scratch(S_GE, slots, &ge.p));
+    MX_CUDA_TRY(g->scratch(S_OVF, 1, &ovf.p));
+    MX_CUDA_TRY(g->scratch(S_CNT, max_chunks, &cnt.p));
+    MX_CUDA_TRY(g->scratch(S_HDR, 3, &header.p));
+    MX_CUDA_TRY(cudaMemsetAsync(ovf.p, 0, sizeof(u32), s));
+    MX_CUDA_TRY(g->res_off.reserve(max_chunks + 1, s));
+    MX_CUDA_TRY(g->res_seed.reserve(max_chunks, s));
+    MX_CUDA_TRY(g->res_id.reserve(max_chunks, s));
+    MX_CUDA_TRY(g->res_mkey.reserve(slots, s));
+    MX_CUDA_TRY(g->res_file.reserve(slots, s));
+    MX_CUDA_TRY(g->res_start.reserve(slots, s));
+    MX_CUDA_TRY(g->res_end.reserve(slots, s));
+    {
+      MxPhase ph("emit", s);
+      emit_small_kernel<<<(unsigned)max_chunks, NM_THREADS, 0, s>>>(a, out.p, gm.p, gf.p, gs.p, ge.p, cnt.p, ovf.p);
+      mx_count_launch();
+      finalize_small_kernel<<<1, 256, 0, s>>>(out.p, cnt.p, gm.p, gf.p, gs.p, ge.p, g->res_mkey.p, g->res_file.p,
+                                              g->res_start.p, g->res_end.p, g->res_off.p, g->res_seed.p, g->res_id.p,
+                                              g->next_chunk_id, g->chunk_prefix.p, g->chunk_prefix_len, header.p);
+      mx_count_launch();
+    }
+    // one pinned host mirror of the whole result, copied in the same sync
+    const long long mirror = 8 * (3 + 1) + (long long)(max_chunks + 1) * 8 + (long long)max_chunks * 16 +
+                             slots * 16 + Km * 8;
+    if (g->h_small_bytes < mirror) {
+      if (g->h_small) cudaFreeHost(g->h_small);
+      g->h_small = nullptr;
+      MX_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&g->h_small), mirror));
+      g->h_small_bytes = mirror;
+    }
+    unsigned char* hp = g->h_small;
+    long long* hdr = reinterpret_cast<long long*>(hp);
+    u32* h_ovf_p = reinterpret_cast<u32*>(hp + 24);
+    unsigned char* body = hp + 32;
+    MX_CUDA_TRY(cudaMemcpyAsync(hdr, header.p, 3 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    MX_CUDA_TRY(cudaMemcpyAsync(h_ovf_p, ovf.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    MX_CUDA_TRY(cudaMemcpyAsync(body, g->res_off.p, sizeof(long long) * (max_chunks + 1), cudaMemcpyDeviceToHost, s));
+    body += sizeof(long long) * (max_chunks + 1);
+    MX_CUDA_TRY(cudaMemcpyAsync(body, g->res_seed.p, sizeof(u64) * max_chunks, cudaMemcpyDeviceToHost, s));
+    body += sizeof(u64) * max_chunks;
+    MX_CUDA_TRY(cudaMemcpyAsync(body, g->res_id.p, sizeof(long long) * max_chunks, cudaMemcpyDeviceToHost, s));
+    body += sizeof(long long) * max_chunks;
+    for (u32* src : {g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p}) {
+      MX_CUDA_TRY(cudaMemcpyAsync(body, src, sizeof(u32) * slots, cudaMemcpyDeviceToHost, s));
+      body += sizeof(u32) * slots;
+    }
+    MX_CUDA_TRY(cudaMemcpyAsync(g->report.data(), report.p, sizeof(long long) * Km, cudaMemcpyDeviceToHost, s));
+    MX_CUDA_TRY(cudaStreamSynchronize(s));
+    const u32 h_ovf = *h_ovf_p;
+    g->h_small_valid = hdr[0];
+    g->h_small_cap = max_chunks;
+    g->h_small_slots = slots;
+    MX_CUDA_TRY(cudaGetLastError());
+    if (h_ovf) return mx_fail(MX_ERR_UNSUPPORTED, "a chunk has %u ranges before merging (> %d supported)", h_ovf, NM_CAP);
+    g->res_chunks = hdr[0];
+    g->res_ranges = hdr[1];
+    g->next_chunk_id += hdr[0];
+    *n_out = hdr[0];
+    return hdr[2] ? MX_EXHAUSTED : MX_OK;
+  }
   long long h_out[4];
   MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaMemcpyAsync(g->report.data(), report.p, sizeof(long long) * Km, cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
   ph_plan.reset();
   if (w.mode == 0) {
-    commit_segments_kernel<<<Km, 128, 0, s>>>(Km, w.s_off.p, w.seg_comp.p, w.seg_lo.p, w.seg_pre.p, pos.p,
+    commit_segments_kernel<<<Km, 128, 0, s>>>(Km, w.s_off, w.seg_comp, w.seg_lo, w.seg_pre, pos.p,
                                               g->consumed.p);
     mx_count_launch();
   }
-  int rc = emit(g, w, phases, terms, h_out[0], h_out[1], s);
+  int rc = emit(g, w, phases.p, terms.p, h_out[0], h_out[1], s);
   if (rc != MX_OK) return rc;
   *n_out = h_out[0];
   return h_out[3] ? MX_EXHAUSTED : MX_OK;
@@ -1242,17 +1476,17 @@ int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long 
   w.mode = 2;
   w.n_streams = 1;
   if (K == 0) {
-    int rc = emit(g, w, DevBuf<Phase>(), DevBuf<Term>(), 0, 0, s);
+    int rc = emit(g, w, nullptr, nullptr, 0, 0, s);
     return rc != MX_OK ? rc : MX_EXHAUSTED;
   }
   std::vector<u32> so = {0u, (u32)K};
-  MX_CUDA_TRY(w.s_off.alloc(2, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(w.s_off.p, so.data(), sizeof(u32) * 2, cudaMemcpyHostToDevice, s));
-  MX_CUDA_TRY(w.seg_comp.alloc(K, s));
-  MX_CUDA_TRY(w.seg_lo.alloc(K, s));
-  MX_CUDA_TRY(w.seg_pre.alloc(K + 1, s));
-  build_segments_kernel<<<1, 32, 0, s>>>(2, 1, w.s_off.p, g->comp_order.p, g->comp_total.p, g->consumed.p,
-                                         w.seg_comp.p, w.seg_lo.p, w.seg_pre.p);
+  MX_CUDA_TRY(g->scratch(S_SOFF, 2, &w.s_off));
+  MX_CUDA_TRY(cudaMemcpyAsync(w.s_off, so.data(), sizeof(u32) * 2, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(g->scratch(S_SEGC, K, &w.seg_comp));
+  MX_CUDA_TRY(g->scratch(S_SEGLO, K, &w.seg_lo));
+  MX_CUDA_TRY(g->scratch(S_SEGPRE, K + 1, &w.seg_pre));
+  build_segments_kernel<<<1, 32, 0, s>>>(2, 1, w.s_off, g->comp_order.p, g->comp_total.p, g->consumed.p,
+                                         w.seg_comp, w.seg_lo, w.seg_pre);
   mx_count_launch();
   DevBuf<Phase> phases;
   DevBuf<Term> terms;
@@ -1262,14 +1496,14 @@ int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long 
   MX_CUDA_TRY(terms.alloc(2, s));
   MX_CUDA_TRY(out.alloc(4, s));
   MX_CUDA_TRY(pos.alloc(1, s));
-  plan_arbitrary_kernel<<<1, 32, 0, s>>>(w.seg_pre.p, K, chunk_size, max_chunks, phases.p, terms.p, out.p, pos.p);
+  plan_arbitrary_kernel<<<1, 32, 0, s>>>(w.seg_pre, K, chunk_size, max_chunks, phases.p, terms.p, out.p, pos.p);
   mx_count_launch();
   long long h_out[4];
   MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
-  commit_segments_kernel<<<1, 128, 0, s>>>(1, w.s_off.p, w.seg_comp.p, w.seg_lo.p, w.seg_pre.p, pos.p, g->consumed.p);
+  commit_segments_kernel<<<1, 128, 0, s>>>(1, w.s_off, w.seg_comp, w.seg_lo, w.seg_pre, pos.p, g->consumed.p);
   mx_count_launch();
-  int rc = emit(g, w, phases, terms, h_out[0], h_out[1], s);
+  int rc = emit(g, w, phases.p, terms.p, h_out[0], h_out[1], s);
   if (rc != MX_OK) return rc;
   *n_out = h_out[0];
   return h_out[3] ? MX_EXHAUSTED : MX_OK;

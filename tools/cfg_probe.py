@@ -88,6 +88,36 @@ def cfg4(steps: int):
     print(f"cfg4: {steps} steps, generate {np.median(t_chunk) * 1e6:.0f} us/chunk (median), "
           f"feedback {np.median(t_fb) * 1e6:.0f} us/step, refits at {src.state.fit_steps[:3]}..., "
           f"max feedback {max(t_fb) * 1e3:.1f} ms")
+    # breakdown of one step
+    import ctypes as C
+
+    from paper_2502_19790_b200 import MixtureSpec, _lib
+
+    parts = {k: [] for k in ("compute_pi", "spec", "plan", "to_host", "chunk", "feedback")}
+    for step in range(steps + 1, steps + 101):
+        t = time.perf_counter()
+        pi = src.state.compute_pi()
+        parts["compute_pi"].append(time.perf_counter() - t)
+        t = time.perf_counter()
+        spec = MixtureSpec(pi, 1024)
+        parts["spec"].append(time.perf_counter() - t)
+        t = time.perf_counter()
+        n, _, (mkeys, _) = gen._plan(spec, 1)
+        parts["plan"].append(time.perf_counter() - t)
+        t = time.perf_counter()
+        b = gen._result(spec, mkeys, None)
+        b.to_host()
+        parts["to_host"].append(time.perf_counter() - t)
+        t = time.perf_counter()
+        b.chunk(0)
+        parts["chunk"].append(time.perf_counter() - t)
+        gen._next_id += n
+        t = time.perf_counter()
+        sums, counts = domain_loss_device(losses, tags, D)
+        s, c = sums.cpu().numpy(), counts.cpu().numpy()
+        src.observe_feedback(step, {dom[i]: (float(s[i]), int(c[i])) for i in range(D)})
+        parts["feedback"].append(time.perf_counter() - t)
+    print("cfg4 breakdown (median us):", {k: round(np.median(v) * 1e6) for k, v in parts.items()})
 
 
 if __name__ == "__main__":
