@@ -475,6 +475,414 @@ __global__ void plan_kernel(PlanArgs a) {
   a.out[3] = exhausted;
 }
 
+// ---------------------------------------------------------------------------
+// Many mixture keys (disjoint streams), e.g. cfg 5: 10k keys, Zipf weights.
+// One 1024-thread CTA. The per-key pass loops run in parallel; the best-effort
+// redistribution loop (chunks.py:223-229) is sequential by nature and runs on
+// thread 0, but each step is O(r): for a small shortfall r the reference's
+// apportion (mixtures.py:158-184) gives one unit to each of the r alive keys
+// with the largest share = w / wsum * r, i.e. the first r alive keys in
+// (w desc, key asc) order -- exactly, whenever (1) every share + 1e-9 < 1 (all
+// floors 0, checked against a bound on wsum) and (2) the r-th and (r+1)-th
+// weights are equal or separated by more than the rounding of two flops.
+// Otherwise a cooperative exact apportion runs (CPython-compensated wsum,
+// floors, radix select of the leftover units by (frac desc, key asc)).
+constexpr int BIG_THREADS = 1024;
+constexpr int BIG_MAX_KM = 16384;
+
+struct BigArgs {
+  int Km;
+  long long C;
+  int strict;
+  long long max_chunks;
+  const double* w;       // [Km] key order
+  const u32* order_w;    // [Km] keys by (w desc, key asc)
+  const u32* rank_w;     // [Km] position of key in order_w
+  const u64* seg_pre;
+  const u32* s_off;
+  u64* pos;              // [Km] stream position (relative to the plan)
+  u64* slen;             // [Km] scratch: stream lengths
+  int* counts;           // [Km] scratch: apportion(w, C)
+  int* took;             // [Km] scratch
+  u32* list;             // [Km] scratch: newly dead keys
+  long long* base;       // [Km] scratch (exact apportion)
+  unsigned long long* fkey;  // [Km] scratch (exact apportion)
+  Phase* phases;
+  long long cap_phases;
+  Term* terms;
+  long long cap_terms;
+  long long* out;
+  long long* report;
+};
+
+struct BigShared {
+  double wsum, werr;  // alive weight sum (exact after big_apportion) and its error bound
+  long long acc;
+  int i_list, alive, slow_r, slow_d, status, flag, digit, need;
+  unsigned long long thr;
+  u32 hist[256];
+  u32 wpart[BIG_THREADS / 32];
+};
+
+__device__ __forceinline__ u32 big_find(u32* nxt, u32 p) {
+  u32 r = p;
+  while (nxt[r] != r) r = nxt[r];
+  while (nxt[p] != r) {
+    const u32 t = nxt[p];
+    nxt[p] = r;
+    p = t;
+  }
+  return r;
+}
+
+// block sum of a per-thread long long
+__device__ long long big_sum(long long v, BigShared& sh) {
+  __shared__ long long s_part[BIG_THREADS / 32];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) s_part[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int i = 0; i < BIG_THREADS / 32; ++i) t += s_part[i];
+    sh.acc = t;
+  }
+  __syncthreads();
+  return sh.acc;
+}
+
+// Exact apportion(w restricted to keys with !dead, total): target[m] += count.
+__device__ void big_apportion(const BigArgs& a, const unsigned char* dead, long long total, int* target,
+                              BigShared& sh) {
+  const int tid = threadIdx.x;
+  const int Km = a.Km;
+  if (tid == 0) {  // CPython 3.12 sum(): Neumaier, keys in key order
+    double s = 0.0, c = 0.0;
+    for (int m = 0; m < Km; ++m) {
+      if (dead && dead[m]) continue;
+      const double x = a.w[m];
+      const double t = s + x;
+      if (fabs(s) >= fabs(x)) c += (s - t) + x;
+      else c += (x - t) + s;
+      s = t;
+    }
+    sh.wsum = c != 0.0 ? s + c : s;
+  }
+  __syncthreads();
+  const double wsum = sh.wsum;
+  const double tot = (double)total;
+  long long assigned = 0;
+  for (int m = tid; m < Km; m += BIG_THREADS) {
+    if (dead && dead[m]) {
+      a.base[m] = 0;
+      a.fkey[m] = ~0ull;
+      continue;
+    }
+    const double share = a.w[m] / wsum * tot;
+    const long long b = (long long)(share + 1e-9);
+    double fr = share - (double)b;
+    fr = fr > 0.0 ? fr : 0.0;
+    a.base[m] = b;
+    a.fkey[m] = ~(unsigned long long)__double_as_longlong(fr);  // larger frac -> smaller key
+    assigned += b;
+  }
+  const long long left = total - big_sum(assigned, sh);
+  unsigned long long thr = 0;
+  int need = 0;
+  if (left > 0) {  // radix select: the left-th smallest (fkey, key) among alive keys
+    unsigned long long prefix = 0, mask = 0;
+    if (tid == 0) sh.need = (int)left;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int d = tid; d < 256; d += BIG_THREADS) sh.hist[d] = 0;
+      __syncthreads();
+      for (int m = tid; m < Km; m += BIG_THREADS) {
+        if (dead && dead[m]) continue;
+        const unsigned long long f = a.fkey[m];
+        if ((f & mask) == prefix) atomicAdd(&sh.hist[(f >> shift) & 255], 1u);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int nd = sh.need;
+        u32 cum = 0;
+        int dg = 255;
+        for (int d = 0; d < 256; ++d) {
+          if ((int)(cum + sh.hist[d]) >= nd) {
+            dg = d;
+            break;
+          }
+          cum += sh.hist[d];
+        }
+        sh.digit = dg;
+        sh.need = nd - (int)cum;
+      }
+      __syncthreads();
+      prefix |= (unsigned long long)sh.digit << shift;
+      mask |= 0xffull << shift;
+      __syncthreads();
+    }
+    thr = prefix;
+    need = sh.need;  // how many keys with fkey == thr (lowest key first) get a unit
+  }
+  // apply: base + 1 for fkey < thr, and the first `need` keys (in key order) with fkey == thr
+  int taken = 0;  // running count of equal keys before this round
+  for (int b0 = 0; b0 < Km; b0 += BIG_THREADS) {
+    const int m = b0 + tid;
+    bool eq = false;
+    long long add = 0;
+    if (m < Km && !(dead && dead[m])) {
+      add = a.base[m];
+      if (left > 0) {
+        const unsigned long long f = a.fkey[m];
+        if (f < thr) add += 1;
+        eq = f == thr;
+      }
+    }
+    // ordered rank among equal keys in this round
+    const u32 bal = __ballot_sync(MX_FULL, eq);
+    const int lane = tid & 31, warp = tid >> 5;
+    if (lane == 0) sh.wpart[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0;
+    for (int x = 0; x < warp; ++x) before += sh.wpart[x];
+    int total_eq = 0;
+    for (int x = 0; x < BIG_THREADS / 32; ++x) total_eq += sh.wpart[x];
+    const int rank = taken + before + __popc(bal & ((1u << lane) - 1));
+    if (eq && rank < need) add += 1;
+    if (m < Km && add) target[m] += (int)add;
+    taken += total_eq;
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a) {
+  extern __shared__ __align__(16) unsigned char big_smem[];
+  __shared__ BigShared sh;
+  __shared__ long long s_min[BIG_THREADS / 32];
+  const int Km = a.Km, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  int* rem = reinterpret_cast<int*>(big_smem);                   // [Km]
+  u32* nxt = reinterpret_cast<u32*>(big_smem + 4 * (size_t)Km);  // [Km+1] skip list over order_w
+  unsigned char* dead = big_smem + 8 * (size_t)Km + 4;           // [Km] 1 dead, 2 newly dead this pass
+  for (int m = tid; m < Km; m += BIG_THREADS) {
+    a.slen[m] = a.seg_pre[a.s_off[m + 1] + m];
+    a.counts[m] = 0;
+    a.pos[m] = 0;
+  }
+  __syncthreads();
+  big_apportion(a, nullptr, a.C, a.counts, sh);  // counts = apportion(weights, chunk_size)
+  const double wsum_all = sh.wsum;                // CPython sum over all keys
+  __syncthreads();
+  long long chunks = 0, n_ph = 0, n_terms = 0, exhausted = 0;
+  while (chunks < a.max_chunks && n_ph < a.cap_phases && a.cap_terms - n_terms >= Km) {
+    // ---------------- simulate one generate() at count level (chunks.py:214-231)
+    for (int m = tid; m < Km; m += BIG_THREADS) {
+      rem[m] = a.counts[m];
+      dead[m] = 0;
+      a.took[m] = 0;
+    }
+    for (int p = tid; p <= Km; p += BIG_THREADS) nxt[p] = (u32)p;
+    if (tid == 0) {
+      sh.wsum = wsum_all;
+      sh.werr = wsum_all * 1e-15;
+      sh.alive = Km;
+      sh.status = 0;  // 0 running, 2 None
+    }
+    __syncthreads();
+    while (true) {
+      // one pass over the keys with open counts
+      int any_rem = 0, any_new = 0;
+      for (int m = tid; m < Km; m += BIG_THREADS) {
+        int r = rem[m];
+        if (r <= 0) continue;
+        const long long avail = (long long)(a.slen[m] - a.pos[m]) - a.took[m];
+        const int g = r < avail ? r : (int)(avail > 0 ? avail : 0);
+        a.took[m] += g;
+        r -= g;
+        rem[m] = r;
+        any_rem |= r > 0;
+        if (g == 0) {  // found nothing with an open count
+          dead[m] = 2;
+          any_new = 1;
+        }
+      }
+      any_rem = __syncthreads_or(any_rem);
+      any_new = __syncthreads_or(any_new);
+      if (!any_new) {
+        if (!any_rem) break;  // chunk complete
+        continue;
+      }
+      if (a.strict) {
+        for (int m = tid; m < Km; m += BIG_THREADS) a.report[m] = rem[m];
+        if (tid == 0) sh.status = 2;
+        __syncthreads();
+        break;
+      }
+      // newly dead keys in key order
+      int n_list = 0;
+      for (int b0 = 0; b0 < Km; b0 += BIG_THREADS) {
+        const int m = b0 + tid;
+        const bool nd = m < Km && dead[m] == 2;
+        const u32 bal = __ballot_sync(MX_FULL, nd);
+        if (lane == 0) sh.wpart[warp] = __popc(bal);
+        __syncthreads();
+        int before = 0, tot = 0;
+        for (int x = 0; x < BIG_THREADS / 32; ++x) {
+          if (x < warp) before += sh.wpart[x];
+          tot += sh.wpart[x];
+        }
+        if (nd) {
+          a.list[n_list + before + __popc(bal & ((1u << lane) - 1))] = (u32)m;
+          dead[m] = 0;  // becomes dead when the redistribution loop reaches it
+        }
+        n_list += tot;
+        __syncthreads();
+      }
+      if (tid == 0) sh.i_list = 0;
+      __syncthreads();
+      while (true) {
+        if (tid == 0) {
+          sh.flag = 0;
+          double wsum = sh.wsum, werr = sh.werr;
+          int alive = sh.alive;
+          int i = sh.i_list;
+          for (; i < n_list; ++i) {
+            const u32 d = a.list[i];
+            dead[d] = 1;
+            nxt[a.rank_w[d]] = a.rank_w[d] + 1;  // unlink from the weight order
+            --alive;
+            wsum -= a.w[d];
+            werr += fabs(wsum) * 2.3e-16;
+            if (alive == 0) {
+              sh.status = 2;
+              break;
+            }
+            const int r = rem[d];
+            if (r > 0) {
+              // fast path certificate (see above)
+              const u32 p1 = big_find(nxt, 0);
+              const double w1 = a.w[a.order_w[p1]];
+              const double wlo = (wsum - werr) * (1.0 - 1e-14);
+              bool ok = wlo > 0.0 && w1 / wlo * (double)r * (1.0 + 1e-14) + 1e-9 < 1.0 - 1e-12;
+              u32 p = p1, last = p1;
+              for (int j = 0; ok && j < r; ++j) {
+                if (p >= (u32)Km) {
+                  ok = false;
+                  break;
+                }
+                last = p;
+                p = big_find(nxt, p + 1);
+              }
+              if (ok && p < (u32)Km) {  // selection boundary separated (or an exact tie)?
+                const double wr = a.w[a.order_w[last]], wq = a.w[a.order_w[p]];
+                ok = wr == wq || wr > wq * (1.0 + 4e-15);
+              }
+              if (!ok) {
+                sh.flag = 1;
+                sh.slow_r = r;
+                sh.slow_d = (int)d;
+                break;
+              }
+              p = p1;
+              for (int j = 0; j < r; ++j) {
+                rem[a.order_w[p]] += 1;
+                p = big_find(nxt, p + 1);
+              }
+            }
+            rem[d] = 0;
+          }
+          sh.i_list = i;
+          sh.wsum = wsum;
+          sh.werr = werr;
+          sh.alive = alive;
+        }
+        __syncthreads();
+        if (sh.status == 2 || !sh.flag) break;
+        big_apportion(a, dead, sh.slow_r, rem, sh);  // exact general case; sets sh.wsum exactly
+        if (tid == 0) {
+          rem[sh.slow_d] = 0;
+          sh.i_list += 1;
+          sh.werr = sh.wsum * 1e-15;
+        }
+        __syncthreads();
+      }
+      if (sh.status == 2) {
+        for (int m = tid; m < Km; m += BIG_THREADS) a.report[m] = rem[m];
+        __syncthreads();
+        break;
+      }
+    }
+    __syncthreads();
+    if (sh.status == 2) {  // None: the failed attempt's takes stay consumed
+      for (int m = tid; m < Km; m += BIG_THREADS) a.pos[m] += (u64)a.took[m];
+      exhausted = 1;
+      break;
+    }
+    // ---------------- the chunk repeats while every key can serve its take
+    long long rep = a.max_chunks - chunks;
+    {
+      long long my = rep;
+      for (int m = tid; m < Km; m += BIG_THREADS) {
+        const int t = a.took[m];
+        if (t <= 0) continue;
+        const long long r = (long long)(a.slen[m] - a.pos[m]) / t;
+        my = r < my ? r : my;
+      }
+      for (int d = 16; d > 0; d >>= 1) {
+        const long long o = __shfl_xor_sync(MX_FULL, my, d);
+        my = o < my ? o : my;
+      }
+      if (lane == 0) s_min[warp] = my;
+      __syncthreads();
+      for (int i = 0; i < BIG_THREADS / 32; ++i) rep = s_min[i] < rep ? s_min[i] : rep;
+      __syncthreads();
+    }
+    if (rep < 1) rep = 1;
+    // terms: keys with a take, in key order
+    long long nt = 0;
+    for (int b0 = 0; b0 < Km; b0 += BIG_THREADS) {
+      const int m = b0 + tid;
+      const bool has = m < Km && a.took[m] > 0;
+      const u32 bal = __ballot_sync(MX_FULL, has);
+      if (lane == 0) sh.wpart[warp] = __popc(bal);
+      __syncthreads();
+      int before = 0, tot = 0;
+      for (int x = 0; x < BIG_THREADS / 32; ++x) {
+        if (x < warp) before += sh.wpart[x];
+        tot += sh.wpart[x];
+      }
+      if (has) {
+        Term& tm = a.terms[n_terms + nt + before + __popc(bal & ((1u << lane) - 1))];
+        tm.m = (u32)m;
+        tm.stream = (u32)m;
+        tm.base = a.pos[m];
+        tm.len = (u64)a.took[m];
+        tm.stride = (u64)a.took[m];
+        a.pos[m] += (u64)a.took[m] * (u64)rep;
+      }
+      nt += tot;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      Phase& ph = a.phases[n_ph];
+      ph.chunk_begin = chunks;
+      ph.n_chunks = rep;
+      ph.term_begin = n_terms;
+      ph.n_terms = nt;
+    }
+    ++n_ph;
+    n_terms += nt;
+    chunks += rep;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    a.out[0] = chunks;
+    a.out[1] = n_ph;
+    a.out[2] = n_terms;
+    a.out[3] = exhausted;
+  }
+}
+
 // arbitrary mode: one stream, chunk k = [k*C, (k+1)*C) clipped
 __global__ void plan_arbitrary_kernel(const u64* seg_pre, long long nseg, long long C, long long max_chunks,
                                       Phase* phases, Term* terms, long long* out, u64* pos) {
@@ -1358,7 +1766,53 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   pa.cap_terms = cap_terms;
   pa.out = out.p;
   pa.report = report.p;
-  plan_kernel<<<1, 32, 0, s>>>(pa);
+  const bool big = w.mode == 0 && Km > PLAN_SMEM_KM && Km <= BIG_MAX_KM && mix->chunk_size < (1ll << 31) &&
+                   getenv("MX_PLAN_SERIAL") == nullptr;
+  if (big) {
+    // keys by (weight desc, key asc) and each key's rank in that order
+    std::vector<u32> ow(2 * (size_t)Km);
+    for (int m = 0; m < Km; ++m) ow[m] = (u32)m;
+    const double* wt = mix->weights;
+    std::sort(ow.begin(), ow.begin() + Km, [wt](u32 x, u32 y) { return wt[x] != wt[y] ? wt[x] > wt[y] : x < y; });
+    for (int r = 0; r < Km; ++r) ow[Km + ow[r]] = (u32)r;
+    u32* order_w = front.p;
+    u32* rank_w = reinterpret_cast<u32*>(ap_frac.p);
+    MX_CUDA_TRY(cudaMemcpyAsync(order_w, ow.data(), sizeof(u32) * Km, cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(cudaMemcpyAsync(rank_w, ow.data() + Km, sizeof(u32) * Km, cudaMemcpyHostToDevice, s));
+    BigArgs ba{};
+    ba.Km = Km;
+    ba.C = mix->chunk_size;
+    ba.strict = mix->strict;
+    ba.max_chunks = max_chunks;
+    ba.w = wts_p;
+    ba.order_w = order_w;
+    ba.rank_w = rank_w;
+    ba.seg_pre = w.seg_pre;
+    ba.s_off = w.s_off;
+    ba.pos = pos.p;
+    ba.base = scratch_ll.p;
+    ba.fkey = reinterpret_cast<unsigned long long*>(scratch_ll.p + Km);
+    ba.slen = reinterpret_cast<u64*>(scratch_ll.p + 2 * Km);
+    ba.counts = reinterpret_cast<int*>(scratch_ll.p + 3 * Km);
+    ba.took = ba.counts + Km;
+    ba.list = reinterpret_cast<u32*>(ap_idx.p);
+    ba.phases = phases.p;
+    ba.cap_phases = cap_phases;
+    ba.terms = terms.p;
+    ba.cap_terms = cap_terms;
+    ba.out = out.p;
+    ba.report = report.p;
+    const size_t smem = 9 * (size_t)Km + 4;
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+      MX_CUDA_TRY(cudaFuncSetAttribute(plan_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(9 * (size_t)BIG_MAX_KM + 4)));
+      smem_set = 9 * (size_t)BIG_MAX_KM + 4;
+    }
+    plan_big_kernel<<<1, BIG_THREADS, smem, s>>>(ba);
+  } else {
+    plan_kernel<<<1, 32, 0, s>>>(pa);
+  }
   mx_count_launch();
   if (max_chunks <= SMALL_MAX_CHUNKS && mix->chunk_size <= NM_CAP) {
     // small plan: emission driven by device-side counts, one host sync

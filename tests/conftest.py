@@ -19,7 +19,7 @@ ROOT = Path(__file__).resolve().parent.parent
 GOLDEN = ROOT / "tests" / "golden"
 sys.path.insert(0, str(ROOT))
 
-STAGE12_CASES = ["cfg1_r1", "cfg1_r64", "cfg2_small", "filters_nulls", "multi_tags", "depletion", "cfg5_small"]
+STAGE12_CASES = ["cfg1_r1", "cfg1_r64", "cfg2_small", "filters_nulls", "multi_tags", "depletion", "cfg5_small", "cfg5_wide"]
 
 
 def pytest_configure(config):

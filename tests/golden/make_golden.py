@@ -95,17 +95,20 @@ def index_table(index):
 def run_chunks(index, spec_fn, limit, arbitrary=None):
     gen = ChunkGenerator(index, JOB_SEED)
     chunks, states = [], {}
+    exhausted = False
     for i in range(limit):
         if i in (1, 3):
             states[str(i)] = gen.state_dict()
         c = gen.generate_arbitrary(arbitrary) if arbitrary else gen.generate(spec_fn())
         if c is None:
+            exhausted = True
             break
         chunks.append(c.serialize().decode("ascii"))
     report = None
     if gen.last_report is not None:
         report = {k.canonical_string(): v for k, v in gen.last_report.items()}
-    return {"chunks": chunks, "report": report, "states": states, "final_state": gen.state_dict()}
+    return {"chunks": chunks, "report": report, "states": states, "final_state": gen.state_dict(),
+            "exhausted": exhausted}
 
 
 def spec_json(spec: MixtureSpec):
@@ -208,6 +211,20 @@ def main():
     weights = {k: float(x) for k, x in zip(keys, w)}
     weights = normalize_weights(weights)
     stage12_case("cfg5_small", cc, [], {"zipf": MixtureSpec(weights, 1024)}, limit=80)
+    # H: more mixture keys than the serial planner keeps on chip (> 256), Zipf
+    # weights, uniform weights (exact share ties) and a Zipf subset
+    rt = synth.make_runs(150_000, 16, synth.numbered_props((8, 9, 10), ["caption_len", "dataset", "resolution"]),
+                         16, seed=8, zipf=1.05)
+    cc = synth.expand_numpy(rt)
+    keys = build_index(inject(cc).filter_intervals([])).component_keys()
+    rng = np.random.Generator(np.random.PCG64(56))
+    w = 1.0 / np.arange(1, len(keys) + 1) ** 0.8
+    w = w[rng.permutation(len(keys))]
+    zipf = normalize_weights({k: float(x) for k, x in zip(keys, w)})
+    uniform = normalize_weights({k: 1.0 for k in keys})
+    sub = normalize_weights({k: float(x) for k, x in list(zip(keys, w))[: 300]})
+    stage12_case("cfg5_wide", cc, [], {"zipf": MixtureSpec(zipf, 1024), "uniform": MixtureSpec(uniform, 4096),
+                                       "subset": MixtureSpec(sub, 700)}, limit=80)
     stage3()
 
 
