@@ -273,7 +273,7 @@ def our_arm(args):
     scan_bytes = n * 4 * len(rt.run_codes) + 16 * n_iv
     achieved = scan_bytes / (scan_avg * 1e-3) / 1e9
     traffic = None
-    tf = ROOT / "profiles" / "scan_runs_traffic.json"
+    tf = ROOT / "profiles" / "scan_traffic.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get("bytes_per_launch")
     line = {
@@ -286,7 +286,7 @@ def our_arm(args):
                 "ranges": n_ranges},
         "phases_ms": {p: round(v[0] / max(v[1], 1), 4) for p, v in phases.items()},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "scan_runs_kernel",
+                     "traffic": traffic, "kernel": "scan_fast_kernel (the scan_runs phase: scan_fast + deferred-tile scan_list + tail scan_direct)",
                      "bytes_per_launch": scan_bytes, "peak_kind": peak_kind,
                      "note": "algorithmic bytes = N*4*P column reads + 16 B per interval record"},
         "e2e": {"value": world * n / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,

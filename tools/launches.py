@@ -8,7 +8,7 @@ hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 h, data = rows[hi], rows[hi + 1:]
 ki, mi, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
 agg = collections.defaultdict(lambda: [0, 0.0])
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 for r in data:
     if r[mi] != "gpu__time_duration.sum":
         continue
