@@ -344,19 +344,19 @@ constexpr int FAST_MAX_FS = 4;
 // Tile body of the fast path, given the raw key sums st[j][q] of this thread's
 // samples (tile-local index warp*512 + 128j + 4lane + q). s_fs: the tile's
 // file starts (local, padded with 1<<30), visible to the CTA.
-__device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, long long tile, u32 (&st)[4][4],
+//
+// st holds RAW key sums: a sample passes iff st < fail_limit, and a failing
+// neighbour (raw sum >= fail_limit, or FAIL from the tile metadata) always
+// compares unequal to a passing key, so no per-sample clamp is needed.
+template <int SEGS>
+__device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, long long tile, u32 (&st)[SEGS][4],
                                           TileScratch& sc, const int* s_fs) {
-  constexpr int SEGS = 4;
   constexpr int WT = 32 * 4 * SEGS;
   constexpr int TILE = (S1_THREADS / 32) * WT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long t0 = tile * TILE;
   const int lw = warp * WT + 4 * lane;  // tile-local index of this thread's sample (j=0, q=0)
   const u32 lim = a.fail_limit;
-#pragma unroll
-  for (int j = 0; j < SEGS; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) st[j][q] = st[j][q] < lim ? st[j][q] : FAIL;
   if (lane == 0) sc.warp_first[warp] = st[0][0];
   if (lane == 31) sc.warp_last[warp] = st[SEGS - 1][3];
   __syncthreads();
@@ -396,9 +396,9 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
       const u32 cur = st[j][q];
       const u32 prv = q == 0 ? prev_last : st[j][q - 1];
       const u32 nxt = q == 3 ? next_first : st[j][q + 1];
-      const bool pass = !(cur & FAIL);
-      sm |= (u32)(pass && (((fsb >> q) & 1) || (prv & FAIL) || prv != cur)) << q;
-      em |= (u32)(pass && (((fsb >> (q + 1)) & 1) || (nxt & FAIL) || nxt != cur)) << q;
+      const bool pass = cur < lim;
+      sm |= (u32)(pass && (((fsb >> q) & 1) || prv != cur)) << q;
+      em |= (u32)(pass && (((fsb >> (q + 1)) & 1) || nxt != cur)) << q;
     }
     starts[j] = sm;
     ends[j] = em;
@@ -419,7 +419,7 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
   }
   if (lane == 0) sc.warp_tot[warp] = acc;
   if (warp == S1_THREADS / 32 - 1 && lane == 31)
-    sc.last_open = (!(st[SEGS - 1][3] & FAIL) && !((ends[SEGS - 1] >> 3) & 1)) ? 1u : 0u;
+    sc.last_open = (st[SEGS - 1][3] < lim && !((ends[SEGS - 1] >> 3) & 1)) ? 1u : 0u;
   __syncthreads();
   if (warp == 0) {
     const u32 x = lane < S1_THREADS / 32 ? sc.warp_tot[lane] : 0;
@@ -430,7 +430,7 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
       a.tile_open[tile] = (inc > 0 && sc.last_open) ? 1u : 0u;
     }
   }
-  if (tid == 0) a.tile_head[tile] = (!(st[0][0] & FAIL) && !(starts[0] & 1)) ? -1 : 0;
+  if (tid == 0) a.tile_head[tile] = (st[0][0] < lim && !(starts[0] & 1)) ? -1 : 0;
   __shared__ u32 s_off[FAST_MAX_FS + 1];  // local sample -> in-file sample offset per file of the tile
   if (tid <= FAST_MAX_FS) s_off[tid] = tid == 0 ? (u32)(t0 - m.fbase) : (u32)(-s_fs[tid - 1]);
   __syncthreads();
@@ -465,41 +465,44 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
   }
 }
 
-template <int PC>
-__device__ __forceinline__ void lut_sums(const u32* s_lut, const S1Args& a, const int4 (&v)[PC][4], u32 (&st)[4][4]) {
+template <int PC, int SEGS>
+__device__ __forceinline__ void lut_sums(const u32* s_lut, const S1Args& a, const int4 (&v)[PC][SEGS],
+                                         u32 (&st)[SEGS][4]) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
+  for (int j = 0; j < SEGS; ++j)
 #pragma unroll
     for (int q = 0; q < 4; ++q) st[j][q] = 0;
 #pragma unroll
   for (int p = 0; p < PC; ++p) {
     const u32* L = s_lut + a.lut_off[p] + 1;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < SEGS; ++j) {
       st[j][0] += L[v[p][j].x]; st[j][1] += L[v[p][j].y];
       st[j][2] += L[v[p][j].z]; st[j][3] += L[v[p][j].w];
     }
   }
 }
 
-// one CTA per full tile, loads in registers
-template <int PC>
-__global__ void __launch_bounds__(S1_THREADS, 2)
+// one CTA per full tile, loads in registers. SEGS = int4 segments per thread:
+// 4 (4096-sample tiles, 2 CTAs/SM) or 2 (2048-sample tiles, 4 CTAs/SM: the
+// same bytes in flight per SM, split over twice as many independent CTAs).
+template <int PC, int SEGS>
+__global__ void __launch_bounds__(S1_THREADS, SEGS == 2 ? 4 : 2)
 scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
-  constexpr int TILE = S1_THREADS * 16;
+  constexpr int TILE = S1_THREADS * 4 * SEGS;
   extern __shared__ __align__(16) u32 s_lut[];
   __shared__ TileScratch sc;
   __shared__ int s_fs[FAST_MAX_FS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long tile = blockIdx.x;
   const long long t0 = tile * TILE;
-  const int lw = warp * 512 + 4 * lane;
-  int4 v[PC][4];
+  const int lw = warp * 128 * SEGS + 4 * lane;
+  int4 v[PC][SEGS];
 #pragma unroll
   for (int p = 0; p < PC; ++p) {
     const int32_t* col = a.cols[p] + t0 + lw;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) v[p][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + 128 * j));
+    for (int j = 0; j < SEGS; ++j) v[p][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + 128 * j));
   }
   for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
   const TileMeta m = meta[tile];
@@ -509,9 +512,9 @@ scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
   }
   if (tid < FAST_MAX_FS) s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - t0) : 1 << 30;
   __syncthreads();
-  u32 st[4][4];
-  lut_sums<PC>(s_lut, a, v, st);
-  fast_tile(a, m, tile, st, sc, s_fs);
+  u32 st[SEGS][4];
+  lut_sums<PC, SEGS>(s_lut, a, v, st);
+  fast_tile<SEGS>(a, m, tile, st, sc, s_fs);
 }
 
 // persistent CTAs, every full tile's columns + metadata streamed into a ring
@@ -567,9 +570,9 @@ scan_fast_pipe_kernel(S1Args a, const TileMeta* __restrict__ meta, long long nfu
       if (tid < FAST_MAX_FS)
         s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - tile * TILE) : 1 << 30;
       u32 st[4][4];
-      lut_sums<PC>(s_lut, a, v, st);
+      lut_sums<PC, 4>(s_lut, a, v, st);
       __syncthreads();  // s_fs
-      fast_tile(a, m, tile, st, sc, s_fs);
+      fast_tile<4>(a, m, tile, st, sc, s_fs);
     }
     __syncthreads();  // slot s and the tile scratch are free again
     if (tid == 0) issue(s);

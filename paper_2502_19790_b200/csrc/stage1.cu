@@ -605,11 +605,11 @@ static void launch_direct(const S1Args& a, const TileMeta* m, long long ntiles, 
   }
 }
 
-template <int PC>
+template <int PC, int SEGS>
 static void launch_fast(const S1Args& a, const TileMeta* m, long long nfull, int lut_total, cudaStream_t s) {
   if (nfull <= 0) return;
   const char* env = getenv("MX_SCAN");
-  if (env && !strcmp(env, "fastpipe")) {  // persistent + TMA ring variant
+  if (SEGS == 4 && env && !strcmp(env, "fastpipe")) {  // persistent + TMA ring variant
     int dev = 0, n_sm = 148, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -623,7 +623,7 @@ static void launch_fast(const S1Args& a, const TileMeta* m, long long nfull, int
     kernel<<<(unsigned)std::min<long long>(nfull, n_sm), S1_THREADS, dyn, s>>>(a, m, nfull, stages, lut_bytes);
     return;
   }
-  scan_fast_kernel<PC><<<(unsigned)nfull, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m);
+  scan_fast_kernel<PC, SEGS><<<(unsigned)nfull, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m);
 }
 
 // full tiles through scan_fast_kernel when it applies, the rest generically
@@ -632,14 +632,14 @@ static void dispatch_direct(const S1Args& a, const TileMeta* m, long long ntiles
                             cudaStream_t s, long long nfull_aligned) {
   const int pc = smem_lut && a.lut_sum ? a.n_props : 0;
   long long done = 0;
-  if (SEGS == 4 && nfull_aligned > 0 && pc >= 1 && pc <= 6) {
+  if (nfull_aligned > 0 && pc >= 1 && pc <= 6) {
     switch (pc) {
-      case 1: launch_fast<1>(a, m, nfull_aligned, lut_total, s); break;
-      case 2: launch_fast<2>(a, m, nfull_aligned, lut_total, s); break;
-      case 3: launch_fast<3>(a, m, nfull_aligned, lut_total, s); break;
-      case 4: launch_fast<4>(a, m, nfull_aligned, lut_total, s); break;
-      case 5: launch_fast<5>(a, m, nfull_aligned, lut_total, s); break;
-      default: launch_fast<6>(a, m, nfull_aligned, lut_total, s); break;
+      case 1: launch_fast<1, SEGS>(a, m, nfull_aligned, lut_total, s); break;
+      case 2: launch_fast<2, SEGS>(a, m, nfull_aligned, lut_total, s); break;
+      case 3: launch_fast<3, SEGS>(a, m, nfull_aligned, lut_total, s); break;
+      case 4: launch_fast<4, SEGS>(a, m, nfull_aligned, lut_total, s); break;
+      case 5: launch_fast<5, SEGS>(a, m, nfull_aligned, lut_total, s); break;
+      default: launch_fast<6, SEGS>(a, m, nfull_aligned, lut_total, s); break;
     }
     done = nfull_aligned;
     // tiles the fast kernel deferred (more file starts than it handles)
@@ -725,7 +725,10 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
       }
     }
   }
-  constexpr int direct_segs = 4;
+  // direct-mode tile: 2 int4 segments per thread (2048-sample tiles, 4 CTAs
+  // per SM) unless MX_SCAN_SEGS=4 (4096-sample tiles, 2 CTAs per SM)
+  const char* segs_env = getenv("MX_SCAN_SEGS");
+  const int direct_segs = (segs_env && atoi(segs_env) == 4) ? 4 : 2;
   const int tile_len = use_v1 ? S1_TILE : (use_pipe ? 1024 * pipe_segs : 1024 * direct_segs);
   const int ntiles = (int)((n + tile_len - 1) / tile_len);
   bool aligned = true;
@@ -789,8 +792,9 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
         else if (pipe_segs == 2) rc = dispatch_pipe<2>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes, n_sm, s);
         else rc = dispatch_pipe<1>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes, n_sm, s);
       } else {
-        dispatch_direct<direct_segs>(a, tmeta.p, ntiles, smem_lut, lut_total, s,
-                                     getenv("MX_SCAN_NOFAST") ? 0 : nstaged);
+        const long long nfast = getenv("MX_SCAN_NOFAST") ? 0 : nstaged;
+        if (direct_segs == 4) dispatch_direct<4>(a, tmeta.p, ntiles, smem_lut, lut_total, s, nfast);
+        else dispatch_direct<2>(a, tmeta.p, ntiles, smem_lut, lut_total, s, nfast);
       }
       mx_count_launch();
       if (rc != MX_OK) return rc;
