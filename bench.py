@@ -19,9 +19,13 @@ recorded by the library on the launching stream.
 
 --impl reference times the CPU oracle port (oracle/oracle.py, a numpy/stdlib
 restatement of the reference's own algorithm) on a bounded slice of the same
-workload on the host cores. Under torchrun with N > 1 every rank indexes its
-own 100M-sample file shard (weak scaling) and the step time is the max over
-ranks.
+workload on the host cores. Under torchrun with N > 1 rank r owns its own
+100M-sample shard = global files [r*F, (r+1)*F) of ONE N x 100M-sample catalog
+(weak scaling, cfg 3 shape) and the step is the file-sharded pipeline: local
+stage 1, NCCL all-gather of the per-(key, file) block tables, hybrid index +
+global cursor layout + plan (replicated), local emission, NCCL all-gather of
+every rank's pieces and the device merge into the global chunks. Step time =
+max over ranks.
 """
 
 from __future__ import annotations
@@ -123,13 +127,21 @@ def device_columns(rt, device):
     return {p: torch.repeat_interleave(torch.from_numpy(c).to(device), lens) for p, c in rt.run_codes.items()}
 
 
-def run_step(meta, cols, spec, stream=None):
+def run_step(meta, cols, spec, stream=None, shard=None):
     """One job on the device: index + cursor layout + every chunk. Returns
-    (index, batch) so callers can read sizes."""
+    (index, batch) so callers can read sizes. With `shard` = (file_lo,
+    file_ds, file_ids) of the global catalog (N > 1): the file-sharded
+    pipeline -- local stage 1, all-gather of block tables, hybrid index,
+    global cursor layout + plan, local emission, all-gather + device merge
+    of every rank's pieces into the global chunks (paralle.py, shard.cu)."""
     from paper_2502_19790_b200 import ChunkGenerator, DeviceCatalog, build_index_from_catalog
+    from paper_2502_19790_b200.parallel import build_sharded_index
 
     dcat = DeviceCatalog(meta, columns=cols, nullable={p: False for p in cols})
-    idx = build_index_from_catalog(dcat, [], stream=stream)
+    if shard is None:
+        idx = build_index_from_catalog(dcat, [], stream=stream)
+    else:
+        idx = build_sharded_index(dcat, [], *shard, stream=stream)
     gen = ChunkGenerator(idx, CFG["job_seed"], stream=stream)
     batch = gen.plan_batch(spec, 1 << 40)
     return idx, gen, batch
@@ -188,16 +200,21 @@ def our_arm(args):
     from paper_2502_19790_b200.catalog import ColumnarCatalog
 
     rank, world, local = env_rank()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    device = torch.device("cuda", local if world > 1 else 0)
+    device = torch.device("cuda", local % torch.cuda.device_count() if world > 1 else 0)
     torch.cuda.set_device(device)
+    if world > 1:
+        # nccl on the real multi-GPU run; MX_BENCH_BACKEND=gloo lets N ranks
+        # share one GPU to exercise the same code path
+        dist.init_process_group(os.environ.get("MX_BENCH_BACKEND", "nccl"))
     L = _lib.lib()
     rt = make_workload(rank, args.scale)
     meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
     cols = device_columns(rt, device)
     spec = synth.cfg2_mixture(CFG["chunk_size"])
+    shard = None
+    if world > 1:  # rank r owns global files [r*F, (r+1)*F) of one W*F-file catalog
+        nf = len(rt.file_sizes)
+        shard = (rank * nf, np.zeros(world * nf, np.int32), np.arange(1, world * nf + 1, dtype=np.int64))
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -206,7 +223,7 @@ def our_arm(args):
             dist.barrier()
 
     for _ in range(args.warmup):
-        idx, gen, batch = run_step(meta, cols, spec)
+        idx, gen, batch = run_step(meta, cols, spec, shard=shard)
         del idx, gen, batch
     barrier()
     # ---------------------------------------------------------------- timed
@@ -219,8 +236,9 @@ def our_arm(args):
     ev0.record(stream)
     n_chunks = n_ranges = n_iv = 0
     for _ in range(args.steps):
-        idx, gen, batch = run_step(meta, cols, spec)
-        n_chunks, n_ranges, n_iv = batch.n_chunks, batch.n_ranges, idx.n_intervals
+        idx, gen, batch = run_step(meta, cols, spec, shard=shard)
+        n_chunks, n_ranges = batch.n_chunks, batch.n_ranges  # global chunks (merged when sharded)
+        n_iv = getattr(idx, "local_index", idx).n_intervals  # intervals this rank's scan wrote
         n_keys, n_blocks = idx.n_keys, idx.n_blocks
         del idx, gen, batch
     ev1.record(stream)
@@ -244,7 +262,9 @@ def our_arm(args):
 
     def e2e_step():
         dcols = {p: x.to(device, non_blocking=True) for p, x in pinned.items()}
-        idx, gen, batch = run_step(meta, dcols, spec)
+        idx, gen, batch = run_step(meta, dcols, spec, shard=shard)
+        if rank != 0:  # the merged global chunks are read back on the root
+            return 0
         h = batch.to_host()
         return sum(v.nbytes for k, v in h.items() if k in ("off", "ids", "seeds")) + 16 * batch.n_ranges
 
@@ -281,7 +301,7 @@ def our_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": dict(CFG, parallelism=f"file-sharded x{world}" if world > 1 else "single GPU"),
-        "chunks_per_s": world * n_chunks / (ms_max * 1e-3),
+        "chunks_per_s": n_chunks / (ms_max * 1e-3),
         "job": {"samples": n, "intervals": n_iv, "keys": n_keys, "blocks": n_blocks, "chunks": n_chunks,
                 "ranges": n_ranges},
         "phases_ms": {p: round(v[0] / max(v[1], 1), 4) for p, v in phases.items()},

@@ -148,6 +148,10 @@ int mx_gen_result_copy(const mx_gen* gen, int64_t* chunk_offsets, int64_t* chunk
 int mx_gen_result_device(const mx_gen* gen, const int64_t** chunk_offsets, const uint64_t** seeds,
                          const uint32_t** mkey, const uint32_t** file_index, const uint32_t** start,
                          const uint32_t** end);
+/* Copy of the last plan's result into caller DEVICE buffers: chunk_offsets
+ * [n_chunks+1], pieces [n_ranges] (file_index = index into the file table). */
+int mx_gen_result_export(const mx_gen* gen, int64_t* chunk_offsets, uint32_t* mkey, uint32_t* file_index,
+                         uint32_t* start, uint32_t* end, void* stream);
 /* Shortfall report of the last generate() that returned None: host [n_mkeys]. */
 int mx_gen_report(const mx_gen* gen, int64_t* remaining);
 /* Remember / restore the cursor state and next chunk id on the device (used
@@ -165,6 +169,51 @@ int mx_gen_component_order(const mx_gen* gen, uint32_t* order);
 /* RangeCursor._ranges of one component: host outputs sized by n_ranges. */
 int mx_gen_cursor_ranges(const mx_gen* gen, uint32_t comp, int64_t* n_ranges, int32_t* ds,
                          int64_t* file_id, uint32_t* start, uint32_t* end, int64_t capacity);
+
+/* ------------------------------------------------------------------ multi-GPU
+ * File-sharded index. Rank r indexes the contiguous global
+ * file range [file_lo, file_hi) with mx_index_build (local file indices
+ * 0..file_hi-file_lo-1), exports its (key, file) block table, and after an
+ * all-gather of the tables builds the hybrid index whose keys, blocks, cursor
+ * shuffles and chunk plans are those of the whole catalog
+ * [RangeCursor index.py:126-147 over files of every rank]. Chunks planned on
+ * a hybrid index hold only this rank's pieces; mx_chunks_merge interleaves the
+ * ranks' chunk CSRs into the global (mixture key, file, start) order. */
+
+/* Device rows uint32[n_blocks][4] = (packed key, file_base + file index,
+ * samples, intervals), in (packed key, file) order. */
+int mx_index_block_table(const mx_index* index, int64_t file_base, uint32_t* rows, void* stream);
+/* Host copy of the realized packed keys [n_keys] (ascending). */
+int mx_index_packed_keys(const mx_index* index, uint32_t* packed);
+
+typedef struct mx_shard_desc {
+  int32_t world, rank;
+  int64_t file_lo, file_hi;      /* this rank's global file indices */
+  int32_t n_files;               /* global file table: */
+  const int32_t* file_ds;        /*   host [n_files] dataset ids (nondecreasing) */
+  const int64_t* file_ids;       /*   host [n_files] file ids */
+  const uint32_t* tables;        /* device uint32[world][cap][4] gathered block rows */
+  const int64_t* counts;         /* host [world] rows per rank */
+  int64_t cap;
+  const uint32_t* global_keys;   /* host [n_global_keys] sorted union of packed keys */
+  int64_t n_global_keys;
+} mx_shard_desc;
+
+int mx_index_build_sharded(const mx_index* local, const mx_shard_desc* desc, void* stream, mx_index** out);
+/* Sharded cursor state: a key whose frontier lies inside another rank's
+ * block reports pos = offset = -1 (mx_gen_get_cursors) / consumed = -1
+ * (mx_gen_cursor_to_consumed); the owner reports the value, so a MAX
+ * all-reduce over ranks completes it. */
+int mx_gen_cursor_to_consumed(const mx_gen* gen, const int64_t* pos, const int64_t* offset, int64_t* consumed);
+int mx_gen_set_consumed(mx_gen* gen, const int64_t* consumed);
+/* Root-side merge of `world` per-rank chunk CSRs of the same n_chunks chunks:
+ * offs device int64[world][n_chunks+1]; piece arrays device uint32[world][cap]
+ * (rank q's pieces at q*cap). Outputs: out_off device int64[n_chunks+1],
+ * pieces device uint32[sum of ranks' pieces]. */
+int mx_chunks_merge(int32_t world, int64_t n_chunks, int64_t cap, const int64_t* offs, const uint32_t* mkey,
+                    const uint32_t* file_index, const uint32_t* start, const uint32_t* end, int64_t* out_off,
+                    uint32_t* out_mkey, uint32_t* out_file_index, uint32_t* out_start, uint32_t* out_end,
+                    void* stream);
 
 /* ------------------------------------------------------------------ stage 3
  * Per-domain loss reduction [per_domain_loss client.py:582-598]: device

@@ -74,6 +74,23 @@ class MixtureDesc(C.Structure):
     ]
 
 
+class ShardDesc(C.Structure):
+    _fields_ = [
+        ("world", i32),
+        ("rank", i32),
+        ("file_lo", i64),
+        ("file_hi", i64),
+        ("n_files", i32),
+        ("file_ds", P(i32)),
+        ("file_ids", P(i64)),
+        ("tables", vp),
+        ("counts", P(i64)),
+        ("cap", i64),
+        ("global_keys", P(u32)),
+        ("n_global_keys", i64),
+    ]
+
+
 _SIGS = {
     "mx_last_error": (C.c_char_p, []),
     "mx_abi_version": (C.c_int, []),
@@ -94,6 +111,7 @@ _SIGS = {
     "mx_gen_result_copy": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "mx_gen_result_device": (C.c_int, [vp, P(vp), P(vp), P(vp), P(vp), P(vp), P(vp)]),
     "mx_gen_report": (C.c_int, [vp, vp]),
+    "mx_gen_result_export": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "mx_gen_mark": (C.c_int, [vp]),
     "mx_gen_reset_to_mark": (C.c_int, [vp]),
     "mx_gen_next_chunk_id": (C.c_int, [vp, P(i64)]),
@@ -102,6 +120,12 @@ _SIGS = {
     "mx_gen_set_cursors": (C.c_int, [vp, vp, vp]),
     "mx_gen_component_order": (C.c_int, [vp, vp]),
     "mx_gen_cursor_ranges": (C.c_int, [vp, u32, P(i64), vp, vp, vp, vp, i64]),
+    "mx_index_block_table": (C.c_int, [vp, i64, vp, vp]),
+    "mx_index_packed_keys": (C.c_int, [vp, vp]),
+    "mx_index_build_sharded": (C.c_int, [vp, P(ShardDesc), vp, P(vp)]),
+    "mx_gen_cursor_to_consumed": (C.c_int, [vp, vp, vp, vp]),
+    "mx_gen_set_consumed": (C.c_int, [vp, vp]),
+    "mx_chunks_merge": (C.c_int, [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "mx_domain_loss": (C.c_int, [vp, vp, i64, i32, vp, vp, vp]),
     "mx_fit_power_law": (C.c_int, [i32, vp, vp, vp, vp, vp, vp]),
     "mx_ado_pi": (C.c_int, [i32, vp, vp, vp, dbl, dbl, dbl, vp, vp, vp, vp]),

@@ -240,12 +240,30 @@ class ChunkGenerator:
         pos, off = np.zeros(k, np.int64), np.zeros(k, np.int64)
         if k:
             _lib.check(_lib.lib().mx_gen_get_cursors(self._h, _lib.ptr(pos), _lib.ptr(off)))
+        sh = getattr(self.index, "shard", None)
+        if sh is not None:  # a frontier inside another rank's block is answered by its owner
+            from .parallel import _max_allreduce
+
+            both = _max_allreduce(np.concatenate([pos, off]), sh.group, self.index.catalog.device)
+            pos, off = both[:k], both[k:]
         return pos, off
 
     def _set_cursor_state(self, pos, off) -> None:
-        if self.index.n_keys:
-            _lib.check(_lib.lib().mx_gen_set_cursors(self._h, _lib.ptr(np.ascontiguousarray(pos, np.int64)),
-                                                     _lib.ptr(np.ascontiguousarray(off, np.int64))))
+        if not self.index.n_keys:
+            return
+        L = _lib.lib()
+        pos = np.ascontiguousarray(pos, np.int64)
+        off = np.ascontiguousarray(off, np.int64)
+        sh = getattr(self.index, "shard", None)
+        if sh is None:
+            _lib.check(L.mx_gen_set_cursors(self._h, _lib.ptr(pos), _lib.ptr(off)))
+            return
+        from .parallel import _max_allreduce
+
+        used = np.zeros(self.index.n_keys, np.int64)
+        _lib.check(L.mx_gen_cursor_to_consumed(self._h, _lib.ptr(pos), _lib.ptr(off), _lib.ptr(used)))
+        used = np.ascontiguousarray(_max_allreduce(used, sh.group, self.index.catalog.device))
+        _lib.check(L.mx_gen_set_consumed(self._h, _lib.ptr(used)))
 
     def _plan(self, spec, max_chunks: int, arbitrary_size: int | None = None) -> tuple[int, bool, list | None]:
         L = _lib.lib()
@@ -267,7 +285,12 @@ class ChunkGenerator:
     def _result(self, spec, mkeys, arbitrary_size) -> "ChunkBatch":
         nc, nr = C.c_int64(), C.c_int64()
         _lib.check(_lib.lib().mx_gen_result_sizes(self._h, C.byref(nc), C.byref(nr)))
-        return ChunkBatch(self, nc.value, nr.value, mkeys, spec, arbitrary_size)
+        batch = ChunkBatch(self, nc.value, nr.value, mkeys, spec, arbitrary_size)
+        if getattr(self.index, "shard", None) is not None:  # collective: interleave every rank's pieces
+            from .parallel import merge_batch
+
+            batch = merge_batch(self, batch, self.stream)
+        return batch
 
     def plan_batch(self, spec: MixtureSpec | None, max_chunks: int, arbitrary_size: int | None = None) -> "ChunkBatch":
         """Plan + emit up to ``max_chunks`` chunks on the device (bulk API).

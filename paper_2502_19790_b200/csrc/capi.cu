@@ -252,6 +252,55 @@ int mx_index_export_intervals(const mx_index* index, uint32_t* key_rank, int32_t
   return MX_OK;
 }
 
+int mx_index_block_table(const mx_index* index, int64_t file_base, uint32_t* rows, void* stream) {
+  MX_CHECK_ARG(index && (rows || index->d.n_blocks == 0), "null argument");
+  MX_CHECK_ARG(file_base >= 0 && file_base + index->d.n_files < (1ll << 32), "file_base out of range");
+  g_err.clear();
+  return index_block_table(&index->d, (u32)file_base, reinterpret_cast<uint4*>(rows), (cudaStream_t)stream);
+}
+
+int mx_index_packed_keys(const mx_index* index, uint32_t* packed) {
+  MX_CHECK_ARG(index && (packed || index->d.n_keys == 0), "null argument");
+  if (index->d.n_keys == 0) return MX_OK;
+  cudaError_t e = cudaMemcpy(packed, index->d.key_packed.p, sizeof(u32) * index->d.n_keys, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "packed keys", __FILE__, __LINE__);
+  return MX_OK;
+}
+
+int mx_index_build_sharded(const mx_index* local, const mx_shard_desc* desc, void* stream, mx_index** out) {
+  MX_CHECK_ARG(local && desc && out, "null argument");
+  MX_CHECK_ARG(desc->world >= 1 && desc->rank >= 0 && desc->rank < desc->world, "bad world/rank");
+  MX_CHECK_ARG(desc->file_lo >= 0 && desc->file_hi - desc->file_lo == local->d.n_files &&
+                   desc->file_hi <= desc->n_files,
+               "file range does not match the local index");
+  MX_CHECK_ARG(desc->n_global_keys == 0 || desc->global_keys, "null global keys");
+  MX_CHECK_ARG(desc->file_ds && desc->file_ids && desc->counts, "null file table or counts");
+  for (int q = 0; q < desc->world; ++q)
+    MX_CHECK_ARG(desc->counts[q] >= 0 && desc->counts[q] <= desc->cap, "block count exceeds cap");
+  g_err.clear();
+  keep_pool_warm();
+  mx_index* ix = new mx_index();
+  int rc = index_build_sharded(&local->d, desc, (cudaStream_t)stream, &ix->d);
+  if (rc < 0) {
+    delete ix;
+    return rc;
+  }
+  *out = ix;
+  return MX_OK;
+}
+
+int mx_chunks_merge(int32_t world, int64_t n_chunks, int64_t cap, const int64_t* offs, const uint32_t* mkey,
+                    const uint32_t* file_index, const uint32_t* start, const uint32_t* end, int64_t* out_off,
+                    uint32_t* out_mkey, uint32_t* out_file_index, uint32_t* out_start, uint32_t* out_end,
+                    void* stream) {
+  MX_CHECK_ARG(world >= 1 && n_chunks >= 0 && cap >= 0, "bad sizes");
+  MX_CHECK_ARG(offs && out_off, "null offsets");
+  g_err.clear();
+  return chunks_merge(world, n_chunks, cap, reinterpret_cast<const long long*>(offs), mkey, file_index, start, end,
+                      reinterpret_cast<long long*>(out_off), out_mkey, out_file_index, out_start, out_end,
+                      (cudaStream_t)stream);
+}
+
 int mx_gen_create(mx_index* index, const uint8_t* cursor_prefix, int32_t cursor_prefix_len, const uint8_t* chunk_prefix,
                   int32_t chunk_prefix_len, uint64_t order_seed, void* stream, mx_gen** out) {
   MX_CHECK_ARG(index && out, "null argument");
@@ -374,6 +423,34 @@ int mx_gen_result_device(const mx_gen* gen, const int64_t** chunk_offsets, const
   return MX_OK;
 }
 
+int mx_gen_result_export(const mx_gen* gen, int64_t* chunk_offsets, uint32_t* mkey, uint32_t* file_index,
+                         uint32_t* start, uint32_t* end, void* stream) {
+  MX_CHECK_ARG(gen && chunk_offsets, "null argument");
+  const GenData& g = gen->d;
+  const long long C = g.res_chunks, R = g.res_ranges;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (g.h_small_valid == C && C > 0 && g.h_small) {  // small plan: the pinned mirror holds the result
+    const unsigned char* b = g.h_small + 32;
+    const long long cap = g.h_small_cap, slots = g.h_small_slots;
+    e = cudaMemcpyAsync(chunk_offsets, b, sizeof(long long) * (C + 1), cudaMemcpyHostToDevice, s);
+    b += sizeof(long long) * (cap + 1) + sizeof(u64) * cap + sizeof(long long) * cap;
+    const u32* h = reinterpret_cast<const u32*>(b);
+    u32* dst[4] = {mkey, file_index, start, end};
+    for (int f = 0; f < 4 && e == cudaSuccess; ++f)
+      if (dst[f] && R) e = cudaMemcpyAsync(dst[f], h + f * slots, sizeof(u32) * R, cudaMemcpyHostToDevice, s);
+  } else {
+    e = cudaMemcpyAsync(chunk_offsets, g.res_off.p, sizeof(long long) * (C + 1), cudaMemcpyDeviceToDevice, s);
+    const u32* src[4] = {g.res_mkey.p, g.res_file.p, g.res_start.p, g.res_end.p};
+    u32* dst[4] = {mkey, file_index, start, end};
+    for (int f = 0; f < 4 && e == cudaSuccess; ++f)
+      if (dst[f] && R) e = cudaMemcpyAsync(dst[f], src[f], sizeof(u32) * R, cudaMemcpyDeviceToDevice, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "result export", __FILE__, __LINE__);
+  return MX_OK;
+}
+
 int mx_gen_report(const mx_gen* gen, int64_t* remaining) {
   MX_CHECK_ARG(gen && remaining, "null argument");
   for (size_t i = 0; i < gen->d.report.size(); ++i) remaining[i] = gen->d.report[i];
@@ -432,15 +509,29 @@ static int cursor_tables(const GenData& g, std::vector<u32>& kbf, std::vector<u3
   return MX_OK;
 }
 
+// sharded index: real-interval prefix (rcum) and whether each cursor position
+// is local
+static int shard_tables(const GenData& g, std::vector<unsigned long long>& rcum, std::vector<u32>& lcnt) {
+  const IndexData& d = *g.ix;
+  rcum.resize(d.n_intervals + 1);
+  lcnt.resize(d.n_intervals + 1);
+  cudaError_t e = cudaMemcpy(rcum.data(), g.rcum.p, sizeof(u64) * rcum.size(), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(lcnt.data(), g.lcnt.p, sizeof(u32) * lcnt.size(), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "shard tables", __FILE__, __LINE__);
+  return MX_OK;
+}
+
 int mx_gen_get_cursors(const mx_gen* gen, int64_t* pos, int64_t* offset) {
   MX_CHECK_ARG(gen && pos && offset, "null argument");
   const GenData& g = gen->d;
   const long long K = g.K;
   if (K == 0) return MX_OK;
-  std::vector<u32> kbf, bf;
-  std::vector<unsigned long long> ccum, used(K);
+  std::vector<u32> kbf, bf, lcnt;
+  std::vector<unsigned long long> ccum, used(K), rcum;
   int rc = cursor_tables(g, kbf, bf, ccum);
   if (rc) return rc;
+  const bool sharded = g.ix->sharded && g.ix->n_intervals > 0;
+  if (sharded && (rc = shard_tables(g, rcum, lcnt))) return rc;
   cudaError_t e = cudaMemcpy(used.data(), g.consumed.p, sizeof(u64) * K, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return mx_fail_cuda(e, "cursors", __FILE__, __LINE__);
   for (long long k = 0; k < K; ++k) {
@@ -454,12 +545,71 @@ int mx_gen_get_cursors(const mx_gen* gen, int64_t* pos, int64_t* offset) {
     }
     pos[k] = lo - ib;
     offset[k] = (int64_t)(used[k] - (ccum[lo] - base));
+    if (sharded) {
+      const bool local = lo < ie && lcnt[lo + 1] > lcnt[lo];
+      if (offset[k] > 0 && !local) {  // inside another rank's block: its owner answers
+        pos[k] = offset[k] = -1;
+      } else {
+        pos[k] = (int64_t)(rcum[lo] - rcum[ib]);
+      }
+    }
   }
+  return MX_OK;
+}
+
+int mx_gen_cursor_to_consumed(const mx_gen* gen, const int64_t* pos, const int64_t* offset, int64_t* consumed) {
+  MX_CHECK_ARG(gen && pos && offset && consumed, "null argument");
+  const GenData& g = gen->d;
+  const long long K = g.K;
+  if (K == 0) return MX_OK;
+  std::vector<u32> kbf, bf, lcnt;
+  std::vector<unsigned long long> ccum, rcum;
+  int rc = cursor_tables(g, kbf, bf, ccum);
+  if (rc) return rc;
+  const bool sharded = g.ix->sharded && g.ix->n_intervals > 0;
+  if (sharded && (rc = shard_tables(g, rcum, lcnt))) return rc;
+  for (long long k = 0; k < K; ++k) {
+    const long long ib = bf[kbf[k]], ie = bf[kbf[k + 1]];
+    const long long n_real = sharded ? (long long)(rcum[ie] - rcum[ib]) : ie - ib;
+    if (pos[k] < 0 || pos[k] > n_real || offset[k] < 0)
+      return mx_fail(MX_ERR_INVALID, "cursor state out of range for component %lld", k);
+    long long j = ib + pos[k];
+    if (sharded) {  // cursor position holding real range pos[k]: rcum[j] <= pos < rcum[j+1]
+      long long lo = ib, hi = ie;
+      while (lo < hi) {
+        long long mid = (lo + hi + 1) / 2;
+        if ((long long)(rcum[mid] - rcum[ib]) <= pos[k]) lo = mid; else hi = mid - 1;
+      }
+      j = lo;
+      if ((long long)(rcum[j] - rcum[ib]) < pos[k]) {  // strictly inside a remote block
+        consumed[k] = -1;
+        continue;
+      }
+    }
+    const unsigned long long used = ccum[j] - ccum[ib] + (unsigned long long)offset[k];
+    if (used > ccum[ie] - ccum[ib]) return mx_fail(MX_ERR_INVALID, "cursor offset beyond component %lld", k);
+    consumed[k] = (int64_t)used;
+  }
+  return MX_OK;
+}
+
+int mx_gen_set_consumed(mx_gen* gen, const int64_t* consumed) {
+  MX_CHECK_ARG(gen && consumed, "null argument");
+  GenData& g = gen->d;
+  const long long K = g.K;
+  if (K == 0) return MX_OK;
+  for (long long k = 0; k < K; ++k)
+    if (consumed[k] < 0 || (unsigned long long)consumed[k] > g.h_comp_total[k])
+      return mx_fail(MX_ERR_INVALID, "consumed samples out of range for component %lld", k);
+  cudaError_t e = cudaMemcpy(g.consumed.p, consumed, sizeof(u64) * K, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "set consumed", __FILE__, __LINE__);
   return MX_OK;
 }
 
 int mx_gen_set_cursors(mx_gen* gen, const int64_t* pos, const int64_t* offset) {
   MX_CHECK_ARG(gen && pos && offset, "null argument");
+  if (gen->d.ix->sharded)
+    return mx_fail(MX_ERR_INVALID, "sharded generator: use mx_gen_cursor_to_consumed + mx_gen_set_consumed");
   GenData& g = gen->d;
   const long long K = g.K;
   if (K == 0) return MX_OK;

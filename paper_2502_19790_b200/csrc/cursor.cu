@@ -305,6 +305,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   comp_total_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
                                                                ix->iv_cum.p, g->comp_total.p);
   mx_count_launch();
+  if (int rc = gen_local_lists(g, s)) return rc;  // sharded index: this rank's cursor positions
   MX_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
   MX_CUDA_TRY(cudaGetLastError());
   g->h_comp_order.resize(K);

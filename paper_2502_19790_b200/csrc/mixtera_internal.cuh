@@ -78,6 +78,12 @@ struct IndexData {
   int32_t str_base[MX_MAX_PROPS] = {};
   DevBuf<uint8_t> str_bytes;
   DevBuf<long long> str_off;
+  // file-sharded hybrid index (shard.cu): this rank's intervals + one
+  // pseudo-interval per remote (key, file) block; files [file_lo, file_hi)
+  // are local, iv_nreal = real intervals behind each entry (1 if local)
+  bool sharded = false;
+  long long file_lo = 0, file_hi = 0;
+  DevBuf<u32> iv_nreal;
 };
 
 struct GenData {
@@ -92,6 +98,10 @@ struct GenData {
   DevBuf<u64> comp_total;
   std::vector<unsigned long long> h_comp_total;
   DevBuf<u64> consumed;
+  // sharded index only: lcnt u32[I+1] local intervals before each cursor
+  // position, lpos u32[#local] their positions, rcum u64[I+1] real intervals
+  DevBuf<u32> lcnt, lpos;
+  DevBuf<u64> rcum;
   DevBuf<uint8_t> chunk_prefix;
   int chunk_prefix_len = 0;
   long long next_chunk_id = 0;
@@ -140,6 +150,13 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
                  cudaStream_t s, GenData* g);
 int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, long long* n_out);
 int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long long* n_out);
+int index_finalize(IndexData* ix, long long I, cudaStream_t s);
+int index_block_table(const IndexData* ix, u32 file_base, uint4* out, cudaStream_t s);
+int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream_t s, IndexData* out);
+int gen_local_lists(GenData* g, cudaStream_t s);
+int chunks_merge(int W, long long C, long long cap, const long long* offs, const u32* mkey, const u32* file,
+                 const u32* start, const u32* end, long long* out_off, u32* o_mkey, u32* o_file, u32* o_start,
+                 u32* o_end, cudaStream_t s);
 
 }  // namespace mx
 

@@ -869,6 +869,30 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   } else {
     ix.iv_key.take(k2); ix.iv_file.take(f2); ix.iv_start.take(s2); ix.iv_end.take(e2);
   }
+  return index_finalize(&ix, I, s);
+}
+
+// Block / key structure and cumulative lengths of the interval table
+// (iv_key, iv_file, iv_start, iv_end) sorted by (packed key, file, start):
+// blk_*, key_*, iv_cum, n_keys, n_blocks. IndexBuildError on an empty or
+// overlapping interval (index.py:32-47).
+int index_finalize(IndexData* ixp, long long I, cudaStream_t s) {
+  IndexData& ix = *ixp;
+  ix.n_intervals = I;
+  if (I == 0) {
+    ix.n_keys = ix.n_blocks = 0;
+    return MX_OK;
+  }
+  DevBuf<u64> scratch64;
+  DevBuf<u32> ctr;
+  DevBuf<DevError> err;
+  MX_CUDA_TRY(scratch64.alloc(2, s));
+  MX_CUDA_TRY(ctr.alloc(2, s));
+  MX_CUDA_TRY(err.alloc(1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(scratch64.p, 0, sizeof(u64) * 2, s));
+  MX_CUDA_TRY(cudaMemsetAsync(err.p, 0xff, sizeof(u64), s));
+  MX_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(err.p) + 8, 0, 8, s));
+  DevError h_err;
   // ---- boundaries and cumulative lengths
   const int stiles = (int)((I + SC_TILE - 1) / SC_TILE);
   DevBuf<u64> st2;
@@ -880,11 +904,11 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(ix.key_packed.alloc(I, s));
   MX_CUDA_TRY(ix.iv_cum.alloc(I + 1, s));
   MX_CUDA_TRY(cudaMemsetAsync(st2.p, 0, sizeof(u64) * stiles, s));
-  MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32) * 4, s));
+  MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32) * 2, s));
   std::unique_ptr<MxPhase> ph_scan(new MxPhase("index_scans", s));
   index_bounds_kernel<<<stiles, SC_THREADS, 0, s>>>(ix.iv_key.p, ix.iv_file.p, I, st2.p, ctr.p,
                                                     ix.blk_first.p, ix.blk_file.p, ix.blk_key.p,
-                                                    ix.key_blk_first.p, ix.key_packed.p, scratch64.p + 1);
+                                                    ix.key_blk_first.p, ix.key_packed.p, scratch64.p);
   mx_count_launch();
   MX_CUDA_TRY(cudaMemsetAsync(st2.p, 0, sizeof(u64) * stiles, s));
   interval_cum_kernel<<<stiles, SC_THREADS, 0, s>>>(ix.iv_start.p, ix.iv_end.p, I, st2.p, ctr.p + 1,
@@ -893,7 +917,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   ph_scan.reset();
   MX_CUDA_TRY(cudaGetLastError());
   u64 tot = 0;
-  MX_CUDA_TRY(cudaMemcpyAsync(&tot, scratch64.p + 1, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(&tot, scratch64.p, sizeof(u64), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaMemcpyAsync(&h_err, err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
   if (h_err.overlap) return mx_fail(MX_ERR_INDEX, "empty or overlapping interval in index build");

@@ -934,6 +934,9 @@ struct EmitArgs {
   const u32* iv_start;
   const u32* iv_end;
   const u32* iv_file;
+  // sharded (hybrid) index: cut only this rank's intervals (shard.cu)
+  const u32* lcnt;
+  const u32* lpos;
 };
 
 __device__ __forceinline__ long long ub_u64(const u64* v, long long lo, long long hi, u64 x) {
@@ -979,18 +982,24 @@ __device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink s
     const u64 cb = a.ccum[ib];
     long long j = ub_u64(a.ccum, ib, ie, cb + lo_abs) - 1;
     const long long j1 = ub_u64(a.ccum, ib, ie, cb + hi_abs - 1) - 1;
-    if (!WRITE) {
+    auto cut = [&](long long jj) {
+      const u32 iv = a.civ[jj];
+      const u64 off = a.ccum[jj] - cb;
+      const u64 len = a.ccum[jj + 1] - a.ccum[jj];
+      const u64 from = lo_abs > off ? lo_abs : off;
+      const u64 to = hi_abs < off + len ? hi_abs : off + len;
+      sink(n++, a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
+           a.iv_start[iv] + (u32)(to - off));
+    };
+    if (a.lcnt) {  // local intervals among cursor positions [j, j1]
+      const u32 r0 = a.lcnt[j], r1 = a.lcnt[j1 + 1];
+      if (!WRITE) n += r1 - r0;
+      else
+        for (u32 r = r0; r < r1; ++r) cut(a.lpos[r]);
+    } else if (!WRITE) {
       n += (u64)(j1 - j + 1);
     } else {
-      for (; j <= j1; ++j) {
-        const u32 iv = a.civ[j];
-        const u64 off = a.ccum[j] - cb;
-        const u64 len = a.ccum[j + 1] - a.ccum[j];
-        const u64 from = lo_abs > off ? lo_abs : off;
-        const u64 to = hi_abs < off + len ? hi_abs : off + len;
-        sink(n++, a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
-             a.iv_start[iv] + (u32)(to - off));
-      }
+      for (; j <= j1; ++j) cut(j);
     }
     x = seg_end < y ? seg_end : y;
     ++i;
@@ -1534,6 +1543,8 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Term* 
   a.iv_start = ix->iv_start.p;
   a.iv_end = ix->iv_end.p;
   a.iv_file = ix->iv_file.p;
+  a.lcnt = g->lcnt.p;
+  a.lpos = g->lpos.p;
   DevBuf<u64> pair_off;
   MX_CUDA_TRY(pair_off.alloc(n_pairs + 1, s));
   const unsigned pb = (unsigned)((n_pairs + 255) / 256);
@@ -1836,6 +1847,8 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     a.iv_start = ix->iv_start.p;
     a.iv_end = ix->iv_end.p;
     a.iv_file = ix->iv_file.p;
+    a.lcnt = g->lcnt.p;
+    a.lpos = g->lpos.p;
     const long long slots = max_chunks * NM_CAP;
     struct { u32* p; } gm, gf, gs, ge, ovf;
     struct { u64* p; } cnt;

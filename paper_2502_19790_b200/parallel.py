@@ -93,3 +93,193 @@ def gather_blocks(table: np.ndarray, group=None, device=None) -> np.ndarray:
     outs = [torch.zeros_like(buf) for _ in range(world)]
     dist.all_gather(outs, buf, group=group)
     return merge_blocks([o[: int(s.item())].cpu().numpy() for o, s in zip(outs, sizes)])
+
+
+# ---------------------------------------------------------------------------
+# File-sharded device index + chunk emission (csrc/shard.cu)
+# ---------------------------------------------------------------------------
+def _coll_device(group, device):
+    """Where collective tensors live: the GPU for NCCL, host memory otherwise
+    (gloo; used by the multi-process tests on one GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def all_gather_rows(t, group=None):
+    """All-gather a [n, ...] tensor whose n differs per rank. Returns the
+    stacked, zero-padded [world, cap, ...] tensor (on t's device) and the
+    per-rank row counts (host list)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    cdev = _coll_device(group, t.device)
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=cdev)
+    sizes = torch.zeros(world, dtype=torch.int64, device=cdev)
+    dist.all_gather_into_tensor(sizes, n, group=group)
+    counts = [int(x) for x in sizes.tolist()]
+    cap = max(max(counts), 1)
+    buf = torch.zeros((cap, *t.shape[1:]), dtype=t.dtype, device=cdev)
+    if t.shape[0]:
+        buf[: t.shape[0]] = t.to(cdev)
+    out = torch.empty((world * cap, *t.shape[1:]), dtype=t.dtype, device=cdev)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    return out.view(world, cap, *t.shape[1:]).to(t.device), counts
+
+
+def global_nullable(part: ColumnarCatalog, group=None) -> dict:
+    """Collective: per-property "holds a null anywhere in the catalog" flags
+    (MAX over ranks). The packed-key layout depends on them (codec.py), so
+    every shard's DeviceCatalog must be built with the GLOBAL flags."""
+    import torch
+    import torch.distributed as dist
+
+    props = sorted(part.vocab)
+    flags = np.array([bool((np.asarray(part.columns[p]) < 0).any()) for p in props], dtype=np.int64)
+    if dist.is_available() and dist.is_initialized():
+        flags = _max_allreduce(flags, group, None)
+    return {p: bool(f) for p, f in zip(props, flags.tolist())}
+
+
+class ShardInfo:
+    def __init__(self, world, rank, group, file_lo, file_hi, file_ds, file_ids):
+        self.world, self.rank, self.group = world, rank, group
+        self.file_lo, self.file_hi = file_lo, file_hi
+        self.file_ds, self.file_ids = file_ds, file_ids
+
+
+def build_sharded_index(local_catalog, predicates=(), file_lo: int = 0, file_ds=None, file_ids=None,
+                        group=None, stream=None):
+    """Collective: every rank passes its contiguous file shard (a
+    ``DeviceCatalog`` whose files are the global files
+    ``[file_lo, file_lo + n_local)``) and the GLOBAL file table
+    (``file_ds``, ``file_ids``). Returns the hybrid ``ChunkerIndex``: global
+    keys, blocks and per-key totals, this rank's intervals (csrc/shard.cu).
+    Exchange: one all-gather of key lists (tiny) and one of block tables."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+    from .index import ChunkerIndex, build_index_from_catalog
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    codec = local_catalog.codec
+    layout = np.array([codec.key_bits, *codec.shift, *codec.width], dtype=np.int64)
+    lay, _ = all_gather_rows(torch.from_numpy(layout).view(1, -1), group)
+    if not bool((lay == lay[0]).all()):
+        raise ValueError("ranks disagree on the packed-key layout: build every shard's DeviceCatalog with the "
+                         "same vocabulary and parallel.global_nullable() flags")
+    local = build_index_from_catalog(local_catalog, predicates, stream=stream)
+    L = _lib.lib()
+    dev = local_catalog.device
+    packed = np.zeros(local.n_keys, np.uint32)
+    _lib.check(L.mx_index_packed_keys(local.handle, _lib.ptr(packed)))
+    keys, kcounts = all_gather_rows(torch.from_numpy(packed.astype(np.int64)), group)
+    gkeys = np.unique(np.concatenate([keys[q, : kcounts[q]].numpy() for q in range(world)])).astype(np.uint32)
+    rows = torch.empty((max(local.n_blocks, 1), 4), dtype=torch.int32, device=dev)
+    if local.n_blocks:
+        _lib.check(L.mx_index_block_table(local.handle, int(file_lo), rows.data_ptr(),
+                                          C.c_void_p(_lib.stream_ptr(stream))))
+    tables, counts = all_gather_rows(rows[: local.n_blocks], group)
+    tables = tables.contiguous()
+    file_ds = np.ascontiguousarray(file_ds, dtype=np.int32)
+    file_ids = np.ascontiguousarray(file_ids, dtype=np.int64)
+    counts_np = np.asarray(counts, dtype=np.int64)
+    d = _lib.ShardDesc()
+    P = C.POINTER
+    d.world, d.rank = world, rank
+    d.file_lo, d.file_hi = int(file_lo), int(file_lo) + local_catalog.host.n_files
+    d.n_files = len(file_ids)
+    d.file_ds = file_ds.ctypes.data_as(P(C.c_int32))
+    d.file_ids = file_ids.ctypes.data_as(P(C.c_int64))
+    d.tables = tables.data_ptr()
+    d.counts = counts_np.ctypes.data_as(P(C.c_int64))
+    d.cap = tables.shape[1]
+    d.global_keys = gkeys.ctypes.data_as(P(C.c_uint32))
+    d.n_global_keys = len(gkeys)
+    out = C.c_void_p()
+    _lib.check(L.mx_index_build_sharded(local.handle, C.byref(d), C.c_void_p(_lib.stream_ptr(stream)),
+                                        C.byref(out)))
+    idx = ChunkerIndex(out.value, local_catalog, stream)
+    idx.shard = ShardInfo(world, rank, group, d.file_lo, d.file_hi, file_ds, file_ids)
+    idx.local_index = local
+    return idx
+
+
+def _max_allreduce(arr: np.ndarray, group, device) -> np.ndarray:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int64)).to(_coll_device(group, device))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t.cpu().numpy()
+
+
+class MergedChunkBatch:
+    """Global chunk CSR (every rank's pieces interleaved into the reference's
+    (mixture key, file, start) order); identical on every rank."""
+
+    def __init__(self, local_batch, off, pieces, file_ds, file_ids):
+        self.__dict__.update({k: v for k, v in local_batch.__dict__.items() if not k.startswith("_")})
+        self._gen = local_batch._gen
+        self._off, self._pieces = off, pieces
+        self._file_ds, self._file_ids = file_ds, file_ids
+        self.n_ranges = int(pieces.shape[1])
+        self._host = None
+
+    def to_host(self) -> dict:
+        from . import _lib
+
+        if self._host is None:
+            n = self.n_chunks
+            ids, seeds = np.zeros(n, np.int64), np.zeros(n, np.uint64)
+            loc_off = np.zeros(n + 1, np.int64)
+            _lib.check(_lib.lib().mx_gen_result_copy(self._gen._h, _lib.ptr(loc_off), _lib.ptr(ids),
+                                                     _lib.ptr(seeds), 0, 0, 0, 0, 0))
+            p = self._pieces.cpu().numpy().view(np.uint32)
+            fidx = p[1].astype(np.int64)
+            self._host = dict(off=self._off.cpu().numpy(), ids=ids, seeds=seeds, mkey=p[0].copy(),
+                              ds=self._file_ds[fidx], fid=self._file_ids[fidx], start=p[2].copy(), end=p[3].copy())
+        return self._host
+
+    def chunk(self, i: int):
+        from .chunks import ChunkBatch
+
+        return ChunkBatch.chunk(self, i)
+
+
+def merge_batch(gen, batch, stream=None):
+    """Collective: all-gather every rank's local chunk CSR of the same chunks
+    and interleave them on the device (mx_chunks_merge)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+
+    sh = gen.index.shard
+    dev = gen.index.catalog.device
+    L = _lib.lib()
+    n, r = batch.n_chunks, batch.n_ranges
+    off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    pieces = torch.empty((max(r, 1), 4), dtype=torch.int32, device=dev)
+    cols = pieces.t().contiguous() if r else torch.empty((4, 1), dtype=torch.int32, device=dev)
+    sp = C.c_void_p(_lib.stream_ptr(stream))
+    _lib.check(L.mx_gen_result_export(gen._h, off.data_ptr(), *(cols[f].data_ptr() for f in range(4)), sp))
+    offs, _ = all_gather_rows(off.view(1, -1), sh.group)  # [W, 1, n+1]
+    offs = offs.view(sh.world, n + 1).contiguous()
+    g, counts = all_gather_rows(cols.t()[:r].contiguous(), sh.group)  # [W, cap, 4]
+    cap = g.shape[1]
+    g4 = g.permute(2, 0, 1).contiguous()  # [4, W, cap]
+    total = int(sum(counts))
+    out_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    out = torch.empty((4, max(total, 1)), dtype=torch.int32, device=dev)
+    _lib.check(L.mx_chunks_merge(sh.world, n, cap, offs.data_ptr(), *(g4[f].data_ptr() for f in range(4)),
+                                 out_off.data_ptr(), *(out[f].data_ptr() for f in range(4)), sp))
+    return MergedChunkBatch(batch, out_off, out[:, :total], sh.file_ds, sh.file_ids)
