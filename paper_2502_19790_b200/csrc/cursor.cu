@@ -61,21 +61,25 @@ __global__ void key_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix
   seeds[k] = b.seed63();
 }
 
-constexpr int CS_WARPS = 4;
-constexpr int CS_LCAP = 1536;
+// Per-warp shared memory: MT state + outputs + window pairs + the key's block
+// list (list_cap entries; a key with more blocks shuffles in global memory).
+constexpr int CS_FIXED = 2 * MT_N + 64;
 
-__global__ void __launch_bounds__(CS_WARPS * 32)
+__global__ void __launch_bounds__(128)
 cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file, const int32_t* file_ds,
-                      const u64* seeds, const u32* mt_base, u32* grp, u32* gid, u32* cur_blk) {
-  __shared__ u32 s_mt[CS_WARPS][MT_N];
-  __shared__ u32 s_out[CS_WARPS][MT_N];
-  __shared__ u32 s_list[CS_WARPS][CS_LCAP];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (long long k = blockIdx.x * (long long)CS_WARPS + w; k < K; k += (long long)gridDim.x * CS_WARPS) {
+                      const u64* seeds, const u32* mt_base, u32* grp, u32* gid, u32* cur_blk, int list_cap) {
+  extern __shared__ __align__(16) u32 cs_dyn[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpc = blockDim.x >> 5;
+  u32* mine = cs_dyn + (size_t)w * (CS_FIXED + list_cap);
+  u32* s_mt = mine;
+  u32* s_out = mine + MT_N;
+  uint2* s_pairs = reinterpret_cast<uint2*>(mine + 2 * MT_N);
+  u32* s_list = mine + CS_FIXED;
+  for (long long k = blockIdx.x * (long long)wpc + w; k < K; k += (long long)gridDim.x * wpc) {
     const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
     const int nb = (int)(b1 - b0);
-    const bool in_smem = nb <= CS_LCAP;
-    u32* work = in_smem ? s_list[w] : cur_blk + b0;
+    const bool in_smem = nb <= list_cap;
+    u32* work = in_smem ? s_list : cur_blk + b0;
     // dataset groups (blocks are file-sorted and ds is nondecreasing in file
     // order): one group when first and last block share a dataset, else a
     // warp-parallel scan of dataset changes
@@ -103,7 +107,7 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
       for (int i = lane; i < nb; i += 32) work[i] = b0 + (u32)i;
     }
     __syncwarp();
-    WarpMT mt{s_mt[w], s_out[w], MT_N};
+    WarpMT mt{s_mt, s_out, s_pairs, MT_N};
     mt.seed(mt_base, seeds[k]);
     mt.shuffle(gid + b0, G);  // dataset order (one stream for the whole key)
     int pos = 0;
@@ -120,9 +124,17 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
     }
     __syncwarp();
     if (in_smem)
-      for (int i = lane; i < nb; i += 32) cur_blk[b0 + i] = s_list[w][i];
+      for (int i = lane; i < nb; i += 32) cur_blk[b0 + i] = s_list[i];
     __syncwarp();
   }
+}
+
+__global__ void max_blocks_kernel(long long K, const u32* key_blk_first, u32* out) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  u32 v = k < K ? key_blk_first[k + 1] - key_blk_first[k] : 0u;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v = max(v, __shfl_xor_sync(MX_FULL, v, d));
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
 }
 
 // civ: interval ids in cursor order; key k keeps its sorted-order index range
@@ -209,11 +221,13 @@ constexpr int CO_SMEM = 8192;
 // one warp: shuffle of the K component ranks (chunks.py:139-141)
 __global__ void __launch_bounds__(32) component_order_kernel(long long K, u64 seed, const u32* mt_base, u32* order) {
   __shared__ u32 s_mt[MT_N], s_out[MT_N];
+  __shared__ uint2 s_pairs[32];
   __shared__ u32 s_ord[CO_SMEM];
   const int lane = threadIdx.x;
   u32* x = K <= CO_SMEM ? s_ord : order;
   for (long long i = lane; i < K; i += 32) x[i] = (u32)i;
-  WarpMT mt{s_mt, s_out, MT_N};
+  __syncwarp();
+  WarpMT mt{s_mt, s_out, s_pairs, MT_N};
   mt.seed(mt_base, seed);
   mt.shuffle(x, (int)K);
   if (x != order)
@@ -274,11 +288,25 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   MX_CUDA_TRY(g->cur_blk.alloc(B, s));
   {
     MxPhase ph2("cursor_shuffle", s);
-    long long blocks = (K + CS_WARPS - 1) / CS_WARPS;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    cursor_shuffle_kernel<<<(unsigned)blocks, CS_WARPS * 32, 0, s>>>(K, ix->key_blk_first.p, ix->blk_file.p,
-                                                                   ix->file_ds.p, seeds.p, mt_base.p, grp.p,
-                                                                   gid.p, g->cur_blk.p);
+    // list capacity = the largest key's block count (up to 16K entries, 64 KB)
+    DevBuf<u32> mx_nb;
+    MX_CUDA_TRY(mx_nb.alloc(1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(mx_nb.p, 0, sizeof(u32), s));
+    max_blocks_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, mx_nb.p);
+    mx_count_launch();
+    u32 h_nb = 0;
+    MX_CUDA_TRY(cudaMemcpyAsync(&h_nb, mx_nb.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    MX_CUDA_TRY(cudaStreamSynchronize(s));
+    const int cap = (int)std::min<u32>((h_nb + 31) / 32 * 32, 16384);
+    const size_t per_warp = sizeof(u32) * (CS_FIXED + cap);
+    const int wpc = per_warp <= 12 * 1024 ? 4 : 1;
+    const size_t dyn = per_warp * wpc;
+    MX_CUDA_TRY(cudaFuncSetAttribute(cursor_shuffle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    long long blocks = (K + wpc - 1) / wpc;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    cursor_shuffle_kernel<<<(unsigned)blocks, wpc * 32, dyn, s>>>(K, ix->key_blk_first.p, ix->blk_file.p,
+                                                                ix->file_ds.p, seeds.p, mt_base.p, grp.p, gid.p,
+                                                                g->cur_blk.p, cap);
     mx_count_launch();
   }
   MX_CUDA_TRY(g->civ.alloc(I, s));

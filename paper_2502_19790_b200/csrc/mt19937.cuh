@@ -91,43 +91,75 @@ struct MT {
 // ---------------------------------------------------------------------------
 // Warp-cooperative form of the same generator (bit-identical output).
 //  * seeding: init_genrand(19650218) is seed-independent, so it comes from a
-//    precomputed table (`base`); init_by_array's recurrence runs on lane 0
-//    with the previous word in a register (the old words are plain loads);
+//    precomputed table (`base`); init_by_array's sequential recurrence runs
+//    on EVERY lane in lockstep, 32 old words at a time loaded lane-parallel
+//    and broadcast by shuffles, so only the xor-shift-multiply chain is on
+//    the critical path (no shared-memory round trip per step);
 //  * generation: the twist is split into three data-parallel ranges
 //    ([0,227) reads only old words, [227,454) reads words of the first range,
 //    [454,623) of the second, then word 623) and tempered into `out`;
-//  * consumption (rejection sampling + Fisher-Yates swaps) stays on lane 0,
-//    reading the 624-output buffer; the warp refills it when drained.
+//  * rejection sampling is resolved 32 draws at a time: lane l takes output
+//    pos+l and the number A_l of accepted draws before it (which fixes the
+//    bound i - A_l + 1 it is tested against) is found by fixed-point
+//    iteration of A = prefix_popcount(accept(A)) -- after s rounds lanes
+//    0..s are exact, and a fixed point IS the sequential answer;
+//  * the Fisher-Yates swaps of the accepted draws run on lane 0 from a
+//    shared-memory pair list with the next pair prefetched.
 struct WarpMT {
   uint32_t* s;    // state [624]
   uint32_t* out;  // tempered outputs [624]
+  uint2* pairs;   // [32] accepted (i, j) of one window
   int pos;        // next unread output (624 = drained)
+
+  template <typename F>
+  __device__ __forceinline__ uint32_t chain(int a0, int a1, uint32_t prev, F f) {  // s[a] = f(s[a], prev, a)
+    const int lane = threadIdx.x & 31;
+    for (int b = a0; b < a1; b += 32) {
+      const int a = b + lane;
+      const uint32_t mine = a < a1 ? s[a] : 0u;
+      uint32_t res = 0;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const uint32_t sv = __shfl_sync(0xffffffffu, mine, t);
+        if (b + t < a1) {
+          prev = f(sv, prev, b + t);
+          if (lane == t) res = prev;
+        }
+      }
+      if (a < a1) s[a] = res;
+    }
+    __syncwarp();
+    return prev;
+  }
 
   __device__ void seed(const uint32_t* base, unsigned long long seed_v) {
     const int lane = threadIdx.x & 31;
     for (int k = lane; k < MT_N; k += 32) s[k] = base[k];
     __syncwarp();
-    if (lane == 0) {
-      uint32_t key[2] = {(uint32_t)seed_v, (uint32_t)(seed_v >> 32)};
-      const int klen = (seed_v >> 32) ? 2 : 1;
-      int a = 1, b = 0;
-      uint32_t prev = s[0];
-      for (int k = MT_N > klen ? MT_N : klen; k; --k) {
-        const uint32_t v = (s[a] ^ ((prev ^ (prev >> 30)) * 1664525u)) + key[b] + (uint32_t)b;
-        s[a] = v;
-        prev = v;
-        ++a; ++b;
-        if (a >= MT_N) { s[0] = s[MT_N - 1]; prev = s[0]; a = 1; }
-        if (b >= klen) b = 0;
-      }
-      for (int k = MT_N - 1; k; --k) {
-        const uint32_t v = (s[a] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)a;
-        s[a] = v;
-        prev = v;
-        ++a;
-        if (a >= MT_N) { s[0] = s[MT_N - 1]; prev = s[0]; a = 1; }
-      }
-      s[0] = 0x80000000u;
+    const uint32_t key0 = (uint32_t)seed_v, key1 = (uint32_t)(seed_v >> 32);
+    const bool two = key1 != 0;  // klen = 2
+    auto f1 = [&](uint32_t sv, uint32_t prev, int a) {  // iteration k = a - 1, b = k % klen
+      const uint32_t b = two ? (uint32_t)((a - 1) & 1) : 0u;
+      return (sv ^ ((prev ^ (prev >> 30)) * 1664525u)) + (b ? key1 : key0) + b;
+    };
+    auto f2 = [](uint32_t sv, uint32_t prev, int a) {
+      return (sv ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)a;
+    };
+    uint32_t prev = chain(1, MT_N, base[0], f1);  // init_by_array loop 1, a = 1..623
+    // wrap (s[0] = s[623]), then iteration 623 at a = 1 (b = 623 % klen)
+    {
+      const uint32_t b = two ? 1u : 0u;
+      const uint32_t v = (s[1] ^ ((prev ^ (prev >> 30)) * 1664525u)) + (b ? key1 : key0) + b;
+      __syncwarp();
+      if (lane == 0) { s[0] = prev; s[1] = v; }
+      prev = v;
+      __syncwarp();
+    }
+    prev = chain(2, MT_N, prev, f2);  // loop 2, a = 2..623
+    {
+      const uint32_t v = (s[1] ^ ((prev ^ (prev >> 30)) * 1566083941u)) - 1u;  // wrap, a = 1
+      __syncwarp();
+      if (lane == 0) { s[1] = v; s[0] = 0x80000000u; }
     }
     pos = MT_N;
     __syncwarp();
@@ -172,30 +204,49 @@ struct WarpMT {
     __syncwarp();
   }
 
-  // random.shuffle(x[0..n)) by the whole warp (lane 0 swaps)
+  // random.shuffle(x[0..n)) by the whole warp
   template <typename T>
   __device__ void shuffle(T* x, int n) {
     const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
     int i = n - 1;
     while (i >= 1) {
       if (pos >= MT_N) refill();
-      if (lane == 0) {
-        int p = pos;
-        while (i >= 1 && p < MT_N) {
-          const uint32_t bound = (uint32_t)(i + 1);
-          const int kb = 32 - __clz(bound);
-          const uint32_t r = out[p++] >> (32 - kb);
-          if (r < bound) {
-            const T t = x[i];
-            x[i] = x[r];
-            x[r] = t;
-            --i;
-          }
+      const bool valid = pos + lane < MT_N;
+      const uint32_t u = valid ? out[pos + lane] : 0u;
+      uint32_t A = 0, acc_mask, act_mask, r = 0;
+      for (;;) {  // fixed point: A = accepted draws before this lane
+        const int ii = i - (int)A;
+        const bool active = valid && ii >= 1;
+        bool acc = false;
+        if (active) {
+          const uint32_t bound = (uint32_t)ii + 1u;
+          r = u >> __clz(bound);  // getrandbits(bound.bit_length())
+          acc = r < bound;
         }
-        pos = p;
+        acc_mask = __ballot_sync(0xffffffffu, acc);
+        const uint32_t A2 = __popc(acc_mask & lt);
+        if (__all_sync(0xffffffffu, A2 == A)) {
+          act_mask = __ballot_sync(0xffffffffu, active);
+          if (acc) pairs[A] = make_uint2((uint32_t)ii, r);
+          break;
+        }
+        A = A2;
       }
-      i = __shfl_sync(0xffffffffu, i, 0);
-      pos = __shfl_sync(0xffffffffu, pos, 0);
+      const int m = __popc(acc_mask);
+      __syncwarp();
+      if (lane == 0 && m > 0) {
+        uint2 nx = pairs[0];
+        for (int k = 0; k < m; ++k) {
+          const uint2 cu = nx;
+          if (k + 1 < m) nx = pairs[k + 1];
+          const T a = x[cu.x], b = x[cu.y];
+          x[cu.x] = b;
+          x[cu.y] = a;
+        }
+      }
+      pos += __popc(act_mask);
+      i -= m;
       __syncwarp();
     }
   }

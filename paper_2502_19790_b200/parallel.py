@@ -187,7 +187,21 @@ def build_sharded_index(local_catalog, predicates=(), file_lo: int = 0, file_ds=
         _lib.check(L.mx_index_block_table(local.handle, int(file_lo), rows.data_ptr(),
                                           C.c_void_p(_lib.stream_ptr(stream))))
     tables, counts = all_gather_rows(rows[: local.n_blocks], group)
-    tables = tables.contiguous()
+    return hybrid_index(local, local_catalog, tables.contiguous(), counts, gkeys, file_lo, file_ds, file_ids,
+                        world, rank, group, stream)
+
+
+def hybrid_index(local, local_catalog, tables, counts, gkeys, file_lo, file_ds, file_ids, world, rank,
+                 group=None, stream=None):
+    """The hybrid ChunkerIndex from already-exchanged block tables
+    (device int32 [world, cap, 4]), per-rank row counts and the sorted global
+    key union (mx_index_build_sharded)."""
+    import ctypes as C
+
+    from . import _lib
+    from .index import ChunkerIndex
+
+    L = _lib.lib()
     file_ds = np.ascontiguousarray(file_ds, dtype=np.int32)
     file_ids = np.ascontiguousarray(file_ids, dtype=np.int64)
     counts_np = np.asarray(counts, dtype=np.int64)

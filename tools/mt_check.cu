@@ -20,12 +20,13 @@ __global__ void ref_kernel(const unsigned long long* seeds, int n, uint32_t* out
 
 __global__ void warp_kernel(const unsigned long long* seeds, int n, const uint32_t* base, uint32_t* out) {
   __shared__ uint32_t st[4][MT_N], buf[4][MT_N];
+  __shared__ uint2 pairs[4][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * 4 + w;
   uint32_t* x = out + (long long)b * n;
   for (int i = lane; i < n; i += 32) x[i] = i;
   __syncwarp();
-  WarpMT mt{st[w], buf[w], MT_N};
+  WarpMT mt{st[w], buf[w], pairs[w], MT_N};
   mt.seed(base, seeds[b]);
   mt.shuffle(x, 1);
   mt.shuffle(x, n);
@@ -33,9 +34,9 @@ __global__ void warp_kernel(const unsigned long long* seeds, int n, const uint32
 
 int main() {
   const int B = 64;
-  for (int n : {2, 3, 20, 700, 2000}) {
+  for (int n : {2, 3, 20, 700, 2000, 6000, 70000}) {
     std::vector<unsigned long long> seeds(B);
-    for (int i = 0; i < B; ++i) seeds[i] = 0x9e3779b97f4a7c15ull * (i + 1) >> 1;
+    for (int i = 0; i < B; ++i) seeds[i] = i % 2 ? 0x9e3779b97f4a7c15ull * (i + 1) >> 1 : 12345ull * i + 7;
     unsigned long long* ds;
     uint32_t *o1, *o2, *base;
     cudaMalloc(&ds, 8 * B);

@@ -54,8 +54,18 @@ def main(rep):
             d["dram_gbs"] = d["dram_bytes_per_launch"] / d["duration"] / 1e9
         out.append(d)
     sass = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--csv", "--print-source", "sass"))))
-    if len(sass) > 2:
-        h, data = sass[1], sass[2:]
+    # one section per profiled kernel: a "Kernel Name" row, a header row, data rows
+    sections, cur = [], None
+    for r in sass:
+        if r and r[0] == "Kernel Name":
+            cur = {"h": None, "rows": []}
+            sections.append(cur)
+        elif cur is not None and cur["h"] is None:
+            cur["h"] = r
+        elif cur is not None and len(r) == len(cur["h"]):
+            cur["rows"].append(r)
+    for k, sec in enumerate(sections[: len(out)]):
+        h, data = sec["h"], sec["rows"]
         si, ie, src = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed"), h.index("Source")
         mix, stall = collections.Counter(), collections.Counter()
         for r in data:
@@ -66,10 +76,10 @@ def main(rep):
             mix[op] += int(r[ie] or 0)
             stall[op] += int(r[si] or 0)
         ti, ts = max(sum(mix.values()), 1), max(sum(stall.values()), 1)
-        out[0]["sass_mix_pct"] = {k: round(100 * v / ti, 1) for k, v in mix.most_common(16)}
-        out[0]["stall_share_pct_by_opcode"] = {k: round(100 * v / ts, 1) for k, v in stall.most_common(10)}
+        out[k]["sass_mix_pct"] = {o: round(100 * v / ti, 1) for o, v in mix.most_common(16)}
+        out[k]["stall_share_pct_by_opcode"] = {o: round(100 * v / ts, 1) for o, v in stall.most_common(10)}
         top = sorted(data, key=lambda r: -int(r[si] or 0))[:8]
-        out[0]["top_stall_instructions"] = [f"{r[si]} samples: {r[src].strip()}" for r in top]
+        out[k]["top_stall_instructions"] = [f"{r[si]} samples: {r[src].strip()}" for r in top]
     print(json.dumps(out, indent=1))
 
 

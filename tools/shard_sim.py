@@ -1,0 +1,129 @@
+"""Per-rank device cost of the file-sharded pipeline at N ranks, on ONE GPU.
+
+Builds the N ranks' local indexes (bench workload, 100M samples each at
+--scale 1), then replays every rank's hybrid build, generator, plan and the
+root merge sequentially, timing each with CUDA events. Collectives are
+replaced by in-memory concatenation (their NVLink cost is estimated from the
+bytes printed). Usage: python tools/shard_sim.py --world 8 [--scale 1.0]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import bench  # noqa: E402
+from paper_2502_19790_b200 import ChunkGenerator, DeviceCatalog, _lib, build_index_from_catalog, synth  # noqa: E402
+from paper_2502_19790_b200.catalog import ColumnarCatalog  # noqa: E402
+from paper_2502_19790_b200.parallel import hybrid_index  # noqa: E402
+
+
+def timed(fn):
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    a.record()
+    out = fn()
+    b.record()
+    torch.cuda.synchronize()
+    return out, a.elapsed_time(b), (time.perf_counter() - t0) * 1e3
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--world", type=int, default=8)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--ranks", default="0", help="comma list of ranks to time (all are run)")
+    args = ap.parse_args()
+    W = args.world
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    L = _lib.lib()
+    spec = synth.cfg2_mixture(bench.CFG["chunk_size"])
+    locs = []
+    for q in range(W):
+        rt = bench.make_workload(q, args.scale)
+        meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
+        cols = bench.device_columns(rt, dev)
+        dcat = DeviceCatalog(meta, columns=cols, nullable={p: False for p in cols})
+        idx, ms, _ = timed(lambda: build_index_from_catalog(dcat, []))
+        nf = len(rt.file_sizes)
+        rows = torch.empty((max(idx.n_blocks, 1), 4), dtype=torch.int32, device=dev)
+        _lib.check(L.mx_index_block_table(idx.handle, q * nf, rows.data_ptr(), C.c_void_p(_lib.stream_ptr())))
+        packed = np.zeros(idx.n_keys, np.uint32)
+        _lib.check(L.mx_index_packed_keys(idx.handle, _lib.ptr(packed)))
+        dcat.columns = {p: c[:0] for p, c in dcat.columns.items()}  # free the 2 GB of columns
+        del cols
+        locs.append(dict(idx=idx, dcat=dcat, rows=rows[: idx.n_blocks], packed=packed, nf=nf, stage1_ms=ms))
+        torch.cuda.empty_cache()
+    counts = [len(x["rows"]) for x in locs]
+    cap = max(counts)
+    tables = torch.zeros((W, cap, 4), dtype=torch.int32, device=dev)
+    for q, x in enumerate(locs):
+        tables[q, : counts[q]] = x["rows"]
+    gkeys = np.unique(np.concatenate([x["packed"] for x in locs])).astype(np.uint32)
+    nf = locs[0]["nf"]
+    file_ds, file_ids = np.zeros(W * nf, np.int32), np.arange(1, W * nf + 1, dtype=np.int64)
+    report = {"world": W, "samples_per_rank": int(locs[0]["idx"].n_samples), "block_rows": counts,
+              "table_allgather_bytes": int(W * cap * 16), "stage1_ms": [round(x["stage1_ms"], 3) for x in locs]}
+    timed_ranks = {int(r) for r in args.ranks.split(",")}
+    results = []
+    per_rank = {}
+    for r, x in enumerate(locs):
+        L.mx_profile_reset()
+        L.mx_profile_enable(1)
+        hyb, t_h, _ = timed(lambda: hybrid_index(x["idx"], x["dcat"], tables, counts, gkeys, r * nf, file_ds,
+                                                  file_ids, W, r))
+        del hyb.shard  # no collectives here: keep the local result
+        gen, t_g, _ = timed(lambda: ChunkGenerator(hyb, bench.CFG["job_seed"]))
+        batch, t_p, _ = timed(lambda: gen.plan_batch(spec, 1 << 40))
+        L.mx_profile_enable(0)
+        phases = {p: round(_lib.profile_read(p)[0], 4) for p in ("index_scans", "cursor_layout", "cursor_shuffle",
+                                                                 "plan", "emit")}
+        n, rr = batch.n_chunks, batch.n_ranges
+        off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        cols4 = torch.empty((4, max(rr, 1)), dtype=torch.int32, device=dev)
+        _lib.check(L.mx_gen_result_export(gen._h, off.data_ptr(), *(cols4[f].data_ptr() for f in range(4)),
+                                          C.c_void_p(_lib.stream_ptr())))
+        results.append((off, cols4[:, :rr], rr))
+        if r in timed_ranks:
+            per_rank[r] = {"hybrid_intervals": hyb.n_intervals, "hybrid_ms": round(t_h, 3),
+                           "gen_create_ms": round(t_g, 3), "plan_emit_ms": round(t_p, 3), "phases_ms": phases,
+                           "chunks": n, "local_pieces": rr}
+        del gen, hyb, batch
+    report["ranks"] = per_rank
+    # root merge of the N local CSRs
+    n = results[0][0].numel() - 1
+    capr = max(max(x[2] for x in results), 1)
+    offs = torch.stack([x[0] for x in results]).contiguous()
+    g4 = torch.zeros((4, W, capr), dtype=torch.int32, device=dev)
+    for q, (_, c4, rr) in enumerate(results):
+        g4[:, q, :rr] = c4
+    total = sum(x[2] for x in results)
+    out_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    out = torch.empty((4, max(total, 1)), dtype=torch.int32, device=dev)
+
+    def merge():
+        _lib.check(L.mx_chunks_merge(W, n, capr, offs.data_ptr(), *(g4[f].data_ptr() for f in range(4)),
+                                     out_off.data_ptr(), *(out[f].data_ptr() for f in range(4)),
+                                     C.c_void_p(_lib.stream_ptr())))
+
+    merge()
+    _, t_m, _ = timed(merge)
+    report.update(merge_ms=round(t_m, 3), global_pieces=int(total), pieces_allgather_bytes=int(W * capr * 16),
+                  global_chunks=int(n))
+    print(json.dumps(report))
+
+
+if __name__ == "__main__":
+    main()
