@@ -27,7 +27,7 @@ bit 31 of an entry marks a code that fails the conjunctive filter
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -54,9 +54,29 @@ class KeyCodec:
     count_shift: int  # -1 if no nullable property
     key_bits: int
     rank_mask: int
+    # derived tables, computed once per codec (a catalog serves many jobs)
+    _memo: dict = field(default_factory=dict, repr=False, compare=False)
+
+    _built = None  # class-level cache of build(): signature -> KeyCodec
 
     @staticmethod
     def build(vocab: dict, nullable: dict) -> "KeyCodec":
+        props = sorted(vocab)
+        sig = (tuple((p, tuple(_as_tuple(v) for v in vocab[p])) for p in props),
+               tuple(bool(nullable.get(p, True)) for p in props))
+        if KeyCodec._built is None:
+            KeyCodec._built = {}
+        hit = KeyCodec._built.get(sig)
+        if hit is not None:
+            return hit
+        codec = KeyCodec._build(vocab, nullable)
+        if len(KeyCodec._built) > 64:
+            KeyCodec._built.clear()
+        KeyCodec._built[sig] = codec
+        return codec
+
+    @staticmethod
+    def _build(vocab: dict, nullable: dict) -> "KeyCodec":
         props = sorted(vocab)
         sorted_values, code_rank = [], []
         for p in props:
@@ -95,6 +115,14 @@ class KeyCodec:
     # ---------------------------------------------------------------- LUTs
     def luts(self, cat: ColumnarCatalog, preds: list[FilterPredicate]) -> tuple[np.ndarray, np.ndarray]:
         """Concatenated per-property LUT (entry code+1) and its offsets."""
+        key = ("luts", tuple(preds), tuple(sorted(cat.multiple.items())))
+        hit = self._memo.get(key)
+        if hit is None:
+            hit = self._luts(cat, preds)
+            self._memo[key] = hit
+        return hit
+
+    def _luts(self, cat: ColumnarCatalog, preds: list[FilterPredicate]) -> tuple[np.ndarray, np.ndarray]:
         parts, offs = [], [0]
         for j, p in enumerate(self.props):
             ok = cat.pass_table(p, preds)
@@ -125,6 +153,13 @@ class KeyCodec:
 
     def key_strings(self) -> tuple[bytes, np.ndarray, np.ndarray]:
         """Canonical-string pieces "esc(prop):esc(v1),esc(v2)" per (prop, rank)."""
+        hit = self._memo.get("key_strings")
+        if hit is None:
+            hit = self._key_strings()
+            self._memo["key_strings"] = hit
+        return hit
+
+    def _key_strings(self) -> tuple[bytes, np.ndarray, np.ndarray]:
         blobs, offs, base = [], [0], []
         for j, p in enumerate(self.props):
             base.append(len(blobs))
@@ -139,6 +174,16 @@ class KeyCodec:
         """Per mixture key, per property, bit r = a component holding value
         rank r there matches on that property (rank 0 = null -> property not
         shared -> vacuously true; ``mixtures.py:100-109``)."""
+        key = ("allow", tuple(k.entries for k in mkeys))
+        hit = self._memo.get(key)
+        if hit is None:
+            hit = self._allow_table(mkeys)
+            if len(self._memo) > 256:
+                self._memo.clear()
+            self._memo[key] = hit
+        return hit
+
+    def _allow_table(self, mkeys: list[MixtureKey]) -> tuple[np.ndarray, np.ndarray, int]:
         base, at = [], 0
         for j in range(len(self.props)):
             base.append(at)

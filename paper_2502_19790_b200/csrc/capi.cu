@@ -41,6 +41,65 @@ static std::vector<PendingPhase> g_pending;
 
 void mx_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// Host->device copies of small host arrays (LUTs, mixture tables, sentinels)
+// go through a per-thread pinned staging ring: a cudaMemcpyAsync from
+// PAGEABLE memory synchronises the stream before it starts, which would
+// drain the GPU pipeline at every upload. The ring has two halves; a half is
+// reused only after the events recorded behind its copies have completed.
+namespace {
+struct PinnedRing {
+  static constexpr size_t kHalf = 2u << 20;
+  char* buf = nullptr;
+  int half = 0;
+  size_t used = 0;
+  std::vector<cudaEvent_t> pending[2], pool;
+  ~PinnedRing() {
+    for (int h = 0; h < 2; ++h)
+      for (cudaEvent_t e : pending[h]) cudaEventDestroy(e);
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    if (buf) cudaFreeHost(buf);
+  }
+};
+thread_local PinnedRing g_ring;
+}  // namespace
+
+cudaError_t mx_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  PinnedRing& r = g_ring;
+  const size_t need = (bytes + 255) & ~size_t(255);
+  if (need > PinnedRing::kHalf) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  if (!r.buf) {
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&r.buf), 2 * PinnedRing::kHalf, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      r.buf = nullptr;
+      return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+    }
+  }
+  if (r.used + need > PinnedRing::kHalf) {  // switch halves; wait for the other half's copies
+    r.half ^= 1;
+    r.used = 0;
+    for (cudaEvent_t e : r.pending[r.half]) {
+      cudaEventSynchronize(e);
+      r.pool.push_back(e);
+    }
+    r.pending[r.half].clear();
+  }
+  char* stage = r.buf + (size_t)r.half * PinnedRing::kHalf + r.used;
+  r.used += need;
+  memcpy(stage, src, bytes);
+  cudaError_t e = cudaMemcpyAsync(dst, stage, bytes, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t ev;
+  if (!r.pool.empty()) {
+    ev = r.pool.back();
+    r.pool.pop_back();
+  } else if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) {
+    return e;
+  }
+  r.pending[r.half].push_back(ev);
+  return cudaEventRecord(ev, s);
+}
+
 // Keep memory freed with cudaFreeAsync cached in the device's default pool
 // (the default release threshold of 0 hands it back to the driver at every
 // synchronisation, which makes each job re-map gigabytes of HBM).
@@ -171,10 +230,9 @@ int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out) {
     cudaError_t e = d.str_off.alloc(n_pieces + 1, s);
     if (e == cudaSuccess) e = d.str_bytes.alloc(nbytes > 0 ? nbytes : 1, s);
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(d.str_off.p, desc->key_string_offsets, sizeof(long long) * (n_pieces + 1),
-                          cudaMemcpyHostToDevice, s);
+      e = mx_h2d(d.str_off.p, desc->key_string_offsets, sizeof(long long) * (n_pieces + 1), s);
     if (e == cudaSuccess && nbytes > 0)
-      e = cudaMemcpyAsync(d.str_bytes.p, desc->key_strings, nbytes, cudaMemcpyHostToDevice, s);
+      e = mx_h2d(d.str_bytes.p, desc->key_strings, nbytes, s);
     if (e != cudaSuccess) rc = mx_fail_cuda(e, "key strings", __FILE__, __LINE__);
   }
   if (rc == MX_OK) rc = stage1_build(desc, s, &d);
@@ -201,14 +259,7 @@ int mx_index_sizes(const mx_index* index, int64_t* n_keys, int64_t* n_blocks, in
   if (n_keys) *n_keys = d.n_keys;
   if (n_blocks) *n_blocks = d.n_blocks;
   if (n_intervals) *n_intervals = d.n_intervals;
-  if (n_samples) {
-    unsigned long long t = 0;
-    if (d.n_intervals > 0) {
-      cudaError_t e = cudaMemcpy(&t, d.iv_cum.p + d.n_intervals, sizeof(t), cudaMemcpyDeviceToHost);
-      if (e != cudaSuccess) return mx_fail_cuda(e, "sizes", __FILE__, __LINE__);
-    }
-    *n_samples = (int64_t)t;
-  }
+  if (n_samples) *n_samples = d.indexed_samples;
   return MX_OK;
 }
 
@@ -311,7 +362,7 @@ int mx_gen_create(mx_index* index, const uint8_t* cursor_prefix, int32_t cursor_
   int rc = MX_OK;
   cudaError_t e = g->d.chunk_prefix.alloc(chunk_prefix_len > 0 ? chunk_prefix_len : 1, s);
   if (e == cudaSuccess && chunk_prefix_len > 0)
-    e = cudaMemcpyAsync(g->d.chunk_prefix.p, chunk_prefix, chunk_prefix_len, cudaMemcpyHostToDevice, s);
+    e = mx_h2d(g->d.chunk_prefix.p, chunk_prefix, chunk_prefix_len, s);
   if (e != cudaSuccess) rc = mx_fail_cuda(e, "chunk prefix", __FILE__, __LINE__);
   g->d.chunk_prefix_len = chunk_prefix_len;
   if (rc == MX_OK) rc = cursor_build(&index->d, cursor_prefix, cursor_prefix_len, order_seed, s, &g->d);
@@ -598,6 +649,7 @@ int mx_gen_set_consumed(mx_gen* gen, const int64_t* consumed) {
   GenData& g = gen->d;
   const long long K = g.K;
   if (K == 0) return MX_OK;
+  if (int rc = gen_host_mirrors(&g)) return rc;
   for (long long k = 0; k < K; ++k)
     if (consumed[k] < 0 || (unsigned long long)consumed[k] > g.h_comp_total[k])
       return mx_fail(MX_ERR_INVALID, "consumed samples out of range for component %lld", k);
@@ -631,6 +683,7 @@ int mx_gen_set_cursors(mx_gen* gen, const int64_t* pos, const int64_t* offset) {
 
 int mx_gen_component_order(const mx_gen* gen, uint32_t* order) {
   MX_CHECK_ARG(gen && order, "null argument");
+  if (int rc = gen_host_mirrors(const_cast<GenData*>(&gen->d))) return rc;
   memcpy(order, gen->d.h_comp_order.data(), sizeof(u32) * gen->d.K);
   return MX_OK;
 }

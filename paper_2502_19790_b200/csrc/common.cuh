@@ -114,6 +114,9 @@ struct DevError {
 
 int mx_fail_cuda(cudaError_t e, const char* what, const char* file, int line);
 int mx_fail(int code, const char* fmt, ...);
+// stream-ordered upload of a (small) pageable host array through pinned
+// staging, without the implicit stream synchronisation of a pageable copy
+cudaError_t mx_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
 // Launch accounting and per-phase CUDA-event timing (capi.cu). A phase timer
 // records events on the launching stream when profiling is enabled

@@ -129,14 +129,6 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
   }
 }
 
-__global__ void max_blocks_kernel(long long K, const u32* key_blk_first, u32* out) {
-  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  u32 v = k < K ? key_blk_first[k + 1] - key_blk_first[k] : 0u;
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) v = max(v, __shfl_xor_sync(MX_FULL, v, d));
-  if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
-}
-
 // civ: interval ids in cursor order; key k keeps its sorted-order index range
 __global__ void __launch_bounds__(256)
 cursor_intervals_kernel(long long K, const u32* key_blk_first, const u32* blk_first, const u32* cur_blk, u32* civ) {
@@ -224,14 +216,20 @@ __global__ void __launch_bounds__(32) component_order_kernel(long long K, u64 se
   __shared__ uint2 s_pairs[32];
   __shared__ u32 s_ord[CO_SMEM];
   const int lane = threadIdx.x;
-  u32* x = K <= CO_SMEM ? s_ord : order;
-  for (long long i = lane; i < K; i += 32) x[i] = (u32)i;
+  const bool in_smem = K <= CO_SMEM;
+  for (long long i = lane; i < K; i += 32) {
+    if (in_smem) s_ord[i] = (u32)i;
+    else order[i] = (u32)i;
+  }
   __syncwarp();
   WarpMT mt{s_mt, s_out, s_pairs, MT_N};
   mt.seed(mt_base, seed);
-  mt.shuffle(x, (int)K);
-  if (x != order)
-    for (long long i = lane; i < K; i += 32) order[i] = x[i];
+  if (in_smem) {
+    mt.shuffle(s_ord, (int)K);
+    for (long long i = lane; i < K; i += 32) order[i] = s_ord[i];
+  } else {
+    mt.shuffle(order, (int)K);
+  }
 }
 
 int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, unsigned long long order_seed,
@@ -257,7 +255,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   if (h_base[0] != 19650218u) mt_base_table(h_base);
   DevBuf<u32> mt_base;
   MX_CUDA_TRY(mt_base.alloc(MT_N, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(mt_base.p, h_base, sizeof(h_base), cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(mx_h2d(mt_base.p, h_base, sizeof(h_base), s));
   MX_CUDA_TRY(g->comp_order.alloc(K, s));
   MX_CUDA_TRY(cudaEventRecord(ev_fork, s));
   MX_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
@@ -268,7 +266,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   DevBuf<u64> seeds;
   MX_CUDA_TRY(pre.alloc(prefix_len > 0 ? prefix_len : 1, s));
   if (prefix_len > 0)
-    MX_CUDA_TRY(cudaMemcpyAsync(pre.p, cursor_prefix, prefix_len, cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(mx_h2d(pre.p, cursor_prefix, prefix_len, s));
   MX_CUDA_TRY(seeds.alloc(K, s));
   KeyStrView v{};
   v.key_packed = ix->key_packed.p;
@@ -289,15 +287,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   {
     MxPhase ph2("cursor_shuffle", s);
     // list capacity = the largest key's block count (up to 16K entries, 64 KB)
-    DevBuf<u32> mx_nb;
-    MX_CUDA_TRY(mx_nb.alloc(1, s));
-    MX_CUDA_TRY(cudaMemsetAsync(mx_nb.p, 0, sizeof(u32), s));
-    max_blocks_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, mx_nb.p);
-    mx_count_launch();
-    u32 h_nb = 0;
-    MX_CUDA_TRY(cudaMemcpyAsync(&h_nb, mx_nb.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
-    MX_CUDA_TRY(cudaStreamSynchronize(s));
-    const int cap = (int)std::min<u32>((h_nb + 31) / 32 * 32, 16384);
+    const int cap = (int)std::min<long long>((ix->max_key_blocks + 31) / 32 * 32, 16384);
     const size_t per_warp = sizeof(u32) * (CS_FIXED + cap);
     const int wpc = per_warp <= 12 * 1024 ? 4 : 1;
     const size_t dyn = per_warp * wpc;
@@ -336,11 +326,20 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   if (int rc = gen_local_lists(g, s)) return rc;  // sharded index: this rank's cursor positions
   MX_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
   MX_CUDA_TRY(cudaGetLastError());
-  g->h_comp_order.resize(K);
-  g->h_comp_total.resize(K);
-  MX_CUDA_TRY(cudaMemcpyAsync(g->h_comp_order.data(), g->comp_order.p, sizeof(u32) * K, cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(g->h_comp_total.data(), g->comp_total.p, sizeof(u64) * K, cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  g->mirrors_valid = false;  // host copies of comp_order / comp_total on first use
+  return MX_OK;
+}
+
+int gen_host_mirrors(GenData* g) {
+  if (g->mirrors_valid || g->K == 0) return MX_OK;
+  g->h_comp_order.resize(g->K);
+  g->h_comp_total.resize(g->K);
+  MX_CUDA_TRY(cudaMemcpyAsync(g->h_comp_order.data(), g->comp_order.p, sizeof(u32) * g->K, cudaMemcpyDeviceToHost,
+                              g->stream));
+  MX_CUDA_TRY(cudaMemcpyAsync(g->h_comp_total.data(), g->comp_total.p, sizeof(u64) * g->K, cudaMemcpyDeviceToHost,
+                              g->stream));
+  MX_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  g->mirrors_valid = true;
   return MX_OK;
 }
 

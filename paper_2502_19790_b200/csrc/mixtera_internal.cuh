@@ -64,6 +64,8 @@ struct IndexData {
   int n_files = 0;
   u32 key_bits = 0;
   long long n_intervals = 0, n_keys = 0, n_blocks = 0;
+  long long indexed_samples = 0;  // iv_cum[n_intervals]
+  long long max_key_blocks = 0;   // blocks of the largest key
   DevBuf<u32> iv_key, iv_file, iv_start, iv_end;
   DevBuf<u64> iv_cum;
   DevBuf<u32> blk_first, blk_file, blk_key;
@@ -97,6 +99,7 @@ struct GenData {
   DevBuf<u64> ccum;
   DevBuf<u64> comp_total;
   std::vector<unsigned long long> h_comp_total;
+  bool mirrors_valid = false;  // h_comp_order / h_comp_total filled (gen_host_mirrors)
   DevBuf<u64> consumed;
   // sharded index only: lcnt u32[I+1] local intervals before each cursor
   // position, lpos u32[#local] their positions, rcum u64[I+1] real intervals
@@ -154,6 +157,7 @@ int index_finalize(IndexData* ix, long long I, cudaStream_t s);
 int index_block_table(const IndexData* ix, u32 file_base, uint4* out, cudaStream_t s);
 int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream_t s, IndexData* out);
 int gen_local_lists(GenData* g, cudaStream_t s);
+int gen_host_mirrors(GenData* g);
 int chunks_merge(int W, long long C, long long cap, const long long* offs, const u32* mkey, const u32* file,
                  const u32* start, const u32* end, long long* out_off, u32* o_mkey, u32* o_file, u32* o_start,
                  u32* o_end, cudaStream_t s);

@@ -111,20 +111,32 @@ struct WarpMT {
   uint2* pairs;   // [32] accepted (i, j) of one window
   int pos;        // next unread output (624 = drained)
 
+  // s[a] = f(s[a], prev, t) for a in [a0, a1), t = (a - a0) & 31 (compile-time
+  // in full batches); every lane runs the chain, lane t keeps word a0+32m+t
   template <typename F>
-  __device__ __forceinline__ uint32_t chain(int a0, int a1, uint32_t prev, F f) {  // s[a] = f(s[a], prev, a)
+  __device__ __forceinline__ uint32_t chain(int a0, int a1, uint32_t prev, F f) {
     const int lane = threadIdx.x & 31;
-    for (int b = a0; b < a1; b += 32) {
-      const int a = b + lane;
-      const uint32_t mine = a < a1 ? s[a] : 0u;
+    int b = a0;
+    for (; b + 32 <= a1; b += 32) {
+      const uint32_t mine = s[b + lane];
+      uint32_t sv[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) sv[t] = __shfl_sync(0xffffffffu, mine, t);
       uint32_t res = 0;
 #pragma unroll
       for (int t = 0; t < 32; ++t) {
-        const uint32_t sv = __shfl_sync(0xffffffffu, mine, t);
-        if (b + t < a1) {
-          prev = f(sv, prev, b + t);
-          if (lane == t) res = prev;
-        }
+        prev = f(sv[t], prev, b + t, t);
+        res = lane == t ? prev : res;
+      }
+      s[b + lane] = res;
+    }
+    if (b < a1) {  // tail batch
+      const int a = b + lane;
+      const uint32_t mine = a < a1 ? s[a] : 0u;
+      uint32_t res = 0;
+      for (int t = 0; t < a1 - b; ++t) {
+        prev = f(__shfl_sync(0xffffffffu, mine, t), prev, b + t, t);
+        res = lane == t ? prev : res;
       }
       if (a < a1) s[a] = res;
     }
@@ -137,19 +149,19 @@ struct WarpMT {
     for (int k = lane; k < MT_N; k += 32) s[k] = base[k];
     __syncwarp();
     const uint32_t key0 = (uint32_t)seed_v, key1 = (uint32_t)(seed_v >> 32);
-    const bool two = key1 != 0;  // klen = 2
-    auto f1 = [&](uint32_t sv, uint32_t prev, int a) {  // iteration k = a - 1, b = k % klen
-      const uint32_t b = two ? (uint32_t)((a - 1) & 1) : 0u;
-      return (sv ^ ((prev ^ (prev >> 30)) * 1664525u)) + (b ? key1 : key0) + b;
+    // init_by_array adds key[b] + b with b = k % klen (k = a - 1 in loop 1):
+    // batches start at a = 1 + 32m, so b = t & 1 when klen = 2
+    const uint32_t kb0 = key0, kb1 = key1 ? key1 + 1u : key0;
+    auto f1 = [&](uint32_t sv, uint32_t prev, int, int t) {
+      return (sv ^ ((prev ^ (prev >> 30)) * 1664525u)) + ((t & 1) ? kb1 : kb0);
     };
-    auto f2 = [](uint32_t sv, uint32_t prev, int a) {
+    auto f2 = [](uint32_t sv, uint32_t prev, int a, int) {
       return (sv ^ ((prev ^ (prev >> 30)) * 1566083941u)) - (uint32_t)a;
     };
     uint32_t prev = chain(1, MT_N, base[0], f1);  // init_by_array loop 1, a = 1..623
     // wrap (s[0] = s[623]), then iteration 623 at a = 1 (b = 623 % klen)
     {
-      const uint32_t b = two ? 1u : 0u;
-      const uint32_t v = (s[1] ^ ((prev ^ (prev >> 30)) * 1664525u)) + (b ? key1 : key0) + b;
+      const uint32_t v = (s[1] ^ ((prev ^ (prev >> 30)) * 1664525u)) + kb1;
       __syncwarp();
       if (lane == 0) { s[0] = prev; s[1] = v; }
       prev = v;
@@ -235,15 +247,30 @@ struct WarpMT {
       }
       const int m = __popc(acc_mask);
       __syncwarp();
-      if (lane == 0 && m > 0) {
-        uint2 nx = pairs[0];
-        for (int k = 0; k < m; ++k) {
-          const uint2 cu = nx;
-          if (k + 1 < m) nx = pairs[k + 1];
-          const T a = x[cu.x], b = x[cu.y];
-          x[cu.x] = b;
-          x[cu.y] = a;
+      // the window's swaps k = 0..m-1 touch x[i-k] and x[j_k] (j_k <= i-k).
+      // Swap k commutes with all earlier ones unless an earlier swap touched
+      // one of its positions: j_k' == j_k, or j_k' == i-k (k' < k). Each
+      // round runs the conflict-free prefix in parallel, one lane per swap.
+      const bool mine = lane < m;
+      const uint2 pr = mine ? pairs[lane] : make_uint2(0u, 0u);
+      int k0 = 0;
+      while (k0 < m) {
+        const bool live = mine && lane >= k0;
+        // earlier live lane with the same j
+        const uint32_t same = __match_any_sync(0xffffffffu, live ? pr.y : 0xffffffffu);
+        uint32_t conflict = __ballot_sync(0xffffffffu, live && (same & ((1u << lane) - 1u) & ~((1u << k0) - 1u)));
+        // a live lane whose j equals a LATER live lane's top i - k
+        const int hit = (int)((uint32_t)i - pr.y);  // lane whose top is j
+        const uint32_t hm = (live && hit > lane && hit < m) ? (1u << hit) : 0u;
+        conflict |= __reduce_or_sync(0xffffffffu, hm);
+        const int k1 = conflict ? __ffs(conflict) - 1 : m;  // first lane that must wait
+        if (live && lane < k1) {
+          const T a = x[pr.x], b = x[pr.y];
+          x[pr.x] = b;
+          x[pr.y] = a;
         }
+        __syncwarp();
+        k0 = k1;
       }
       pos += __popc(act_mask);
       i -= m;

@@ -217,7 +217,7 @@ int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream
   h.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
   h.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
   MX_CUDA_TRY(h.file_ds.alloc(d->n_files, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(h.file_ds.p, d->file_ds, sizeof(int32_t) * d->n_files, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(mx_h2d(h.file_ds.p, d->file_ds, sizeof(int32_t) * d->n_files, s));
   if (Kg == 0) {
     h.n_intervals = h.n_keys = h.n_blocks = 0;
     return MX_OK;
@@ -229,8 +229,8 @@ int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream
   MX_CUDA_TRY(D.alloc((long long)W * (Kg + 1), s));
   MX_CUDA_TRY(OFF.alloc(Kg * W + 1, s));
   MX_CUDA_TRY(counts.alloc(W, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(gkeys.p, d->global_keys, sizeof(u32) * Kg, cudaMemcpyHostToDevice, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(counts.p, d->counts, sizeof(long long) * W, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(mx_h2d(gkeys.p, d->global_keys, sizeof(u32) * Kg, s));
+  MX_CUDA_TRY(mx_h2d(counts.p, d->counts, sizeof(long long) * W, s));
   ShardArgs a{};
   a.world = W;
   a.rank = d->rank;

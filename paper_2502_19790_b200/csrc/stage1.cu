@@ -667,7 +667,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   const int lut_total = d->lut_offsets[d->n_props];
   DevBuf<u32> lut;
   MX_CUDA_TRY(lut.alloc(lut_total, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(lut.p, d->lut, sizeof(u32) * lut_total, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(mx_h2d(lut.p, d->lut, sizeof(u32) * lut_total, s));
   a.lut = lut.p;
   // sum-keying LUT: fail flag as a count above the key bits (needs key_bits +
   // bitlen(P) <= 31), see scan_direct_kernel
@@ -680,7 +680,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     for (int i = 0; i < lut_total; ++i)
       ls[i] = (d->lut[i] & ~FAIL) + ((d->lut[i] >> 31) << d->key_bits);
     MX_CUDA_TRY(lut_sum.alloc(lut_total, s));
-    MX_CUDA_TRY(cudaMemcpyAsync(lut_sum.p, ls.data(), sizeof(u32) * lut_total, cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(mx_h2d(lut_sum.p, ls.data(), sizeof(u32) * lut_total, s));
     a.lut_sum = lut_sum.p;
     a.fail_limit = 1u << d->key_bits;
   }
@@ -690,7 +690,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   a.rank_mask = d->rank_mask;
   // file table copies (ds and ids are needed for exports and cursors)
   MX_CUDA_TRY(ix.file_ds.alloc(d->n_files, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(ix.file_ds.p, d->file_ds, sizeof(int32_t) * d->n_files, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(mx_h2d(ix.file_ds.p, d->file_ds, sizeof(int32_t) * d->n_files, s));
   ix.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
   ix.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
 
@@ -839,9 +839,13 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   u32 *kb = k2.p, *fb = f2.p, *sb = s2.p, *eb = e2.p;
   std::unique_ptr<MxPhase> ph_sort(new MxPhase("radix_sort", s));
   if (slot_mode) {  // per-tile slots -> dense records (order preserved)
-    DevBuf<u64> toff;
+    DevBuf<u64> toff, tst;
+    const int otiles = (int)((ntiles + TO_THREADS * TO_ITEMS - 1) / (TO_THREADS * TO_ITEMS));
     MX_CUDA_TRY(toff.alloc(ntiles + 1, s));
-    tile_offsets_kernel<<<1, 1024, 0, s>>>(ntiles, t_cnt.p, toff.p);
+    MX_CUDA_TRY(tst.alloc(otiles, s));
+    MX_CUDA_TRY(cudaMemsetAsync(tst.p, 0, sizeof(u64) * otiles, s));
+    MX_CUDA_TRY(cudaMemsetAsync(ctr.p + 2, 0, sizeof(u32), s));
+    tile_offsets_kernel<<<otiles, TO_THREADS, 0, s>>>(ntiles, t_cnt.p, toff.p, tst.p, ctr.p + 2);
     mx_count_launch();
     slot_compact_kernel<<<std::min(ntiles, n_sm * 16), 256, 0, s>>>(ntiles, tile_len, t_cnt.p, toff.p, rk.p, rf.p,
                                                                      rs.p, re.p, k2.p, f2.p, s2.p, e2.p);
@@ -870,6 +874,20 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     ix.iv_key.take(k2); ix.iv_file.take(f2); ix.iv_start.take(s2); ix.iv_end.take(e2);
   }
   return index_finalize(&ix, I, s);
+}
+
+// max over keys of (blocks of the key); totals = (n_keys << 32) | n_blocks
+__global__ void key_maxblk_kernel(const u32* key_blk_first, const u64* totals, u32* out) {
+  const u64 t = *totals;
+  const long long K = (long long)(t >> 32), B = (long long)(t & 0xffffffffull);
+  u32 m = 0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < K; k += (long long)gridDim.x * blockDim.x) {
+    const u32 end = k + 1 < K ? key_blk_first[k + 1] : (u32)B;
+    m = max(m, end - key_blk_first[k]);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(MX_FULL, m, d));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
 // Block / key structure and cumulative lengths of the interval table
@@ -915,19 +933,29 @@ int index_finalize(IndexData* ixp, long long I, cudaStream_t s) {
                                                     ix.iv_cum.p, err.p);
   mx_count_launch();
   ph_scan.reset();
+  // largest key (in blocks): sizes the cursor shuffle's shared-memory lists
+  DevBuf<u32> maxblk;
+  MX_CUDA_TRY(maxblk.alloc(1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(maxblk.p, 0, sizeof(u32), s));
+  key_maxblk_kernel<<<64, 256, 0, s>>>(ix.key_blk_first.p, scratch64.p, maxblk.p);
+  mx_count_launch();
   MX_CUDA_TRY(cudaGetLastError());
-  u64 tot = 0;
+  u64 tot = 0, samples = 0;
+  u32 h_maxblk = 0;
+  MX_CUDA_TRY(cudaMemcpyAsync(&h_maxblk, maxblk.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaMemcpyAsync(&tot, scratch64.p, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(&samples, ix.iv_cum.p + I, sizeof(u64), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaMemcpyAsync(&h_err, err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
   if (h_err.overlap) return mx_fail(MX_ERR_INDEX, "empty or overlapping interval in index build");
   ix.n_keys = (long long)(tot >> 32);
   ix.n_blocks = (long long)(tot & 0xffffffffull);
-  // sentinels
+  ix.indexed_samples = (long long)samples;
+  ix.max_key_blocks = (long long)h_maxblk;
+  // sentinels (stream-ordered; no host wait)
   const u32 sI = (u32)I, sB = (u32)ix.n_blocks;
-  MX_CUDA_TRY(cudaMemcpyAsync(ix.blk_first.p + ix.n_blocks, &sI, sizeof(u32), cudaMemcpyHostToDevice, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(ix.key_blk_first.p + ix.n_keys, &sB, sizeof(u32), cudaMemcpyHostToDevice, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  MX_CUDA_TRY(mx_h2d(ix.blk_first.p + ix.n_blocks, &sI, sizeof(u32), s));
+  MX_CUDA_TRY(mx_h2d(ix.key_blk_first.p + ix.n_keys, &sB, sizeof(u32), s));
   return MX_OK;
 }
 

@@ -1368,17 +1368,6 @@ __global__ void chunk_seed_kernel(long long n, long long first_id, const uint8_t
   ids[k] = id;
 }
 
-// pair prefix over phases (single CTA)
-__global__ void pair_prefix_kernel(const Phase* ph, long long n, u64* pre) {
-  if (threadIdx.x != 0) return;
-  u64 run = 0;
-  for (long long p = 0; p < n; ++p) {
-    pre[p] = run;
-    run += (u64)ph[p].n_chunks * (u64)ph[p].n_terms;
-  }
-  pre[n] = run;
-}
-
 // ------------------------------------------------------------------ small plans
 // A plan of a few chunks (ADO: one chunk per call) is emitted by two kernels
 // and one host sync: one CTA per chunk cuts all its terms into shared memory,
@@ -1503,8 +1492,14 @@ struct PlanWork {  // stream segment tables (generator scratch slots)
 enum ScratchSlot { S_WTS, S_SOFF, S_SEGC, S_SEGLO, S_SEGPRE, S_PHASES, S_TERMS, S_LL, S_OUT, S_REPORT, S_FLAGS,
                    S_POS, S_APIDX, S_APFRAC, S_FRONT, S_GM, S_GF, S_GS, S_GE, S_OVF, S_CNT, S_HDR };
 
-static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Term* terms,
-                long long n_chunks, long long n_phases, cudaStream_t s) {
+// Emission of a planned batch. Only ONE host synchronisation (at the end):
+// the pair prefix comes from the host copy of the phases, and the piece /
+// range buffers are sized by the bound pieces <= pairs + segments + intervals
+// (a (chunk, term) range yields one piece plus one per interval or stream
+// segment boundary inside it, and every stream position belongs to exactly
+// one range), so no count has to travel to the host mid-way.
+static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase* h_phases, const Term* terms,
+                long long n_chunks, long long n_phases, long long n_seg, cudaStream_t s) {
   IndexData* ix = g->ix;
   MxPhase ph("emit", s);
   g->h_small_valid = 0;
@@ -1515,17 +1510,18 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Term* 
   MX_CUDA_TRY(g->res_id.reserve(n_chunks > 0 ? n_chunks : 1, s));
   if (n_chunks == 0) {
     const long long z = 0;
-    MX_CUDA_TRY(cudaMemcpyAsync(g->res_off.p, &z, sizeof(z), cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(mx_h2d(g->res_off.p, &z, sizeof(z), s));
     MX_CUDA_TRY(cudaStreamSynchronize(s));
     return MX_OK;
   }
+  std::vector<u64> h_pre(n_phases + 1);
+  h_pre[0] = 0;
+  for (long long p = 0; p < n_phases; ++p)
+    h_pre[p + 1] = h_pre[p] + (u64)h_phases[p].n_chunks * (u64)h_phases[p].n_terms;
+  const u64 n_pairs = h_pre[n_phases];
   DevBuf<u64> pair_pre;
   MX_CUDA_TRY(pair_pre.alloc(n_phases + 1, s));
-  pair_prefix_kernel<<<1, 32, 0, s>>>(phases, n_phases, pair_pre.p);
-  mx_count_launch();
-  u64 n_pairs = 0;
-  MX_CUDA_TRY(cudaMemcpyAsync(&n_pairs, pair_pre.p + n_phases, sizeof(u64), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  MX_CUDA_TRY(mx_h2d(pair_pre.p, h_pre.data(), sizeof(u64) * (n_phases + 1), s));
   EmitArgs a{};
   a.phases = phases;
   a.n_phases = n_phases;
@@ -1553,11 +1549,8 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Term* 
   // exclusive scan of counts in place (each element is read and written by
   // the same thread; the total lands in [n_pairs])
   if (int rc = excl_scan<u64>(pair_off.p, (long long)n_pairs, pair_off.p, s)) return rc;
-  u64 n_pieces = 0;
-  MX_CUDA_TRY(cudaMemcpyAsync(&n_pieces, pair_off.p + n_pairs, sizeof(u64), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
   DevBuf<u32> pm, pf, ps, pe;
-  const long long cap = n_pieces > 0 ? (long long)n_pieces : 1;
+  const long long cap = (long long)n_pairs + n_seg + ix->n_intervals + 1;
   MX_CUDA_TRY(pm.alloc(cap, s));
   MX_CUDA_TRY(pf.alloc(cap, s));
   MX_CUDA_TRY(ps.alloc(cap, s));
@@ -1587,18 +1580,10 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Term* 
     mx_count_launch();
   }
   if (int rc = excl_scan<long long>(mcnt.p, n_chunks, g->res_off.p, s)) return rc;
-  u32 h_big = 0;
-  long long total = 0;
-  MX_CUDA_TRY(cudaMemcpyAsync(&h_big, big.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(&total, g->res_off.p + n_chunks, sizeof(long long), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
-  if (h_big) return mx_fail(MX_ERR_UNSUPPORTED, "a chunk has %u ranges before merging (> %d supported)", h_big, NM_CAP);
-  g->res_ranges = total;
-  const long long rc = total > 0 ? total : 1;
-  MX_CUDA_TRY(g->res_mkey.reserve(rc, s));
-  MX_CUDA_TRY(g->res_file.reserve(rc, s));
-  MX_CUDA_TRY(g->res_start.reserve(rc, s));
-  MX_CUDA_TRY(g->res_end.reserve(rc, s));
+  MX_CUDA_TRY(g->res_mkey.reserve(cap, s));
+  MX_CUDA_TRY(g->res_file.reserve(cap, s));
+  MX_CUDA_TRY(g->res_start.reserve(cap, s));
+  MX_CUDA_TRY(g->res_end.reserve(cap, s));
   {
     const long long grid = std::min<long long>((n_chunks + 7) / 8, 148 * 16);
     compact_warp_kernel<<<(unsigned)grid, 256, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
@@ -1609,7 +1594,13 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Term* 
                                                                       g->chunk_prefix_len, g->res_seed.p, g->res_id.p);
   mx_count_launch();
   MX_CUDA_TRY(cudaGetLastError());
+  u32 h_big = 0;
+  long long total = 0;
+  MX_CUDA_TRY(cudaMemcpyAsync(&h_big, big.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(&total, g->res_off.p + n_chunks, sizeof(long long), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_big) return mx_fail(MX_ERR_UNSUPPORTED, "a chunk has %u ranges before merging (> %d supported)", h_big, NM_CAP);
+  g->res_ranges = total;
   g->next_chunk_id += n_chunks;
   return MX_OK;
 }
@@ -1642,7 +1633,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   ma.allow_words = mix->allow_words;
   double* wts_p = nullptr;
   MX_CUDA_TRY(g->scratch(S_WTS, Km, &wts_p));
-  MX_CUDA_TRY(cudaMemcpyAsync(wts_p, mix->weights, sizeof(double) * Km, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(mx_h2d(wts_p, mix->weights, sizeof(double) * Km, s));
   // matching depends only on the mixture KEYS (not the weights): reuse the
   // previous plan's per-key component lists when the keys are unchanged
   // (ADO re-plans every chunk with new weights over the same domains)
@@ -1654,7 +1645,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   if (!cached) {
     DevBuf<u32> allow, L_cnt, hits;
     MX_CUDA_TRY(allow.alloc((long long)n_allow, s));
-    MX_CUDA_TRY(cudaMemcpyAsync(allow.p, mix->allow, sizeof(u32) * n_allow, cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(mx_h2d(allow.p, mix->allow, sizeof(u32) * n_allow, s));
     ma.allow = allow.p;
     MX_CUDA_TRY(L_cnt.alloc(Km, s));
     MX_CUDA_TRY(hits.alloc(K > 0 ? K : 1, s));
@@ -1672,8 +1663,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     g->match_shared = false;
     for (long long c = 0; c < K; ++c) g->match_shared |= h_hits[c] > 1;
     MX_CUDA_TRY(g->match_L_off.alloc(Km + 1, s));
-    MX_CUDA_TRY(cudaMemcpyAsync(g->match_L_off.p, g->match_off.data(), sizeof(u32) * (Km + 1), cudaMemcpyHostToDevice,
-                                s));
+    MX_CUDA_TRY(mx_h2d(g->match_L_off.p, g->match_off.data(), sizeof(u32) * (Km + 1), s));
     MX_CUDA_TRY(g->match_L.alloc(g->match_off[Km] > 0 ? g->match_off[Km] : 1, s));
     if (K > 0) {
       match_fill_kernel<<<Km, 256, 0, s>>>(ma, g->match_L_off.p, g->match_L.p);
@@ -1705,7 +1695,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     std::vector<u32> so(K + 1);
     for (long long c = 0; c <= K; ++c) so[c] = (u32)c;
     MX_CUDA_TRY(g->scratch(S_SOFF, K + 1, &w.s_off));
-    MX_CUDA_TRY(cudaMemcpyAsync(w.s_off, so.data(), sizeof(u32) * (K + 1), cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(mx_h2d(w.s_off, so.data(), sizeof(u32) * (K + 1), s));
     MX_CUDA_TRY(g->scratch(S_SEGC, K, &w.seg_comp));
     MX_CUDA_TRY(g->scratch(S_SEGLO, K, &w.seg_lo));
     MX_CUDA_TRY(g->scratch(S_SEGPRE, 2 * K, &w.seg_pre));
@@ -1788,8 +1778,8 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     for (int r = 0; r < Km; ++r) ow[Km + ow[r]] = (u32)r;
     u32* order_w = front.p;
     u32* rank_w = reinterpret_cast<u32*>(ap_frac.p);
-    MX_CUDA_TRY(cudaMemcpyAsync(order_w, ow.data(), sizeof(u32) * Km, cudaMemcpyHostToDevice, s));
-    MX_CUDA_TRY(cudaMemcpyAsync(rank_w, ow.data() + Km, sizeof(u32) * Km, cudaMemcpyHostToDevice, s));
+    MX_CUDA_TRY(mx_h2d(order_w, ow.data(), sizeof(u32) * Km, s));
+    MX_CUDA_TRY(mx_h2d(rank_w, ow.data() + Km, sizeof(u32) * Km, s));
     BigArgs ba{};
     ba.Km = Km;
     ba.C = mix->chunk_size;
@@ -1917,8 +1907,10 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     return hdr[2] ? MX_EXHAUSTED : MX_OK;
   }
   long long h_out[4];
+  std::vector<Phase> h_phases(cap_phases);
   MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaMemcpyAsync(g->report.data(), report.p, sizeof(long long) * Km, cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(h_phases.data(), phases.p, sizeof(Phase) * cap_phases, cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
   ph_plan.reset();
   if (w.mode == 0) {
@@ -1926,7 +1918,8 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
                                               g->consumed.p);
     mx_count_launch();
   }
-  int rc = emit(g, w, phases.p, terms.p, h_out[0], h_out[1], s);
+  const long long n_seg = w.mode == 0 ? (long long)h_off[Km] : K;
+  int rc = emit(g, w, phases.p, h_phases.data(), terms.p, h_out[0], h_out[1], n_seg, s);
   if (rc != MX_OK) return rc;
   *n_out = h_out[0];
   return h_out[3] ? MX_EXHAUSTED : MX_OK;
@@ -1943,12 +1936,12 @@ int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long 
   w.mode = 2;
   w.n_streams = 1;
   if (K == 0) {
-    int rc = emit(g, w, nullptr, nullptr, 0, 0, s);
+    int rc = emit(g, w, nullptr, nullptr, nullptr, 0, 0, 0, s);
     return rc != MX_OK ? rc : MX_EXHAUSTED;
   }
   std::vector<u32> so = {0u, (u32)K};
   MX_CUDA_TRY(g->scratch(S_SOFF, 2, &w.s_off));
-  MX_CUDA_TRY(cudaMemcpyAsync(w.s_off, so.data(), sizeof(u32) * 2, cudaMemcpyHostToDevice, s));
+  MX_CUDA_TRY(mx_h2d(w.s_off, so.data(), sizeof(u32) * 2, s));
   MX_CUDA_TRY(g->scratch(S_SEGC, K, &w.seg_comp));
   MX_CUDA_TRY(g->scratch(S_SEGLO, K, &w.seg_lo));
   MX_CUDA_TRY(g->scratch(S_SEGPRE, K + 1, &w.seg_pre));
@@ -1966,11 +1959,13 @@ int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long 
   plan_arbitrary_kernel<<<1, 32, 0, s>>>(w.seg_pre, K, chunk_size, max_chunks, phases.p, terms.p, out.p, pos.p);
   mx_count_launch();
   long long h_out[4];
+  Phase h_phases[2];
   MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(h_phases, phases.p, sizeof(h_phases), cudaMemcpyDeviceToHost, s));
   MX_CUDA_TRY(cudaStreamSynchronize(s));
   commit_segments_kernel<<<1, 128, 0, s>>>(1, w.s_off, w.seg_comp, w.seg_lo, w.seg_pre, pos.p, g->consumed.p);
   mx_count_launch();
-  int rc = emit(g, w, phases.p, terms.p, h_out[0], h_out[1], s);
+  int rc = emit(g, w, phases.p, h_phases, terms.p, h_out[0], h_out[1], K, s);
   if (rc != MX_OK) return rc;
   *n_out = h_out[0];
   return h_out[3] ? MX_EXHAUSTED : MX_OK;
