@@ -113,6 +113,20 @@ def redistribute_best_effort(remaining, shortfall_key, progress_keys, weights):
     return remaining
 
 
+_TORCH_OF = {np.int64: "int64", np.uint64: "uint64", np.int32: "int32", np.uint32: "uint32"}
+
+
+def _pinned(n: int, dtype) -> np.ndarray:
+    """Host array in page-locked memory (torch's caching host allocator), so
+    the result read-back is a direct DMA instead of a staged pageable copy."""
+    import torch
+
+    if n < 4096:
+        return np.zeros(n, dtype)
+    t = torch.empty(n, dtype=getattr(torch, _TORCH_OF[dtype]), pin_memory=True)
+    return t.numpy()
+
+
 class ChunkBatch:
     """Device CSR of consecutive chunks (valid until the generator plans again)."""
 
@@ -131,9 +145,9 @@ class ChunkBatch:
     def to_host(self) -> dict[str, np.ndarray]:
         if self._host is None:
             n, r = self.n_chunks, self.n_ranges
-            h = dict(off=np.zeros(n + 1, np.int64), ids=np.zeros(n, np.int64), seeds=np.zeros(n, np.uint64),
-                     mkey=np.zeros(r, np.uint32), ds=np.zeros(r, np.int32), fid=np.zeros(r, np.int64),
-                     start=np.zeros(r, np.uint32), end=np.zeros(r, np.uint32))
+            h = dict(off=_pinned(n + 1, np.int64), ids=_pinned(n, np.int64), seeds=_pinned(n, np.uint64),
+                     mkey=_pinned(r, np.uint32), ds=_pinned(r, np.int32), fid=_pinned(r, np.int64),
+                     start=_pinned(r, np.uint32), end=_pinned(r, np.uint32))
             _lib.check(_lib.lib().mx_gen_result_copy(
                 self._gen._h, *(_lib.ptr(h[x]) for x in ("off", "ids", "seeds", "mkey", "ds", "fid", "start", "end"))))
             self._host = h

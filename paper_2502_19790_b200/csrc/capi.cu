@@ -174,6 +174,21 @@ int mx_fail_cuda(cudaError_t e, const char* what, const char* file, int line) {
 
 using namespace mx;
 
+__global__ void map_files_kernel(const u32* fidx, long long n, const int32_t* file_ds, const long long* file_ids,
+                                 int32_t* ds, long long* fid) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u32 f = fidx[i];
+  ds[i] = file_ds[f];
+  fid[i] = file_ids[f];
+}
+
+void map_files(const u32* fidx, long long n, const int32_t* file_ds, const long long* file_ids, int32_t* ds,
+               long long* fid, cudaStream_t s) {
+  map_files_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(fidx, n, file_ds, file_ids, ds, fid);
+  mx_count_launch();
+}
+
 extern "C" {
 
 const char* mx_last_error(void) { return g_err.c_str(); }
@@ -438,25 +453,31 @@ int mx_gen_result_copy(const mx_gen* gen, int64_t* chunk_offsets, int64_t* chunk
     }
     return MX_OK;
   }
-  if (chunk_offsets) e = cudaMemcpyAsync(chunk_offsets, g.res_off.p, sizeof(long long) * (C + 1), cudaMemcpyDeviceToHost, s);
+  // dataset / file id per range mapped on the device, then one D2H per array
+  // (fast when the caller's buffers are pinned, as ChunkBatch.to_host's are)
+  DevBuf<int32_t> d_ds;
+  DevBuf<long long> d_fid;
+  if (R && (ds || file_id)) {
+    e = d_ds.alloc(R, s);
+    if (e == cudaSuccess) e = d_fid.alloc(R, s);
+    if (e == cudaSuccess) {
+      map_files(g.res_file.p, R, g.ix->file_ds.p, g.ix->file_ids.p, d_ds.p, d_fid.p, s);
+      e = cudaGetLastError();
+    }
+  }
+  if (e == cudaSuccess && chunk_offsets)
+    e = cudaMemcpyAsync(chunk_offsets, g.res_off.p, sizeof(long long) * (C + 1), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && chunk_ids && C)
     e = cudaMemcpyAsync(chunk_ids, g.res_id.p, sizeof(long long) * C, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && seeds && C) e = cudaMemcpyAsync(seeds, (const void*)g.res_seed.p, sizeof(u64) * C, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && mkey && R) e = cudaMemcpyAsync(mkey, g.res_mkey.p, sizeof(u32) * R, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && start && R) e = cudaMemcpyAsync(start, g.res_start.p, sizeof(u32) * R, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && end && R) e = cudaMemcpyAsync(end, g.res_end.p, sizeof(u32) * R, cudaMemcpyDeviceToHost, s);
-  std::vector<u32> f;
-  if (e == cudaSuccess && R && (ds || file_id)) {
-    f.resize(R);
-    e = cudaMemcpyAsync(f.data(), g.res_file.p, sizeof(u32) * R, cudaMemcpyDeviceToHost, s);
-  }
+  if (e == cudaSuccess && R && ds) e = cudaMemcpyAsync(ds, d_ds.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && R && file_id)
+    e = cudaMemcpyAsync(file_id, d_fid.p, sizeof(long long) * R, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return mx_fail_cuda(e, "result copy", __FILE__, __LINE__);
-  if (!f.empty())
-    for (long long i = 0; i < R; ++i) {
-      if (ds) ds[i] = g.ix->h_file_ds[f[i]];
-      if (file_id) file_id[i] = g.ix->h_file_ids[f[i]];
-    }
   return MX_OK;
 }
 

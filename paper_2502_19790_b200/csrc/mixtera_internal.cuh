@@ -71,6 +71,7 @@ struct IndexData {
   DevBuf<u32> blk_first, blk_file, blk_key;
   DevBuf<u32> key_blk_first, key_packed;
   DevBuf<int32_t> file_ds;
+  DevBuf<long long> file_ids;  // device copy of h_file_ids (result read-back mapping)
   std::vector<int32_t> h_file_ds;
   std::vector<int64_t> h_file_ids;
   // key codec (canonical strings for cursor seeds)

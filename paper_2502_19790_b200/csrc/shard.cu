@@ -216,6 +216,8 @@ int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream
   MX_CUDA_TRY(cudaMemcpyAsync(h.str_bytes.p, loc->str_bytes.p, loc->str_bytes.n, cudaMemcpyDeviceToDevice, s));
   h.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
   h.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
+  MX_CUDA_TRY(h.file_ids.alloc(d->n_files, s));
+  MX_CUDA_TRY(mx_h2d(h.file_ids.p, d->file_ids, sizeof(long long) * d->n_files, s));
   MX_CUDA_TRY(h.file_ds.alloc(d->n_files, s));
   MX_CUDA_TRY(mx_h2d(h.file_ds.p, d->file_ds, sizeof(int32_t) * d->n_files, s));
   if (Kg == 0) {

@@ -693,6 +693,8 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(mx_h2d(ix.file_ds.p, d->file_ds, sizeof(int32_t) * d->n_files, s));
   ix.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
   ix.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
+  MX_CUDA_TRY(ix.file_ids.alloc(d->n_files, s));
+  MX_CUDA_TRY(mx_h2d(ix.file_ids.p, d->file_ids, sizeof(long long) * d->n_files, s));
 
   // ---- stage-1 pass variant (MX_SCAN = direct (default) | pipe | v1):
   //  direct: one CTA per 4096-sample tile, slot output (scan_direct_kernel)
