@@ -152,6 +152,24 @@ int mx_gen_result_device(const mx_gen* gen, const int64_t** chunk_offsets, const
  * [n_chunks+1], pieces [n_ranges] (file_index = index into the file table). */
 int mx_gen_result_export(const mx_gen* gen, int64_t* chunk_offsets, uint32_t* mkey, uint32_t* file_index,
                          uint32_t* start, uint32_t* end, void* stream);
+/* Canonical chunk bytes of the last plan on the device [Chunk.serialize
+ * chunks.py:54-93, canonical_json seeding.py:36-42]. key_json: the JSON-quoted
+ * canonical strings of the result's keys (mixture keys, or component keys for
+ * arbitrary chunks), key_rank their ranks in string order; file_rank: rank of
+ * every file of the index in (str(ds), str(fid)) order; mixture_json: the
+ * spec's canonical JSON ("null" for arbitrary chunks). */
+typedef struct mx_json_desc {
+  int64_t n_keys;
+  const uint8_t* key_json;
+  const int64_t* key_json_off; /* [n_keys+1] */
+  const uint32_t* key_rank;    /* [n_keys] */
+  const uint32_t* file_rank;   /* [n_files] */
+  const uint8_t* mixture_json;
+  int32_t mixture_len;
+} mx_json_desc;
+int mx_gen_result_json(mx_gen* gen, const mx_json_desc* desc, int64_t* total_bytes, void* stream);
+/* Host copy of the serialized result: bytes [total_bytes], offsets [n_chunks+1]. */
+int mx_gen_result_json_copy(const mx_gen* gen, uint8_t* bytes, int64_t* offsets);
 /* Shortfall report of the last generate() that returned None: host [n_mkeys]. */
 int mx_gen_report(const mx_gen* gen, int64_t* remaining);
 /* Remember / restore the cursor state and next chunk id on the device (used

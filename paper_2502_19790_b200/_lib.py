@@ -91,6 +91,18 @@ class ShardDesc(C.Structure):
     ]
 
 
+class JsonDesc(C.Structure):
+    _fields_ = [
+        ("n_keys", i64),
+        ("key_json", P(C.c_uint8)),
+        ("key_json_off", P(i64)),
+        ("key_rank", P(u32)),
+        ("file_rank", P(u32)),
+        ("mixture_json", P(C.c_uint8)),
+        ("mixture_len", i32),
+    ]
+
+
 _SIGS = {
     "mx_last_error": (C.c_char_p, []),
     "mx_abi_version": (C.c_int, []),
@@ -112,6 +124,8 @@ _SIGS = {
     "mx_gen_result_device": (C.c_int, [vp, P(vp), P(vp), P(vp), P(vp), P(vp), P(vp)]),
     "mx_gen_report": (C.c_int, [vp, vp]),
     "mx_gen_result_export": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "mx_gen_result_json": (C.c_int, [vp, P(JsonDesc), P(i64), vp]),
+    "mx_gen_result_json_copy": (C.c_int, [vp, vp, vp]),
     "mx_gen_mark": (C.c_int, [vp]),
     "mx_gen_reset_to_mark": (C.c_int, [vp]),
     "mx_gen_next_chunk_id": (C.c_int, [vp, P(i64)]),

@@ -127,6 +127,14 @@ def _pinned(n: int, dtype) -> np.ndarray:
     return t.numpy()
 
 
+def _pinned_bytes(n: int) -> np.ndarray:
+    import torch
+
+    if n < 4096:
+        return np.zeros(max(n, 1), np.uint8)
+    return torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy()
+
+
 class ChunkBatch:
     """Device CSR of consecutive chunks (valid until the generator plans again)."""
 
@@ -152,6 +160,41 @@ class ChunkBatch:
                 self._gen._h, *(_lib.ptr(h[x]) for x in ("off", "ids", "seeds", "mkey", "ds", "fid", "start", "end"))))
             self._host = h
         return self._host
+
+    def serialize_all(self) -> tuple[bytes, np.ndarray]:
+        """Canonical bytes of every chunk of the batch, built on the device
+        (``csrc/serialize.cu``): one blob + offsets [n_chunks + 1]; chunk i is
+        ``blob[off[i]:off[i+1]]`` == ``self.chunk(i).serialize()``."""
+        import json
+
+        L = _lib.lib()
+        keys = self._gen.index.component_keys() if self.arbitrary else list(self.mkeys)
+        strs = [k.canonical_string() for k in keys]
+        kj = [json.dumps(x, ensure_ascii=True).encode("ascii") for x in strs]
+        koff = np.zeros(len(kj) + 1, np.int64)
+        koff[1:] = np.cumsum([len(b) for b in kj])
+        order = sorted(range(len(strs)), key=strs.__getitem__)
+        krank = np.zeros(len(strs), np.uint32)
+        krank[order] = np.arange(len(strs), dtype=np.uint32)
+        mix = b"null" if self.arbitrary or self.spec is None else canonical_json_bytes(self.spec.to_json())
+        frank = self._gen.index.file_string_ranks()
+        blob_k = np.frombuffer(b"".join(kj) or b"\0", dtype=np.uint8)
+        blob_m = np.frombuffer(mix, dtype=np.uint8)
+        d = _lib.JsonDesc()
+        P = C.POINTER
+        d.n_keys = len(kj)
+        d.key_json = blob_k.ctypes.data_as(P(C.c_uint8))
+        d.key_json_off = koff.ctypes.data_as(P(C.c_int64))
+        d.key_rank = krank.ctypes.data_as(P(C.c_uint32))
+        d.file_rank = frank.ctypes.data_as(P(C.c_uint32))
+        d.mixture_json = blob_m.ctypes.data_as(P(C.c_uint8))
+        d.mixture_len = len(mix)
+        total = C.c_int64()
+        _lib.check(L.mx_gen_result_json(self._gen._h, C.byref(d), C.byref(total), 0))
+        off = _pinned(self.n_chunks + 1, np.int64)
+        buf = _pinned_bytes(total.value)
+        _lib.check(L.mx_gen_result_json_copy(self._gen._h, _lib.ptr(buf), _lib.ptr(off)))
+        return buf[: total.value].tobytes(), off
 
     def chunk(self, i: int) -> Chunk:
         h = self.to_host()

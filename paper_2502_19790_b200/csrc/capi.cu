@@ -523,6 +523,29 @@ int mx_gen_result_export(const mx_gen* gen, int64_t* chunk_offsets, uint32_t* mk
   return MX_OK;
 }
 
+int mx_gen_result_json(mx_gen* gen, const mx_json_desc* desc, int64_t* total_bytes, void* stream) {
+  MX_CHECK_ARG(gen && desc && total_bytes, "null argument");
+  MX_CHECK_ARG(desc->n_keys >= 0 && desc->n_keys < 65536, "n_keys outside [0, 65536)");
+  MX_CHECK_ARG(desc->key_json_off && desc->key_rank && desc->file_rank && desc->mixture_json, "null table");
+  g_err.clear();
+  (void)stream;
+  int rc = gen_result_json(&gen->d, desc, gen->d.stream);
+  *total_bytes = gen->d.json_bytes;
+  return rc;
+}
+
+int mx_gen_result_json_copy(const mx_gen* gen, uint8_t* bytes, int64_t* offsets) {
+  MX_CHECK_ARG(gen, "null generator");
+  const GenData& g = gen->d;
+  cudaError_t e = cudaSuccess;
+  if (offsets) e = cudaMemcpyAsync(offsets, g.json_off.p, sizeof(long long) * (g.res_chunks + 1), cudaMemcpyDeviceToHost, g.stream);
+  if (e == cudaSuccess && bytes && g.json_bytes)
+    e = cudaMemcpyAsync(bytes, g.json.p, g.json_bytes, cudaMemcpyDeviceToHost, g.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g.stream);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "json copy", __FILE__, __LINE__);
+  return MX_OK;
+}
+
 int mx_gen_report(const mx_gen* gen, int64_t* remaining) {
   MX_CHECK_ARG(gen && remaining, "null argument");
   for (size_t i = 0; i < gen->d.report.size(); ++i) remaining[i] = gen->d.report[i];

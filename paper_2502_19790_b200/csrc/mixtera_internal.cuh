@@ -115,6 +115,10 @@ struct GenData {
   DevBuf<long long> res_id;
   DevBuf<u64> res_seed;
   DevBuf<u32> res_mkey, res_file, res_start, res_end;
+  // canonical JSON of the last result (serialize.cu)
+  DevBuf<uint8_t> json;
+  DevBuf<long long> json_off;
+  long long json_bytes = 0;
   std::vector<long long> report;
   int last_mkeys = 0;
   // mark / reset of the cursor state (look-ahead rewinds without host copies)
@@ -159,6 +163,8 @@ int index_block_table(const IndexData* ix, u32 file_base, uint4* out, cudaStream
 int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream_t s, IndexData* out);
 int gen_local_lists(GenData* g, cudaStream_t s);
 int gen_host_mirrors(GenData* g);
+int excl_scan_ll(const u64* in, long long n, long long* out, cudaStream_t s);
+int gen_result_json(GenData* g, const mx_json_desc* d, cudaStream_t s);
 int chunks_merge(int W, long long C, long long cap, const long long* offs, const u32* mkey, const u32* file,
                  const u32* start, const u32* end, long long* out_off, u32* o_mkey, u32* o_file, u32* o_start,
                  u32* o_end, cudaStream_t s);

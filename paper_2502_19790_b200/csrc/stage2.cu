@@ -1292,6 +1292,8 @@ static int excl_scan(const u64* in, long long n, OUT* out, cudaStream_t s) {
   return MX_OK;
 }
 
+int excl_scan_ll(const u64* in, long long n, long long* out, cudaStream_t s) { return excl_scan<long long>(in, n, out, s); }
+
 // Dense copy of each chunk's merged ranges (one warp per chunk).
 __global__ void compact_warp_kernel(long long n_chunks, const u64* chunk_piece_off, const long long* res_off,
                                     const u32* pm, const u32* pf, const u32* ps, const u32* pe, u32* rm, u32* rf,
@@ -1648,6 +1650,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     MX_CUDA_TRY(mx_h2d(allow.p, mix->allow, sizeof(u32) * n_allow, s));
     ma.allow = allow.p;
     MX_CUDA_TRY(L_cnt.alloc(Km, s));
+    MX_CUDA_TRY(cudaMemsetAsync(L_cnt.p, 0, sizeof(u32) * Km, s));  // stays 0 for an empty index
     MX_CUDA_TRY(hits.alloc(K > 0 ? K : 1, s));
     MX_CUDA_TRY(cudaMemsetAsync(hits.p, 0, sizeof(u32) * (K > 0 ? K : 1), s));
     if (K > 0) {
@@ -1726,6 +1729,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   struct { double* p; } ap_frac;
   struct { u32* p; } front;
   MX_CUDA_TRY(g->scratch(S_PHASES, cap_phases, &phases.p));
+  MX_CUDA_TRY(cudaMemsetAsync(phases.p, 0, sizeof(Phase) * cap_phases, s));  // copied back whole
   MX_CUDA_TRY(g->scratch(S_TERMS, cap_terms, &terms.p));
   MX_CUDA_TRY(g->scratch(S_LL, 5LL * Km, &scratch_ll.p));
   MX_CUDA_TRY(g->scratch(S_OUT, 4, &out.p));

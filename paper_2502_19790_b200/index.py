@@ -139,6 +139,25 @@ class ChunkerIndex:
         return [(ks[r], int(d), int(f), int(a), int(b))
                 for r, d, f, a, b in zip(t["key"], t["ds"], t["fid"], t["start"], t["end"])]
 
+    def file_table(self) -> tuple[np.ndarray, np.ndarray]:
+        """(dataset ids, file ids) of the index's file table (the global table
+        for a file-sharded index)."""
+        sh = getattr(self, "shard", None)
+        if sh is not None:
+            return sh.file_ds, sh.file_ids
+        return self.catalog.file_ds, self.catalog.file_ids
+
+    def file_string_ranks(self) -> np.ndarray:
+        """u32 rank of every file in (str(ds), str(fid)) order: the order in
+        which canonical chunk JSON (sort_keys) lists datasets and files."""
+        if getattr(self, "_frank", None) is None:
+            ds, fid = self.file_table()
+            order = np.lexsort((np.asarray(fid).astype(str), np.asarray(ds).astype(str)))
+            rank = np.empty(len(order), np.uint32)
+            rank[order] = np.arange(len(order), dtype=np.uint32)
+            self._frank = rank
+        return self._frank
+
     # ---------------------------------------------------------- reference duck type
     def component_keys(self) -> list[MixtureKey]:
         if self._keys is None:
