@@ -5,6 +5,12 @@
 //    with __match_any_sync and summed by the group leader in lane order into
 //    a warp-private shared-memory accumulator; warps, then CTAs, are combined
 //    in a fixed order, so the f64 sums are bit-reproducible run to run.
+//    For <= 32 domains (the ADO case: 22 Pile domains) domain_loss_priv_kernel
+//    replaces it: every thread owns a private shared-memory row of K (f64 sum,
+//    u32 count) bins, streams its tokens with 16-byte loads (4 tokens per
+//    load, coalesced across the CTA) and accumulates without atomics or
+//    warp votes; rows are combined per domain in a fixed order, so the sums
+//    stay run-to-run reproducible. HBM-bound: B3 = T x (4 + 4) bytes.
 //  * fit_kernel: fit_power_law (ado.py:121-168), one CTA per domain, one warp
 //    per epsilon candidate (grid of 50, then a 201-point linspace refinement),
 //    closed-form log-linear regression + SSE in f64, strict-< argmin with
@@ -76,6 +82,68 @@ domain_loss_kernel(const float* loss, const int32_t* tags, long long n, int K, l
     }
     part_sum[(long long)blockIdx.x * K + k] = s;
     part_cnt[(long long)blockIdx.x * K + k] = c;
+  }
+}
+
+constexpr int DLP_THREADS = 256;
+constexpr int DLP_MAXK = 32;
+
+__global__ void __launch_bounds__(DLP_THREADS)
+domain_loss_priv_kernel(const float* __restrict__ loss, const int32_t* __restrict__ tags, long long n, int K,
+                        double* part_sum, long long* part_cnt, u32* bad) {
+  extern __shared__ __align__(16) unsigned char dlp_dyn[];
+  double* s_sum = reinterpret_cast<double*>(dlp_dyn);                            // [K][DLP_THREADS]
+  u32* s_cnt = reinterpret_cast<u32*>(dlp_dyn + sizeof(double) * K * DLP_THREADS);  // [K][DLP_THREADS]
+  const int tid = threadIdx.x;
+  for (int k = 0; k < K; ++k) {
+    s_sum[k * DLP_THREADS + tid] = 0.0;
+    s_cnt[k * DLP_THREADS + tid] = 0;
+  }
+  u32 badv = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(loss) | reinterpret_cast<uintptr_t>(tags)) & 15) == 0;
+  const long long stride = (long long)gridDim.x * DLP_THREADS * 4;
+  auto add = [&](int t, float v) {
+    if ((unsigned)t >= (unsigned)K) {
+      badv = 1;
+      return;
+    }
+    s_sum[t * DLP_THREADS + tid] += (double)v;
+    s_cnt[t * DLP_THREADS + tid] += 1u;
+  };
+  long long i = ((long long)blockIdx.x * DLP_THREADS + tid) * 4;
+  if (vec) {
+    for (; i + 4 <= n; i += stride) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(loss + i));
+      const int4 t = __ldcs(reinterpret_cast<const int4*>(tags + i));
+      add(t.x, v.x);
+      add(t.y, v.y);
+      add(t.z, v.z);
+      add(t.w, v.w);
+    }
+  }
+  for (; i < n; i += stride)  // tail (or unaligned input): same token order per thread
+    for (long long j = i; j < i + 4 && j < n; ++j) add(tags[j], loss[j]);
+  if (badv) atomicOr(bad, 1u);
+  __syncthreads();
+  // fixed-order combine: warp w sums domains k = w, w + 8, ...; lanes take
+  // threads lane, lane + 32, ... then a fixed shuffle tree
+  const int lane = tid & 31, w = tid >> 5;
+  for (int k = w; k < K; k += DLP_THREADS / 32) {
+    double sv = 0.0;
+    long long cv = 0;
+    for (int x = lane; x < DLP_THREADS; x += 32) {
+      sv += s_sum[k * DLP_THREADS + x];
+      cv += s_cnt[k * DLP_THREADS + x];
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      sv += __shfl_xor_sync(MX_FULL, sv, d);
+      cv += __shfl_xor_sync(MX_FULL, cv, d);
+    }
+    if (lane == 0) {
+      part_sum[(long long)blockIdx.x * K + k] = sv;
+      part_cnt[(long long)blockIdx.x * K + k] = cv;
+    }
   }
 }
 
@@ -361,8 +429,14 @@ __global__ void credit_kernel(int k, double rate, const double* pi, double* cred
 int domain_loss(const float* losses, const int32_t* tags, long long n, int K, double* sums, long long* counts,
                 cudaStream_t s) {
   if (K < 1 || K > DL_MAXK) return mx_fail(MX_ERR_UNSUPPORTED, "n_domains=%d outside [1, %d]", K, DL_MAXK);
+  const bool priv = K <= DLP_MAXK;
   long long per_block = 16384;
-  int blocks = (int)((n + per_block - 1) / per_block);
+  int blocks;
+  if (priv) {  // ~8K tokens per CTA, at most 4 CTAs per SM resident
+    blocks = (int)std::min<long long>((n + 8191) / 8192, 148 * 4);
+  } else {
+    blocks = (int)((n + per_block - 1) / per_block);
+  }
   if (blocks < 1) blocks = 1;
   DevBuf<double> ps;
   DevBuf<long long> pc;
@@ -371,7 +445,18 @@ int domain_loss(const float* losses, const int32_t* tags, long long n, int K, do
   MX_CUDA_TRY(pc.alloc((long long)blocks * K, s));
   MX_CUDA_TRY(bad.alloc(1, s));
   MX_CUDA_TRY(cudaMemsetAsync(bad.p, 0, sizeof(u32), s));
-  domain_loss_kernel<<<blocks, DL_THREADS, 0, s>>>(losses, tags, n, K, per_block, ps.p, pc.p, bad.p);
+  if (priv) {
+    const size_t smem = (sizeof(double) + sizeof(u32)) * (size_t)K * DLP_THREADS;
+    static size_t smem_set = 0;
+    if (smem > 48 * 1024 && smem > smem_set) {
+      MX_CUDA_TRY(cudaFuncSetAttribute(domain_loss_priv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)((sizeof(double) + sizeof(u32)) * DLP_MAXK * DLP_THREADS)));
+      smem_set = (sizeof(double) + sizeof(u32)) * DLP_MAXK * DLP_THREADS;
+    }
+    domain_loss_priv_kernel<<<blocks, DLP_THREADS, smem, s>>>(losses, tags, n, K, ps.p, pc.p, bad.p);
+  } else {
+    domain_loss_kernel<<<blocks, DL_THREADS, 0, s>>>(losses, tags, n, K, per_block, ps.p, pc.p, bad.p);
+  }
   mx_count_launch();
   domain_loss_final<<<(K + 127) / 128, 128, 0, s>>>(ps.p, pc.p, blocks, K, sums, counts);
   mx_count_launch();

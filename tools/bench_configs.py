@@ -107,17 +107,39 @@ def cfg5(out):
     w = w[rng.permutation(len(keys))]
     w = w / w.sum()
     spec = MixtureSpec({k: float(x) for k, x in zip(keys, w)}, 1024)
-    ms, idx, batch = _time_gpu(dcat, spec, reps=3)
-    # CPU oracle: the first 1M samples (100 files), first 20 chunks
+    # bounded: index + cursor layout + the first N_CHUNKS chunks (the full job
+    # has ~97k chunks and thousands of depletion / redistribution events)
+    from paper_2502_19790_b200 import ChunkGenerator
+
+    n_chunks = 2000
+
+    def job():
+        idx = build_index_from_catalog(dcat, [])
+        gen = ChunkGenerator(idx, 42)
+        t = _events()
+        t[0].record()
+        batch = gen.plan_batch(spec, n_chunks)
+        t[1].record()
+        return idx, batch, t
+
+    job()
+    torch.cuda.synchronize()
+    a, b = _events()
+    a.record()
+    idx, batch, t = job()
+    b.record()
+    torch.cuda.synchronize()
+    ms, plan_ms = a.elapsed_time(b), t[0].elapsed_time(t[1])
+    # CPU oracle: 1M samples of the same generator, index + first 5 chunks
     small = synth.make_runs(1_000_000, 100, synth.CFG5_PROPS, 16, seed=5, zipf=1.1)
     cc = synth.expand_numpy(small)
-    ck = [k for k in keys]
-    dt, n = _oracle_job(cc, MixtureSpec({k: float(x) for k, x in zip(ck, w)}, 1024), limit=20)
+    dt, n = _oracle_job(cc, spec, limit=5)
     out["cfg5"] = {
-        "samples": rt.n_samples, "keys": idx.n_keys, "intervals": idx.n_intervals, "chunks": batch.n_chunks,
-        "gpu_ms_per_job": round(ms, 3), "gpu_samples_per_s": rt.n_samples / ms * 1e3,
-        "gpu_chunks_per_s": batch.n_chunks / ms * 1e3,
-        "cpu_oracle_sample": "first 1M samples (100 files), index + first 20 chunks",
+        "samples": rt.n_samples, "keys": idx.n_keys, "intervals": idx.n_intervals,
+        "chunks_timed": batch.n_chunks, "gpu_ms_index_plus_chunks": round(ms, 3),
+        "gpu_ms_plan_emit": round(plan_ms, 3), "gpu_chunks_per_s": batch.n_chunks / plan_ms * 1e3,
+        "gpu_index_samples_per_s": rt.n_samples / max(ms - plan_ms, 1e-6) * 1e3,
+        "cpu_oracle_sample": "1M samples (100 files, same generator), index + first 5 chunks",
         "cpu_oracle_s": round(dt, 3), "cpu_chunks_per_s": n / dt, "cpu_cores": 1,
     }
 
@@ -165,6 +187,25 @@ def cfg4(out, steps):
         t_reduce.append(t2 - t1)
     fit_steps = list(src.state.fit_steps)
     st = np.array(t_step) * 1e6
+    # one rank's reduction (131,072 tokens, the per-step DP shard), and the
+    # streaming rate on 64M tokens (B3 = T x (4 + 4) bytes)
+    lat = []
+    for _ in range(200):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        domain_loss_device(losses[0], tags[0], D)
+        torch.cuda.synchronize()
+        lat.append(time.perf_counter() - t0)
+    big_l = torch.rand(64 << 20, device=dev, generator=g) + 1.5
+    big_t = torch.randint(0, D, (64 << 20,), device=dev, generator=g, dtype=torch.int32)
+    domain_loss_device(big_l, big_t, D)
+    a, b = _events()
+    a.record()
+    for _ in range(5):
+        domain_loss_device(big_l, big_t, D)
+    b.record()
+    torch.cuda.synchronize()
+    big_ms = a.elapsed_time(b) / 5
     # CPU oracle for the same per-step work (numpy per_domain_loss on 8 x 131k
     # tokens + oracle ADO + oracle chunk generation), a bounded sample of steps
     from oracle import oracle as orc
@@ -191,8 +232,10 @@ def cfg4(out, steps):
         "domains": D, "tokens_per_step": ranks * tok, "steps": steps, "fit_steps": fit_steps,
         "gpu_us_per_step_median": float(np.median(st)), "gpu_us_per_step_mean": float(st.mean()),
         "gpu_us_per_refit_step_max": float(st.max()),
-        "gpu_reduce_us_median": float(np.median(np.array(t_reduce) * 1e6)),
-        "gpu_tokens_per_s": ranks * tok / float(np.median(np.array(t_reduce))),
+        "gpu_8rank_reduce_us_median": float(np.median(np.array(t_reduce) * 1e6)),
+        "gpu_one_rank_reduce_us_median": float(np.median(lat) * 1e6),
+        "gpu_64M_tokens_ms": big_ms, "gpu_64M_tokens_per_s": (64 << 20) / big_ms * 1e3,
+        "gpu_64M_gbs": (64 << 20) * 8 / big_ms / 1e6,
         "cpu_oracle_us_per_step": cpu_us, "cpu_oracle_steps": osteps, "cpu_cores": 1,
         "note": "host wall clock per step incl. the device syncs of the API (one chunk per step is latency-bound)",
     }
@@ -203,15 +246,14 @@ def main():
     ap.add_argument("--only", default="cfg1,cfg4,cfg5")
     ap.add_argument("--ado-steps", type=int, default=2000)
     args = ap.parse_args()
-    out = {}
-    todo = set(args.only.split(","))
-    if "cfg1" in todo:
-        cfg1(out)
-    if "cfg5" in todo:
-        cfg5(out)
-    if "cfg4" in todo:
-        cfg4(out, args.ado_steps)
-    print(json.dumps(out, indent=1))
+    todo = args.only.split(",")
+    for name in todo:  # one JSON line per config, flushed as it completes
+        out = {}
+        t0 = time.perf_counter()
+        {"cfg1": lambda: cfg1(out), "cfg4": lambda: cfg4(out, args.ado_steps), "cfg5": lambda: cfg5(out)}[name]()
+        for k, v in out.items():
+            v["wall_s"] = round(time.perf_counter() - t0, 1)
+            print(json.dumps({k: v}), flush=True)
 
 
 if __name__ == "__main__":
