@@ -9,14 +9,16 @@
 //
 // Kernels: key_seed_kernel (device BLAKE2b of each key's canonical string),
 // cursor_shuffle_kernel (one warp per key; MT19937 state and the key's block
-// list staged in shared memory, the sequential Fisher-Yates run by one lane),
-// cursor_intervals_kernel (expand shuffled blocks to interval ids, warp scan),
+// list (16-bit offsets) in shared memory; warp-parallel rejection sampling and
+// conflict-free swap rounds, csrc/mt19937.cuh), CursorIvF (shuffled blocks ->
+// interval ids, one reduce-then-scan over all keys),
 // cum_len_kernel (u64 look-back scan of lengths in cursor order),
 // component_order_kernel (one shuffle of K ranks).
 #include "blake2b.cuh"
 #include "common.cuh"
 #include "mixtera_internal.cuh"
 #include "mt19937.cuh"
+#include "scan.cuh"
 
 namespace mx {
 
@@ -63,6 +65,10 @@ __global__ void key_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix
 
 // Per-warp shared memory: MT state + outputs + window pairs + the key's block
 // list (list_cap entries; a key with more blocks shuffles in global memory).
+// Per-warp shared memory: MT state + outputs + window pairs (CS_FIXED words)
+// and the key's block list as 16-bit offsets from the key's first block
+// (list_cap entries; a key with more blocks shuffles its u32 list in global
+// memory). Half-width entries double the keys resident per SM.
 constexpr int CS_FIXED = 2 * MT_N + 64;
 
 __global__ void __launch_bounds__(128)
@@ -70,16 +76,15 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
                       const u64* seeds, const u32* mt_base, u32* grp, u32* gid, u32* cur_blk, int list_cap) {
   extern __shared__ __align__(16) u32 cs_dyn[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpc = blockDim.x >> 5;
-  u32* mine = cs_dyn + (size_t)w * (CS_FIXED + list_cap);
+  u32* mine = cs_dyn + (size_t)w * (CS_FIXED + list_cap / 2);
   u32* s_mt = mine;
   u32* s_out = mine + MT_N;
   uint2* s_pairs = reinterpret_cast<uint2*>(mine + 2 * MT_N);
-  u32* s_list = mine + CS_FIXED;
+  unsigned short* s_list = reinterpret_cast<unsigned short*>(mine + CS_FIXED);
   for (long long k = blockIdx.x * (long long)wpc + w; k < K; k += (long long)gridDim.x * wpc) {
     const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
     const int nb = (int)(b1 - b0);
     const bool in_smem = nb <= list_cap;
-    u32* work = in_smem ? s_list : cur_blk + b0;
     // dataset groups (blocks are file-sorted and ds is nondecreasing in file
     // order): one group when first and last block share a dataset, else a
     // warp-parallel scan of dataset changes
@@ -99,12 +104,9 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
         }
         G += __popc(hm);
       }
-    } else {
-      if (lane == 0) {
-        grp[b0] = 0;
-        gid[b0] = 0;
-      }
-      for (int i = lane; i < nb; i += 32) work[i] = b0 + (u32)i;
+    } else if (lane == 0) {
+      grp[b0] = 0;
+      gid[b0] = 0;
     }
     __syncwarp();
     WarpMT mt{s_mt, s_out, s_pairs, MT_N};
@@ -115,91 +117,61 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
       const u32 gi = gid[b0 + g];
       const int s = (int)grp[b0 + gi];
       const int e = gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
-      if (G > 1) {  // single group: already filled above
-        for (int b = s + lane; b < e; b += 32) work[pos + b - s] = b0 + (u32)b;
+      // the dataset's blocks in file order, then shuffled (file order within
+      // the dataset, index.py:140-143)
+      if (in_smem) {
+        for (int b = s + lane; b < e; b += 32) s_list[pos + b - s] = (unsigned short)b;
         __syncwarp();
+        mt.shuffle(s_list + pos, e - s);
+      } else {
+        for (int b = s + lane; b < e; b += 32) cur_blk[b0 + pos + b - s] = b0 + (u32)b;
+        __syncwarp();
+        mt.shuffle(cur_blk + b0 + pos, e - s);
       }
-      mt.shuffle(work + pos, e - s);  // file order within the dataset
       pos += e - s;
     }
     __syncwarp();
     if (in_smem)
-      for (int i = lane; i < nb; i += 32) cur_blk[b0 + i] = s_list[i];
+      for (int i = lane; i < nb; i += 32) cur_blk[b0 + i] = b0 + s_list[i];
     __syncwarp();
   }
 }
 
-// civ: interval ids in cursor order; key k keeps its sorted-order index range
-__global__ void __launch_bounds__(256)
-cursor_intervals_kernel(long long K, const u32* key_blk_first, const u32* blk_first, const u32* cur_blk, u32* civ) {
-  const int lane = threadIdx.x & 31;
-  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
-  for (long long k = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5); k < K; k += warps) {
-    const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
-    u32 out = blk_first[b0];
-    for (u32 pos = b0; pos < b1; pos += 32) {
-      const u32 my = pos + lane;
-      u32 blk = 0, cnt = 0;
-      if (my < b1) {
-        blk = cur_blk[my];
-        cnt = blk_first[blk + 1] - blk_first[blk];
-      }
-      u32 inc = warp_incl_scan(cnt);
-      u32 dst = out + inc - cnt;
-      for (u32 t = 0; t < cnt; ++t) civ[dst + t] = blk_first[blk] + t;
-      out += __shfl_sync(MX_FULL, inc, 31);
-    }
+// civ: interval ids in cursor order. Cursor positions of key k occupy the
+// same index range as its intervals in sorted order, and keys are stored
+// consecutively, so the output position of block p (in cursor order, keys
+// concatenated) is the exclusive prefix of interval counts over [0, p).
+struct CursorIvF {
+  const u32* cur_blk;
+  const u32* blk_first;
+  u32* civ;
+  __device__ u64 value(long long p) const {
+    const u32 b = cur_blk[p];
+    return blk_first[b + 1] - blk_first[b];
   }
-}
+  __device__ void apply(long long p, u64 ex, u64 v) const {
+    const u32 f = blk_first[cur_blk[p]];
+    for (u32 t = 0; t < (u32)v; ++t) civ[ex + t] = f + t;
+  }
+  __device__ void total(u64) const {}
+};
 
-constexpr int CL_THREADS = 256;
-constexpr int CL_ITEMS = 8;
-constexpr int CL_TILE = CL_THREADS * CL_ITEMS;
-
-// cum[j+1] = sum of lengths of intervals perm[0..j] (perm = civ)
-__global__ void __launch_bounds__(CL_THREADS)
-cum_len_kernel(const u32* perm, const u32* start, const u32* end, long long n, u64* status, u32* tile_ctr, u64* cum) {
-  __shared__ u64 s_w[CL_THREADS / 32 + 1];
-  __shared__ int s_tile;
-  __shared__ u64 s_excl;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const int tile = s_tile;
-  const long long b = (long long)tile * CL_TILE + threadIdx.x * CL_ITEMS;
-  u64 v[CL_ITEMS], sum = 0;
-#pragma unroll
-  for (int q = 0; q < CL_ITEMS; ++q) {
-    long long i = b + q;
-    u64 l = 0;
-    if (i < n) {
-      u32 iv = perm[i];
-      l = end[iv] - start[iv];
-    }
-    v[q] = l;
-    sum += l;
+// ccum[j + 1] = samples of cursor positions [0, j] (interval perm[j])
+struct CumPermF {
+  const u32* perm;
+  const u32* start;
+  const u32* end;
+  u64* cum;
+  __device__ u64 value(long long j) const {
+    const u32 iv = perm[j];
+    return end[iv] - start[iv];
   }
-  u64 inc = warp_incl_scan(sum);
-  if (lane == 31) s_w[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    u64 x = lane < CL_THREADS / 32 ? s_w[lane] : 0;
-    u64 xi = warp_incl_scan(x);
-    if (lane < CL_THREADS / 32) s_w[lane] = xi - x;
-    u64 tot = __shfl_sync(MX_FULL, xi, 31);
-    u64 t = lookback_exclusive(status, tile, tot);
-    if (lane == 0) s_excl = t;
+  __device__ void apply(long long j, u64 ex, u64 v) const {
+    if (j == 0) cum[0] = 0;
+    cum[j + 1] = ex + v;
   }
-  __syncthreads();
-  u64 run = s_excl + s_w[warp] + inc - sum;
-  if (tile == 0 && threadIdx.x == 0) cum[0] = 0;
-#pragma unroll
-  for (int q = 0; q < CL_ITEMS; ++q) {
-    long long i = b + q;
-    run += v[q];
-    if (i < n) cum[i + 1] = run;
-  }
-}
+  __device__ void total(u64) const {}
+};
 
 __global__ void comp_total_kernel(long long K, const u32* key_blk_first, const u32* blk_first, const u64* iv_cum,
                                   u64* total) {
@@ -287,8 +259,8 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   {
     MxPhase ph2("cursor_shuffle", s);
     // list capacity = the largest key's block count (up to 16K entries, 64 KB)
-    const int cap = (int)std::min<long long>((ix->max_key_blocks + 31) / 32 * 32, 16384);
-    const size_t per_warp = sizeof(u32) * (CS_FIXED + cap);
+    const int cap = (int)std::min<long long>((ix->max_key_blocks + 63) / 64 * 64, 32768);
+    const size_t per_warp = sizeof(u32) * CS_FIXED + sizeof(unsigned short) * cap;
     const int wpc = per_warp <= 12 * 1024 ? 4 : 1;
     const size_t dyn = per_warp * wpc;
     MX_CUDA_TRY(cudaFuncSetAttribute(cursor_shuffle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
@@ -300,25 +272,9 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     mx_count_launch();
   }
   MX_CUDA_TRY(g->civ.alloc(I, s));
-  {
-    long long blocks = (K + 7) / 8;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    cursor_intervals_kernel<<<(unsigned)blocks, 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
-                                                            g->cur_blk.p, g->civ.p);
-    mx_count_launch();
-  }
+  if (int rc = gs_run(B, CursorIvF{g->cur_blk.p, ix->blk_first.p, g->civ.p}, s)) return rc;
   MX_CUDA_TRY(g->ccum.alloc(I + 1, s));
-  {
-    const int tiles = (int)((I + CL_TILE - 1) / CL_TILE);
-    DevBuf<u64> st;
-    DevBuf<u32> ctr;
-    MX_CUDA_TRY(st.alloc(tiles, s));
-    MX_CUDA_TRY(ctr.alloc(1, s));
-    MX_CUDA_TRY(cudaMemsetAsync(st.p, 0, sizeof(u64) * tiles, s));
-    MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32), s));
-    cum_len_kernel<<<tiles, CL_THREADS, 0, s>>>(g->civ.p, ix->iv_start.p, ix->iv_end.p, I, st.p, ctr.p, g->ccum.p);
-    mx_count_launch();
-  }
+  if (int rc = gs_run(I, CumPermF{g->civ.p, ix->iv_start.p, ix->iv_end.p, g->ccum.p}, s)) return rc;
   MX_CUDA_TRY(g->comp_total.alloc(K, s));
   comp_total_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
                                                                ix->iv_cum.p, g->comp_total.p);

@@ -86,6 +86,7 @@ struct IndexData {
   // are local, iv_nreal = real intervals behind each entry (1 if local)
   bool sharded = false;
   long long file_lo = 0, file_hi = 0;
+  long long n_local = 0;  // this rank's (real) intervals in the hybrid index
   DevBuf<u32> iv_nreal;
 };
 
@@ -105,7 +106,7 @@ struct GenData {
   // sharded index only: lcnt u32[I+1] local intervals before each cursor
   // position, lpos u32[#local] their positions, rcum u64[I+1] real intervals
   DevBuf<u32> lcnt, lpos;
-  DevBuf<u64> rcum;
+  DevBuf<u64> rcum, lstart;  // lstart[r] = ccum[lpos[r]]
   DevBuf<uint8_t> chunk_prefix;
   int chunk_prefix_len = 0;
   long long next_chunk_id = 0;

@@ -680,54 +680,6 @@ scan_pipe_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles, 
   }
 }
 
-// Exclusive scan of per-tile run counts: one CTA per 2048 counts (8
-// consecutive per thread, 16-byte loads), decoupled look-back across CTAs.
-// off[n] = total.
-constexpr int TO_THREADS = 256;
-constexpr int TO_ITEMS = 8;
-__global__ void __launch_bounds__(TO_THREADS)
-tile_offsets_kernel(long long n, const u32* cnt, u64* off, u64* status, u32* ctr) {
-  __shared__ u64 s_w[TO_THREADS / 32 + 1];
-  __shared__ int s_tile;
-  __shared__ u64 s_excl;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u);
-  __syncthreads();
-  const int tile = s_tile;
-  const long long i0 = (long long)tile * TO_THREADS * TO_ITEMS + (long long)threadIdx.x * TO_ITEMS;
-  u32 v[TO_ITEMS];
-  if (i0 + TO_ITEMS <= n) {
-    const uint4 a = *reinterpret_cast<const uint4*>(cnt + i0);
-    const uint4 b = *reinterpret_cast<const uint4*>(cnt + i0 + 4);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  } else {
-#pragma unroll
-    for (int q = 0; q < TO_ITEMS; ++q) v[q] = i0 + q < n ? cnt[i0 + q] : 0u;
-  }
-  u64 sum = 0;
-#pragma unroll
-  for (int q = 0; q < TO_ITEMS; ++q) sum += v[q];
-  const u64 inc = warp_incl_scan(sum);
-  if (lane == 31) s_w[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    const u64 x = lane < TO_THREADS / 32 ? s_w[lane] : 0;
-    const u64 xi = warp_incl_scan(x);
-    if (lane < TO_THREADS / 32) s_w[lane] = xi - x;
-    const u64 tot = __shfl_sync(MX_FULL, xi, 31);
-    const u64 t = lookback_exclusive(status, tile, tot);
-    if (lane == 0) s_excl = t;
-  }
-  __syncthreads();
-  u64 run = s_excl + s_w[warp] + inc - sum;
-#pragma unroll
-  for (int q = 0; q < TO_ITEMS; ++q) {
-    if (i0 + q < n) off[i0 + q] = run;
-    run += v[q];
-    if (i0 + q == n - 1) off[n] = run;
-  }
-}
-
 // Dense copy of the slot records (one warp per tile, order preserved).
 __global__ void slot_compact_kernel(long long ntiles, long long tile_len, const u32* cnt, const u64* off,
                                     const u32* k, const u32* f, const u32* s, const u32* e, u32* k2, u32* f2, u32* s2,

@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "mixtera_internal.cuh"
+#include "scan.cuh"
 
 namespace mx {
 
@@ -448,125 +449,6 @@ radix_downsweep(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2i
   }
 }
 
-// ---------------------------------------------------------------- finalize
-constexpr int SC_THREADS = 256;
-constexpr int SC_ITEMS = 8;
-constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
-
-// Block-wide exclusive scan helper for u64 (returns exclusive, writes total).
-__device__ __forceinline__ u64 block_excl_u64(u64 v, u64* s_w, u64* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  u64 inc = warp_incl_scan(v);
-  if (lane == 31) s_w[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    u64 x = lane < SC_THREADS / 32 ? s_w[lane] : 0;
-    u64 xi = warp_incl_scan(x);
-    if (lane < SC_THREADS / 32) s_w[lane] = xi - x;
-    if (lane == 31) s_w[SC_THREADS / 32] = xi;
-  }
-  __syncthreads();
-  *total = s_w[SC_THREADS / 32];
-  return s_w[warp] + inc - v;
-}
-
-// Boundary flags -> key ranks / block ids; writes the block + key tables.
-// Packed value: (key changes << 32) | block changes.
-__global__ void __launch_bounds__(SC_THREADS)
-index_bounds_kernel(const u32* key, const u32* file, long long n, u64* status, u32* tile_ctr,
-                    u32* blk_first, u32* blk_file, u32* blk_key,
-                    u32* key_blk_first, u32* key_packed, u64* totals) {
-  __shared__ u64 s_w[SC_THREADS / 32 + 1];
-  __shared__ int s_tile;
-  __shared__ u64 s_excl;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const int tile = s_tile;
-  const long long b = (long long)tile * SC_TILE + threadIdx.x * SC_ITEMS;
-  u64 v[SC_ITEMS];
-  u64 sum = 0;
-#pragma unroll
-  for (int q = 0; q < SC_ITEMS; ++q) {
-    long long i = b + q;
-    u64 f = 0;
-    if (i < n) {
-      bool kc = i == 0 || key[i] != key[i - 1];
-      bool bc = kc || file[i] != file[i - 1];
-      f = ((u64)kc << 32) | (u64)bc;
-    }
-    v[q] = f;
-    sum += f;
-  }
-  u64 tot;
-  u64 ex = block_excl_u64(sum, s_w, &tot);
-  if (threadIdx.x < 32) {
-    u64 t = lookback_exclusive(status, tile, tot);
-    if (threadIdx.x == 0) {
-      s_excl = t;
-      if ((long long)(tile + 1) * SC_TILE >= n) *totals = t + tot;
-    }
-  }
-  __syncthreads();
-  u64 run = s_excl + ex;
-#pragma unroll
-  for (int q = 0; q < SC_ITEMS; ++q) {
-    long long i = b + q;
-    run += v[q];
-    if (i < n && (v[q] & 1)) {
-      u32 k = (u32)(run >> 32) - 1, blk = (u32)run - 1;
-      blk_first[blk] = (u32)i;
-      blk_file[blk] = file[i];
-      blk_key[blk] = k;
-      if (v[q] >> 32) {
-        key_blk_first[k] = blk;
-        key_packed[k] = key[i];
-      }
-    }
-  }
-}
-
-// u64 inclusive scan of interval lengths -> cum[i + 1]; cum[0] = 0.
-__global__ void __launch_bounds__(SC_THREADS)
-interval_cum_kernel(const u32* start, const u32* end, long long n, u64* status, u32* tile_ctr,
-                    u64* cum, DevError* err) {
-  __shared__ u64 s_w[SC_THREADS / 32 + 1];
-  __shared__ int s_tile;
-  __shared__ u64 s_excl;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const int tile = s_tile;
-  const long long b = (long long)tile * SC_TILE + threadIdx.x * SC_ITEMS;
-  u64 v[SC_ITEMS];
-  u64 sum = 0;
-#pragma unroll
-  for (int q = 0; q < SC_ITEMS; ++q) {
-    long long i = b + q;
-    u64 l = 0;
-    if (i < n) {
-      u32 s = start[i], e = end[i];
-      if (e <= s) atomicOr(&err->overlap, 1u);
-      l = e > s ? e - s : 0;
-    }
-    v[q] = l;
-    sum += l;
-  }
-  u64 tot;
-  u64 ex = block_excl_u64(sum, s_w, &tot);
-  if (threadIdx.x < 32) {
-    u64 t = lookback_exclusive(status, tile, tot);
-    if (threadIdx.x == 0) s_excl = t;
-  }
-  __syncthreads();
-  u64 run = s_excl + ex;
-  if (b == 0 && threadIdx.x == 0) cum[0] = 0;
-#pragma unroll
-  for (int q = 0; q < SC_ITEMS; ++q) {
-    long long i = b + q;
-    run += v[q];
-    if (i < n) cum[i + 1] = run;
-  }
-}
-
 // ---------------------------------------------------------------- host side
 template <int SEGS, int PC>
 static int launch_pipe(const S1Args& a, const TileMeta* m, long long ntiles, long long nstaged, int stages,
@@ -648,6 +530,16 @@ static void dispatch_direct(const S1Args& a, const TileMeta* m, long long ntiles
   }
   launch_direct<SEGS, 0>(a, m, ntiles, smem_lut, lut_total, s, done);
 }
+
+// exclusive offsets of the per-tile run counts (slots -> dense records)
+struct TileOffF {
+  const u32* cnt;
+  u64* off;
+  long long n;
+  __device__ u64 value(long long i) const { return cnt[i]; }
+  __device__ void apply(long long i, u64 ex, u64) const { off[i] = ex; }
+  __device__ void total(u64 t) const { off[n] = t; }
+};
 
 int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   if (d->n_props < 1 || d->n_props > MX_MAX_PROPS)
@@ -841,14 +733,9 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   u32 *kb = k2.p, *fb = f2.p, *sb = s2.p, *eb = e2.p;
   std::unique_ptr<MxPhase> ph_sort(new MxPhase("radix_sort", s));
   if (slot_mode) {  // per-tile slots -> dense records (order preserved)
-    DevBuf<u64> toff, tst;
-    const int otiles = (int)((ntiles + TO_THREADS * TO_ITEMS - 1) / (TO_THREADS * TO_ITEMS));
+    DevBuf<u64> toff;
     MX_CUDA_TRY(toff.alloc(ntiles + 1, s));
-    MX_CUDA_TRY(tst.alloc(otiles, s));
-    MX_CUDA_TRY(cudaMemsetAsync(tst.p, 0, sizeof(u64) * otiles, s));
-    MX_CUDA_TRY(cudaMemsetAsync(ctr.p + 2, 0, sizeof(u32), s));
-    tile_offsets_kernel<<<otiles, TO_THREADS, 0, s>>>(ntiles, t_cnt.p, toff.p, tst.p, ctr.p + 2);
-    mx_count_launch();
+    if (int rc = gs_run(ntiles, TileOffF{t_cnt.p, toff.p, ntiles}, s)) return rc;
     slot_compact_kernel<<<std::min(ntiles, n_sm * 16), 256, 0, s>>>(ntiles, tile_len, t_cnt.p, toff.p, rk.p, rf.p,
                                                                      rs.p, re.p, k2.p, f2.p, s2.p, e2.p);
     mx_count_launch();
@@ -877,6 +764,52 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   }
   return index_finalize(&ix, I, s);
 }
+
+// key / block boundaries: value = (key change << 32) | (key or file change);
+// the inclusive count gives the dense key rank and (key, file) block id
+struct BoundsF {
+  const u32* key;
+  const u32* file;
+  u32 *blk_first, *blk_file, *blk_key, *key_blk_first, *key_packed;
+  u64* totals;
+  __device__ u64 value(long long i) const {
+    const bool kc = i == 0 || key[i] != key[i - 1];
+    const bool bc = kc || file[i] != file[i - 1];
+    return ((u64)kc << 32) | (u64)bc;
+  }
+  __device__ void apply(long long i, u64 ex, u64 v) const {
+    if (!(v & 1)) return;
+    const u64 run = ex + v;
+    const u32 k = (u32)(run >> 32) - 1, blk = (u32)run - 1;
+    blk_first[blk] = (u32)i;
+    blk_file[blk] = file[i];
+    blk_key[blk] = k;
+    if (v >> 32) {
+      key_blk_first[k] = blk;
+      key_packed[k] = key[i];
+    }
+  }
+  __device__ void total(u64 t) const { *totals = t; }
+};
+
+// cum[i + 1] = samples of intervals [0, i]; an empty or inverted interval
+// flags IndexBuildError
+struct CumF {
+  const u32* start;
+  const u32* end;
+  u64* cum;
+  DevError* err;
+  __device__ u64 value(long long i) const {
+    const u32 s = start[i], e = end[i];
+    return e > s ? e - s : 0;
+  }
+  __device__ void apply(long long i, u64 ex, u64 v) const {
+    if (i == 0) cum[0] = 0;
+    cum[i + 1] = ex + v;
+    if (end[i] <= start[i]) atomicOr(&err->overlap, 1u);
+  }
+  __device__ void total(u64) const {}
+};
 
 // max over keys of (blocks of the key); totals = (n_keys << 32) | n_blocks
 __global__ void key_maxblk_kernel(const u32* key_blk_first, const u64* totals, u32* out) {
@@ -914,26 +847,17 @@ int index_finalize(IndexData* ixp, long long I, cudaStream_t s) {
   MX_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(err.p) + 8, 0, 8, s));
   DevError h_err;
   // ---- boundaries and cumulative lengths
-  const int stiles = (int)((I + SC_TILE - 1) / SC_TILE);
-  DevBuf<u64> st2;
-  MX_CUDA_TRY(st2.alloc(stiles, s));
   MX_CUDA_TRY(ix.blk_first.alloc(I + 1, s));
   MX_CUDA_TRY(ix.blk_file.alloc(I, s));
   MX_CUDA_TRY(ix.blk_key.alloc(I, s));
   MX_CUDA_TRY(ix.key_blk_first.alloc(I + 1, s));
   MX_CUDA_TRY(ix.key_packed.alloc(I, s));
   MX_CUDA_TRY(ix.iv_cum.alloc(I + 1, s));
-  MX_CUDA_TRY(cudaMemsetAsync(st2.p, 0, sizeof(u64) * stiles, s));
-  MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32) * 2, s));
   std::unique_ptr<MxPhase> ph_scan(new MxPhase("index_scans", s));
-  index_bounds_kernel<<<stiles, SC_THREADS, 0, s>>>(ix.iv_key.p, ix.iv_file.p, I, st2.p, ctr.p,
-                                                    ix.blk_first.p, ix.blk_file.p, ix.blk_key.p,
-                                                    ix.key_blk_first.p, ix.key_packed.p, scratch64.p);
-  mx_count_launch();
-  MX_CUDA_TRY(cudaMemsetAsync(st2.p, 0, sizeof(u64) * stiles, s));
-  interval_cum_kernel<<<stiles, SC_THREADS, 0, s>>>(ix.iv_start.p, ix.iv_end.p, I, st2.p, ctr.p + 1,
-                                                    ix.iv_cum.p, err.p);
-  mx_count_launch();
+  if (int rc = gs_run(I, BoundsF{ix.iv_key.p, ix.iv_file.p, ix.blk_first.p, ix.blk_file.p, ix.blk_key.p,
+                                 ix.key_blk_first.p, ix.key_packed.p, scratch64.p}, s))
+    return rc;
+  if (int rc = gs_run(I, CumF{ix.iv_start.p, ix.iv_end.p, ix.iv_cum.p, err.p}, s)) return rc;
   ph_scan.reset();
   // largest key (in blocks): sizes the cursor shuffle's shared-memory lists
   DevBuf<u32> maxblk;

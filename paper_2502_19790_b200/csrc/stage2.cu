@@ -39,6 +39,7 @@
 #include "blake2b.cuh"
 #include "common.cuh"
 #include "mixtera_internal.cuh"
+#include "scan.cuh"
 
 namespace mx {
 
@@ -934,9 +935,11 @@ struct EmitArgs {
   const u32* iv_start;
   const u32* iv_end;
   const u32* iv_file;
-  // sharded (hybrid) index: cut only this rank's intervals (shard.cu)
+  // sharded (hybrid) index: cut only this rank's intervals (shard.cu);
+  // lstart[r] = stream offset (ccum) of the r-th local cursor position
   const u32* lcnt;
   const u32* lpos;
+  const u64* lstart;
 };
 
 __device__ __forceinline__ long long ub_u64(const u64* v, long long lo, long long hi, u64 x) {
@@ -980,6 +983,31 @@ __device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink s
     const long long ib = a.blk_first[a.key_blk_first[c]];
     const long long ie = a.blk_first[a.key_blk_first[c + 1]];
     const u64 cb = a.ccum[ib];
+    if (a.lcnt) {  // sharded: search only this rank's intervals of component c
+      const long long r0 = a.lcnt[ib], r1 = a.lcnt[ie];
+      // first local interval ending after lo, first starting at or after hi
+      long long ra = ub_u64(a.lstart, r0, r1, cb + lo_abs) - 1;
+      if (ra < r0) ra = r0;
+      else if (a.ccum[a.lpos[ra] + 1] <= cb + lo_abs) ++ra;
+      const long long rb = ub_u64(a.lstart, r0, r1, cb + hi_abs - 1);
+      if (!WRITE) {
+        if (rb > ra) n += (u64)(rb - ra);
+      } else {
+        for (long long r = ra; r < rb; ++r) {
+          const long long jj = a.lpos[r];
+          const u32 iv = a.civ[jj];
+          const u64 off = a.ccum[jj] - cb;
+          const u64 len = a.ccum[jj + 1] - a.ccum[jj];
+          const u64 from = lo_abs > off ? lo_abs : off;
+          const u64 to = hi_abs < off + len ? hi_abs : off + len;
+          sink(n++, a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
+               a.iv_start[iv] + (u32)(to - off));
+        }
+      }
+      x = seg_end < y ? seg_end : y;
+      ++i;
+      continue;
+    }
     long long j = ub_u64(a.ccum, ib, ie, cb + lo_abs) - 1;
     const long long j1 = ub_u64(a.ccum, ib, ie, cb + hi_abs - 1) - 1;
     auto cut = [&](long long jj) {
@@ -991,12 +1019,7 @@ __device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink s
       sink(n++, a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
            a.iv_start[iv] + (u32)(to - off));
     };
-    if (a.lcnt) {  // local intervals among cursor positions [j, j1]
-      const u32 r0 = a.lcnt[j], r1 = a.lcnt[j1 + 1];
-      if (!WRITE) n += r1 - r0;
-      else
-        for (u32 r = r0; r < r1; ++r) cut(a.lpos[r]);
-    } else if (!WRITE) {
+    if (!WRITE) {
       n += (u64)(j1 - j + 1);
     } else {
       for (; j <= j1; ++j) cut(j);
@@ -1175,14 +1198,90 @@ normalize_kernel(const u32* big_list, const u32* big_cnt, const u64* chunk_piece
   }
 }
 
+// One thread: sort n <= 4 pieces by (mixture key, file, start) and merge
+// contiguous ones in place.
+__device__ __forceinline__ void normalize_tiny(u64 o0, u32 n, u32* pm, u32* pf, u32* ps, u32* pe, u64* cnt) {
+  unsigned long long hi[4];
+  u32 lo[4], en[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool ok = (u32)i < n;
+    hi[i] = ok ? ((unsigned long long)pm[o0 + i] << 32) | pf[o0 + i] : ~0ull;
+    lo[i] = ok ? ps[o0 + i] : ~0u;
+    en[i] = ok ? pe[o0 + i] : ~0u;
+  }
+  auto cswap = [&](int a, int b) {
+    if (hi[b] < hi[a] || (hi[b] == hi[a] && lo[b] < lo[a])) {
+      const unsigned long long th = hi[a];
+      hi[a] = hi[b];
+      hi[b] = th;
+      const u32 tl = lo[a];
+      lo[a] = lo[b];
+      lo[b] = tl;
+      const u32 te = en[a];
+      en[a] = en[b];
+      en[b] = te;
+    }
+  };
+  cswap(0, 1);
+  cswap(2, 3);
+  cswap(0, 2);
+  cswap(1, 3);
+  cswap(1, 2);
+  u32 m = 0;
+#pragma unroll
+  for (u32 i = 0; i < 4; ++i) {
+    if (i >= n) break;
+    if (m > 0 && hi[i] == hi[m - 1] && lo[i] == en[m - 1]) {
+      en[m - 1] = en[i];
+    } else {
+      hi[m] = hi[i];
+      lo[m] = lo[i];
+      en[m] = en[i];
+      ++m;
+    }
+  }
+  for (u32 i = 0; i < m; ++i) {
+    pm[o0 + i] = (u32)(hi[i] >> 32);
+    pf[o0 + i] = (u32)hi[i];
+    ps[o0 + i] = lo[i];
+    pe[o0 + i] = en[i];
+  }
+  *cnt = m;
+}
+
+// Thread per chunk: chunks of <= 4 pieces are normalised here (the sharded
+// case has ~2-3 local pieces per chunk); the others are listed for the warp
+// kernel.
+__global__ void normalize_tiny_kernel(long long n_chunks, const u64* chunk_piece_off, u32* pm, u32* pf, u32* ps,
+                                      u32* pe, u64* merged_cnt, u32* wide_list, u32* wide_cnt) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool in = k < n_chunks;
+  u64 o0 = 0;
+  u32 n = 0;
+  if (in) {
+    o0 = chunk_piece_off[k];
+    n = (u32)(chunk_piece_off[k + 1] - o0);
+  }
+  const bool wide = in && n > 4;
+  const u32 wm = __ballot_sync(MX_FULL, wide);
+  u32 base = 0;
+  if ((threadIdx.x & 31) == 0 && wm) base = atomicAdd(wide_cnt, (u32)__popc(wm));
+  base = __shfl_sync(MX_FULL, base, 0);
+  if (wide) wide_list[base + __popc(wm & ((1u << (threadIdx.x & 31)) - 1))] = (u32)k;
+  else if (in) normalize_tiny(o0, n, pm, pf, ps, pe, merged_cnt + k);
+}
+
 // Chunks of <= 32 pieces (the common case): one warp per chunk, bitonic sort
 // of (mixture key, file, start) across lanes with shuffles, merge by ballot.
 __global__ void __launch_bounds__(256)
-normalize_warp_kernel(long long n_chunks, const u64* chunk_piece_off, u32* pm, u32* pf, u32* ps, u32* pe,
-                      u64* merged_cnt, u32* big_list, u32* big_cnt) {
+normalize_warp_kernel(const u32* wide_list, const u32* wide_cnt, const u64* chunk_piece_off, u32* pm, u32* pf,
+                      u32* ps, u32* pe, u64* merged_cnt, u32* big_list, u32* big_cnt) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long k = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n_chunks; k += warps) {
+  const long long n_wide = *wide_cnt;
+  for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_wide; w += warps) {
+    const long long k = wide_list[w];
     const u64 o0 = chunk_piece_off[k];
     const u32 n = (u32)(chunk_piece_off[k + 1] - o0);
     if (n > 32) {  // left to normalize_kernel
@@ -1231,65 +1330,26 @@ normalize_warp_kernel(long long n_chunks, const u64* chunk_piece_off, u32* pm, u
   }
 }
 
-// Exclusive scan (decoupled look-back) of u64 counts; out[n] = total.
+// Exclusive scan of u64 counts (reduce-then-scan, scan.cuh); out[n] = total.
 template <typename OUT>
-__global__ void __launch_bounds__(256)
-excl_scan_kernel(const u64* in, long long n, OUT* out, u64* status, u32* tile_ctr) {
-  constexpr int ITEMS = 8, TILE = 256 * ITEMS;
-  __shared__ u64 s_w[9];
-  __shared__ int s_tile;
-  __shared__ u64 s_excl;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const int tile = s_tile;
-  const long long b = (long long)tile * TILE + threadIdx.x * ITEMS;
-  u64 v[ITEMS], sum = 0;
-#pragma unroll
-  for (int q = 0; q < ITEMS; ++q) {
-    v[q] = b + q < n ? in[b + q] : 0;
-    sum += v[q];
-  }
-  const u64 inc = warp_incl_scan(sum);
-  if (lane == 31) s_w[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    const u64 x = lane < 8 ? s_w[lane] : 0;
-    const u64 xi = warp_incl_scan(x);
-    if (lane < 8) s_w[lane] = xi - x;
-    const u64 tot = __shfl_sync(MX_FULL, xi, 31);
-    const u64 t = lookback_exclusive(status, tile, tot);
-    if (lane == 0) {
-      s_excl = t;
-      if ((long long)(tile + 1) * TILE >= n) out[n] = (OUT)(t + tot);
-    }
-  }
-  __syncthreads();
-  u64 run = s_excl + s_w[warp] + inc - sum;
-#pragma unroll
-  for (int q = 0; q < ITEMS; ++q) {
-    if (b + q < n) out[b + q] = (OUT)run;
-    run += v[q];
-  }
-}
+struct ExclScanF {
+  const u64* in;
+  OUT* out;
+  long long n;
+  __device__ u64 value(long long i) const { return in[i]; }
+  __device__ void apply(long long i, u64 ex, u64) const { out[i] = (OUT)ex; }
+  __device__ void total(u64 t) const { out[n] = (OUT)t; }
+};
 
+// exclusive scan of u64 counts; out[n] = total (in == out allowed: an item is
+// read and written by the same thread)
 template <typename OUT>
 static int excl_scan(const u64* in, long long n, OUT* out, cudaStream_t s) {
-  const long long tiles = (n + 2047) / 2048;
-  if (tiles == 0) {
+  if (n <= 0) {
     MX_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(OUT), s));
     return MX_OK;
   }
-  DevBuf<u64> st;
-  DevBuf<u32> ctr;
-  MX_CUDA_TRY(st.alloc(tiles, s));
-  MX_CUDA_TRY(ctr.alloc(1, s));
-  MX_CUDA_TRY(cudaMemsetAsync(st.p, 0, sizeof(u64) * tiles, s));
-  MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32), s));
-  excl_scan_kernel<OUT><<<(unsigned)tiles, 256, 0, s>>>(in, n, out, st.p, ctr.p);
-  mx_count_launch();
-  MX_CUDA_TRY(cudaGetLastError());
-  return MX_OK;
+  return gs_run(n, ExclScanF<OUT>{in, out, n}, s);
 }
 
 int excl_scan_ll(const u64* in, long long n, long long* out, cudaStream_t s) { return excl_scan<long long>(in, n, out, s); }
@@ -1298,15 +1358,39 @@ int excl_scan_ll(const u64* in, long long n, long long* out, cudaStream_t s) { r
 __global__ void compact_warp_kernel(long long n_chunks, const u64* chunk_piece_off, const long long* res_off,
                                     const u32* pm, const u32* pf, const u32* ps, const u32* pe, u32* rm, u32* rf,
                                     u32* rs, u32* re) {
+  const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long k = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n_chunks; k += warps) {
-    const u64 src = chunk_piece_off[k];
-    const long long dst = res_off[k], n = res_off[k + 1] - dst;
-    for (long long i = threadIdx.x & 31; i < n; i += 32) {
-      rm[dst + i] = pm[src + i];
-      rf[dst + i] = pf[src + i];
-      rs[dst + i] = ps[src + i];
-      re[dst + i] = pe[src + i];
+  // a warp takes 32 consecutive chunks: each lane copies its own chunk when
+  // it has <= 4 ranges, then the warp copies the larger ones together
+  for (long long g = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; g < n_chunks;
+       g += warps * 32) {
+    const long long k = g + lane;
+    long long n = 0, dst = 0;
+    u64 src = 0;
+    if (k < n_chunks) {
+      src = chunk_piece_off[k];
+      dst = res_off[k];
+      n = res_off[k + 1] - dst;
+    }
+    u32 wide = __ballot_sync(MX_FULL, n > 4);
+    if (n <= 4)
+      for (long long i = 0; i < n; ++i) {
+        rm[dst + i] = pm[src + i];
+        rf[dst + i] = pf[src + i];
+        rs[dst + i] = ps[src + i];
+        re[dst + i] = pe[src + i];
+      }
+    while (wide) {
+      const int l = __ffs(wide) - 1;
+      wide &= wide - 1;
+      const u64 s0 = __shfl_sync(MX_FULL, src, l);
+      const long long d0 = __shfl_sync(MX_FULL, dst, l), n0 = __shfl_sync(MX_FULL, n, l);
+      for (long long i = lane; i < n0; i += 32) {
+        rm[d0 + i] = pm[s0 + i];
+        rf[d0 + i] = pf[s0 + i];
+        rs[d0 + i] = ps[s0 + i];
+        re[d0 + i] = pe[s0 + i];
+      }
     }
   }
 }
@@ -1356,17 +1440,46 @@ __global__ void compact_kernel(long long n_chunks, const u64* chunk_piece_off, c
 // chunk seeds: derive_seed(job_seed, "chunk", chunk_id)  (chunks.py:188)
 __global__ void chunk_seed_kernel(long long n, long long first_id, const uint8_t* prefix, int prefix_len, u64* seeds,
                                   long long* ids) {
+  __shared__ uint8_t s_pre[96];
+  for (int i = threadIdx.x; i < prefix_len && i < 96; i += blockDim.x) s_pre[i] = prefix[i];
+  __syncthreads();
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= n) return;
-  uint8_t dec[20];
   const long long id = first_id + k;
-  int dl = u64_to_dec((u64)id, dec);
-  Blake2b b;
-  b.init();
-  b.bytes(prefix, prefix_len);
-  b.len8((u64)dl);
-  b.bytes(dec, dl);
-  seeds[k] = b.seed63();
+  // message = prefix || len8BE(len(str(id))) || str(id)   (seeding.py:18-28)
+  u64 v = (u64)id;
+  int dl = 1;
+  for (u64 t = v; t >= 10; t /= 10) ++dl;
+  if (prefix_len + 8 + dl <= 128 && prefix_len <= 96) {
+    u64 dec[3] = {0, 0, 0};  // str(id) as bytes, 8 per word (registers: constant indices below)
+    {
+      u64 t = v;
+      for (int pos = dl - 1; pos >= 0; --pos) {
+        const u64 c = (u64)('0' + t % 10);
+        t /= 10;
+        if (pos < 8) dec[0] |= c << (8 * pos);
+        else if (pos < 16) dec[1] |= c << (8 * (pos - 8));
+        else dec[2] |= c << (8 * (pos - 16));
+      }
+    }
+    const int P = prefix_len;
+    seeds[k] = blake2b_seed63_1block(P + 8 + dl, [&](int i) -> uint8_t {
+      if (i < P) return s_pre[i];
+      if (i < P + 8) return (uint8_t)(i == P + 7 ? dl : 0);  // dl < 256
+      const int d = i - P - 8;                                // digit d of str(id)
+      const u64 word = d < 8 ? dec[0] : d < 16 ? dec[1] : dec[2];
+      return (uint8_t)(word >> (8 * (d & 7)));
+    });
+  } else {
+    uint8_t dec[20];
+    u64_to_dec(v, dec);
+    Blake2b b;
+    b.init();
+    b.bytes(prefix, prefix_len);
+    b.len8((u64)dl);
+    b.bytes(dec, dl);
+    seeds[k] = b.seed63();
+  }
   ids[k] = id;
 }
 
@@ -1543,6 +1656,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   a.iv_file = ix->iv_file.p;
   a.lcnt = g->lcnt.p;
   a.lpos = g->lpos.p;
+  a.lstart = g->lstart.p;
   DevBuf<u64> pair_off;
   MX_CUDA_TRY(pair_off.alloc(n_pairs + 1, s));
   const unsigned pb = (unsigned)((n_pairs + 255) / 256);
@@ -1572,9 +1686,16 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
     MX_CUDA_TRY(blist.alloc(n_chunks, s));
     MX_CUDA_TRY(bcnt.alloc(1, s));
     MX_CUDA_TRY(cudaMemsetAsync(bcnt.p, 0, sizeof(u32), s));
+    DevBuf<u32> wlist, wcnt;
+    MX_CUDA_TRY(wlist.alloc(n_chunks, s));
+    MX_CUDA_TRY(wcnt.alloc(1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(wcnt.p, 0, sizeof(u32), s));
+    normalize_tiny_kernel<<<(unsigned)((n_chunks + 255) / 256), 256, 0, s>>>(n_chunks, cpo.p, pm.p, pf.p, ps.p, pe.p,
+                                                                           mcnt.p, wlist.p, wcnt.p);
+    mx_count_launch();
     const long long wgrid = std::min<long long>((n_chunks + 7) / 8, 148 * 16);
-    normalize_warp_kernel<<<(unsigned)wgrid, 256, 0, s>>>(n_chunks, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p, blist.p,
-                                                          bcnt.p);
+    normalize_warp_kernel<<<(unsigned)wgrid, 256, 0, s>>>(wlist.p, wcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p,
+                                                          blist.p, bcnt.p);
     mx_count_launch();
     long long grid = n_chunks < 148 * 4 ? n_chunks : 148 * 4;
     normalize_kernel<<<(unsigned)grid, NM_THREADS, 0, s>>>(blist.p, bcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p,
@@ -1587,7 +1708,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(g->res_start.reserve(cap, s));
   MX_CUDA_TRY(g->res_end.reserve(cap, s));
   {
-    const long long grid = std::min<long long>((n_chunks + 7) / 8, 148 * 16);
+    const long long grid = std::min<long long>((n_chunks + 255) / 256, 148 * 16);
     compact_warp_kernel<<<(unsigned)grid, 256, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
                                                        g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p);
     mx_count_launch();
@@ -1843,6 +1964,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     a.iv_file = ix->iv_file.p;
     a.lcnt = g->lcnt.p;
     a.lpos = g->lpos.p;
+    a.lstart = g->lstart.p;
     const long long slots = max_chunks * NM_CAP;
     struct { u32* p; } gm, gf, gs, ge, ovf;
     struct { u64* p; } cnt;

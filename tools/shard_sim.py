@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--world", type=int, default=8)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--ranks", default="0", help="comma list of ranks to time (all are run)")
+    ap.add_argument("--trace", action="store_true", help="CUPTI kernel summary of rank 0's hybrid+gen+plan")
     args = ap.parse_args()
     W = args.world
     dev = torch.device("cuda", 0)
@@ -79,7 +80,13 @@ def main():
     timed_ranks = {int(r) for r in args.ranks.split(",")}
     results = []
     per_rank = {}
+    prof = None
     for r, x in enumerate(locs):
+        if args.trace and r == 0:
+            from torch.profiler import ProfilerActivity, profile
+
+            prof = profile(activities=[ProfilerActivity.CUDA])
+            prof.__enter__()
         L.mx_profile_reset()
         L.mx_profile_enable(1)
         hyb, t_h, _ = timed(lambda: hybrid_index(x["idx"], x["dcat"], tables, counts, gkeys, r * nf, file_ds,
@@ -96,6 +103,18 @@ def main():
         _lib.check(L.mx_gen_result_export(gen._h, off.data_ptr(), *(cols4[f].data_ptr() for f in range(4)),
                                           C.c_void_p(_lib.stream_ptr())))
         results.append((off, cols4[:, :rr], rr))
+        if prof is not None and r == 0:
+            torch.cuda.synchronize()
+            prof.__exit__(None, None, None)
+            agg = {}
+            for e in prof.events():
+                if e.device_type.name == "CUDA":
+                    a = agg.setdefault(e.name[:60], [0, 0.0])
+                    a[0] += 1
+                    a[1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+            for k, (n_, us) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
+                print(f"  {us:9.1f} us  x{n_:3d}  {k}", file=sys.stderr)
+            prof = None
         if r in timed_ranks:
             per_rank[r] = {"hybrid_intervals": hyb.n_intervals, "hybrid_ms": round(t_h, 3),
                            "gen_create_ms": round(t_g, 3), "plan_emit_ms": round(t_p, 3), "phases_ms": phases,
@@ -120,6 +139,16 @@ def main():
 
     merge()
     _, t_m, _ = timed(merge)
+    if args.trace:
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA]) as pm:
+            merge()
+            torch.cuda.synchronize()
+        for e in pm.key_averages():
+            if e.device_type.name == "CUDA":
+                t = getattr(e, "device_time_total", 0) or getattr(e, "cuda_time_total", 0)
+                print(f"  merge: {t:9.1f} us  {e.key[:60]}", file=sys.stderr)
     report.update(merge_ms=round(t_m, 3), global_pieces=int(total), pieces_allgather_bytes=int(W * capr * 16),
                   global_chunks=int(n))
     print(json.dumps(report))
