@@ -1,6 +1,7 @@
 // C-ABI entry points (include/mixtera_b200.h): argument checks, handle
 // ownership, error strings, host<->device copies of small results.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -259,6 +260,10 @@ int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out) {
   return MX_OK;
 }
 
+// Device buffers are released stream-ordered (cudaFreeAsync); waiting for
+// the stream here keeps the pool's next allocations of the same sizes on
+// already-released memory (measured: without it the next job's allocations
+// stall and a cfg2 job takes 2.6-3.3 ms instead of 1.66 ms).
 int mx_index_free(mx_index* index) {
   if (!index) return MX_OK;
   cudaStream_t s = index->d.stream;

@@ -1357,9 +1357,22 @@ int excl_scan_ll(const u64* in, long long n, long long* out, cudaStream_t s) { r
 // Dense copy of each chunk's merged ranges (one warp per chunk).
 __global__ void compact_warp_kernel(long long n_chunks, const u64* chunk_piece_off, const long long* res_off,
                                     const u32* pm, const u32* pf, const u32* ps, const u32* pe, u32* rm, u32* rf,
-                                    u32* rs, u32* re) {
+                                    u32* rs, u32* re, bool grouped) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  if (!grouped) {  // larger chunks (single GPU): one warp per chunk
+    for (long long k = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); k < n_chunks; k += warps) {
+      const u64 src = chunk_piece_off[k];
+      const long long dst = res_off[k], n = res_off[k + 1] - dst;
+      for (long long i = lane; i < n; i += 32) {
+        rm[dst + i] = pm[src + i];
+        rf[dst + i] = pf[src + i];
+        rs[dst + i] = ps[src + i];
+        re[dst + i] = pe[src + i];
+      }
+    }
+    return;
+  }
   // a warp takes 32 consecutive chunks: each lane copies its own chunk when
   // it has <= 4 ranges, then the warp copies the larger ones together
   for (long long g = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; g < n_chunks;
@@ -1708,9 +1721,12 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(g->res_start.reserve(cap, s));
   MX_CUDA_TRY(g->res_end.reserve(cap, s));
   {
-    const long long grid = std::min<long long>((n_chunks + 255) / 256, 148 * 16);
+    // few ranges per chunk (sharded ranks): lanes copy chunks; else warps
+    const bool grouped = g->ix->sharded;
+    const long long grid = std::min<long long>(grouped ? (n_chunks + 255) / 256 : (n_chunks + 7) / 8, 148 * 16);
     compact_warp_kernel<<<(unsigned)grid, 256, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
-                                                       g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p);
+                                                       g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p,
+                                                       grouped);
     mx_count_launch();
   }
   chunk_seed_kernel<<<(unsigned)((n_chunks + 127) / 128), 128, 0, s>>>(n_chunks, g->next_chunk_id, g->chunk_prefix.p,

@@ -55,7 +55,18 @@ class DeviceCatalog:
         return self.host.n_samples
 
     def descriptor(self, preds: list[FilterPredicate]):
-        """C struct for mx_index_build; returns (desc, keepalive)."""
+        """C struct for mx_index_build; returns (desc, keepalive). Cached per
+        predicate list: a catalog serves many jobs with the same filters."""
+        key = tuple(preds)
+        cache = self.__dict__.setdefault("_desc_cache", {})
+        hit = cache.get(key)
+        if hit is None:
+            if len(cache) > 64:
+                cache.clear()
+            hit = cache[key] = self._descriptor(preds)
+        return hit
+
+    def _descriptor(self, preds: list[FilterPredicate]):
         codec = self.codec
         lut, lut_off = codec.luts(self.host, preds)
         cols = (C.c_void_p * len(codec.props))(*[self.columns[p].data_ptr() for p in codec.props])
@@ -234,5 +245,4 @@ def build_index_from_catalog(catalog, predicates: Sequence = (), stream=None) ->
     L = _lib.lib()
     out = C.c_void_p()
     _lib.check(L.mx_index_build(C.byref(desc), C.c_void_p(_lib.stream_ptr(stream)), C.byref(out)))
-    del keep
     return ChunkerIndex(out.value, catalog, stream)
