@@ -963,8 +963,10 @@ __device__ __forceinline__ int phase_of_pair(const EmitArgs& a, u64 pair) {
 // Walk the stream range of term `tm` for the kr-th chunk of its phase: the
 // intervals (in cursor order) it cuts. WRITE=false: count pieces; WRITE=true:
 // sink(i, mixture key, file index, start, end) for the i-th piece.
+// WRITE with lanes > 1: the pieces are split over `lanes` cooperating
+// threads (piece t by lane t % lanes); every lane returns the full count.
 template <bool WRITE, typename Sink>
-__device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink sink) {
+__device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink sink, int lane = 0, int lanes = 1) {
   const u32 s = tm.stream;
   const long long sb = a.s_off[s], se = a.s_off[s + 1];
   const u64* pre = a.seg_pre + s;  // stream s prefix lives at seg_pre[i + s]
@@ -993,16 +995,17 @@ __device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink s
       if (!WRITE) {
         if (rb > ra) n += (u64)(rb - ra);
       } else {
-        for (long long r = ra; r < rb; ++r) {
+        for (long long r = ra + lane; r < rb; r += lanes) {
           const long long jj = a.lpos[r];
           const u32 iv = a.civ[jj];
           const u64 off = a.ccum[jj] - cb;
           const u64 len = a.ccum[jj + 1] - a.ccum[jj];
           const u64 from = lo_abs > off ? lo_abs : off;
           const u64 to = hi_abs < off + len ? hi_abs : off + len;
-          sink(n++, a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
+          sink(n + (u64)(r - ra), a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
                a.iv_start[iv] + (u32)(to - off));
         }
+        if (rb > ra) n += (u64)(rb - ra);
       }
       x = seg_end < y ? seg_end : y;
       ++i;
@@ -1010,20 +1013,18 @@ __device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink s
     }
     long long j = ub_u64(a.ccum, ib, ie, cb + lo_abs) - 1;
     const long long j1 = ub_u64(a.ccum, ib, ie, cb + hi_abs - 1) - 1;
-    auto cut = [&](long long jj) {
-      const u32 iv = a.civ[jj];
-      const u64 off = a.ccum[jj] - cb;
-      const u64 len = a.ccum[jj + 1] - a.ccum[jj];
-      const u64 from = lo_abs > off ? lo_abs : off;
-      const u64 to = hi_abs < off + len ? hi_abs : off + len;
-      sink(n++, a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
-           a.iv_start[iv] + (u32)(to - off));
-    };
-    if (!WRITE) {
-      n += (u64)(j1 - j + 1);
-    } else {
-      for (; j <= j1; ++j) cut(j);
+    if (WRITE) {
+      for (long long jj = j + lane; jj <= j1; jj += lanes) {
+        const u32 iv = a.civ[jj];
+        const u64 off = a.ccum[jj] - cb;
+        const u64 len = a.ccum[jj + 1] - a.ccum[jj];
+        const u64 from = lo_abs > off ? lo_abs : off;
+        const u64 to = hi_abs < off + len ? hi_abs : off + len;
+        sink(n + (u64)(jj - j), a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
+             a.iv_start[iv] + (u32)(to - off));
+      }
     }
+    n += (u64)(j1 - j + 1);
     x = seg_end < y ? seg_end : y;
     ++i;
   }
@@ -1033,7 +1034,7 @@ __device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink s
 // Walk the stream range of one (chunk, term) pair. WRITE=false: count pieces.
 template <bool WRITE>
 __device__ u64 walk_pair(const EmitArgs& a, u64 pair, long long* chunk_out, u32* pm, u32* pf, u32* ps, u32* pe,
-                         u64 out_base) {
+                         u64 out_base, int lane = 0, int lanes = 1) {
   const int p = phase_of_pair(a, pair);
   const Phase ph = a.phases[p];
   const u64 local = pair - a.pair_pre[p];
@@ -1041,12 +1042,15 @@ __device__ u64 walk_pair(const EmitArgs& a, u64 pair, long long* chunk_out, u32*
   const Term tm = a.terms[ph.term_begin + (long long)(local % (u64)ph.n_terms)];
   if (chunk_out) *chunk_out = ph.chunk_begin + kr;
   if (WRITE) {
-    return walk_term<true>(a, tm, kr, [&](u64 i, u32 m, u32 f, u32 s0, u32 e0) {
-      pm[out_base + i] = m;
-      pf[out_base + i] = f;
-      ps[out_base + i] = s0;
-      pe[out_base + i] = e0;
-    });
+    return walk_term<true>(
+        a, tm, kr,
+        [&](u64 i, u32 m, u32 f, u32 s0, u32 e0) {
+          pm[out_base + i] = m;
+          pf[out_base + i] = f;
+          ps[out_base + i] = s0;
+          pe[out_base + i] = e0;
+        },
+        lane, lanes);
   }
   return walk_term<false>(a, tm, kr, [](u64, u32, u32, u32, u32) {});
 }
@@ -1057,10 +1061,30 @@ __global__ void emit_count_kernel(EmitArgs a, u64 n_pairs, u64* pair_cnt) {
   pair_cnt[pr] = walk_pair<false>(a, pr, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
 }
 
-__global__ void emit_write_kernel(EmitArgs a, u64 n_pairs, const u64* pair_off, u32* pm, u32* pf, u32* ps, u32* pe) {
+// thread per (chunk, term) pair; pairs of more than 32 pieces (iid layouts:
+// ~500 intervals per term) are listed for emit_write_warp_kernel
+__global__ void emit_write_kernel(EmitArgs a, u64 n_pairs, const u64* pair_off, u32* pm, u32* pf, u32* ps, u32* pe,
+                                  u32* long_list, u32* long_cnt) {
   u64 pr = blockIdx.x * (u64)blockDim.x + threadIdx.x;
   if (pr >= n_pairs) return;
+  if (pair_off[pr + 1] - pair_off[pr] > 32) {
+    long_list[atomicAdd(long_cnt, 1u)] = (u32)pr;
+    return;
+  }
   walk_pair<true>(a, pr, nullptr, pm, pf, ps, pe, pair_off[pr]);
+}
+
+// one warp per long pair: the lanes cut its intervals in parallel
+__global__ void __launch_bounds__(256) emit_write_warp_kernel(EmitArgs a, const u64* pair_off, u32* pm, u32* pf,
+                                                              u32* ps, u32* pe, const u32* long_list,
+                                                              const u32* long_cnt) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long n = *long_cnt;
+  for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n; w += warps) {
+    const u64 pr = long_list[w];
+    walk_pair<true>(a, pr, nullptr, pm, pf, ps, pe, pair_off[pr], lane, 32);
+  }
 }
 
 // first pair of every chunk (+ sentinel) -> piece range per chunk
@@ -1168,9 +1192,10 @@ __device__ u32 sort_merge(uint4* s, u32 n, int tid, int nt, u32* s_flags) {
 }
 
 constexpr int NM_THREADS = 256;
+constexpr int NMB_THREADS = 1024;  // normalize_kernel: one compare-exchange per thread per stage at 2048
 constexpr int NM_CAP = 2048;
 
-__global__ void __launch_bounds__(NM_THREADS)
+__global__ void __launch_bounds__(NMB_THREADS)
 normalize_kernel(const u32* big_list, const u32* big_cnt, const u64* chunk_piece_off, u32* pm, u32* pf, u32* ps,
                  u32* pe, u64* merged_cnt, u32* too_big) {
   __shared__ uint4 s[NM_CAP];
@@ -1184,10 +1209,10 @@ normalize_kernel(const u32* big_list, const u32* big_cnt, const u64* chunk_piece
       if (threadIdx.x == 0) atomicMax(too_big, n);
       continue;
     }
-    for (u32 i = threadIdx.x; i < n; i += NM_THREADS) s[i] = make_uint4(pm[o0 + i], pf[o0 + i], ps[o0 + i], pe[o0 + i]);
+    for (u32 i = threadIdx.x; i < n; i += NMB_THREADS) s[i] = make_uint4(pm[o0 + i], pf[o0 + i], ps[o0 + i], pe[o0 + i]);
     __syncthreads();
-    u32 m = n ? sort_merge(s, n, threadIdx.x, NM_THREADS, s_flags) : 0;
-    for (u32 i = threadIdx.x; i < m; i += NM_THREADS) {
+    u32 m = n ? sort_merge(s, n, threadIdx.x, NMB_THREADS, s_flags) : 0;
+    for (u32 i = threadIdx.x; i < m; i += NMB_THREADS) {
       pm[o0 + i] = s[i].x;
       pf[o0 + i] = s[i].y;
       ps[o0 + i] = s[i].z;
@@ -1684,8 +1709,17 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(pf.alloc(cap, s));
   MX_CUDA_TRY(ps.alloc(cap, s));
   MX_CUDA_TRY(pe.alloc(cap, s));
-  emit_write_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p);
-  mx_count_launch();
+  {
+    DevBuf<u32> llist, lcnt;
+    MX_CUDA_TRY(llist.alloc(n_pairs, s));
+    MX_CUDA_TRY(lcnt.alloc(1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(lcnt.p, 0, sizeof(u32), s));
+    emit_write_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p);
+    mx_count_launch();
+    const long long wgrid = std::min<long long>(((long long)n_pairs + 7) / 8, 148 * 16);
+    emit_write_warp_kernel<<<(unsigned)wgrid, 256, 0, s>>>(a, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p);
+    mx_count_launch();
+  }
   DevBuf<u64> cpo, mcnt;
   DevBuf<u32> big;
   MX_CUDA_TRY(cpo.alloc(n_chunks + 1, s));
@@ -1711,7 +1745,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
                                                           blist.p, bcnt.p);
     mx_count_launch();
     long long grid = n_chunks < 148 * 4 ? n_chunks : 148 * 4;
-    normalize_kernel<<<(unsigned)grid, NM_THREADS, 0, s>>>(blist.p, bcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p,
+    normalize_kernel<<<(unsigned)grid, NMB_THREADS, 0, s>>>(blist.p, bcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p,
                                                            big.p);
     mx_count_launch();
   }

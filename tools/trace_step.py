@@ -28,13 +28,20 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--out", default="gpurun_out/trace.json")
     ap.add_argument("--cprofile", action="store_true", help="host Python profile of 20 steps instead")
+    ap.add_argument("--cfg1r1", action="store_true", help="trace the iid cfg1 job instead of cfg2")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    rt = bench.make_workload(0, args.scale)
-    meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
-    cols = bench.device_columns(rt, dev)
-    spec = synth.cfg2_mixture(bench.CFG["chunk_size"])
-    dcat = bench.device_catalog(meta, cols)
+    if args.cfg1r1:  # iid 1M-sample cfg1 (long chunks, ~1000 ranges each)
+        from paper_2502_19790_b200 import DeviceCatalog
+
+        dcat = DeviceCatalog(synth.expand_numpy(synth.config("cfg1", layout_r=1)))
+        spec = synth.cfg1_mixtures()["disjoint"]
+    else:
+        rt = bench.make_workload(0, args.scale)
+        meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
+        cols = bench.device_columns(rt, dev)
+        spec = synth.cfg2_mixture(bench.CFG["chunk_size"])
+        dcat = bench.device_catalog(meta, cols)
     for _ in range(3):
         bench.run_step(dcat, spec)
     torch.cuda.synchronize()
