@@ -80,6 +80,11 @@ class Chunk:
                      MixtureSpec.from_json(mix) if mix else None)
 
     def serialize(self) -> bytes:
+        # bytes produced on the device for a planned batch (csrc/serialize.cu),
+        # valid while data / mixture are the objects they were built from
+        dev = getattr(self, "_device_bytes", None)
+        if dev is not None and dev[1] is self.data and dev[2] is self.mixture:
+            return dev[0]
         return canonical_json_bytes(self.to_json())
 
     @staticmethod
@@ -196,7 +201,22 @@ class ChunkBatch:
         _lib.check(L.mx_gen_result_json_copy(self._gen._h, _lib.ptr(buf), _lib.ptr(off)))
         return buf[: total.value].tobytes(), off
 
-    def chunk(self, i: int) -> Chunk:
+    DEVICE_JSON_MIN = 64  # batches at least this large serialise on the device
+
+    def chunk(self, i: int, mixture=None) -> Chunk:
+        """Chunk i of the batch; ``mixture`` (the spec in force) defaults to the
+        batch's spec. Large batches carry device-built canonical bytes."""
+        c = self._chunk(i)
+        if mixture is not None:
+            c.mixture = mixture
+        if self.n_chunks >= self.DEVICE_JSON_MIN and (self.arbitrary or c.mixture is self.spec):
+            if getattr(self, "_json", None) is None:
+                self._json = self.serialize_all()
+            blob, off = self._json
+            c._device_bytes = (blob[int(off[i]):int(off[i + 1])], c.data, c.mixture)
+        return c
+
+    def _chunk(self, i: int) -> Chunk:
         h = self.to_host()
         a, b = int(h["off"][i]), int(h["off"][i + 1])
         data: RangeMap = {}
@@ -378,9 +398,7 @@ class ChunkGenerator:
         same = b is not None and b.arbitrary_size == arbitrary_size and (
             arbitrary_size is not None or b.spec == spec)
         if same and self._served < b.n_chunks:
-            c = b.chunk(self._served)
-            if arbitrary_size is None:
-                c.mixture = spec
+            c = b.chunk(self._served, mixture=spec if arbitrary_size is None else None)
             self._served += 1
             self._next_id += 1
             return c

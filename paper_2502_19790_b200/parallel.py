@@ -262,10 +262,13 @@ class MergedChunkBatch:
                               ds=self._file_ds[fidx], fid=self._file_ids[fidx], start=p[2].copy(), end=p[3].copy())
         return self._host
 
-    def chunk(self, i: int):
+    def chunk(self, i: int, mixture=None):
         from .chunks import ChunkBatch
 
-        return ChunkBatch.chunk(self, i)
+        c = ChunkBatch._chunk(self, i)
+        if mixture is not None:
+            c.mixture = mixture
+        return c
 
 
 def merge_batch(gen, batch, stream=None):

@@ -60,3 +60,30 @@ def test_device_json_string_order_of_ids():
             c.mixture = spec
             want.append(c.serialize().decode("ascii"))
         assert got == want
+
+
+def test_served_chunks_carry_device_bytes():
+    """Chunks handed out from a large look-ahead batch serialise to the
+    device-built bytes, identical to the host canonical JSON."""
+    from paper_2502_19790_b200 import ChunkGenerator, DeviceCatalog, build_index_from_catalog
+    from paper_2502_19790_b200.seeding import canonical_json_bytes
+
+    cc, g = load_golden("cfg2_small")
+    idx = build_index_from_catalog(DeviceCatalog(cc), golden_predicates(g))
+    spec = spec_from_json(g["mixtures"]["cfg2"])
+    gen = ChunkGenerator(idx, g["job_seed"])
+    batch = gen.plan_batch(spec, 10_000)
+    assert batch.n_chunks >= batch.DEVICE_JSON_MIN
+    for i in range(batch.n_chunks):
+        c = batch.chunk(i)
+        assert getattr(c, "_device_bytes", None) is not None
+        assert c.serialize() == canonical_json_bytes(c.to_json())
+    # the sequential API: look-ahead batches double (1, 2, ..., 64, 128)
+    gen2 = ChunkGenerator(idx, g["job_seed"])
+    got = []
+    while True:
+        c = gen2.generate(spec)
+        if c is None:
+            break
+        got.append(c.serialize().decode("ascii"))
+    assert got == g["runs"]["cfg2"]["chunks"]
