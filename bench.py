@@ -17,9 +17,11 @@ and copies the full chunk CSR back (D2H inside). The roofline line is for the
 dominant kernel (scan_runs, stage 1's streaming pass), timed with CUDA events
 recorded by the library on the launching stream.
 
---impl reference times the CPU oracle port (oracle/oracle.py, a numpy/stdlib
-restatement of the reference's own algorithm) on a bounded slice of the same
-workload on the host cores. Under torchrun with N > 1 rank r owns its own
+--impl reference times the reference's own CPU path -- the unmodified
+mixplane package installed under baseline/_ref (filter_intervals ->
+build_index -> ChunkGenerator.generate to exhaustion) -- on a bounded slice of
+the same workload on the host cores; without baseline/_ref the CPU oracle port
+(oracle/oracle.py) stands in and the line says kind "port". Under torchrun with N > 1 rank r owns its own
 100M-sample shard = global files [r*F, (r+1)*F) of ONE N x 100M-sample catalog
 (weak scaling, cfg 3 shape) and the step is the file-sharded pipeline: local
 stage 1, NCCL all-gather of the per-(key, file) block tables, hybrid index +
@@ -51,7 +53,7 @@ CFG = dict(workload="cfg2: 100M samples, 10k files, 5 props (4,5,5,4,5) -> 2000 
                     "static 4-key best-effort mixture, chunk 1024, seed 42",
            n_samples=100_000_000, n_files=10_000, props=5, run_mean=64, chunk_size=1024, job_seed=42,
            l2="inputs (2 GB of columns) exceed the 126 MB L2; no flush needed")
-REF_SAMPLE = 4_000_000  # --impl reference: samples per step (bounded CPU slice)
+REF_SAMPLE = 2_000_000  # --impl reference: samples per step (bounded CPU slice, ~5 s through the reference)
 CPU_SAMPLE = 10_000_000  # cpu_baseline leg of our arm
 
 
@@ -173,15 +175,81 @@ def cpu_port(n_samples: int, rank: int = 0):
     return dt, chunks
 
 
+def _reference_pkg():
+    """The unmodified reference (mixplane) installed under baseline/_ref, or
+    None when it is absent (then the oracle port stands in)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "mixplane").is_dir():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import mixplane  # noqa: F401
+    except Exception:
+        return None
+    return mixplane
+
+
+def _reference_catalog(cc):
+    """A reference MetadataCatalog holding exactly cc's int32 code columns
+    (the columnar _FileStore layout the reference keeps after registration,
+    catalog.py:265-275; SURVEY.md §8d "oracle injector")."""
+    from mixplane import catalog as rcat
+
+    cat = rcat.MetadataCatalog()
+    props = sorted(cc.columns)
+    cat._props = {p: rcat.PropertyDef(p, "string", True, False) for p in props}
+    cat._vocab = {p: list(cc.vocab[p]) for p in props}
+    cat._vocab_idx = {p: {v: i for i, v in enumerate(cc.vocab[p])} for p in props}
+    nds = int(cc.file_ds.max()) + 1
+    cat._dataset_names = [f"ds{d}" for d in range(nds)]
+    cat._dataset_schemas = {d: rcat.PropertySchema([cat._props[p] for p in props]) for d in range(nds)}
+    cat._dataset_files = {d: [] for d in range(nds)}
+    for i, fid in enumerate(cc.file_ids.tolist()):
+        ds = int(cc.file_ds[i])
+        a, b = int(cc.file_offsets[i]), int(cc.file_offsets[i + 1])
+        store = rcat._FileStore(path=f"/synthetic/{fid}.jsonl", dataset_id=ds, n_samples=b - a, content_hash="0" * 32)
+        for p in props:
+            store.codes[p] = cc.columns[p][a:b].astype(np.int32).copy()
+        cat._files[fid] = store
+        cat._dataset_files[ds].append(fid)
+    return cat
+
+
+def reference_run(n_samples: int):
+    """The reference's own job on a bounded slice of the workload:
+    filter_intervals -> build_index -> ChunkGenerator.generate until None
+    (server.py:112-163), single thread (GIL-bound, build_index workers=1)."""
+    from mixplane.chunks import ChunkGenerator as RGen
+    from mixplane.index import build_index as rbuild
+    from mixplane.mixtures import MixtureKey as RKey, MixtureSpec as RSpec
+
+    from paper_2502_19790_b200 import synth
+
+    f = max(1, n_samples // (CFG["n_samples"] // CFG["n_files"]))
+    cc = synth.expand_numpy(synth.make_runs(n_samples, f, synth.CFG2_PROPS, CFG["run_mean"], seed=2))
+    cat = _reference_catalog(cc)
+    spec = synth.cfg2_mixture(CFG["chunk_size"])
+    rspec = RSpec({RKey.of({p: list(v) for p, v in k.entries}): w for k, w in spec.weights.items()}, spec.chunk_size)
+    t0 = time.perf_counter()
+    gen = RGen(rbuild(cat.filter_intervals([])), CFG["job_seed"])
+    chunks = 0
+    while gen.generate(rspec) is not None:
+        chunks += 1
+    return time.perf_counter() - t0, chunks
+
+
 def reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
+    real = _reference_pkg() is not None
+    run = reference_run if real else cpu_port
     for _ in range(args.warmup):
-        cpu_port(REF_SAMPLE)
+        run(REF_SAMPLE)
     times, chunks = [], 0
     for _ in range(args.steps):
-        dt, chunks = cpu_port(REF_SAMPLE)
+        dt, chunks = run(REF_SAMPLE)
         times.append(dt)
     t = sum(times) / len(times)
     v = REF_SAMPLE / t
@@ -191,9 +259,11 @@ def reference_arm(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": dict(CFG, workload=CFG["workload"] + f" (CPU slice: first {REF_SAMPLE:,} samples)"),
         "chunks_per_s": chunks / t,
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{REF_SAMPLE:,} samples of the cfg2 layout per step (oracle/oracle.py, "
-                                   "numpy + CPython stdlib, single thread like the GIL-bound reference)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "reference" if real else "port",
+                         "sample": f"{REF_SAMPLE:,} samples of the cfg2 layout per step through "
+                                   + ("the unmodified reference (baseline/_ref mixplane: filter_intervals, "
+                                      "build_index, ChunkGenerator.generate to exhaustion), single thread"
+                                      if real else "oracle/oracle.py (numpy + CPython stdlib), single thread")},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -323,11 +393,15 @@ def our_arm(args):
         "clocks": clk,
     }
     if not args.no_cpu_baseline and world == 1:
-        dt, chunks = cpu_port(CPU_SAMPLE)
-        line["cpu_baseline"] = {"value": CPU_SAMPLE / dt, "unit": UNIT, "cores": 1, "kind": "port",
-                                "chunks_per_s": chunks / dt,
-                                "sample": f"first {CPU_SAMPLE:,} samples ({CPU_SAMPLE // 10_000} files) of the cfg2 "
-                                          "layout through oracle/oracle.py (numpy + CPython stdlib, 1 thread)"}
+        real = _reference_pkg() is not None
+        n_cpu = REF_SAMPLE if real else CPU_SAMPLE
+        dt, chunks = (reference_run if real else cpu_port)(n_cpu)
+        line["cpu_baseline"] = {
+            "value": n_cpu / dt, "unit": UNIT, "cores": 1, "kind": "reference" if real else "port",
+            "chunks_per_s": chunks / dt,
+            "sample": f"first {n_cpu:,} samples ({n_cpu // 10_000} files) of the cfg2 layout through "
+                      + ("the unmodified reference (baseline/_ref), 1 thread" if real
+                         else "oracle/oracle.py (numpy + CPython stdlib), 1 thread")}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
