@@ -21,8 +21,9 @@ recorded by the library on the launching stream.
 mixplane package installed under baseline/_ref (filter_intervals ->
 build_index -> ChunkGenerator.generate to exhaustion) -- on a bounded slice of
 the same workload on the host cores; without baseline/_ref the CPU oracle port
-(oracle/oracle.py) stands in and the line says kind "port". Under torchrun with N > 1 rank r owns its own
-100M-sample shard = global files [r*F, (r+1)*F) of ONE N x 100M-sample catalog
+(oracle/oracle.py) stands in and the line says kind "port".
+
+Under torchrun with N > 1 rank r owns its own 100M-sample shard = global files [r*F, (r+1)*F) of ONE N x 100M-sample catalog
 (weak scaling, cfg 3 shape) and the step is the file-sharded pipeline: local
 stage 1, NCCL all-gather of the per-(key, file) block tables, hybrid index +
 global cursor layout + plan (replicated), local emission, NCCL all-gather of
