@@ -81,11 +81,19 @@ def main():
     results = []
     per_rank = {}
     prof = None
+    # warm-up (first-call costs: side stream, pool growth) on rank 0, untimed
+    x = locs[0]
+    hyb = hybrid_index(x["idx"], x["dcat"], tables, counts, gkeys, 0, file_ds, file_ids, W, 0)
+    del hyb.shard
+    gen = ChunkGenerator(hyb, bench.CFG["job_seed"])
+    gen.plan_batch(spec, 1 << 40)
+    del gen, hyb
+    torch.cuda.synchronize()
     for r, x in enumerate(locs):
         if args.trace and r == 0:
             from torch.profiler import ProfilerActivity, profile
 
-            prof = profile(activities=[ProfilerActivity.CUDA])
+            prof = profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU])
             prof.__enter__()
         L.mx_profile_reset()
         L.mx_profile_enable(1)
@@ -114,6 +122,20 @@ def main():
                     a[1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
             for k, (n_, us) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
                 print(f"  {us:9.1f} us  x{n_:3d}  {k}", file=sys.stderr)
+            prof.export_chrome_trace("/tmp/sim_trace.json")
+            ev = json.load(open("/tmp/sim_trace.json"))["traceEvents"]
+            gpu = sorted([e for e in ev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")],
+                         key=lambda e: e["ts"])
+            end = gpu[0]["ts"]
+            t0 = end
+            for e in gpu:
+                gap = e["ts"] - end
+                if gap > 20:
+                    print(f"  gap {gap:8.1f} us before {e['name'][:60]} at {e['ts'] - t0:9.1f}", file=sys.stderr)
+                end = max(end, e["ts"] + e["dur"])
+            cpu = [e for e in ev if e.get("ph") == "X" and e.get("cat") == "cuda_runtime" and e["dur"] > 30]
+            for e in sorted(cpu, key=lambda e: e["ts"]):
+                print(f"  host {e['name'][:30]} {e['dur']:8.1f} us at {e['ts'] - t0:9.1f}", file=sys.stderr)
             prof = None
         if r in timed_ranks:
             per_rank[r] = {"hybrid_intervals": hyb.n_intervals, "hybrid_ms": round(t_h, 3),
