@@ -304,6 +304,10 @@ int mx_index_export_intervals(const mx_index* index, uint32_t* key_rank, int32_t
                               uint32_t* start, uint32_t* end) {
   MX_CHECK_ARG(index, "null index");
   const IndexData& d = index->d;
+  if (d.sharded)
+    return mx_fail(MX_ERR_UNSUPPORTED,
+                   "a file-sharded index holds only this rank's intervals (remote files are per-file blocks); "
+                   "export the local index instead");
   const long long I = d.n_intervals;
   if (I == 0) return MX_OK;
   std::vector<u32> f(I), bk(d.n_blocks), bf(d.n_blocks + 1);
@@ -743,6 +747,8 @@ int mx_gen_cursor_ranges(const mx_gen* gen, uint32_t comp, int64_t* n_ranges, in
   const GenData& g = gen->d;
   const IndexData& d = *g.ix;
   if ((long long)comp >= g.K) return mx_fail(MX_ERR_INVALID, "component %u out of range", comp);
+  if (d.sharded)
+    return mx_fail(MX_ERR_UNSUPPORTED, "cursor ranges of a file-sharded generator are distributed over the ranks");
   u32 kb[2], ib, ie;
   cudaError_t e = cudaMemcpy(kb, d.key_blk_first.p + comp, sizeof(u32) * 2, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemcpy(&ib, d.blk_first.p + kb[0], sizeof(u32), cudaMemcpyDeviceToHost);

@@ -56,6 +56,7 @@ def _run_case(rank, world, case):
     idx = build_sharded_index(dcat, golden_predicates(g), f0, cc.file_ds, cc.file_ids)
     res = {"keys": [k.canonical_string() for k in idx.component_keys()],
            "counts": {k.canonical_string(): v for k, v in idx.key_sample_counts().items()},
+           "local_table": [list(r) for r in idx.local_index.table()],
            "runs": {}}
     for name, run in g["runs"].items():
         gen = ChunkGenerator(idx, g["job_seed"])
@@ -105,6 +106,11 @@ def _check(case, world):
     _, g = load_golden(case)
     res = _spawn(case, world)
     assert sorted(res) == list(range(world))
+    # stage 1 on the shards: the union of the ranks' local tables is the
+    # reference's index (key order, then dataset, file id, start)
+    order = {k: i for i, k in enumerate(res[0]["keys"])}
+    rows = sorted((r for x in res.values() for r in x["local_table"]), key=lambda r: (order[r[0]], r[1], r[2], r[3]))
+    assert rows == g["index"], f"{case} sharded stage 1"
     for rank, r in res.items():
         assert r["keys"] == sorted(r["counts"], key=r["keys"].index)
         for name, run in g["runs"].items():
