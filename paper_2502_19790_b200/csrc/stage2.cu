@@ -557,17 +557,27 @@ __device__ void big_apportion(const BigArgs& a, const unsigned char* dead, long 
                               BigShared& sh) {
   const int tid = threadIdx.x;
   const int Km = a.Km;
-  if (tid == 0) {  // CPython 3.12 sum(): Neumaier, keys in key order
+  if (tid < 32) {  // CPython 3.12 sum(): Neumaier, keys in key order
+    // warp 0: 32 weights per coalesced load, broadcast by shuffles; every
+    // lane runs the same sequential recurrence (no memory on its critical path)
+    const int lane = tid;
     double s = 0.0, c = 0.0;
-    for (int m = 0; m < Km; ++m) {
-      if (dead && dead[m]) continue;
-      const double x = a.w[m];
-      const double t = s + x;
-      if (fabs(s) >= fabs(x)) c += (s - t) + x;
-      else c += (x - t) + s;
-      s = t;
+    for (int b = 0; b < Km; b += 32) {
+      const int m = b + lane;
+      const bool live = m < Km && !(dead && dead[m]);
+      const double xm = m < Km ? a.w[m] : 0.0;
+      u32 mk = __ballot_sync(MX_FULL, live);
+      while (mk) {
+        const int t = __ffs(mk) - 1;
+        mk &= mk - 1;
+        const double x = __shfl_sync(MX_FULL, xm, t);
+        const double tt = s + x;
+        if (fabs(s) >= fabs(x)) c += (s - tt) + x;
+        else c += (x - tt) + s;
+        s = tt;
+      }
     }
-    sh.wsum = c != 0.0 ? s + c : s;
+    if (lane == 0) sh.wsum = c != 0.0 ? s + c : s;
   }
   __syncthreads();
   const double wsum = sh.wsum;
@@ -656,7 +666,7 @@ __device__ void big_apportion(const BigArgs& a, const unsigned char* dead, long 
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a) {
+__global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a, int stage_w) {
   extern __shared__ __align__(16) unsigned char big_smem[];
   __shared__ BigShared sh;
   __shared__ long long s_min[BIG_THREADS / 32];
@@ -665,6 +675,18 @@ __global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a) {
   int* rem = reinterpret_cast<int*>(big_smem);                   // [Km]
   u32* nxt = reinterpret_cast<u32*>(big_smem + 4 * (size_t)Km);  // [Km+1] skip list over order_w
   unsigned char* dead = big_smem + 8 * (size_t)Km + 4;           // [Km] 1 dead, 2 newly dead this pass
+  if (stage_w) {  // weights + weight order in shared memory: the sequential redistribution
+    const size_t wo = (9 * (size_t)Km + 4 + 15) & ~(size_t)15;   // steps read them one by one
+    double* sw = reinterpret_cast<double*>(big_smem + wo);
+    u32* sow = reinterpret_cast<u32*>(big_smem + wo + 8 * (size_t)Km);
+    for (int m = tid; m < Km; m += BIG_THREADS) {
+      sw[m] = a.w[m];
+      sow[m] = a.order_w[m];
+    }
+    a.w = sw;
+    a.order_w = sow;
+    __syncthreads();
+  }
   for (int m = tid; m < Km; m += BIG_THREADS) {
     a.slen[m] = a.seg_pre[a.s_off[m + 1] + m];
     a.counts[m] = 0;
@@ -1978,14 +2000,20 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     ba.cap_terms = cap_terms;
     ba.out = out.p;
     ba.report = report.p;
-    const size_t smem = 9 * (size_t)Km + 4;
+    int dev = 0, optin = 0;
+    MX_CUDA_TRY(cudaGetDevice(&dev));
+    MX_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const size_t base_smem = 9 * (size_t)Km + 4;
+    const size_t staged = ((base_smem + 15) & ~(size_t)15) + 12 * (size_t)Km;
+    const int stage_w = staged + sizeof(BigShared) + 2048 <= (size_t)optin ? 1 : 0;
+    const size_t smem = stage_w ? staged : base_smem;
     static size_t smem_set = 0;
     if (smem > smem_set) {
       MX_CUDA_TRY(cudaFuncSetAttribute(plan_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(9 * (size_t)BIG_MAX_KM + 4)));
-      smem_set = 9 * (size_t)BIG_MAX_KM + 4;
+                                       optin - (int)sizeof(BigShared) - 1024));
+      smem_set = optin - sizeof(BigShared) - 1024;
     }
-    plan_big_kernel<<<1, BIG_THREADS, smem, s>>>(ba);
+    plan_big_kernel<<<1, BIG_THREADS, smem, s>>>(ba, stage_w);
   } else {
     plan_kernel<<<1, 32, 0, s>>>(pa);
   }
