@@ -7,10 +7,11 @@
 //    in a fixed order, so the f64 sums are bit-reproducible run to run.
 //    For <= 32 domains (the ADO case: 22 Pile domains) domain_loss_priv_kernel
 //    replaces it: every thread owns a private shared-memory row of K (f64 sum,
-//    u32 count) bins, streams its tokens with 16-byte loads (4 tokens per
-//    load, coalesced across the CTA) and accumulates without atomics or
-//    warp votes; rows are combined per domain in a fixed order, so the sums
-//    stay run-to-run reproducible. HBM-bound: B3 = T x (4 + 4) bytes.
+//    u32 count) bins and 32 consecutive tokens per tile (16-byte loads), keeps
+//    the current same-tag run in registers and flushes it to its bin when the
+//    tag changes (ADO batches are single-domain sequences); no atomics or warp
+//    votes; rows are combined per domain in a fixed order, so the sums stay
+//    run-to-run reproducible. HBM-bound: B3 = T x (4 + 4) bytes.
 //  * fit_kernel: fit_power_law (ado.py:121-168), one CTA per domain, one warp
 //    per epsilon candidate (grid of 50, then a 201-point linspace refinement),
 //    closed-form log-linear regression + SSE in f64, strict-< argmin with
@@ -87,6 +88,7 @@ domain_loss_kernel(const float* loss, const int32_t* tags, long long n, int K, l
 
 constexpr int DLP_THREADS = 256;
 constexpr int DLP_MAXK = 32;
+constexpr int DLP_RUN = 32;  // consecutive tokens per thread per tile
 
 __global__ void __launch_bounds__(DLP_THREADS)
 domain_loss_priv_kernel(const float* __restrict__ loss, const int32_t* __restrict__ tags, long long n, int K,
@@ -100,29 +102,61 @@ domain_loss_priv_kernel(const float* __restrict__ loss, const int32_t* __restric
     s_cnt[k * DLP_THREADS + tid] = 0;
   }
   u32 badv = 0;
-  const bool vec = ((reinterpret_cast<uintptr_t>(loss) | reinterpret_cast<uintptr_t>(tags)) & 15) == 0;
-  const long long stride = (long long)gridDim.x * DLP_THREADS * 4;
+  // a thread owns DLP_RUN consecutive tokens per tile and keeps the running
+  // (tag, sum, count) of the current same-tag run in registers, flushing to
+  // its shared-memory bin when the tag changes: ADO batches are sequences of
+  // thousands of single-domain tokens, so flushes are rare
+  int cur_t = -1;
+  double cur_s = 0.0;
+  u32 cur_c = 0;
+  auto flush = [&]() {
+    if (cur_c) {
+      s_sum[cur_t * DLP_THREADS + tid] += cur_s;
+      s_cnt[cur_t * DLP_THREADS + tid] += cur_c;
+    }
+  };
   auto add = [&](int t, float v) {
     if ((unsigned)t >= (unsigned)K) {
       badv = 1;
       return;
     }
-    s_sum[t * DLP_THREADS + tid] += (double)v;
-    s_cnt[t * DLP_THREADS + tid] += 1u;
+    if (t != cur_t) {
+      flush();
+      cur_t = t;
+      cur_s = 0.0;
+      cur_c = 0;
+    }
+    cur_s += (double)v;
+    ++cur_c;
   };
-  long long i = ((long long)blockIdx.x * DLP_THREADS + tid) * 4;
-  if (vec) {
-    for (; i + 4 <= n; i += stride) {
-      const float4 v = __ldcs(reinterpret_cast<const float4*>(loss + i));
-      const int4 t = __ldcs(reinterpret_cast<const int4*>(tags + i));
-      add(t.x, v.x);
-      add(t.y, v.y);
-      add(t.z, v.z);
-      add(t.w, v.w);
+  const bool vec = ((reinterpret_cast<uintptr_t>(loss) | reinterpret_cast<uintptr_t>(tags)) & 15) == 0;
+  // a warp owns 32 * DLP_RUN consecutive tokens per tile; step q, lane l reads
+  // tokens [q * 128 + 4l, +4): coalesced 16-byte loads, and a lane's tokens
+  // stay inside one sequence for many steps
+  const long long tile = (long long)DLP_THREADS * DLP_RUN;
+  const int ln = tid & 31, wp = tid >> 5;
+  for (long long t0 = (long long)blockIdx.x * tile; t0 < n; t0 += (long long)gridDim.x * tile) {
+    const long long wb = t0 + (long long)wp * 32 * DLP_RUN;
+    if (vec && wb + 32 * DLP_RUN <= n) {
+#pragma unroll 4
+      for (int q = 0; q < DLP_RUN / 4; ++q) {
+        const long long i = wb + q * 128 + 4 * ln;
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(loss + i));
+        const int4 t = __ldcs(reinterpret_cast<const int4*>(tags + i));
+        add(t.x, v.x);
+        add(t.y, v.y);
+        add(t.z, v.z);
+        add(t.w, v.w);
+      }
+    } else {
+      for (int q = 0; q < DLP_RUN / 4; ++q)
+        for (int r = 0; r < 4; ++r) {
+          const long long j = wb + q * 128 + 4 * ln + r;
+          if (j < n) add(tags[j], loss[j]);
+        }
     }
   }
-  for (; i < n; i += stride)  // tail (or unaligned input): same token order per thread
-    for (long long j = i; j < i + 4 && j < n; ++j) add(tags[j], loss[j]);
+  flush();
   if (badv) atomicOr(bad, 1u);
   __syncthreads();
   // fixed-order combine: warp w sums domains k = w, w + 8, ...; lanes take
@@ -432,8 +466,17 @@ int domain_loss(const float* losses, const int32_t* tags, long long n, int K, do
   const bool priv = K <= DLP_MAXK;
   long long per_block = 16384;
   int blocks;
-  if (priv) {  // ~8K tokens per CTA, at most 4 CTAs per SM resident
-    blocks = (int)std::min<long long>((n + 8191) / 8192, 148 * 4);
+  if (priv) {  // one wave of resident CTAs (grid-stride over 8K-token tiles)
+    int dev = 0, n_sm = 148, occ = 1;
+    MX_CUDA_TRY(cudaGetDevice(&dev));
+    MX_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    const size_t smem = (sizeof(double) + sizeof(u32)) * (size_t)K * DLP_THREADS;
+    if (smem > 48 * 1024)
+      MX_CUDA_TRY(cudaFuncSetAttribute(domain_loss_priv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)((sizeof(double) + sizeof(u32)) * DLP_MAXK * DLP_THREADS)));
+    MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, domain_loss_priv_kernel, DLP_THREADS, smem));
+    blocks = (int)std::min<long long>((n + DLP_THREADS * DLP_RUN - 1) / (DLP_THREADS * DLP_RUN),
+                                      (long long)n_sm * std::max(occ, 1));
   } else {
     blocks = (int)((n + per_block - 1) / per_block);
   }
@@ -447,12 +490,6 @@ int domain_loss(const float* losses, const int32_t* tags, long long n, int K, do
   MX_CUDA_TRY(cudaMemsetAsync(bad.p, 0, sizeof(u32), s));
   if (priv) {
     const size_t smem = (sizeof(double) + sizeof(u32)) * (size_t)K * DLP_THREADS;
-    static size_t smem_set = 0;
-    if (smem > 48 * 1024 && smem > smem_set) {
-      MX_CUDA_TRY(cudaFuncSetAttribute(domain_loss_priv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)((sizeof(double) + sizeof(u32)) * DLP_MAXK * DLP_THREADS)));
-      smem_set = (sizeof(double) + sizeof(u32)) * DLP_MAXK * DLP_THREADS;
-    }
     domain_loss_priv_kernel<<<blocks, DLP_THREADS, smem, s>>>(losses, tags, n, K, ps.p, pc.p, bad.p);
   } else {
     domain_loss_kernel<<<blocks, DL_THREADS, 0, s>>>(losses, tags, n, K, per_block, ps.p, pc.p, bad.p);

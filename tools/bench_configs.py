@@ -164,7 +164,9 @@ def cfg4(out, steps):
     g = torch.Generator(device="cuda").manual_seed(4)
     dev = torch.device("cuda", 0)
     losses = [torch.rand(tok, device=dev, generator=g) + 1.5 for _ in range(ranks)]
-    tags = [torch.randint(0, D, (tok,), device=dev, generator=g, dtype=torch.int32) for _ in range(ranks)]
+    # single-domain sequences of 2,048 tokens: 64 per rank per step
+    tags = [torch.randint(0, D, (tok // 2048,), device=dev, generator=g, dtype=torch.int32).repeat_interleave(2048)
+            for _ in range(ranks)]
     torch.cuda.synchronize()
     t_step, t_reduce = [], []
     for step in range(1, steps + 1):
@@ -197,15 +199,21 @@ def cfg4(out, steps):
         torch.cuda.synchronize()
         lat.append(time.perf_counter() - t0)
     big_l = torch.rand(64 << 20, device=dev, generator=g) + 1.5
-    big_t = torch.randint(0, D, (64 << 20,), device=dev, generator=g, dtype=torch.int32)
-    domain_loss_device(big_l, big_t, D)
-    a, b = _events()
-    a.record()
-    for _ in range(5):
-        domain_loss_device(big_l, big_t, D)
-    b.record()
-    torch.cuda.synchronize()
-    big_ms = a.elapsed_time(b) / 5
+    big_t = torch.randint(0, D, ((64 << 20) // 2048,), device=dev, generator=g, dtype=torch.int32)
+    big_t = big_t.repeat_interleave(2048)
+    rnd_t = torch.randint(0, D, (64 << 20,), device=dev, generator=g, dtype=torch.int32)
+
+    def rate(tg):
+        domain_loss_device(big_l, tg, D)
+        a, b = _events()
+        a.record()
+        for _ in range(5):
+            domain_loss_device(big_l, tg, D)
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / 5
+
+    big_ms, rnd_ms = rate(big_t), rate(rnd_t)
     # CPU oracle for the same per-step work (numpy per_domain_loss on 8 x 131k
     # tokens + oracle ADO + oracle chunk generation), a bounded sample of steps
     from oracle import oracle as orc
@@ -235,7 +243,8 @@ def cfg4(out, steps):
         "gpu_8rank_reduce_us_median": float(np.median(np.array(t_reduce) * 1e6)),
         "gpu_one_rank_reduce_us_median": float(np.median(lat) * 1e6),
         "gpu_64M_tokens_ms": big_ms, "gpu_64M_tokens_per_s": (64 << 20) / big_ms * 1e3,
-        "gpu_64M_gbs": (64 << 20) * 8 / big_ms / 1e6,
+        "gpu_64M_gbs": (64 << 20) * 8 / big_ms / 1e6, "gpu_64M_random_tags_ms": rnd_ms,
+        "tags": "single-domain sequences of 2,048 tokens (random per-token tags: gpu_64M_random_tags_ms)",
         "cpu_oracle_us_per_step": cpu_us, "cpu_oracle_steps": osteps, "cpu_cores": 1,
         "note": "host wall clock per step incl. the device syncs of the API (one chunk per step is latency-bound)",
     }
