@@ -37,6 +37,9 @@
 #include <memory>
 
 #include "blake2b.cuh"
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "mixtera_internal.cuh"
 #include "scan.cuh"
@@ -514,6 +517,7 @@ struct BigArgs {
   long long cap_terms;
   long long* out;
   long long* report;
+  unsigned long long* stats;  // optional (MX_PLAN_STATS): section cycle / event counters
 };
 
 struct BigShared {
@@ -552,87 +556,205 @@ __device__ long long big_sum(long long v, BigShared& sh) {
   return sh.acc;
 }
 
+template <typename T, typename Op>
+__device__ T big_reduce(T v, Op op) {  // block-wide reduction, result on every thread
+  __shared__ T s_r[BIG_THREADS / 32];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v = op(v, __shfl_xor_sync(MX_FULL, v, d));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) s_r[warp] = v;
+  __syncthreads();
+  T r = s_r[0];
+  for (int x = 1; x < BIG_THREADS / 32; ++x) r = op(r, s_r[x]);
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+
 // Exact apportion(w restricted to keys with !dead, total): target[m] += count.
+// wsum must be CPython's Neumaier sum in key order, which is sequential. The
+// sum is first taken in parallel in double-double (within ~2 ulp of
+// CPython's); the floors and the leftover selection computed from it are
+// accepted when they are provably insensitive to that difference (no share
+// within eta of a floor boundary, the selection boundary separated by more
+// than eta or a tie of identical weights). Otherwise the sequential sum runs
+// (one warp, shuffle-fed) and everything is recomputed.
 __device__ void big_apportion(const BigArgs& a, const unsigned char* dead, long long total, int* target,
                               BigShared& sh) {
   const int tid = threadIdx.x;
   const int Km = a.Km;
-  if (tid < 32) {  // CPython 3.12 sum(): Neumaier, keys in key order
-    // warp 0: 32 weights per coalesced load, broadcast by shuffles; every
-    // lane runs the same sequential recurrence (no memory on its critical path)
-    const int lane = tid;
-    double s = 0.0, c = 0.0;
-    for (int b = 0; b < Km; b += 32) {
-      const int m = b + lane;
-      const bool live = m < Km && !(dead && dead[m]);
-      const double xm = m < Km ? a.w[m] : 0.0;
-      u32 mk = __ballot_sync(MX_FULL, live);
-      while (mk) {
-        const int t = __ffs(mk) - 1;
-        mk &= mk - 1;
-        const double x = __shfl_sync(MX_FULL, xm, t);
-        const double tt = s + x;
-        if (fabs(s) >= fabs(x)) c += (s - tt) + x;
-        else c += (x - tt) + s;
-        s = tt;
+  unsigned long long t_a = clock64();
+  {  // parallel double-double sum of the alive weights
+    double hi = 0.0, lo = 0.0, e;
+    for (int m = tid; m < Km; m += BIG_THREADS) {
+      if (dead && dead[m]) continue;
+      two_sum(hi, a.w[m], hi, e);
+      lo += e;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const double oh = __shfl_xor_sync(MX_FULL, hi, d), ol = __shfl_xor_sync(MX_FULL, lo, d);
+      two_sum(hi, oh, hi, e);
+      lo = lo + ol + e;
+    }
+    __shared__ double s_hi[BIG_THREADS / 32], s_lo[BIG_THREADS / 32];
+    const int lane = tid & 31, warp = tid >> 5;
+    if (lane == 0) {
+      s_hi[warp] = hi;
+      s_lo[warp] = lo;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double H = 0.0, Lo = 0.0;
+      for (int x = 0; x < BIG_THREADS / 32; ++x) {
+        two_sum(H, s_hi[x], H, e);
+        Lo += s_lo[x] + e;
       }
+      sh.wsum = H + Lo;
     }
-    if (lane == 0) sh.wsum = c != 0.0 ? s + c : s;
+    __syncthreads();
   }
-  __syncthreads();
-  const double wsum = sh.wsum;
+  bool exact = false;
   const double tot = (double)total;
-  long long assigned = 0;
-  for (int m = tid; m < Km; m += BIG_THREADS) {
-    if (dead && dead[m]) {
-      a.base[m] = 0;
-      a.fkey[m] = ~0ull;
-      continue;
-    }
-    const double share = a.w[m] / wsum * tot;
-    const long long b = (long long)(share + 1e-9);
-    double fr = share - (double)b;
-    fr = fr > 0.0 ? fr : 0.0;
-    a.base[m] = b;
-    a.fkey[m] = ~(unsigned long long)__double_as_longlong(fr);  // larger frac -> smaller key
-    assigned += b;
-  }
-  const long long left = total - big_sum(assigned, sh);
+  long long left = 0;
   unsigned long long thr = 0;
   int need = 0;
-  if (left > 0) {  // radix select: the left-th smallest (fkey, key) among alive keys
-    unsigned long long prefix = 0, mask = 0;
-    if (tid == 0) sh.need = (int)left;
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      for (int d = tid; d < 256; d += BIG_THREADS) sh.hist[d] = 0;
-      __syncthreads();
-      for (int m = tid; m < Km; m += BIG_THREADS) {
-        if (dead && dead[m]) continue;
-        const unsigned long long f = a.fkey[m];
-        if ((f & mask) == prefix) atomicAdd(&sh.hist[(f >> shift) & 255], 1u);
-      }
-      __syncthreads();
-      if (tid == 0) {
-        int nd = sh.need;
-        u32 cum = 0;
-        int dg = 255;
-        for (int d = 0; d < 256; ++d) {
-          if ((int)(cum + sh.hist[d]) >= nd) {
-            dg = d;
-            break;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (attempt == 1) {
+      exact = true;
+      if (tid < 32) {  // CPython 3.12 sum(): Neumaier, keys in key order
+        // warp 0: 32 weights per coalesced load, broadcast by shuffles; every
+        // lane runs the same sequential recurrence
+        const int lane = tid;
+        double s = 0.0, c = 0.0;
+        for (int b = 0; b < Km; b += 32) {
+          const int m = b + lane;
+          const bool live = m < Km && !(dead && dead[m]);
+          const double xm = m < Km ? a.w[m] : 0.0;
+          u32 mk = __ballot_sync(MX_FULL, live);
+          while (mk) {
+            const int t = __ffs(mk) - 1;
+            mk &= mk - 1;
+            const double x = __shfl_sync(MX_FULL, xm, t);
+            const double tt = s + x;
+            if (fabs(s) >= fabs(x)) c += (s - tt) + x;
+            else c += (x - tt) + s;
+            s = tt;
           }
-          cum += sh.hist[d];
         }
-        sh.digit = dg;
-        sh.need = nd - (int)cum;
+        if (lane == 0) sh.wsum = c != 0.0 ? s + c : s;
       }
       __syncthreads();
-      prefix |= (unsigned long long)sh.digit << shift;
-      mask |= 0xffull << shift;
-      __syncthreads();
+      if (a.stats && tid == 0) {
+        const unsigned long long t_b = clock64();
+        a.stats[12] += t_b - t_a;
+        t_a = t_b;
+      }
     }
-    thr = prefix;
-    need = sh.need;  // how many keys with fkey == thr (lowest key first) get a unit
+    const double wsum = sh.wsum;
+    long long assigned = 0;
+    bool unstable = false;
+    double smax = 0.0;
+    for (int m = tid; m < Km; m += BIG_THREADS) {
+      if (dead && dead[m]) {
+        a.base[m] = 0;
+        a.fkey[m] = ~0ull;
+        continue;
+      }
+      const double share = a.w[m] / wsum * tot;
+      const double s9 = share + 1e-9;
+      const long long b = (long long)s9;
+      double fr = share - (double)b;
+      if (!exact) {
+        const double eta = fabs(share) * 4e-14 + 1e-290;
+        unstable |= (s9 - (double)b) < eta || ((double)b + 1.0 - s9) < eta || (fr != 0.0 && fabs(fr) < eta);
+        smax = share > smax ? share : smax;
+      }
+      fr = fr > 0.0 ? fr : 0.0;
+      a.base[m] = b;
+      a.fkey[m] = ~(unsigned long long)__double_as_longlong(fr);  // larger frac -> smaller key
+      assigned += b;
+    }
+    if (!exact && __syncthreads_or(unstable)) continue;
+    left = total - big_sum(assigned, sh);
+    thr = 0;
+    need = 0;
+    if (left > 0) {  // radix select: the left-th smallest (fkey, key) among alive keys
+      unsigned long long prefix = 0, mask = 0;
+      if (tid == 0) sh.need = (int)left;
+      for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int d = tid; d < 256; d += BIG_THREADS) sh.hist[d] = 0;
+        __syncthreads();
+        for (int m = tid; m < Km; m += BIG_THREADS) {
+          if (dead && dead[m]) continue;
+          const unsigned long long f = a.fkey[m];
+          if ((f & mask) == prefix) atomicAdd(&sh.hist[(f >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int nd = sh.need;
+          u32 cum = 0;
+          int dg = 255;
+          for (int d = 0; d < 256; ++d) {
+            if ((int)(cum + sh.hist[d]) >= nd) {
+              dg = d;
+              break;
+            }
+            cum += sh.hist[d];
+          }
+          sh.digit = dg;
+          sh.need = nd - (int)cum;
+        }
+        __syncthreads();
+        prefix |= (unsigned long long)sh.digit << shift;
+        mask |= 0xffull << shift;
+        __syncthreads();
+      }
+      thr = prefix;
+      need = sh.need;  // how many keys with fkey == thr (lowest key first) get a unit
+    }
+    if (exact || left <= 0) break;
+    // certificate of the leftover selection under the wsum uncertainty
+    const double eta_f = big_reduce(smax, [](double x, double y) { return x > y ? x : y; }) * 4e-14 + 1e-290;
+    unsigned long long prev = 0, next = ~0ull;  // nearest fkeys strictly below / above thr
+    int grp = 0;
+    double wmin = 1e308, wmax = -1e308;
+    for (int m = tid; m < Km; m += BIG_THREADS) {
+      if (dead && dead[m]) continue;
+      const unsigned long long f = a.fkey[m];
+      if (f < thr) prev = f > prev ? f : prev;
+      else if (f > thr) next = f < next ? f : next;
+      else {
+        ++grp;
+        wmin = a.w[m] < wmin ? a.w[m] : wmin;
+        wmax = a.w[m] > wmax ? a.w[m] : wmax;
+      }
+    }
+    prev = big_reduce(prev, [](unsigned long long x, unsigned long long y) { return x > y ? x : y; });
+    next = big_reduce(next, [](unsigned long long x, unsigned long long y) { return x < y ? x : y; });
+    grp = big_reduce(grp, [](int x, int y) { return x + y; });
+    wmin = big_reduce(wmin, [](double x, double y) { return x < y ? x : y; });
+    wmax = big_reduce(wmax, [](double x, double y) { return x > y ? x : y; });
+    auto frac_of = [](unsigned long long f) { return __longlong_as_double((long long)~f); };
+    const double f_thr = frac_of(thr);
+    bool ok = next == ~0ull || f_thr - frac_of(next) > eta_f;
+    if (need < grp) {  // the tie group is split by key order: it must tie in CPython too
+      ok = ok && (f_thr == 0.0 || wmin == wmax);
+      ok = ok && (thr == 0 || prev == 0 || frac_of(prev) - f_thr > eta_f || prev == thr);
+    }
+    if (ok) break;
+  }
+  if (a.stats && tid == 0) {
+    const unsigned long long t_b = clock64();
+    a.stats[13] += t_b - t_a;
+    t_a = t_b;
+    if (exact) a.stats[14] += 1;
   }
   // apply: base + 1 for fkey < thr, and the first `need` keys (in key order) with fkey == thr
   int taken = 0;  // running count of equal keys before this round
@@ -666,7 +788,18 @@ __device__ void big_apportion(const BigArgs& a, const unsigned char* dead, long 
   __syncthreads();
 }
 
+// MX_PLAN_STATS: thread 0 accumulates cycles per section into a.stats
+#define BIG_TICK(slot)                                       \
+  do {                                                       \
+    if (a.stats && tid == 0) {                               \
+      const unsigned long long now_ = clock64();             \
+      a.stats[slot] += now_ - tick_;                         \
+      tick_ = now_;                                          \
+    }                                                        \
+  } while (0)
+
 __global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a, int stage_w) {
+  unsigned long long tick_ = clock64();
   extern __shared__ __align__(16) unsigned char big_smem[];
   __shared__ BigShared sh;
   __shared__ long long s_min[BIG_THREADS / 32];
@@ -731,6 +864,8 @@ __global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a, int st
       }
       any_rem = __syncthreads_or(any_rem);
       any_new = __syncthreads_or(any_new);
+      BIG_TICK(0);
+      if (a.stats && tid == 0) a.stats[8] += 1;
       if (!any_new) {
         if (!any_rem) break;  // chunk complete
         continue;
@@ -763,6 +898,8 @@ __global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a, int st
       }
       if (tid == 0) sh.i_list = 0;
       __syncthreads();
+      BIG_TICK(1);
+      if (a.stats && tid == 0) a.stats[9] += n_list;
       while (true) {
         if (tid == 0) {
           sh.flag = 0;
@@ -820,8 +957,11 @@ __global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a, int st
           sh.alive = alive;
         }
         __syncthreads();
+        BIG_TICK(2);
         if (sh.status == 2 || !sh.flag) break;
         big_apportion(a, dead, sh.slow_r, rem, sh);  // exact general case; sets sh.wsum exactly
+        BIG_TICK(3);
+        if (a.stats && tid == 0) a.stats[10] += 1;
         if (tid == 0) {
           rem[sh.slow_d] = 0;
           sh.i_list += 1;
@@ -886,6 +1026,8 @@ __global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a, int st
       nt += tot;
       __syncthreads();
     }
+    BIG_TICK(4);
+    if (a.stats && tid == 0) a.stats[11] += 1;
     if (tid == 0) {
       Phase& ph = a.phases[n_ph];
       ph.chunk_begin = chunks;
@@ -2005,15 +2147,33 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     MX_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     const size_t base_smem = 9 * (size_t)Km + 4;
     const size_t staged = ((base_smem + 15) & ~(size_t)15) + 12 * (size_t)Km;
-    const int stage_w = staged + sizeof(BigShared) + 2048 <= (size_t)optin ? 1 : 0;
+    cudaFuncAttributes fa{};
+    MX_CUDA_TRY(cudaFuncGetAttributes(&fa, plan_big_kernel));
+    const size_t dyn_max = (size_t)optin - fa.sharedSizeBytes;
+    const int stage_w = staged <= dyn_max ? 1 : 0;
     const size_t smem = stage_w ? staged : base_smem;
     static size_t smem_set = 0;
     if (smem > smem_set) {
-      MX_CUDA_TRY(cudaFuncSetAttribute(plan_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       optin - (int)sizeof(BigShared) - 1024));
-      smem_set = optin - sizeof(BigShared) - 1024;
+      MX_CUDA_TRY(cudaFuncSetAttribute(plan_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
+      smem_set = dyn_max;
+    }
+    DevBuf<unsigned long long> stats;
+    const bool want_stats = getenv("MX_PLAN_STATS") != nullptr;
+    if (want_stats) {
+      MX_CUDA_TRY(stats.alloc(16, s));
+      MX_CUDA_TRY(cudaMemsetAsync(stats.p, 0, 16 * sizeof(unsigned long long), s));
+      ba.stats = stats.p;
     }
     plan_big_kernel<<<1, BIG_THREADS, smem, s>>>(ba, stage_w);
+    if (want_stats) {
+      unsigned long long h[16];
+      MX_CUDA_TRY(cudaMemcpyAsync(h, stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+      MX_CUDA_TRY(cudaStreamSynchronize(s));
+      fprintf(stderr,
+              "plan_big: cycles pass %llu list %llu redistribute %llu exact %llu phase %llu | passes %llu dead %llu "
+              "exact %llu phases %llu | apportion: sequential-sum cycles %llu rest %llu, sequential sums %llu\n",
+              h[0], h[1], h[2], h[3], h[4], h[8], h[9], h[10], h[11], h[12], h[13], h[14]);
+    }
   } else {
     plan_kernel<<<1, 32, 0, s>>>(pa);
   }
