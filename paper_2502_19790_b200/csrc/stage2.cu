@@ -697,19 +697,31 @@ __device__ void big_apportion(const BigArgs& a, const unsigned char* dead, long 
           if ((f & mask) == prefix) atomicAdd(&sh.hist[(f >> shift) & 255], 1u);
         }
         __syncthreads();
-        if (tid == 0) {
-          int nd = sh.need;
-          u32 cum = 0;
-          int dg = 255;
-          for (int d = 0; d < 256; ++d) {
-            if ((int)(cum + sh.hist[d]) >= nd) {
-              dg = d;
-              break;
-            }
-            cum += sh.hist[d];
+        if (tid < 32) {  // warp 0: which digit holds the need-th key (8 bins per lane + warp scan)
+          const int nd = sh.need;
+          u32 c8[8], sum8 = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            c8[q] = sh.hist[tid * 8 + q];
+            sum8 += c8[q];
           }
-          sh.digit = dg;
-          sh.need = nd - (int)cum;
+          const u32 inc = warp_incl_scan(sum8);
+          const u32 exc = inc - sum8;
+          const bool here = (int)exc < nd && (int)inc >= nd;
+          if (here) {
+            u32 cum = exc;
+            int dg = tid * 8 + 7;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if ((int)(cum + c8[q]) >= nd) {
+                dg = tid * 8 + q;
+                break;
+              }
+              cum += c8[q];
+            }
+            sh.digit = dg;
+            sh.need = nd - (int)cum;
+          }
         }
         __syncthreads();
         prefix |= (unsigned long long)sh.digit << shift;
