@@ -918,10 +918,17 @@ __global__ void __launch_bounds__(BIG_THREADS) plan_big_kernel(BigArgs a, int st
           double wsum = sh.wsum, werr = sh.werr;
           int alive = sh.alive;
           int i = sh.i_list;
+          // the next dead key and its weight rank are loaded one event ahead
+          u32 d_nx = i < n_list ? a.list[i] : 0u;
+          u32 rk_nx = i < n_list ? a.rank_w[d_nx] : 0u;
           for (; i < n_list; ++i) {
-            const u32 d = a.list[i];
+            const u32 d = d_nx, rk = rk_nx;
+            if (i + 1 < n_list) {
+              d_nx = a.list[i + 1];
+              rk_nx = a.rank_w[d_nx];
+            }
             dead[d] = 1;
-            nxt[a.rank_w[d]] = a.rank_w[d] + 1;  // unlink from the weight order
+            nxt[rk] = rk + 1;  // unlink from the weight order
             --alive;
             wsum -= a.w[d];
             werr += fabs(wsum) * 2.3e-16;
