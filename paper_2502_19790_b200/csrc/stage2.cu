@@ -1247,10 +1247,10 @@ __global__ void emit_count_kernel(EmitArgs a, u64 n_pairs, u64* pair_cnt) {
 // thread per (chunk, term) pair; pairs of more than 32 pieces (iid layouts:
 // ~500 intervals per term) are listed for emit_write_warp_kernel
 __global__ void emit_write_kernel(EmitArgs a, u64 n_pairs, const u64* pair_off, u32* pm, u32* pf, u32* ps, u32* pe,
-                                  u32* long_list, u32* long_cnt) {
+                                  u32* long_list, u32* long_cnt, u32 warp_min) {
   u64 pr = blockIdx.x * (u64)blockDim.x + threadIdx.x;
   if (pr >= n_pairs) return;
-  if (pair_off[pr + 1] - pair_off[pr] > 32) {
+  if (pair_off[pr + 1] - pair_off[pr] > warp_min) {
     long_list[atomicAdd(long_cnt, 1u)] = (u32)pr;
     return;
   }
@@ -1897,7 +1897,8 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
     MX_CUDA_TRY(llist.alloc(n_pairs, s));
     MX_CUDA_TRY(lcnt.alloc(1, s));
     MX_CUDA_TRY(cudaMemsetAsync(lcnt.p, 0, sizeof(u32), s));
-    emit_write_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p);
+    static const u32 warp_min = getenv("MX_EMIT_WARP_MIN") ? (u32)atoi(getenv("MX_EMIT_WARP_MIN")) : 32u;
+    emit_write_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p, warp_min);
     mx_count_launch();
     const long long wgrid = std::min<long long>(((long long)n_pairs + 7) / 8, 148 * 16);
     emit_write_warp_kernel<<<(unsigned)wgrid, 256, 0, s>>>(a, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p);
