@@ -198,6 +198,18 @@ class ChunkerIndex:
     def matching_keys(self, mixture_key: MixtureKey) -> list[MixtureKey]:
         return [k for k in self.component_keys() if mixture_key.matches(k)]
 
+    def cursor(self, key: MixtureKey, seed: int) -> "RangeCursor":
+        """``ChunkerIndex.cursor`` (``index.py:78-79``): the key's RangeCursor for
+        a job seed. The seeded layout is the one the device generator builds
+        (``csrc/cursor.cu``); take / state are the reference's bookkeeping."""
+        from .chunks import ChunkGenerator
+
+        gens = self.__dict__.setdefault("_cursor_gens", {})
+        gen = gens.get(int(seed))
+        if gen is None:
+            gen = gens[int(seed)] = ChunkGenerator(self, int(seed))
+        return RangeCursor(key, gen.cursor_ranges(key), int(seed))
+
     def key_sample_counts(self) -> dict[MixtureKey, int]:
         keys = self.component_keys()
         return {k: int(n) for k, n in zip(keys, self._counts)}
@@ -222,6 +234,53 @@ class ChunkerIndex:
         return mine == conv
 
     __hash__ = None
+
+
+class RangeCursor:
+    """One key's remaining samples as ranges in the seeded order
+    (``index.py:118-189``): ``take(n)``, ``depleted``, ``state_dict`` /
+    ``load_state``; ``_ranges`` is the device-computed layout."""
+
+    def __init__(self, key: MixtureKey, ranges: list[tuple[int, int, int, int]], seed: int):
+        self.key = key
+        self.seed = seed
+        self._ranges = list(ranges)
+        self._pos = 0
+        self._offset = 0
+        self.remaining_total = sum(e - s for _, _, s, e in self._ranges)
+
+    def take(self, n: int) -> list[tuple[int, int, int, int]]:
+        if n < 1:
+            raise ValueError("take() needs n >= 1")
+        out = []
+        need = n
+        while need > 0 and self._pos < len(self._ranges):
+            ds, fid, start, end = self._ranges[self._pos]
+            cur = start + self._offset
+            if end - cur <= need:
+                out.append((ds, fid, cur, end))
+                need -= end - cur
+                self._pos += 1
+                self._offset = 0
+            else:
+                out.append((ds, fid, cur, cur + need))
+                self._offset += need
+                need = 0
+        self.remaining_total -= n - need
+        return out
+
+    @property
+    def depleted(self) -> bool:
+        return self.remaining_total == 0
+
+    def state_dict(self) -> dict:
+        return {"pos": self._pos, "offset": self._offset}
+
+    def load_state(self, state) -> None:
+        self._pos = int(state["pos"])
+        self._offset = int(state["offset"])
+        consumed = sum(e - s for _, _, s, e in self._ranges[: self._pos]) + self._offset
+        self.remaining_total = sum(e - s for _, _, s, e in self._ranges) - consumed
 
 
 def build_index_from_catalog(catalog, predicates: Sequence = (), stream=None) -> ChunkerIndex:

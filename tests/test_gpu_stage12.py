@@ -100,3 +100,44 @@ def test_restore_mid_stream_resumes_identically():
     for i in range(5):
         gen3.generate(spec)
     assert gen3.state_dict() == st
+
+
+@pytest.mark.parametrize("case", ["cfg1_r64", "filters_nulls"])
+def test_index_cursor_take_and_state(case):
+    """ChunkerIndex.cursor(key, seed) (index.py:78-79, RangeCursor :118-189):
+    the seeded layout is the golden one and take / depletion / state follow
+    the reference semantics (replayed here on the golden range list)."""
+    idx, g = _index(case)
+    for k in idx.component_keys()[:6]:
+        cur = idx.cursor(k, g["job_seed"])
+        ranges = [tuple(r) for r in g["cursors"][k.canonical_string()]]
+        assert cur._ranges == ranges
+        total = sum(e - s for _, _, s, e in ranges)
+        with pytest.raises(ValueError):
+            cur.take(0)
+        # reference take() replayed on the golden list
+        pos, off, served = 0, 0, 0
+        for n in (1, 7, 100, 3, 10_000, 10_000_000):
+            got = cur.take(n)
+            want, need = [], n
+            while need > 0 and pos < len(ranges):
+                ds, fid, s, e = ranges[pos]
+                c = s + off
+                if e - c <= need:
+                    want.append((ds, fid, c, e))
+                    need -= e - c
+                    pos, off = pos + 1, 0
+                else:
+                    want.append((ds, fid, c, c + need))
+                    off += need
+                    need = 0
+            served += n - need
+            assert got == want
+            assert cur.remaining_total == total - served
+            if n == 100:
+                st = cur.state_dict()
+                assert st == {"pos": pos, "offset": off}
+                other = idx.cursor(k, g["job_seed"])
+                other.load_state(st)
+                assert other.remaining_total == cur.remaining_total
+        assert cur.depleted and cur.take(5) == []
