@@ -333,6 +333,41 @@ def our_arm(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     n = rt.n_samples
+    # ------------------------------------------------------------ two jobs in flight
+    # (the reference server runs one thread per job): 2 host threads, 2 streams
+    concurrent = None
+    if world == 1 and args.concurrent:
+        import threading
+
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        per = max(1, args.steps // 2)
+
+        def worker(st):
+            with torch.cuda.stream(st):
+                for _ in range(per):
+                    i_, g_, b_ = run_step(dcat, spec, stream=st)
+                    del i_, g_, b_
+
+        for _ in range(2):  # warm the second stream / thread-local state
+            worker(streams[1])
+        barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for st in streams:
+            st.wait_stream(stream)
+        ths = [threading.Thread(target=worker, args=(st,)) for st in streams]
+        for t_ in ths:
+            t_.start()
+        for t_ in ths:
+            t_.join()
+        for st in streams:
+            stream.wait_stream(st)
+        c1.record(stream)
+        barrier()
+        cms = c0.elapsed_time(c1) / (2 * per)
+        concurrent = {"jobs_in_flight": 2, "jobs": 2 * per, "ms_per_job": cms, "value": n / (cms * 1e-3),
+                      "unit": UNIT, "note": "two host threads, one CUDA stream each, the same job repeated; "
+                                            "amortised time per job"}
     # ------------------------------------------------------------ e2e (host buffers)
     pinned = {p: c.cpu().pin_memory() for p, c in cols.items()}
     del cols, dcat
@@ -399,6 +434,7 @@ def our_arm(args):
         "e2e": {"value": world * n / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": ems},
         "gpu_launches": int(launches * args.steps),
+        **({"concurrent_jobs": concurrent} if concurrent else {}),
         "clocks": clk,
     }
     if not args.no_cpu_baseline and world == 1:
@@ -424,6 +460,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of the cfg2 size (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--concurrent", action="store_true",
+                    help="also time two jobs in flight (two host threads, two streams); diagnostic")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

@@ -141,3 +141,38 @@ def test_index_cursor_take_and_state(case):
                 other.load_state(st)
                 assert other.remaining_total == cur.remaining_total
         assert cur.depleted and cur.take(5) == []
+
+
+def test_concurrent_jobs_on_two_streams():
+    """Distinct jobs on distinct streams from two host threads (the reference
+    server runs one thread per connection) give the sequential results."""
+    import threading
+
+    import torch
+
+    from paper_2502_19790_b200 import ChunkGenerator, DeviceCatalog, build_index_from_catalog
+
+    cc, g = load_golden("cfg2_small")
+    dcat = DeviceCatalog(cc)
+    spec = spec_from_json(g["mixtures"]["cfg2"])
+
+    def job(stream, seed, out, key):
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                idx = build_index_from_catalog(dcat, golden_predicates(g), stream=stream)
+                gen = ChunkGenerator(idx, seed, stream=stream)
+                batch = gen.plan_batch(spec, 10_000)
+                h = batch.to_host()
+                out[key] = {k: v.copy() for k, v in h.items()}
+
+    want = {}
+    job(torch.cuda.current_stream(), g["job_seed"], want, "a")
+    job(torch.cuda.current_stream(), 7, want, "b")
+    got = {}
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    t1 = threading.Thread(target=job, args=(s1, g["job_seed"], got, "a"))
+    t2 = threading.Thread(target=job, args=(s2, 7, got, "b"))
+    t1.start(); t2.start(); t1.join(); t2.join()
+    for key in ("a", "b"):
+        for f in want[key]:
+            assert (got[key][f] == want[key][f]).all(), (key, f)
