@@ -5,8 +5,11 @@
 Workload (BASELINE.json configs[1], SURVEY.md §8d cfg 2): 100M samples in
 10,000 files, 5 int32 property columns (cards 4,5,5,4,5 -> 2,000 component
 keys), run layout R=64, static multi-property best-effort mixture, chunk 1024,
-job seed 42. Synthetic metadata (seeded run table expanded on the device);
-2 GB of columns > 126 MB L2, so no L2 flush is needed between steps.
+job seed 42. Synthetic metadata (seeded run table expanded on the device).
+Catalog layout (--layout): "tuples" (default) dictionary-encodes the rows once
+at registration into ONE int32 row-tuple code column (400 MB); "columns" keeps
+one int32 column per property (2 GB). Both exceed the 126 MB L2, so no L2
+flush is needed between steps.
 
 One STEP = the whole job on the device: stage 1 (filter + key pack + runs +
 grouping into the ChunkerIndex) + RangeCursor layout + emission of EVERY chunk
@@ -54,6 +57,10 @@ CFG = dict(workload="cfg2: 100M samples, 10k files, 5 props (4,5,5,4,5) -> 2000 
                     "static 4-key best-effort mixture, chunk 1024, seed 42",
            n_samples=100_000_000, n_files=10_000, props=5, run_mean=64, chunk_size=1024, job_seed=42,
            l2="inputs (2 GB of columns) exceed the 126 MB L2; no flush needed")
+LAYOUT_NOTE = {
+    "tuples": "row tuples: one int32 code column (rows dictionary-encoded at registration) + per-query tuple LUT",
+    "columns": "one int32 code column per property + per-query per-property LUTs",
+}
 REF_SAMPLE = 2_000_000  # --impl reference: samples per step (bounded CPU slice, ~5 s through the reference)
 CPU_SAMPLE = 10_000_000  # cpu_baseline leg of our arm
 
@@ -130,12 +137,27 @@ def device_columns(rt, device):
     return {p: torch.repeat_interleave(torch.from_numpy(c).to(device), lens) for p, c in rt.run_codes.items()}
 
 
-def device_catalog(meta, cols):
+def device_catalog(meta, cols, table=None):
     """The catalog over HBM-resident columns (built once per catalog, like the
-    reference's registered MetadataCatalog; every job reuses it)."""
+    reference's registered MetadataCatalog; every job reuses it). With
+    `table` (row-tuple layout) `cols` is {"tuples": int32 tuple-code column}."""
     from paper_2502_19790_b200 import DeviceCatalog
 
+    if table is not None:
+        return DeviceCatalog(meta, tuples=(cols["tuples"], table), nullable={p: False for p in meta.vocab})
     return DeviceCatalog(meta, columns=cols, nullable={p: False for p in cols})
+
+
+def layout_columns(rt, cols, layout):
+    """(columns dict, tuple table or None) in the requested catalog layout:
+    "tuples" dictionary-encodes the rows once at registration (untimed, like
+    the reference's value interning) into one int32 row-tuple code column."""
+    if layout != "tuples":
+        return cols, None
+    from paper_2502_19790_b200 import DeviceCatalog
+
+    codes, table = DeviceCatalog.encode_row_tuples_device(cols, [len(rt.vocab[p]) for p in sorted(rt.vocab)])
+    return {"tuples": codes}, table
 
 
 def run_step(dcat, spec, stream=None, shard=None):
@@ -287,7 +309,8 @@ def our_arm(args):
     L = _lib.lib()
     rt = make_workload(rank, args.scale)
     meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
-    cols = device_columns(rt, device)
+    cols, table = layout_columns(rt, device_columns(rt, device), args.layout)
+    n_cols = len(cols)
     spec = synth.cfg2_mixture(CFG["chunk_size"])
     shard = None
     if world > 1:  # rank r owns global files [r*F, (r+1)*F) of one W*F-file catalog
@@ -300,7 +323,7 @@ def our_arm(args):
         if world > 1:
             dist.barrier()
 
-    dcat = device_catalog(meta, cols)
+    dcat = device_catalog(meta, cols, table)
     for _ in range(args.warmup):
         idx, gen, batch = run_step(dcat, spec, shard=shard)
         del idx, gen, batch
@@ -376,7 +399,7 @@ def our_arm(args):
 
     def e2e_step():
         dcols = {p: x.to(device, non_blocking=True) for p, x in pinned.items()}
-        idx, gen, batch = run_step(device_catalog(meta, dcols), spec, shard=shard)
+        idx, gen, batch = run_step(device_catalog(meta, dcols, table), spec, shard=shard)
         if rank != 0:  # the merged global chunks are read back on the root
             return 0
         h = batch.to_host()
@@ -404,7 +427,7 @@ def our_arm(args):
     peak, peak_kind = peaks()
     scan_ms, scan_n = phases["scan_runs"]
     scan_avg = scan_ms / max(scan_n, 1)
-    scan_bytes = n * 4 * len(rt.run_codes) + 16 * n_iv
+    scan_bytes = n * 4 * n_cols + 16 * n_iv
     step_bytes = scan_bytes + 8 * n_blocks + 16 * n_keys + 16 * n_iv + 20 * n_ranges + 8 * n_chunks
     achieved = scan_bytes / (scan_avg * 1e-3) / 1e9
     traffic = None
@@ -415,7 +438,10 @@ def our_arm(args):
         "metric": METRIC, "value": world * n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": dict(CFG, parallelism=f"file-sharded x{world}" if world > 1 else "single GPU"),
+        "config": dict(CFG, parallelism=f"file-sharded x{world}" if world > 1 else "single GPU",
+                       layout=LAYOUT_NOTE[args.layout],
+                       l2=f"inputs ({n * 4 * n_cols / 1e9:.1f} GB of code columns) exceed the 126 MB L2; "
+                          "no flush needed"),
         "chunks_per_s": n_chunks / (ms_max * 1e-3),
         "job": {"samples": n, "intervals": n_iv, "keys": n_keys, "blocks": n_blocks, "chunks": n_chunks,
                 "ranges": n_ranges},
@@ -423,12 +449,12 @@ def our_arm(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "scan_fast_kernel (the scan_runs phase: scan_fast + deferred-tile scan_list + tail scan_direct)",
                      "bytes_per_launch": scan_bytes, "peak_kind": peak_kind,
-                     "note": "algorithmic bytes = N*4*P column reads + 16 B per interval record"},
+                     "note": "algorithmic bytes = N*4*C code-column reads (C = 1 row-tuple column, or P per-property columns) + 16 B per interval record"},
         # the whole job against the same peak (B1 + B2 per step)
         "roofline_step": {
             "bytes": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
             "frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
-            "note": "B1 = N*4*P + 16*I + 8*B + 16*K, B2 = 16*I (intervals touched) + 20*ranges + 8*chunks; "
+            "note": "B1 = N*4*C + 16*I + 8*B + 16*K, B2 = 16*I (intervals touched) + 20*ranges + 8*chunks; "
                     "the gap to the scan's fraction is the latency-bound cursor / plan / emission work and "
                     "the host synchronisations between them"},
         "e2e": {"value": world * n / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -458,6 +484,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layout", default="tuples", choices=["tuples", "columns"],
+                    help="catalog layout in HBM: one row-tuple code column, or one code column per property")
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of the cfg2 size (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--concurrent", action="store_true",

@@ -83,6 +83,15 @@ typedef struct mx_catalog_desc {
   const uint8_t* key_strings;
   const int64_t* key_string_offsets; /* host [n_pieces+1] */
   const int32_t* key_string_base;    /* host [n_props] */
+  /* Row-tuple layout (ABI 2). 0 = one code column per property, as above.
+   * > 0 = the catalog stores its rows dictionary-encoded: columns[0..n_columns)
+   * hold row-tuple codes and lut/lut_offsets have n_columns segments whose
+   * entry (code+1) is the tuple's whole packed key | 0x80000000 if any of its
+   * property codes fails the filter (the sum / OR of the per-property entries,
+   * codec.py). n_key_pieces = number of key-string pieces (the per-property
+   * cardinalities are then not derivable from lut_offsets). */
+  int32_t n_columns;
+  int32_t n_key_pieces;
 } mx_catalog_desc;
 
 /* Fused filter + interval detection + index build

@@ -59,6 +59,8 @@ class CatalogDesc(C.Structure):
         ("key_strings", P(C.c_uint8)),
         ("key_string_offsets", P(i64)),
         ("key_string_base", P(i32)),
+        ("n_columns", i32),
+        ("n_key_pieces", i32),
     ]
 
 

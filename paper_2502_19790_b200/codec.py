@@ -139,6 +139,25 @@ class KeyCodec:
             offs.append(offs[-1] + card + 1)
         return np.concatenate(parts).astype(np.uint32), np.array(offs, dtype=np.int32)
 
+    def tuple_luts(self, cat: ColumnarCatalog, preds: list[FilterPredicate],
+                   table: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+        """LUT over row-tuple codes (``encode_row_tuples``): entry (t+1) is the
+        sum of row tuple t's per-property entries (its whole packed key) with
+        FAIL set when any of its property codes fails the filter -- exactly
+        what the per-property scan computes for a row holding those codes."""
+        lut, off = self.luts(cat, preds)
+        t = np.asarray(table, dtype=np.int64)
+        key = np.zeros(len(t), dtype=np.uint64)
+        fail = np.zeros(len(t), dtype=bool)
+        for j in range(len(self.props)):
+            e = lut[off[j] + t[:, j] + 1]
+            key += (e & ~FAIL).astype(np.uint64)
+            fail |= (e & FAIL) != 0
+        out = np.empty(len(t) + 1, dtype=np.uint32)
+        out[0] = FAIL  # no row holds code -1
+        out[1:] = key.astype(np.uint32) | np.where(fail, FAIL, np.uint32(0)).astype(np.uint32)
+        return out, np.array([0, len(out)], dtype=np.int32)
+
     # ---------------------------------------------------------------- keys
     def rank_of(self, packed: int, j: int) -> int:
         return (int(packed) >> self.shift[j]) & ((1 << self.width[j]) - 1)

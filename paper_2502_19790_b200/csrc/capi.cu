@@ -218,7 +218,7 @@ int mx_profile_read(const char* phase, double* total_ms, int64_t* count) {
   if (count) *count = it == g_prof.end() ? 0 : it->second.count;
   return MX_OK;
 }
-int mx_abi_version(void) { return 1; }
+int mx_abi_version(void) { return 2; }
 
 int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out) {
   MX_CHECK_ARG(desc && out, "null argument");
@@ -237,8 +237,8 @@ int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out) {
   int rc = MX_OK;
   // key strings for device BLAKE2b
   {
-    int n_pieces = 0;
-    for (int p = 0; p < desc->n_props && p < MX_MAX_PROPS; ++p) {
+    int n_pieces = desc->n_columns > 0 ? desc->n_key_pieces : 0;
+    for (int p = 0; desc->n_columns <= 0 && p < desc->n_props && p < MX_MAX_PROPS; ++p) {
       int card = (desc->lut_offsets[p + 1] - desc->lut_offsets[p]) - 1;
       n_pieces = std::max(n_pieces, desc->key_string_base[p] + card);
     }

@@ -23,6 +23,10 @@
 #include "common.cuh"
 
 #define MX_SMEM_LUT_MAX 12288
+// scan_fast_kernel stages LUTs up to this many entries per CTA; larger ones
+// (row-tuple layout) are read through L1 (one CTA per 2048-sample tile: a
+// staged 2,000-entry LUT is as many bytes as the tile's column)
+#define MX_STAGED_LUT_MAX 512
 
 namespace mx {
 

@@ -465,7 +465,7 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
   }
 }
 
-template <int PC, int SEGS>
+template <int PC, int SEGS, bool GLUT = false>
 __device__ __forceinline__ void lut_sums(const u32* s_lut, const S1Args& a, const int4 (&v)[PC][SEGS],
                                          u32 (&st)[SEGS][4]) {
 #pragma unroll
@@ -474,11 +474,20 @@ __device__ __forceinline__ void lut_sums(const u32* s_lut, const S1Args& a, cons
     for (int q = 0; q < 4; ++q) st[j][q] = 0;
 #pragma unroll
   for (int p = 0; p < PC; ++p) {
-    const u32* L = s_lut + a.lut_off[p] + 1;
+    if (GLUT) {  // large LUT (row-tuple layout): read-only path, L1-resident
+      const u32* __restrict__ L = a.lut_sum + a.lut_off[p] + 1;
 #pragma unroll
-    for (int j = 0; j < SEGS; ++j) {
-      st[j][0] += L[v[p][j].x]; st[j][1] += L[v[p][j].y];
-      st[j][2] += L[v[p][j].z]; st[j][3] += L[v[p][j].w];
+      for (int j = 0; j < SEGS; ++j) {
+        st[j][0] += __ldg(L + v[p][j].x); st[j][1] += __ldg(L + v[p][j].y);
+        st[j][2] += __ldg(L + v[p][j].z); st[j][3] += __ldg(L + v[p][j].w);
+      }
+    } else {
+      const u32* L = s_lut + a.lut_off[p] + 1;
+#pragma unroll
+      for (int j = 0; j < SEGS; ++j) {
+        st[j][0] += L[v[p][j].x]; st[j][1] += L[v[p][j].y];
+        st[j][2] += L[v[p][j].z]; st[j][3] += L[v[p][j].w];
+      }
     }
   }
 }
@@ -486,8 +495,14 @@ __device__ __forceinline__ void lut_sums(const u32* s_lut, const S1Args& a, cons
 // one CTA per full tile, loads in registers. SEGS = int4 segments per thread:
 // 4 (4096-sample tiles, 2 CTAs/SM) or 2 (2048-sample tiles, 4 CTAs/SM: the
 // same bytes in flight per SM, split over twice as many independent CTAs).
-template <int PC, int SEGS>
-__global__ void __launch_bounds__(S1_THREADS, SEGS == 2 ? 4 : 2)
+// GLUT: the LUT is read through L1 instead of being staged per CTA -- for a
+// row-tuple LUT (thousands of entries) staging would copy as many bytes per
+// CTA as the tile's column itself.
+// OCC: resident CTAs per SM the register budget is cut for. A single code
+// column (row-tuple layout) has 5x fewer bytes in flight per CTA than the
+// 5-property case, so it runs more CTAs per SM instead.
+template <int PC, int SEGS, bool GLUT = false, int OCC = (SEGS == 2 ? 4 : 2)>
+__global__ void __launch_bounds__(S1_THREADS, OCC)
 scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
   constexpr int TILE = S1_THREADS * 4 * SEGS;
   extern __shared__ __align__(16) u32 s_lut[];
@@ -504,7 +519,8 @@ scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
 #pragma unroll
     for (int j = 0; j < SEGS; ++j) v[p][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + 128 * j));
   }
-  for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
+  if (!GLUT)
+    for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
   const TileMeta m = meta[tile];
   if (m.nf > FAST_MAX_FS) {  // many tiny files: deferred to scan_list_kernel
     if (tid == 0) a.defer_list[atomicAdd(a.defer_cnt, 1u)] = (u32)tile;
@@ -513,8 +529,55 @@ scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
   if (tid < FAST_MAX_FS) s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - t0) : 1 << 30;
   __syncthreads();
   u32 st[SEGS][4];
-  lut_sums<PC, SEGS>(s_lut, a, v, st);
+  lut_sums<PC, SEGS, GLUT>(s_lut, a, v, st);
   fast_tile<SEGS>(a, m, tile, st, sc, s_fs);
+}
+
+// Single code column (row-tuple layout): 8 KB of column per 2048-sample tile
+// is too little work per CTA -- one CTA per tile is then bound by the CTA
+// launch rate (~0.9 us per CTA per SM whatever the occupancy: 0.29 ms for
+// 48.8k tiles). Persistent CTAs walk the tiles grid-stride and prefetch the
+// next tile's column segments into registers while finishing the current one.
+template <int SEGS, bool GLUT, int OCC>
+__global__ void __launch_bounds__(S1_THREADS, OCC)
+scan_fast1_kernel(S1Args a, const TileMeta* __restrict__ meta, long long nfull) {
+  constexpr int TILE = S1_THREADS * 4 * SEGS;
+  extern __shared__ __align__(16) u32 s_lut[];
+  __shared__ TileScratch sc;
+  __shared__ int s_fs[FAST_MAX_FS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lw = warp * 128 * SEGS + 4 * lane;
+  const int32_t* col = a.cols[0] + lw;
+  int4 v[1][SEGS];
+  long long tile = blockIdx.x;
+  if (tile < nfull) {
+#pragma unroll
+    for (int j = 0; j < SEGS; ++j) v[0][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + tile * TILE + 128 * j));
+  }
+  if (!GLUT)
+    for (int i = tid; i < a.lut_off[1]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
+  for (; tile < nfull; tile += gridDim.x) {
+    const long long t0 = tile * TILE;
+    const TileMeta m = meta[tile];
+    int4 cur[1][SEGS];
+#pragma unroll
+    for (int j = 0; j < SEGS; ++j) cur[0][j] = v[0][j];
+    const long long nxt = tile + gridDim.x;
+    if (nxt < nfull) {
+#pragma unroll
+      for (int j = 0; j < SEGS; ++j) v[0][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + nxt * TILE + 128 * j));
+    }
+    if (m.nf > FAST_MAX_FS) {  // CTA-uniform: many tiny files, deferred to scan_list_kernel
+      if (tid == 0) a.defer_list[atomicAdd(a.defer_cnt, 1u)] = (u32)tile;
+      continue;
+    }
+    __syncthreads();  // the previous tile's readers of s_fs / sc / s_off are done (and the LUT is staged)
+    if (tid < FAST_MAX_FS) s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - t0) : 1 << 30;
+    __syncthreads();
+    u32 st[SEGS][4];
+    lut_sums<1, SEGS, GLUT>(s_lut, a, cur, st);
+    fast_tile<SEGS>(a, m, tile, st, sc, s_fs);
+  }
 }
 
 // persistent CTAs, every full tile's columns + metadata streamed into a ring

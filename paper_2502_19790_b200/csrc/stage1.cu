@@ -505,7 +505,36 @@ static void launch_fast(const S1Args& a, const TileMeta* m, long long nfull, int
     kernel<<<(unsigned)std::min<long long>(nfull, n_sm), S1_THREADS, dyn, s>>>(a, m, nfull, stages, lut_bytes);
     return;
   }
-  scan_fast_kernel<PC, SEGS><<<(unsigned)nfull, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m);
+  if constexpr (PC == 1 && SEGS == 2) {
+    // one code column: more CTAs per SM (MX_FAST1_OCC = 4 | 6 | 8, default
+    // 8); MX_SCAN=fast1_persist selects persistent grid-stride CTAs
+    // (measured slower: 0.35 vs 0.29 ms at cfg2)
+    const char* occ_env = getenv("MX_FAST1_OCC");
+    const int occ = occ_env ? atoi(occ_env) : 8;
+    const bool persist = env && !strcmp(env, "fast1_persist");
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const bool g = lut_total > MX_STAGED_LUT_MAX;
+    const size_t dyn = g ? 0 : sizeof(u32) * lut_total;
+    const int o = occ >= 8 ? 8 : (occ >= 6 ? 6 : 4);
+    const unsigned pgrid = (unsigned)std::min<long long>(nfull, (long long)n_sm * o);
+#define MX_FAST1_LAUNCH(O)                                                                        \
+  if (persist) {                                                                                  \
+    if (g) scan_fast1_kernel<SEGS, true, O><<<pgrid, S1_THREADS, dyn, s>>>(a, m, nfull);          \
+    else scan_fast1_kernel<SEGS, false, O><<<pgrid, S1_THREADS, dyn, s>>>(a, m, nfull);           \
+  } else {                                                                                        \
+    if (g) scan_fast_kernel<PC, SEGS, true, O><<<(unsigned)nfull, S1_THREADS, dyn, s>>>(a, m);    \
+    else scan_fast_kernel<PC, SEGS, false, O><<<(unsigned)nfull, S1_THREADS, dyn, s>>>(a, m);     \
+  }
+    if (o == 8) { MX_FAST1_LAUNCH(8) } else if (o == 6) { MX_FAST1_LAUNCH(6) } else { MX_FAST1_LAUNCH(4) }
+#undef MX_FAST1_LAUNCH
+    return;
+  }
+  if (lut_total > MX_STAGED_LUT_MAX)
+    scan_fast_kernel<PC, SEGS, true><<<(unsigned)nfull, S1_THREADS, 0, s>>>(a, m);
+  else
+    scan_fast_kernel<PC, SEGS><<<(unsigned)nfull, S1_THREADS, sizeof(u32) * lut_total, s>>>(a, m);
 }
 
 // full tiles through scan_fast_kernel when it applies, the rest generically
@@ -544,6 +573,9 @@ struct TileOffF {
 int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   if (d->n_props < 1 || d->n_props > MX_MAX_PROPS)
     return mx_fail(MX_ERR_UNSUPPORTED, "n_props=%d outside [1, %d]", d->n_props, MX_MAX_PROPS);
+  // scanned columns: one per property, or the row-tuple code column(s)
+  const int NC = d->n_columns > 0 ? d->n_columns : d->n_props;
+  if (NC > MX_MAX_PROPS) return mx_fail(MX_ERR_UNSUPPORTED, "n_columns=%d > %d", NC, MX_MAX_PROPS);
   if (d->key_bits > 31)
     return mx_fail(MX_ERR_UNSUPPORTED, "packed key needs %u bits (> 31)", d->key_bits);
   if (d->n_files < 1) return mx_fail(MX_ERR_QUERY, "catalog is empty");
@@ -553,10 +585,10 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   ix.key_bits = d->key_bits;
   const long long n = d->n_samples;
   S1Args a{};
-  a.n_props = d->n_props;
-  for (int p = 0; p < d->n_props; ++p) a.cols[p] = d->columns[p];
-  for (int p = 0; p <= d->n_props; ++p) a.lut_off[p] = d->lut_offsets[p];
-  const int lut_total = d->lut_offsets[d->n_props];
+  a.n_props = NC;
+  for (int p = 0; p < NC; ++p) a.cols[p] = d->columns[p];
+  for (int p = 0; p <= NC; ++p) a.lut_off[p] = d->lut_offsets[p];
+  const int lut_total = d->lut_offsets[NC];
   DevBuf<u32> lut;
   MX_CUDA_TRY(lut.alloc(lut_total, s));
   MX_CUDA_TRY(mx_h2d(lut.p, d->lut, sizeof(u32) * lut_total, s));
@@ -565,7 +597,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   // bitlen(P) <= 31), see scan_direct_kernel
   DevBuf<u32> lut_sum;
   int pbits = 0;
-  while ((1 << pbits) <= d->n_props) ++pbits;
+  while ((1 << pbits) <= NC) ++pbits;
   const bool sum_ok = d->key_bits + pbits <= 31;
   if (sum_ok) {
     std::vector<u32> ls(lut_total);
@@ -602,7 +634,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   MX_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int lut_bytes = smem_lut ? (lut_total * 4 + 127) / 128 * 128 : 0;
-  const int P = d->n_props;
+  const int P = NC;
   // pipe geometry: the widest tile whose ring of >= 2 slots fits, then as
   // many slots (<= 4) as fit in ~200 KB
   int pipe_segs = 1, stages = 2;

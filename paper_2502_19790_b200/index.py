@@ -25,15 +25,30 @@ from .mixtures import MixtureKey, sorted_keys
 class DeviceCatalog:
     """A ``ColumnarCatalog`` uploaded to HBM (columns in property-name order)."""
 
-    def __init__(self, host: ColumnarCatalog, columns=None, nullable=None, device=None):
+    def __init__(self, host: ColumnarCatalog, columns=None, nullable=None, device=None, tuples=None):
+        """``tuples`` = (int32 row-tuple code column in HBM, int32[T, P] tuple
+        table in property-name order) selects the row-tuple layout
+        (``encode_row_tuples`` / ``encode_row_tuples_device``): stage 1 then
+        scans one 4-byte column instead of one per property."""
         import torch
 
         self.host = host
         self.device = torch.device(device or "cuda")
         props = sorted(host.vocab)
-        if columns is None:
-            columns = {p: torch.from_numpy(host.columns[p]).to(self.device) for p in props}
-        self.columns = {p: columns[p].contiguous() for p in props}
+        self.tuple_codes = self.tuple_table = None
+        if tuples is not None:
+            codes, table = tuples
+            self.tuple_codes = codes.contiguous()
+            self.tuple_table = np.ascontiguousarray(table, dtype=np.int32)
+            if self.tuple_table.ndim != 2 or self.tuple_table.shape[1] != len(props):
+                raise ValueError("tuple table must be [T, n_props]")
+            self.columns = None
+            if nullable is None:
+                nullable = {p: bool((self.tuple_table[:, j] < 0).any()) for j, p in enumerate(props)}
+        else:
+            if columns is None:
+                columns = {p: torch.from_numpy(host.columns[p]).to(self.device) for p in props}
+            self.columns = {p: columns[p].contiguous() for p in props}
         if nullable is None:
             nullable = {p: bool((self.columns[p] < 0).any().item()) for p in props}
         self.nullable = nullable
@@ -45,6 +60,27 @@ class DeviceCatalog:
         self.file_ds = np.ascontiguousarray(ds, dtype=np.int32)
         self.file_ids = np.ascontiguousarray(host.file_ids, dtype=np.int64)
         self._strings = self.codec.key_strings()
+
+    @staticmethod
+    def encode_row_tuples_device(columns: dict, cards) -> tuple:
+        """Device twin of ``catalog.encode_row_tuples`` for HBM-resident
+        columns ({prop: int32 tensor}, property-name order): (int32 codes in
+        HBM, int32[T, P] host tuple table)."""
+        import torch
+
+        from .catalog import _tuple_radix, row_tuple_table
+
+        props = sorted(columns)
+        mult = _tuple_radix(cards)
+        r = None
+        for p, m in zip(props, mult):
+            t = (columns[p].to(torch.int64) + 1) * m
+            r = t if r is None else r.add_(t)
+        u, inv = torch.unique(r, sorted=True, return_inverse=True)
+        del r
+        if u.numel() >= 1 << 31:
+            raise ValueError("more than 2^31 distinct row tuples")
+        return inv.to(torch.int32), row_tuple_table(u.cpu().numpy(), cards)
 
     @staticmethod
     def from_reference(cat, device=None) -> "DeviceCatalog":
@@ -68,8 +104,12 @@ class DeviceCatalog:
 
     def _descriptor(self, preds: list[FilterPredicate]):
         codec = self.codec
-        lut, lut_off = codec.luts(self.host, preds)
-        cols = (C.c_void_p * len(codec.props))(*[self.columns[p].data_ptr() for p in codec.props])
+        if self.tuple_codes is not None:
+            lut, lut_off = codec.tuple_luts(self.host, preds, self.tuple_table)
+            cols = (C.c_void_p * 1)(self.tuple_codes.data_ptr())
+        else:
+            lut, lut_off = codec.luts(self.host, preds)
+            cols = (C.c_void_p * len(codec.props))(*[self.columns[p].data_ptr() for p in codec.props])
         blob, soff, sbase = self._strings
         keep = dict(
             lut=np.ascontiguousarray(lut), lut_off=np.ascontiguousarray(lut_off), cols=cols,
@@ -95,6 +135,9 @@ class DeviceCatalog:
         d.key_strings = keep["blob"].ctypes.data_as(P(C.c_uint8))
         d.key_string_offsets = keep["soff"].ctypes.data_as(P(C.c_int64))
         d.key_string_base = keep["sbase"].ctypes.data_as(P(C.c_int32))
+        if self.tuple_codes is not None:
+            d.n_columns = 1
+            d.n_key_pieces = len(soff) - 1
         return d, keep
 
 

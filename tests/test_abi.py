@@ -27,4 +27,4 @@ def test_library_loads_and_exports_all_symbols():
     h = _lib.load_library()
     for name in _declared():
         assert hasattr(h, name), name
-    assert h.mx_abi_version() == 1
+    assert h.mx_abi_version() == 2

@@ -10,37 +10,58 @@ from conftest import STAGE12_CASES, golden_predicates, load_golden, spec_from_js
 pytestmark = pytest.mark.gpu
 
 
-def _index(case):
+def tuple_catalog(cc):
+    """The same catalog in the row-tuple layout (one int32 tuple-code column)."""
+    import numpy as np
+    import torch
+
+    from paper_2502_19790_b200 import DeviceCatalog
+    from paper_2502_19790_b200.catalog import encode_row_tuples
+
+    props = sorted(cc.vocab)
+    codes, table = encode_row_tuples([cc.columns[p] for p in props], [len(cc.vocab[p]) for p in props])
+    assert np.array_equal(table[codes].T, np.stack([cc.columns[p] for p in props]))
+    return DeviceCatalog(cc, tuples=(torch.from_numpy(codes).cuda(), table))
+
+
+def _index(case, layout="columns"):
     from paper_2502_19790_b200 import DeviceCatalog, build_index_from_catalog
 
     cc, g = load_golden(case)
-    idx = build_index_from_catalog(DeviceCatalog(cc), golden_predicates(g))
+    dcat = DeviceCatalog(cc) if layout == "columns" else tuple_catalog(cc)
+    idx = build_index_from_catalog(dcat, golden_predicates(g))
     return idx, g
 
 
+LAYOUTS = ["columns", "tuples"]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("case", STAGE12_CASES)
-def test_index_matches_reference(case):
-    idx, g = _index(case)
+def test_index_matches_reference(case, layout):
+    idx, g = _index(case, layout)
     assert [list(r) for r in idx.table()] == g["index"]
     assert idx.n_intervals == len(g["index"])
 
 
+@pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("case", STAGE12_CASES)
-def test_cursors_and_component_order_match_reference(case):
+def test_cursors_and_component_order_match_reference(case, layout):
     from paper_2502_19790_b200 import ChunkGenerator
 
-    idx, g = _index(case)
+    idx, g = _index(case, layout)
     gen = ChunkGenerator(idx, g["job_seed"])
     assert [k.canonical_string() for k in gen._component_order] == g["component_order"]
     for k in idx.component_keys():
         assert [list(r) for r in gen.cursor_ranges(k)] == g["cursors"][k.canonical_string()]
 
 
+@pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("case", STAGE12_CASES)
-def test_chunk_sequences_match_reference(case):
+def test_chunk_sequences_match_reference(case, layout):
     from paper_2502_19790_b200 import ChunkGenerator
 
-    idx, g = _index(case)
+    idx, g = _index(case, layout)
     for name, run in g["runs"].items():
         gen = ChunkGenerator(idx, g["job_seed"])
         got, states = [], {}
@@ -176,3 +197,20 @@ def test_concurrent_jobs_on_two_streams():
     for key in ("a", "b"):
         for f in want[key]:
             assert (got[key][f] == want[key][f]).all(), (key, f)
+
+
+def test_device_tuple_encoding_matches_host():
+    """encode_row_tuples_device == encode_row_tuples (codes and table)."""
+    import numpy as np
+    import torch
+
+    from paper_2502_19790_b200 import DeviceCatalog
+    from paper_2502_19790_b200.catalog import encode_row_tuples
+
+    cc, _ = load_golden("filters_nulls")
+    props = sorted(cc.vocab)
+    cards = [len(cc.vocab[p]) for p in props]
+    hc, ht = encode_row_tuples([cc.columns[p] for p in props], cards)
+    dc, dt = DeviceCatalog.encode_row_tuples_device(
+        {p: torch.from_numpy(cc.columns[p]).cuda() for p in props}, cards)
+    assert np.array_equal(dc.cpu().numpy(), hc) and np.array_equal(dt, ht)

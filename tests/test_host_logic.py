@@ -184,3 +184,31 @@ def test_synth_is_deterministic_and_covers_every_sample():
     assert a.run_lengths().sum() == 50_000 and a.file_sizes.sum() == 50_000
     fs = np.concatenate(([0], np.cumsum(a.file_sizes)[:-1]))
     assert np.isin(fs, a.run_starts).all()  # runs are cut at every file start
+
+
+@pytest.mark.parametrize("case", ["filters_nulls", "multi_tags", "cfg5_small"])
+def test_row_tuple_lut_equals_per_property_status(case):
+    """Row-tuple layout: the folded LUT gives every row the status (packed key,
+    fail bit) the per-property scan computes from its codes."""
+    from conftest import golden_predicates, load_golden
+    from paper_2502_19790_b200.catalog import encode_row_tuples
+    from paper_2502_19790_b200.codec import FAIL
+
+    cc, g = load_golden(case)
+    props = sorted(cc.vocab)
+    nullable = {p: bool((cc.columns[p] < 0).any()) for p in props}
+    codec = KeyCodec.build(cc.vocab, nullable)
+    preds = cc.validated(golden_predicates(g))
+    lut, off = codec.luts(cc, preds)
+    key = np.zeros(cc.n_samples, np.uint64)
+    fail = np.zeros(cc.n_samples, bool)
+    for j, p in enumerate(props):
+        e = lut[off[j] + cc.columns[p] + 1]
+        key += (e & ~FAIL).astype(np.uint64)
+        fail |= (e & FAIL) != 0
+    want = key.astype(np.uint32) | np.where(fail, FAIL, np.uint32(0)).astype(np.uint32)
+    codes, table = encode_row_tuples([cc.columns[p] for p in props], [len(cc.vocab[p]) for p in props])
+    assert np.array_equal(table[codes].T, np.stack([cc.columns[p] for p in props]))
+    tl, toff = codec.tuple_luts(cc, preds, table)
+    assert list(toff) == [0, len(table) + 1]
+    assert np.array_equal(tl[codes + 1], want)
