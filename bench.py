@@ -7,7 +7,7 @@ Workload (BASELINE.json configs[1], SURVEY.md §8d cfg 2): 100M samples in
 keys), run layout R=64, static multi-property best-effort mixture, chunk 1024,
 job seed 42. Synthetic metadata (seeded run table expanded on the device).
 Catalog layout (--layout): "tuples" (default) dictionary-encodes the rows once
-at registration into ONE int32 row-tuple code column (400 MB); "columns" keeps
+at registration into ONE u16 row-tuple code column (200 MB); "columns" keeps
 one int32 column per property (2 GB). Both exceed the 126 MB L2, so no L2
 flush is needed between steps.
 
@@ -58,7 +58,7 @@ CFG = dict(workload="cfg2: 100M samples, 10k files, 5 props (4,5,5,4,5) -> 2000 
            n_samples=100_000_000, n_files=10_000, props=5, run_mean=64, chunk_size=1024, job_seed=42,
            l2="inputs (2 GB of columns) exceed the 126 MB L2; no flush needed")
 LAYOUT_NOTE = {
-    "tuples": "row tuples: one int32 code column (rows dictionary-encoded at registration) + per-query tuple LUT",
+    "tuples": "row tuples: one u16 code column (rows dictionary-encoded at registration, 2,000 tuples) + per-query tuple LUT",
     "columns": "one int32 code column per property + per-query per-property LUTs",
 }
 REF_SAMPLE = 2_000_000  # --impl reference: samples per step (bounded CPU slice, ~5 s through the reference)
@@ -311,6 +311,7 @@ def our_arm(args):
     meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
     cols, table = layout_columns(rt, device_columns(rt, device), args.layout)
     n_cols = len(cols)
+    code_bytes = next(iter(cols.values())).element_size()  # 2: u16 row-tuple codes
     spec = synth.cfg2_mixture(CFG["chunk_size"])
     shard = None
     if world > 1:  # rank r owns global files [r*F, (r+1)*F) of one W*F-file catalog
@@ -395,7 +396,7 @@ def our_arm(args):
     pinned = {p: c.cpu().pin_memory() for p, c in cols.items()}
     del cols, dcat
     torch.cuda.empty_cache()
-    h2d = sum(x.numel() * 4 for x in pinned.values())
+    h2d = sum(x.numel() * x.element_size() for x in pinned.values())
 
     def e2e_step():
         dcols = {p: x.to(device, non_blocking=True) for p, x in pinned.items()}
@@ -427,7 +428,7 @@ def our_arm(args):
     peak, peak_kind = peaks()
     scan_ms, scan_n = phases["scan_runs"]
     scan_avg = scan_ms / max(scan_n, 1)
-    scan_bytes = n * 4 * n_cols + 16 * n_iv
+    scan_bytes = n * code_bytes * n_cols + 16 * n_iv
     step_bytes = scan_bytes + 8 * n_blocks + 16 * n_keys + 16 * n_iv + 20 * n_ranges + 8 * n_chunks
     achieved = scan_bytes / (scan_avg * 1e-3) / 1e9
     traffic = None
@@ -440,7 +441,7 @@ def our_arm(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": dict(CFG, parallelism=f"file-sharded x{world}" if world > 1 else "single GPU",
                        layout=LAYOUT_NOTE[args.layout],
-                       l2=f"inputs ({n * 4 * n_cols / 1e9:.1f} GB of code columns) exceed the 126 MB L2; "
+                       l2=f"inputs ({n * code_bytes * n_cols / 1e9:.1f} GB of code columns) exceed the 126 MB L2; "
                           "no flush needed"),
         "chunks_per_s": n_chunks / (ms_max * 1e-3),
         "job": {"samples": n, "intervals": n_iv, "keys": n_keys, "blocks": n_blocks, "chunks": n_chunks,
@@ -449,12 +450,12 @@ def our_arm(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "scan_fast_kernel (the scan_runs phase: scan_fast + deferred-tile scan_list + tail scan_direct)",
                      "bytes_per_launch": scan_bytes, "peak_kind": peak_kind,
-                     "note": "algorithmic bytes = N*4*C code-column reads (C = 1 row-tuple column, or P per-property columns) + 16 B per interval record"},
+                     "note": "algorithmic bytes = N*b*C code-column reads (C = 1 row-tuple column of b = 2-byte codes, or P per-property int32 columns) + 16 B per interval record"},
         # the whole job against the same peak (B1 + B2 per step)
         "roofline_step": {
             "bytes": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
             "frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
-            "note": "B1 = N*4*C + 16*I + 8*B + 16*K, B2 = 16*I (intervals touched) + 20*ranges + 8*chunks; "
+            "note": "B1 = N*b*C + 16*I + 8*B + 16*K, B2 = 16*I (intervals touched) + 20*ranges + 8*chunks; "
                     "the gap to the scan's fraction is the latency-bound cursor / plan / emission work and "
                     "the host synchronisations between them"},
         "e2e": {"value": world * n / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,

@@ -92,6 +92,10 @@ typedef struct mx_catalog_desc {
    * cardinalities are then not derivable from lut_offsets). */
   int32_t n_columns;
   int32_t n_key_pieces;
+  /* bytes per code: 4 (int32, also when 0) or 2 (u16 codes; a row-tuple
+   * dictionary of <= 65,536 tuples). Columns must be 16-byte (int32) / 8-byte
+   * (u16) aligned for the vector-load path; others take the scalar path. */
+  int32_t column_bytes;
 } mx_catalog_desc;
 
 /* Fused filter + interval detection + index build

@@ -61,6 +61,7 @@ class CatalogDesc(C.Structure):
         ("key_string_base", P(i32)),
         ("n_columns", i32),
         ("n_key_pieces", i32),
+        ("column_bytes", i32),
     ]
 
 

@@ -294,3 +294,11 @@ def encode_row_tuples(columns: Sequence[np.ndarray], cards: Sequence[int]) -> tu
         raise ValueError("more than 2^31 distinct row tuples")
     return inv.astype(np.int32).reshape(n), row_tuple_table(u, cards)
 
+
+def narrow_codes(codes: np.ndarray, n_tuples: int) -> np.ndarray:
+    """u16 view of row-tuple codes when the dictionary has <= 65,536 tuples
+    (stored as int16 bits, ``column_bytes`` 2 at the C-ABI), else unchanged."""
+    if n_tuples > 1 << 16:
+        return codes
+    return np.asarray(codes).astype(np.uint16).view(np.int16)
+

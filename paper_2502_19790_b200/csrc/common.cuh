@@ -27,6 +27,13 @@ __device__ __forceinline__ int4 ld_stream_v4(const int4* p) {
   return r;
 }
 
+// four consecutive u16 codes (8-byte aligned) widened to an int4
+__device__ __forceinline__ int4 ld_stream_u16x4(const void* p) {
+  u32 lo, hi;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "l"(p));
+  return make_int4((int)(lo & 0xffffu), (int)(lo >> 16), (int)(hi & 0xffffu), (int)(hi >> 16));
+}
+
 __device__ __forceinline__ int ld_stream(const int* p) {
   int r;
   asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));

@@ -251,7 +251,7 @@ __device__ __forceinline__ void direct_tile(const S1Args& a, const TileMeta* __r
     for (int p = 0; p < PMAX; ++p)
 #pragma unroll
       for (int j = 0; j < SEGS; ++j)
-        v[p][j] = ld_stream_v4(reinterpret_cast<const int4*>(a.cols[p] + wbase + 128 * j + 4 * lane));
+        v[p][j] = codes4(a, p, wbase + 128 * j + 4 * lane);
   }
   // 2. LUT to shared memory + tile metadata (overlaps the loads in flight).
   //    With PC > 0 the LUT carries the filter-fail flag as a COUNT above the
@@ -291,12 +291,11 @@ __device__ __forceinline__ void direct_tile(const S1Args& a, const TileMeta* __r
   } else {
     for (int p = 0; p < P; ++p) {
       const int lo = a.lut_off[p] + 1;
-      const int32_t* col = a.cols[p];
 #pragma unroll
       for (int j = 0; j < SEGS; ++j) {
         const long long i = wbase + 128 * j + 4 * lane;
         if (i + 4 <= a.n) {
-          const int4 x = ld_stream_v4(reinterpret_cast<const int4*>(col + i));
+          const int4 x = codes4(a, p, i);
           add(j, 0, lut_get<SMEM_LUT>(s_lut, a.lut, lo + x.x));
           add(j, 1, lut_get<SMEM_LUT>(s_lut, a.lut, lo + x.y));
           add(j, 2, lut_get<SMEM_LUT>(s_lut, a.lut, lo + x.z));
@@ -304,7 +303,7 @@ __device__ __forceinline__ void direct_tile(const S1Args& a, const TileMeta* __r
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (i + q < a.n) add(j, q, lut_get<SMEM_LUT>(s_lut, a.lut, lo + col[i + q]));
+            if (i + q < a.n) add(j, q, lut_get<SMEM_LUT>(s_lut, a.lut, lo + code_at(a, p, i + q)));
         }
       }
     }
@@ -515,9 +514,8 @@ scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
   int4 v[PC][SEGS];
 #pragma unroll
   for (int p = 0; p < PC; ++p) {
-    const int32_t* col = a.cols[p] + t0 + lw;
 #pragma unroll
-    for (int j = 0; j < SEGS; ++j) v[p][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + 128 * j));
+    for (int j = 0; j < SEGS; ++j) v[p][j] = codes4(a, p, t0 + lw + 128 * j);
   }
   if (!GLUT)
     for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
@@ -547,12 +545,11 @@ scan_fast1_kernel(S1Args a, const TileMeta* __restrict__ meta, long long nfull) 
   __shared__ int s_fs[FAST_MAX_FS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lw = warp * 128 * SEGS + 4 * lane;
-  const int32_t* col = a.cols[0] + lw;
   int4 v[1][SEGS];
   long long tile = blockIdx.x;
   if (tile < nfull) {
 #pragma unroll
-    for (int j = 0; j < SEGS; ++j) v[0][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + tile * TILE + 128 * j));
+    for (int j = 0; j < SEGS; ++j) v[0][j] = codes4(a, 0, tile * TILE + lw + 128 * j);
   }
   if (!GLUT)
     for (int i = tid; i < a.lut_off[1]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
@@ -565,7 +562,7 @@ scan_fast1_kernel(S1Args a, const TileMeta* __restrict__ meta, long long nfull) 
     const long long nxt = tile + gridDim.x;
     if (nxt < nfull) {
 #pragma unroll
-      for (int j = 0; j < SEGS; ++j) v[0][j] = ld_stream_v4(reinterpret_cast<const int4*>(col + nxt * TILE + 128 * j));
+      for (int j = 0; j < SEGS; ++j) v[0][j] = codes4(a, 0, nxt * TILE + lw + 128 * j);
     }
     if (m.nf > FAST_MAX_FS) {  // CTA-uniform: many tiny files, deferred to scan_list_kernel
       if (tid == 0) a.defer_list[atomicAdd(a.defer_cnt, 1u)] = (u32)tile;

@@ -40,7 +40,8 @@ constexpr int S1_FILE_CAP = 512;                // file starts cached per tile
 constexpr u32 FAIL = 0x80000000u;
 
 struct S1Args {
-  const int32_t* cols[MX_MAX_PROPS];
+  const int32_t* cols[MX_MAX_PROPS];  // int32 codes, or u16 codes when u16 (row-tuple layout)
+  int u16;
   int lut_off[MX_MAX_PROPS + 1];
   int n_props;
   const u32* lut;  // device copy of the concatenated LUT
@@ -70,6 +71,15 @@ __device__ __forceinline__ u32 lut_get(const u32* s_lut, const u32* g_lut, int i
   return SMEM_LUT ? s_lut[idx] : __ldg(g_lut + idx);
 }
 
+// code of sample i in column p / four consecutive codes (i % 4 == 0)
+__device__ __forceinline__ int code_at(const S1Args& a, int p, long long i) {
+  return a.u16 ? (int)reinterpret_cast<const uint16_t*>(a.cols[p])[i] : a.cols[p][i];
+}
+__device__ __forceinline__ int4 codes4(const S1Args& a, int p, long long i) {
+  return a.u16 ? ld_stream_u16x4(reinterpret_cast<const uint16_t*>(a.cols[p]) + i)
+               : ld_stream_v4(reinterpret_cast<const int4*>(a.cols[p] + i));
+}
+
 // Status word of one sample: packed key, bit 31 set when it fails the filter
 // or lies outside [0, n).
 template <bool SMEM_LUT>
@@ -77,7 +87,7 @@ __device__ u32 sample_status(const S1Args& a, const u32* s_lut, long long i) {
   if (i < 0 || i >= a.n) return FAIL;
   u32 key = 0, any = 0;
   for (int p = 0; p < a.n_props; ++p) {
-    int c = a.cols[p][i];
+    int c = code_at(a, p, i);
     u32 e = lut_get<SMEM_LUT>(s_lut, a.lut, a.lut_off[p] + c + 1);
     key += e & ~FAIL;
     any |= e;
@@ -154,13 +164,12 @@ scan_runs_kernel(S1Args a) {
     for (int q = 0; q < 4; ++q) anyf[j][q] = 0;
   const bool full = wbase + S1_WARP <= a.n;
   for (int p = 0; p < a.n_props; ++p) {
-    const int32_t* col = a.cols[p];
     const int lo = a.lut_off[p] + 1;
     if (full) {
       int4 v[S1_SEGS];
 #pragma unroll
       for (int j = 0; j < S1_SEGS; ++j)
-        v[j] = ld_stream_v4(reinterpret_cast<const int4*>(col + wbase + 128 * j + 4 * lane));
+        v[j] = codes4(a, p, wbase + 128 * j + 4 * lane);
 #pragma unroll
       for (int j = 0; j < S1_SEGS; ++j) {
         u32 e0 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v[j].x);
@@ -179,7 +188,7 @@ scan_runs_kernel(S1Args a) {
         for (int q = 0; q < 4; ++q) {
           long long i = wbase + 128 * j + 4 * lane + q;
           if (i < a.n) {
-            u32 e = lut_get<SMEM_LUT>(s_lut, a.lut, lo + col[i]);
+            u32 e = lut_get<SMEM_LUT>(s_lut, a.lut, lo + code_at(a, p, i));
             st[j][q] += e & ~FAIL;
             anyf[j][q] |= e;
           }
@@ -491,7 +500,7 @@ template <int PC, int SEGS>
 static void launch_fast(const S1Args& a, const TileMeta* m, long long nfull, int lut_total, cudaStream_t s) {
   if (nfull <= 0) return;
   const char* env = getenv("MX_SCAN");
-  if (SEGS == 4 && env && !strcmp(env, "fastpipe")) {  // persistent + TMA ring variant
+  if (SEGS == 4 && env && !strcmp(env, "fastpipe") && !a.u16) {  // persistent + TMA ring variant
     int dev = 0, n_sm = 148, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -586,6 +595,9 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   const long long n = d->n_samples;
   S1Args a{};
   a.n_props = NC;
+  if (d->column_bytes != 0 && d->column_bytes != 2 && d->column_bytes != 4)
+    return mx_fail(MX_ERR_UNSUPPORTED, "column_bytes=%d (2 or 4)", d->column_bytes);
+  a.u16 = d->column_bytes == 2;
   for (int p = 0; p < NC; ++p) a.cols[p] = d->columns[p];
   for (int p = 0; p <= NC; ++p) a.lut_off[p] = d->lut_offsets[p];
   const int lut_total = d->lut_offsets[NC];
@@ -627,7 +639,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   const bool smem_lut = lut_total <= MX_SMEM_LUT_MAX;
   const char* scan_env = getenv("MX_SCAN");
   const bool use_v1 = scan_env && !strcmp(scan_env, "v1");
-  const bool use_pipe = scan_env && (!strcmp(scan_env, "pipe") || !strcmp(scan_env, "tma")) && smem_lut;
+  const bool use_pipe = scan_env && (!strcmp(scan_env, "pipe") || !strcmp(scan_env, "tma")) && smem_lut && !a.u16;
   const bool slot_mode = !use_v1;
   int dev = 0, n_sm = 148, smem_optin = 0;
   MX_CUDA_TRY(cudaGetDevice(&dev));
@@ -658,7 +670,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   const int tile_len = use_v1 ? S1_TILE : (use_pipe ? 1024 * pipe_segs : 1024 * direct_segs);
   const int ntiles = (int)((n + tile_len - 1) / tile_len);
   bool aligned = true;
-  for (int p = 0; p < P; ++p) aligned &= (reinterpret_cast<uintptr_t>(d->columns[p]) % 16) == 0;
+  for (int p = 0; p < P; ++p) aligned &= (reinterpret_cast<uintptr_t>(d->columns[p]) % (a.u16 ? 8 : 16)) == 0;
   const long long nstaged = aligned ? n / tile_len : 0;
   DevBuf<TileMeta> tmeta;
   DevBuf<u32> rk, rf, rs, re;

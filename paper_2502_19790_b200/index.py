@@ -38,6 +38,8 @@ class DeviceCatalog:
         self.tuple_codes = self.tuple_table = None
         if tuples is not None:
             codes, table = tuples
+            if codes.dtype not in (torch.int32, torch.int16):
+                raise ValueError("tuple codes must be int32, or int16 holding u16 codes")
             self.tuple_codes = codes.contiguous()
             self.tuple_table = np.ascontiguousarray(table, dtype=np.int32)
             if self.tuple_table.ndim != 2 or self.tuple_table.shape[1] != len(props):
@@ -62,10 +64,11 @@ class DeviceCatalog:
         self._strings = self.codec.key_strings()
 
     @staticmethod
-    def encode_row_tuples_device(columns: dict, cards) -> tuple:
+    def encode_row_tuples_device(columns: dict, cards, narrow: bool = True) -> tuple:
         """Device twin of ``catalog.encode_row_tuples`` for HBM-resident
-        columns ({prop: int32 tensor}, property-name order): (int32 codes in
-        HBM, int32[T, P] host tuple table)."""
+        columns ({prop: int32 tensor}, property-name order): (codes in HBM,
+        int32[T, P] host tuple table). With ``narrow`` and <= 65,536 tuples
+        the codes are u16 (stored as int16: half the bytes to scan / upload)."""
         import torch
 
         from .catalog import _tuple_radix, row_tuple_table
@@ -80,7 +83,10 @@ class DeviceCatalog:
         del r
         if u.numel() >= 1 << 31:
             raise ValueError("more than 2^31 distinct row tuples")
-        return inv.to(torch.int32), row_tuple_table(u.cpu().numpy(), cards)
+        table = row_tuple_table(u.cpu().numpy(), cards)
+        if narrow and u.numel() <= 1 << 16:
+            return torch.where(inv >= 1 << 15, inv - (1 << 16), inv).to(torch.int16), table
+        return inv.to(torch.int32), table
 
     @staticmethod
     def from_reference(cat, device=None) -> "DeviceCatalog":
@@ -138,6 +144,7 @@ class DeviceCatalog:
         if self.tuple_codes is not None:
             d.n_columns = 1
             d.n_key_pieces = len(soff) - 1
+            d.column_bytes = self.tuple_codes.element_size()
         return d, keep
 
 

@@ -10,17 +10,21 @@ from conftest import STAGE12_CASES, golden_predicates, load_golden, spec_from_js
 pytestmark = pytest.mark.gpu
 
 
-def tuple_catalog(cc):
-    """The same catalog in the row-tuple layout (one int32 tuple-code column)."""
+def tuple_catalog(cc, narrow=False):
+    """The same catalog in the row-tuple layout (one tuple-code column: int32,
+    or u16 with `narrow`)."""
     import numpy as np
     import torch
 
     from paper_2502_19790_b200 import DeviceCatalog
-    from paper_2502_19790_b200.catalog import encode_row_tuples
+    from paper_2502_19790_b200.catalog import encode_row_tuples, narrow_codes
 
     props = sorted(cc.vocab)
     codes, table = encode_row_tuples([cc.columns[p] for p in props], [len(cc.vocab[p]) for p in props])
     assert np.array_equal(table[codes].T, np.stack([cc.columns[p] for p in props]))
+    if narrow:
+        codes = narrow_codes(codes, len(table))
+        assert codes.dtype == np.int16
     return DeviceCatalog(cc, tuples=(torch.from_numpy(codes).cuda(), table))
 
 
@@ -28,12 +32,12 @@ def _index(case, layout="columns"):
     from paper_2502_19790_b200 import DeviceCatalog, build_index_from_catalog
 
     cc, g = load_golden(case)
-    dcat = DeviceCatalog(cc) if layout == "columns" else tuple_catalog(cc)
+    dcat = DeviceCatalog(cc) if layout == "columns" else tuple_catalog(cc, narrow=layout == "tuples16")
     idx = build_index_from_catalog(dcat, golden_predicates(g))
     return idx, g
 
 
-LAYOUTS = ["columns", "tuples"]
+LAYOUTS = ["columns", "tuples", "tuples16"]
 
 
 @pytest.mark.parametrize("layout", LAYOUTS)
@@ -214,3 +218,36 @@ def test_device_tuple_encoding_matches_host():
     dc, dt = DeviceCatalog.encode_row_tuples_device(
         {p: torch.from_numpy(cc.columns[p]).cuda() for p in props}, cards)
     assert np.array_equal(dc.cpu().numpy(), hc) and np.array_equal(dt, ht)
+
+
+@pytest.mark.parametrize("n_files", [1, 37])
+def test_u16_tuple_codes_above_32767_match_columns(n_files):
+    """> 32,768 distinct row tuples (u16 codes with the top bit set) index
+    exactly like the per-property layout, across file boundaries."""
+    import numpy as np
+    import torch
+
+    from paper_2502_19790_b200 import DeviceCatalog, build_index_from_catalog
+    from paper_2502_19790_b200.catalog import ColumnarCatalog
+
+    rng = np.random.default_rng(7)
+    n = 300_001
+    vocab = {"a": [f"a{i}" for i in range(50)], "b": [f"b{i}" for i in range(50)], "c": [f"c{i}" for i in range(30)]}
+    # runs of random length so intervals are not all length 1
+    lens = rng.integers(1, 8, size=n)
+    cols = {p: np.repeat(rng.integers(0, len(v), size=n), lens)[:n].astype(np.int32) for p, v in vocab.items()}
+    cuts = np.sort(rng.choice(np.arange(1, n), size=n_files - 1, replace=False)) if n_files > 1 else np.array([], int)
+    offs = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    cc = ColumnarCatalog.from_arrays(cols, vocab, np.diff(offs))
+    want = build_index_from_catalog(DeviceCatalog(cc), [])
+    dcat16 = tuple_catalog(cc, narrow=True)
+    assert len(dcat16.tuple_table) > 1 << 15
+    got = build_index_from_catalog(dcat16, [])
+    for k in ("key", "ds", "fid", "start", "end"):
+        assert np.array_equal(got.interval_table()[k], want.interval_table()[k]), k
+    assert np.array_equal(got.packed_keys()[0], want.packed_keys()[0])
+    # device encoder narrows the same way
+    dc, dt = DeviceCatalog.encode_row_tuples_device({p: torch.from_numpy(c).cuda() for p, c in cols.items()},
+                                                    [len(vocab[p]) for p in sorted(vocab)])
+    assert dc.dtype == torch.int16 and np.array_equal(dt, dcat16.tuple_table)
+    assert np.array_equal(dc.cpu().numpy(), dcat16.tuple_codes.cpu().numpy())
