@@ -431,10 +431,15 @@ def our_arm(args):
     scan_bytes = n * code_bytes * n_cols + 16 * n_iv
     step_bytes = scan_bytes + 8 * n_blocks + 16 * n_keys + 16 * n_iv + 20 * n_ranges + 8 * n_chunks
     achieved = scan_bytes / (scan_avg * 1e-3) / 1e9
-    traffic = None
+    b_per_sample = code_bytes * n_cols
+    traffic, prof = None, {}
     tf = ROOT / "profiles" / "scan_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+        prof = json.loads(tf.read_text()).get(args.layout, {})
+        traffic = prof.get("bytes_per_launch")
+    # the u16 single-column scan is instruction-issue bound (ncu issue-active),
+    # not HBM bound: say so next to its HBM fraction
+    issue = prof.get("issue_active_pct")
     line = {
         "metric": METRIC, "value": world * n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -450,7 +455,10 @@ def our_arm(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "scan_fast_kernel (the scan_runs phase: scan_fast + deferred-tile scan_list + tail scan_direct)",
                      "bytes_per_launch": scan_bytes, "peak_kind": peak_kind,
-                     "note": "algorithmic bytes = N*b*C code-column reads (C = 1 row-tuple column of b = 2-byte codes, or P per-property int32 columns) + 16 B per interval record"},
+                     "note": "algorithmic bytes = N*b*C code-column reads (C = 1 row-tuple column of b = 2-byte codes, or P per-property int32 columns) + 16 B per interval record"
+                             + (f"; at {b_per_sample} B/sample this kernel is instruction-issue bound "
+                                f"(ncu: {issue:.0f}% issue-active, {prof.get('inst_executed', 0) / n:.2f} warp "
+                                f"instructions per sample), not HBM bound" if issue and code_bytes * n_cols <= 2 else "")},
         # the whole job against the same peak (B1 + B2 per step)
         "roofline_step": {
             "bytes": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",

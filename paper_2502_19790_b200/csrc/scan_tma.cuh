@@ -384,23 +384,21 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
       for (int k = 0; k < FAST_MAX_FS; ++k) {
         const int d = fs[k] - li0;  // file start k relative to this thread's first sample
         if (d >= 0 && d <= 4) fsb |= 1u << d;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) sel += (u32)(d <= q) << (3 * q);  // files started at or before sample q
+        // +1 in the 3-bit field of every sample q >= d (files started at or before q)
+        const int dc = min(max(d, 0), 4);
+        sel += 0x249u & (0xfffu << (3 * dc));
       }
     }
     fsel[j] = sel;
-    u32 sm = 0, em = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const u32 cur = st[j][q];
-      const u32 prv = q == 0 ? prev_last : st[j][q - 1];
-      const u32 nxt = q == 3 ? next_first : st[j][q + 1];
-      const bool pass = cur < lim;
-      sm |= (u32)(pass && (((fsb >> q) & 1) || prv != cur)) << q;
-      em |= (u32)(pass && (((fsb >> (q + 1)) & 1) || nxt != cur)) << q;
-    }
-    starts[j] = sm;
-    ends[j] = em;
+    // boundary bits: bit q = sample q starts a new run candidate (file start or
+    // key change vs its predecessor), bit 4 = the next thread's first sample does
+    const u32 bnd = fsb | (u32)(prev_last != st[j][0]) | ((u32)(st[j][0] != st[j][1]) << 1) |
+                    ((u32)(st[j][1] != st[j][2]) << 2) | ((u32)(st[j][2] != st[j][3]) << 3) |
+                    ((u32)(st[j][3] != next_first) << 4);
+    const u32 pm = (u32)(st[j][0] < lim) | ((u32)(st[j][1] < lim) << 1) | ((u32)(st[j][2] < lim) << 2) |
+                   ((u32)(st[j][3] < lim) << 3);
+    starts[j] = pm & bnd;
+    ends[j] = pm & (bnd >> 1);
   }
   // tile-local compaction (same slot layout as finish_tile)
   u32 pack = 0;
@@ -442,22 +440,23 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
   const u32 wb = sc.warp_tot[warp];
 #pragma unroll
   for (int j = 0; j < SEGS; ++j) {
-    if (!(starts[j] | ends[j])) continue;
     u32 run = wb + seg_base[j];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    // visit only this segment's events, in sample order (start before end)
+    for (u32 ev = starts[j] | ends[j]; ev; ev &= ev - 1) {
+      const int q = __ffs(ev) - 1;
       const u32 li = (u32)(lw + 128 * j + q);
       const u32 fo = (fsel[j] >> (3 * q)) & 7;  // file = m.fa + fo
+      const u32 off = li + s_off[fo];
       if ((starts[j] >> q) & 1) {
-        const u32 key = st[j][q];
+        const u32 key = q == 0 ? st[j][0] : q == 1 ? st[j][1] : q == 2 ? st[j][2] : st[j][3];
         rk[run] = key;
         rf[run] = (u32)m.fa + fo;
-        rs[run] = li + s_off[fo];
+        rs[run] = off;
         if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)(t0 + li));
         ++run;
       }
       if ((ends[j] >> q) & 1) {
-        if (run > 0) re[run - 1] = li + 1 + s_off[fo];
+        if (run > 0) re[run - 1] = off + 1;
         else a.tile_head[tile] = t0 + li + 1;
       }
     }
