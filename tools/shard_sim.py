@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--world", type=int, default=8)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--ranks", default="0", help="comma list of ranks to time (all are run)")
+    ap.add_argument("--layout", default="tuples", choices=["tuples", "columns"])
     ap.add_argument("--trace", action="store_true", help="CUPTI kernel summary of rank 0's hybrid+gen+plan")
     args = ap.parse_args()
     W = args.world
@@ -55,15 +56,18 @@ def main():
     for q in range(W):
         rt = bench.make_workload(q, args.scale)
         meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
-        cols = bench.device_columns(rt, dev)
-        dcat = DeviceCatalog(meta, columns=cols, nullable={p: False for p in cols})
+        cols, table = bench.layout_columns(rt, bench.device_columns(rt, dev), args.layout)
+        dcat = bench.device_catalog(meta, cols, table)
         idx, ms, _ = timed(lambda: build_index_from_catalog(dcat, []))
         nf = len(rt.file_sizes)
         rows = torch.empty((max(idx.n_blocks, 1), 4), dtype=torch.int32, device=dev)
         _lib.check(L.mx_index_block_table(idx.handle, q * nf, rows.data_ptr(), C.c_void_p(_lib.stream_ptr())))
         packed = np.zeros(idx.n_keys, np.uint32)
         _lib.check(L.mx_index_packed_keys(idx.handle, _lib.ptr(packed)))
-        dcat.columns = {p: c[:0] for p, c in dcat.columns.items()}  # free the 2 GB of columns
+        if dcat.columns is not None:  # free the code columns
+            dcat.columns = {p: c[:0] for p, c in dcat.columns.items()}
+        else:
+            dcat.tuple_codes = dcat.tuple_codes[:0]
         del cols
         locs.append(dict(idx=idx, dcat=dcat, rows=rows[: idx.n_blocks], packed=packed, nf=nf, stage1_ms=ms))
         torch.cuda.empty_cache()
@@ -75,7 +79,7 @@ def main():
     gkeys = np.unique(np.concatenate([x["packed"] for x in locs])).astype(np.uint32)
     nf = locs[0]["nf"]
     file_ds, file_ids = np.zeros(W * nf, np.int32), np.arange(1, W * nf + 1, dtype=np.int64)
-    report = {"world": W, "samples_per_rank": int(locs[0]["idx"].n_samples), "block_rows": counts,
+    report = {"world": W, "layout": args.layout, "samples_per_rank": int(locs[0]["idx"].n_samples), "block_rows": counts,
               "table_allgather_bytes": int(W * cap * 16), "stage1_ms": [round(x["stage1_ms"], 3) for x in locs]}
     timed_ranks = {int(r) for r in args.ranks.split(",")}
     results = []
