@@ -64,6 +64,47 @@ struct PinnedRing {
 thread_local PinnedRing g_ring;
 }  // namespace
 
+namespace {
+struct PinnedReadback {
+  static constexpr size_t kCap = 256u << 10;
+  char* buf = nullptr;
+  bool failed = false;
+  ~PinnedReadback() {
+    if (buf) cudaFreeHost(buf);
+  }
+};
+thread_local PinnedReadback g_rb;
+}  // namespace
+
+cudaError_t D2HBatch::add(void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  PinnedReadback& r = g_rb;
+  if (!r.buf && !r.failed) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&r.buf), PinnedReadback::kCap, cudaHostAllocDefault) != cudaSuccess) {
+      r.buf = nullptr;
+      r.failed = true;
+      cudaGetLastError();
+    }
+  }
+  const size_t need = (bytes + 15) & ~size_t(15);
+  if (!r.buf || n == 16 || used + need > PinnedReadback::kCap)
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaMemcpyAsync(r.buf + used, src, bytes, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return e;
+  items[n++] = Item{dst, used, bytes};
+  used += need;
+  return cudaSuccess;
+}
+
+cudaError_t D2HBatch::sync() {
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  for (int i = 0; i < n; ++i) memcpy(items[i].dst, g_rb.buf + items[i].off, items[i].bytes);
+  n = 0;
+  used = 0;
+  return cudaSuccess;
+}
+
 cudaError_t mx_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return cudaSuccess;
   PinnedRing& r = g_ring;

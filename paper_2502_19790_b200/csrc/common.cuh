@@ -125,6 +125,24 @@ int mx_fail(int code, const char* fmt, ...);
 // staging, without the implicit stream synchronisation of a pageable copy
 cudaError_t mx_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
+// Small device->host reads gathered into a per-thread pinned block and
+// delivered after ONE stream synchronisation: a cudaMemcpyAsync into
+// pageable memory blocks the host per call (~10 us round trip each).
+// Reads that do not fit are copied directly (pageable, still correct).
+struct D2HBatch {
+  struct Item {
+    void* dst;
+    size_t off, bytes;
+  };
+  cudaStream_t s;
+  Item items[16];
+  int n = 0;
+  size_t used = 0;
+  explicit D2HBatch(cudaStream_t st) : s(st) {}
+  cudaError_t add(void* dst, const void* src, size_t bytes);
+  cudaError_t sync();  // cudaStreamSynchronize + deliver every read
+};
+
 // Launch accounting and per-phase CUDA-event timing (capi.cu). A phase timer
 // records events on the launching stream when profiling is enabled
 // (mx_profile_enable); totals are read back with mx_profile_read.

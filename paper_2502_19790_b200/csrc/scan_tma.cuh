@@ -499,7 +499,7 @@ __device__ __forceinline__ void lut_sums(const u32* s_lut, const S1Args& a, cons
 // OCC: resident CTAs per SM the register budget is cut for. A single code
 // column (row-tuple layout) has 5x fewer bytes in flight per CTA than the
 // 5-property case, so it runs more CTAs per SM instead.
-template <int PC, int SEGS, bool GLUT = false, int OCC = (SEGS == 2 ? 4 : 2)>
+template <int PC, int SEGS, bool GLUT = false, int OCC = (SEGS == 2 || PC == 1 ? 4 : 2)>
 __global__ void __launch_bounds__(S1_THREADS, OCC)
 scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
   constexpr int TILE = S1_THREADS * 4 * SEGS;

@@ -744,9 +744,12 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   }
   u64 h_runs = 0;
   DevError h_err;
-  MX_CUDA_TRY(cudaMemcpyAsync(&h_runs, scratch64.p, sizeof(u64), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(&h_err, err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  {
+    D2HBatch rb(s);
+    MX_CUDA_TRY(rb.add(&h_runs, scratch64.p, sizeof(u64)));
+    MX_CUDA_TRY(rb.add(&h_err, err.p, sizeof(DevError)));
+    MX_CUDA_TRY(rb.sync());
+  }
   if (h_err.null_key_sample != ~0ull) {
     const long long g = (long long)h_err.null_key_sample;
     std::vector<long long> off(d->n_files + 1);
@@ -912,11 +915,14 @@ int index_finalize(IndexData* ixp, long long I, cudaStream_t s) {
   MX_CUDA_TRY(cudaGetLastError());
   u64 tot = 0, samples = 0;
   u32 h_maxblk = 0;
-  MX_CUDA_TRY(cudaMemcpyAsync(&h_maxblk, maxblk.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(&tot, scratch64.p, sizeof(u64), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(&samples, ix.iv_cum.p + I, sizeof(u64), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(&h_err, err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  {
+    D2HBatch rb(s);
+    MX_CUDA_TRY(rb.add(&h_maxblk, maxblk.p, sizeof(u32)));
+    MX_CUDA_TRY(rb.add(&tot, scratch64.p, sizeof(u64)));
+    MX_CUDA_TRY(rb.add(&samples, ix.iv_cum.p + I, sizeof(u64)));
+    MX_CUDA_TRY(rb.add(&h_err, err.p, sizeof(DevError)));
+    MX_CUDA_TRY(rb.sync());
+  }
   if (h_err.overlap) return mx_fail(MX_ERR_INDEX, "empty or overlapping interval in index build");
   ix.n_keys = (long long)(tot >> 32);
   ix.n_blocks = (long long)(tot & 0xffffffffull);

@@ -1953,9 +1953,12 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(cudaGetLastError());
   u32 h_big = 0;
   long long total = 0;
-  MX_CUDA_TRY(cudaMemcpyAsync(&h_big, big.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(&total, g->res_off.p + n_chunks, sizeof(long long), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  {
+    D2HBatch rb(s);
+    MX_CUDA_TRY(rb.add(&h_big, big.p, sizeof(u32)));
+    MX_CUDA_TRY(rb.add(&total, g->res_off.p + n_chunks, sizeof(long long)));
+    MX_CUDA_TRY(rb.sync());
+  }
   if (h_big) return mx_fail(MX_ERR_UNSUPPORTED, "a chunk has %u ranges before merging (> %d supported)", h_big, NM_CAP);
   g->res_ranges = total;
   g->next_chunk_id += n_chunks;
@@ -2013,9 +2016,12 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
       mx_count_launch();
     }
     std::vector<u32> h_cnt(Km), h_hits(K > 0 ? K : 1, 0);
-    MX_CUDA_TRY(cudaMemcpyAsync(h_cnt.data(), L_cnt.p, sizeof(u32) * Km, cudaMemcpyDeviceToHost, s));
-    if (K > 0) MX_CUDA_TRY(cudaMemcpyAsync(h_hits.data(), hits.p, sizeof(u32) * K, cudaMemcpyDeviceToHost, s));
-    MX_CUDA_TRY(cudaStreamSynchronize(s));
+    {
+      D2HBatch rb(s);
+      MX_CUDA_TRY(rb.add(h_cnt.data(), L_cnt.p, sizeof(u32) * Km));
+      if (K > 0) MX_CUDA_TRY(rb.add(h_hits.data(), hits.p, sizeof(u32) * K));
+      MX_CUDA_TRY(rb.sync());
+    }
     g->match_off.assign(Km + 1, 0);
     for (int m = 0; m < Km; ++m) g->match_off[m + 1] = g->match_off[m] + h_cnt[m];
     g->match_shared = false;
@@ -2292,10 +2298,13 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   }
   long long h_out[4];
   std::vector<Phase> h_phases(cap_phases);
-  MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(g->report.data(), report.p, sizeof(long long) * Km, cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(h_phases.data(), phases.p, sizeof(Phase) * cap_phases, cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  {
+    D2HBatch rb(s);
+    MX_CUDA_TRY(rb.add(h_out, out.p, sizeof(h_out)));
+    MX_CUDA_TRY(rb.add(g->report.data(), report.p, sizeof(long long) * Km));
+    MX_CUDA_TRY(rb.add(h_phases.data(), phases.p, sizeof(Phase) * cap_phases));
+    MX_CUDA_TRY(rb.sync());
+  }
   ph_plan.reset();
   if (w.mode == 0) {
     commit_segments_kernel<<<Km, 128, 0, s>>>(Km, w.s_off, w.seg_comp, w.seg_lo, w.seg_pre, pos.p,
@@ -2344,9 +2353,12 @@ int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long 
   mx_count_launch();
   long long h_out[4];
   Phase h_phases[2];
-  MX_CUDA_TRY(cudaMemcpyAsync(h_out, out.p, sizeof(h_out), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaMemcpyAsync(h_phases, phases.p, sizeof(h_phases), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  {
+    D2HBatch rb(s);
+    MX_CUDA_TRY(rb.add(h_out, out.p, sizeof(h_out)));
+    MX_CUDA_TRY(rb.add(h_phases, phases.p, sizeof(h_phases)));
+    MX_CUDA_TRY(rb.sync());
+  }
   commit_segments_kernel<<<1, 128, 0, s>>>(1, w.s_off, w.seg_comp, w.seg_lo, w.seg_pre, pos.p, g->consumed.p);
   mx_count_launch();
   int rc = emit(g, w, phases.p, h_phases, terms.p, h_out[0], h_out[1], K, s);

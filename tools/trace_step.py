@@ -27,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--out", default="gpurun_out/trace.json")
+    ap.add_argument("--layout", default="tuples", choices=["tuples", "columns"])
     ap.add_argument("--cprofile", action="store_true", help="host Python profile of 20 steps instead")
     ap.add_argument("--cfg1r1", action="store_true", help="trace the iid cfg1 job instead of cfg2")
     args = ap.parse_args()
@@ -39,9 +40,9 @@ def main():
     else:
         rt = bench.make_workload(0, args.scale)
         meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
-        cols = bench.device_columns(rt, dev)
+        cols, table = bench.layout_columns(rt, bench.device_columns(rt, dev), args.layout)
         spec = synth.cfg2_mixture(bench.CFG["chunk_size"])
-        dcat = bench.device_catalog(meta, cols)
+        dcat = bench.device_catalog(meta, cols, table)
     for _ in range(3):
         bench.run_step(dcat, spec)
     torch.cuda.synchronize()
