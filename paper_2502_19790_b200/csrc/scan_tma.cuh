@@ -367,6 +367,10 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
 #pragma unroll
   for (int k = 0; k < FAST_MAX_FS; ++k) fs[k] = s_fs[k];  // local file starts in (0, TILE], padded
   u32 starts[SEGS], ends[SEGS], fsel[SEGS];  // fsel: 3 bits per sample = file offset in the tile
+  // A run that ends right before the next run starts (same file, both inside
+  // the tile) is closed by that START event (wend), so its end event is
+  // dropped (ekeep): most runs then cost one event instead of two.
+  u32 wend[SEGS], ekeep[SEGS];
 #pragma unroll
   for (int j = 0; j < SEGS; ++j) {
     u32 prev_last = __shfl_up_sync(MX_FULL, st[j][3], 1);
@@ -399,6 +403,13 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
                    ((u32)(st[j][3] < lim) << 3);
     starts[j] = pm & bnd;
     ends[j] = pm & (bnd >> 1);
+    const u32 ppm = ((pm << 1) | (u32)(prev_last < lim)) & 0xfu;  // predecessor passes
+    u32 w = starts[j] & ppm & ~fsb;
+    if (j == 0 && lane == 0 && warp == 0) w &= ~1u;  // the predecessor is in the previous tile
+    const bool tile_last = j == SEGS - 1 && lane == 31 && warp == S1_THREADS / 32 - 1;
+    const u32 n3 = (next_first < lim && !((fsb >> 4) & 1) && !tile_last) ? 8u : 0u;
+    wend[j] = w;
+    ekeep[j] = ends[j] & ~((w >> 1) | n3);
   }
   // tile-local compaction (same slot layout as finish_tile)
   u32 pack = 0;
@@ -442,12 +453,16 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
   for (int j = 0; j < SEGS; ++j) {
     u32 run = wb + seg_base[j];
     // visit only this segment's events, in sample order (start before end)
-    for (u32 ev = starts[j] | ends[j]; ev; ev &= ev - 1) {
+    for (u32 ev = starts[j] | ekeep[j]; ev; ev &= ev - 1) {
       const int q = __ffs(ev) - 1;
       const u32 li = (u32)(lw + 128 * j + q);
       const u32 fo = (fsel[j] >> (3 * q)) & 7;  // file = m.fa + fo
       const u32 off = li + s_off[fo];
       if ((starts[j] >> q) & 1) {
+        if ((wend[j] >> q) & 1) {  // close the run ending at li - 1 (same file)
+          if (run > 0) re[run - 1] = off;
+          else a.tile_head[tile] = t0 + li;
+        }
         const u32 key = q == 0 ? st[j][0] : q == 1 ? st[j][1] : q == 2 ? st[j][2] : st[j][3];
         rk[run] = key;
         rf[run] = (u32)m.fa + fo;
@@ -455,7 +470,7 @@ __device__ __forceinline__ void fast_tile(const S1Args& a, const TileMeta& m, lo
         if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)(t0 + li));
         ++run;
       }
-      if ((ends[j] >> q) & 1) {
+      if ((ekeep[j] >> q) & 1) {
         if (run > 0) re[run - 1] = off + 1;
         else a.tile_head[tile] = t0 + li + 1;
       }
