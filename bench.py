@@ -239,21 +239,28 @@ def _reference_catalog(cc):
     return cat
 
 
-def reference_run(n_samples: int):
-    """The reference's own job on a bounded slice of the workload:
-    filter_intervals -> build_index -> ChunkGenerator.generate until None
-    (server.py:112-163), single thread (GIL-bound, build_index workers=1)."""
-    from mixplane.chunks import ChunkGenerator as RGen
-    from mixplane.index import build_index as rbuild
+def reference_prepare(n_samples: int, seed: int = 2):
+    """A reference catalog over a bounded slice of the cfg2 layout (registration
+    is not timed) and the cfg2 mixture as a reference MixtureSpec."""
     from mixplane.mixtures import MixtureKey as RKey, MixtureSpec as RSpec
 
     from paper_2502_19790_b200 import synth
 
     f = max(1, n_samples // (CFG["n_samples"] // CFG["n_files"]))
-    cc = synth.expand_numpy(synth.make_runs(n_samples, f, synth.CFG2_PROPS, CFG["run_mean"], seed=2))
+    cc = synth.expand_numpy(synth.make_runs(n_samples, f, synth.CFG2_PROPS, CFG["run_mean"], seed=seed))
     cat = _reference_catalog(cc)
     spec = synth.cfg2_mixture(CFG["chunk_size"])
     rspec = RSpec({RKey.of({p: list(v) for p, v in k.entries}): w for k, w in spec.weights.items()}, spec.chunk_size)
+    return cat, rspec
+
+
+def reference_job(cat, rspec):
+    """The reference's own job: filter_intervals -> build_index ->
+    ChunkGenerator.generate until None (server.py:112-163), one thread
+    (GIL-bound, build_index workers=1)."""
+    from mixplane.chunks import ChunkGenerator as RGen
+    from mixplane.index import build_index as rbuild
+
     t0 = time.perf_counter()
     gen = RGen(rbuild(cat.filter_intervals([])), CFG["job_seed"])
     chunks = 0
@@ -262,30 +269,84 @@ def reference_run(n_samples: int):
     return time.perf_counter() - t0, chunks
 
 
+def reference_run(n_samples: int):
+    return reference_job(*reference_prepare(n_samples))
+
+
+def _ref_proc(wid, n_samples, rounds, barrier, q):
+    """One host process of the reference arm: its own slice (seed per worker),
+    every round started together with the other workers."""
+    _reference_pkg()
+    cat, rspec = reference_prepare(n_samples, seed=2 + wid)
+    for r in range(rounds):
+        barrier.wait()
+        dt, chunks = reference_job(cat, rspec)
+        q.put((wid, r, dt, chunks))
+
+
+def reference_parallel(n_samples: int, workers: int, warmup: int, steps: int):
+    """The reference on `workers` host processes at once (the reference is
+    pure Python and GIL-bound, so processes are how it uses the cores): each
+    process runs the job on its own n_samples slice; a step's time is the
+    slowest worker's. Returns (per-step max times, chunks per worker-job)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("fork")
+    barrier, q = ctx.Barrier(workers), ctx.Queue()
+    procs = [ctx.Process(target=_ref_proc, args=(w, n_samples, warmup + steps, barrier, q), daemon=True)
+             for w in range(workers)]
+    for pr in procs:
+        pr.start()
+    res = [q.get() for _ in range(workers * (warmup + steps))]
+    for pr in procs:
+        pr.join()
+    per_round = {}
+    for _, r, dt, ch in res:
+        per_round.setdefault(r, []).append((dt, ch))
+    times = [max(dt for dt, _ in per_round[r]) for r in range(warmup, warmup + steps)]
+    chunks = sum(ch for _, ch in per_round[warmup + steps - 1]) / workers
+    return times, chunks
+
+
+def host_workers() -> int:
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    cap = int(os.environ.get("MX_REF_WORKERS", "0") or 0)
+    return max(1, min(n, cap) if cap else min(n, 128))
+
+
 def reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
     real = _reference_pkg() is not None
-    run = reference_run if real else cpu_port
-    for _ in range(args.warmup):
-        run(REF_SAMPLE)
-    times, chunks = [], 0
-    for _ in range(args.steps):
-        dt, chunks = run(REF_SAMPLE)
-        times.append(dt)
+    workers = host_workers() if real else 1
+    if real:
+        times, chunks = reference_parallel(REF_SAMPLE, workers, args.warmup, args.steps)
+    else:
+        for _ in range(args.warmup):
+            cpu_port(REF_SAMPLE)
+        times, chunks = [], 0
+        for _ in range(args.steps):
+            dt, chunks = cpu_port(REF_SAMPLE)
+            times.append(dt)
     t = sum(times) / len(times)
-    v = REF_SAMPLE / t
+    v = workers * REF_SAMPLE / t
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": dict(CFG, workload=CFG["workload"] + f" (CPU slice: first {REF_SAMPLE:,} samples)"),
-        "chunks_per_s": chunks / t,
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "reference" if real else "port",
-                         "sample": f"{REF_SAMPLE:,} samples of the cfg2 layout per step through "
+        "config": dict(CFG, workload=CFG["workload"] + f" (CPU slices: {workers} x {REF_SAMPLE:,} samples)"),
+        "chunks_per_s": workers * chunks / t,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "reference" if real else "port",
+                         "sample": (f"{workers} host processes at once, each running the job on its own "
+                                    f"{REF_SAMPLE:,}-sample slice of the cfg2 layout per step, through "
+                                    if real else f"{REF_SAMPLE:,} samples of the cfg2 layout per step through ")
                                    + ("the unmodified reference (baseline/_ref mixplane: filter_intervals, "
-                                      "build_index, ChunkGenerator.generate to exhaustion), single thread"
+                                      "build_index, ChunkGenerator.generate to exhaustion); step time = the "
+                                      "slowest process"
                                       if real else "oracle/oracle.py (numpy + CPython stdlib), single thread")},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -481,14 +542,19 @@ def our_arm(args):
     }
     if not args.no_cpu_baseline and world == 1:
         real = _reference_pkg() is not None
-        n_cpu = REF_SAMPLE if real else CPU_SAMPLE
-        dt, chunks = (reference_run if real else cpu_port)(n_cpu)
-        line["cpu_baseline"] = {
-            "value": n_cpu / dt, "unit": UNIT, "cores": 1, "kind": "reference" if real else "port",
-            "chunks_per_s": chunks / dt,
-            "sample": f"first {n_cpu:,} samples ({n_cpu // 10_000} files) of the cfg2 layout through "
-                      + ("the unmodified reference (baseline/_ref), 1 thread" if real
-                         else "oracle/oracle.py (numpy + CPython stdlib), 1 thread")}
+        if real:
+            # the reference arm itself, one step on every host core, in a fresh
+            # process (no fork of this CUDA-initialised one)
+            out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
+                                  "--warmup", "0"], capture_output=True, text=True, timeout=600)
+            ref = json.loads(out.stdout.strip().splitlines()[-1])
+            line["cpu_baseline"] = dict(ref["cpu_baseline"], chunks_per_s=ref["chunks_per_s"])
+        else:
+            dt, chunks = cpu_port(CPU_SAMPLE)
+            line["cpu_baseline"] = {
+                "value": CPU_SAMPLE / dt, "unit": UNIT, "cores": 1, "kind": "port", "chunks_per_s": chunks / dt,
+                "sample": f"first {CPU_SAMPLE:,} samples ({CPU_SAMPLE // 10_000} files) of the cfg2 layout "
+                          "through oracle/oracle.py (numpy + CPython stdlib), 1 thread"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
