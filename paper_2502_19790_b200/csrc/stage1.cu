@@ -458,6 +458,126 @@ radix_downsweep(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2i
   }
 }
 
+// Staged variant: 4096-record tiles; records are first placed at their
+// tile-local sorted position in shared memory (64 KB), then written out in
+// that order, so consecutive threads write consecutive addresses of the same
+// digit bucket (~16 records per digit per tile at cfg2) instead of 4-byte
+// scattered stores into four arrays.
+constexpr int RS2_ITEMS = 16;
+constexpr int RS2_TILE = RS_THREADS * RS2_ITEMS;  // 4096
+
+__global__ void __launch_bounds__(RS_THREADS)
+radix_upsweep2(const u32* keys, long long n, int shift, u32* hist, int ntiles) {
+  __shared__ u32 h[256];
+  const int tid = threadIdx.x;
+  h[tid] = 0;
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * RS2_TILE;
+#pragma unroll 4
+  for (int k = 0; k < RS2_ITEMS; ++k) {
+    long long i = base + k * RS_THREADS + tid;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  hist[(long long)tid * ntiles + blockIdx.x] = h[tid];
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+radix_downsweep2(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2in, u32* kout, u32* p0out,
+                 u32* p1out, u32* p2out, long long n, int shift, const u32* hist, const u32* digit_tot,
+                 int ntiles) {
+  extern __shared__ __align__(16) u32 s_stage[];  // [4][RS2_TILE]
+  __shared__ u32 s_base[256], s_loc[256];
+  __shared__ u32 s_wcnt[RS_WARPS][256];
+  __shared__ u32 s_w[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {  // global digit bases: exclusive scan of digit totals + this tile's row prefix
+    u32 x = digit_tot[tid];
+    u32 inc = warp_incl_scan(x);
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      u32 y = lane < 8 ? s_w[lane] : 0;
+      u32 yi = warp_incl_scan(y);
+      if (lane < 8) s_w[lane] = yi - y;
+    }
+    __syncthreads();
+    s_base[tid] = s_w[warp] + inc - x + hist[(long long)tid * ntiles + blockIdx.x];
+  }
+#pragma unroll
+  for (int w = 0; w < RS_WARPS; ++w) s_wcnt[w][tid] = 0;
+  __syncthreads();
+  // warp w owns the contiguous records [w * 512, (w + 1) * 512) of the tile
+  const long long t0 = (long long)blockIdx.x * RS2_TILE;
+  const long long base = t0 + warp * (32 * RS2_ITEMS);
+  u32 dig[RS2_ITEMS], rank[RS2_ITEMS];
+#pragma unroll
+  for (int k = 0; k < RS2_ITEMS; ++k) {
+    const long long i = base + k * 32 + lane;
+    const bool ok = i < n;
+    const u32 d = ok ? (kin[i] >> shift) & 0xff : 0x100u;
+    const u32 peers = __match_any_sync(MX_FULL, d);
+    const u32 before = __popc(peers & ((1u << lane) - 1));
+    const u32 cur = s_wcnt[warp][d & 0xff];
+    __syncwarp();
+    rank[k] = cur + before;
+    dig[k] = d;
+    if (ok && before == 0) s_wcnt[warp][d] = cur + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  u32 tot;
+  {  // per digit: exclusive scan over warps, then over digits (tile-local bucket starts)
+    u32 run = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+      u32 c = s_wcnt[w][tid];
+      s_wcnt[w][tid] = run;
+      run += c;
+    }
+    tot = run;
+    u32 inc = warp_incl_scan(tot);
+    __syncthreads();
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      u32 y = lane < 8 ? s_w[lane] : 0;
+      u32 yi = warp_incl_scan(y);
+      if (lane < 8) s_w[lane] = yi - y;
+    }
+    __syncthreads();
+    s_loc[tid] = s_w[warp] + inc - tot;
+  }
+  __syncthreads();
+  u32* sk = s_stage;
+  u32* sa = s_stage + RS2_TILE;
+  u32* sb = s_stage + 2 * RS2_TILE;
+  u32* sc = s_stage + 3 * RS2_TILE;
+#pragma unroll
+  for (int k = 0; k < RS2_ITEMS; ++k) {
+    const long long i = base + k * 32 + lane;
+    if (dig[k] < 0x100u) {
+      const u32 d = dig[k];
+      const u32 pos = s_loc[d] + s_wcnt[warp][d] + rank[k];
+      sk[pos] = kin[i];
+      sa[pos] = p0in[i];
+      sb[pos] = p1in[i];
+      sc[pos] = p2in[i];
+    }
+  }
+  __syncthreads();
+  const int cnt = (int)(n - t0 < RS2_TILE ? n - t0 : RS2_TILE);
+  for (int i = tid; i < cnt; i += RS_THREADS) {
+    const u32 key = sk[i];
+    const u32 d = (key >> shift) & 0xff;
+    const u32 dst = s_base[d] + (u32)i - s_loc[d];
+    kout[dst] = key;
+    p0out[dst] = sa[i];
+    p1out[dst] = sb[i];
+    p2out[dst] = sc[i];
+  }
+}
+
 // ---------------------------------------------------------------- host side
 template <int SEGS, int PC>
 static int launch_pipe(const S1Args& a, const TileMeta* m, long long ntiles, long long nstaged, int stages,
@@ -788,7 +908,26 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     mx_count_launch();
     std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);
   }
-  for (int pass = 0; pass < passes; ++pass) {
+  const char* rs_env = getenv("MX_RADIX");
+  const bool staged = !(rs_env && !strcmp(rs_env, "direct"));
+  const int rtiles2 = (int)((I + RS2_TILE - 1) / RS2_TILE);
+  if (staged) {
+    MX_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(4 * RS2_TILE * sizeof(u32))));
+  }
+  for (int pass = 0; staged && pass < passes; ++pass) {
+    const int shift = 8 * pass;
+    radix_upsweep2<<<rtiles2, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles2);
+    mx_count_launch();
+    radix_rowscan<<<256, 256, 0, s>>>(hist.p, rtiles2, dtot.p);
+    mx_count_launch();
+    radix_downsweep2<<<rtiles2, RS_THREADS, 4 * RS2_TILE * sizeof(u32), s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I,
+                                                                             shift, hist.p, dtot.p, rtiles2);
+    mx_count_launch();
+    MX_CUDA_TRY(cudaGetLastError());
+    std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);
+  }
+  for (int pass = 0; !staged && pass < passes; ++pass) {
     const int shift = 8 * pass;
     const u32* seg = nullptr;
     const int tiles = rtiles;
