@@ -1257,6 +1257,56 @@ __global__ void emit_write_kernel(EmitArgs a, u64 n_pairs, const u64* pair_off, 
   walk_pair<true>(a, pr, nullptr, pm, pf, ps, pe, pair_off[pr]);
 }
 
+// Same, with each warp's pieces staged in shared memory: the 32 pairs of a
+// warp own one contiguous output range [pair_off[first], pair_off[last+1]),
+// so the lanes write their pieces there as 16-byte records and the warp then
+// stores the range coalesced into the four piece arrays (direct per-lane
+// stores put 32 lanes ~5 records apart on every store instruction). Warps
+// with a long pair (cut later by emit_write_warp_kernel) or a range above
+// EW_CAP store directly.
+constexpr int EW_THREADS = 128;
+constexpr int EW_CAP = 640;
+__global__ void __launch_bounds__(EW_THREADS) emit_write_staged_kernel(EmitArgs a, u64 n_pairs, const u64* pair_off,
+                                                                       u32* pm, u32* pf, u32* ps, u32* pe,
+                                                                       u32* long_list, u32* long_cnt, u32 warp_min) {
+  __shared__ uint4 s_rec[EW_THREADS / 32][EW_CAP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 pr = blockIdx.x * (u64)EW_THREADS + threadIdx.x;
+  const u64 first = blockIdx.x * (u64)EW_THREADS + warp * 32;
+  if (first >= n_pairs) return;  // warp-uniform
+  const bool valid = pr < n_pairs;
+  const u64 lo_i = valid ? pair_off[pr] : 0, hi_i = valid ? pair_off[pr + 1] : 0;
+  const bool is_long = valid && hi_i - lo_i > warp_min;
+  if (is_long) long_list[atomicAdd(long_cnt, 1u)] = (u32)pr;
+  const u64 last = first + 31 < n_pairs ? first + 31 : n_pairs - 1;
+  const u64 w_lo = pair_off[first], w_hi = pair_off[last + 1];
+  const bool staged = !__any_sync(MX_FULL, is_long) && w_hi - w_lo <= (u64)EW_CAP;
+  if (!staged) {
+    if (valid && !is_long) walk_pair<true>(a, pr, nullptr, pm, pf, ps, pe, lo_i);
+    return;
+  }
+  uint4* rec = s_rec[warp];
+  if (valid) {
+    const u64 base = lo_i - w_lo;
+    const int p = phase_of_pair(a, pr);
+    const Phase php = a.phases[p];
+    const u64 local = pr - a.pair_pre[p];
+    const long long kr = (long long)(local / (u64)php.n_terms);
+    const Term tm = a.terms[php.term_begin + (long long)(local % (u64)php.n_terms)];
+    walk_term<true>(a, tm, kr, [&](u64 i, u32 m, u32 f, u32 s0, u32 e0) { rec[base + i] = make_uint4(m, f, s0, e0); },
+                    0, 1);
+  }
+  __syncwarp();
+  const int cnt = (int)(w_hi - w_lo);
+  for (int i = lane; i < cnt; i += 32) {
+    const uint4 r = rec[i];
+    pm[w_lo + i] = r.x;
+    pf[w_lo + i] = r.y;
+    ps[w_lo + i] = r.z;
+    pe[w_lo + i] = r.w;
+  }
+}
+
 // one warp per long pair: the lanes cut its intervals in parallel
 __global__ void __launch_bounds__(256) emit_write_warp_kernel(EmitArgs a, const u64* pair_off, u32* pm, u32* pf,
                                                               u32* ps, u32* pe, const u32* long_list,
@@ -1898,7 +1948,12 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
     MX_CUDA_TRY(lcnt.alloc(1, s));
     MX_CUDA_TRY(cudaMemsetAsync(lcnt.p, 0, sizeof(u32), s));
     static const u32 warp_min = getenv("MX_EMIT_WARP_MIN") ? (u32)atoi(getenv("MX_EMIT_WARP_MIN")) : 32u;
-    emit_write_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p, warp_min);
+    static const bool ew_direct = getenv("MX_EMIT_DIRECT") != nullptr;
+    if (ew_direct)
+      emit_write_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p, warp_min);
+    else
+      emit_write_staged_kernel<<<(unsigned)((n_pairs + EW_THREADS - 1) / EW_THREADS), EW_THREADS, 0, s>>>(
+          a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p, warp_min);
     mx_count_launch();
     const long long wgrid = std::min<long long>(((long long)n_pairs + 7) / 8, 148 * 16);
     emit_write_warp_kernel<<<(unsigned)wgrid, 256, 0, s>>>(a, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p);
