@@ -162,6 +162,9 @@ struct CumPermF {
   const u32* start;
   const u32* end;
   u64* cum;
+  const u32* file;
+  u32* cfile;   // file / start of cursor position j (the emission's gathers, done once here)
+  u32* cstart;
   __device__ u64 value(long long j) const {
     const u32 iv = perm[j];
     return end[iv] - start[iv];
@@ -169,6 +172,9 @@ struct CumPermF {
   __device__ void apply(long long j, u64 ex, u64 v) const {
     if (j == 0) cum[0] = 0;
     cum[j + 1] = ex + v;
+    const u32 iv = perm[j];
+    cfile[j] = file[iv];
+    cstart[j] = start[iv];
   }
   __device__ void total(u64) const {}
 };
@@ -274,7 +280,11 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   MX_CUDA_TRY(g->civ.alloc(I, s));
   if (int rc = gs_run(B, CursorIvF{g->cur_blk.p, ix->blk_first.p, g->civ.p}, s)) return rc;
   MX_CUDA_TRY(g->ccum.alloc(I + 1, s));
-  if (int rc = gs_run(I, CumPermF{g->civ.p, ix->iv_start.p, ix->iv_end.p, g->ccum.p}, s)) return rc;
+  MX_CUDA_TRY(g->cfile.alloc(I, s));
+  MX_CUDA_TRY(g->cstart.alloc(I, s));
+  if (int rc = gs_run(I, CumPermF{g->civ.p, ix->iv_start.p, ix->iv_end.p, g->ccum.p, ix->iv_file.p, g->cfile.p,
+                                   g->cstart.p}, s))
+    return rc;
   MX_CUDA_TRY(g->comp_total.alloc(K, s));
   comp_total_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
                                                                ix->iv_cum.p, g->comp_total.p);

@@ -102,6 +102,7 @@ struct GenData {
   std::vector<u32> h_comp_order;
   DevBuf<u32> cur_blk;
   DevBuf<u32> civ;
+  DevBuf<u32> cfile, cstart;  // iv_file / iv_start in cursor order (emission reads them sequentially)
   DevBuf<u64> ccum;
   DevBuf<u64> comp_total;
   std::vector<unsigned long long> h_comp_total;

@@ -1114,6 +1114,8 @@ struct EmitArgs {
   const u32* key_blk_first;
   const u32* blk_first;
   const u32* civ;
+  const u32* cfile;   // iv_file / iv_start in cursor order
+  const u32* cstart;
   const u64* ccum;
   const u32* iv_start;
   const u32* iv_end;
@@ -1180,13 +1182,12 @@ __device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink s
       } else {
         for (long long r = ra + lane; r < rb; r += lanes) {
           const long long jj = a.lpos[r];
-          const u32 iv = a.civ[jj];
           const u64 off = a.ccum[jj] - cb;
           const u64 len = a.ccum[jj + 1] - a.ccum[jj];
           const u64 from = lo_abs > off ? lo_abs : off;
           const u64 to = hi_abs < off + len ? hi_abs : off + len;
-          sink(n + (u64)(r - ra), a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
-               a.iv_start[iv] + (u32)(to - off));
+          const u32 st0 = a.cstart[jj];
+          sink(n + (u64)(r - ra), a.arbitrary ? c : tm.m, a.cfile[jj], st0 + (u32)(from - off), st0 + (u32)(to - off));
         }
         if (rb > ra) n += (u64)(rb - ra);
       }
@@ -1198,13 +1199,12 @@ __device__ u64 walk_term(const EmitArgs& a, const Term& tm, long long kr, Sink s
     const long long j1 = ub_u64(a.ccum, ib, ie, cb + hi_abs - 1) - 1;
     if (WRITE) {
       for (long long jj = j + lane; jj <= j1; jj += lanes) {
-        const u32 iv = a.civ[jj];
         const u64 off = a.ccum[jj] - cb;
         const u64 len = a.ccum[jj + 1] - a.ccum[jj];
         const u64 from = lo_abs > off ? lo_abs : off;
         const u64 to = hi_abs < off + len ? hi_abs : off + len;
-        sink(n + (u64)(jj - j), a.arbitrary ? c : tm.m, a.iv_file[iv], a.iv_start[iv] + (u32)(from - off),
-             a.iv_start[iv] + (u32)(to - off));
+        const u32 st0 = a.cstart[jj];
+        sink(n + (u64)(jj - j), a.arbitrary ? c : tm.m, a.cfile[jj], st0 + (u32)(from - off), st0 + (u32)(to - off));
       }
     }
     n += (u64)(j1 - j + 1);
@@ -1921,6 +1921,8 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   a.key_blk_first = ix->key_blk_first.p;
   a.blk_first = ix->blk_first.p;
   a.civ = g->civ.p;
+  a.cfile = g->cfile.p;
+  a.cstart = g->cstart.p;
   a.ccum = g->ccum.p;
   a.iv_start = ix->iv_start.p;
   a.iv_end = ix->iv_end.p;
@@ -2277,6 +2279,8 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     a.key_blk_first = ix->key_blk_first.p;
     a.blk_first = ix->blk_first.p;
     a.civ = g->civ.p;
+    a.cfile = g->cfile.p;
+    a.cstart = g->cstart.p;
     a.ccum = g->ccum.p;
     a.iv_start = ix->iv_start.p;
     a.iv_end = ix->iv_end.p;
