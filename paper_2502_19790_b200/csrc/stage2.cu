@@ -1894,6 +1894,23 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(g->res_off.reserve(n_chunks + 1, s));
   MX_CUDA_TRY(g->res_seed.reserve(n_chunks > 0 ? n_chunks : 1, s));
   MX_CUDA_TRY(g->res_id.reserve(n_chunks > 0 ? n_chunks : 1, s));
+  // chunk seeds depend only on chunk ids: hash them on a side stream while
+  // the pieces are cut, normalised and compacted on `s`
+  static thread_local cudaStream_t seed_side = nullptr;
+  static thread_local cudaEvent_t seed_fork = nullptr, seed_join = nullptr;
+  if (!seed_side) {
+    MX_CUDA_TRY(cudaStreamCreateWithFlags(&seed_side, cudaStreamNonBlocking));
+    MX_CUDA_TRY(cudaEventCreateWithFlags(&seed_fork, cudaEventDisableTiming));
+    MX_CUDA_TRY(cudaEventCreateWithFlags(&seed_join, cudaEventDisableTiming));
+  }
+  if (n_chunks > 0) {
+    MX_CUDA_TRY(cudaEventRecord(seed_fork, s));
+    MX_CUDA_TRY(cudaStreamWaitEvent(seed_side, seed_fork, 0));
+    chunk_seed_kernel<<<(unsigned)((n_chunks + 127) / 128), 128, 0, seed_side>>>(
+        n_chunks, g->next_chunk_id, g->chunk_prefix.p, g->chunk_prefix_len, g->res_seed.p, g->res_id.p);
+    mx_count_launch();
+    MX_CUDA_TRY(cudaEventRecord(seed_join, seed_side));
+  }
   if (n_chunks == 0) {
     const long long z = 0;
     MX_CUDA_TRY(mx_h2d(g->res_off.p, &z, sizeof(z), s));
@@ -2004,9 +2021,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
                                                        grouped);
     mx_count_launch();
   }
-  chunk_seed_kernel<<<(unsigned)((n_chunks + 127) / 128), 128, 0, s>>>(n_chunks, g->next_chunk_id, g->chunk_prefix.p,
-                                                                      g->chunk_prefix_len, g->res_seed.p, g->res_id.p);
-  mx_count_launch();
+  MX_CUDA_TRY(cudaStreamWaitEvent(s, seed_join, 0));  // chunk seeds (side stream) done
   MX_CUDA_TRY(cudaGetLastError());
   u32 h_big = 0;
   long long total = 0;
