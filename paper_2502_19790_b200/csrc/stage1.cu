@@ -458,16 +458,15 @@ radix_downsweep(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2i
   }
 }
 
-// Staged variant: 4096-record tiles; records are first placed at their
+// Staged variant: 4096-record tiles (RS2_ITEMS 16; 8 = 2048); records are first placed at their
 // tile-local sorted position in shared memory (64 KB), then written out in
 // that order, so consecutive threads write consecutive addresses of the same
 // digit bucket (~16 records per digit per tile at cfg2) instead of 4-byte
 // scattered stores into four arrays.
-constexpr int RS2_ITEMS = 16;
-constexpr int RS2_TILE = RS_THREADS * RS2_ITEMS;  // 4096
-
+template <int RS2_ITEMS>
 __global__ void __launch_bounds__(RS_THREADS)
 radix_upsweep2(const u32* keys, long long n, int shift, u32* hist, int ntiles) {
+  constexpr int RS2_TILE = RS_THREADS * RS2_ITEMS;
   __shared__ u32 h[256];
   const int tid = threadIdx.x;
   h[tid] = 0;
@@ -482,10 +481,12 @@ radix_upsweep2(const u32* keys, long long n, int shift, u32* hist, int ntiles) {
   hist[(long long)tid * ntiles + blockIdx.x] = h[tid];
 }
 
+template <int RS2_ITEMS>
 __global__ void __launch_bounds__(RS_THREADS)
 radix_downsweep2(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2in, u32* kout, u32* p0out,
                  u32* p1out, u32* p2out, long long n, int shift, const u32* hist, const u32* digit_tot,
                  int ntiles) {
+  constexpr int RS2_TILE = RS_THREADS * RS2_ITEMS;
   extern __shared__ __align__(16) u32 s_stage[];  // [4][RS2_TILE]
   __shared__ u32 s_base[256], s_loc[256];
   __shared__ u32 s_wcnt[RS_WARPS][256];
@@ -910,19 +911,28 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   }
   const char* rs_env = getenv("MX_RADIX");
   const bool staged = !(rs_env && !strcmp(rs_env, "direct"));
-  const int rtiles2 = (int)((I + RS2_TILE - 1) / RS2_TILE);
+  const char* ri_env = getenv("MX_RADIX_ITEMS");
+  const int ritems = ri_env && atoi(ri_env) == 16 ? 16 : 8;
+  const int rtile2 = RS_THREADS * ritems;
+  const int rtiles2 = (int)((I + rtile2 - 1) / rtile2);
+  const size_t rsmem = 4 * (size_t)rtile2 * sizeof(u32);
   if (staged) {
-    MX_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(4 * RS2_TILE * sizeof(u32))));
+    MX_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(4 * RS_THREADS * 16 * sizeof(u32))));
   }
   for (int pass = 0; staged && pass < passes; ++pass) {
     const int shift = 8 * pass;
-    radix_upsweep2<<<rtiles2, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles2);
+    if (ritems == 16) radix_upsweep2<16><<<rtiles2, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles2);
+    else radix_upsweep2<8><<<rtiles2, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles2);
     mx_count_launch();
     radix_rowscan<<<256, 256, 0, s>>>(hist.p, rtiles2, dtot.p);
     mx_count_launch();
-    radix_downsweep2<<<rtiles2, RS_THREADS, 4 * RS2_TILE * sizeof(u32), s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I,
-                                                                             shift, hist.p, dtot.p, rtiles2);
+    if (ritems == 16)
+      radix_downsweep2<16><<<rtiles2, RS_THREADS, rsmem, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p,
+                                                              dtot.p, rtiles2);
+    else
+      radix_downsweep2<8><<<rtiles2, RS_THREADS, rsmem, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p,
+                                                             dtot.p, rtiles2);
     mx_count_launch();
     MX_CUDA_TRY(cudaGetLastError());
     std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);
