@@ -758,15 +758,40 @@ scan_pipe_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles, 
 __global__ void slot_compact_kernel(long long ntiles, long long tile_len, const u32* cnt, const u64* off,
                                     const u32* k, const u32* f, const u32* s, const u32* e, u32* k2, u32* f2, u32* s2,
                                     u32* e2) {
+  // four tiles per warp in flight: their counts / offsets, then their first
+  // 32 records each, are loaded before anything is stored
+  constexpr int U = 4;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long t = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles; t += warps) {
-    const u32 c = cnt[t];
-    const u64 src = (u64)t * tile_len, dst = off[t];
-    for (u32 i = threadIdx.x & 31; i < c; i += 32) {
-      k2[dst + i] = k[src + i];
-      f2[dst + i] = f[src + i];
-      s2[dst + i] = s[src + i];
-      e2[dst + i] = e[src + i];
+  const u32 lane = threadIdx.x & 31;
+  for (long long t0 = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t0 < ntiles; t0 += U * warps) {
+    u32 c[U];
+    u64 dst[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long t = t0 + u * warps;
+      c[u] = t < ntiles ? cnt[t] : 0;
+      dst[u] = t < ntiles ? off[t] : 0;
+    }
+    u32 vk[U], vf[U], vs[U], ve[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const u64 src = (u64)(t0 + u * warps) * tile_len + lane;
+      if (lane < c[u]) {
+        vk[u] = k[src]; vf[u] = f[src]; vs[u] = s[src]; ve[u] = e[src];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (lane < c[u]) {
+        k2[dst[u] + lane] = vk[u]; f2[dst[u] + lane] = vf[u]; s2[dst[u] + lane] = vs[u]; e2[dst[u] + lane] = ve[u];
+      }
+      const u64 src = (u64)(t0 + u * warps) * tile_len;
+      for (u32 i = lane + 32; i < c[u]; i += 32) {  // tiles with more than 32 runs
+        k2[dst[u] + i] = k[src + i];
+        f2[dst[u] + i] = f[src + i];
+        s2[dst[u] + i] = s[src + i];
+        e2[dst[u] + i] = e[src + i];
+      }
     }
   }
 }
