@@ -104,6 +104,32 @@ typedef struct mx_catalog_desc {
  * an un-keyable (all-null) sample or an empty catalog. An empty result is a
  * valid index with 0 keys (the server raises "matches no samples"). */
 int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out);
+/* Index from explicit interval rows [build_index(rows, workers) index.py:88-115,
+ * the reference's entry point when rows come from anywhere but the catalog
+ * (tests, composed paths)]. Host arrays [n_rows]: key = 1-based rank of the
+ * row's component key in MixtureKey.sort_key order (so the packed key order
+ * is the key order), file = index into the file table, which is sorted by
+ * (dataset id, file id); start / end half-open. Key strings: piece k-1 is the
+ * canonical string of key rank k (mixtures.py:118-121), offsets [n_keys+1].
+ * On the device: sort by (key, file, start), reject empty intervals and
+ * overlaps inside one (key, file) (MX_ERR_INDEX, index.py:32-47), merge
+ * adjacent intervals, then the same key / block / cumulative tables as
+ * mx_index_build. The result does not depend on the row order (= workers). */
+typedef struct mx_rows_desc {
+  int64_t n_rows;
+  const uint32_t* key;
+  const uint32_t* file;
+  const uint32_t* start;
+  const uint32_t* end;
+  int32_t n_files;
+  const int32_t* file_ds;  /* host int32[n_files] */
+  const int64_t* file_ids; /* host int64[n_files] */
+  int32_t n_keys;
+  uint32_t key_bits;       /* bits of the largest rank (<= 31) */
+  const uint8_t* key_strings;
+  const int64_t* key_string_offsets; /* host [n_keys+1] */
+} mx_rows_desc;
+int mx_index_build_rows(const mx_rows_desc* desc, void* stream, mx_index** out);
 int mx_index_free(mx_index* index);
 int mx_index_sizes(const mx_index* index, int64_t* n_keys, int64_t* n_blocks,
                    int64_t* n_intervals, int64_t* n_samples);

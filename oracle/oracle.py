@@ -35,6 +35,7 @@ import hashlib
 import json
 import math
 import random
+import sys
 from bisect import bisect_right
 
 import numpy as np
@@ -289,6 +290,29 @@ def apportion(weights: dict, total: int) -> dict:
     return base
 
 
+def apportion_vec(w: np.ndarray, total: int) -> np.ndarray:
+    """``apportion`` over weights already in key order, vectorised: the same
+    IEEE operations element by element (``share = w / wsum * total``,
+    ``int(share + 1e-9)``, ``max(0, share - base)``) and the same
+    (-frac, key order) leftover order; ``wsum`` is CPython's compensated
+    ``sum`` (the builtin on 3.12+, ``neumaier_sum`` otherwise)."""
+    if total < 0:
+        raise OracleError("MixtureError", "total must be nonnegative")
+    wl = w.tolist()
+    wsum = float(sum(wl)) if sys.version_info >= (3, 12) else neumaier_sum(wl)
+    if wsum <= 0:
+        raise OracleError("MixtureError", "weights must sum to a positive value")
+    share = w / wsum * float(total)
+    base = np.trunc(share + TOL)
+    frac = np.maximum(share - base, 0.0)
+    out = base.astype(np.int64)
+    left = int(total - int(out.sum()))
+    if left > 0:
+        order = np.lexsort((np.arange(len(w)), -frac))
+        out[order[:left]] += 1
+    return out
+
+
 class OracleGenerator:
     """``ChunkGenerator`` replayed over per-component consumed offsets."""
 
@@ -349,20 +373,26 @@ class OracleGenerator:
         return OracleChunk(cid, data, seed_of(self.seed, "chunk", cid), weights, chunk_size, strict)
 
     def generate(self, weights: dict, chunk_size: int, strict: bool = False):
+        """``ChunkGenerator.generate`` (``chunks.py:194-230``) with the per-key
+        state in arrays indexed by mixture-key order (``sorted_keys``), so
+        10k-key mixtures (cfg 5) replay in reasonable time. Same passes, same
+        death / redistribution order (``redistribute_best_effort``,
+        ``chunks.py:109-130``: the shortfall is apportioned over every
+        not-yet-dead key, in key order, by the original weights)."""
         weights = {as_key(k): float(v) for k, v in weights.items()}
         if strict and chunk_size < len(weights):
             raise OracleError("MixtureError", "chunk size below the number of mixture keys")
-        remaining = apportion(weights, chunk_size)
-        mkeys = sorted(remaining, key=key_order)
+        mkeys = sorted(weights, key=key_order)
+        w = np.array([weights[k] for k in mkeys], dtype=np.float64)
+        remaining = apportion_vec(w, chunk_size)
+        dead = np.zeros(len(mkeys), dtype=bool)
         data: dict = {}
-        dead: set = set()
         self.last_report = None
-        while any(v > 0 for v in remaining.values()):
+        while (remaining > 0).any():
             found = {}
-            for m in mkeys:
-                need = remaining[m]
-                if need <= 0:
-                    continue
+            for i in np.flatnonzero(remaining > 0).tolist():
+                m = mkeys[i]
+                need = int(remaining[i])
                 got = 0
                 for r in self._matching(m):
                     if need <= 0:
@@ -377,26 +407,24 @@ class OracleGenerator:
                         data.setdefault(m, {}).setdefault(d, {}).setdefault(f, []).append((a, b))
                     got += t
                     need -= t
-                found[m] = got
-                remaining[m] -= got
-            newly = sorted((m for m, g in found.items() if g == 0 and remaining[m] > 0), key=key_order)
+                found[i] = got
+                remaining[i] -= got
+            newly = sorted(i for i, g in found.items() if g == 0 and remaining[i] > 0)
             if not newly:
                 continue
             if strict:
-                self.last_report = {m: v for m, v in remaining.items() if v > 0}
+                self.last_report = {mkeys[i]: int(remaining[i]) for i in np.flatnonzero(remaining > 0)}
                 return None
-            for m in newly:
-                dead.add(m)
-                alive = [k for k in remaining if k not in dead]
-                if not alive:
-                    self.last_report = {k: v for k, v in remaining.items() if v > 0}
+            for i in newly:
+                dead[i] = True
+                alive = np.flatnonzero(~dead)
+                if len(alive) == 0:
+                    self.last_report = {mkeys[j]: int(remaining[j]) for j in np.flatnonzero(remaining > 0)}
                     return None
-                short = remaining[m]
+                short = int(remaining[i])
                 if short > 0:
-                    extra = apportion({k: weights[k] for k in alive}, short)
-                    for k, x in extra.items():
-                        remaining[k] += x
-                remaining[m] = 0
+                    remaining[alive] += apportion_vec(w[alive], short)
+                remaining[i] = 0
         return self._chunk(data, weights, chunk_size, strict)
 
     def generate_arbitrary(self, chunk_size: int):

@@ -21,7 +21,7 @@ from .errors import (
     SchemaError,
     ServerError,
 )
-from .index import ChunkerIndex, DeviceCatalog, RangeCursor, build_index_from_catalog
+from .index import ChunkerIndex, DeviceCatalog, RangeCursor, build_index, build_index_from_catalog
 from .mixtures import (
     HierarchicalMixtureSpec,
     HierarchyBranch,

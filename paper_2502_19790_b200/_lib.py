@@ -94,6 +94,23 @@ class ShardDesc(C.Structure):
     ]
 
 
+class RowsDesc(C.Structure):
+    _fields_ = [
+        ("n_rows", i64),
+        ("key", P(u32)),
+        ("file", P(u32)),
+        ("start", P(u32)),
+        ("end", P(u32)),
+        ("n_files", i32),
+        ("file_ds", P(i32)),
+        ("file_ids", P(i64)),
+        ("n_keys", i32),
+        ("key_bits", u32),
+        ("key_strings", P(C.c_uint8)),
+        ("key_string_offsets", P(i64)),
+    ]
+
+
 class JsonDesc(C.Structure):
     _fields_ = [
         ("n_keys", i64),
@@ -114,6 +131,7 @@ _SIGS = {
     "mx_profile_reset": (C.c_int, []),
     "mx_profile_read": (C.c_int, [C.c_char_p, P(dbl), P(i64)]),
     "mx_index_build": (C.c_int, [P(CatalogDesc), vp, P(vp)]),
+    "mx_index_build_rows": (C.c_int, [P(RowsDesc), vp, P(vp)]),
     "mx_index_free": (C.c_int, [vp]),
     "mx_index_sizes": (C.c_int, [vp, P(i64), P(i64), P(i64), P(i64)]),
     "mx_index_export_keys": (C.c_int, [vp, vp, vp]),

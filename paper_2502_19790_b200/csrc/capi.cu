@@ -301,6 +301,39 @@ int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out) {
   return MX_OK;
 }
 
+int mx_index_build_rows(const mx_rows_desc* desc, void* stream, mx_index** out) {
+  MX_CHECK_ARG(desc && out, "null argument");
+  MX_CHECK_ARG(desc->n_rows >= 0 && desc->n_files >= 0 && desc->n_keys >= 0, "negative size");
+  if (desc->key_bits > 31) return mx_fail(MX_ERR_UNSUPPORTED, "rows index: %u key bits (> 31)", desc->key_bits);
+  g_err.clear();
+  keep_pool_warm();
+  cudaStream_t s = (cudaStream_t)stream;
+  mx_index* ix = new mx_index();
+  ix->d.stream = s;
+  IndexData& d = ix->d;
+  // one "property" whose value rank IS the key rank; piece k-1 = key k's string
+  d.n_props = 1;
+  d.field_shift[0] = 0;
+  d.field_width[0] = desc->key_bits;
+  d.str_base[0] = 0;
+  int rc = MX_OK;
+  {
+    const long long nbytes = desc->key_string_offsets[desc->n_keys];
+    cudaError_t e = d.str_off.alloc(desc->n_keys + 1, s);
+    if (e == cudaSuccess) e = d.str_bytes.alloc(nbytes > 0 ? nbytes : 1, s);
+    if (e == cudaSuccess) e = mx_h2d(d.str_off.p, desc->key_string_offsets, sizeof(long long) * (desc->n_keys + 1), s);
+    if (e == cudaSuccess && nbytes > 0) e = mx_h2d(d.str_bytes.p, desc->key_strings, nbytes, s);
+    if (e != cudaSuccess) rc = mx_fail_cuda(e, "key strings", __FILE__, __LINE__);
+  }
+  if (rc == MX_OK) rc = rows_build(desc, s, &d);
+  if (rc < 0) {
+    delete ix;
+    return rc;
+  }
+  *out = ix;
+  return MX_OK;
+}
+
 // Device buffers are released stream-ordered (cudaFreeAsync); waiting for
 // the stream here keeps the pool's next allocations of the same sizes on
 // already-released memory (measured: without it the next job's allocations

@@ -165,6 +165,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
 int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, long long* n_out);
 int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long long* n_out);
 int index_finalize(IndexData* ix, long long I, cudaStream_t s);
+int rows_build(const mx_rows_desc* d, cudaStream_t s, IndexData* out);
 int index_block_table(const IndexData* ix, u32 file_base, uint4* out, cudaStream_t s);
 int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream_t s, IndexData* out);
 int gen_local_lists(GenData* g, cudaStream_t s);

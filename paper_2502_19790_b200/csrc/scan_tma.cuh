@@ -545,52 +545,6 @@ scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
   fast_tile<SEGS>(a, m, tile, st, sc, s_fs);
 }
 
-// Single code column (row-tuple layout): 8 KB of column per 2048-sample tile
-// is too little work per CTA -- one CTA per tile is then bound by the CTA
-// launch rate (~0.9 us per CTA per SM whatever the occupancy: 0.29 ms for
-// 48.8k tiles). Persistent CTAs walk the tiles grid-stride and prefetch the
-// next tile's column segments into registers while finishing the current one.
-template <int SEGS, bool GLUT, int OCC>
-__global__ void __launch_bounds__(S1_THREADS, OCC)
-scan_fast1_kernel(S1Args a, const TileMeta* __restrict__ meta, long long nfull) {
-  constexpr int TILE = S1_THREADS * 4 * SEGS;
-  extern __shared__ __align__(16) u32 s_lut[];
-  __shared__ TileScratch sc;
-  __shared__ int s_fs[FAST_MAX_FS];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lw = warp * 128 * SEGS + 4 * lane;
-  int4 v[1][SEGS];
-  long long tile = blockIdx.x;
-  if (tile < nfull) {
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j) v[0][j] = codes4(a, 0, tile * TILE + lw + 128 * j);
-  }
-  if (!GLUT)
-    for (int i = tid; i < a.lut_off[1]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
-  for (; tile < nfull; tile += gridDim.x) {
-    const long long t0 = tile * TILE;
-    const TileMeta m = meta[tile];
-    int4 cur[1][SEGS];
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j) cur[0][j] = v[0][j];
-    const long long nxt = tile + gridDim.x;
-    if (nxt < nfull) {
-#pragma unroll
-      for (int j = 0; j < SEGS; ++j) v[0][j] = codes4(a, 0, nxt * TILE + lw + 128 * j);
-    }
-    if (m.nf > FAST_MAX_FS) {  // CTA-uniform: many tiny files, deferred to scan_list_kernel
-      if (tid == 0) a.defer_list[atomicAdd(a.defer_cnt, 1u)] = (u32)tile;
-      continue;
-    }
-    __syncthreads();  // the previous tile's readers of s_fs / sc / s_off are done (and the LUT is staged)
-    if (tid < FAST_MAX_FS) s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - t0) : 1 << 30;
-    __syncthreads();
-    u32 st[SEGS][4];
-    lut_sums<1, SEGS, GLUT>(s_lut, a, cur, st);
-    fast_tile<SEGS>(a, m, tile, st, sc, s_fs);
-  }
-}
-
 // persistent CTAs, every full tile's columns + metadata streamed into a ring
 // of shared-memory slots by cp.async.bulk (TMA); same tile body
 template <int PC>

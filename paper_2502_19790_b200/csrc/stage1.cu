@@ -322,6 +322,7 @@ scan_runs_kernel(S1Args a) {
 }  // namespace mx
 
 #include "scan_tma.cuh"
+#include "scan_u16.cuh"
 
 namespace mx {
 
@@ -636,29 +637,31 @@ static void launch_fast(const S1Args& a, const TileMeta* m, long long nfull, int
     return;
   }
   if constexpr (PC == 1 && SEGS == 2) {
-    // one code column: more CTAs per SM (MX_FAST1_OCC = 4 | 6 | 8, default
-    // 8); MX_SCAN=fast1_persist selects persistent grid-stride CTAs
-    // (measured slower: 0.35 vs 0.29 ms at cfg2)
-    const char* occ_env = getenv("MX_FAST1_OCC");
-    const int occ = occ_env ? atoi(occ_env) : 8;
-    const bool persist = env && !strcmp(env, "fast1_persist");
-    int dev = 0, n_sm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (a.u16 && (reinterpret_cast<uintptr_t>(a.cols[0]) % 16) == 0) {
+      // one u16 code column (row-tuple layout): change-driven persistent
+      // kernel (scan_u16.cuh), LUT staged per CTA when it fits
+      int dev = 0, n_sm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+      const int entries = lut_total - 1;
+      const bool slut = entries <= U16_SMEM_LUT_MAX;
+      const size_t dyn = slut ? sizeof(u32) * (size_t)entries : 0;
+      int per_sm = 8;
+      if (slut) {
+        cudaFuncSetAttribute(scan_u16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<true>, U16_THREADS, dyn);
+      } else {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<false>, U16_THREADS, 0);
+      }
+      const unsigned grid = (unsigned)std::min<long long>(nfull, (long long)n_sm * std::max(1, per_sm));
+      if (slut) scan_u16_kernel<true><<<grid, U16_THREADS, dyn, s>>>(a, m, nfull);
+      else scan_u16_kernel<false><<<grid, U16_THREADS, 0, s>>>(a, m, nfull);
+      return;
+    }
     const bool g = lut_total > MX_STAGED_LUT_MAX;
     const size_t dyn = g ? 0 : sizeof(u32) * lut_total;
-    const int o = occ >= 8 ? 8 : (occ >= 6 ? 6 : 4);
-    const unsigned pgrid = (unsigned)std::min<long long>(nfull, (long long)n_sm * o);
-#define MX_FAST1_LAUNCH(O)                                                                        \
-  if (persist) {                                                                                  \
-    if (g) scan_fast1_kernel<SEGS, true, O><<<pgrid, S1_THREADS, dyn, s>>>(a, m, nfull);          \
-    else scan_fast1_kernel<SEGS, false, O><<<pgrid, S1_THREADS, dyn, s>>>(a, m, nfull);           \
-  } else {                                                                                        \
-    if (g) scan_fast_kernel<PC, SEGS, true, O><<<(unsigned)nfull, S1_THREADS, dyn, s>>>(a, m);    \
-    else scan_fast_kernel<PC, SEGS, false, O><<<(unsigned)nfull, S1_THREADS, dyn, s>>>(a, m);     \
-  }
-    if (o == 8) { MX_FAST1_LAUNCH(8) } else if (o == 6) { MX_FAST1_LAUNCH(6) } else { MX_FAST1_LAUNCH(4) }
-#undef MX_FAST1_LAUNCH
+    if (g) scan_fast_kernel<PC, SEGS, true, 8><<<(unsigned)nfull, S1_THREADS, dyn, s>>>(a, m);
+    else scan_fast_kernel<PC, SEGS, false, 8><<<(unsigned)nfull, S1_THREADS, dyn, s>>>(a, m);
     return;
   }
   if (lut_total > MX_STAGED_LUT_MAX)
@@ -1082,6 +1085,145 @@ int index_finalize(IndexData* ixp, long long I, cudaStream_t s) {
   MX_CUDA_TRY(mx_h2d(ix.blk_first.p + ix.n_blocks, &sI, sizeof(u32), s));
   MX_CUDA_TRY(mx_h2d(ix.key_blk_first.p + ix.n_keys, &sB, sizeof(u32), s));
   return MX_OK;
+}
+
+
+// ---------------------------------------------------------------- rows index
+// build_index(rows) (index.py:88-115) from explicit interval rows: LSD sort
+// by (key, file, start) with the staged radix passes (start digits, then
+// file, then key; each pass is stable), then one scan that rejects empty
+// rows and overlaps inside a (key, file) and merges adjacent rows
+// (_merge_intervals, index.py:32-47), then index_finalize.
+
+static int radix_sort_by(u32*& k, u32*& p0, u32*& p1, u32*& p2, u32*& k2, u32*& q0, u32*& q1, u32*& q2,
+                         long long n, int bits, u32* hist, u32* dtot, cudaStream_t s) {
+  constexpr int IT = 8;
+  const int tile = RS_THREADS * IT;
+  const int tiles = (int)((n + tile - 1) / tile);
+  const size_t smem = 4 * (size_t)tile * sizeof(u32);
+  for (int shift = 0; shift < bits; shift += 8) {
+    radix_upsweep2<IT><<<tiles, RS_THREADS, 0, s>>>(k, n, shift, hist, tiles);
+    mx_count_launch();
+    radix_rowscan<<<256, 256, 0, s>>>(hist, tiles, dtot);
+    mx_count_launch();
+    radix_downsweep2<IT><<<tiles, RS_THREADS, smem, s>>>(k, p0, p1, p2, k2, q0, q1, q2, n, shift, hist, dtot, tiles);
+    mx_count_launch();
+    MX_CUDA_TRY(cudaGetLastError());
+    std::swap(k, k2); std::swap(p0, q0); std::swap(p1, q1); std::swap(p2, q2);
+  }
+  return MX_OK;
+}
+
+static int bits_of(unsigned long long v) {
+  int b = 0;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+// rows sorted by (key, file, start): head = not adjacent to the previous row
+// of the same (key, file); empty rows / overlaps flag err (first row index)
+struct RowMergeF {
+  const u32 *key, *file, *start, *end;
+  long long n;
+  u32 *okey, *ofile, *ostart, *oend;
+  u64* count;
+  unsigned long long* bad;  // [0] = first empty row, [1] = first overlapping row
+  __device__ bool same(long long i) const { return i > 0 && key[i] == key[i - 1] && file[i] == file[i - 1]; }
+  __device__ u64 value(long long i) const { return !(same(i) && start[i] == end[i - 1]); }
+  __device__ void apply(long long i, u64 ex, u64 v) const {
+    if (end[i] <= start[i]) atomicMin(&bad[0], (unsigned long long)i);
+    if (same(i) && start[i] < end[i - 1]) atomicMin(&bad[1], (unsigned long long)i);
+    const long long pos = (long long)(ex + v) - 1;
+    if (v) {
+      okey[pos] = key[i];
+      ofile[pos] = file[i];
+      ostart[pos] = start[i];
+    }
+    if (i + 1 == n || value(i + 1)) oend[pos] = end[i];
+  }
+  __device__ void total(u64 t) const { *count = t; }
+};
+
+int rows_build(const mx_rows_desc* d, cudaStream_t s, IndexData* out) {
+  IndexData& ix = *out;
+  const long long n = d->n_rows;
+  ix.n_files = d->n_files;
+  ix.key_bits = d->key_bits;
+  MX_CUDA_TRY(ix.file_ds.alloc(std::max(1, d->n_files), s));
+  MX_CUDA_TRY(ix.file_ids.alloc(std::max(1, d->n_files), s));
+  if (d->n_files > 0) {
+    MX_CUDA_TRY(mx_h2d(ix.file_ds.p, d->file_ds, sizeof(int32_t) * d->n_files, s));
+    MX_CUDA_TRY(mx_h2d(ix.file_ids.p, d->file_ids, sizeof(long long) * d->n_files, s));
+  }
+  ix.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
+  ix.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
+  if (n == 0) {
+    ix.n_intervals = ix.n_keys = ix.n_blocks = 0;
+    return MX_OK;
+  }
+  DevBuf<u32> a[4], b[4], hist, dtot;
+  const u32* src[4] = {d->key, d->file, d->start, d->end};
+  for (int j = 0; j < 4; ++j) {
+    MX_CUDA_TRY(a[j].alloc(n, s));
+    MX_CUDA_TRY(b[j].alloc(n, s));
+    MX_CUDA_TRY(mx_h2d(a[j].p, src[j], sizeof(u32) * n, s));
+  }
+  u32 max_start = 0;
+  for (long long i = 0; i < n; ++i) max_start = std::max(max_start, d->start[i]);
+  const int tiles = (int)((n + RS_THREADS * 8 - 1) / (RS_THREADS * 8));
+  MX_CUDA_TRY(hist.alloc((long long)256 * tiles, s));
+  MX_CUDA_TRY(dtot.alloc(256, s));
+  MX_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(4 * RS_THREADS * 8 * sizeof(u32))));
+  u32 *k = a[0].p, *f = a[1].p, *st = a[2].p, *en = a[3].p;
+  u32 *k2 = b[0].p, *f2 = b[1].p, *st2 = b[2].p, *en2 = b[3].p;
+  // least significant field first: start, then file, then key
+  if (int rc = radix_sort_by(st, k, f, en, st2, k2, f2, en2, n, bits_of(max_start), hist.p, dtot.p, s)) return rc;
+  if (int rc = radix_sort_by(f, k, st, en, f2, k2, st2, en2, n, bits_of((u32)std::max(0, d->n_files - 1)), hist.p,
+                             dtot.p, s))
+    return rc;
+  if (int rc = radix_sort_by(k, f, st, en, k2, f2, st2, en2, n, (int)d->key_bits, hist.p, dtot.p, s)) return rc;
+  MX_CUDA_TRY(ix.iv_key.alloc(n, s));
+  MX_CUDA_TRY(ix.iv_file.alloc(n, s));
+  MX_CUDA_TRY(ix.iv_start.alloc(n, s));
+  MX_CUDA_TRY(ix.iv_end.alloc(n, s));
+  DevBuf<u64> tot;
+  DevBuf<unsigned long long> bad;
+  MX_CUDA_TRY(tot.alloc(1, s));
+  MX_CUDA_TRY(bad.alloc(2, s));
+  MX_CUDA_TRY(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long) * 2, s));
+  if (int rc = gs_run(n, RowMergeF{k, f, st, en, n, ix.iv_key.p, ix.iv_file.p, ix.iv_start.p, ix.iv_end.p, tot.p,
+                                   bad.p},
+                      s))
+    return rc;
+  u64 h_tot = 0;
+  unsigned long long h_bad[2];
+  {
+    D2HBatch rb(s);
+    MX_CUDA_TRY(rb.add(&h_tot, tot.p, sizeof(u64)));
+    MX_CUDA_TRY(rb.add(h_bad, bad.p, sizeof(h_bad)));
+    MX_CUDA_TRY(rb.sync());
+  }
+  for (int which = 0; which < 2; ++which) {
+    if (h_bad[which] == ~0ull) continue;
+    u32 row[4], prev_end = 0;
+    const long long i = (long long)h_bad[which];
+    const u32* srt[4] = {k, f, st, en};
+    for (int j = 0; j < 4; ++j) MX_CUDA_TRY(cudaMemcpy(&row[j], srt[j] + i, sizeof(u32), cudaMemcpyDeviceToHost));
+    const long long fid = (long long)d->file_ids[row[1]];
+    if (which == 0)
+      return mx_fail(MX_ERR_INDEX, "file %lld: empty interval [%u,%u)", fid, row[2], row[3]);
+    u32 prev_start = 0;
+    MX_CUDA_TRY(cudaMemcpy(&prev_start, st + i - 1, sizeof(u32), cudaMemcpyDeviceToHost));
+    MX_CUDA_TRY(cudaMemcpy(&prev_end, en + i - 1, sizeof(u32), cudaMemcpyDeviceToHost));
+    return mx_fail(MX_ERR_INDEX, "file %lld: overlapping intervals [%u,%u) and [%u,%u)", fid, prev_start, prev_end,
+                   row[2], row[3]);
+  }
+  const long long I = (long long)h_tot;
+  ix.n_samples_total = 0;
+  int rc = index_finalize(&ix, I, s);
+  ix.n_samples_total = ix.indexed_samples;
+  return rc;
 }
 
 }  // namespace mx

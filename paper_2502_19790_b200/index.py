@@ -333,6 +333,126 @@ class RangeCursor:
         self.remaining_total = sum(e - s for _, _, s, e in self._ranges) - consumed
 
 
+class RowsCodec:
+    """Key codec of an index built from explicit rows (``build_index``): one
+    field holding the key's 1-based rank in ``sort_key`` order, so the packed
+    order is the key order; the keys themselves are the caller's objects
+    (reference ``MixtureKey``s under the drop-in)."""
+
+    props = ["\0key"]
+
+    def __init__(self, keys: list):
+        self.keys = keys
+        self.key_bits = max(1, len(keys).bit_length())
+        if self.key_bits > 31:
+            raise NotImplementedError(f"{len(keys)} distinct keys (> 2^31 - 1)")
+        self.shift, self.width = [0], [self.key_bits]
+        self._memo = {}
+
+    def decode(self, packed: int):
+        return self.keys[int(packed) - 1]
+
+    def key_strings(self):
+        hit = self._memo.get("strings")
+        if hit is None:
+            blobs = [k.canonical_string().encode("utf-8") for k in self.keys]
+            off = np.zeros(len(blobs) + 1, dtype=np.int64)
+            off[1:] = np.cumsum([len(b) for b in blobs]) if blobs else []
+            hit = self._memo["strings"] = (b"".join(blobs), off, np.zeros(1, np.int32))
+        return hit
+
+    def allow_table(self, mkeys):
+        """Bit r of mixture key m = component key rank r matches m
+        (``mixtures.py:100-109``); bit 0 (no key) is never held."""
+        key = ("allow", tuple(tuple(getattr(k, "entries", ())) for k in mkeys))
+        hit = self._memo.get(key)
+        if hit is None:
+            words = (len(self.keys) + 1 + 31) // 32
+            bits = np.zeros((len(mkeys), words * 32), dtype=bool)
+            for m, mk in enumerate(mkeys):
+                bits[m, 1:len(self.keys) + 1] = [mk.matches(k) for k in self.keys]
+            table = np.packbits(bits.reshape(len(mkeys), words, 32)[:, :, ::-1], axis=2).view(">u4")
+            hit = (table.reshape(len(mkeys), words).astype(np.uint32), np.zeros(1, np.int32), words)
+            if len(self._memo) > 256:
+                self._memo.clear()
+            self._memo[key] = hit
+        return hit
+
+
+class _RowsSource:
+    """The "catalog" of a rows-built index: its file table and codec."""
+
+    def __init__(self, codec: RowsCodec, file_ds: np.ndarray, file_ids: np.ndarray, device):
+        self.codec = codec
+        self.file_ds = file_ds
+        self.file_ids = file_ids
+        self.device = device
+
+
+def build_index(rows, workers: int = 1, stream=None) -> ChunkerIndex:
+    """``build_index(rows, workers)`` (``index.py:88-115``) on the GPU.
+
+    ``rows`` are ``IntervalRow``-like objects (``dataset_id, file_id, key,
+    start, end``) or a device ``ChunkerIndex`` (returned as is: the catalog
+    seam already built it). Rows are packed into flat arrays (the one host
+    pass over the caller's Python objects), then sorted by (key, file,
+    start), checked (empty / overlapping -> ``IndexBuildError``) and merged
+    on the device. ``workers`` is accepted for signature parity; the result
+    never depends on it (nor on the row order)."""
+    import torch
+
+    if isinstance(rows, ChunkerIndex):
+        return rows
+    rows = list(rows)
+    keyset = {}
+    for r in rows:
+        keyset.setdefault(r.key, None)
+    keys = sorted(keyset, key=MixtureKey.sort_key)
+    rank = {k: i + 1 for i, k in enumerate(keys)}
+    n = len(rows)
+    ds = np.fromiter((r.dataset_id for r in rows), dtype=np.int64, count=n)
+    fid = np.fromiter((r.file_id for r in rows), dtype=np.int64, count=n)
+    st = np.fromiter((r.start for r in rows), dtype=np.int64, count=n)
+    en = np.fromiter((r.end for r in rows), dtype=np.int64, count=n)
+    kr = np.fromiter((rank[r.key] for r in rows), dtype=np.uint32, count=n)
+    if n and (min(st.min(), en.min()) < 0 or max(st.max(), en.max()) >= 1 << 32):
+        raise NotImplementedError("interval bounds outside [0, 2^32)")
+    if n and (ds.min() < -(1 << 31) or ds.max() >= 1 << 31):
+        raise NotImplementedError("dataset ids outside int32")
+    pairs = np.unique(np.stack([ds, fid], axis=1), axis=0) if n else np.zeros((0, 2), np.int64)
+    file_ix = np.zeros(n, dtype=np.uint32)
+    if n:  # index of (ds, fid) in the (ds, fid)-sorted file table
+        order = np.lexsort((fid, ds))
+        brk = np.ones(n, dtype=bool)
+        brk[1:] = (ds[order][1:] != ds[order][:-1]) | (fid[order][1:] != fid[order][:-1])
+        file_ix[order] = (np.cumsum(brk) - 1).astype(np.uint32)
+    codec = RowsCodec(keys)
+    f_ds = np.ascontiguousarray(pairs[:, 0], dtype=np.int32)
+    f_ids = np.ascontiguousarray(pairs[:, 1], dtype=np.int64)
+    blob, soff, _ = codec.key_strings()
+    keep = dict(k=kr, f=file_ix, s=np.ascontiguousarray(st, np.uint32), e=np.ascontiguousarray(en, np.uint32),
+                blob=np.frombuffer(blob, dtype=np.uint8).copy() if blob else np.zeros(1, np.uint8), soff=soff)
+    P = C.POINTER
+    d = _lib.RowsDesc()
+    d.n_rows = n
+    d.key = keep["k"].ctypes.data_as(P(C.c_uint32))
+    d.file = keep["f"].ctypes.data_as(P(C.c_uint32))
+    d.start = keep["s"].ctypes.data_as(P(C.c_uint32))
+    d.end = keep["e"].ctypes.data_as(P(C.c_uint32))
+    d.n_files = len(f_ds)
+    d.file_ds = f_ds.ctypes.data_as(P(C.c_int32))
+    d.file_ids = f_ids.ctypes.data_as(P(C.c_int64))
+    d.n_keys = len(keys)
+    d.key_bits = codec.key_bits
+    d.key_strings = keep["blob"].ctypes.data_as(P(C.c_uint8))
+    d.key_string_offsets = keep["soff"].ctypes.data_as(P(C.c_int64))
+    L = _lib.lib()
+    out = C.c_void_p()
+    _lib.check(L.mx_index_build_rows(C.byref(d), C.c_void_p(_lib.stream_ptr(stream)), C.byref(out)))
+    src = _RowsSource(codec, f_ds, f_ids, torch.device("cuda", torch.cuda.current_device()))
+    return ChunkerIndex(out.value, src, stream)
+
+
 def build_index_from_catalog(catalog, predicates: Sequence = (), stream=None) -> ChunkerIndex:
     """Fused filter + intervals + index on the GPU.
 

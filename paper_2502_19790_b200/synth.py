@@ -158,3 +158,17 @@ def cfg2_mixture(chunk_size: int = 1024):
         },
         chunk_size,
     )
+
+
+def cfg5_mixture(keys, chunk_size: int = 1024):
+    """cfg 5's static best-effort mixture: every realized key,
+    weights proportional to Zipf(0.8) ranks in a seeded shuffled order, so
+    weights differ from the data shares and keys deplete one by one. ``keys``
+    are the index's component keys in key order."""
+    from .mixtures import MixtureSpec
+
+    rng = np.random.Generator(np.random.PCG64(5))
+    w = 1.0 / np.arange(1, len(keys) + 1) ** 0.8
+    w = w[rng.permutation(len(keys))]
+    w = w / w.sum()
+    return MixtureSpec({k: float(x) for k, x in zip(keys, w)}, chunk_size)
