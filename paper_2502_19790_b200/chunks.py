@@ -31,7 +31,12 @@ _CHUNK_VERSION = 1
 RangeMap = dict  # MixtureKey -> {ds: {fid: [(start, end)]}}
 
 
-class Chunk:
+class _ChunkBase:
+    """Placeholder base: ``dropin.install`` swaps it for the reference's
+    ``Chunk`` (a class whose only base is ``object`` cannot be re-based)."""
+
+
+class Chunk(_ChunkBase):
     """Sample pointers of one chunk + its mixture snapshot (``chunks.py:26-106``)."""
 
     def __init__(self, chunk_id: int, data: RangeMap, seed: int, mixture: MixtureSpec | None = None):

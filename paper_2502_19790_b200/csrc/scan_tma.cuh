@@ -1,17 +1,18 @@
 // Stage-1 streaming pass (included by stage1.cu).
 //
-// Two launch shapes share one tile body (`finish_tile`):
-//  * scan_direct_kernel -- one CTA per 4096-sample tile; every 128-bit column
-//    load of a thread is issued up front; thousands of independent CTAs keep
-//    HBM busy through occupancy.
-//  * scan_pipe_kernel   -- persistent CTAs, each owning a ring of shared-memory
-//    slots filled by cp.async.bulk (TMA bulk copies, SASS UBLKCP) completing
-//    on mbarriers, so the next tiles' column bytes stream in while the current
-//    tile is keyed.
-// Both write each tile's runs into the tile's own slot region (tile-local
+// Per-property int32 columns (and wide tuple codes): one CTA per 2048-sample
+// tile, every 128-bit column load of a thread issued up front; thousands of
+// independent CTAs keep HBM busy through occupancy.
+//  * scan_fast_kernel   -- full tiles with <= 4 file starts (fast_tile);
+//  * scan_list_kernel   -- the tiles it deferred (more file starts);
+//  * scan_direct_kernel -- everything else (finish_tile).
+// All write each tile's runs into the tile's own slot region (tile-local
 // scan, no inter-tile dependency); run ends that fall into a later tile are
 // patched by slot_fixup_kernel and slot_compact_kernel densifies the records.
-// Per-tile file bookkeeping comes precomputed from tile_meta_kernel.
+// Per-tile file bookkeeping comes precomputed from tile_meta_kernel. (The
+// persistent cp.async.bulk / mbarrier ring variant measured slower than
+// occupancy here -- 2.1 vs 0.65 ms at cfg2 -- and was removed; see git
+// history and DESIGN.md.)
 #pragma once
 
 namespace mx {
@@ -42,36 +43,6 @@ __global__ void tile_meta_kernel(S1Args a, long long tile_len, long long ntiles,
   meta[t] = m;
 }
 
-__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_tx(u64* bar, u32 bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "MX_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra MX_WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-constexpr int TMA_MAX_STAGES = 4;
 constexpr int TMA_FILE_CAP = 256;
 
 struct TileScratch {  // per-CTA shared scratch of one tile
@@ -543,169 +514,6 @@ scan_fast_kernel(S1Args a, const TileMeta* __restrict__ meta) {
   u32 st[SEGS][4];
   lut_sums<PC, SEGS, GLUT>(s_lut, a, v, st);
   fast_tile<SEGS>(a, m, tile, st, sc, s_fs);
-}
-
-// persistent CTAs, every full tile's columns + metadata streamed into a ring
-// of shared-memory slots by cp.async.bulk (TMA); same tile body
-template <int PC>
-__global__ void __launch_bounds__(S1_THREADS, 1)
-scan_fast_pipe_kernel(S1Args a, const TileMeta* __restrict__ meta, long long nfull, int stages, int lut_bytes) {
-  constexpr int TILE = S1_THREADS * 16;
-  extern __shared__ __align__(128) unsigned char dyn[];
-  u32* s_lut = reinterpret_cast<u32*>(dyn);
-  int32_t* s_codes = reinterpret_cast<int32_t*>(dyn + lut_bytes);  // [stages][PC][TILE]
-  TileMeta* s_meta = reinterpret_cast<TileMeta*>(s_codes + (long long)stages * PC * TILE);
-  __shared__ __align__(8) u64 s_bar[TMA_MAX_STAGES];
-  __shared__ long long s_tile[TMA_MAX_STAGES];
-  __shared__ TileScratch sc;
-  __shared__ int s_fs[FAST_MAX_FS];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < a.lut_off[PC]; i += S1_THREADS) s_lut[i] = a.lut_sum[i];
-  auto issue = [&](int s) {  // thread 0: claim the next full tile into slot s
-    const long long t = (long long)atomicAdd(a.tile_ctr, 1u);
-    s_tile[s] = t;
-    if (t < nfull) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_tx(&s_bar[s], (u32)(PC * TILE * 4 + sizeof(TileMeta)));
-#pragma unroll
-      for (int p = 0; p < PC; ++p)
-        bulk_g2s(s_codes + ((long long)s * PC + p) * TILE, a.cols[p] + t * TILE, TILE * 4, &s_bar[s]);
-      bulk_g2s(&s_meta[s], meta + t, sizeof(TileMeta), &s_bar[s]);
-    }
-  };
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < stages; ++s) issue(s);
-  }
-  __syncthreads();
-  const int lw = warp * 512 + 4 * lane;
-  for (int it = 0;; ++it) {
-    const int s = it % stages;
-    const long long tile = s_tile[s];
-    if (tile >= nfull) break;
-    mbar_wait(&s_bar[s], (u32)((it / stages) & 1));
-    const TileMeta m = s_meta[s];
-    if (m.nf > FAST_MAX_FS) {
-      if (tid == 0) a.defer_list[atomicAdd(a.defer_cnt, 1u)] = (u32)tile;
-    } else {
-      int4 v[PC][4];
-      const int32_t* c = s_codes + (long long)s * PC * TILE + lw;
-#pragma unroll
-      for (int p = 0; p < PC; ++p)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[p][j] = *reinterpret_cast<const int4*>(c + p * TILE + 128 * j);
-      if (tid < FAST_MAX_FS)
-        s_fs[tid] = tid < m.nf ? (int)(a.file_off[m.fa + 1 + tid] - tile * TILE) : 1 << 30;
-      u32 st[4][4];
-      lut_sums<PC, 4>(s_lut, a, v, st);
-      __syncthreads();  // s_fs
-      fast_tile<4>(a, m, tile, st, sc, s_fs);
-    }
-    __syncthreads();  // slot s and the tile scratch are free again
-    if (tid == 0) issue(s);
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Persistent CTAs with a TMA ring (cp.async.bulk + mbarrier). Tiles are
-// claimed in increasing order from an atomic counter; slot s of the ring holds
-// every column's tile plus the tile's metadata. Requires the shared-memory LUT
-// and 16-byte aligned columns; the (partial) last tile is read directly.
-template <int SEGS, int PC>
-__global__ void __launch_bounds__(S1_THREADS, 2)
-scan_pipe_kernel(S1Args a, const TileMeta* __restrict__ meta, long long ntiles, long long nstaged, int stages,
-                 int lut_bytes) {
-  constexpr int WT = 32 * 4 * SEGS;
-  constexpr int TILE = (S1_THREADS / 32) * WT;
-  constexpr bool SUMF = PC > 0;
-  extern __shared__ __align__(128) unsigned char dyn[];
-  u32* s_lut = reinterpret_cast<u32*>(dyn);
-  const int P = PC > 0 ? PC : a.n_props;
-  int32_t* s_codes = reinterpret_cast<int32_t*>(dyn + lut_bytes);  // [stages][P][TILE]
-  TileMeta* s_meta = reinterpret_cast<TileMeta*>(s_codes + (long long)stages * P * TILE);
-  __shared__ __align__(8) u64 s_bar[TMA_MAX_STAGES];
-  __shared__ long long s_tile[TMA_MAX_STAGES];
-  __shared__ TileScratch sc;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  {
-    const u32* src = SUMF ? a.lut_sum : a.lut;
-    for (int i = tid; i < a.lut_off[P]; i += S1_THREADS) s_lut[i] = src[i];
-  }
-  auto issue = [&](int s) {  // thread 0: claim the next tile into slot s
-    const long long t = (long long)atomicAdd(a.tile_ctr, 1u);
-    s_tile[s] = t;
-    if (t < nstaged) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_tx(&s_bar[s], (u32)(P * TILE * 4 + sizeof(TileMeta)));
-      for (int p = 0; p < P; ++p)
-        bulk_g2s(s_codes + ((long long)s * P + p) * TILE, a.cols[p] + t * TILE, TILE * 4, &s_bar[s]);
-      bulk_g2s(&s_meta[s], meta + t, sizeof(TileMeta), &s_bar[s]);
-    }
-  };
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < stages; ++s) issue(s);
-  }
-  __syncthreads();
-  for (int it = 0;; ++it) {
-    const int s = it % stages;
-    const long long tile = s_tile[s];
-    if (tile >= ntiles) break;
-    const bool staged = tile < nstaged;
-    if (staged) mbar_wait(&s_bar[s], (u32)((it / stages) & 1));
-    const TileMeta m = staged ? s_meta[s] : meta[tile];
-    const long long wbase = tile * TILE + (long long)warp * WT;
-    u32 st[SEGS][4], anyf[SEGS][4];
-#pragma unroll
-    for (int j = 0; j < SEGS; ++j)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) st[j][q] = anyf[j][q] = 0;
-    for (int p = 0; p < P; ++p) {
-      const int lo = a.lut_off[p] + 1;
-      if (staged) {
-        const int32_t* c = s_codes + ((long long)s * P + p) * TILE + warp * WT + 4 * lane;
-#pragma unroll
-        for (int j = 0; j < SEGS; ++j) {
-          const int4 v = *reinterpret_cast<const int4*>(c + 128 * j);
-          const u32 e[4] = {s_lut[lo + v.x], s_lut[lo + v.y], s_lut[lo + v.z], s_lut[lo + v.w]};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (SUMF) {
-              st[j][q] += e[q];
-            } else {
-              st[j][q] += e[q] & ~FAIL;
-              anyf[j][q] |= e[q];
-            }
-          }
-        }
-      } else {
-        const int32_t* col = a.cols[p];
-#pragma unroll
-        for (int j = 0; j < SEGS; ++j)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const long long i = wbase + 128 * j + 4 * lane + q;
-            if (i < a.n) {
-              const u32 e = s_lut[lo + col[i]];
-              if (SUMF) {
-                st[j][q] += e;
-              } else {
-                st[j][q] += e & ~FAIL;
-                anyf[j][q] |= e;
-              }
-            }
-          }
-      }
-    }
-    normalise_status<SUMF, SEGS>(a, wbase, st, anyf);
-    finish_tile<SEGS>(a, m, tile, wbase, st, sc);
-    __syncthreads();  // slot s and the tile scratch are free again
-    if (tid == 0) issue(s);
-    __syncthreads();
-  }
 }
 
 // Dense copy of the slot records (one warp per tile, order preserved).

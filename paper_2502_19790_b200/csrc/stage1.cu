@@ -3,21 +3,22 @@
 // Replaces MetadataCatalog.filter_intervals (catalog.py:549-605) +
 // build_index (index.py:88-115) with three device passes:
 //
-//  1. scan_runs_kernel: ONE streaming pass over the int32 code columns.
-//     Per sample: code -> (packed key contribution | filter-fail bit) via a
+//  1. ONE streaming pass over the code column(s) (scan_u16.cuh for a u16
+//     row-tuple column, scan_tma.cuh for per-property int32 columns). Per
+//     sample: code -> (packed key contribution | filter-fail flag) via a
 //     shared-memory LUT, sum over properties = order-preserving packed key
-//     (codec.py explains the layout), run boundaries from neighbour compares
-//     (__shfl_up/down across lanes, shared memory across warps, direct halo
-//     loads across tiles), file boundaries from the tile's file-start list.
-//     Run starts are compacted with a warp byte-packed scan + block scan +
-//     decoupled look-back, and written as SoA interval records
-//     (key, file, start, end) in (file, start) order.
+//     (codec.py explains the layout), run boundaries from neighbour compares,
+//     file boundaries from the tile's file-start list. Runs are compacted
+//     tile-locally into per-tile slot regions as SoA interval records
+//     (key, file, start, end) in (file, start) order; slot_fixup_kernel
+//     closes runs that cross tiles and slot_compact_kernel densifies them.
 //  2. an LSD radix sort of the records by packed key (8-bit digits, stable
 //     warp-multisplit ranking) -> (key, file, start) order. The packed key is
 //     order-preserving, so this IS MixtureKey.sort_key order (index.py:50-55
 //     component_keys()).
-//  3. two look-back scans: key/block boundary flags -> dense key ranks and
-//     (key, file) block ids; interval lengths -> u64 cumulative samples.
+//  3. two reduce-then-scan passes (scan.cuh): key/block boundary flags ->
+//     dense key ranks and (key, file) block ids; interval lengths -> u64
+//     cumulative samples.
 //
 // Algorithmic bytes: B1 = N*sum(w_p) + 16*I + 8*B_kf + 16*K.
 #include <stdlib.h>
@@ -104,220 +105,6 @@ __device__ __forceinline__ int upper_bound_ll(const long long* v, int n, long lo
   return lo;
 }
 
-template <bool SMEM_LUT>
-__global__ void __launch_bounds__(S1_THREADS)
-scan_runs_kernel(S1Args a) {
-  extern __shared__ u32 s_lut[];
-  __shared__ long long s_fstart[S1_FILE_CAP];
-  __shared__ int s_fa, s_nf, s_overflow, s_tile;
-  __shared__ long long s_fbase;
-  __shared__ u32 s_warp_first[S1_THREADS / 32], s_warp_last[S1_THREADS / 32];
-  __shared__ u32 s_warp_tot[S1_THREADS / 32];
-  __shared__ u64 s_tile_excl;
-  __shared__ u32 s_halo_prev, s_halo_next;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (SMEM_LUT) {
-    for (int i = tid; i < a.lut_off[a.n_props]; i += S1_THREADS) s_lut[i] = a.lut[i];
-  }
-  if (tid == 0) s_tile = atomicAdd(a.tile_ctr, 1u);
-  __syncthreads();
-  const int tile = s_tile;
-  const long long t0 = (long long)tile * S1_TILE;
-
-  // file starts inside (t0, t0 + TILE]
-  if (tid == 0) {
-    int fa = upper_bound_ll(a.file_off, a.n_files + 1, t0) - 1;
-    if (fa >= a.n_files) fa = a.n_files - 1;
-    s_fa = fa;
-    s_fbase = a.file_off[fa];
-    s_halo_prev = sample_status<SMEM_LUT>(a, s_lut, t0 - 1);
-    s_halo_next = sample_status<SMEM_LUT>(a, s_lut, t0 + S1_TILE);
-  }
-  __syncthreads();
-  const int fa = s_fa;
-  for (int k = tid; k < S1_FILE_CAP; k += S1_THREADS) {
-    int f = fa + 1 + k;
-    s_fstart[k] = f <= a.n_files ? a.file_off[f] : (1ll << 62);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int m = upper_bound_ll(s_fstart, S1_FILE_CAP, t0 + S1_TILE);
-    s_nf = m;
-    s_overflow = (m == S1_FILE_CAP) ? 1 : 0;
-  }
-  __syncthreads();
-  const int nf = s_nf;
-  const bool overflow = s_overflow;
-
-  // ---- load codes (coalesced int4 per lane per segment) and build status
-  const long long wbase = t0 + (long long)warp * S1_WARP;
-  u32 st[S1_SEGS][4];
-#pragma unroll
-  for (int j = 0; j < S1_SEGS; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) st[j][q] = 0;
-  u32 anyf[S1_SEGS][4];
-#pragma unroll
-  for (int j = 0; j < S1_SEGS; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) anyf[j][q] = 0;
-  const bool full = wbase + S1_WARP <= a.n;
-  for (int p = 0; p < a.n_props; ++p) {
-    const int lo = a.lut_off[p] + 1;
-    if (full) {
-      int4 v[S1_SEGS];
-#pragma unroll
-      for (int j = 0; j < S1_SEGS; ++j)
-        v[j] = codes4(a, p, wbase + 128 * j + 4 * lane);
-#pragma unroll
-      for (int j = 0; j < S1_SEGS; ++j) {
-        u32 e0 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v[j].x);
-        u32 e1 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v[j].y);
-        u32 e2 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v[j].z);
-        u32 e3 = lut_get<SMEM_LUT>(s_lut, a.lut, lo + v[j].w);
-        st[j][0] += e0 & ~FAIL; anyf[j][0] |= e0;
-        st[j][1] += e1 & ~FAIL; anyf[j][1] |= e1;
-        st[j][2] += e2 & ~FAIL; anyf[j][2] |= e2;
-        st[j][3] += e3 & ~FAIL; anyf[j][3] |= e3;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < S1_SEGS; ++j)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          long long i = wbase + 128 * j + 4 * lane + q;
-          if (i < a.n) {
-            u32 e = lut_get<SMEM_LUT>(s_lut, a.lut, lo + code_at(a, p, i));
-            st[j][q] += e & ~FAIL;
-            anyf[j][q] |= e;
-          }
-        }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < S1_SEGS; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      long long i = wbase + 128 * j + 4 * lane + q;
-      st[j][q] = (i < a.n) ? ((anyf[j][q] & FAIL) | st[j][q]) : FAIL;
-    }
-
-  // ---- neighbours across warps
-  if (lane == 0) s_warp_first[warp] = st[0][0];
-  if (lane == 31) s_warp_last[warp] = st[S1_SEGS - 1][3];
-  __syncthreads();
-  const u32 warp_prev = warp == 0 ? s_halo_prev : s_warp_last[warp - 1];
-  const u32 warp_next = warp == S1_THREADS / 32 - 1 ? s_halo_next : s_warp_first[warp + 1];
-
-  // ---- file membership per sample
-  auto fstart_of = [&](int f) -> long long {
-    if (overflow) return a.file_off[f];
-    return f == fa ? s_fbase : s_fstart[f - fa - 1];
-  };
-  auto file_of = [&](long long i) -> int {
-    if (overflow) {
-      int f = upper_bound_ll(a.file_off, a.n_files + 1, i) - 1;
-      return f;
-    }
-    return fa + upper_bound_ll(s_fstart, nf, i);
-  };
-
-  u32 starts[S1_SEGS], ends[S1_SEGS];
-  int fidx[S1_SEGS][4];
-#pragma unroll
-  for (int j = 0; j < S1_SEGS; ++j) {
-    u32 prev_last = __shfl_up_sync(MX_FULL, st[j][3], 1);
-    u32 next_first = __shfl_down_sync(MX_FULL, st[j][0], 1);
-    u32 seg_prev = __shfl_sync(MX_FULL, st[j > 0 ? j - 1 : 0][3], 31);
-    u32 seg_next = __shfl_sync(MX_FULL, st[j < S1_SEGS - 1 ? j + 1 : 0][0], 0);
-    if (lane == 0) prev_last = j == 0 ? warp_prev : seg_prev;
-    if (lane == 31) next_first = j == S1_SEGS - 1 ? warp_next : seg_next;
-    const long long i0 = wbase + 128 * j + 4 * lane;
-    int f = file_of(i0);
-    u32 sm = 0, em = 0;
-    bool fs_cur = (i0 < a.n) && fstart_of(f) == i0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const long long i = i0 + q;
-      fidx[j][q] = f;
-      const u32 cur = st[j][q];
-      const u32 prv = q == 0 ? prev_last : st[j][q - 1];
-      const u32 nxt = q == 3 ? next_first : st[j][q + 1];
-      // does sample i+1 start a new file?
-      bool fs_next;
-      int fn = f;
-      if (overflow) {
-        fn = (i + 1 < a.n) ? file_of(i + 1) : f;
-        fs_next = (i + 1 < a.n) && fstart_of(fn) == i + 1;
-      } else {
-        int k = f - fa;  // index into s_fstart of the next file start
-        fs_next = k < nf && s_fstart[k] == i + 1;
-        if (fs_next) fn = f + 1;
-        // skip empty files (duplicate offsets)
-        while (fs_next && fn - fa < nf && s_fstart[fn - fa] == i + 1) ++fn;
-      }
-      const bool pass = !(cur & FAIL);
-      const bool start = pass && (fs_cur || (prv & FAIL) || prv != cur);
-      const bool end = pass && (fs_next || (nxt & FAIL) || nxt != cur);
-      sm |= (u32)start << q;
-      em |= (u32)end << q;
-      fs_cur = fs_next;
-      f = fn;
-    }
-    starts[j] = sm;
-    ends[j] = em;
-  }
-
-  // ---- compaction: byte-packed per-segment counts, warp scan, block scan
-  u32 pack = 0;
-#pragma unroll
-  for (int j = 0; j < S1_SEGS; ++j) pack |= (u32)__popc(starts[j]) << (8 * j);
-  const u32 incl = warp_incl_scan(pack);
-  const u32 excl = incl - pack;
-  const u32 wtot = __shfl_sync(MX_FULL, incl, 31);
-  u32 seg_base[S1_SEGS];
-  u32 acc = 0;
-#pragma unroll
-  for (int j = 0; j < S1_SEGS; ++j) {
-    seg_base[j] = acc + ((excl >> (8 * j)) & 0xff);
-    acc += (wtot >> (8 * j)) & 0xff;
-  }
-  if (lane == 0) s_warp_tot[warp] = acc;
-  __syncthreads();
-  if (warp == 0) {
-    u32 v = lane < S1_THREADS / 32 ? s_warp_tot[lane] : 0;
-    u32 inc = warp_incl_scan(v);
-    u32 tile_agg = __shfl_sync(MX_FULL, inc, 31);
-    if (lane < S1_THREADS / 32) s_warp_tot[lane] = inc - v;
-    u64 tex = lookback_exclusive(a.status, tile, tile_agg);
-    if (lane == 0) {
-      s_tile_excl = tex;
-      if ((long long)(tile + 1) * S1_TILE >= a.n) *a.n_runs = tex + tile_agg;
-    }
-  }
-  __syncthreads();
-  const u64 base = s_tile_excl + s_warp_tot[warp];
-
-  // ---- emit records
-#pragma unroll
-  for (int j = 0; j < S1_SEGS; ++j) {
-    u64 run = base + seg_base[j];  // number of run starts before this thread's segment j
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const long long i = wbase + 128 * j + 4 * lane + q;
-      if ((starts[j] >> q) & 1) {
-        const u32 key = st[j][q];
-        a.rec_key[run] = key;
-        a.rec_file[run] = (u32)fidx[j][q];
-        a.rec_start[run] = (u32)(i - fstart_of(fidx[j][q]));
-        if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)i);
-        ++run;
-      }
-      if ((ends[j] >> q) & 1) a.rec_end[run - 1] = (u32)(i + 1 - fstart_of(fidx[j][q]));
-    }
-  }
-}
 
 }  // namespace mx
 
@@ -328,28 +115,8 @@ namespace mx {
 
 // ---------------------------------------------------------------- radix sort
 constexpr int RS_THREADS = 256;
-constexpr int RS_ITEMS = 4;  // small tiles: enough CTAs for ~1M-record sorts
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096, warp-striped
 constexpr int RS_WARPS = RS_THREADS / 32;
 
-__global__ void __launch_bounds__(RS_THREADS)
-radix_upsweep(const u32* keys, long long n, int shift, u32* hist, int ntiles, const u32* seg_cnt) {
-  // seg_cnt != null: tile b's elements are the first seg_cnt[b] slots of
-  // [b*RS_TILE, (b+1)*RS_TILE) (stage-1 slot output); else dense [0, n)
-  __shared__ u32 h[256];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  h[tid] = 0;
-  __syncthreads();
-  const long long lim = seg_cnt ? (long long)blockIdx.x * RS_TILE + seg_cnt[blockIdx.x] : n;
-  const long long base = (long long)blockIdx.x * RS_TILE + warp * (32 * RS_ITEMS);
-#pragma unroll 4
-  for (int k = 0; k < RS_ITEMS; ++k) {
-    long long i = base + k * 32 + lane;
-    if (i < lim) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
-  }
-  __syncthreads();
-  hist[(long long)tid * ntiles + blockIdx.x] = h[tid];
-}
 
 // one CTA per digit: exclusive scan of its row across tiles, row total out
 __global__ void __launch_bounds__(256)
@@ -391,73 +158,6 @@ radix_rowscan(u32* hist, int ntiles, u32* digit_tot) {
   if (tid == 0) digit_tot[blockIdx.x] = s_carry;
 }
 
-__global__ void __launch_bounds__(RS_THREADS)
-radix_downsweep(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2in,
-                u32* kout, u32* p0out, u32* p1out, u32* p2out,
-                long long n, int shift, const u32* hist, const u32* digit_tot, int ntiles,
-                const u32* seg_cnt) {
-  __shared__ u32 s_base[256];
-  const long long lim = seg_cnt ? (long long)blockIdx.x * RS_TILE + seg_cnt[blockIdx.x] : n;
-  __shared__ u32 s_wcnt[RS_WARPS][256];
-  __shared__ u32 s_w[8];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  {  // digit bases = exclusive scan of digit totals + this tile's row prefix
-    u32 x = digit_tot[tid];
-    u32 inc = warp_incl_scan(x);
-    if (lane == 31) s_w[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-      u32 y = lane < 8 ? s_w[lane] : 0;
-      u32 yi = warp_incl_scan(y);
-      if (lane < 8) s_w[lane] = yi - y;
-    }
-    __syncthreads();
-    s_base[tid] = s_w[warp] + inc - x + hist[(long long)tid * ntiles + blockIdx.x];
-  }
-#pragma unroll
-  for (int w = 0; w < RS_WARPS; ++w) s_wcnt[w][tid] = 0;
-  __syncthreads();
-  const long long base = (long long)blockIdx.x * RS_TILE + warp * (32 * RS_ITEMS);
-  u32 key[RS_ITEMS];
-  u32 rank[RS_ITEMS];
-#pragma unroll
-  for (int k = 0; k < RS_ITEMS; ++k) {
-    long long i = base + k * 32 + lane;
-    bool ok = i < lim;
-    key[k] = ok ? kin[i] : 0;
-    u32 d = (key[k] >> shift) & 0xff;
-    u32 peers = __match_any_sync(MX_FULL, ok ? d : 0x100u);
-    u32 before = __popc(peers & ((1u << lane) - 1));
-    u32 cur = s_wcnt[warp][d & 0xff];
-    __syncwarp();
-    rank[k] = cur + before;
-    if (ok && before == 0) s_wcnt[warp][d] = cur + __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  {  // per digit: exclusive scan over warps
-    u32 run = 0;
-#pragma unroll
-    for (int w = 0; w < RS_WARPS; ++w) {
-      u32 c = s_wcnt[w][tid];
-      s_wcnt[w][tid] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < RS_ITEMS; ++k) {
-    long long i = base + k * 32 + lane;
-    if (i < lim) {
-      u32 d = (key[k] >> shift) & 0xff;
-      u32 dst = s_base[d] + s_wcnt[warp][d] + rank[k];
-      kout[dst] = key[k];
-      p0out[dst] = p0in[i];
-      p1out[dst] = p1in[i];
-      p2out[dst] = p2in[i];
-    }
-  }
-}
 
 // Staged variant: 4096-record tiles (RS2_ITEMS 16; 8 = 2048); records are first placed at their
 // tile-local sorted position in shared memory (64 KB), then written out in
@@ -581,30 +281,7 @@ radix_downsweep2(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2
 }
 
 // ---------------------------------------------------------------- host side
-template <int SEGS, int PC>
-static int launch_pipe(const S1Args& a, const TileMeta* m, long long ntiles, long long nstaged, int stages,
-                       int lut_bytes, int n_sm, cudaStream_t s) {
-  auto kernel = scan_pipe_kernel<SEGS, PC>;
-  const size_t dyn = lut_bytes + (size_t)stages * a.n_props * (32 * 4 * SEGS * (S1_THREADS / 32)) * 4 +
-                     (size_t)stages * sizeof(TileMeta);
-  MX_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-  int occ = 1;
-  MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, S1_THREADS, dyn));
-  const long long grid = std::min<long long>(ntiles, (long long)n_sm * std::max(occ, 1));
-  kernel<<<(unsigned)grid, S1_THREADS, dyn, s>>>(a, m, ntiles, nstaged, stages, lut_bytes);
-  return MX_OK;
-}
 
-template <int SEGS>
-static int dispatch_pipe(const S1Args& a, const TileMeta* m, long long ntiles, long long nstaged, int stages,
-                         int lut_bytes, int n_sm, cudaStream_t s) {
-  switch (a.lut_sum ? a.n_props : 0) {
-    case 2: return launch_pipe<SEGS, 2>(a, m, ntiles, nstaged, stages, lut_bytes, n_sm, s);
-    case 3: return launch_pipe<SEGS, 3>(a, m, ntiles, nstaged, stages, lut_bytes, n_sm, s);
-    case 5: return launch_pipe<SEGS, 5>(a, m, ntiles, nstaged, stages, lut_bytes, n_sm, s);
-    default: return launch_pipe<SEGS, 0>(a, m, ntiles, nstaged, stages, lut_bytes, n_sm, s);
-  }
-}
 
 template <int SEGS, int PC>
 static void launch_direct(const S1Args& a, const TileMeta* m, long long ntiles, bool smem_lut, int lut_total,
@@ -621,43 +298,7 @@ static void launch_direct(const S1Args& a, const TileMeta* m, long long ntiles, 
 template <int PC, int SEGS>
 static void launch_fast(const S1Args& a, const TileMeta* m, long long nfull, int lut_total, cudaStream_t s) {
   if (nfull <= 0) return;
-  const char* env = getenv("MX_SCAN");
-  if (SEGS == 4 && env && !strcmp(env, "fastpipe") && !a.u16) {  // persistent + TMA ring variant
-    int dev = 0, n_sm = 148, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const int lut_bytes = (lut_total * 4 + 127) / 128 * 128;
-    const int stage = PC * S1_THREADS * 16 * 4 + (int)sizeof(TileMeta);
-    const int stages = std::min(TMA_MAX_STAGES, (optin - 16 * 1024 - lut_bytes) / stage);
-    const size_t dyn = lut_bytes + (size_t)stages * stage;
-    auto kernel = scan_fast_pipe_kernel<PC>;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    kernel<<<(unsigned)std::min<long long>(nfull, n_sm), S1_THREADS, dyn, s>>>(a, m, nfull, stages, lut_bytes);
-    return;
-  }
   if constexpr (PC == 1 && SEGS == 2) {
-    if (a.u16 && (reinterpret_cast<uintptr_t>(a.cols[0]) % 16) == 0) {
-      // one u16 code column (row-tuple layout): change-driven persistent
-      // kernel (scan_u16.cuh), LUT staged per CTA when it fits
-      int dev = 0, n_sm = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-      const int entries = lut_total - 1;
-      const bool slut = entries <= U16_SMEM_LUT_MAX;
-      const size_t dyn = slut ? sizeof(u32) * (size_t)entries : 0;
-      int per_sm = 8;
-      if (slut) {
-        cudaFuncSetAttribute(scan_u16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<true>, U16_THREADS, dyn);
-      } else {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<false>, U16_THREADS, 0);
-      }
-      const unsigned grid = (unsigned)std::min<long long>(nfull, (long long)n_sm * std::max(1, per_sm));
-      if (slut) scan_u16_kernel<true><<<grid, U16_THREADS, dyn, s>>>(a, m, nfull);
-      else scan_u16_kernel<false><<<grid, U16_THREADS, 0, s>>>(a, m, nfull);
-      return;
-    }
     const bool g = lut_total > MX_STAGED_LUT_MAX;
     const size_t dyn = g ? 0 : sizeof(u32) * lut_total;
     if (g) scan_fast_kernel<PC, SEGS, true, 8><<<(unsigned)nfull, S1_THREADS, dyn, s>>>(a, m);
@@ -761,51 +402,33 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   //  pipe:   persistent CTAs + TMA ring, slot output (scan_pipe_kernel)
   //  v1:     one CTA per tile, decoupled look-back output (scan_runs_kernel)
   const bool smem_lut = lut_total <= MX_SMEM_LUT_MAX;
-  const char* scan_env = getenv("MX_SCAN");
-  const bool use_v1 = scan_env && !strcmp(scan_env, "v1");
-  const bool use_pipe = scan_env && (!strcmp(scan_env, "pipe") || !strcmp(scan_env, "tma")) && smem_lut && !a.u16;
-  const bool slot_mode = !use_v1;
-  int dev = 0, n_sm = 148, smem_optin = 0;
+  int dev = 0, n_sm = 148;
   MX_CUDA_TRY(cudaGetDevice(&dev));
   MX_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  MX_CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const int lut_bytes = smem_lut ? (lut_total * 4 + 127) / 128 * 128 : 0;
-  const int P = NC;
-  // pipe geometry: the widest tile whose ring of >= 2 slots fits, then as
-  // many slots (<= 4) as fit in ~200 KB
-  int pipe_segs = 1, stages = 2;
-  {
-    const char* kb = getenv("MX_PIPE_KB");  // per-CTA ring budget (2 CTAs/SM by default)
-    const int budget = std::min(smem_optin - 8 * 1024, (kb ? atoi(kb) : 100) * 1024);
-    const int cand[3] = {4, 2, 1};
-    for (int c = 0; c < 3; ++c) {
-      const int stage_bytes = P * 1024 * cand[c] * 4 + (int)sizeof(TileMeta);
-      if (lut_bytes + 2 * stage_bytes <= budget) {
-        pipe_segs = cand[c];
-        stages = std::min(TMA_MAX_STAGES, (budget - lut_bytes) / stage_bytes);
-        break;
-      }
-    }
-  }
-  // direct-mode tile: 2 int4 segments per thread (2048-sample tiles, 4 CTAs
-  // per SM) unless MX_SCAN_SEGS=4 (4096-sample tiles, 2 CTAs per SM)
-  const char* segs_env = getenv("MX_SCAN_SEGS");
-  const int direct_segs = (segs_env && atoi(segs_env) == 4) ? 4 : 2;
-  const int tile_len = use_v1 ? S1_TILE : (use_pipe ? 1024 * pipe_segs : 1024 * direct_segs);
-  const int ntiles = (int)((n + tile_len - 1) / tile_len);
+  // Two stage-1 passes, both writing per-tile slot regions (tile-local
+  // compaction, no inter-tile dependency) fixed up by slot_fixup_kernel:
+  //  * one u16 row-tuple column, 16-byte aligned: scan_u16_kernel
+  //    (scan_u16.cuh), change-driven, warp segments of 1024 samples;
+  //  * otherwise (per-property int32 columns, wide tuple codes):
+  //    scan_fast_kernel over full 2048-sample tiles + scan_list_kernel for
+  //    tiles with many file starts + scan_direct_kernel for the rest.
+  const bool u16_path = a.u16 && NC == 1 && a.lut_sum != nullptr &&
+                        (reinterpret_cast<uintptr_t>(d->columns[0]) % 16) == 0;
+  const int tile_len = u16_path ? SEG_LEN : 2048;
+  const long long ntiles = (n + tile_len - 1) / tile_len;
   bool aligned = true;
-  for (int p = 0; p < P; ++p) aligned &= (reinterpret_cast<uintptr_t>(d->columns[p]) % (a.u16 ? 8 : 16)) == 0;
+  for (int p = 0; p < NC; ++p) aligned &= (reinterpret_cast<uintptr_t>(d->columns[p]) % (a.u16 ? 8 : 16)) == 0;
   const long long nstaged = aligned ? n / tile_len : 0;
   DevBuf<TileMeta> tmeta;
+  DevBuf<int> seg_fa;
   DevBuf<u32> rk, rf, rs, re;
-  DevBuf<u64> status, scratch64;
-  DevBuf<u32> ctr;
+  DevBuf<u64> scratch64;
   DevBuf<DevError> err;
-  // worst case every sample is its own run; slot mode addresses whole tiles
-  const long long cap = std::max<long long>(1, slot_mode ? (long long)ntiles * tile_len : n);
+  // worst case every sample is its own run; slots address whole tiles
+  const long long cap = std::max<long long>(1, ntiles * tile_len);
   DevBuf<u32> t_cnt, t_open, defer;
   DevBuf<long long> t_head;
-  if (slot_mode && ntiles > 0) {
+  if (ntiles > 0) {
     MX_CUDA_TRY(t_cnt.alloc(ntiles, s));
     MX_CUDA_TRY(t_open.alloc(ntiles, s));
     MX_CUDA_TRY(t_head.alloc(ntiles, s));
@@ -821,48 +444,48 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(rf.alloc(cap, s));
   MX_CUDA_TRY(rs.alloc(cap, s));
   MX_CUDA_TRY(re.alloc(cap, s));
-  MX_CUDA_TRY(status.alloc(ntiles > 0 ? ntiles : 1, s));
   MX_CUDA_TRY(scratch64.alloc(4, s));
-  MX_CUDA_TRY(ctr.alloc(4, s));
   MX_CUDA_TRY(err.alloc(1, s));
-  MX_CUDA_TRY(cudaMemsetAsync(status.p, 0, sizeof(u64) * (ntiles > 0 ? ntiles : 1), s));
-  MX_CUDA_TRY(cudaMemsetAsync(ctr.p, 0, sizeof(u32) * 4, s));
   MX_CUDA_TRY(cudaMemsetAsync(scratch64.p, 0, sizeof(u64) * 4, s));
   MX_CUDA_TRY(cudaMemsetAsync(err.p, 0xff, sizeof(u64), s));
   MX_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(err.p) + 8, 0, 8, s));
   a.rec_key = rk.p; a.rec_file = rf.p; a.rec_start = rs.p; a.rec_end = re.p;
-  a.status = status.p; a.tile_ctr = ctr.p; a.n_runs = scratch64.p; a.err = err.p;
-  if (ntiles > 0 && use_v1) {
-    MxPhase ph("scan_runs", s);
-    if (smem_lut) {
-      scan_runs_kernel<true><<<ntiles, S1_THREADS, sizeof(u32) * lut_total, s>>>(a);
-      mx_count_launch();
-    } else {
-      scan_runs_kernel<false><<<ntiles, S1_THREADS, 0, s>>>(a);
-      mx_count_launch();
-    }
-    MX_CUDA_TRY(cudaGetLastError());
-  } else if (ntiles > 0) {
-    MX_CUDA_TRY(tmeta.alloc(ntiles, s));
-    tile_meta_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(a, tile_len, ntiles, tmeta.p);
+  a.n_runs = scratch64.p; a.err = err.p;
+  if (ntiles > 0 && u16_path) {
+    MX_CUDA_TRY(seg_fa.alloc(ntiles + 1, s));
+    seg_file_kernel<<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, s>>>(a.file_off, a.n_files, n, ntiles, seg_fa.p);
     mx_count_launch();
     {
       MxPhase ph("scan_runs", s);
-      int rc = MX_OK;
-      if (use_pipe) {
-        if (pipe_segs == 4) rc = dispatch_pipe<4>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes, n_sm, s);
-        else if (pipe_segs == 2) rc = dispatch_pipe<2>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes, n_sm, s);
-        else rc = dispatch_pipe<1>(a, tmeta.p, ntiles, nstaged, stages, lut_bytes, n_sm, s);
+      const int entries = lut_total - 1;
+      const bool slut = entries <= U16_SMEM_LUT_MAX;
+      const size_t dyn = sizeof(U16Warp) * U16_WARPS + (slut ? sizeof(u32) * (size_t)entries : 0);
+      int per_sm = 1;
+      if (slut) {
+        MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<true>, U16_WARPS * 32, dyn));
       } else {
-        const long long nfast = getenv("MX_SCAN_NOFAST") ? 0 : nstaged;
-        if (direct_segs == 4) dispatch_direct<4>(a, tmeta.p, ntiles, smem_lut, lut_total, s, nfast);
-        else dispatch_direct<2>(a, tmeta.p, ntiles, smem_lut, lut_total, s, nfast);
+        MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<false>, U16_WARPS * 32, dyn));
       }
+      const long long want = (ntiles + U16_WARPS - 1) / U16_WARPS;
+      const unsigned grid = (unsigned)std::min<long long>(want, (long long)n_sm * std::max(1, per_sm));
+      if (slut) scan_u16_kernel<true><<<grid, U16_WARPS * 32, dyn, s>>>(a, seg_fa.p, ntiles);
+      else scan_u16_kernel<false><<<grid, U16_WARPS * 32, dyn, s>>>(a, seg_fa.p, ntiles);
       mx_count_launch();
-      if (rc != MX_OK) return rc;
+      MX_CUDA_TRY(cudaGetLastError());
     }
-    slot_fixup_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(ntiles, tile_len, t_cnt.p, t_open.p, t_head.p, rf.p,
-                                                          a.file_off, re.p, scratch64.p);
+  } else if (ntiles > 0) {
+    MX_CUDA_TRY(tmeta.alloc(ntiles, s));
+    tile_meta_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, s>>>(a, tile_len, ntiles, tmeta.p);
+    mx_count_launch();
+    MxPhase ph("scan_runs", s);
+    dispatch_direct<2>(a, tmeta.p, ntiles, smem_lut, lut_total, s, nstaged);
+    mx_count_launch();
+  }
+  if (ntiles > 0) {
+    slot_fixup_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, s>>>(ntiles, tile_len, t_cnt.p, t_open.p, t_head.p,
+                                                                     rf.p, a.file_off, re.p, scratch64.p);
     mx_count_launch();
     MX_CUDA_TRY(cudaGetLastError());
   }
@@ -890,66 +513,40 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     ix.n_blocks = 0;
     return MX_OK;
   }
-  // ---- radix sort by packed key
+  // ---- per-tile slots -> dense records (order preserved), then LSD radix
+  // sort by packed key (8-bit digits, stable, 2048-record tiles)
   const int passes = (d->key_bits + 7) / 8;
-  const int rtiles = (int)((I + RS_TILE - 1) / RS_TILE);
+  constexpr int RIT = 8;
+  const int rtile2 = RS_THREADS * RIT;
+  const int rtiles2 = (int)((I + rtile2 - 1) / rtile2);
+  const size_t rsmem = 4 * (size_t)rtile2 * sizeof(u32);
   DevBuf<u32> k2, f2, s2, e2, hist, dtot;
   MX_CUDA_TRY(k2.alloc(I, s));
   MX_CUDA_TRY(f2.alloc(I, s));
   MX_CUDA_TRY(s2.alloc(I, s));
   MX_CUDA_TRY(e2.alloc(I, s));
-  MX_CUDA_TRY(hist.alloc((long long)256 * std::max(rtiles, slot_mode ? ntiles : 0), s));
+  MX_CUDA_TRY(hist.alloc((long long)256 * rtiles2, s));
   MX_CUDA_TRY(dtot.alloc(256, s));
   u32 *ka = rk.p, *fa_ = rf.p, *sa = rs.p, *ea = re.p;
   u32 *kb = k2.p, *fb = f2.p, *sb = s2.p, *eb = e2.p;
   std::unique_ptr<MxPhase> ph_sort(new MxPhase("radix_sort", s));
-  if (slot_mode) {  // per-tile slots -> dense records (order preserved)
+  {
     DevBuf<u64> toff;
     MX_CUDA_TRY(toff.alloc(ntiles + 1, s));
     if (int rc = gs_run(ntiles, TileOffF{t_cnt.p, toff.p, ntiles}, s)) return rc;
-    slot_compact_kernel<<<std::min(ntiles, n_sm * 16), 256, 0, s>>>(ntiles, tile_len, t_cnt.p, toff.p, rk.p, rf.p,
-                                                                     rs.p, re.p, k2.p, f2.p, s2.p, e2.p);
+    slot_compact_kernel<<<(unsigned)std::min<long long>(ntiles, (long long)n_sm * 16), 256, 0, s>>>(
+        ntiles, tile_len, t_cnt.p, toff.p, rk.p, rf.p, rs.p, re.p, k2.p, f2.p, s2.p, e2.p);
     mx_count_launch();
     std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);
   }
-  const char* rs_env = getenv("MX_RADIX");
-  const bool staged = !(rs_env && !strcmp(rs_env, "direct"));
-  const char* ri_env = getenv("MX_RADIX_ITEMS");
-  const int ritems = ri_env && atoi(ri_env) == 16 ? 16 : 8;
-  const int rtile2 = RS_THREADS * ritems;
-  const int rtiles2 = (int)((I + rtile2 - 1) / rtile2);
-  const size_t rsmem = 4 * (size_t)rtile2 * sizeof(u32);
-  if (staged) {
-    MX_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(4 * RS_THREADS * 16 * sizeof(u32))));
-  }
-  for (int pass = 0; staged && pass < passes; ++pass) {
+  for (int pass = 0; pass < passes; ++pass) {
     const int shift = 8 * pass;
-    if (ritems == 16) radix_upsweep2<16><<<rtiles2, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles2);
-    else radix_upsweep2<8><<<rtiles2, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles2);
+    radix_upsweep2<RIT><<<rtiles2, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, rtiles2);
     mx_count_launch();
     radix_rowscan<<<256, 256, 0, s>>>(hist.p, rtiles2, dtot.p);
     mx_count_launch();
-    if (ritems == 16)
-      radix_downsweep2<16><<<rtiles2, RS_THREADS, rsmem, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p,
-                                                              dtot.p, rtiles2);
-    else
-      radix_downsweep2<8><<<rtiles2, RS_THREADS, rsmem, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p,
-                                                             dtot.p, rtiles2);
-    mx_count_launch();
-    MX_CUDA_TRY(cudaGetLastError());
-    std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);
-  }
-  for (int pass = 0; !staged && pass < passes; ++pass) {
-    const int shift = 8 * pass;
-    const u32* seg = nullptr;
-    const int tiles = rtiles;
-    radix_upsweep<<<tiles, RS_THREADS, 0, s>>>(ka, I, shift, hist.p, tiles, seg);
-    mx_count_launch();
-    radix_rowscan<<<256, 256, 0, s>>>(hist.p, tiles, dtot.p);
-    mx_count_launch();
-    radix_downsweep<<<tiles, RS_THREADS, 0, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p, dtot.p, tiles,
-                                                 seg);
+    radix_downsweep2<RIT><<<rtiles2, RS_THREADS, rsmem, s>>>(ka, fa_, sa, ea, kb, fb, sb, eb, I, shift, hist.p,
+                                                            dtot.p, rtiles2);
     mx_count_launch();
     MX_CUDA_TRY(cudaGetLastError());
     std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);

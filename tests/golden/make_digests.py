@@ -59,11 +59,53 @@ def spec_for(case, keys):
     return synth.cfg2_mixture(), None
 
 
+def chunked_intervals(rt, block=100_000_000):
+    """``oracle.filter_intervals`` over file blocks of ~``block`` samples
+    (intervals never cross files, ``catalog.py:559-604``), concatenated with
+    one key table: the 1B-sample catalog does not fit the host as one
+    expansion."""
+    import numpy as np
+
+    from paper_2502_19790_b200.catalog import ColumnarCatalog
+
+    sizes = rt.file_sizes
+    off = np.concatenate(([0], np.cumsum(sizes)))
+    ends = np.append(rt.run_starts[1:], rt.n_samples)
+    keys, key_of, parts = [], {}, []
+    f0 = 0
+    while f0 < len(sizes):
+        f1 = int(np.searchsorted(off, off[f0] + block, side="right")) - 1
+        f1 = max(f1, f0 + 1)
+        a, b = int(off[f0]), int(off[f1])
+        r0 = int(np.searchsorted(rt.run_starts, a, side="right")) - 1
+        r1 = int(np.searchsorted(rt.run_starts, b, side="left"))
+        lens = np.minimum(ends[r0:r1], b) - np.maximum(rt.run_starts[r0:r1], a)
+        cols = {p: np.repeat(c[r0:r1], lens).astype(np.int32) for p, c in rt.run_codes.items()}
+        sub = ColumnarCatalog.from_arrays(cols, rt.vocab, sizes[f0:f1], file_ids=np.arange(f0 + 1, f1 + 1))
+        iv = orc.filter_intervals(sub, [])
+        remap = np.empty(len(iv["keys"]), dtype=np.int64)
+        for j, k in enumerate(iv["keys"]):
+            if k not in key_of:
+                key_of[k] = len(keys)
+                keys.append(k)
+            remap[j] = key_of[k]
+        iv["key"] = remap[iv["key"]] if len(remap) else iv["key"]
+        parts.append(iv)
+        print("  block", f0, f1, len(iv["start"]), "intervals", flush=True)
+        f0 = f1
+    out = {x: np.concatenate([p[x] for p in parts]) for x in ("ds", "fid", "key", "start", "end")}
+    out["keys"] = keys
+    return out
+
+
 def run(case):
     t0 = time.time()
-    cc = synth.expand_numpy(catalog(case))
-    idx = orc.build_index(cc, [])
-    del cc
+    if case == "cfg3":
+        idx = orc.OracleIndex(chunked_intervals(catalog(case)))
+    else:
+        cc = synth.expand_numpy(catalog(case))
+        idx = orc.build_index(cc, [])
+        del cc
     ks = [orc.key_string(k) for k in idx.keys]
     out = {"samples": int((idx.end - idx.start).sum()), "intervals": int(len(idx.start)), "keys": len(ks),
            "index_sha256": index_digest(ks, idx.rank, idx.ds, idx.fid, idx.start, idx.end)}
