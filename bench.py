@@ -511,7 +511,8 @@ def our_arm(args):
     line = {
         "metric": METRIC, "value": world * n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "u16" if code_bytes == 2 else "int32",
+        "data": "synthetic",
         "config": dict(CFG, parallelism=f"file-sharded x{world}" if world > 1 else "single GPU",
                        layout=LAYOUT_NOTE[args.layout],
                        l2=f"inputs ({n * code_bytes * n_cols / 1e9:.1f} GB of code columns) exceed the 126 MB L2; "
@@ -521,7 +522,9 @@ def our_arm(args):
                 "ranges": n_ranges},
         "phases_ms": {p: round(v[0] / max(v[1], 1), 4) for p, v in phases.items()},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "scan_fast_kernel (the scan_runs phase: scan_fast + deferred-tile scan_list + tail scan_direct)",
+                     "traffic": traffic, "kernel": ("scan_u16_kernel (the scan_runs phase: change-driven warp segments over the u16 row-tuple column)"
+                                if code_bytes == 2 else "scan_fast_kernel (the scan_runs phase: scan_fast + "
+                                "deferred-tile scan_list + tail scan_direct)"),
                      "bytes_per_launch": scan_bytes, "peak_kind": peak_kind,
                      "note": "algorithmic bytes = N*b*C code-column reads (C = 1 row-tuple column of b = 2-byte codes, or P per-property int32 columns) + 16 B per interval record"
                              + (f"; at {b_per_sample} B/sample this kernel is instruction-issue bound "
@@ -540,6 +543,8 @@ def our_arm(args):
         **({"concurrent_jobs": concurrent} if concurrent else {}),
         "clocks": clk,
     }
+    if world == 1 and not args.no_extras:
+        line["more"] = extra_measurements(args, rt, meta, spec, device)
     if not args.no_cpu_baseline and world == 1:
         real = _reference_pkg() is not None
         if real:
@@ -560,6 +565,141 @@ def our_arm(args):
         dist.destroy_process_group()
 
 
+def _timed_steps(fn, steps, warmup):
+    """Device time per call of fn (CUDA events on the current stream)."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def extra_measurements(args, rt, meta, spec, device) -> dict:
+    """Secondary lines of the N=1 run (rank 0): what a drop-in user gets.
+
+    * columns_layout: the same job over one int32 code column per property
+      (the layout DeviceCatalog.from_reference builds for a reference catalog);
+    * registration: the one-time row-tuple dictionary encoding of those
+      columns on the device (encode_row_tuples_device), which the headline
+      layout needs before its first job;
+    * north_star_1b: the cfg3 catalog (1B samples, 100k files, R=64) indexed
+      and chunked on ONE B200, u16 row-tuple layout, every chunk emitted;
+    * dropin_serving: the whole cfg2 job through the reference seam the
+      server calls per chunk (ChunkGenerator.generate + Chunk.serialize,
+      server.py:143-163), host wall clock."""
+    import torch
+
+    from paper_2502_19790_b200 import ChunkGenerator, DeviceCatalog, _lib, build_index_from_catalog, synth
+
+    out = {}
+    steps = max(3, min(args.steps, 10))
+    peak, _ = peaks()
+    # ---- per-property int32 columns + registration of the tuple layout
+    cols = device_columns(rt, device)
+    dcat = device_catalog(meta, cols, None)
+    cres = {}
+
+    def cjob():
+        i_, g_, b_ = run_step(dcat, spec)
+        cres["intervals"] = i_.n_intervals
+
+    cjob()
+    _lib.lib().mx_profile_reset()
+    _lib.lib().mx_profile_enable(1)
+    ms = _timed_steps(cjob, steps, 1)
+    scan_ms, scan_n = _lib.profile_read("scan_runs")
+    _lib.lib().mx_profile_enable(0)
+    n = rt.n_samples
+    scan_bytes = n * 4 * len(cols) + 16 * cres["intervals"]
+    scan_avg = scan_ms / max(scan_n, 1)
+    out["columns_layout"] = {
+        "ms_per_step": ms, "value": n / (ms * 1e-3), "unit": UNIT,
+        "scan_ms": scan_avg, "scan_roofline_frac": scan_bytes / (scan_avg * 1e-3) / 1e9 / peak,
+        "note": "one int32 code column per property (2 GB at cfg2), the layout of a catalog adopted from the "
+                "reference (DeviceCatalog.from_reference)"}
+    cards = [len(rt.vocab[p]) for p in sorted(rt.vocab)]
+    enc_ms = _timed_steps(lambda: DeviceCatalog.encode_row_tuples_device(cols, cards), 3, 1)
+    out["registration"] = {
+        "tuple_encode_ms": enc_ms,
+        "note": "row-tuple dictionary encoding of the int32 columns on the device (mixed-radix tuple value + "
+                "unique), once per registered catalog; not part of a job"}
+    del dcat, cols
+    torch.cuda.empty_cache()
+    # ---- drop-in serving: per-chunk generate() + serialize() for the whole job
+    tcols, table = layout_columns(rt, device_columns(rt, device), "tuples")
+    dcat = device_catalog(meta, tcols, table)
+    idx = build_index_from_catalog(dcat, [])
+    for rep in range(2):  # the first pass warms the pinned pools
+        gen = ChunkGenerator(idx, CFG["job_seed"])
+        t0 = time.perf_counter()
+        n_ch = n_bytes = 0
+        while (c := gen.generate(spec)) is not None:
+            n_bytes += len(c.serialize())
+            n_ch += 1
+        dt = time.perf_counter() - t0
+    out["dropin_serving"] = {
+        "chunks": n_ch, "seconds": dt, "chunks_per_s": n_ch / dt, "bytes_per_s": n_bytes / dt,
+        "note": "ChunkGenerator.generate(spec) + Chunk.serialize() once per chunk until None, as the reference "
+                "server calls them (server.py:143-163); the generator plans ahead on the device (look-ahead "
+                "doubling) and chunks carry device-built canonical bytes with a lazy data dict; index built "
+                "once, host wall clock"}
+    del gen, idx, dcat, tcols
+    torch.cuda.empty_cache()
+    # ---- north star: 1B samples on one GPU
+    big = synth.config("cfg3", scale=args.scale)
+    bmeta = synth.ColumnarCatalog.meta_only(big.vocab, big.file_sizes)
+    codes, btable = run_level_tuples(big, device)
+    bcat = device_catalog(bmeta, {"tuples": codes}, btable)
+    res = {}
+
+    def job():
+        i_, g_, b_ = run_step(bcat, spec)
+        res.update(chunks=b_.n_chunks, ranges=b_.n_ranges, intervals=i_.n_intervals, blocks=i_.n_blocks)
+
+    bms = _timed_steps(job, 3, 1)
+    bn = big.n_samples
+    b_bytes = bn * 2 + 16 * res["intervals"] + 8 * res["blocks"] + 16 * 2000 + 16 * res["intervals"] + \
+        20 * res["ranges"] + 8 * res["chunks"]
+    out["north_star_1b"] = {
+        "samples": bn, "files": len(big.file_sizes), "ms_per_job": bms, "value": bn / (bms * 1e-3), "unit": UNIT,
+        "chunks": res["chunks"], "chunks_per_s": res["chunks"] / (bms * 1e-3), "intervals": res["intervals"],
+        "roofline_step": {"bytes": b_bytes, "achieved": b_bytes / (bms * 1e-3) / 1e9, "peak": peak,
+                          "frac": b_bytes / (bms * 1e-3) / 1e9 / peak},
+        "note": "cfg3 catalog (seed 3) on ONE device, u16 row-tuple column (2 GB), cfg2 mixture, every chunk; "
+                "bit-exact vs the oracle in tests/test_gpu_parity_scale.py::test_cfg3_one_billion_samples_one_gpu"}
+    del bcat, codes
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_level_tuples(rt, device):
+    """u16 row-tuple column of a run table, encoded at RUN level (every sample
+    of a run holds its run's tuple), identical to encode_row_tuples_device on
+    the expanded columns without materialising 20 GB of int32 columns."""
+    import torch
+
+    from paper_2502_19790_b200.catalog import narrow_codes, row_tuple_table, _tuple_radix
+
+    props = sorted(rt.run_codes)
+    cards = [len(rt.vocab[p]) for p in props]
+    mult = _tuple_radix(cards)
+    r = np.zeros(len(rt.run_starts), dtype=np.int64)
+    for p, m in zip(props, mult):
+        r += (rt.run_codes[p].astype(np.int64) + 1) * m
+    u, inv = np.unique(r, return_inverse=True)
+    table = row_tuple_table(u, cards)
+    run_codes = torch.from_numpy(narrow_codes(inv.astype(np.int32), len(u))).to(device)
+    lens = torch.from_numpy(rt.run_lengths()).to(device)
+    return torch.repeat_interleave(run_codes, lens), table
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -570,6 +710,8 @@ def main():
                     help="catalog layout in HBM: one row-tuple code column, or one code column per property")
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of the cfg2 size (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the secondary lines (columns layout, registration, 1B job, drop-in serving)")
     ap.add_argument("--concurrent", action="store_true",
                     help="also time two jobs in flight (two host threads, two streams); diagnostic")
     args = ap.parse_args()

@@ -37,13 +37,36 @@ class _ChunkBase:
 
 
 class Chunk(_ChunkBase):
-    """Sample pointers of one chunk + its mixture snapshot (``chunks.py:26-106``)."""
+    """Sample pointers of one chunk + its mixture snapshot (``chunks.py:26-106``).
+
+    A chunk handed out of a device batch is LAZY: ``data`` (the nested
+    key -> ds -> fid -> ranges dict) is built from the batch's host arrays
+    only when someone reads it, and ``serialize()`` returns the canonical
+    bytes built on the device -- the server (``server.py:143-163``) only
+    ever calls ``serialize()``, so serving a chunk costs no Python dicts."""
 
     def __init__(self, chunk_id: int, data: RangeMap, seed: int, mixture: MixtureSpec | None = None):
         self.chunk_id = chunk_id
-        self.data = data
+        self._data = data
+        self._src = None  # (batch, index) of a lazy chunk
         self.seed = seed
         self.mixture = mixture
+        self._device_bytes = None
+
+    @property
+    def data(self) -> RangeMap:
+        if self._data is None and self._src is not None:
+            batch, i = self._src
+            self._data = batch._chunk_data(i)
+            dev = self._device_bytes
+            if dev is not None and dev[1] is None:
+                self._device_bytes = (dev[0], self._data, dev[2])
+        return self._data
+
+    @data.setter
+    def data(self, value: RangeMap) -> None:
+        self._data = value
+        self._src = None
 
     def samples_per_key(self) -> dict[MixtureKey, int]:
         return {
@@ -86,9 +109,11 @@ class Chunk(_ChunkBase):
 
     def serialize(self) -> bytes:
         # bytes produced on the device for a planned batch (csrc/serialize.cu),
-        # valid while data / mixture are the objects they were built from
-        dev = getattr(self, "_device_bytes", None)
-        if dev is not None and dev[1] is self.data and dev[2] is self.mixture:
+        # valid while data (still lazy, or the object built from the same
+        # arrays) and mixture are the ones they were built from
+        dev = self._device_bytes
+        if dev is not None and dev[2] is self.mixture and (
+                (self._data is None and self._src is not None) or dev[1] is self._data):
             return dev[0]
         return canonical_json_bytes(self.to_json())
 
@@ -210,27 +235,40 @@ class ChunkBatch:
 
     def chunk(self, i: int, mixture=None) -> Chunk:
         """Chunk i of the batch; ``mixture`` (the spec in force) defaults to the
-        batch's spec. Large batches carry device-built canonical bytes."""
-        c = self._chunk(i)
+        batch's spec. Large batches carry device-built canonical bytes and a
+        lazy ``data``."""
+        h = self.to_host()
+        c = Chunk(int(h["ids"][i]), None, int(h["seeds"][i]), None if self.arbitrary else self.spec)
+        c._src = (self, i)
         if mixture is not None:
             c.mixture = mixture
-        if self.n_chunks >= self.DEVICE_JSON_MIN and (self.arbitrary or c.mixture is self.spec):
+        if self.n_chunks >= self.DEVICE_JSON_MIN and self._json_ok() and (self.arbitrary or c.mixture is self.spec):
             if getattr(self, "_json", None) is None:
                 self._json = self.serialize_all()
             blob, off = self._json
-            c._device_bytes = (blob[int(off[i]):int(off[i + 1])], c.data, c.mixture)
+            c._device_bytes = (blob[int(off[i]):int(off[i + 1])], None, c.mixture)
         return c
 
+    def _json_ok(self) -> bool:
+        """Device JSON ranks keys in 16 bits (csrc/serialize.cu); wider key
+        sets serialise on the host."""
+        n = len(self._gen.index.component_keys()) if self.arbitrary else len(self.mkeys)
+        return n < 65536
+
     def _chunk(self, i: int) -> Chunk:
+        c = self.chunk(i)
+        c.data  # materialise
+        return c
+
+    def _chunk_data(self, i: int) -> RangeMap:
         h = self.to_host()
         a, b = int(h["off"][i]), int(h["off"][i + 1])
         data: RangeMap = {}
-        comp_keys = self._gen.index.component_keys() if self.arbitrary else None
+        keys = self._gen.index.component_keys() if self.arbitrary else self.mkeys
         for m, d, f, s, e in zip(h["mkey"][a:b].tolist(), h["ds"][a:b].tolist(), h["fid"][a:b].tolist(),
                                  h["start"][a:b].tolist(), h["end"][a:b].tolist()):
-            key = comp_keys[m] if self.arbitrary else self.mkeys[m]
-            data.setdefault(key, {}).setdefault(d, {}).setdefault(f, []).append((s, e))
-        return Chunk(int(h["ids"][i]), data, int(h["seeds"][i]), None if self.arbitrary else self.spec)
+            data.setdefault(keys[m], {}).setdefault(d, {}).setdefault(f, []).append((s, e))
+        return data
 
 
 class ChunkGenerator:

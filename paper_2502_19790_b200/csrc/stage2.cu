@@ -190,6 +190,7 @@ struct PlanArgs {
   // mode 0 / 2: stream lengths
   const u64* seg_pre;
   const u32* s_off;
+  const u64* slen;  // mode 0: length of stream m (staged in shared memory by plan_kernel)
   // mode 1
   const u32* L_off;
   const u32* L;
@@ -346,7 +347,7 @@ __device__ int simulate_chunk(PlanArgs& a, long long* n_terms) {
       if (a.mode == 1) {
         g = take_shared(a, m, a.rem[m], n_terms);
       } else {
-        u64 len = a.seg_pre[a.s_off[m + 1] + m + 1 - 1];  // end of stream m
+        const u64 len = a.slen ? a.slen[m] : a.seg_pre[a.s_off[m + 1] + m];  // end of stream m
         long long avail = (long long)(len - a.pos[m]) - a.took[m];
         g = a.rem[m] < avail ? a.rem[m] : avail;
       }
@@ -384,19 +385,30 @@ constexpr int PLAN_SMEM_KM = 256;
 
 __global__ void plan_kernel(PlanArgs a) {
   // The planner is one sequential thread: keep its per-key state in shared
-  // memory when it fits (each access is then ~30 cycles instead of an L2 trip).
+  // memory when it fits (each access is then ~30 cycles instead of an L2
+  // trip); the warp stages the weights and stream lengths in parallel first,
+  // so the sequential replay never waits on a dependent global load.
   __shared__ long long s_ll[5][PLAN_SMEM_KM];
   __shared__ unsigned char s_flags[2][PLAN_SMEM_KM];
-  __shared__ u64 s_pos[PLAN_SMEM_KM];
+  __shared__ u64 s_pos[PLAN_SMEM_KM], s_len[PLAN_SMEM_KM];
   __shared__ int s_idx[PLAN_SMEM_KM];
   __shared__ double s_frac[PLAN_SMEM_KM], s_w[PLAN_SMEM_KM];
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (blockIdx.x != 0) return;
   const int Km = a.Km;
+  const bool staged = Km <= PLAN_SMEM_KM && a.mode != 1;
+  if (staged) {
+    for (int m = threadIdx.x; m < Km; m += blockDim.x) {
+      s_w[m] = a.w[m];
+      if (a.mode == 0) s_len[m] = a.seg_pre[a.s_off[m + 1] + m];
+    }
+    __syncwarp();
+  }
+  if (threadIdx.x != 0) return;
   u64* pos_out = a.pos;
   long long* report_out = a.report;
-  if (Km <= PLAN_SMEM_KM && a.mode != 1) {
-    for (int m = 0; m < Km; ++m) s_w[m] = a.w[m];
+  if (staged) {
     a.w = s_w;
+    if (a.mode == 0) a.slen = s_len;
     a.counts = s_ll[0];
     a.rem = s_ll[1];
     a.found = s_ll[2];
@@ -443,7 +455,7 @@ __global__ void plan_kernel(PlanArgs a) {
     long long rep = a.max_chunks - chunks;
     for (int m = 0; m < Km; ++m) {
       if (a.took[m] <= 0) continue;
-      u64 len = a.seg_pre[a.s_off[m + 1] + m];
+      const u64 len = a.slen ? a.slen[m] : a.seg_pre[a.s_off[m + 1] + m];
       long long avail = (long long)(len - a.pos[m]);
       long long r = avail / a.took[m];
       if (r < rep) rep = r;

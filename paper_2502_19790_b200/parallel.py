@@ -263,12 +263,21 @@ class MergedChunkBatch:
         return self._host
 
     def chunk(self, i: int, mixture=None):
-        from .chunks import ChunkBatch
+        """Lazy chunk i (host canonical bytes: the device JSON of the local
+        result does not describe the merged chunks)."""
+        from .chunks import Chunk
 
-        c = ChunkBatch._chunk(self, i)
+        h = self.to_host()
+        c = Chunk(int(h["ids"][i]), None, int(h["seeds"][i]), None if self.arbitrary else self.spec)
+        c._src = (self, i)
         if mixture is not None:
             c.mixture = mixture
         return c
+
+    def _chunk_data(self, i: int):
+        from .chunks import ChunkBatch
+
+        return ChunkBatch._chunk_data(self, i)
 
 
 def merge_batch(gen, batch, stream=None):

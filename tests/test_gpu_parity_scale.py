@@ -144,8 +144,13 @@ def test_cfg3_one_billion_samples_one_gpu():
 
     from paper_2502_19790_b200 import synth
 
+    import bench
+    from paper_2502_19790_b200.catalog import ColumnarCatalog
+
     want = _need("cfg3")
-    dcat = _catalog(synth.config("cfg3"), "tuples")
+    rt = synth.config("cfg3")
+    codes, table = bench.run_level_tuples(rt, torch.device("cuda", 0))  # the bench's 1B construction
+    dcat = bench.device_catalog(ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes), {"tuples": codes}, table)
     idx, gen, batch = _job(dcat, synth.cfg2_mixture())
     _check_index(idx, want)
     _check_chunks(gen, batch, want)
