@@ -105,6 +105,124 @@ cudaError_t D2HBatch::sync() {
   return cudaSuccess;
 }
 
+namespace {
+struct AuxPool {
+  std::mutex mu;
+  std::map<int, std::vector<cudaStream_t>> streams;
+  std::map<int, std::vector<cudaEvent_t>> events;
+};
+AuxPool& aux_pool() {
+  static AuxPool* p = new AuxPool();  // never destroyed: streams live for the process
+  return *p;
+}
+}  // namespace
+
+cudaError_t mx::aux_streams(int dev, cudaStream_t out[3]) {
+  AuxPool& p = aux_pool();
+  std::lock_guard<std::mutex> lk(p.mu);
+  std::vector<cudaStream_t>& v = p.streams[dev];
+  while (v.size() < 3) {
+    cudaStream_t st;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+    v.push_back(st);
+  }
+  for (int i = 0; i < 3; ++i) out[i] = v[i];
+  return cudaSuccess;
+}
+
+cudaError_t mx::aux_event_take(int dev, cudaEvent_t* e) {
+  AuxPool& p = aux_pool();
+  {
+    std::lock_guard<std::mutex> lk(p.mu);
+    std::vector<cudaEvent_t>& v = p.events[dev];
+    if (!v.empty()) {
+      *e = v.back();
+      v.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+}
+
+void mx::aux_event_give(int dev, cudaEvent_t e) {
+  AuxPool& p = aux_pool();
+  std::lock_guard<std::mutex> lk(p.mu);
+  p.events[dev].push_back(e);
+}
+
+// pinned slots for deferred index sizes (IndexData::Pending)
+namespace {
+struct PendPool {
+  std::mutex mu;
+  char* base = nullptr;
+  std::vector<int> free_slots;
+  static constexpr int kSlots = 4096;
+};
+PendPool& pend_pool() {
+  static PendPool* p = new PendPool();
+  return *p;
+}
+}  // namespace
+
+mx::IndexData::Pending* mx::pend_slot_take() {
+  PendPool& p = pend_pool();
+  std::lock_guard<std::mutex> lk(p.mu);
+  if (!p.base) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&p.base), sizeof(mx::IndexData::Pending) * PendPool::kSlots,
+                      cudaHostAllocDefault) != cudaSuccess) {
+      p.base = nullptr;
+      cudaGetLastError();
+      return nullptr;
+    }
+    for (int i = PendPool::kSlots - 1; i >= 0; --i) p.free_slots.push_back(i);
+  }
+  if (p.free_slots.empty()) return nullptr;
+  const int i = p.free_slots.back();
+  p.free_slots.pop_back();
+  return reinterpret_cast<mx::IndexData::Pending*>(p.base) + i;
+}
+
+void mx::pend_slot_give(mx::IndexData::Pending* slot) {
+  PendPool& p = pend_pool();
+  std::lock_guard<std::mutex> lk(p.mu);
+  p.free_slots.push_back((int)(slot - reinterpret_cast<mx::IndexData::Pending*>(p.base)));
+}
+
+int mx::ix_resolve(mx::IndexData* ix) {
+  if (!ix->pend) return MX_OK;
+  cudaError_t e = cudaEventSynchronize(ix->pend_ev);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "index sizes", __FILE__, __LINE__);
+  const mx::IndexData::Pending h = *ix->pend;
+  pend_slot_give(ix->pend);
+  aux_event_give(ix->pend_dev, ix->pend_ev);
+  ix->pend = nullptr;
+  ix->pend_ev = nullptr;
+  if (h.err.overlap) return mx_fail(MX_ERR_INDEX, "empty or overlapping interval in index build");
+  ix->n_keys = (long long)(h.totals >> 32);
+  ix->n_blocks = (long long)(h.totals & 0xffffffffull);
+  ix->indexed_samples = (long long)h.samples;
+  ix->max_key_blocks = (long long)h.maxblk;
+  return MX_OK;
+}
+
+mx::IndexData::~IndexData() {
+  if (pend) {
+    cudaEventSynchronize(pend_ev);  // the copy into the slot must land first
+    pend_slot_give(pend);
+    aux_event_give(pend_dev, pend_ev);
+  }
+}
+
+cudaError_t D2HBatch::sync_event(cudaEvent_t e) {
+  cudaError_t r = cudaEventSynchronize(e);
+  if (r != cudaSuccess) return r;
+  for (int i = 0; i < n; ++i) memcpy(items[i].dst, g_rb.buf + items[i].off, items[i].bytes);
+  n = 0;
+  used = 0;
+  return cudaSuccess;
+}
+
 cudaError_t mx_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return cudaSuccess;
   PinnedRing& r = g_ring;
@@ -349,6 +467,7 @@ int mx_index_free(mx_index* index) {
 int mx_index_sizes(const mx_index* index, int64_t* n_keys, int64_t* n_blocks, int64_t* n_intervals,
                    int64_t* n_samples) {
   MX_CHECK_ARG(index, "null index");
+  if (int rc = ix_resolve(const_cast<IndexData*>(&index->d))) return rc;
   const IndexData& d = index->d;
   if (n_keys) *n_keys = d.n_keys;
   if (n_blocks) *n_blocks = d.n_blocks;
@@ -359,6 +478,7 @@ int mx_index_sizes(const mx_index* index, int64_t* n_keys, int64_t* n_blocks, in
 
 int mx_index_export_keys(const mx_index* index, uint32_t* packed, int64_t* samples) {
   MX_CHECK_ARG(index, "null index");
+  if (int rc = ix_resolve(const_cast<IndexData*>(&index->d))) return rc;
   const IndexData& d = index->d;
   const long long K = d.n_keys;
   if (K == 0) return MX_OK;
@@ -377,6 +497,7 @@ int mx_index_export_keys(const mx_index* index, uint32_t* packed, int64_t* sampl
 int mx_index_export_intervals(const mx_index* index, uint32_t* key_rank, int32_t* ds, int64_t* file_id,
                               uint32_t* start, uint32_t* end) {
   MX_CHECK_ARG(index, "null index");
+  if (int rc = ix_resolve(const_cast<IndexData*>(&index->d))) return rc;
   const IndexData& d = index->d;
   if (d.sharded)
     return mx_fail(MX_ERR_UNSUPPORTED,
@@ -402,6 +523,8 @@ int mx_index_export_intervals(const mx_index* index, uint32_t* key_rank, int32_t
 }
 
 int mx_index_block_table(const mx_index* index, int64_t file_base, uint32_t* rows, void* stream) {
+  if (index)
+    if (int rc = ix_resolve(const_cast<IndexData*>(&index->d))) return rc;
   MX_CHECK_ARG(index && (rows || index->d.n_blocks == 0), "null argument");
   MX_CHECK_ARG(file_base >= 0 && file_base + index->d.n_files < (1ll << 32), "file_base out of range");
   g_err.clear();
@@ -409,6 +532,8 @@ int mx_index_block_table(const mx_index* index, int64_t file_base, uint32_t* row
 }
 
 int mx_index_packed_keys(const mx_index* index, uint32_t* packed) {
+  if (index)
+    if (int rc = ix_resolve(const_cast<IndexData*>(&index->d))) return rc;
   MX_CHECK_ARG(index && (packed || index->d.n_keys == 0), "null argument");
   if (index->d.n_keys == 0) return MX_OK;
   cudaError_t e = cudaMemcpy(packed, index->d.key_packed.p, sizeof(u32) * index->d.n_keys, cudaMemcpyDeviceToHost);
@@ -417,6 +542,8 @@ int mx_index_packed_keys(const mx_index* index, uint32_t* packed) {
 }
 
 int mx_index_build_sharded(const mx_index* local, const mx_shard_desc* desc, void* stream, mx_index** out) {
+  if (local)
+    if (int rc = ix_resolve(const_cast<IndexData*>(&local->d))) return rc;
   MX_CHECK_ARG(local && desc && out, "null argument");
   MX_CHECK_ARG(desc->world >= 1 && desc->rank >= 0 && desc->rank < desc->world, "bad world/rank");
   MX_CHECK_ARG(desc->file_lo >= 0 && desc->file_hi - desc->file_lo == local->d.n_files &&
@@ -455,6 +582,7 @@ int mx_gen_create(mx_index* index, const uint8_t* cursor_prefix, int32_t cursor_
   MX_CHECK_ARG(index && out, "null argument");
   g_err.clear();
   keep_pool_warm();
+  if (int rc = ix_resolve(&index->d)) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   mx_gen* g = new mx_gen();
   int rc = MX_OK;
@@ -491,6 +619,7 @@ int mx_gen_plan(mx_gen* gen, const mx_mixture_desc* mix, int64_t max_chunks, int
 }
 
 int mx_gen_plan_arbitrary(mx_gen* gen, int64_t chunk_size, int64_t max_chunks, int64_t* n_out) {
+  if (gen) gen->d.fresh_layout = false;  // state changes on the generator stream: later plans wait for it
   MX_CHECK_ARG(gen && n_out, "null argument");
   MX_CHECK_ARG(max_chunks >= 1, "max_chunks must be >= 1");
   g_err.clear();
@@ -607,6 +736,7 @@ int mx_gen_result_export(const mx_gen* gen, int64_t* chunk_offsets, uint32_t* mk
 }
 
 int mx_gen_result_json(mx_gen* gen, const mx_json_desc* desc, int64_t* total_bytes, void* stream) {
+  if (gen) gen->d.fresh_layout = false;  // state changes on the generator stream: later plans wait for it
   MX_CHECK_ARG(gen && desc && total_bytes, "null argument");
   MX_CHECK_ARG(desc->n_keys >= 0 && desc->n_keys < 65536, "n_keys outside [0, 65536)");
   MX_CHECK_ARG(desc->key_json_off && desc->key_rank && desc->file_rank && desc->mixture_json, "null table");
@@ -650,6 +780,7 @@ int mx_gen_mark(mx_gen* gen) {
 }
 
 int mx_gen_reset_to_mark(mx_gen* gen) {
+  if (gen) gen->d.fresh_layout = false;  // state changes on the generator stream: later plans wait for it
   MX_CHECK_ARG(gen, "null generator");
   GenData& g = gen->d;
   if (!g.mark_consumed.p) return mx_fail(MX_ERR_INVALID, "no mark set");
@@ -772,6 +903,7 @@ int mx_gen_cursor_to_consumed(const mx_gen* gen, const int64_t* pos, const int64
 }
 
 int mx_gen_set_consumed(mx_gen* gen, const int64_t* consumed) {
+  if (gen) gen->d.fresh_layout = false;  // state changes on the generator stream: later plans wait for it
   MX_CHECK_ARG(gen && consumed, "null argument");
   GenData& g = gen->d;
   const long long K = g.K;
@@ -786,6 +918,7 @@ int mx_gen_set_consumed(mx_gen* gen, const int64_t* consumed) {
 }
 
 int mx_gen_set_cursors(mx_gen* gen, const int64_t* pos, const int64_t* offset) {
+  if (gen) gen->d.fresh_layout = false;  // state changes on the generator stream: later plans wait for it
   MX_CHECK_ARG(gen && pos && offset, "null argument");
   if (gen->d.ix->sharded)
     return mx_fail(MX_ERR_INVALID, "sharded generator: use mx_gen_cursor_to_consumed + mx_gen_set_consumed");

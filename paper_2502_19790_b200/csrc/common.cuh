@@ -141,6 +141,9 @@ struct D2HBatch {
   explicit D2HBatch(cudaStream_t st) : s(st) {}
   cudaError_t add(void* dst, const void* src, size_t bytes);
   cudaError_t sync();  // cudaStreamSynchronize + deliver every read
+  // wait only for the copies queued so far (an event recorded behind them),
+  // so later work on the stream keeps running; no other batch in between
+  cudaError_t sync_event(cudaEvent_t e);
 };
 
 // Launch accounting and per-phase CUDA-event timing (capi.cu). A phase timer

@@ -220,26 +220,26 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   MX_CUDA_TRY(cudaMemsetAsync(g->consumed.p, 0, sizeof(u64) * (K > 0 ? K : 1), s));
   if (K == 0) return MX_OK;
   MxPhase ph("cursor_layout", s);
+  MX_CUDA_TRY(g->aux_init());
+  // per-component totals first: the first plan (on g->pstream) waits only
+  // for them, not for the shuffles below
+  MX_CUDA_TRY(g->comp_total.alloc(K, s));
+  comp_total_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
+                                                               ix->iv_cum.p, g->comp_total.p);
+  mx_count_launch();
   // the component-order shuffle (one sequential Fisher-Yates over K ranks)
   // runs on a side stream, overlapped with the per-key cursor shuffles
-  static thread_local cudaStream_t side = nullptr;
-  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (!side) {
-    MX_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    MX_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    MX_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-  }
   static thread_local uint32_t h_base[MT_N];
   if (h_base[0] != 19650218u) mt_base_table(h_base);
   DevBuf<u32> mt_base;
   MX_CUDA_TRY(mt_base.alloc(MT_N, s));
   MX_CUDA_TRY(mx_h2d(mt_base.p, h_base, sizeof(h_base), s));
   MX_CUDA_TRY(g->comp_order.alloc(K, s));
-  MX_CUDA_TRY(cudaEventRecord(ev_fork, s));
-  MX_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
-  component_order_kernel<<<1, 32, 0, side>>>(K, order_seed, mt_base.p, g->comp_order.p);
+  MX_CUDA_TRY(cudaEventRecord(g->ev_tot, s));
+  MX_CUDA_TRY(cudaStreamWaitEvent(g->ostream, g->ev_tot, 0));
+  component_order_kernel<<<1, 32, 0, g->ostream>>>(K, order_seed, mt_base.p, g->comp_order.p);
   mx_count_launch();
-  MX_CUDA_TRY(cudaEventRecord(ev_join, side));
+  MX_CUDA_TRY(cudaEventRecord(g->ev_order, g->ostream));
   DevBuf<uint8_t> pre;
   DevBuf<u64> seeds;
   MX_CUDA_TRY(pre.alloc(prefix_len > 0 ? prefix_len : 1, s));
@@ -285,12 +285,9 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   if (int rc = gs_run(I, CumPermF{g->civ.p, ix->iv_start.p, ix->iv_end.p, g->ccum.p, ix->iv_file.p, g->cfile.p,
                                    g->cstart.p}, s))
     return rc;
-  MX_CUDA_TRY(g->comp_total.alloc(K, s));
-  comp_total_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
-                                                               ix->iv_cum.p, g->comp_total.p);
-  mx_count_launch();
   if (int rc = gen_local_lists(g, s)) return rc;  // sharded index: this rank's cursor positions
-  MX_CUDA_TRY(cudaStreamWaitEvent(s, ev_join, 0));
+  MX_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_order, 0));
+  g->fresh_layout = true;
   MX_CUDA_TRY(cudaGetLastError());
   g->mirrors_valid = false;  // host copies of comp_order / comp_total on first use
   return MX_OK;

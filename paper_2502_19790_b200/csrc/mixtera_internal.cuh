@@ -92,7 +92,31 @@ struct IndexData {
   long long file_lo = 0, file_hi = 0;
   long long n_local = 0;  // this rank's (real) intervals in the hybrid index
   DevBuf<u32> iv_nreal;
+  // sizes still travelling to the host (index_finalize with defer): the
+  // build returns without waiting; ix_resolve() waits for them on first use
+  struct Pending {
+    u32 maxblk, pad;
+    u64 totals, samples;
+    DevError err;
+  };
+  Pending* pend = nullptr;  // slot of the pinned pool (capi.cu)
+  cudaEvent_t pend_ev = nullptr;
+  int pend_dev = -1;
+  ~IndexData();
 };
+
+IndexData::Pending* pend_slot_take();  // nullptr: pool exhausted (finalize then waits)
+void pend_slot_give(IndexData::Pending* slot);
+// completes a deferred index_finalize (sizes, IndexBuildError); MX_OK when
+// nothing is pending
+int ix_resolve(IndexData* ix);
+
+// per-device auxiliary streams (created once, shared by every generator on
+// the device; non-blocking) and a pool of timing-disabled events (capi.cu):
+// creating streams per generator costs ~50 us each
+cudaError_t aux_streams(int dev, cudaStream_t out[3]);
+cudaError_t aux_event_take(int dev, cudaEvent_t* e);
+void aux_event_give(int dev, cudaEvent_t e);
 
 struct GenData {
   IndexData* ix = nullptr;
@@ -137,17 +161,46 @@ struct GenData {
   bool match_shared = false;
   std::vector<u32> match_off;  // host copy of L_off
   DevBuf<u32> match_L_off, match_L;
-  // grow-only scratch for per-call planning (small plans allocate nothing)
+  // grow-only scratch for per-call planning (small plans allocate nothing);
+  // allocated in stream order on the stream that first writes it (`st`)
   DevBuf<unsigned char> ws[24];
   template <typename T>
-  cudaError_t scratch(int slot, long long n, T** out) {
+  cudaError_t scratch(int slot, long long n, T** out, cudaStream_t st) {
     const long long bytes = (long long)sizeof(T) * (n > 0 ? n : 1);
     if (ws[slot].n < bytes) {
-      cudaError_t e = ws[slot].alloc(bytes + bytes / 2, stream);
+      // the old buffer is freed in order on the requesting stream: every
+      // earlier user (plan stream or generator stream) is ordered before it
+      ws[slot].s = st;
+      cudaError_t e = ws[slot].alloc(bytes + bytes / 2, st);
       if (e != cudaSuccess) return e;
     }
     *out = reinterpret_cast<T*>(ws[slot].p);
     return cudaSuccess;
+  }
+  template <typename T>
+  cudaError_t scratch(int slot, long long n, T** out) { return scratch(slot, n, out, stream); }
+  // Auxiliary streams of this generator (created on its device by
+  // cursor_build): the component-order shuffle, planning, chunk seeds. The
+  // first plan after the cursor layout waits only for the component totals
+  // (ev_tot), so matching and the count-level plan overlap the per-key
+  // cursor shuffles; every later plan is ordered after all work on `stream`.
+  cudaStream_t ostream = nullptr, pstream = nullptr, sstream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_order = nullptr, ev_tot = nullptr, ev_ready = nullptr;
+  cudaEvent_t ev_plan = nullptr, ev_seg = nullptr, ev_seed_fork = nullptr, ev_seed = nullptr;
+  bool fresh_layout = false;  // no work on `stream` since cursor_build except the layout itself
+  int aux_dev = -1;
+  cudaError_t aux_init() {  // streams shared per device, events pooled (capi.cu)
+    if (ostream) return cudaSuccess;
+    cudaError_t e = cudaGetDevice(&aux_dev);
+    cudaStream_t st[3];
+    if (e == cudaSuccess) e = aux_streams(aux_dev, st);
+    if (e != cudaSuccess) return e;
+    ostream = st[0];
+    pstream = st[1];
+    sstream = st[2];
+    for (cudaEvent_t* x : {&ev_fork, &ev_order, &ev_tot, &ev_ready, &ev_plan, &ev_seg, &ev_seed_fork, &ev_seed})
+      if (e == cudaSuccess) e = aux_event_take(aux_dev, x);
+    return e;
   }
   // pinned host mirror of a small plan's result (one D2H per call)
   unsigned char* h_small = nullptr;
@@ -156,6 +209,8 @@ struct GenData {
   long long h_small_cap = 0, h_small_slots = 0;  // layout of the mirror
   ~GenData() {
     if (h_small) cudaFreeHost(h_small);
+    for (cudaEvent_t x : {ev_fork, ev_order, ev_tot, ev_ready, ev_plan, ev_seg, ev_seed_fork, ev_seed})
+      if (x) aux_event_give(aux_dev, x);
   }
 };
 
@@ -164,7 +219,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
                  cudaStream_t s, GenData* g);
 int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, long long* n_out);
 int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long long* n_out);
-int index_finalize(IndexData* ix, long long I, cudaStream_t s);
+int index_finalize(IndexData* ix, long long I, cudaStream_t s, bool defer = false);
 int rows_build(const mx_rows_desc* d, cudaStream_t s, IndexData* out);
 int index_block_table(const IndexData* ix, u32 file_base, uint4* out, cudaStream_t s);
 int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream_t s, IndexData* out);

@@ -265,7 +265,7 @@ __device__ __forceinline__ void direct_tile(const S1Args& a, const TileMeta* __r
 #pragma unroll
       for (int j = 0; j < SEGS; ++j) {
         const long long i = wbase + 128 * j + 4 * lane;
-        if (i + 4 <= a.n) {
+        if (a.vec_ok && i + 4 <= a.n) {
           const int4 x = codes4(a, p, i);
           add(j, 0, lut_get<SMEM_LUT>(s_lut, a.lut, lo + x.x));
           add(j, 1, lut_get<SMEM_LUT>(s_lut, a.lut, lo + x.y));

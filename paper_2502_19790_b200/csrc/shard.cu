@@ -33,7 +33,7 @@
 
 namespace mx {
 
-int index_finalize(IndexData* ix, long long I, cudaStream_t s);
+// (index_finalize: mixtera_internal.cuh)
 
 __global__ void block_table_kernel(long long B, const u32* blk_key, const u32* key_packed, const u32* blk_file,
                                    const u32* blk_first, const u64* iv_cum, u32 file_base, uint4* out) {

@@ -43,6 +43,7 @@ constexpr u32 FAIL = 0x80000000u;
 struct S1Args {
   const int32_t* cols[MX_MAX_PROPS];  // int32 codes, or u16 codes when u16 (row-tuple layout)
   int u16;
+  int vec_ok;            // every column aligned for 4-code vector loads
   int lut_off[MX_MAX_PROPS + 1];
   int n_props;
   const u32* lut;  // device copy of the concatenated LUT
@@ -419,6 +420,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   bool aligned = true;
   for (int p = 0; p < NC; ++p) aligned &= (reinterpret_cast<uintptr_t>(d->columns[p]) % (a.u16 ? 8 : 16)) == 0;
   const long long nstaged = aligned ? n / tile_len : 0;
+  a.vec_ok = aligned;
   DevBuf<TileMeta> tmeta;
   DevBuf<int> seg_fa;
   DevBuf<u32> rk, rf, rs, re;
@@ -558,7 +560,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   } else {
     ix.iv_key.take(k2); ix.iv_file.take(f2); ix.iv_start.take(s2); ix.iv_end.take(e2);
   }
-  return index_finalize(&ix, I, s);
+  return index_finalize(&ix, I, s, /*defer=*/true);
 }
 
 // key / block boundaries: value = (key change << 32) | (key or file change);
@@ -607,6 +609,15 @@ struct CumF {
   __device__ void total(u64) const {}
 };
 
+// blk_first[B] = I, key_blk_first[K] = B from the device totals
+__global__ void sentinel_kernel(const u64* totals, u32 I, u32* blk_first, u32* key_blk_first) {
+  if (threadIdx.x != 0) return;
+  const u64 t = *totals;
+  const u32 K = (u32)(t >> 32), B = (u32)(t & 0xffffffffull);
+  blk_first[B] = I;
+  key_blk_first[K] = B;
+}
+
 // max over keys of (blocks of the key); totals = (n_keys << 32) | n_blocks
 __global__ void key_maxblk_kernel(const u32* key_blk_first, const u64* totals, u32* out) {
   const u64 t = *totals;
@@ -625,7 +636,7 @@ __global__ void key_maxblk_kernel(const u32* key_blk_first, const u64* totals, u
 // (iv_key, iv_file, iv_start, iv_end) sorted by (packed key, file, start):
 // blk_*, key_*, iv_cum, n_keys, n_blocks. IndexBuildError on an empty or
 // overlapping interval (index.py:32-47).
-int index_finalize(IndexData* ixp, long long I, cudaStream_t s) {
+int index_finalize(IndexData* ixp, long long I, cudaStream_t s, bool defer) {
   IndexData& ix = *ixp;
   ix.n_intervals = I;
   if (I == 0) {
@@ -662,6 +673,28 @@ int index_finalize(IndexData* ixp, long long I, cudaStream_t s) {
   key_maxblk_kernel<<<64, 256, 0, s>>>(ix.key_blk_first.p, scratch64.p, maxblk.p);
   mx_count_launch();
   MX_CUDA_TRY(cudaGetLastError());
+  if (defer) {
+    // no host wait: sizes land in a pinned slot, the sentinels are written
+    // from the device totals, ix_resolve() completes the sizes on first use
+    IndexData::Pending* slot = pend_slot_take();
+    int dev = 0;
+    cudaEvent_t ev = nullptr;
+    if (slot && cudaGetDevice(&dev) == cudaSuccess && aux_event_take(dev, &ev) == cudaSuccess) {
+      MX_CUDA_TRY(cudaMemcpyAsync(&slot->maxblk, maxblk.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+      MX_CUDA_TRY(cudaMemcpyAsync(&slot->totals, scratch64.p, sizeof(u64), cudaMemcpyDeviceToHost, s));
+      MX_CUDA_TRY(cudaMemcpyAsync(&slot->samples, ix.iv_cum.p + I, sizeof(u64), cudaMemcpyDeviceToHost, s));
+      MX_CUDA_TRY(cudaMemcpyAsync(&slot->err, err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
+      MX_CUDA_TRY(cudaEventRecord(ev, s));
+      sentinel_kernel<<<1, 32, 0, s>>>(scratch64.p, (u32)I, ix.blk_first.p, ix.key_blk_first.p);
+      mx_count_launch();
+      MX_CUDA_TRY(cudaGetLastError());
+      ix.pend = slot;
+      ix.pend_ev = ev;
+      ix.pend_dev = dev;
+      return MX_OK;
+    }
+    if (slot) pend_slot_give(slot);
+  }
   u64 tot = 0, samples = 0;
   u32 h_maxblk = 0;
   {

@@ -70,24 +70,40 @@ __device__ __forceinline__ bool mkey_matches(const MatchArgs& a, int m, u32 pack
   return true;
 }
 
-// one CTA per mixture key: count matches, and the per-component hit counts
-__global__ void match_count_kernel(MatchArgs a, u32* L_cnt, u32* comp_hits) {
+// one CTA per mixture key: count matches, the per-component hit counts and
+// the key's stream length (remaining samples of its matching components).
+// Order-free (components by rank), so it need not wait for the component
+// order shuffle.
+__global__ void match_count_kernel(MatchArgs a, u32* L_cnt, u32* comp_hits, const u64* comp_total,
+                                   const u64* consumed, u64* m_tot) {
   __shared__ u32 s_cnt;
+  __shared__ unsigned long long s_tot;
   const int m = blockIdx.x;
-  if (threadIdx.x == 0) s_cnt = 0;
+  if (threadIdx.x == 0) {
+    s_cnt = 0;
+    s_tot = 0;
+  }
   __syncthreads();
   u32 c = 0;
-  for (long long pos = threadIdx.x; pos < a.K; pos += blockDim.x) {
-    u32 comp = a.comp_order[pos];
+  u64 t = 0;
+  for (long long comp = threadIdx.x; comp < a.K; comp += blockDim.x) {
     if (mkey_matches(a, m, a.key_packed[comp])) {
       ++c;
+      t += comp_total[comp] - consumed[comp];
       atomicAdd(comp_hits + comp, 1u);
     }
   }
   c = warp_sum(c);
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, c);
+  t = warp_sum(t);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_cnt, c);
+    atomicAdd(&s_tot, (unsigned long long)t);
+  }
   __syncthreads();
-  if (threadIdx.x == 0) L_cnt[m] = s_cnt;
+  if (threadIdx.x == 0) {
+    L_cnt[m] = s_cnt;
+    m_tot[m] = s_tot;
+  }
 }
 
 // one CTA per mixture key: ordered compaction of matching components
@@ -399,7 +415,7 @@ __global__ void plan_kernel(PlanArgs a) {
   if (staged) {
     for (int m = threadIdx.x; m < Km; m += blockDim.x) {
       s_w[m] = a.w[m];
-      if (a.mode == 0) s_len[m] = a.seg_pre[a.s_off[m + 1] + m];
+      if (a.mode == 0) s_len[m] = a.slen ? a.slen[m] : a.seg_pre[a.s_off[m + 1] + m];
     }
     __syncwarp();
   }
@@ -1923,7 +1939,7 @@ struct PlanWork {  // stream segment tables (generator scratch slots)
 };
 
 enum ScratchSlot { S_WTS, S_SOFF, S_SEGC, S_SEGLO, S_SEGPRE, S_PHASES, S_TERMS, S_LL, S_OUT, S_REPORT, S_FLAGS,
-                   S_POS, S_APIDX, S_APFRAC, S_FRONT, S_GM, S_GF, S_GS, S_GE, S_OVF, S_CNT, S_HDR };
+                   S_POS, S_APIDX, S_APFRAC, S_FRONT, S_GM, S_GF, S_GS, S_GE, S_OVF, S_CNT, S_HDR, S_MTOT };
 
 // Emission of a planned batch. Only ONE host synchronisation (at the end):
 // the pair prefix comes from the host copy of the phases, and the piece /
@@ -1943,13 +1959,10 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(g->res_id.reserve(n_chunks > 0 ? n_chunks : 1, s));
   // chunk seeds depend only on chunk ids: hash them on a side stream while
   // the pieces are cut, normalised and compacted on `s`
-  static thread_local cudaStream_t seed_side = nullptr;
-  static thread_local cudaEvent_t seed_fork = nullptr, seed_join = nullptr;
-  if (!seed_side) {
-    MX_CUDA_TRY(cudaStreamCreateWithFlags(&seed_side, cudaStreamNonBlocking));
-    MX_CUDA_TRY(cudaEventCreateWithFlags(&seed_fork, cudaEventDisableTiming));
-    MX_CUDA_TRY(cudaEventCreateWithFlags(&seed_join, cudaEventDisableTiming));
-  }
+  // (per-generator stream and events: created on the generator's device)
+  MX_CUDA_TRY(g->aux_init());
+  cudaStream_t seed_side = g->sstream;
+  cudaEvent_t seed_fork = g->ev_seed_fork, seed_join = g->ev_seed;
   if (n_chunks > 0) {
     MX_CUDA_TRY(cudaEventRecord(seed_fork, s));
     MX_CUDA_TRY(cudaStreamWaitEvent(seed_side, seed_fork, 0));
@@ -2094,8 +2107,24 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   return MX_OK;
 }
 
+// per mixture key the matching components IN COMPONENT ORDER
+// (chunks.py:139-141): waits for the component-order shuffle
+static cudaError_t match_fill(GenData* g, const MatchArgs& ma, cudaStream_t s) {
+  if (ma.K <= 0) return cudaSuccess;
+  if (g->ev_order) {
+    cudaError_t e = cudaStreamWaitEvent(s, g->ev_order, 0);
+    if (e != cudaSuccess) return e;
+  }
+  match_fill_kernel<<<ma.Km, 256, 0, s>>>(ma, g->match_L_off.p, g->match_L.p);
+  mx_count_launch();
+  return cudaGetLastError();
+}
+
 int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, long long* n_out) {
-  cudaStream_t s = g->stream;
+  // Matching and the count-level plan run on the generator's plan stream;
+  // emission runs on the generator's stream (`ms`) after it waits for them.
+  const cudaStream_t ms = g->stream;
+  cudaStream_t s = g->pstream;
   IndexData* ix = g->ix;
   const int Km = mix->n_mkeys;
   const long long K = g->K;
@@ -2106,6 +2135,21 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     return mx_fail(MX_ERR_MIXTURE, "chunk size %lld below the number of mixture keys (%d)", (long long)mix->chunk_size, Km);
   g->report.assign(Km, 0);
   g->last_mkeys = Km;
+  if (!s) {  // empty index: no auxiliary streams
+    MX_CUDA_TRY(g->aux_init());
+    s = g->pstream;
+  }
+  // the first plan after the cursor layout needs only the component totals
+  // (recorded before the per-key shuffles); later plans see everything
+  if (g->fresh_layout && g->ev_tot) {
+    MX_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_tot, 0));
+  } else {
+    MX_CUDA_TRY(cudaEventRecord(g->ev_ready, ms));
+    MX_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_ready, 0));
+  }
+  const bool fresh = g->fresh_layout;
+  g->fresh_layout = false;
+  const bool small = max_chunks <= SMALL_MAX_CHUNKS && mix->chunk_size <= NM_CAP;
   std::unique_ptr<MxPhase> ph_plan(new MxPhase("plan", s));
   // ---- matching
   MatchArgs ma{};
@@ -2121,7 +2165,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   }
   ma.allow_words = mix->allow_words;
   double* wts_p = nullptr;
-  MX_CUDA_TRY(g->scratch(S_WTS, Km, &wts_p));
+  MX_CUDA_TRY(g->scratch(S_WTS, Km, &wts_p, s));
   MX_CUDA_TRY(mx_h2d(wts_p, mix->weights, sizeof(double) * Km, s));
   // matching depends only on the mixture KEYS (not the weights): reuse the
   // previous plan's per-key component lists when the keys are unchanged
@@ -2131,8 +2175,14 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
                       (int)g->match_base.size() == ix->n_props &&
                       std::equal(g->match_base.begin(), g->match_base.end(), mix->allow_base) &&
                       std::equal(g->match_allow.begin(), g->match_allow.end(), mix->allow);
+  // early plan: a disjoint mixture of few keys is planned from the stream
+  // LENGTHS alone (no component order needed); its ordered segment tables
+  // are built after the component-order shuffle, while the host reads the plan
+  bool early = false;
+  u64* m_tot = nullptr;
+  DevBuf<u32> allow;
   if (!cached) {
-    DevBuf<u32> allow, L_cnt, hits;
+    DevBuf<u32> L_cnt, hits;
     MX_CUDA_TRY(allow.alloc((long long)n_allow, s));
     MX_CUDA_TRY(mx_h2d(allow.p, mix->allow, sizeof(u32) * n_allow, s));
     ma.allow = allow.p;
@@ -2140,8 +2190,10 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     MX_CUDA_TRY(cudaMemsetAsync(L_cnt.p, 0, sizeof(u32) * Km, s));  // stays 0 for an empty index
     MX_CUDA_TRY(hits.alloc(K > 0 ? K : 1, s));
     MX_CUDA_TRY(cudaMemsetAsync(hits.p, 0, sizeof(u32) * (K > 0 ? K : 1), s));
+    MX_CUDA_TRY(g->scratch(S_MTOT, Km, &m_tot, s));
+    MX_CUDA_TRY(cudaMemsetAsync(m_tot, 0, sizeof(u64) * Km, s));
     if (K > 0) {
-      match_count_kernel<<<Km, 256, 0, s>>>(ma, L_cnt.p, hits.p);
+      match_count_kernel<<<Km, 256, 0, s>>>(ma, L_cnt.p, hits.p, g->comp_total.p, g->consumed.p, m_tot);
       mx_count_launch();
     }
     std::vector<u32> h_cnt(Km), h_hits(K > 0 ? K : 1, 0);
@@ -2158,10 +2210,8 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     MX_CUDA_TRY(g->match_L_off.alloc(Km + 1, s));
     MX_CUDA_TRY(mx_h2d(g->match_L_off.p, g->match_off.data(), sizeof(u32) * (Km + 1), s));
     MX_CUDA_TRY(g->match_L.alloc(g->match_off[Km] > 0 ? g->match_off[Km] : 1, s));
-    if (K > 0) {
-      match_fill_kernel<<<Km, 256, 0, s>>>(ma, g->match_L_off.p, g->match_L.p);
-      mx_count_launch();
-    }
+    early = fresh && !g->match_shared && Km <= PLAN_SMEM_KM && !small && getenv("MX_PLAN_LATE") == nullptr;
+    if (!early) MX_CUDA_TRY(match_fill(g, ma, s));
     g->match_allow.assign(mix->allow, mix->allow + n_allow);
     g->match_base.assign(mix->allow_base, mix->allow_base + ix->n_props);
     g->match_words = mix->allow_words;
@@ -2177,21 +2227,23 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     w.n_streams = Km;
     w.s_off = L_off.p;
     const long long nseg = h_off[Km];
-    MX_CUDA_TRY(g->scratch(S_SEGC, nseg, &w.seg_comp));
-    MX_CUDA_TRY(g->scratch(S_SEGLO, nseg, &w.seg_lo));
-    MX_CUDA_TRY(g->scratch(S_SEGPRE, nseg + Km, &w.seg_pre));
-    build_segments_kernel<<<(Km + 3) / 4, 128, 0, s>>>(0, Km, w.s_off, L.p, g->comp_total.p, g->consumed.p,
-                                                          w.seg_comp, w.seg_lo, w.seg_pre);
-    mx_count_launch();
+    MX_CUDA_TRY(g->scratch(S_SEGC, nseg, &w.seg_comp, s));
+    MX_CUDA_TRY(g->scratch(S_SEGLO, nseg, &w.seg_lo, s));
+    MX_CUDA_TRY(g->scratch(S_SEGPRE, nseg + Km, &w.seg_pre, s));
+    if (!early) {
+      build_segments_kernel<<<(Km + 3) / 4, 128, 0, s>>>(0, Km, w.s_off, L.p, g->comp_total.p, g->consumed.p,
+                                                            w.seg_comp, w.seg_lo, w.seg_pre);
+      mx_count_launch();
+    }
   } else {
     w.n_streams = (int)K;
     std::vector<u32> so(K + 1);
     for (long long c = 0; c <= K; ++c) so[c] = (u32)c;
-    MX_CUDA_TRY(g->scratch(S_SOFF, K + 1, &w.s_off));
+    MX_CUDA_TRY(g->scratch(S_SOFF, K + 1, &w.s_off, s));
     MX_CUDA_TRY(mx_h2d(w.s_off, so.data(), sizeof(u32) * (K + 1), s));
-    MX_CUDA_TRY(g->scratch(S_SEGC, K, &w.seg_comp));
-    MX_CUDA_TRY(g->scratch(S_SEGLO, K, &w.seg_lo));
-    MX_CUDA_TRY(g->scratch(S_SEGPRE, 2 * K, &w.seg_pre));
+    MX_CUDA_TRY(g->scratch(S_SEGC, K, &w.seg_comp, s));
+    MX_CUDA_TRY(g->scratch(S_SEGLO, K, &w.seg_lo, s));
+    MX_CUDA_TRY(g->scratch(S_SEGPRE, 2 * K, &w.seg_pre, s));
     build_segments_kernel<<<(unsigned)std::min<long long>((K + 3) / 4, 148 * 16), 128, 0, s>>>(1, (int)K, w.s_off, nullptr, g->comp_total.p,
                                                                       g->consumed.p, w.seg_comp, w.seg_lo,
                                                                       w.seg_pre);
@@ -2218,17 +2270,17 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   struct { int* p; } ap_idx;
   struct { double* p; } ap_frac;
   struct { u32* p; } front;
-  MX_CUDA_TRY(g->scratch(S_PHASES, cap_phases, &phases.p));
+  MX_CUDA_TRY(g->scratch(S_PHASES, cap_phases, &phases.p, s));
   MX_CUDA_TRY(cudaMemsetAsync(phases.p, 0, sizeof(Phase) * cap_phases, s));  // copied back whole
-  MX_CUDA_TRY(g->scratch(S_TERMS, cap_terms, &terms.p));
-  MX_CUDA_TRY(g->scratch(S_LL, 5LL * Km, &scratch_ll.p));
-  MX_CUDA_TRY(g->scratch(S_OUT, 4, &out.p));
-  MX_CUDA_TRY(g->scratch(S_REPORT, Km, &report.p));
-  MX_CUDA_TRY(g->scratch(S_FLAGS, 2LL * Km, &flags.p));
-  MX_CUDA_TRY(g->scratch(S_POS, Km, &pos.p));
-  MX_CUDA_TRY(g->scratch(S_APIDX, Km, &ap_idx.p));
-  MX_CUDA_TRY(g->scratch(S_APFRAC, Km, &ap_frac.p));
-  MX_CUDA_TRY(g->scratch(S_FRONT, Km, &front.p));
+  MX_CUDA_TRY(g->scratch(S_TERMS, cap_terms, &terms.p, s));
+  MX_CUDA_TRY(g->scratch(S_LL, 5LL * Km, &scratch_ll.p, s));
+  MX_CUDA_TRY(g->scratch(S_OUT, 4, &out.p, s));
+  MX_CUDA_TRY(g->scratch(S_REPORT, Km, &report.p, s));
+  MX_CUDA_TRY(g->scratch(S_FLAGS, 2LL * Km, &flags.p, s));
+  MX_CUDA_TRY(g->scratch(S_POS, Km, &pos.p, s));
+  MX_CUDA_TRY(g->scratch(S_APIDX, Km, &ap_idx.p, s));
+  MX_CUDA_TRY(g->scratch(S_APFRAC, Km, &ap_frac.p, s));
+  MX_CUDA_TRY(g->scratch(S_FRONT, Km, &front.p, s));
   MX_CUDA_TRY(cudaMemsetAsync(front.p, 0, sizeof(u32) * Km, s));
   MX_CUDA_TRY(cudaMemsetAsync(report.p, 0, sizeof(long long) * Km, s));
   PlanArgs pa{};
@@ -2238,6 +2290,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   pa.strict = mix->strict;
   pa.max_chunks = max_chunks;
   pa.w = wts_p;
+  pa.slen = early ? m_tot : nullptr;  // early plan: stream lengths from the matching pass
   pa.seg_pre = w.seg_pre;
   pa.s_off = w.s_off;
   pa.L_off = L_off.p;
@@ -2333,8 +2386,12 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     plan_kernel<<<1, 32, 0, s>>>(pa);
   }
   mx_count_launch();
-  if (max_chunks <= SMALL_MAX_CHUNKS && mix->chunk_size <= NM_CAP) {
+  if (small) {
     // small plan: emission driven by device-side counts, one host sync
+    MX_CUDA_TRY(cudaEventRecord(g->ev_seg, s));
+    MX_CUDA_TRY(cudaStreamWaitEvent(ms, g->ev_seg, 0));
+    ph_plan.reset();
+    s = ms;
     if (w.mode == 0) {
       commit_segments_kernel<<<Km, 128, 0, s>>>(Km, w.s_off, w.seg_comp, w.seg_lo, w.seg_pre, pos.p,
                                                 g->consumed.p);
@@ -2364,13 +2421,13 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     struct { u32* p; } gm, gf, gs, ge, ovf;
     struct { u64* p; } cnt;
     struct { long long* p; } header;
-    MX_CUDA_TRY(g->scratch(S_GM, slots, &gm.p));
-    MX_CUDA_TRY(g->scratch(S_GF, slots, &gf.p));
-    MX_CUDA_TRY(g->scratch(S_GS, slots, &gs.p));
-    MX_CUDA_TRY(g->scratch(S_GE, slots, &ge.p));
-    MX_CUDA_TRY(g->scratch(S_OVF, 1, &ovf.p));
-    MX_CUDA_TRY(g->scratch(S_CNT, max_chunks, &cnt.p));
-    MX_CUDA_TRY(g->scratch(S_HDR, 3, &header.p));
+    MX_CUDA_TRY(g->scratch(S_GM, slots, &gm.p, s));
+    MX_CUDA_TRY(g->scratch(S_GF, slots, &gf.p, s));
+    MX_CUDA_TRY(g->scratch(S_GS, slots, &gs.p, s));
+    MX_CUDA_TRY(g->scratch(S_GE, slots, &ge.p, s));
+    MX_CUDA_TRY(g->scratch(S_OVF, 1, &ovf.p, s));
+    MX_CUDA_TRY(g->scratch(S_CNT, max_chunks, &cnt.p, s));
+    MX_CUDA_TRY(g->scratch(S_HDR, 3, &header.p, s));
     MX_CUDA_TRY(cudaMemsetAsync(ovf.p, 0, sizeof(u32), s));
     MX_CUDA_TRY(g->res_off.reserve(max_chunks + 1, s));
     MX_CUDA_TRY(g->res_seed.reserve(max_chunks, s));
@@ -2434,9 +2491,24 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     MX_CUDA_TRY(rb.add(h_out, out.p, sizeof(h_out)));
     MX_CUDA_TRY(rb.add(g->report.data(), report.p, sizeof(long long) * Km));
     MX_CUDA_TRY(rb.add(h_phases.data(), phases.p, sizeof(Phase) * cap_phases));
-    MX_CUDA_TRY(rb.sync());
+    if (early) {
+      // the plan's result travels while the ordered lists and segment tables
+      // are built behind the component-order shuffle
+      MX_CUDA_TRY(cudaEventRecord(g->ev_plan, s));
+      MX_CUDA_TRY(match_fill(g, ma, s));
+      build_segments_kernel<<<(Km + 3) / 4, 128, 0, s>>>(0, Km, w.s_off, L.p, g->comp_total.p, g->consumed.p,
+                                                            w.seg_comp, w.seg_lo, w.seg_pre);
+      mx_count_launch();
+      MX_CUDA_TRY(cudaGetLastError());
+      MX_CUDA_TRY(rb.sync_event(g->ev_plan));
+    } else {
+      MX_CUDA_TRY(rb.sync());
+    }
   }
   ph_plan.reset();
+  MX_CUDA_TRY(cudaEventRecord(g->ev_seg, s));
+  MX_CUDA_TRY(cudaStreamWaitEvent(ms, g->ev_seg, 0));
+  s = ms;
   if (w.mode == 0) {
     commit_segments_kernel<<<Km, 128, 0, s>>>(Km, w.s_off, w.seg_comp, w.seg_lo, w.seg_pre, pos.p,
                                               g->consumed.p);

@@ -156,10 +156,7 @@ class ChunkerIndex:
         self.catalog = catalog
         self.codec = catalog.codec
         self.stream = stream
-        L = _lib.lib()
-        k, b, i, n = (C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64())
-        _lib.check(L.mx_index_sizes(self._h, C.byref(k), C.byref(b), C.byref(i), C.byref(n)))
-        self.n_keys, self.n_blocks, self.n_intervals, self.n_samples = k.value, b.value, i.value, n.value
+        self._sizes = None  # read on first use: the build returns before its sizes reach the host
         self._keys = None
         self._nested = None
         self._counts = None
@@ -169,6 +166,18 @@ class ChunkerIndex:
         if h is not None and h.value and _lib._handle is not None:
             _lib._handle.mx_index_free(h)
             self._h = None
+
+    def _size(self, i: int) -> int:
+        if self._sizes is None:
+            k, b, n_iv, n = (C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64())
+            _lib.check(_lib.lib().mx_index_sizes(self._h, C.byref(k), C.byref(b), C.byref(n_iv), C.byref(n)))
+            self._sizes = (k.value, b.value, n_iv.value, n.value)
+        return self._sizes[i]
+
+    n_keys = property(lambda self: self._size(0))
+    n_blocks = property(lambda self: self._size(1))
+    n_intervals = property(lambda self: self._size(2))
+    n_samples = property(lambda self: self._size(3))
 
     @property
     def handle(self) -> C.c_void_p:
