@@ -260,6 +260,46 @@ cudaError_t mx_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   return cudaEventRecord(ev, s);
 }
 
+cudaError_t mx_h2d_gather(void* dst, const void* const* src, const size_t* bytes, const size_t* off, int n,
+                          size_t total, cudaStream_t s) {
+  if (total == 0) return cudaSuccess;
+  PinnedRing& r = g_ring;
+  const size_t need = (total + 255) & ~size_t(255);
+  if (need > PinnedRing::kHalf || (!r.buf && cudaHostAlloc(reinterpret_cast<void**>(&r.buf), 2 * PinnedRing::kHalf,
+                                                            cudaHostAllocDefault) != cudaSuccess)) {
+    if (!r.buf) cudaGetLastError();
+    for (int i = 0; i < n; ++i) {  // no staging space: one copy per item
+      cudaError_t e = mx_h2d(static_cast<char*>(dst) + off[i], src[i], bytes[i], s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  if (r.used + need > PinnedRing::kHalf) {
+    r.half ^= 1;
+    r.used = 0;
+    for (cudaEvent_t e : r.pending[r.half]) {
+      cudaEventSynchronize(e);
+      r.pool.push_back(e);
+    }
+    r.pending[r.half].clear();
+  }
+  char* stage = r.buf + (size_t)r.half * PinnedRing::kHalf + r.used;
+  r.used += need;
+  for (int i = 0; i < n; ++i)
+    if (bytes[i]) memcpy(stage + off[i], src[i], bytes[i]);
+  cudaError_t e = cudaMemcpyAsync(dst, stage, total, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t ev;
+  if (!r.pool.empty()) {
+    ev = r.pool.back();
+    r.pool.pop_back();
+  } else if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) {
+    return e;
+  }
+  r.pending[r.half].push_back(ev);
+  return cudaEventRecord(ev, s);
+}
+
 // Keep memory freed with cudaFreeAsync cached in the device's default pool
 // (the default release threshold of 0 hands it back to the driver at every
 // synchronisation, which makes each job re-map gigabytes of HBM).
@@ -394,22 +434,7 @@ int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out) {
     d.str_base[p] = desc->key_string_base[p];
   }
   int rc = MX_OK;
-  // key strings for device BLAKE2b
-  {
-    int n_pieces = desc->n_columns > 0 ? desc->n_key_pieces : 0;
-    for (int p = 0; desc->n_columns <= 0 && p < desc->n_props && p < MX_MAX_PROPS; ++p) {
-      int card = (desc->lut_offsets[p + 1] - desc->lut_offsets[p]) - 1;
-      n_pieces = std::max(n_pieces, desc->key_string_base[p] + card);
-    }
-    const long long nbytes = desc->key_string_offsets[n_pieces];
-    cudaError_t e = d.str_off.alloc(n_pieces + 1, s);
-    if (e == cudaSuccess) e = d.str_bytes.alloc(nbytes > 0 ? nbytes : 1, s);
-    if (e == cudaSuccess)
-      e = mx_h2d(d.str_off.p, desc->key_string_offsets, sizeof(long long) * (n_pieces + 1), s);
-    if (e == cudaSuccess && nbytes > 0)
-      e = mx_h2d(d.str_bytes.p, desc->key_strings, nbytes, s);
-    if (e != cudaSuccess) rc = mx_fail_cuda(e, "key strings", __FILE__, __LINE__);
-  }
+  // key strings, LUTs and file tables are uploaded by stage1_build in one copy
   if (rc == MX_OK) rc = stage1_build(desc, s, &d);
   if (rc < 0) {
     delete ix;

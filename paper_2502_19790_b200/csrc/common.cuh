@@ -124,6 +124,27 @@ int mx_fail(int code, const char* fmt, ...);
 // stream-ordered upload of a (small) pageable host array through pinned
 // staging, without the implicit stream synchronisation of a pageable copy
 cudaError_t mx_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
+// several host arrays -> one device block with ONE copy (staged together in
+// the pinned ring); item i lands at dst + off[i]
+cudaError_t mx_h2d_gather(void* dst, const void* const* src, const size_t* bytes, const size_t* off, int n,
+                          size_t total, cudaStream_t s);
+struct Uploads {
+  static constexpr int kMax = 16;
+  const void* src[kMax];
+  size_t bytes[kMax], off[kMax];
+  int n = 0;
+  size_t total = 0;
+  size_t add(const void* p, size_t b) {  // offset of the item in the block (256-byte aligned)
+    const size_t o = (total + 255) & ~size_t(255);
+    src[n] = p;
+    bytes[n] = b;
+    off[n] = o;
+    ++n;
+    total = o + b;
+    return o;
+  }
+  cudaError_t run(void* dst, cudaStream_t s) const { return mx_h2d_gather(dst, src, bytes, off, n, total, s); }
+};
 
 // Small device->host reads gathered into a per-thread pinned block and
 // delivered after ONE stream synchronisation: a cudaMemcpyAsync into

@@ -35,6 +35,7 @@ struct DevBuf {
   T* p = nullptr;
   long long n = 0;
   cudaStream_t s = 0;
+  bool own = true;  // false: a view into a block owned elsewhere (borrow)
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -43,22 +44,30 @@ struct DevBuf {
     release();
     s = stream;
     n = count;
+    own = true;
     if (count <= 0) return cudaSuccess;
     return cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (size_t)count, stream);
+  }
+  void borrow(void* ptr, long long count) {
+    release();
+    p = reinterpret_cast<T*>(ptr);
+    n = count;
+    own = false;
   }
   cudaError_t reserve(long long count, cudaStream_t stream) {  // grow-only
     if (p && n >= count) return cudaSuccess;
     return alloc(count, stream);
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && own) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
+    own = true;
   }
   void take(DevBuf& o) {
     release();
-    p = o.p; n = o.n; s = o.s;
-    o.p = nullptr; o.n = 0;
+    p = o.p; n = o.n; s = o.s; own = o.own;
+    o.p = nullptr; o.n = 0; o.own = true;
   }
 };
 
@@ -85,6 +94,9 @@ struct IndexData {
   int32_t str_base[MX_MAX_PROPS] = {};
   DevBuf<uint8_t> str_bytes;
   DevBuf<long long> str_off;
+  // one device block holding the small per-build host uploads (key strings,
+  // file tables, LUTs: one copy); str_*, file_* may be views into it
+  DevBuf<uint8_t> consts;
   // file-sharded hybrid index (shard.cu): this rank's intervals + one
   // pseudo-interval per remote (key, file) block; files [file_lo, file_hi)
   // are local, iv_nreal = real intervals behind each entry (1 if local)

@@ -367,23 +367,39 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   for (int p = 0; p < NC; ++p) a.cols[p] = d->columns[p];
   for (int p = 0; p <= NC; ++p) a.lut_off[p] = d->lut_offsets[p];
   const int lut_total = d->lut_offsets[NC];
-  DevBuf<u32> lut;
-  MX_CUDA_TRY(lut.alloc(lut_total, s));
-  MX_CUDA_TRY(mx_h2d(lut.p, d->lut, sizeof(u32) * lut_total, s));
-  a.lut = lut.p;
   // sum-keying LUT: fail flag as a count above the key bits (needs key_bits +
   // bitlen(P) <= 31), see scan_direct_kernel
-  DevBuf<u32> lut_sum;
   int pbits = 0;
   while ((1 << pbits) <= NC) ++pbits;
   const bool sum_ok = d->key_bits + pbits <= 31;
+  std::vector<u32> ls;
   if (sum_ok) {
-    std::vector<u32> ls(lut_total);
+    ls.resize(lut_total);
     for (int i = 0; i < lut_total; ++i)
       ls[i] = (d->lut[i] & ~FAIL) + ((d->lut[i] >> 31) << d->key_bits);
-    MX_CUDA_TRY(lut_sum.alloc(lut_total, s));
-    MX_CUDA_TRY(mx_h2d(lut_sum.p, ls.data(), sizeof(u32) * lut_total, s));
-    a.lut_sum = lut_sum.p;
+  }
+  // key-string pieces (device BLAKE2b of the canonical key strings)
+  int n_pieces = d->n_columns > 0 ? d->n_key_pieces : 0;
+  for (int p = 0; d->n_columns <= 0 && p < d->n_props && p < MX_MAX_PROPS; ++p) {
+    const int card = (d->lut_offsets[p + 1] - d->lut_offsets[p]) - 1;
+    n_pieces = std::max(n_pieces, d->key_string_base[p] + card);
+  }
+  const long long str_nbytes = d->key_string_offsets[n_pieces];
+  // every small host array of the build in ONE device block and ONE copy
+  Uploads up;
+  const size_t o_soff = up.add(d->key_string_offsets, sizeof(long long) * (n_pieces + 1));
+  const size_t o_sbytes = up.add(d->key_strings, str_nbytes > 0 ? (size_t)str_nbytes : 0);
+  const size_t o_lut = up.add(d->lut, sizeof(u32) * lut_total);
+  const size_t o_lsum = up.add(ls.data(), sizeof(u32) * ls.size());
+  const size_t o_fds = up.add(d->file_ds, sizeof(int32_t) * d->n_files);
+  const size_t o_fid = up.add(d->file_ids, sizeof(long long) * d->n_files);
+  MX_CUDA_TRY(ix.consts.alloc((long long)up.total + 16, s));
+  MX_CUDA_TRY(up.run(ix.consts.p, s));
+  ix.str_off.borrow(ix.consts.p + o_soff, n_pieces + 1);
+  ix.str_bytes.borrow(ix.consts.p + o_sbytes, str_nbytes > 0 ? str_nbytes : 1);
+  a.lut = reinterpret_cast<const u32*>(ix.consts.p + o_lut);
+  if (sum_ok) {
+    a.lut_sum = reinterpret_cast<const u32*>(ix.consts.p + o_lsum);
     a.fail_limit = 1u << d->key_bits;
   }
   a.n = n;
@@ -391,12 +407,10 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   a.n_files = d->n_files;
   a.rank_mask = d->rank_mask;
   // file table copies (ds and ids are needed for exports and cursors)
-  MX_CUDA_TRY(ix.file_ds.alloc(d->n_files, s));
-  MX_CUDA_TRY(mx_h2d(ix.file_ds.p, d->file_ds, sizeof(int32_t) * d->n_files, s));
+  ix.file_ds.borrow(ix.consts.p + o_fds, d->n_files);
+  ix.file_ids.borrow(ix.consts.p + o_fid, d->n_files);
   ix.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
   ix.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
-  MX_CUDA_TRY(ix.file_ids.alloc(d->n_files, s));
-  MX_CUDA_TRY(mx_h2d(ix.file_ids.p, d->file_ids, sizeof(long long) * d->n_files, s));
 
   // ---- stage-1 pass variant (MX_SCAN = direct (default) | pipe | v1):
   //  direct: one CTA per 4096-sample tile, slot output (scan_direct_kernel)

@@ -508,6 +508,213 @@ __global__ void plan_kernel(PlanArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Fused matching + count-level plan for a mixture of <= 32 keys (the common
+// static / hierarchical case, e.g. cfg 2): ONE launch, no host round trip
+// between matching and planning, and the plan replay is lane-parallel (lane m
+// owns mixture key m) instead of one thread walking every key in turn.
+// Matching is order-free (per-key stream LENGTHS only), so this runs before
+// the component-order shuffle finishes; the ordered lists / segment tables are
+// built afterwards for emission. Same arithmetic as plan_kernel (mode 0):
+// CPython's sequential Neumaier sum, int(share + 1e-9), the (-frac, key)
+// leftover order, best-effort redistribution in key order, strict stop.
+// If any component matches two mixture keys (shared streams), out[4] = 1 and
+// nothing is planned: the caller takes the general path.
+constexpr int FP_THREADS = 1024;
+constexpr int FP_MAX_KM = 32;
+
+struct FusedPlanArgs {
+  MatchArgs ma;
+  const u64* comp_total;
+  const u64* consumed;
+  long long C;
+  int strict;
+  long long max_chunks;
+  const double* w;
+  u32* L_off;       // [Km + 1] matching components per key (prefix)
+  u64* pos;         // [Km] stream position after the plan
+  Phase* phases;
+  long long cap_phases;
+  Term* terms;
+  long long cap_terms;
+  long long* out;   // [0] chunks [1] phases [2] terms [3] exhausted [4] shared
+  long long* report;
+};
+
+// apportion over the lanes whose `skip` is false (apportion_add)
+__device__ __forceinline__ long long fp_apportion(double w, bool skip, bool mine, int Km, long long total) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0, c = 0.0;  // sequential Neumaier sum in key order, in every lane
+  for (int j = 0; j < Km; ++j) {
+    const double x = __shfl_sync(MX_FULL, w, j);
+    const int sk = __shfl_sync(MX_FULL, (int)skip, j);
+    if (sk) continue;
+    const double t = s + x;
+    if (fabs(s) >= fabs(x)) c += (s - t) + x;
+    else c += (x - t) + s;
+    s = t;
+  }
+  const double wsum = c != 0.0 ? s + c : s;
+  if (!(wsum > 0.0)) return 0;
+  const bool alive = mine && !skip;
+  long long base = 0;
+  double fr = 0.0;
+  if (alive) {
+    const double share = w / wsum * (double)total;
+    base = (long long)(share + 1e-9);
+    const double f = share - (double)base;
+    fr = f > 0.0 ? f : 0.0;
+  }
+  const long long left = total - warp_sum(base);
+  if (left > 0) {
+    long long rank = 0;  // alive keys before this one in (frac desc, key asc) order
+    for (int j = 0; j < Km; ++j) {
+      const double fj = __shfl_sync(MX_FULL, fr, j);
+      const int aj = !__shfl_sync(MX_FULL, (int)skip, j);
+      if (aj && (fj > fr || (fj == fr && j < lane))) ++rank;
+    }
+    if (alive && rank < left) base += 1;
+  }
+  return base;
+}
+
+__global__ void __launch_bounds__(FP_THREADS) plan_fused_kernel(FusedPlanArgs a) {
+  __shared__ u32 s_cnt[FP_MAX_KM];
+  __shared__ unsigned long long s_tot[FP_MAX_KM];
+  __shared__ int s_shared;
+  const int Km = a.ma.Km, tid = threadIdx.x;
+  if (tid < FP_MAX_KM) {
+    s_cnt[tid] = 0;
+    s_tot[tid] = 0;
+  }
+  if (tid == 0) s_shared = 0;
+  __syncthreads();
+  // ---- matching (order-free): per key count and remaining samples
+  for (long long comp = tid; comp < a.ma.K; comp += FP_THREADS) {
+    const u32 packed = a.ma.key_packed[comp];
+    int hit = -1, nm = 0;
+    for (int m = 0; m < Km; ++m)
+      if (mkey_matches(a.ma, m, packed)) {
+        hit = m;
+        ++nm;
+        atomicAdd(&s_cnt[m], 1u);
+      }
+    if (nm > 1) s_shared = 1;
+    if (nm == 1) atomicAdd(&s_tot[hit], (unsigned long long)(a.comp_total[comp] - a.consumed[comp]));
+  }
+  __syncthreads();
+  if (tid >= 32) return;
+  const int lane = tid;
+  if (lane == 0) {
+    u32 o = 0;
+    for (int m = 0; m < Km; ++m) {
+      a.L_off[m] = o;
+      o += s_cnt[m];
+    }
+    a.L_off[Km] = o;
+    a.out[4] = s_shared;
+  }
+  if (s_shared) {
+    if (lane == 0) a.out[0] = a.out[1] = a.out[2] = a.out[3] = 0;
+    return;
+  }
+  // ---- plan (warp 0; lane m = mixture key m)
+  const bool mine = lane < Km;
+  const double w = mine ? a.w[lane] : 0.0;
+  const u64 len = mine ? (u64)s_tot[lane] : 0;
+  u64 pos = 0;
+  const long long counts = fp_apportion(w, !mine, mine, Km, a.C);
+  long long chunks = 0, n_ph = 0, n_terms = 0, exhausted = 0, rem = 0, took = 0, report = 0;
+  while (chunks < a.max_chunks) {
+    if (n_ph >= a.cap_phases) break;
+    if (a.cap_terms - n_terms < (long long)Km) break;
+    // simulate one generate() (simulate_chunk, mode 0)
+    rem = mine ? counts : 0;
+    took = 0;
+    bool dead = !mine, ok = true;
+    while (true) {
+      if (!__any_sync(MX_FULL, rem > 0)) break;
+      long long found = -1;
+      if (rem > 0) {
+        const long long avail = (long long)(len - pos) - took;
+        const long long g = rem < avail ? rem : avail;
+        took += g;
+        rem -= g;
+        found = g;
+      }
+      u32 newly = __ballot_sync(MX_FULL, found == 0 && rem > 0);
+      if (!newly) continue;
+      if (a.strict) {
+        report = rem;
+        ok = false;
+        break;
+      }
+      while (newly) {  // newly exhausted keys in key order
+        const int m = __ffs(newly) - 1;
+        newly &= newly - 1;
+        if (lane == m) dead = true;
+        if (!__any_sync(MX_FULL, !dead)) {
+          report = rem;
+          ok = false;
+          break;
+        }
+        const long long rm = __shfl_sync(MX_FULL, rem, m);
+        if (rm > 0) rem += fp_apportion(w, dead, mine, Km, rm);
+        if (lane == m) rem = 0;
+      }
+      if (!ok) break;
+    }
+    if (!ok) {
+      pos += (u64)took;
+      exhausted = 1;
+      break;
+    }
+    // every key with took > 0 can serve floor(avail / took) chunks
+    long long rep = a.max_chunks - chunks;
+    if (took > 0) {
+      const long long r = (long long)(len - pos) / took;
+      if (r < rep) rep = r;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const long long o = __shfl_xor_sync(MX_FULL, rep, d);
+      rep = o < rep ? o : rep;
+    }
+    if (rep < 1) rep = 1;
+    const u32 tk = __ballot_sync(MX_FULL, took > 0);
+    const long long nt = __popc(tk);
+    if (took > 0) {
+      Term& tm = a.terms[n_terms + __popc(tk & ((1u << lane) - 1u))];
+      tm.m = (u32)lane;
+      tm.stream = (u32)lane;
+      tm.base = pos;
+      tm.len = (u64)took;
+      tm.stride = (u64)took;
+      pos += (u64)took * (u64)rep;
+    }
+    if (lane == 0) {
+      Phase& ph = a.phases[n_ph];
+      ph.chunk_begin = chunks;
+      ph.n_chunks = rep;
+      ph.term_begin = n_terms;
+      ph.n_terms = nt;
+    }
+    ++n_ph;
+    n_terms += nt;
+    chunks += rep;
+  }
+  if (mine) {
+    a.pos[lane] = pos;
+    if (exhausted) a.report[lane] = report;
+  }
+  if (lane == 0) {
+    a.out[0] = chunks;
+    a.out[1] = n_ph;
+    a.out[2] = n_terms;
+    a.out[3] = exhausted;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Many mixture keys (disjoint streams), e.g. cfg 5: 10k keys, Zipf weights.
 // One 1024-thread CTA. The per-key pass loops run in parallel; the best-effort
 // redistribution loop (chunks.py:223-229) is sequential by nature and runs on
@@ -2175,6 +2382,88 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
                       (int)g->match_base.size() == ix->n_props &&
                       std::equal(g->match_base.begin(), g->match_base.end(), mix->allow_base) &&
                       std::equal(g->match_allow.begin(), g->match_allow.end(), mix->allow);
+  // fused matching + plan (<= 32 keys, bulk): one launch, one host sync;
+  // a mixture with shared components falls through to the general path
+  if (!cached && Km <= FP_MAX_KM && !small && K > 0 && getenv("MX_PLAN_LATE") == nullptr) {
+    DevBuf<u32> f_allow;
+    MX_CUDA_TRY(f_allow.alloc((long long)n_allow, s));
+    MX_CUDA_TRY(mx_h2d(f_allow.p, mix->allow, sizeof(u32) * n_allow, s));
+    ma.allow = f_allow.p;
+    MX_CUDA_TRY(g->match_L_off.alloc(Km + 1, s));
+    long long cap_phases = 4 * (long long)Km + 64;
+    if (cap_phases > max_chunks + 1) cap_phases = max_chunks + 1;
+    const long long cap_terms = cap_phases * (long long)Km;
+    Phase* phases = nullptr;
+    Term* terms = nullptr;
+    long long *out = nullptr, *report = nullptr;
+    u64* pos = nullptr;
+    MX_CUDA_TRY(g->scratch(S_PHASES, cap_phases, &phases, s));
+    MX_CUDA_TRY(g->scratch(S_TERMS, cap_terms, &terms, s));
+    MX_CUDA_TRY(g->scratch(S_OUT, 5, &out, s));
+    MX_CUDA_TRY(g->scratch(S_REPORT, Km, &report, s));
+    MX_CUDA_TRY(g->scratch(S_POS, Km, &pos, s));
+    MX_CUDA_TRY(cudaMemsetAsync(phases, 0, sizeof(Phase) * cap_phases, s));
+    MX_CUDA_TRY(cudaMemsetAsync(report, 0, sizeof(long long) * Km, s));
+    FusedPlanArgs fa{};
+    fa.ma = ma;
+    fa.comp_total = g->comp_total.p;
+    fa.consumed = g->consumed.p;
+    fa.C = mix->chunk_size;
+    fa.strict = mix->strict;
+    fa.max_chunks = max_chunks;
+    fa.w = wts_p;
+    fa.L_off = g->match_L_off.p;
+    fa.pos = pos;
+    fa.phases = phases;
+    fa.cap_phases = cap_phases;
+    fa.terms = terms;
+    fa.cap_terms = cap_terms;
+    fa.out = out;
+    fa.report = report;
+    plan_fused_kernel<<<1, FP_THREADS, 0, s>>>(fa);
+    mx_count_launch();
+    MX_CUDA_TRY(cudaGetLastError());
+    long long h_out[5];
+    std::vector<Phase> h_phases(cap_phases);
+    std::vector<u32> h_loff(Km + 1);
+    {
+      D2HBatch rb(s);
+      MX_CUDA_TRY(rb.add(h_out, out, sizeof(h_out)));
+      MX_CUDA_TRY(rb.add(g->report.data(), report, sizeof(long long) * Km));
+      MX_CUDA_TRY(rb.add(h_phases.data(), phases, sizeof(Phase) * cap_phases));
+      MX_CUDA_TRY(rb.add(h_loff.data(), g->match_L_off.p, sizeof(u32) * (Km + 1)));
+      MX_CUDA_TRY(rb.sync());
+    }
+    if (h_out[4] == 0) {
+      g->match_off.assign(h_loff.begin(), h_loff.end());
+      g->match_shared = false;
+      MX_CUDA_TRY(g->match_L.alloc(h_loff[Km] > 0 ? h_loff[Km] : 1, s));
+      MX_CUDA_TRY(match_fill(g, ma, s));  // ordered lists, behind the component-order shuffle
+      g->match_allow.assign(mix->allow, mix->allow + n_allow);
+      g->match_base.assign(mix->allow_base, mix->allow_base + ix->n_props);
+      g->match_words = mix->allow_words;
+      PlanWork w;
+      w.mode = 0;
+      w.n_streams = Km;
+      w.s_off = g->match_L_off.p;
+      w.max_mkey = Km;
+      const long long nseg = h_loff[Km];
+      MX_CUDA_TRY(g->scratch(S_SEGC, nseg, &w.seg_comp, s));
+      MX_CUDA_TRY(g->scratch(S_SEGLO, nseg, &w.seg_lo, s));
+      MX_CUDA_TRY(g->scratch(S_SEGPRE, nseg + Km, &w.seg_pre, s));
+      build_segments_kernel<<<(Km + 3) / 4, 128, 0, s>>>(0, Km, w.s_off, g->match_L.p, g->comp_total.p,
+                                                            g->consumed.p, w.seg_comp, w.seg_lo, w.seg_pre);
+      mx_count_launch();
+      MX_CUDA_TRY(cudaEventRecord(g->ev_seg, s));
+      MX_CUDA_TRY(cudaStreamWaitEvent(ms, g->ev_seg, 0));
+      ph_plan.reset();
+      commit_segments_kernel<<<Km, 128, 0, ms>>>(Km, w.s_off, w.seg_comp, w.seg_lo, w.seg_pre, pos, g->consumed.p);
+      mx_count_launch();
+      if (int rc = emit(g, w, phases, h_phases.data(), terms, h_out[0], h_out[1], nseg, ms)) return rc;
+      *n_out = h_out[0];
+      return h_out[3] ? MX_EXHAUSTED : MX_OK;
+    }
+  }
   // early plan: a disjoint mixture of few keys is planned from the stream
   // LENGTHS alone (no component order needed); its ordered segment tables
   // are built after the component-order shuffle, while the host reads the plan
