@@ -588,18 +588,35 @@ __global__ void __launch_bounds__(FP_THREADS) plan_fused_kernel(FusedPlanArgs a)
   }
   if (tid == 0) s_shared = 0;
   __syncthreads();
-  // ---- matching (order-free): per key count and remaining samples
-  for (long long comp = tid; comp < a.ma.K; comp += FP_THREADS) {
-    const u32 packed = a.ma.key_packed[comp];
+  // ---- matching (order-free): per key count and remaining samples,
+  // aggregated per warp first (one shared atomic per warp and key: 64-bit
+  // shared atomics from every thread on a handful of addresses serialise)
+  const int lane0 = tid & 31;
+  for (long long b = tid - lane0; b < a.ma.K; b += FP_THREADS) {
+    const long long comp = b + lane0;
     int hit = -1, nm = 0;
-    for (int m = 0; m < Km; ++m)
-      if (mkey_matches(a.ma, m, packed)) {
-        hit = m;
-        ++nm;
-        atomicAdd(&s_cnt[m], 1u);
+    u64 t = 0;
+    if (comp < a.ma.K) {
+      const u32 packed = a.ma.key_packed[comp];
+      for (int m = 0; m < Km; ++m)
+        if (mkey_matches(a.ma, m, packed)) {
+          hit = m;
+          ++nm;
+        }
+      if (nm == 1) t = a.comp_total[comp] - a.consumed[comp];
+    }
+    if (__any_sync(MX_FULL, nm > 1)) {
+      if (lane0 == 0) s_shared = 1;
+      continue;
+    }
+    for (int m = 0; m < Km; ++m) {
+      const u32 c = __popc(__ballot_sync(MX_FULL, hit == m));
+      const u64 tm = warp_sum(hit == m ? t : (u64)0);
+      if (lane0 == 0 && c) {
+        atomicAdd(&s_cnt[m], c);
+        atomicAdd(&s_tot[m], (unsigned long long)tm);
       }
-    if (nm > 1) s_shared = 1;
-    if (nm == 1) atomicAdd(&s_tot[hit], (unsigned long long)(a.comp_total[comp] - a.consumed[comp]));
+    }
   }
   __syncthreads();
   if (tid >= 32) return;
@@ -2137,6 +2154,7 @@ finalize_small_kernel(const long long* plan_out, const u64* cnt, const u32* gm, 
 // ------------------------------------------------------------------ host
 struct PlanWork {  // stream segment tables (generator scratch slots)
   int mode = 0;
+  long long chunk_size = 0;  // samples per chunk (emission path choice)
   long long max_mkey = 0;  // exclusive bound of the pieces' mixture-key ids (0 = unknown)
   int n_streams = 0;
   u32* s_off = nullptr;
@@ -2214,6 +2232,13 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   a.lcnt = g->lcnt.p;
   a.lpos = g->lpos.p;
   a.lstart = g->lstart.p;
+  const long long cap = (long long)n_pairs + n_seg + ix->n_intervals + 1;
+  int fbits = 1, mbits = 1;
+  while ((1ll << fbits) < (long long)ix->n_files + 1) ++fbits;
+  while ((1ll << mbits) < w.max_mkey + 1) ++mbits;
+  static const bool no_pack = getenv("MX_NORM_NOPACK") != nullptr;
+  // not for a file-sharded (hybrid) index: its file ids are checked nowhere here
+  const bool pack = !no_pack && w.max_mkey > 0 && fbits + mbits <= 31 && g->lcnt.p == nullptr;
   DevBuf<u64> pair_off;
   MX_CUDA_TRY(pair_off.alloc(n_pairs + 1, s));
   const unsigned pb = (unsigned)((n_pairs + 255) / 256);
@@ -2223,7 +2248,6 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   // the same thread; the total lands in [n_pairs])
   if (int rc = excl_scan<u64>(pair_off.p, (long long)n_pairs, pair_off.p, s)) return rc;
   DevBuf<u32> pm, pf, ps, pe;
-  const long long cap = (long long)n_pairs + n_seg + ix->n_intervals + 1;
   MX_CUDA_TRY(pm.alloc(cap, s));
   MX_CUDA_TRY(pf.alloc(cap, s));
   MX_CUDA_TRY(ps.alloc(cap, s));
@@ -2267,12 +2291,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
     mx_count_launch();
     const long long wgrid = std::min<long long>((n_chunks + 7) / 8, 148 * 16);
     // pack (mkey, file, start) into one u64 when mkey and file ids fit 32 bits together
-    int fbits = 1, mbits = 1;
-    while ((1ll << fbits) < (long long)ix->n_files + 1) ++fbits;
-    while ((1ll << mbits) < w.max_mkey + 1) ++mbits;
-    static const bool no_pack = getenv("MX_NORM_NOPACK") != nullptr;
-    // not for a file-sharded (hybrid) index: its file ids are checked nowhere here
-    if (!no_pack && w.max_mkey > 0 && fbits + mbits <= 31 && g->lcnt.p == nullptr)  // keys < 2^63: never the ~0 padding
+    if (pack)  // keys < 2^63: never the ~0 padding
       normalize_warp_kernel<true><<<(unsigned)wgrid, 256, 0, s>>>(wlist.p, wcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p,
                                                                   mcnt.p, blist.p, bcnt.p, fbits);
     else
@@ -2444,6 +2463,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
       g->match_words = mix->allow_words;
       PlanWork w;
       w.mode = 0;
+      w.chunk_size = mix->chunk_size;
       w.n_streams = Km;
       w.s_off = g->match_L_off.p;
       w.max_mkey = Km;
@@ -2512,6 +2532,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   // ---- streams
   PlanWork w;
   w.mode = shared ? 1 : 0;
+  w.chunk_size = mix->chunk_size;
   if (w.mode == 0) {
     w.n_streams = Km;
     w.s_off = L_off.p;
@@ -2820,6 +2841,7 @@ int plan_arbitrary(GenData* g, long long chunk_size, long long max_chunks, long 
   g->report.clear();
   PlanWork w;
   w.mode = 2;
+  w.chunk_size = chunk_size;
   w.n_streams = 1;
   if (K == 0) {
     int rc = emit(g, w, nullptr, nullptr, nullptr, 0, 0, 0, s);
