@@ -249,11 +249,19 @@ class ChunkBatch:
             c._device_bytes = (blob[int(off[i]):int(off[i + 1])], None, c.mixture)
         return c
 
+    JSON_MAX_RANGES = 2048  # csrc/serialize.cu JS_CAP: larger chunks sort beyond shared memory
+
     def _json_ok(self) -> bool:
-        """Device JSON ranks keys in 16 bits (csrc/serialize.cu); wider key
-        sets serialise on the host."""
-        n = len(self._gen.index.component_keys()) if self.arbitrary else len(self.mkeys)
-        return n < 65536
+        """Device JSON ranks keys in 16 bits and sorts a chunk's ranges in
+        shared memory (csrc/serialize.cu); wider key sets or chunks of more
+        than JSON_MAX_RANGES ranges serialise on the host."""
+        ok = getattr(self, "_json_ok_v", None)
+        if ok is None:
+            n = len(self._gen.index.component_keys()) if self.arbitrary else len(self.mkeys)
+            off = self.to_host()["off"]
+            ok = n < 65536 and (self.n_chunks == 0 or int(np.diff(off).max()) <= self.JSON_MAX_RANGES)
+            self._json_ok_v = ok
+        return ok
 
     def _chunk(self, i: int) -> Chunk:
         c = self.chunk(i)

@@ -41,6 +41,7 @@ struct JsonArgs {
   int mix_len;
   u32* perm;                     // [R] sorted piece order (chunk-local indices)
   long long* chunk_len;          // [C] bytes per chunk
+  u32* too_big;                  // largest chunk beyond the shared-memory sort (0 = none)
   const long long* json_off;     // [C+1] byte offsets
   uint8_t* out;
 };
@@ -194,6 +195,10 @@ __global__ void __launch_bounds__(256) json_size_block_kernel(JsonArgs a, const 
     const long long c = big_list[bi];
     const long long base = a.off[c];
     const int n = (int)(a.off[c + 1] - base);
+    if (n > JS_CAP) {  // beyond the shared-memory sort: the caller serialises on the host
+      if (threadIdx.x == 0) atomicMax(a.too_big, (u32)n);
+      continue;
+    }
     int np = 64;
     while (np < n) np <<= 1;
     for (int i = threadIdx.x; i < np; i += blockDim.x) s_k[i] = i < n ? sort_key(a, base, i) : ~0ull;
@@ -309,8 +314,8 @@ int gen_result_json(GenData* g, const mx_json_desc* d, cudaStream_t s) {
   MX_CUDA_TRY(perm.alloc(R > 0 ? R : 1, s));
   MX_CUDA_TRY(len.alloc(C, s));
   MX_CUDA_TRY(blist.alloc(C, s));
-  MX_CUDA_TRY(bcnt.alloc(1, s));
-  MX_CUDA_TRY(cudaMemsetAsync(bcnt.p, 0, sizeof(u32), s));
+  MX_CUDA_TRY(bcnt.alloc(2, s));  // [big-chunk count, largest chunk beyond JS_CAP]
+  MX_CUDA_TRY(cudaMemsetAsync(bcnt.p, 0, 2 * sizeof(u32), s));
   JsonArgs a{};
   a.n_chunks = C;
   a.off = g->res_off.p;
@@ -330,6 +335,7 @@ int gen_result_json(GenData* g, const mx_json_desc* d, cudaStream_t s) {
   a.mix_len = d->mixture_len;
   a.perm = perm.p;
   a.chunk_len = len.p;
+  a.too_big = bcnt.p + 1;
   const long long wgrid = std::min<long long>((C + 7) / 8, 148 * 16);
   json_size_warp_kernel<<<(unsigned)wgrid, 256, 0, s>>>(a, blist.p, bcnt.p);
   mx_count_launch();
@@ -337,8 +343,16 @@ int gen_result_json(GenData* g, const mx_json_desc* d, cudaStream_t s) {
   mx_count_launch();
   if (int rc = excl_scan_ll(reinterpret_cast<const u64*>(len.p), C, g->json_off.p, s)) return rc;
   long long total = 0;
-  MX_CUDA_TRY(cudaMemcpyAsync(&total, g->json_off.p + C, sizeof(long long), cudaMemcpyDeviceToHost, s));
-  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  u32 too_big = 0;
+  {
+    D2HBatch rb(s);
+    MX_CUDA_TRY(rb.add(&total, g->json_off.p + C, sizeof(long long)));
+    MX_CUDA_TRY(rb.add(&too_big, bcnt.p + 1, sizeof(u32)));
+    MX_CUDA_TRY(rb.sync());
+  }
+  if (too_big)
+    return mx_fail(MX_ERR_UNSUPPORTED, "device JSON: a chunk has %u ranges (> %d); serialise it on the host", too_big,
+                   JS_CAP);
   MX_CUDA_TRY(g->json.reserve(total > 0 ? total : 1, s));
   a.json_off = g->json_off.p;
   a.out = g->json.p;

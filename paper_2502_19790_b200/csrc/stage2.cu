@@ -1496,19 +1496,6 @@ __global__ void emit_count_kernel(EmitArgs a, u64 n_pairs, u64* pair_cnt) {
   pair_cnt[pr] = walk_pair<false>(a, pr, nullptr, nullptr, nullptr, nullptr, nullptr, 0);
 }
 
-// thread per (chunk, term) pair; pairs of more than 32 pieces (iid layouts:
-// ~500 intervals per term) are listed for emit_write_warp_kernel
-__global__ void emit_write_kernel(EmitArgs a, u64 n_pairs, const u64* pair_off, u32* pm, u32* pf, u32* ps, u32* pe,
-                                  u32* long_list, u32* long_cnt, u32 warp_min) {
-  u64 pr = blockIdx.x * (u64)blockDim.x + threadIdx.x;
-  if (pr >= n_pairs) return;
-  if (pair_off[pr + 1] - pair_off[pr] > warp_min) {
-    long_list[atomicAdd(long_cnt, 1u)] = (u32)pr;
-    return;
-  }
-  walk_pair<true>(a, pr, nullptr, pm, pf, ps, pe, pair_off[pr]);
-}
-
 // Same, with each warp's pieces staged in shared memory: the 32 pairs of a
 // warp own one contiguous output range [pair_off[first], pair_off[last+1]),
 // so the lanes write their pieces there as 16-byte records and the warp then
@@ -1680,6 +1667,77 @@ constexpr int NM_THREADS = 256;
 constexpr int NMB_THREADS = 1024;  // normalize_kernel: one compare-exchange per thread per stage at 2048
 constexpr int NM_CAP = 2048;
 
+// Chunks of more than NM_CAP pieces (e.g. iid data with chunk_size >> 2048):
+// the whole CTA sorts the chunk's pieces in place in global memory with an
+// ascending-only bitonic network (the first step of every merge stage
+// compares i with i ^ (kk - 1)), so positions >= n act as +infinity and never
+// move; then one in-place merge pass in rounds of NMB_THREADS (a merged
+// range's slot never exceeds its first piece's index). `sm` is >= 8 words of
+// shared scratch.
+__device__ __forceinline__ bool gm_less(const u32* pm, const u32* pf, const u32* ps, u64 a, u64 b) {
+  if (pm[a] != pm[b]) return pm[a] < pm[b];
+  if (pf[a] != pf[b]) return pf[a] < pf[b];
+  return ps[a] < ps[b];
+}
+
+__device__ u32 sort_merge_global(u64 o0, u32 n, u32* pm, u32* pf, u32* ps, u32* pe, u32* sm) {
+  const u32 tid = threadIdx.x;
+  u32 np = 1;
+  while (np < n) np <<= 1;
+  for (u32 kk = 2; kk <= np; kk <<= 1) {
+    for (u32 j = kk >> 1; j > 0; j >>= 1) {
+      const bool flip = j == (kk >> 1);
+      for (u32 t = tid; t < np / 2; t += NMB_THREADS) {
+        const u32 i = (t / j) * 2 * j + (t % j);
+        const u32 l = flip ? (i | (kk - 1)) - (i & (kk - 1)) : i + j;  // flip: i ^ (kk - 1) within the block
+        if (l < n && gm_less(pm, pf, ps, o0 + l, o0 + i)) {
+          const u64 a = o0 + i, b = o0 + l;
+          u32 x = pm[a]; pm[a] = pm[b]; pm[b] = x;
+          x = pf[a]; pf[a] = pf[b]; pf[b] = x;
+          x = ps[a]; ps[a] = ps[b]; ps[b] = x;
+          x = pe[a]; pe[a] = pe[b]; pe[b] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // merge: head unless same (mkey, file) as the previous piece and contiguous
+  const int lane = tid & 31, warp = tid >> 5;
+  u32* s_w = sm;               // [32] warp head counts
+  u32* s_prev = sm + 32;       // previous round's last piece: mkey, file, end
+  u32 run = 0;                 // merged ranges so far
+  for (u32 b = 0; b < n; b += NMB_THREADS) {
+    const u32 i = b + tid;
+    const bool ok = i < n;
+    u32 m = 0, f = 0, st = 0, en = 0, pmk = 0, pfl = 0, pen = 0;
+    bool nxt_head = true;
+    if (ok) {
+      m = pm[o0 + i]; f = pf[o0 + i]; st = ps[o0 + i]; en = pe[o0 + i];
+      if (i > 0 && tid == 0) { pmk = s_prev[0]; pfl = s_prev[1]; pen = s_prev[2]; }
+      else if (i > 0) { pmk = pm[o0 + i - 1]; pfl = pf[o0 + i - 1]; pen = pe[o0 + i - 1]; }
+      if (i + 1 < n) nxt_head = !(pm[o0 + i + 1] == m && pf[o0 + i + 1] == f && ps[o0 + i + 1] == en);
+    }
+    const bool head = ok && (i == 0 || !(pmk == m && pfl == f && pen == st));
+    __syncthreads();  // every read of this round before any write
+    if (tid == NMB_THREADS - 1 || i == n - 1) { s_prev[0] = m; s_prev[1] = f; s_prev[2] = en; }
+    const u32 hb = __ballot_sync(MX_FULL, head);
+    if (lane == 0) s_w[warp] = __popc(hb);
+    __syncthreads();
+    u32 before = 0, tot = 0;
+    for (int w = 0; w < NMB_THREADS / 32; ++w) {
+      const u32 c = s_w[w];
+      before += w < warp ? c : 0;
+      tot += c;
+    }
+    const u32 upto = run + before + __popc(hb & ((2u << lane) - 1u));  // heads up to and including i
+    if (head) { pm[o0 + upto - 1] = m; pf[o0 + upto - 1] = f; ps[o0 + upto - 1] = st; }
+    if (ok && nxt_head) pe[o0 + upto - 1] = en;  // last piece of its range
+    run += tot;
+    __syncthreads();
+  }
+  return run;
+}
+
 __global__ void __launch_bounds__(NMB_THREADS)
 normalize_kernel(const u32* big_list, const u32* big_cnt, const u64* chunk_piece_off, u32* pm, u32* pf, u32* ps,
                  u32* pe, u64* merged_cnt, u32* too_big) {
@@ -1690,8 +1748,10 @@ normalize_kernel(const u32* big_list, const u32* big_cnt, const u64* chunk_piece
     const u32 k = big_list[x];
     const u64 o0 = chunk_piece_off[k], o1 = chunk_piece_off[k + 1];
     const u32 n = (u32)(o1 - o0);
-    if (n > NM_CAP) {
-      if (threadIdx.x == 0) atomicMax(too_big, n);
+    if (n > NM_CAP) {  // too large for shared memory: sorted and merged in place in global memory
+      const u32 m = sort_merge_global(o0, n, pm, pf, ps, pe, reinterpret_cast<u32*>(s));
+      if (threadIdx.x == 0) merged_cnt[k] = m;
+      __syncthreads();
       continue;
     }
     for (u32 i = threadIdx.x; i < n; i += NMB_THREADS) s[i] = make_uint4(pm[o0 + i], pf[o0 + i], ps[o0 + i], pe[o0 + i]);
@@ -2236,9 +2296,8 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   int fbits = 1, mbits = 1;
   while ((1ll << fbits) < (long long)ix->n_files + 1) ++fbits;
   while ((1ll << mbits) < w.max_mkey + 1) ++mbits;
-  static const bool no_pack = getenv("MX_NORM_NOPACK") != nullptr;
   // not for a file-sharded (hybrid) index: its file ids are checked nowhere here
-  const bool pack = !no_pack && w.max_mkey > 0 && fbits + mbits <= 31 && g->lcnt.p == nullptr;
+  const bool pack = w.max_mkey > 0 && fbits + mbits <= 31 && g->lcnt.p == nullptr;
   DevBuf<u64> pair_off;
   MX_CUDA_TRY(pair_off.alloc(n_pairs + 1, s));
   const unsigned pb = (unsigned)((n_pairs + 255) / 256);
@@ -2257,13 +2316,9 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
     MX_CUDA_TRY(llist.alloc(n_pairs, s));
     MX_CUDA_TRY(lcnt.alloc(1, s));
     MX_CUDA_TRY(cudaMemsetAsync(lcnt.p, 0, sizeof(u32), s));
-    static const u32 warp_min = getenv("MX_EMIT_WARP_MIN") ? (u32)atoi(getenv("MX_EMIT_WARP_MIN")) : 32u;
-    static const bool ew_direct = getenv("MX_EMIT_DIRECT") != nullptr;
-    if (ew_direct)
-      emit_write_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p, warp_min);
-    else
-      emit_write_staged_kernel<<<(unsigned)((n_pairs + EW_THREADS - 1) / EW_THREADS), EW_THREADS, 0, s>>>(
-          a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p, warp_min);
+    constexpr u32 warp_min = 32;  // pairs with more pieces are cut by a warp (emit_write_warp_kernel)
+    emit_write_staged_kernel<<<(unsigned)((n_pairs + EW_THREADS - 1) / EW_THREADS), EW_THREADS, 0, s>>>(
+        a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p, warp_min);
     mx_count_launch();
     const long long wgrid = std::min<long long>(((long long)n_pairs + 7) / 8, 148 * 16);
     emit_write_warp_kernel<<<(unsigned)wgrid, 256, 0, s>>>(a, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p);

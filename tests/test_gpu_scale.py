@@ -156,3 +156,20 @@ def test_empty_result_and_error_contract():
         ChunkGenerator(full, 1).generate(spec)
     with pytest.raises(MixtureError):
         ChunkGenerator(full, 1).generate_arbitrary(0)
+
+
+@pytest.mark.parametrize("chunk_size", [4096, 8192])
+def test_cfg1_iid_chunks_beyond_shared_memory_sort(oracle, chunk_size):
+    """iid cfg 1 with chunk_size >> 2,048: chunks of thousands of pieces
+    before merging take the in-place global-memory sort (normalize_kernel,
+    sort_merge_global); every chunk of the job equals the oracle's, in bulk
+    and through generate()."""
+    from paper_2502_19790_b200 import MixtureKey, MixtureSpec, synth
+
+    cc = synth.expand_numpy(synth.make_runs(1_000_000, 1000, synth.CFG1_PROPS, 1, seed=1))
+    gidx = _gpu_index(cc)
+    oidx = oracle.build_index(cc, [])
+    spec = MixtureSpec({MixtureKey.of({"language": "en"}): 0.5,
+                        MixtureKey.of({"language": ["de", "es", "fr"]}): 0.5}, chunk_size)
+    assert _chunks_equal(gidx, oidx, oracle, spec, bulk=True) > 1_000_000 // chunk_size // 2
+    assert _chunks_equal(gidx, oidx, oracle, spec, limit=20) == 20
