@@ -272,6 +272,34 @@ int mx_chunks_merge(int32_t world, int64_t n_chunks, int64_t cap, const int64_t*
                     uint32_t* out_mkey, uint32_t* out_file_index, uint32_t* out_start, uint32_t* out_end,
                     void* stream);
 
+/* ------------------------------------------------------------ registration
+ * Metadata registration from JSON-lines bytes in HBM [MetadataCatalog.
+ * register_dataset catalog.py:323-435, _parse_one_file catalog.py:246-262,
+ * iter_records formats.py:47-56, JsonFieldParser catalog.py:168-183,
+ * _normalize_values catalog.py:186-232]; SURVEY.md §8f-3.
+ *
+ * buf: device bytes, 16-byte aligned, n_bytes a multiple of 16, every file
+ * newline-terminated (padding after the last newline is not a line).
+ * Records = non-empty lines in order. Call once with rec_start == NULL to get
+ * n_records (and n_lines), then with device int64 outputs [n_records]: the
+ * record's byte range [start, end) and its global line index. */
+int mx_jsonl_records(const uint8_t* buf, int64_t n_bytes, int64_t* rec_start, int64_t* rec_end,
+                     int64_t* rec_line, int64_t capacity, int64_t* n_records, int64_t* n_lines, void* stream);
+/* Per record and requested top-level field (names: device bytes + offsets
+ * [n_fields+1], n_fields <= 32), device outputs [n_records][n_fields]:
+ * kind 0 missing / 1 value / 2 host / 3 present without a value (null, []);
+ * nelem = distinct elements of the normalised value; hash_a/hash_b = 128-bit
+ * hash of the normalised value (sorted distinct element hashes);
+ * value_start/value_len = byte span of a string value's content, or
+ * ~start / length of a list value. host[n_records] = 1: the record needs the
+ * host's json.loads + parser + normalisation (invalid JSON, escapes in a
+ * key or a requested value, numbers / booleans / nested values in a
+ * requested field, NaN / Infinity, BOM, NUL, > 8 list elements). */
+int mx_jsonl_extract(const uint8_t* buf, const int64_t* rec_start, const int64_t* rec_end, int64_t n_records,
+                     const uint8_t* field_names, const int64_t* field_offsets, int32_t n_fields, uint8_t* kind,
+                     uint8_t* nelem, uint64_t* hash_a, uint64_t* hash_b, int64_t* value_start, int32_t* value_len,
+                     uint8_t* host, void* stream);
+
 /* ------------------------------------------------------------------ stage 3
  * Per-domain loss reduction [per_domain_loss client.py:582-598]: device
  * f32 losses[n], int32 tags[n] in [0, n_domains) -> device f64 sums, int64

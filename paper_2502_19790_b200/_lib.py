@@ -165,6 +165,8 @@ _SIGS = {
     "mx_fit_power_law": (C.c_int, [i32, vp, vp, vp, vp, vp, vp]),
     "mx_ado_pi": (C.c_int, [i32, vp, vp, vp, dbl, dbl, dbl, vp, vp, vp, vp]),
     "mx_ado_credit": (C.c_int, [i32, dbl, vp, vp, vp]),
+    "mx_jsonl_records": (C.c_int, [vp, i64, vp, vp, vp, i64, P(i64), P(i64), vp]),
+    "mx_jsonl_extract": (C.c_int, [vp, vp, vp, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)
