@@ -630,6 +630,7 @@ def extra_measurements(args, rt, meta, spec, device) -> dict:
         "tuple_encode_ms": enc_ms,
         "note": "row-tuple dictionary encoding of the int32 columns on the device (mixed-radix tuple value + "
                 "unique), once per registered catalog; not part of a job"}
+    out["registration"]["jsonl"] = jsonl_registration(device)
     del dcat, cols
     torch.cuda.empty_cache()
     # ---- drop-in serving: per-chunk generate() + serialize() for the whole job
@@ -676,6 +677,62 @@ def extra_measurements(args, rt, meta, spec, device) -> dict:
                 "bit-exact vs the oracle in tests/test_gpu_parity_scale.py::test_cfg3_one_billion_samples_one_gpu"}
     del bcat, codes
     torch.cuda.empty_cache()
+    return out
+
+
+REG_SAMPLES, REG_FILES, REF_REG_FILES = 2_000_000, 200, 10
+
+
+def jsonl_registration(device) -> dict:
+    """cfg2-shaped metadata (2M records in 200 JSON-lines
+    files, 5 properties + id + text) registered by DeviceMetadataCatalog
+    (records, JSON validation and normalised values on the device, interning
+    into HBM code columns) vs the reference's MetadataCatalog.register_dataset
+    on a 10-file slice of the same files, host wall clock."""
+    import tempfile
+
+    import torch
+
+    from paper_2502_19790_b200 import synth
+    from paper_2502_19790_b200.register import DeviceMetadataCatalog
+
+    mp = _reference_pkg()
+    props = sorted(synth.CFG2_PROPS)
+    if mp is not None:
+        parser = mp.JsonFieldParser.for_properties(props)
+        schema = mp.PropertySchema([mp.PropertyDef(p) for p in props])
+    else:
+        from types import SimpleNamespace
+
+        parser = SimpleNamespace(fields=tuple((p, p) for p in props))
+        schema = SimpleNamespace(properties=tuple(SimpleNamespace(name=p, kind="string", nullable=True, multiple=False,
+                                                                  categories=None) for p in props),
+                                 names=lambda: list(props))
+    rt = synth.make_runs(REG_SAMPLES, REG_FILES, synth.CFG2_PROPS, CFG["run_mean"], seed=2)
+    with tempfile.TemporaryDirectory() as td:
+        paths = synth.write_jsonl_corpus(rt, td)
+        nbytes = sum(p.stat().st_size for p in paths)
+        DeviceMetadataCatalog(device).register_dataset("warm", paths, parser, schema)  # pinned staging, kernels
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev = DeviceMetadataCatalog(device)
+        dev.register_dataset("cfg2", paths, parser, schema)
+        torch.cuda.synchronize()
+        gpu_s = time.perf_counter() - t0
+        out = {"records": rt.n_samples, "files": len(paths), "bytes": nbytes, "seconds": gpu_s,
+               "records_per_s": rt.n_samples / gpu_s, "bytes_per_s": nbytes / gpu_s,
+               "breakdown_s": dict(dev.timings)}
+        if mp is not None:
+            sl = paths[:REF_REG_FILES]
+            n_ref = int(sum(rt.file_sizes[:REF_REG_FILES]))
+            t0 = time.perf_counter()
+            mp.MetadataCatalog().register_dataset("cfg2", sl, parser, schema)
+            ref_s = time.perf_counter() - t0
+            out["reference"] = {"records": n_ref, "seconds": ref_s, "records_per_s": n_ref / ref_s, "cores": 1,
+                                "sample": f"first {REF_REG_FILES} files of the same corpus, workers=1"}
+    out["note"] = ("device registration of JSON-lines metadata (csrc/register.cu + register.py), host wall clock "
+                   "incl. reading the files from the page cache, BLAKE2b content hashes, H2D, JSON validation, "
+                   "value extraction, interning and the HBM code columns")
     return out
 
 

@@ -172,3 +172,30 @@ def cfg5_mixture(keys, chunk_size: int = 1024):
     w = w[rng.permutation(len(keys))]
     w = w / w.sum()
     return MixtureSpec({k: float(x) for k, x in zip(keys, w)}, chunk_size)
+
+
+def write_jsonl_corpus(rt: RunTable, directory, text_len: int = 48) -> list:
+    """The run table as JSON-lines files (one per file of the table): every
+    record is {"id": i, <prop>: value, ..., "text": "..."} with the run's
+    property values, the registration input of SURVEY.md §8f-3 (the
+    reference's JsonFieldParser reads the property fields)."""
+    from pathlib import Path
+
+    directory = Path(directory)
+    directory.mkdir(parents=True, exist_ok=True)
+    props = sorted(rt.run_codes)
+    lens = rt.run_lengths()
+    ends = np.cumsum(rt.file_sizes)
+    filler = "x" * text_len
+    paths, buf, f = [], [], 0
+    for r in range(len(rt.run_starts)):
+        pre = "{" + ", ".join(f'"{p}": "{rt.vocab[p][rt.run_codes[p][r]]}"' for p in props) + ', "id": '
+        s = int(rt.run_starts[r])
+        for i in range(s, s + int(lens[r])):
+            buf.append(f'{pre}{i}, "text": "{filler}"}}')
+            if i + 1 == ends[f]:
+                path = directory / f"part{f:05d}.jsonl"
+                path.write_text("\n".join(buf) + "\n")
+                paths.append(path)
+                buf, f = [], f + 1
+    return paths
