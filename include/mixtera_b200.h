@@ -300,6 +300,32 @@ int mx_jsonl_extract(const uint8_t* buf, const int64_t* rec_start, const int64_t
                      uint8_t* nelem, uint64_t* hash_a, uint64_t* hash_b, int64_t* value_start, int32_t* value_len,
                      uint8_t* host, void* stream);
 
+/* ------------------------------------------------------------ client modes
+ * Tokenized processing mode [ChunkStreamer.tokenized client.py:451-506,
+ * tokenizers.py]; SURVEY.md §8f-4.
+ * mx_jsonl_tokenize: per record (spans from mx_jsonl_records) the tokens of
+ * the top-level string field `field`: tokenizer 0 = ByteTokenizer (UTF-8
+ * bytes of the decoded string), 1 = WhitespaceTokenizer (str.split() pieces,
+ * stable_hash("tok", piece) % vocab_size). tokens == NULL: counts[n_records]
+ * and host[n_records] (1 = the host tokenizer must handle the record: no
+ * string value, non-object record, escaped key, lone surrogate). Otherwise
+ * writes the device-path records' tokens at offsets[r] (device int64). */
+int mx_jsonl_tokenize(const uint8_t* buf, const int64_t* rec_start, const int64_t* rec_end, int64_t n_records,
+                      const uint8_t* field, int32_t field_len, int32_t tokenizer, uint32_t vocab_size,
+                      const int64_t* offsets, int64_t* counts, int32_t* tokens, uint8_t* host, void* stream);
+/* Packing of one chunk's key streams into n_windows windows of
+ * seqs_per_window sequences of sequence_length tokens (device arrays):
+ * window slot i holds key slot_key[i]'s sequences [slot_first[i],
+ * slot_first[i+1]) of the window; key m owns samples [key_off[m],
+ * key_off[m+1]) (global record ids, iterator order) with exclusive token
+ * prefix sample_prefix; outputs int32 [n_windows*seqs_per_window*L] tokens
+ * and tags (key_tag[m] per token). */
+int mx_pack_tokens(int64_t n_windows, int32_t sequence_length, int32_t n_slots, const int32_t* slot_key,
+                   const int32_t* slot_first, const int32_t* key_count, const int64_t* key_off,
+                   const int64_t* samples, const int64_t* sample_prefix, const int64_t* token_offsets,
+                   const int32_t* tokens, const int32_t* key_tag, int32_t seqs_per_window, int32_t* out_tokens,
+                   int32_t* out_tags, void* stream);
+
 /* ------------------------------------------------------------------ stage 3
  * Per-domain loss reduction [per_domain_loss client.py:582-598]: device
  * f32 losses[n], int32 tags[n] in [0, n_domains) -> device f64 sums, int64

@@ -167,6 +167,8 @@ _SIGS = {
     "mx_ado_credit": (C.c_int, [i32, dbl, vp, vp, vp]),
     "mx_jsonl_records": (C.c_int, [vp, i64, vp, vp, vp, i64, P(i64), P(i64), vp]),
     "mx_jsonl_extract": (C.c_int, [vp, vp, vp, i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "mx_jsonl_tokenize": (C.c_int, [vp, vp, vp, i64, vp, i32, i32, u32, vp, vp, vp, vp, vp]),
+    "mx_pack_tokens": (C.c_int, [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -16,7 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmxb200.so"
-SOURCES = ["capi.cu", "stage1.cu", "cursor.cu", "stage2.cu", "stage3.cu", "shard.cu", "serialize.cu", "register.cu"]
+SOURCES = ["capi.cu", "stage1.cu", "cursor.cu", "stage2.cu", "stage3.cu", "shard.cu", "serialize.cu", "register.cu", "tokenize.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -83,6 +83,62 @@ def normalize_values(prop, raw: object, where: str) -> tuple[str, ...]:
 _STAGE = None
 
 
+class LoadedJsonl:
+    """JSON-lines files resident in HBM with their record spans."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def load_jsonl(paths, device) -> LoadedJsonl:
+    """Every file into its own slot of one pinned buffer (+1 byte: a newline
+    where the file lacks a final one, else an empty line that iter_records
+    skips), read and BLAKE2b-hashed (_hash_file) by a thread pool, copied to
+    the device; the records (non-empty lines, iter_records order) found by
+    mx_jsonl_records."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
+    sizes = [os.stat(p).st_size for p in paths]
+    starts = np.zeros(len(paths) + 1, np.int64)
+    np.cumsum([n + 1 for n in sizes], out=starts[1:])
+    total = int(starts[-1])
+    padded = max(16, (total + 15) // 16 * 16)
+    host = _staging(padded)
+    hv = host.numpy()
+    hv[total:] = 0x20
+    mv = memoryview(hv)
+
+    def load(i):
+        s0, n = int(starts[i]), sizes[i]
+        with open(paths[i], "rb", buffering=0) as fh:
+            got = fh.readinto(mv[s0:s0 + n])
+        if got != n:
+            raise DataReadError(f"{paths[i]}: short read ({got} of {n} bytes)")
+        hv[s0 + n] = 0x0A
+        digest = hashlib.blake2b(mv[s0:s0 + n], digest_size=16).hexdigest()
+        return digest, int(np.count_nonzero(hv[s0:s0 + n + 1] == 0x0A))
+
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1, max(1, len(paths)))) as pool:
+        done = list(pool.map(load, range(len(paths))))
+    buf = host.to(device, non_blocking=True)
+    L = _lib.lib()
+    stream = C.c_void_p(_lib.stream_ptr())
+    n_rec, n_lines = C.c_int64(), C.c_int64()
+    _lib.check(L.mx_jsonl_records(buf.data_ptr(), padded, None, None, None, 0, C.byref(n_rec), C.byref(n_lines),
+                                  stream))
+    R = n_rec.value
+    rs = torch.empty(max(R, 1), dtype=torch.int64, device=device)
+    re = torch.empty_like(rs)
+    rl = torch.empty_like(rs)
+    _lib.check(L.mx_jsonl_records(buf.data_ptr(), padded, rs.data_ptr(), re.data_ptr(), rl.data_ptr(), R,
+                                  C.byref(n_rec), C.byref(n_lines), stream))
+    return LoadedJsonl(buf=buf, host=hv, starts=starts, digests=[d for d, _ in done],
+                       nl_counts=[c for _, c in done], n_records=R, rs=rs[:R], re=re[:R], rl=rl[:R], padded=padded)
+
+
 def _staging(n: int):
     """Grow-only pinned staging buffer shared by registrations (pinning a few
     hundred MB costs more than reading them from the page cache)."""
@@ -198,50 +254,13 @@ class DeviceMetadataCatalog:
         import torch
 
         t0 = time.perf_counter()
-        # every file into its own slot of one pinned buffer (+1 byte: a
-        # newline where the file lacks a final one, else an empty line that
-        # iter_records skips), read and BLAKE2b-hashed by a thread pool
-        import os
-        from concurrent.futures import ThreadPoolExecutor
-
-        sizes = [os.stat(p).st_size for p in paths]
-        starts = np.zeros(len(paths) + 1, np.int64)
-        np.cumsum([n + 1 for n in sizes], out=starts[1:])
-        total = int(starts[-1])
-        padded = max(16, (total + 15) // 16 * 16)
-        host = _staging(padded)
-        hv = host.numpy()
-        hv[total:] = 0x20
-        mv = memoryview(hv)
-
-        def load(i):
-            s0, n = int(starts[i]), sizes[i]
-            with open(paths[i], "rb", buffering=0) as fh:
-                got = fh.readinto(mv[s0:s0 + n])
-            if got != n:
-                raise DataReadError(f"{paths[i]}: short read ({got} of {n} bytes)")
-            hv[s0 + n] = 0x0A
-            digest = hashlib.blake2b(mv[s0:s0 + n], digest_size=16).hexdigest()
-            return digest, int(np.count_nonzero(hv[s0:s0 + n + 1] == 0x0A))
-
-        with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1, max(1, len(paths)))) as pool:
-            done = list(pool.map(load, range(len(paths))))
-        digests = [d for d, _ in done]
-        nl_counts = [c for _, c in done]
+        lf = load_jsonl(paths, self.device)
         t1 = time.perf_counter()
         dev = self.device
-        buf = host.to(dev, non_blocking=True)
         L = _lib.lib()
         stream = C.c_void_p(_lib.stream_ptr())
-        n_rec, n_lines = C.c_int64(), C.c_int64()
-        _lib.check(L.mx_jsonl_records(buf.data_ptr(), padded, None, None, None, 0, C.byref(n_rec), C.byref(n_lines),
-                                      stream))
-        R = n_rec.value
-        rs = torch.empty(max(R, 1), dtype=torch.int64, device=dev)
-        re = torch.empty_like(rs)
-        rl = torch.empty_like(rs)
-        _lib.check(L.mx_jsonl_records(buf.data_ptr(), padded, rs.data_ptr(), re.data_ptr(), rl.data_ptr(), R,
-                                      C.byref(n_rec), C.byref(n_lines), stream))
+        buf, starts, digests, nl_counts, hv = lf.buf, lf.starts, lf.digests, lf.nl_counts, lf.host
+        R, rs, re, rl = lf.n_records, lf.rs, lf.re, lf.rl
         # files of the records; each file's first global line index
         fstart = torch.from_numpy(starts[:-1]).to(dev)
         rec_file = torch.searchsorted(fstart, rs[:R], right=True) - 1
@@ -271,8 +290,8 @@ class DeviceMetadataCatalog:
                                       hb.data_ptr(), vs.data_ptr(), vl.data_ptr(), flag.data_ptr(), stream))
         self.timings["read_s"] = t1 - t0
         return dict(paths=paths, parser=parser, fields=fields, fpos=fpos, starts=starts, host=hv,
-                    digests=digests, n_records=R, per_file=per_file, first_line=first_line, rs=rs[:R], re=re[:R],
-                    rl=rl[:R], rec_file=rec_file, kind=kind[:R], nelem=nelem[:R], ha=ha[:R], hb=hb[:R],
+                    digests=digests, n_records=R, per_file=per_file, first_line=first_line, rs=rs, re=re,
+                    rl=rl, rec_file=rec_file, kind=kind[:R], nelem=nelem[:R], ha=ha[:R], hb=hb[:R],
                     vs=vs[:R], vl=vl[:R], flag=flag[:R], schema=schema)
 
     def _where(self, ps, r: int) -> tuple[str, int, int]:
