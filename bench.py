@@ -309,12 +309,26 @@ def reference_parallel(n_samples: int, workers: int, warmup: int, steps: int):
 
 
 def host_workers() -> int:
+    """Processes of the reference arm: 1 -- the reference's own path is one
+    GIL-bound process (build_index(rows, workers=1), server.py:115).
+    MX_REF_WORKERS=k runs k file-slice processes instead (a sharded upper
+    bound, labelled as such)."""
     try:
         n = len(os.sched_getaffinity(0))
     except AttributeError:
         n = os.cpu_count() or 1
-    cap = int(os.environ.get("MX_REF_WORKERS", "0") or 0)
-    return max(1, min(n, cap) if cap else min(n, 128))
+    cap = int(os.environ.get("MX_REF_WORKERS", "1") or 1)
+    return max(1, min(n, cap))
+
+
+def arm_config(world: int, layout: str) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    code_bytes, n_cols = (2, 1) if layout == "tuples" else (4, CFG["props"])
+    n = CFG["n_samples"] * world
+    return dict(CFG, parallelism=f"file-sharded x{world}" if world > 1 else "single GPU",
+                layout=LAYOUT_NOTE[layout],
+                l2=f"inputs ({n * code_bytes * n_cols / 1e9:.1f} GB of code columns) exceed the 126 MB L2; "
+                   "no flush needed")
 
 
 def reference_arm(args):
@@ -338,15 +352,19 @@ def reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": dict(CFG, workload=CFG["workload"] + f" (CPU slices: {workers} x {REF_SAMPLE:,} samples)"),
+        "config": arm_config(args.gpus, args.layout),
         "chunks_per_s": workers * chunks / t,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "reference" if real else "port",
-                         "sample": (f"{workers} host processes at once, each running the job on its own "
-                                    f"{REF_SAMPLE:,}-sample slice of the cfg2 layout per step, through "
+                         "sample": ((f"the job on the first {REF_SAMPLE:,} samples (200 files) of the cfg2 "
+                                     "layout per step, one process (the reference's own path is single-core: "
+                                     "GIL-bound, build_index workers=1 at server.py:115), through "
+                                     if workers == 1 else
+                                     f"SHARDED UPPER BOUND: {workers} host processes at once, each running the job "
+                                     f"on its own {REF_SAMPLE:,}-sample slice of the cfg2 layout per step, through ")
                                     if real else f"{REF_SAMPLE:,} samples of the cfg2 layout per step through ")
                                    + ("the unmodified reference (baseline/_ref mixplane: filter_intervals, "
-                                      "build_index, ChunkGenerator.generate to exhaustion); step time = the "
-                                      "slowest process"
+                                      "build_index, ChunkGenerator.generate to exhaustion)"
+                                      + ("; step time = the slowest process" if workers > 1 else "")
                                       if real else "oracle/oracle.py (numpy + CPython stdlib), single thread")},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -513,10 +531,7 @@ def our_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u16" if code_bytes == 2 else "int32",
         "data": "synthetic",
-        "config": dict(CFG, parallelism=f"file-sharded x{world}" if world > 1 else "single GPU",
-                       layout=LAYOUT_NOTE[args.layout],
-                       l2=f"inputs ({n * code_bytes * n_cols / 1e9:.1f} GB of code columns) exceed the 126 MB L2; "
-                          "no flush needed"),
+        "config": arm_config(world, args.layout),
         "chunks_per_s": n_chunks / (ms_max * 1e-3),
         "job": {"samples": n, "intervals": n_iv, "keys": n_keys, "blocks": n_blocks, "chunks": n_chunks,
                 "ranges": n_ranges},
@@ -548,8 +563,8 @@ def our_arm(args):
     if not args.no_cpu_baseline and world == 1:
         real = _reference_pkg() is not None
         if real:
-            # the reference arm itself, one step on every host core, in a fresh
-            # process (no fork of this CUDA-initialised one)
+            # the reference arm itself (one step), in a fresh process (no fork
+            # of this CUDA-initialised one)
             out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
                                   "--warmup", "0"], capture_output=True, text=True, timeout=600)
             ref = json.loads(out.stdout.strip().splitlines()[-1])
