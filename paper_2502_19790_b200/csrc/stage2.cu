@@ -1505,9 +1505,16 @@ __global__ void emit_count_kernel(EmitArgs a, u64 n_pairs, u64* pair_cnt) {
 // EW_CAP store directly.
 constexpr int EW_THREADS = 128;
 constexpr int EW_CAP = 640;
+// sort_terms (mode-0 plans: one term per mixture key and chunk, terms in key
+// order): each thread also sorts its pair's pieces by (file, start) in the
+// stage, so every chunk comes out in the reference's (mixture key, file,
+// start) order without the per-chunk normalisation; flags |= 1 when a piece
+// bypassed the sort (long pair, unstaged warp), |= 2 when two sorted pieces
+// are contiguous (a merge the per-chunk pass must do).
 __global__ void __launch_bounds__(EW_THREADS) emit_write_staged_kernel(EmitArgs a, u64 n_pairs, const u64* pair_off,
                                                                        u32* pm, u32* pf, u32* ps, u32* pe,
-                                                                       u32* long_list, u32* long_cnt, u32 warp_min) {
+                                                                       u32* long_list, u32* long_cnt, u32 warp_min,
+                                                                       int sort_terms, u32* flags) {
   __shared__ uint4 s_rec[EW_THREADS / 32][EW_CAP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const u64 pr = blockIdx.x * (u64)EW_THREADS + threadIdx.x;
@@ -1521,7 +1528,10 @@ __global__ void __launch_bounds__(EW_THREADS) emit_write_staged_kernel(EmitArgs 
   const u64 w_lo = pair_off[first], w_hi = pair_off[last + 1];
   const bool staged = !__any_sync(MX_FULL, is_long) && w_hi - w_lo <= (u64)EW_CAP;
   if (!staged) {
-    if (valid && !is_long) walk_pair<true>(a, pr, nullptr, pm, pf, ps, pe, lo_i);
+    if (valid && !is_long) {
+      walk_pair<true>(a, pr, nullptr, pm, pf, ps, pe, lo_i);
+      if (sort_terms && hi_i - lo_i > 1) long_list[atomicAdd(long_cnt + 1, 1u) + n_pairs] = (u32)pr;  // sort later
+    }
     return;
   }
   uint4* rec = s_rec[warp];
@@ -1534,6 +1544,49 @@ __global__ void __launch_bounds__(EW_THREADS) emit_write_staged_kernel(EmitArgs 
     const Term tm = a.terms[php.term_begin + (long long)(local % (u64)php.n_terms)];
     walk_term<true>(a, tm, kr, [&](u64 i, u32 m, u32 f, u32 s0, u32 e0) { rec[base + i] = make_uint4(m, f, s0, e0); },
                     0, 1);
+    if (sort_terms) {  // this pair's pieces by (file, start): <= 8 in registers, more by sort_pairs_kernel
+      const int n = (int)(hi_i - lo_i);
+      if (n > 8) {
+        long_list[atomicAdd(long_cnt + 1, 1u) + n_pairs] = (u32)pr;
+      } else if (n > 1) {
+        uint4* r = rec + base;
+        unsigned long long k[8];
+        u32 e[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 v = i < n ? r[i] : make_uint4(0u, ~0u, ~0u, 0u);
+          k[i] = ((unsigned long long)v.y << 32) | v.z;
+          e[i] = v.w;
+        }
+        // Batcher odd-even merge sort network for 8 keys (19 comparators)
+        auto cx = [&](int a, int b) {
+          const bool sw = k[b] < k[a];
+          const unsigned long long ka = k[a], kb = k[b];
+          const u32 ea = e[a], eb = e[b];
+          k[a] = sw ? kb : ka;
+          k[b] = sw ? ka : kb;
+          e[a] = sw ? eb : ea;
+          e[b] = sw ? ea : eb;
+        };
+        cx(0, 1); cx(2, 3); cx(4, 5); cx(6, 7);
+        cx(0, 2); cx(1, 3); cx(4, 6); cx(5, 7);
+        cx(1, 2); cx(5, 6); cx(0, 4); cx(3, 7);
+        cx(1, 5); cx(2, 6);
+        cx(1, 4); cx(3, 6);
+        cx(2, 4); cx(3, 5);
+        cx(3, 4);
+        const u32 m = r[0].x;
+        bool merge = false;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < n) {
+            r[i] = make_uint4(m, (u32)(k[i] >> 32), (u32)k[i], e[i]);
+            if (i > 0) merge |= (k[i] >> 32) == (k[i - 1] >> 32) && (u32)k[i] == e[i - 1];
+          }
+        }
+        if (merge) atomicOr(flags, 2u);
+      }
+    }
   }
   __syncwarp();
   const int cnt = (int)(w_hi - w_lo);
@@ -1560,6 +1613,97 @@ __global__ void __launch_bounds__(256) emit_write_warp_kernel(EmitArgs a, const 
 }
 
 // first pair of every chunk (+ sentinel) -> piece range per chunk
+// mode-0 sorted emission: long pairs (> 32 pieces, cut by a warp) -- one CTA
+// each sorts its pieces by (file, start) in shared memory (<= SP_CAP) and
+// flags merges; larger ones flag the per-chunk path
+constexpr int SP_CAP = 2048;
+__global__ void __launch_bounds__(256) sort_pairs_kernel(const u32* lists, const u32* cnts, u64 n_pairs,
+                                                         const u64* pair_off, u32* pm, u32* pf, u32* ps, u32* pe,
+                                                         u32* flags) {
+  __shared__ uint4 sh[SP_CAP];
+  const u32 n_long = cnts[0];
+  for (u32 x = blockIdx.x; x < n_long; x += gridDim.x) {
+    const u32 pr = lists[x];
+    const u64 o0 = pair_off[pr];
+    const u32 n = (u32)(pair_off[pr + 1] - o0);
+    if (n > SP_CAP) {
+      if (threadIdx.x == 0) atomicOr(flags, 1u);
+      continue;
+    }
+    u32 np = 1;
+    while (np < n) np <<= 1;
+    for (u32 i = threadIdx.x; i < np; i += blockDim.x)
+      sh[i] = i < n ? make_uint4(pm[o0 + i], pf[o0 + i], ps[o0 + i], pe[o0 + i]) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    __syncthreads();
+    for (u32 kk = 2; kk <= np; kk <<= 1)
+      for (u32 j = kk >> 1; j > 0; j >>= 1) {
+        for (u32 i = threadIdx.x; i < np; i += blockDim.x) {
+          const u32 l = i ^ j;
+          if (l > i) {
+            const uint4 p = sh[i], q = sh[l];
+            const bool gt = p.y != q.y ? p.y > q.y : p.z > q.z;
+            if (gt == ((i & kk) == 0)) {
+              sh[i] = q;
+              sh[l] = p;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    bool merge = false;
+    for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint4 r = sh[i];
+      if (i > 0) merge |= sh[i - 1].y == r.y && sh[i - 1].w == r.z;
+      pm[o0 + i] = r.x;
+      pf[o0 + i] = r.y;
+      ps[o0 + i] = r.z;
+      pe[o0 + i] = r.w;
+    }
+    if (__syncthreads_or(merge) && threadIdx.x == 0) atomicOr(flags, 2u);
+  }
+}
+
+// pairs of 9..32 pieces (and unstaged warps' pairs): one warp each, register
+// bitonic sort of (file, start) across the lanes
+__global__ void __launch_bounds__(256) sort_pairs_warp_kernel(const u32* lists, const u32* cnts, u64 n_pairs,
+                                                              const u64* pair_off, u32* pm, u32* pf, u32* ps,
+                                                              u32* pe, u32* flags) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long n_uns = cnts[1];
+  for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < n_uns; w += warps) {
+    const u32 pr = lists[n_pairs + w];
+    const u64 o0 = pair_off[pr];
+    const u32 n = (u32)(pair_off[pr + 1] - o0);  // <= 32 (longer pairs are on the long list)
+    const bool ok = (u32)lane < n;
+    unsigned long long key = ok ? ((unsigned long long)pf[o0 + lane] << 32) | ps[o0 + lane] : ~0ull;
+    u32 en = ok ? pe[o0 + lane] : 0u;
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const unsigned long long ok2 = __shfl_xor_sync(MX_FULL, key, j);
+        const u32 oe = __shfl_xor_sync(MX_FULL, en, j);
+        const bool lower = (lane & j) == 0, up = (lane & kk) == 0;
+        const bool take = (lower == up) ? ok2 < key : ok2 > key;
+        if (take) {
+          key = ok2;
+          en = oe;
+        }
+      }
+    }
+    const unsigned long long pk = __shfl_up_sync(MX_FULL, key, 1);
+    const u32 pen = __shfl_up_sync(MX_FULL, en, 1);
+    const bool merge = ok && lane > 0 && (pk >> 32) == (key >> 32) && pen == (u32)key;
+    if (ok) {
+      pf[o0 + lane] = (u32)(key >> 32);
+      ps[o0 + lane] = (u32)key;
+      pe[o0 + lane] = en;
+    }
+    if (__any_sync(MX_FULL, merge) && lane == 0) atomicOr(flags, 2u);
+  }
+}
+
 __global__ void chunk_pieces_kernel(EmitArgs a, long long n_chunks, const u64* pair_off, u64 n_pairs,
                                     u64* chunk_piece_off) {
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -2306,6 +2450,12 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   // exclusive scan of counts in place (each element is read and written by
   // the same thread; the total lands in [n_pairs])
   if (int rc = excl_scan<u64>(pair_off.p, (long long)n_pairs, pair_off.p, s)) return rc;
+  // mode-0 plans on a single-GPU index: chunks come out of the cut already in
+  // (mixture key, file, start) order unless a pair was long / a merge exists
+  const bool sort_terms = w.mode == 0 && g->lcnt.p == nullptr;
+  DevBuf<u32> eflags;
+  MX_CUDA_TRY(eflags.alloc(1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(eflags.p, 0, sizeof(u32), s));
   DevBuf<u32> pm, pf, ps, pe;
   MX_CUDA_TRY(pm.alloc(cap, s));
   MX_CUDA_TRY(pf.alloc(cap, s));
@@ -2313,16 +2463,25 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(pe.alloc(cap, s));
   {
     DevBuf<u32> llist, lcnt;
-    MX_CUDA_TRY(llist.alloc(n_pairs, s));
-    MX_CUDA_TRY(lcnt.alloc(1, s));
-    MX_CUDA_TRY(cudaMemsetAsync(lcnt.p, 0, sizeof(u32), s));
+    MX_CUDA_TRY(llist.alloc(2 * n_pairs, s));  // [long pairs | unstaged pairs to sort]
+    MX_CUDA_TRY(lcnt.alloc(2, s));
+    MX_CUDA_TRY(cudaMemsetAsync(lcnt.p, 0, 2 * sizeof(u32), s));
     constexpr u32 warp_min = 32;  // pairs with more pieces are cut by a warp (emit_write_warp_kernel)
     emit_write_staged_kernel<<<(unsigned)((n_pairs + EW_THREADS - 1) / EW_THREADS), EW_THREADS, 0, s>>>(
-        a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p, warp_min);
+        a, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p, warp_min, sort_terms ? 1 : 0,
+        eflags.p);
     mx_count_launch();
     const long long wgrid = std::min<long long>(((long long)n_pairs + 7) / 8, 148 * 16);
     emit_write_warp_kernel<<<(unsigned)wgrid, 256, 0, s>>>(a, pair_off.p, pm.p, pf.p, ps.p, pe.p, llist.p, lcnt.p);
     mx_count_launch();
+    if (sort_terms) {
+      sort_pairs_warp_kernel<<<148 * 8, 256, 0, s>>>(llist.p, lcnt.p, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p,
+                                                     eflags.p);
+      mx_count_launch();
+      sort_pairs_kernel<<<148 * 2, 256, 0, s>>>(llist.p, lcnt.p, n_pairs, pair_off.p, pm.p, pf.p, ps.p, pe.p,
+                                                eflags.p);
+      mx_count_launch();
+    }
   }
   DevBuf<u64> cpo, mcnt;
   DevBuf<u32> big;
@@ -2332,6 +2491,28 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(cudaMemsetAsync(big.p, 0, sizeof(u32), s));
   chunk_pieces_kernel<<<(unsigned)((n_chunks + 256) / 256), 256, 0, s>>>(a, n_chunks, pair_off.p, n_pairs, cpo.p);
   mx_count_launch();
+  if (sort_terms) {
+    u32 h_flags = 1;
+    long long total = 0;
+    MX_CUDA_TRY(cudaStreamWaitEvent(s, seed_join, 0));  // chunk seeds (side stream) done
+    {
+      D2HBatch rb(s);
+      MX_CUDA_TRY(rb.add(&h_flags, eflags.p, sizeof(u32)));
+      MX_CUDA_TRY(rb.add(&total, cpo.p + n_chunks, sizeof(long long)));
+      MX_CUDA_TRY(rb.sync());
+    }
+    if (h_flags == 0) {  // already normalised: the cut pieces are the result
+      g->res_mkey.take(pm);
+      g->res_file.take(pf);
+      g->res_start.take(ps);
+      g->res_end.take(pe);
+      MX_CUDA_TRY(cudaMemcpyAsync(g->res_off.p, cpo.p, sizeof(long long) * (n_chunks + 1), cudaMemcpyDeviceToDevice,
+                                  s));
+      g->res_ranges = total;
+      g->next_chunk_id += n_chunks;
+      return MX_OK;
+    }
+  }
   {
     DevBuf<u32> blist, bcnt;
     MX_CUDA_TRY(blist.alloc(n_chunks, s));
