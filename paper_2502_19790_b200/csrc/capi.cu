@@ -42,6 +42,21 @@ static std::vector<PendingPhase> g_pending;
 
 void mx_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+#include <chrono>
+void mx_host_mark(const char* label) {
+  static const bool on = getenv("MX_HOST_TIMING") != nullptr;
+  if (!on) return;
+  static thread_local std::vector<std::pair<const char*, double>> marks;
+  const double t = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  if (label) {
+    marks.emplace_back(label, t);
+    return;
+  }
+  for (size_t i = 1; i < marks.size(); ++i) fprintf(stderr, "  %-28s %8.1f us\n", marks[i].first, marks[i].second - marks[i - 1].second);
+  if (!marks.empty()) fprintf(stderr, "  total %8.1f us\n", marks.back().second - marks.front().second);
+  marks.clear();
+}
+
 // Host->device copies of small host arrays (LUTs, mixture tables, sentinels)
 // go through a per-thread pinned staging ring: a cudaMemcpyAsync from
 // PAGEABLE memory synchronises the stream before it starts, which would
@@ -212,6 +227,30 @@ mx::IndexData::~IndexData() {
     pend_slot_give(pend);
     aux_event_give(pend_dev, pend_ev);
   }
+}
+
+namespace {
+struct Workspace {
+  void* p[mx::WS_N] = {};
+  size_t n[mx::WS_N] = {};
+};
+thread_local std::map<cudaStream_t, Workspace> g_ws;
+}  // namespace
+
+cudaError_t mx::ws_get(cudaStream_t s, int slot, size_t bytes, void** out, cudaStream_t alloc, bool alloc_set) {
+  Workspace& w = g_ws[s];
+  const cudaStream_t as = alloc_set ? alloc : s;
+  if (w.n[slot] < bytes) {
+    if (w.p[slot]) cudaFreeAsync(w.p[slot], as);
+    w.p[slot] = nullptr;
+    w.n[slot] = 0;
+    const size_t want = bytes + bytes / 4;
+    cudaError_t e = cudaMallocAsync(&w.p[slot], want, as);
+    if (e != cudaSuccess) return e;
+    w.n[slot] = want;
+  }
+  *out = w.p[slot];
+  return cudaSuccess;
 }
 
 cudaError_t D2HBatch::sync_event(cudaEvent_t e) {
@@ -435,7 +474,9 @@ int mx_index_build(const mx_catalog_desc* desc, void* stream, mx_index** out) {
   }
   int rc = MX_OK;
   // key strings, LUTs and file tables are uploaded by stage1_build in one copy
+  mx_host_mark("build enter");
   if (rc == MX_OK) rc = stage1_build(desc, s, &d);
+  mx_host_mark("build done");
   if (rc < 0) {
     delete ix;
     return rc;
@@ -607,7 +648,9 @@ int mx_gen_create(mx_index* index, const uint8_t* cursor_prefix, int32_t cursor_
   MX_CHECK_ARG(index && out, "null argument");
   g_err.clear();
   keep_pool_warm();
+  mx_host_mark("gen enter");
   if (int rc = ix_resolve(&index->d)) return rc;
+  mx_host_mark("gen index resolved");
   cudaStream_t s = (cudaStream_t)stream;
   mx_gen* g = new mx_gen();
   int rc = MX_OK;
@@ -617,6 +660,7 @@ int mx_gen_create(mx_index* index, const uint8_t* cursor_prefix, int32_t cursor_
   if (e != cudaSuccess) rc = mx_fail_cuda(e, "chunk prefix", __FILE__, __LINE__);
   g->d.chunk_prefix_len = chunk_prefix_len;
   if (rc == MX_OK) rc = cursor_build(&index->d, cursor_prefix, cursor_prefix_len, order_seed, s, &g->d);
+  mx_host_mark("gen cursor launched");
   if (rc < 0) {
     delete g;
     return rc;
@@ -638,7 +682,10 @@ int mx_gen_plan(mx_gen* gen, const mx_mixture_desc* mix, int64_t max_chunks, int
   MX_CHECK_ARG(max_chunks >= 1, "max_chunks must be >= 1");
   g_err.clear();
   long long n = 0;
+  mx_host_mark("plan enter");
   int rc = plan_mixture(&gen->d, mix, max_chunks, &n);
+  mx_host_mark("plan done");
+  mx_host_mark(nullptr);
   *n_out = n;
   return rc;
 }

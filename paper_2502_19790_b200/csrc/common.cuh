@@ -167,6 +167,10 @@ struct D2HBatch {
   cudaError_t sync_event(cudaEvent_t e);
 };
 
+// Host-side checkpoints (MX_HOST_TIMING=1): wall-clock microseconds between
+// labelled points of a C-ABI call, printed to stderr by mx_host_mark(nullptr).
+void mx_host_mark(const char* label);
+
 // Launch accounting and per-phase CUDA-event timing (capi.cu). A phase timer
 // records events on the launching stream when profiling is enabled
 // (mx_profile_enable); totals are read back with mx_profile_read.

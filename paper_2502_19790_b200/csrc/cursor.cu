@@ -14,6 +14,7 @@
 // interval ids, one reduce-then-scan over all keys),
 // cum_len_kernel (u64 look-back scan of lengths in cursor order),
 // component_order_kernel (one shuffle of K ranks).
+#include <map>
 #include "blake2b.cuh"
 #include "common.cuh"
 #include "mixtera_internal.cuh"
@@ -231,21 +232,28 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   // runs on a side stream, overlapped with the per-key cursor shuffles
   static thread_local uint32_t h_base[MT_N];
   if (h_base[0] != 19650218u) mt_base_table(h_base);
-  DevBuf<u32> mt_base;
-  MX_CUDA_TRY(mt_base.alloc(MT_N, s));
-  MX_CUDA_TRY(mx_h2d(mt_base.p, h_base, sizeof(h_base), s));
+  DevBuf<u32> mt_base;  // constant table: uploaded into the stream's workspace once
+  {
+    static thread_local std::map<cudaStream_t, u32*> uploaded;
+    MX_CUDA_TRY(ws_borrow(mt_base, s, WS_MTBASE, MT_N));
+    if (uploaded[s] != mt_base.p) {
+      MX_CUDA_TRY(mx_h2d(mt_base.p, h_base, sizeof(h_base), s));
+      uploaded[s] = mt_base.p;
+    }
+  }
   MX_CUDA_TRY(g->comp_order.alloc(K, s));
   MX_CUDA_TRY(cudaEventRecord(g->ev_tot, s));
   MX_CUDA_TRY(cudaStreamWaitEvent(g->ostream, g->ev_tot, 0));
+  mx_host_mark("cursor prologue");
   component_order_kernel<<<1, 32, 0, g->ostream>>>(K, order_seed, mt_base.p, g->comp_order.p);
   mx_count_launch();
   MX_CUDA_TRY(cudaEventRecord(g->ev_order, g->ostream));
   DevBuf<uint8_t> pre;
   DevBuf<u64> seeds;
-  MX_CUDA_TRY(pre.alloc(prefix_len > 0 ? prefix_len : 1, s));
+  MX_CUDA_TRY(ws_borrow(pre, s, WS_CPRE, prefix_len > 0 ? prefix_len : 1));
   if (prefix_len > 0)
     MX_CUDA_TRY(mx_h2d(pre.p, cursor_prefix, prefix_len, s));
-  MX_CUDA_TRY(seeds.alloc(K, s));
+  MX_CUDA_TRY(ws_borrow(seeds, s, WS_CSEED, K));
   KeyStrView v{};
   v.key_packed = ix->key_packed.p;
   v.n_props = ix->n_props;
@@ -259,8 +267,8 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   key_seed_kernel<<<(unsigned)((K + 127) / 128), 128, 0, s>>>(v, K, pre.p, prefix_len, seeds.p);
   mx_count_launch();
   DevBuf<u32> grp, gid;
-  MX_CUDA_TRY(grp.alloc(B, s));
-  MX_CUDA_TRY(gid.alloc(B, s));
+  MX_CUDA_TRY(ws_borrow(grp, s, WS_CGRP, B));
+  MX_CUDA_TRY(ws_borrow(gid, s, WS_CGID, B));
   MX_CUDA_TRY(g->cur_blk.alloc(B, s));
   {
     MxPhase ph2("cursor_shuffle", s);

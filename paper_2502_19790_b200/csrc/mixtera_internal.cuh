@@ -71,6 +71,27 @@ struct DevBuf {
   }
 };
 
+// Grow-only device workspace per (host thread, stream) for the temporaries
+// of a call (capi.cu): the stage-1 slot arrays are sized by the catalog
+// (16 B per sample), and re-allocating them per job costs host time on the
+// critical path before the first kernel. Buffers are reused in stream order;
+// a view must never outlive the call that borrowed it.
+enum WsSlot { WS_TCNT, WS_TOPEN, WS_THEAD, WS_DEFER, WS_RK, WS_RF, WS_RS, WS_RE, WS_SEGFA, WS_SCR64, WS_ERR,
+              WS_HIST, WS_DTOT, WS_TOFF, WS_GSAGG, WS_CPRE, WS_CSEED, WS_CGRP, WS_CGID, WS_MTBASE,
+              WS_GEN,            // + GenData scratch slot (24 of them)
+              WS_N = WS_GEN + 24 };
+// `s` keys the workspace (a call's stream: work on it is ordered); growth
+// frees / allocates in order on `alloc` (default: s)
+cudaError_t ws_get(cudaStream_t s, int slot, size_t bytes, void** out, cudaStream_t alloc = nullptr,
+                   bool alloc_set = false);
+template <typename T>
+cudaError_t ws_borrow(DevBuf<T>& b, cudaStream_t s, int slot, long long n) {
+  void* p = nullptr;
+  cudaError_t e = ws_get(s, slot, sizeof(T) * (size_t)(n > 0 ? n : 1), &p);
+  if (e == cudaSuccess) b.borrow(p, n);
+  return e;
+}
+
 struct IndexData {
   cudaStream_t stream = 0;
   long long n_samples_total = 0;
@@ -175,19 +196,14 @@ struct GenData {
   DevBuf<u32> match_L_off, match_L;
   // grow-only scratch for per-call planning (small plans allocate nothing);
   // allocated in stream order on the stream that first writes it (`st`)
-  DevBuf<unsigned char> ws[24];
   template <typename T>
   cudaError_t scratch(int slot, long long n, T** out, cudaStream_t st) {
-    const long long bytes = (long long)sizeof(T) * (n > 0 ? n : 1);
-    if (ws[slot].n < bytes) {
-      // the old buffer is freed in order on the requesting stream: every
-      // earlier user (plan stream or generator stream) is ordered before it
-      ws[slot].s = st;
-      cudaError_t e = ws[slot].alloc(bytes + bytes / 2, st);
-      if (e != cudaSuccess) return e;
-    }
-    *out = reinterpret_cast<T*>(ws[slot].p);
-    return cudaSuccess;
+    // per-call temporaries: the requesting stream's workspace (ws_get), so a
+    // new generator per job allocates nothing once the sizes are reached
+    void* p = nullptr;  // keyed by the generator's stream: plans of generators sharing it are ordered
+    cudaError_t e = ws_get(stream, WS_GEN + slot, sizeof(T) * (size_t)(n > 0 ? n : 1), &p, st, true);
+    *out = reinterpret_cast<T*>(p);
+    return e;
   }
   template <typename T>
   cudaError_t scratch(int slot, long long n, T** out) { return scratch(slot, n, out, stream); }

@@ -123,8 +123,8 @@ template <class F>
 int gs_run(long long n, const F& f, cudaStream_t s) {
   if (n <= 0) return MX_OK;
   const long long T = (n + GS_TILE - 1) / GS_TILE;
-  DevBuf<u64> agg;
-  MX_CUDA_TRY(agg.alloc(T + 1, s));
+  DevBuf<u64> agg;  // tile sums: a workspace view (gs_run calls on a stream run in order)
+  MX_CUDA_TRY(ws_borrow(agg, s, WS_GSAGG, T + 1));
   gs_reduce<F><<<(unsigned)T, GS_THREADS, 0, s>>>(n, f, agg.p);
   mx_count_launch();
   gs_scan<<<1, 1024, 0, s>>>(T, agg.p);

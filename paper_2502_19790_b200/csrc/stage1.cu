@@ -346,6 +346,7 @@ struct TileOffF {
 };
 
 int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
+  mx_host_mark("s1 enter");
   if (d->n_props < 1 || d->n_props > MX_MAX_PROPS)
     return mx_fail(MX_ERR_UNSUPPORTED, "n_props=%d outside [1, %d]", d->n_props, MX_MAX_PROPS);
   // scanned columns: one per property, or the row-tuple code column(s)
@@ -393,8 +394,10 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   const size_t o_lsum = up.add(ls.data(), sizeof(u32) * ls.size());
   const size_t o_fds = up.add(d->file_ds, sizeof(int32_t) * d->n_files);
   const size_t o_fid = up.add(d->file_ids, sizeof(long long) * d->n_files);
+  mx_host_mark("s1 host tables");
   MX_CUDA_TRY(ix.consts.alloc((long long)up.total + 16, s));
   MX_CUDA_TRY(up.run(ix.consts.p, s));
+  mx_host_mark("s1 upload");
   ix.str_off.borrow(ix.consts.p + o_soff, n_pieces + 1);
   ix.str_bytes.borrow(ix.consts.p + o_sbytes, str_nbytes > 0 ? str_nbytes : 1);
   a.lut = reinterpret_cast<const u32*>(ix.consts.p + o_lut);
@@ -417,9 +420,14 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   //  pipe:   persistent CTAs + TMA ring, slot output (scan_pipe_kernel)
   //  v1:     one CTA per tile, decoupled look-back output (scan_runs_kernel)
   const bool smem_lut = lut_total <= MX_SMEM_LUT_MAX;
-  int dev = 0, n_sm = 148;
+  int dev = 0;
   MX_CUDA_TRY(cudaGetDevice(&dev));
-  MX_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  static thread_local int sm_dev = -1, sm_count = 148;
+  if (sm_dev != dev) {
+    MX_CUDA_TRY(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
+    sm_dev = dev;
+  }
+  const int n_sm = sm_count;
   // Two stage-1 passes, both writing per-tile slot regions (tile-local
   // compaction, no inter-tile dependency) fixed up by slot_fixup_kernel:
   //  * one u16 row-tuple column, 16-byte aligned: scan_u16_kernel
@@ -445,10 +453,10 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   DevBuf<u32> t_cnt, t_open, defer;
   DevBuf<long long> t_head;
   if (ntiles > 0) {
-    MX_CUDA_TRY(t_cnt.alloc(ntiles, s));
-    MX_CUDA_TRY(t_open.alloc(ntiles, s));
-    MX_CUDA_TRY(t_head.alloc(ntiles, s));
-    MX_CUDA_TRY(defer.alloc(ntiles + 1, s));
+    MX_CUDA_TRY(ws_borrow(t_cnt, s, WS_TCNT, ntiles));
+    MX_CUDA_TRY(ws_borrow(t_open, s, WS_TOPEN, ntiles));
+    MX_CUDA_TRY(ws_borrow(t_head, s, WS_THEAD, ntiles));
+    MX_CUDA_TRY(ws_borrow(defer, s, WS_DEFER, ntiles + 1));
     MX_CUDA_TRY(cudaMemsetAsync(defer.p + ntiles, 0, sizeof(u32), s));
     a.tile_cnt = t_cnt.p;
     a.tile_open = t_open.p;
@@ -456,19 +464,21 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     a.defer_list = defer.p;
     a.defer_cnt = defer.p + ntiles;
   }
-  MX_CUDA_TRY(rk.alloc(cap, s));
-  MX_CUDA_TRY(rf.alloc(cap, s));
-  MX_CUDA_TRY(rs.alloc(cap, s));
-  MX_CUDA_TRY(re.alloc(cap, s));
-  MX_CUDA_TRY(scratch64.alloc(4, s));
-  MX_CUDA_TRY(err.alloc(1, s));
+  mx_host_mark("s1 tile allocs");
+  MX_CUDA_TRY(ws_borrow(rk, s, WS_RK, cap));
+  MX_CUDA_TRY(ws_borrow(rf, s, WS_RF, cap));
+  MX_CUDA_TRY(ws_borrow(rs, s, WS_RS, cap));
+  MX_CUDA_TRY(ws_borrow(re, s, WS_RE, cap));
+  MX_CUDA_TRY(ws_borrow(scratch64, s, WS_SCR64, 4));
+  MX_CUDA_TRY(ws_borrow(err, s, WS_ERR, 1));
   MX_CUDA_TRY(cudaMemsetAsync(scratch64.p, 0, sizeof(u64) * 4, s));
   MX_CUDA_TRY(cudaMemsetAsync(err.p, 0xff, sizeof(u64), s));
   MX_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(err.p) + 8, 0, 8, s));
   a.rec_key = rk.p; a.rec_file = rf.p; a.rec_start = rs.p; a.rec_end = re.p;
   a.n_runs = scratch64.p; a.err = err.p;
+  mx_host_mark("s1 slot allocs");
   if (ntiles > 0 && u16_path) {
-    MX_CUDA_TRY(seg_fa.alloc(ntiles + 1, s));
+    MX_CUDA_TRY(ws_borrow(seg_fa, s, WS_SEGFA, ntiles + 1));
     seg_file_kernel<<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, s>>>(a.file_off, a.n_files, n, ntiles, seg_fa.p);
     mx_count_launch();
     {
@@ -476,13 +486,19 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
       const int entries = lut_total - 1;
       const bool slut = entries <= U16_SMEM_LUT_MAX;
       const size_t dyn = sizeof(U16Warp) * U16_WARPS + (slut ? sizeof(u32) * (size_t)entries : 0);
-      int per_sm = 1;
-      if (slut) {
-        MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-        MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<true>, U16_WARPS * 32, dyn));
-      } else {
-        MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-        MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<false>, U16_WARPS * 32, dyn));
+      // attribute + occupancy per (LUT placement, shared bytes), queried once
+      static thread_local size_t q_dyn[2] = {0, 0};
+      static thread_local int q_per_sm[2] = {1, 1};
+      int& per_sm = q_per_sm[slut ? 1 : 0];
+      if (q_dyn[slut ? 1 : 0] != dyn) {
+        if (slut) {
+          MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+          MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<true>, U16_WARPS * 32, dyn));
+        } else {
+          MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+          MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<false>, U16_WARPS * 32, dyn));
+        }
+        q_dyn[slut ? 1 : 0] = dyn;
       }
       const long long want = (ntiles + U16_WARPS - 1) / U16_WARPS;
       const unsigned grid = (unsigned)std::min<long long>(want, (long long)n_sm * std::max(1, per_sm));
@@ -505,6 +521,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     mx_count_launch();
     MX_CUDA_TRY(cudaGetLastError());
   }
+  mx_host_mark("s1 scan launched");
   u64 h_runs = 0;
   DevError h_err;
   {
@@ -513,6 +530,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     MX_CUDA_TRY(rb.add(&h_err, err.p, sizeof(DevError)));
     MX_CUDA_TRY(rb.sync());
   }
+  mx_host_mark("s1 scan synced");
   if (h_err.null_key_sample != ~0ull) {
     const long long g = (long long)h_err.null_key_sample;
     std::vector<long long> off(d->n_files + 1);
@@ -541,14 +559,14 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(f2.alloc(I, s));
   MX_CUDA_TRY(s2.alloc(I, s));
   MX_CUDA_TRY(e2.alloc(I, s));
-  MX_CUDA_TRY(hist.alloc((long long)256 * rtiles2, s));
-  MX_CUDA_TRY(dtot.alloc(256, s));
+  MX_CUDA_TRY(ws_borrow(hist, s, WS_HIST, (long long)256 * rtiles2));
+  MX_CUDA_TRY(ws_borrow(dtot, s, WS_DTOT, 256));
   u32 *ka = rk.p, *fa_ = rf.p, *sa = rs.p, *ea = re.p;
   u32 *kb = k2.p, *fb = f2.p, *sb = s2.p, *eb = e2.p;
   std::unique_ptr<MxPhase> ph_sort(new MxPhase("radix_sort", s));
   {
     DevBuf<u64> toff;
-    MX_CUDA_TRY(toff.alloc(ntiles + 1, s));
+    MX_CUDA_TRY(ws_borrow(toff, s, WS_TOFF, ntiles + 1));
     if (int rc = gs_run(ntiles, TileOffF{t_cnt.p, toff.p, ntiles}, s)) return rc;
     slot_compact_kernel<<<(unsigned)std::min<long long>(ntiles, (long long)n_sm * 16), 256, 0, s>>>(
         ntiles, tile_len, t_cnt.p, toff.p, rk.p, rf.p, rs.p, re.p, k2.p, f2.p, s2.p, e2.p);
@@ -568,9 +586,13 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     std::swap(ka, kb); std::swap(fa_, fb); std::swap(sa, sb); std::swap(ea, eb);
   }
   ph_sort.reset();
+  mx_host_mark("s1 sort launched");
   // sorted arrays now in (ka, fa_, sa, ea); keep them
-  if (ka == rk.p) {
-    ix.iv_key.take(rk); ix.iv_file.take(rf); ix.iv_start.take(rs); ix.iv_end.take(re);
+  if (ka == rk.p) {  // odd number of passes: the result is in the workspace; copy it out
+    for (auto pr : {std::make_pair(&k2, rk.p), std::make_pair(&f2, rf.p), std::make_pair(&s2, rs.p),
+                    std::make_pair(&e2, re.p)})
+      MX_CUDA_TRY(cudaMemcpyAsync(pr.first->p, pr.second, sizeof(u32) * I, cudaMemcpyDeviceToDevice, s));
+    ix.iv_key.take(k2); ix.iv_file.take(f2); ix.iv_start.take(s2); ix.iv_end.take(e2);
   } else {
     ix.iv_key.take(k2); ix.iv_file.take(f2); ix.iv_start.take(s2); ix.iv_end.take(e2);
   }

@@ -2445,6 +2445,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   DevBuf<u64> pair_off;
   MX_CUDA_TRY(pair_off.alloc(n_pairs + 1, s));
   const unsigned pb = (unsigned)((n_pairs + 255) / 256);
+  mx_host_mark("emit setup");
   emit_count_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p);
   mx_count_launch();
   // exclusive scan of counts in place (each element is read and written by
@@ -2491,6 +2492,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(cudaMemsetAsync(big.p, 0, sizeof(u32), s));
   chunk_pieces_kernel<<<(unsigned)((n_chunks + 256) / 256), 256, 0, s>>>(a, n_chunks, pair_off.p, n_pairs, cpo.p);
   mx_count_launch();
+  mx_host_mark("emit launched");
   if (sort_terms) {
     u32 h_flags = 1;
     long long total = 0;
@@ -2678,6 +2680,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
     plan_fused_kernel<<<1, FP_THREADS, 0, s>>>(fa);
     mx_count_launch();
     MX_CUDA_TRY(cudaGetLastError());
+    mx_host_mark("plan fused launched");
     long long h_out[5];
     std::vector<Phase> h_phases(cap_phases);
     std::vector<u32> h_loff(Km + 1);
@@ -2689,6 +2692,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
       MX_CUDA_TRY(rb.add(h_loff.data(), g->match_L_off.p, sizeof(u32) * (Km + 1)));
       MX_CUDA_TRY(rb.sync());
     }
+    mx_host_mark("plan synced");
     if (h_out[4] == 0) {
       g->match_off.assign(h_loff.begin(), h_loff.end());
       g->match_shared = false;
