@@ -386,9 +386,17 @@ def our_arm(args):
         # share one GPU to exercise the same code path
         dist.init_process_group(os.environ.get("MX_BENCH_BACKEND", "nccl"))
     L = _lib.lib()
-    rt = make_workload(rank, args.scale)
+    strong = args.scaling == "strong"
+    # strong scaling: a fixed total (default the cfg3 1B catalog) split over the
+    # ranks by file; weak: every rank owns its own 100M-sample shard
+    scale = args.total_samples / (world * CFG["n_samples"]) if strong else args.scale
+    rt = make_workload(rank, scale)
     meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
-    cols, table = layout_columns(rt, device_columns(rt, device), args.layout)
+    if strong and args.layout == "tuples":
+        codes, table = run_level_tuples(rt, device)  # no 20 GB int32 expansion at 1B
+        cols = {"tuples": codes}
+    else:
+        cols, table = layout_columns(rt, device_columns(rt, device), args.layout)
     n_cols = len(cols)
     code_bytes = next(iter(cols.values())).element_size()  # 2: u16 row-tuple codes
     spec = synth.cfg2_mixture(CFG["chunk_size"])
@@ -529,9 +537,12 @@ def our_arm(args):
     line = {
         "metric": METRIC, "value": world * n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u16" if code_bytes == 2 else "int32",
-        "data": "synthetic",
-        "config": arm_config(world, args.layout),
+        "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "u16" if code_bytes == 2 else "int32", "data": "synthetic",
+        "config": (dict(arm_config(world, args.layout), workload=f"cfg3 shape: {int(args.total_samples):,} samples "
+                        "in total over all ranks (10k per file), cfg2 properties and mixture, R=64, chunk 1024, "
+                        "seed 42", n_samples=int(args.total_samples), n_files=int(args.total_samples) // 10_000)
+                   if strong else arm_config(world, args.layout)),
         "chunks_per_s": n_chunks / (ms_max * 1e-3),
         "job": {"samples": n, "intervals": n_iv, "keys": n_keys, "blocks": n_blocks, "chunks": n_chunks,
                 "ranges": n_ranges},
@@ -781,6 +792,9 @@ def main():
     ap.add_argument("--layout", default="tuples", choices=["tuples", "columns"],
                     help="catalog layout in HBM: one row-tuple code column, or one code column per property")
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of the cfg2 size (debug only)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak (default): N x 100M samples; strong: --total-samples split over the N ranks")
+    ap.add_argument("--total-samples", type=float, default=1e9, help="strong scaling: samples over all ranks")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the secondary lines (columns layout, registration, 1B job, drop-in serving)")
