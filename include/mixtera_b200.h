@@ -272,6 +272,29 @@ int mx_chunks_merge(int32_t world, int64_t n_chunks, int64_t cap, const int64_t*
                     uint32_t* out_mkey, uint32_t* out_file_index, uint32_t* out_start, uint32_t* out_end,
                     void* stream);
 
+/* Key-partitioned multi-GPU (parallel.build_partitioned). Each global key is
+ * OWNED by one rank; every rank sends the block rows of mx_index_block_table
+ * (global file indices) to the keys' owners. The owner builds an index of
+ * one pseudo-interval [0, samples) per (key, file) block of its keys over the
+ * GLOBAL file table (key codec copied from `like`), and a generator on it:
+ * its per-key cursor shuffles are the reference's over the key's files of
+ * the whole catalog [RangeCursor index.py:126-147], so mx_gen_block_offsets
+ * gives each block's offset in its key's cursor stream (device uint64[n_rows],
+ * in the order of the rows given to mx_index_build_owner). The same call on
+ * rows (packed key, 0, total samples) gives the key-level index every rank
+ * plans on (global per-key totals; chunks.py:188-259 only needs those). */
+int mx_index_build_owner(const mx_index* like, const uint32_t* rows, int64_t n_rows, int32_t n_files,
+                         const int32_t* file_ds, const int64_t* file_ids, void* stream, mx_index** out);
+int mx_gen_block_offsets(mx_gen* gen, uint64_t* offsets, void* stream);
+/* Plans of `gen` (on a key-level index) then emit only `local`'s pieces:
+ * block b of local key k is the key's cursor stream at blk_off[b] (device
+ * uint64[n_blocks]); key_g (device uint32[n_keys]) = its rank in gen's index;
+ * file_lo = global index of local file 0. The buffers must outlive the
+ * generator's plans. Mixtures of <= 32 keys sharing no component (others:
+ * MX_ERR_UNSUPPORTED); pass local == NULL to detach. */
+int mx_gen_set_local(mx_gen* gen, const mx_index* local, const uint64_t* blk_off, const uint32_t* key_g,
+                     int64_t file_lo);
+
 /* ------------------------------------------------------------ registration
  * Metadata registration from JSON-lines bytes in HBM [MetadataCatalog.
  * register_dataset catalog.py:323-435, _parse_one_file catalog.py:246-262,

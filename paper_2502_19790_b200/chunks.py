@@ -296,6 +296,10 @@ class ChunkGenerator:
                                    derive_seed(self.seed, "component-order"),
                                    C.c_void_p(_lib.stream_ptr(stream)), C.byref(out)))
         self._h = out
+        if getattr(index, "partition", None) is not None:  # collective: block offsets from the key owners
+            from .parallel import attach_partition
+
+            attach_partition(self)
         self.last_report: dict | None = None
         self._batch: ChunkBatch | None = None  # planned ahead, not all handed out
         self._served = 0
@@ -364,6 +368,9 @@ class ChunkGenerator:
         return d, keep, mkeys
 
     def _cursor_state(self):
+        if getattr(self.index, "partition", None) is not None:
+            raise NotImplementedError("cursor checkpoints of a key-partitioned generator (use the file-sharded "
+                                      "index, parallel.build_sharded_index, for reference-format states)")
         k = self.index.n_keys
         pos, off = np.zeros(k, np.int64), np.zeros(k, np.int64)
         if k:
@@ -377,6 +384,8 @@ class ChunkGenerator:
         return pos, off
 
     def _set_cursor_state(self, pos, off) -> None:
+        if getattr(self.index, "partition", None) is not None:
+            raise NotImplementedError("cursor checkpoints of a key-partitioned generator")
         if not self.index.n_keys:
             return
         L = _lib.lib()
@@ -414,7 +423,8 @@ class ChunkGenerator:
         nc, nr = C.c_int64(), C.c_int64()
         _lib.check(_lib.lib().mx_gen_result_sizes(self._h, C.byref(nc), C.byref(nr)))
         batch = ChunkBatch(self, nc.value, nr.value, mkeys, spec, arbitrary_size)
-        if getattr(self.index, "shard", None) is not None:  # collective: interleave every rank's pieces
+        if getattr(self.index, "shard", None) is not None or getattr(self.index, "partition", None) is not None:
+            # collective: interleave every rank's pieces
             from .parallel import merge_batch
 
             batch = merge_batch(self, batch, self.stream)

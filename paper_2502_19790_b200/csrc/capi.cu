@@ -631,6 +631,55 @@ int mx_index_build_sharded(const mx_index* local, const mx_shard_desc* desc, voi
   return MX_OK;
 }
 
+int mx_index_build_owner(const mx_index* like, const uint32_t* rows, int64_t n_rows, int32_t n_files,
+                         const int32_t* file_ds, const int64_t* file_ids, void* stream, mx_index** out) {
+  if (like)
+    if (int rc = ix_resolve(const_cast<IndexData*>(&like->d))) return rc;
+  MX_CHECK_ARG(like && out && (rows || n_rows == 0), "null argument");
+  MX_CHECK_ARG(n_rows >= 0 && n_rows < (1ll << 32), "bad row count");
+  MX_CHECK_ARG(n_files >= 1 && file_ds && file_ids, "need the global file table");
+  g_err.clear();
+  keep_pool_warm();
+  mx_index* ix = new mx_index();
+  int rc = owner_index_build(&like->d, rows, n_rows, n_files, file_ds, file_ids, (cudaStream_t)stream, &ix->d);
+  if (rc < 0) {
+    delete ix;
+    return rc;
+  }
+  *out = ix;
+  return MX_OK;
+}
+
+int mx_gen_block_offsets(mx_gen* gen, uint64_t* offsets, void* stream) {
+  MX_CHECK_ARG(gen && (offsets || gen->d.ix->n_intervals == 0), "null argument");
+  g_err.clear();
+  cudaStream_t s = (cudaStream_t)stream;
+  if (s != gen->d.stream) {  // behind the cursor layout
+    cudaEvent_t e;
+    MX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaError_t err = cudaEventRecord(e, gen->d.stream);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(s, e, 0);
+    cudaEventDestroy(e);
+    MX_CUDA_TRY(err);
+  }
+  return gen_block_offsets(&gen->d, reinterpret_cast<u64*>(offsets), s);
+}
+
+int mx_gen_set_local(mx_gen* gen, const mx_index* local, const uint64_t* blk_off, const uint32_t* key_g,
+                     int64_t file_lo) {
+  MX_CHECK_ARG(gen, "null argument");
+  g_err.clear();
+  if (!local) {
+    gen->d.local = LocalSrc{};
+    return MX_OK;
+  }
+  if (int rc = ix_resolve(const_cast<IndexData*>(&local->d))) return rc;
+  MX_CHECK_ARG((blk_off && key_g) || local->d.n_blocks == 0, "null block offsets / key map");
+  MX_CHECK_ARG(file_lo >= 0 && file_lo + local->d.n_files <= gen->d.ix->n_files, "local files outside the file table");
+  gen->d.local = LocalSrc{&local->d, reinterpret_cast<const u64*>(blk_off), key_g, (long long)file_lo};
+  return MX_OK;
+}
+
 int mx_chunks_merge(int32_t world, int64_t n_chunks, int64_t cap, const int64_t* offs, const uint32_t* mkey,
                     const uint32_t* file_index, const uint32_t* start, const uint32_t* end, int64_t* out_off,
                     uint32_t* out_mkey, uint32_t* out_file_index, uint32_t* out_start, uint32_t* out_end,

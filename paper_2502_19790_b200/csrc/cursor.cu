@@ -314,4 +314,35 @@ int gen_host_mirrors(GenData* g) {
   return MX_OK;
 }
 
+
+// Offset of every interval of the generator's index in its key's cursor
+// stream (in the owner index's input row order when it has one, else index
+// order): position j of the cursor layout holds interval
+// civ[j]; key k's positions occupy [blk_first[key_blk_first[k]], ...).
+// On an owner index (one pseudo-interval per (key, file) block) this is each
+// block's cursor-stream offset -- what the file's owner rank needs to place
+// its intervals in the global streams.
+__global__ void block_offsets_kernel(long long I, const u32* civ, const u64* ccum, const u32* blk_key,
+                                     const u32* key_blk_first, const u32* blk_first, const u32* row, u64* out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= I) return;
+  const u32 iv = civ[j];  // == its block (one interval per block)
+  const u32 k = blk_key[iv];
+  out[row ? row[iv] : iv] = ccum[j] - ccum[blk_first[key_blk_first[k]]];
+}
+
+int gen_block_offsets(GenData* g, u64* out, cudaStream_t s) {
+  IndexData* ix = g->ix;
+  if (ix->n_blocks != ix->n_intervals)
+    return mx_fail(MX_ERR_INVALID, "block offsets need an index with one interval per block (an owner index)");
+  const long long I = ix->n_intervals;
+  if (I == 0) return MX_OK;
+  block_offsets_kernel<<<(unsigned)((I + 255) / 256), 256, 0, s>>>(I, g->civ.p, g->ccum.p, ix->blk_key.p,
+                                                                  ix->key_blk_first.p, ix->blk_first.p,
+                                                                  ix->owner_row.n ? ix->owner_row.p : nullptr, out);
+  mx_count_launch();
+  MX_CUDA_TRY(cudaGetLastError());
+  return MX_OK;
+}
+
 }  // namespace mx

@@ -125,6 +125,7 @@ struct IndexData {
   long long file_lo = 0, file_hi = 0;
   long long n_local = 0;  // this rank's (real) intervals in the hybrid index
   DevBuf<u32> iv_nreal;
+  DevBuf<u32> owner_row;  // owner index (owner_index_build): input row of every interval
   // sizes still travelling to the host (index_finalize with defer): the
   // build returns without waiting; ix_resolve() waits for them on first use
   struct Pending {
@@ -150,6 +151,16 @@ int ix_resolve(IndexData* ix);
 cudaError_t aux_streams(int dev, cudaStream_t out[3]);
 cudaError_t aux_event_take(int dev, cudaEvent_t* e);
 void aux_event_give(int dev, cudaEvent_t e);
+
+// Key-partitioned emission (parallel.py build_partitioned): the generator
+// plans over per-key totals (a key-level index) and cuts only THIS rank's
+// intervals, placed by their blocks' offsets in the global cursor streams.
+struct LocalSrc {
+  const IndexData* loc = nullptr;  // this rank's index (file indices local)
+  const u64* blk_off = nullptr;    // device [loc->n_blocks]: block offset in its key's global cursor stream
+  const u32* key_g = nullptr;      // device [loc->n_keys]: global component rank of each local key
+  long long file_lo = 0;           // global index of local file 0
+};
 
 struct GenData {
   IndexData* ix = nullptr;
@@ -216,6 +227,7 @@ struct GenData {
   cudaEvent_t ev_fork = nullptr, ev_order = nullptr, ev_tot = nullptr, ev_ready = nullptr;
   cudaEvent_t ev_plan = nullptr, ev_seg = nullptr, ev_seed_fork = nullptr, ev_seed = nullptr;
   bool fresh_layout = false;  // no work on `stream` since cursor_build except the layout itself
+  LocalSrc local;             // set: plans emit this rank's pieces of the global chunks (emit_local)
   int aux_dev = -1;
   cudaError_t aux_init() {  // streams shared per device, events pooled (capi.cu)
     if (ostream) return cudaSuccess;
@@ -253,6 +265,9 @@ int index_block_table(const IndexData* ix, u32 file_base, uint4* out, cudaStream
 int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream_t s, IndexData* out);
 int gen_local_lists(GenData* g, cudaStream_t s);
 int gen_host_mirrors(GenData* g);
+int gen_block_offsets(GenData* g, u64* out, cudaStream_t s);
+int owner_index_build(const IndexData* src, const u32* rows, long long n, int n_files, const int32_t* file_ds,
+                      const int64_t* file_ids, cudaStream_t s, IndexData* out);
 int excl_scan_ll(const u64* in, long long n, long long* out, cudaStream_t s);
 int gen_result_json(GenData* g, const mx_json_desc* d, cudaStream_t s);
 int chunks_merge(int W, long long C, long long cap, const long long* offs, const u32* mkey, const u32* file,

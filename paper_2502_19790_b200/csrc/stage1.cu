@@ -892,4 +892,87 @@ int rows_build(const mx_rows_desc* d, cudaStream_t s, IndexData* out) {
   return rc;
 }
 
+
+// ---------------------------------------------------------------- owner index
+// Key-partitioned multi-GPU layout: the index an OWNER rank builds over the
+// (key, file) blocks of the keys it owns, gathered from every rank (device
+// rows uint32[n][4] = packed key, global file index, samples, intervals).
+// One pseudo-interval [0, samples) per block, sorted by (packed key, file),
+// the codec (key strings, fields) copied from this rank's local index: its
+// generator's RangeCursor shuffles are the reference's over the key's files
+// of the WHOLE catalog (index.py:134-144), and its cursor prefix sums give
+// every block's offset in its key's cursor stream.
+__global__ void owner_rows_kernel(long long n, const uint4* rows, u32* key, u32* file, u32* start, u32* end) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 r = rows[i];
+  key[i] = r.x;
+  file[i] = r.y;
+  start[i] = (u32)i;  // row id through the sort (owner_row); the pseudo-interval starts at 0
+  end[i] = r.z;
+}
+
+int owner_index_build(const IndexData* src, const u32* rows, long long n, int n_files, const int32_t* file_ds,
+                      const int64_t* file_ids, cudaStream_t s, IndexData* out) {
+  IndexData& ix = *out;
+  ix.stream = s;
+  ix.n_files = n_files;
+  ix.key_bits = src->key_bits;
+  ix.n_props = src->n_props;
+  for (int p = 0; p < MX_MAX_PROPS; ++p) {
+    ix.field_shift[p] = src->field_shift[p];
+    ix.field_width[p] = src->field_width[p];
+    ix.str_base[p] = src->str_base[p];
+  }
+  MX_CUDA_TRY(ix.str_off.alloc(src->str_off.n, s));
+  MX_CUDA_TRY(ix.str_bytes.alloc(src->str_bytes.n, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(ix.str_off.p, src->str_off.p, sizeof(long long) * src->str_off.n,
+                              cudaMemcpyDeviceToDevice, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(ix.str_bytes.p, src->str_bytes.p, src->str_bytes.n, cudaMemcpyDeviceToDevice, s));
+  MX_CUDA_TRY(ix.file_ds.alloc(std::max(1, n_files), s));
+  MX_CUDA_TRY(ix.file_ids.alloc(std::max(1, n_files), s));
+  if (n_files > 0) {
+    MX_CUDA_TRY(mx_h2d(ix.file_ds.p, file_ds, sizeof(int32_t) * n_files, s));
+    MX_CUDA_TRY(mx_h2d(ix.file_ids.p, file_ids, sizeof(long long) * n_files, s));
+  }
+  ix.h_file_ds.assign(file_ds, file_ds + n_files);
+  ix.h_file_ids.assign(file_ids, file_ids + n_files);
+  if (n == 0) {
+    ix.n_intervals = ix.n_keys = ix.n_blocks = 0;
+    return MX_OK;
+  }
+  DevBuf<u32> a[4], b[4], hist, dtot;
+  for (int j = 0; j < 4; ++j) {
+    MX_CUDA_TRY(a[j].alloc(n, s));
+    MX_CUDA_TRY(b[j].alloc(n, s));
+  }
+  owner_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, reinterpret_cast<const uint4*>(rows), a[0].p,
+                                                               a[1].p, a[2].p, a[3].p);
+  mx_count_launch();
+  const int tiles = (int)((n + RS_THREADS * 8 - 1) / (RS_THREADS * 8));
+  MX_CUDA_TRY(hist.alloc((long long)256 * tiles, s));
+  MX_CUDA_TRY(dtot.alloc(256, s));
+  MX_CUDA_TRY(cudaFuncSetAttribute(radix_downsweep2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(4 * RS_THREADS * 8 * sizeof(u32))));
+  u32 *k = a[0].p, *f = a[1].p, *st = a[2].p, *en = a[3].p;
+  u32 *k2 = b[0].p, *f2 = b[1].p, *st2 = b[2].p, *en2 = b[3].p;
+  if (int rc = radix_sort_by(f, k, st, en, f2, k2, st2, en2, n, bits_of((u32)std::max(0, n_files - 1)), hist.p,
+                             dtot.p, s))
+    return rc;
+  if (int rc = radix_sort_by(k, f, st, en, k2, f2, st2, en2, n, (int)ix.key_bits, hist.p, dtot.p, s)) return rc;
+  MX_CUDA_TRY(ix.iv_key.alloc(n, s));
+  MX_CUDA_TRY(ix.iv_file.alloc(n, s));
+  MX_CUDA_TRY(ix.iv_start.alloc(n, s));
+  MX_CUDA_TRY(ix.iv_end.alloc(n, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(ix.iv_key.p, k, sizeof(u32) * n, cudaMemcpyDeviceToDevice, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(ix.iv_file.p, f, sizeof(u32) * n, cudaMemcpyDeviceToDevice, s));
+  MX_CUDA_TRY(ix.owner_row.alloc(n, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(ix.owner_row.p, st, sizeof(u32) * n, cudaMemcpyDeviceToDevice, s));
+  MX_CUDA_TRY(cudaMemsetAsync(ix.iv_start.p, 0, sizeof(u32) * n, s));
+  MX_CUDA_TRY(cudaMemcpyAsync(ix.iv_end.p, en, sizeof(u32) * n, cudaMemcpyDeviceToDevice, s));
+  int rc = index_finalize(&ix, n, s);
+  ix.n_samples_total = ix.indexed_samples;
+  return rc;
+}
+
 }  // namespace mx

@@ -2376,8 +2376,329 @@ enum ScratchSlot { S_WTS, S_SOFF, S_SEGC, S_SEGLO, S_SEGPRE, S_PHASES, S_TERMS, 
 // (a (chunk, term) range yields one piece plus one per interval or stream
 // segment boundary inside it, and every stream position belongs to exactly
 // one range), so no count has to travel to the host mid-way.
+// Per-chunk normalisation of a chunk CSR of cut pieces (cpo offsets) and the
+// dense result: sort by (mixture key, file, start) + merge per chunk, scan of
+// the merged counts, compaction into the generator's result arrays.
+static int normalize_tail(GenData* g, long long n_chunks, DevBuf<u64>& cpo, DevBuf<u64>& mcnt, DevBuf<u32>& big,
+                          DevBuf<u32>& pm, DevBuf<u32>& pf, DevBuf<u32>& ps, DevBuf<u32>& pe, long long cap,
+                          bool pack, int fbits, cudaEvent_t seed_join, cudaStream_t s) {
+  {
+    DevBuf<u32> blist, bcnt;
+    MX_CUDA_TRY(blist.alloc(n_chunks, s));
+    MX_CUDA_TRY(bcnt.alloc(1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(bcnt.p, 0, sizeof(u32), s));
+    DevBuf<u32> wlist, wcnt;
+    MX_CUDA_TRY(wlist.alloc(n_chunks, s));
+    MX_CUDA_TRY(wcnt.alloc(1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(wcnt.p, 0, sizeof(u32), s));
+    normalize_tiny_kernel<<<(unsigned)((n_chunks + 255) / 256), 256, 0, s>>>(n_chunks, cpo.p, pm.p, pf.p, ps.p, pe.p,
+                                                                           mcnt.p, wlist.p, wcnt.p);
+    mx_count_launch();
+    const long long wgrid = std::min<long long>((n_chunks + 7) / 8, 148 * 16);
+    // pack (mkey, file, start) into one u64 when mkey and file ids fit 32 bits together
+    if (pack)  // keys < 2^63: never the ~0 padding
+      normalize_warp_kernel<true><<<(unsigned)wgrid, 256, 0, s>>>(wlist.p, wcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p,
+                                                                  mcnt.p, blist.p, bcnt.p, fbits);
+    else
+      normalize_warp_kernel<false><<<(unsigned)wgrid, 256, 0, s>>>(wlist.p, wcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p,
+                                                                   mcnt.p, blist.p, bcnt.p, 0);
+    mx_count_launch();
+    long long grid = n_chunks < 148 * 4 ? n_chunks : 148 * 4;
+    normalize_kernel<<<(unsigned)grid, NMB_THREADS, 0, s>>>(blist.p, bcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p,
+                                                           big.p);
+    mx_count_launch();
+  }
+  if (int rc = excl_scan<long long>(mcnt.p, n_chunks, g->res_off.p, s)) return rc;
+  MX_CUDA_TRY(g->res_mkey.reserve(cap, s));
+  MX_CUDA_TRY(g->res_file.reserve(cap, s));
+  MX_CUDA_TRY(g->res_start.reserve(cap, s));
+  MX_CUDA_TRY(g->res_end.reserve(cap, s));
+  {
+    // few ranges per chunk (sharded ranks): lanes copy chunks; else warps
+    const bool grouped = g->ix->sharded;
+    const long long grid = std::min<long long>(grouped ? (n_chunks + 255) / 256 : (n_chunks + 7) / 8, 148 * 16);
+    compact_warp_kernel<<<(unsigned)grid, 256, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
+                                                       g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p,
+                                                       grouped);
+    mx_count_launch();
+  }
+  MX_CUDA_TRY(cudaStreamWaitEvent(s, seed_join, 0));  // chunk seeds (side stream) done
+  MX_CUDA_TRY(cudaGetLastError());
+  u32 h_big = 0;
+  long long total = 0;
+  {
+    D2HBatch rb(s);
+    MX_CUDA_TRY(rb.add(&h_big, big.p, sizeof(u32)));
+    MX_CUDA_TRY(rb.add(&total, g->res_off.p + n_chunks, sizeof(long long)));
+    MX_CUDA_TRY(rb.sync());
+  }
+  if (h_big) return mx_fail(MX_ERR_UNSUPPORTED, "a chunk has %u ranges before merging (> %d supported)", h_big, NM_CAP);
+  g->res_ranges = total;
+  g->next_chunk_id += n_chunks;
+  return MX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Local-driven emission (key-partitioned multi-GPU, GenData::local): the plan
+// ran on a key-level index (global per-key totals); this rank walks its OWN
+// intervals: block b of local key kl is component g = key_g[kl] at offset
+// blk_off[b] of g's global cursor stream, which sits in mixture-key stream m
+// at segment seg (mode 0: one stream per component). A stream position maps
+// to a chunk through stream m's terms (phases in chunk order; bases
+// increasing; chunk j of a term covers [base + j*stride, + len)). Work is
+// O(local intervals + pieces), not O(global chunks x terms).
+struct StreamTerm {
+  u64 base, len, stride;  // len > 0, stride >= len (chunks of a term never overlap)
+  long long chunk_begin, n_chunks;
+  u32 m;
+};
+
+struct LocalCut {
+  long long B;             // local blocks
+  const u32* blk_key;      // local index
+  const u32* blk_first;
+  const u64* iv_cum;
+  const u32* iv_file;
+  const u32* iv_start;
+  const u64* blk_off;
+  const u32* key_g;
+  long long file_lo;
+  const int* comp_seg;     // [K] segment of the component in its stream (-1: no mixture key)
+  const int* comp_str;     // [K] its stream (mixture key)
+  const u64* seg_pre;      // stream prefix (segment i of stream m at seg_pre[i + m])
+  const u64* seg_lo;       // consumed part of each segment's component at plan start
+  const u32* st_off;       // [n_streams + 1] term list of every stream
+  const StreamTerm* st;
+  int arbitrary;           // pieces carry the component id (mode 2)
+};
+
+__global__ void comp_seg_kernel(int n_streams, const u32* s_off, const u32* seg_comp, int* comp_seg, int* comp_str) {
+  const int m = blockIdx.x;
+  if (m >= n_streams) return;
+  for (u32 i = s_off[m] + threadIdx.x; i < s_off[m + 1]; i += blockDim.x) {
+    comp_seg[seg_comp[i]] = (int)i;
+    comp_str[seg_comp[i]] = m;
+  }
+}
+
+template <bool WRITE>
+__global__ void local_cut_kernel(LocalCut a, u64* cnt, const u64* off, u32* pc, u32* pm, u32* pf, u32* ps, u32* pe) {
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  const u32 g = a.key_g[a.blk_key[b]];
+  const int seg = a.comp_seg[g];
+  u64 n = 0, o_out = WRITE ? off[b] : 0;
+  if (seg >= 0) {
+    const int m = a.comp_str[g];
+    const u64 ob = a.blk_off[b], lo = a.seg_lo[seg], pre = a.seg_pre[seg + m];
+    const u64 take = a.seg_pre[seg + 1 + m] - pre;  // the segment's part of the component this plan hands out
+    const u32 t_lo = a.st_off[m], t_hi = a.st_off[m + 1];
+    const u32 i0 = a.blk_first[b], i1 = a.blk_first[b + 1];
+    const u64 c0 = a.iv_cum[i0];
+    for (u32 i = i0; i < i1; ++i) {
+      const u64 o = ob + (a.iv_cum[i] - c0), len = a.iv_cum[i + 1] - a.iv_cum[i];
+      if (o + len <= lo || o >= lo + take) continue;  // handed out before / not in this plan
+      const u64 a0 = o > lo ? o : lo, a1 = o + len < lo + take ? o + len : lo + take;
+      const u64 xs = pre + (a0 - lo), xe = pre + (a1 - lo);
+      const u32 s0 = a.iv_start[i] + (u32)(a0 - o);
+      // last term with base <= xs (terms of a stream are disjoint and in stream order)
+      u32 tl = t_lo, th = t_hi;
+      while (tl < th) {
+        const u32 mid = (tl + th) >> 1;
+        if (a.st[mid].base <= xs) tl = mid + 1; else th = mid;
+      }
+      u32 t = tl > t_lo ? tl - 1 : t_lo;
+      u64 x = xs;
+      while (x < xe && t < t_hi) {
+        const StreamTerm T = a.st[t];
+        if (x < T.base) x = T.base;  // positions no term hands out
+        if (x >= xe) break;
+        const long long j = T.stride > 0 ? (long long)((x - T.base) / T.stride) : 0;
+        if (j >= T.n_chunks) {
+          ++t;
+          continue;
+        }
+        const u64 c_lo = T.base + (u64)j * T.stride, c_hi = c_lo + T.len;
+        if (x >= c_hi) {  // between two chunks of a strided term
+          if (j + 1 < T.n_chunks) x = c_lo + T.stride;
+          else ++t;
+          continue;
+        }
+        const u64 e = xe < c_hi ? xe : c_hi;
+        if (WRITE) {
+          const u64 q = o_out + n;
+          pc[q] = (u32)(T.chunk_begin + j);
+          pm[q] = a.arbitrary ? g : T.m;
+          pf[q] = (u32)(a.file_lo + a.iv_file[i]);
+          ps[q] = s0 + (u32)(x - xs);
+          pe[q] = s0 + (u32)(e - xs);
+        }
+        ++n;
+        x = e;
+      }
+    }
+  }
+  if (!WRITE) cnt[b] = n;
+}
+
+// pieces -> chunk CSR (order inside a chunk is settled by the normalisation)
+__global__ void chunk_hist_kernel(long long n, const u32* pc, u64* cc) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(reinterpret_cast<unsigned long long*>(cc + pc[i]), 1ull);
+}
+
+__global__ void chunk_scatter_kernel(long long n, const u32* pc, const u32* pm, const u32* pf, const u32* ps,
+                                     const u32* pe, const u64* cpo, unsigned long long* fill, u32* qm, u32* qf,
+                                     u32* qs, u32* qe) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u32 c = pc[i];
+  const u64 q = cpo[c] + atomicAdd(fill + c, 1ull);
+  qm[q] = pm[i];
+  qf[q] = pf[i];
+  qs[q] = ps[i];
+  qe[q] = pe[i];
+}
+
+static int emit_local(GenData* g, const PlanWork& w, const Phase* h_phases, const Term* terms, long long n_chunks,
+                      long long n_phases, cudaStream_t s) {
+  const int Km = w.n_streams;
+  IndexData* ix = g->ix;  // key-level index (global keys, global file table)
+  const LocalSrc& L = g->local;
+  MxPhase ph("emit", s);
+  g->h_small_valid = 0;
+  g->res_chunks = n_chunks;
+  g->res_ranges = 0;
+  MX_CUDA_TRY(g->res_off.reserve(n_chunks + 1, s));
+  MX_CUDA_TRY(g->res_seed.reserve(n_chunks > 0 ? n_chunks : 1, s));
+  MX_CUDA_TRY(g->res_id.reserve(n_chunks > 0 ? n_chunks : 1, s));
+  MX_CUDA_TRY(g->aux_init());
+  cudaEvent_t seed_join = g->ev_seed;
+  if (n_chunks > 0) {
+    MX_CUDA_TRY(cudaEventRecord(g->ev_seed_fork, s));
+    MX_CUDA_TRY(cudaStreamWaitEvent(g->sstream, g->ev_seed_fork, 0));
+    chunk_seed_kernel<<<(unsigned)((n_chunks + 127) / 128), 128, 0, g->sstream>>>(
+        n_chunks, g->next_chunk_id, g->chunk_prefix.p, g->chunk_prefix_len, g->res_seed.p, g->res_id.p);
+    mx_count_launch();
+    MX_CUDA_TRY(cudaEventRecord(seed_join, g->sstream));
+  }
+  if (n_chunks == 0) {
+    const long long z = 0;
+    MX_CUDA_TRY(mx_h2d(g->res_off.p, &z, sizeof(z), s));
+    MX_CUDA_TRY(cudaStreamSynchronize(s));
+    return MX_OK;
+  }
+  const long long K = g->K;
+  // stream term tables (host: a few hundred terms)
+  long long n_terms = 0;
+  for (long long p = 0; p < n_phases; ++p) n_terms = std::max(n_terms, h_phases[p].term_begin + h_phases[p].n_terms);
+  std::vector<Term> h_terms(n_terms);
+  if (n_terms) {
+    MX_CUDA_TRY(cudaMemcpyAsync(h_terms.data(), terms, sizeof(Term) * n_terms, cudaMemcpyDeviceToHost, s));
+    MX_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  std::vector<std::vector<StreamTerm>> per(Km);
+  for (long long p = 0; p < n_phases; ++p)
+    for (long long t = 0; t < h_phases[p].n_terms; ++t) {
+      const Term& T = h_terms[h_phases[p].term_begin + t];
+      if (T.len == 0 || h_phases[p].n_chunks == 0) continue;
+      if (T.stride < T.len && h_phases[p].n_chunks > 1)
+        return mx_fail(MX_ERR_UNSUPPORTED, "overlapping chunk terms in a partitioned plan");
+      if (!per[T.stream].empty()) {  // the walk needs each stream's terms disjoint and in stream order
+        const StreamTerm& q = per[T.stream].back();
+        if (q.base + (u64)(q.n_chunks - 1) * q.stride + q.len > T.base)
+          return mx_fail(MX_ERR_UNSUPPORTED, "interleaved chunk terms in a partitioned plan");
+      }
+      per[T.stream].push_back(
+          StreamTerm{T.base, T.len, T.stride, h_phases[p].chunk_begin, h_phases[p].n_chunks, T.m});
+    }
+  std::vector<u32> st_off(Km + 1, 0);
+  std::vector<StreamTerm> st;
+  for (int m = 0; m < Km; ++m) {
+    st.insert(st.end(), per[m].begin(), per[m].end());
+    st_off[m + 1] = (u32)st.size();
+  }
+  DevBuf<u32> d_st_off;
+  DevBuf<StreamTerm> d_st;
+  DevBuf<int> comp_seg, comp_str;
+  MX_CUDA_TRY(d_st_off.alloc(Km + 1, s));
+  MX_CUDA_TRY(d_st.alloc(std::max<long long>(1, (long long)st.size()), s));
+  MX_CUDA_TRY(mx_h2d(d_st_off.p, st_off.data(), sizeof(u32) * (Km + 1), s));
+  if (!st.empty()) MX_CUDA_TRY(mx_h2d(d_st.p, st.data(), sizeof(StreamTerm) * st.size(), s));
+  MX_CUDA_TRY(comp_seg.alloc(K, s));
+  MX_CUDA_TRY(comp_str.alloc(K, s));
+  MX_CUDA_TRY(cudaMemsetAsync(comp_seg.p, 0xff, sizeof(int) * K, s));
+  comp_seg_kernel<<<Km, 128, 0, s>>>(Km, w.s_off, w.seg_comp, comp_seg.p, comp_str.p);
+  mx_count_launch();
+  const IndexData* loc = L.loc;
+  const long long B = loc->n_blocks;
+  LocalCut a{};
+  a.B = B;
+  a.blk_key = loc->blk_key.p;
+  a.blk_first = loc->blk_first.p;
+  a.iv_cum = loc->iv_cum.p;
+  a.iv_file = loc->iv_file.p;
+  a.iv_start = loc->iv_start.p;
+  a.blk_off = L.blk_off;
+  a.key_g = L.key_g;
+  a.file_lo = L.file_lo;
+  a.comp_seg = comp_seg.p;
+  a.comp_str = comp_str.p;
+  a.seg_pre = w.seg_pre;
+  a.seg_lo = w.seg_lo;
+  a.st_off = d_st_off.p;
+  a.st = d_st.p;
+  a.arbitrary = w.mode == 2;
+  DevBuf<u64> boff;
+  MX_CUDA_TRY(boff.alloc(B + 1, s));
+  const unsigned bg = (unsigned)((B + 255) / 256);
+  if (B > 0) {
+    local_cut_kernel<false><<<bg, 256, 0, s>>>(a, boff.p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    mx_count_launch();
+  }
+  if (int rc = excl_scan<u64>(boff.p, B, boff.p, s)) return rc;
+  u64 n_p = 0;
+  MX_CUDA_TRY(cudaMemcpyAsync(&n_p, boff.p + B, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  MX_CUDA_TRY(cudaStreamSynchronize(s));
+  const long long cap = (long long)n_p + 1;
+  DevBuf<u32> pc, pm, pf, ps, pe, qm, qf, qs, qe;
+  for (DevBuf<u32>* x : {&pc, &pm, &pf, &ps, &pe, &qm, &qf, &qs, &qe}) MX_CUDA_TRY(x->alloc(cap, s));
+  if (B > 0) {
+    local_cut_kernel<true><<<bg, 256, 0, s>>>(a, nullptr, boff.p, pc.p, pm.p, pf.p, ps.p, pe.p);
+    mx_count_launch();
+  }
+  DevBuf<u64> cc, cpo, mcnt;
+  DevBuf<unsigned long long> fill;
+  DevBuf<u32> big;
+  MX_CUDA_TRY(cc.alloc(n_chunks, s));
+  MX_CUDA_TRY(cpo.alloc(n_chunks + 1, s));
+  MX_CUDA_TRY(mcnt.alloc(n_chunks, s));
+  MX_CUDA_TRY(fill.alloc(n_chunks, s));
+  MX_CUDA_TRY(big.alloc(1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(cc.p, 0, sizeof(u64) * n_chunks, s));
+  MX_CUDA_TRY(cudaMemsetAsync(fill.p, 0, sizeof(unsigned long long) * n_chunks, s));
+  MX_CUDA_TRY(cudaMemsetAsync(big.p, 0, sizeof(u32), s));
+  const long long np = (long long)n_p;
+  if (np > 0) {
+    chunk_hist_kernel<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(np, pc.p, cc.p);
+    mx_count_launch();
+  }
+  if (int rc = excl_scan<u64>(cc.p, n_chunks, cpo.p, s)) return rc;
+  if (np > 0) {
+    chunk_scatter_kernel<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(np, pc.p, pm.p, pf.p, ps.p, pe.p, cpo.p,
+                                                                      fill.p, qm.p, qf.p, qs.p, qe.p);
+    mx_count_launch();
+  }
+  int fbits = 1, mbits = 1;
+  while ((1ll << fbits) < (long long)ix->n_files + 1) ++fbits;
+  while ((1ll << mbits) < (long long)(w.max_mkey > 0 ? w.max_mkey : Km) + 1) ++mbits;
+  const bool pack = fbits + mbits <= 31;
+  return normalize_tail(g, n_chunks, cpo, mcnt, big, qm, qf, qs, qe, cap, pack, fbits, seed_join, s);
+}
+
 static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase* h_phases, const Term* terms,
                 long long n_chunks, long long n_phases, long long n_seg, cudaStream_t s) {
+  if (g->local.loc) return emit_local(g, w, h_phases, terms, n_chunks, n_phases, s);  // key-partitioned rank
   IndexData* ix = g->ix;
   MxPhase ph("emit", s);
   g->h_small_valid = 0;
@@ -2515,60 +2836,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
       return MX_OK;
     }
   }
-  {
-    DevBuf<u32> blist, bcnt;
-    MX_CUDA_TRY(blist.alloc(n_chunks, s));
-    MX_CUDA_TRY(bcnt.alloc(1, s));
-    MX_CUDA_TRY(cudaMemsetAsync(bcnt.p, 0, sizeof(u32), s));
-    DevBuf<u32> wlist, wcnt;
-    MX_CUDA_TRY(wlist.alloc(n_chunks, s));
-    MX_CUDA_TRY(wcnt.alloc(1, s));
-    MX_CUDA_TRY(cudaMemsetAsync(wcnt.p, 0, sizeof(u32), s));
-    normalize_tiny_kernel<<<(unsigned)((n_chunks + 255) / 256), 256, 0, s>>>(n_chunks, cpo.p, pm.p, pf.p, ps.p, pe.p,
-                                                                           mcnt.p, wlist.p, wcnt.p);
-    mx_count_launch();
-    const long long wgrid = std::min<long long>((n_chunks + 7) / 8, 148 * 16);
-    // pack (mkey, file, start) into one u64 when mkey and file ids fit 32 bits together
-    if (pack)  // keys < 2^63: never the ~0 padding
-      normalize_warp_kernel<true><<<(unsigned)wgrid, 256, 0, s>>>(wlist.p, wcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p,
-                                                                  mcnt.p, blist.p, bcnt.p, fbits);
-    else
-      normalize_warp_kernel<false><<<(unsigned)wgrid, 256, 0, s>>>(wlist.p, wcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p,
-                                                                   mcnt.p, blist.p, bcnt.p, 0);
-    mx_count_launch();
-    long long grid = n_chunks < 148 * 4 ? n_chunks : 148 * 4;
-    normalize_kernel<<<(unsigned)grid, NMB_THREADS, 0, s>>>(blist.p, bcnt.p, cpo.p, pm.p, pf.p, ps.p, pe.p, mcnt.p,
-                                                           big.p);
-    mx_count_launch();
-  }
-  if (int rc = excl_scan<long long>(mcnt.p, n_chunks, g->res_off.p, s)) return rc;
-  MX_CUDA_TRY(g->res_mkey.reserve(cap, s));
-  MX_CUDA_TRY(g->res_file.reserve(cap, s));
-  MX_CUDA_TRY(g->res_start.reserve(cap, s));
-  MX_CUDA_TRY(g->res_end.reserve(cap, s));
-  {
-    // few ranges per chunk (sharded ranks): lanes copy chunks; else warps
-    const bool grouped = g->ix->sharded;
-    const long long grid = std::min<long long>(grouped ? (n_chunks + 255) / 256 : (n_chunks + 7) / 8, 148 * 16);
-    compact_warp_kernel<<<(unsigned)grid, 256, 0, s>>>(n_chunks, cpo.p, g->res_off.p, pm.p, pf.p, ps.p, pe.p,
-                                                       g->res_mkey.p, g->res_file.p, g->res_start.p, g->res_end.p,
-                                                       grouped);
-    mx_count_launch();
-  }
-  MX_CUDA_TRY(cudaStreamWaitEvent(s, seed_join, 0));  // chunk seeds (side stream) done
-  MX_CUDA_TRY(cudaGetLastError());
-  u32 h_big = 0;
-  long long total = 0;
-  {
-    D2HBatch rb(s);
-    MX_CUDA_TRY(rb.add(&h_big, big.p, sizeof(u32)));
-    MX_CUDA_TRY(rb.add(&total, g->res_off.p + n_chunks, sizeof(long long)));
-    MX_CUDA_TRY(rb.sync());
-  }
-  if (h_big) return mx_fail(MX_ERR_UNSUPPORTED, "a chunk has %u ranges before merging (> %d supported)", h_big, NM_CAP);
-  g->res_ranges = total;
-  g->next_chunk_id += n_chunks;
-  return MX_OK;
+  return normalize_tail(g, n_chunks, cpo, mcnt, big, pm, pf, ps, pe, cap, pack, fbits, seed_join, s);
 }
 
 // per mixture key the matching components IN COMPONENT ORDER
@@ -2613,7 +2881,7 @@ int plan_mixture(GenData* g, const mx_mixture_desc* mix, long long max_chunks, l
   }
   const bool fresh = g->fresh_layout;
   g->fresh_layout = false;
-  const bool small = max_chunks <= SMALL_MAX_CHUNKS && mix->chunk_size <= NM_CAP;
+  const bool small = max_chunks <= SMALL_MAX_CHUNKS && mix->chunk_size <= NM_CAP && !g->local.loc;
   std::unique_ptr<MxPhase> ph_plan(new MxPhase("plan", s));
   // ---- matching
   MatchArgs ma{};

@@ -212,7 +212,7 @@ class ChunkerIndex:
     def file_table(self) -> tuple[np.ndarray, np.ndarray]:
         """(dataset ids, file ids) of the index's file table (the global table
         for a file-sharded index)."""
-        sh = getattr(self, "shard", None)
+        sh = getattr(self, "shard", None) or getattr(self, "partition", None)
         if sh is not None:
             return sh.file_ds, sh.file_ids
         return self.catalog.file_ds, self.catalog.file_ids

@@ -289,7 +289,7 @@ def merge_batch(gen, batch, stream=None):
 
     from . import _lib
 
-    sh = gen.index.shard
+    sh = getattr(gen.index, "shard", None) or gen.index.partition
     dev = gen.index.catalog.device
     L = _lib.lib()
     n, r = batch.n_chunks, batch.n_ranges
@@ -309,3 +309,155 @@ def merge_batch(gen, batch, stream=None):
     _lib.check(L.mx_chunks_merge(sh.world, n, cap, offs.data_ptr(), *(g4[f].data_ptr() for f in range(4)),
                                  out_off.data_ptr(), *(out[f].data_ptr() for f in range(4)), sp))
     return MergedChunkBatch(batch, out_off, out[:, :total], sh.file_ds, sh.file_ids)
+
+
+# ---------------------------------------------------------------------------
+# Key-partitioned path (SURVEY.md §8(e), strong scaling): no rank holds the
+# global block table. Every global key is OWNED by one rank (its rank in the
+# sorted key union, round robin); the owner alone lays out that key's cursor
+# stream over the key's files of the whole catalog and hands every file owner
+# the offsets of its (key, file) blocks. Every rank plans on the key-level
+# index (global per-key totals: all the planner reads, chunks.py:188-259) and
+# cuts only its own intervals (csrc/stage2.cu emit_local); the per-rank chunk
+# CSRs are interleaved as in the file-sharded path (mx_chunks_merge).
+# ---------------------------------------------------------------------------
+U32_SPLIT = 1 << 31  # pseudo-interval length cap of the key-level index (u32 interval ends)
+
+
+class PartitionInfo(ShardInfo):
+    def __init__(self, world, rank, group, file_lo, file_hi, file_ds, file_ids, local, rows, key_g, key_g_rows):
+        super().__init__(world, rank, group, file_lo, file_hi, file_ds, file_ids)
+        self.local = local            # this rank's ChunkerIndex (local file indices)
+        self.rows = rows              # device int32 [B, 4] local block rows (global file indices)
+        self.key_g = key_g            # device int32 [n_local_keys]: global key rank
+        self.key_g_rows = key_g_rows  # device int64 [B]: global key rank of every block row
+
+
+def _all_to_all_rows(send, splits, group):
+    """Variable all-to-all of the rows of ``send`` (rows grouped by
+    destination, ``splits`` host list). Returns (received rows on send's
+    device, per-source counts)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    cdev = _coll_device(group, send.device)
+    n_out = torch.tensor(splits, dtype=torch.int64, device=cdev)
+    n_in = torch.empty(world, dtype=torch.int64, device=cdev)
+    dist.all_to_all_single(n_in, n_out, group=group)
+    in_splits = [int(x) for x in n_in.tolist()]
+    recv = torch.empty((sum(in_splits), *send.shape[1:]), dtype=send.dtype, device=cdev)
+    dist.all_to_all_single(recv, send.to(cdev), in_splits, list(splits), group=group)
+    return recv.to(send.device), in_splits
+
+
+def build_partitioned_index(local_catalog, predicates=(), file_lo: int = 0, file_ds=None, file_ids=None,
+                            group=None, stream=None):
+    """Collective: the key-level ChunkerIndex every rank plans on (global
+    keys and per-key totals, the global file table), with ``.partition``
+    describing this rank's files. Exchange: one all-gather of (packed key,
+    samples) per key. The block offsets are exchanged per generator seed
+    (``attach_partition``, called by ChunkGenerator)."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+    from .index import ChunkerIndex, build_index_from_catalog
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    codec = local_catalog.codec
+    layout = np.array([codec.key_bits, *codec.shift, *codec.width], dtype=np.int64)
+    lay, _ = all_gather_rows(torch.from_numpy(layout).view(1, -1), group)
+    if not bool((lay == lay[0]).all()):
+        raise ValueError("ranks disagree on the packed-key layout: build every shard's DeviceCatalog with the "
+                         "same vocabulary and parallel.global_nullable() flags")
+    local = build_index_from_catalog(local_catalog, predicates, stream=stream)
+    L = _lib.lib()
+    dev = local_catalog.device
+    packed, samples = local.packed_keys()
+    kt = torch.from_numpy(np.stack([packed.astype(np.int64), samples], axis=1))
+    allk, counts = all_gather_rows(kt, group)
+    cat = np.concatenate([allk[q, : counts[q]].numpy() for q in range(world)]) if sum(counts) else \
+        np.zeros((0, 2), np.int64)
+    gkeys, inv = np.unique(cat[:, 0], return_inverse=True)
+    totals = np.zeros(len(gkeys), np.int64)
+    np.add.at(totals, inv, cat[:, 1])
+    file_ds = np.ascontiguousarray(file_ds, dtype=np.int32)
+    file_ids = np.ascontiguousarray(file_ids, dtype=np.int64)
+    n_files = len(file_ids)
+    # key-level rows (packed key, pseudo file, samples): totals above 2^31 split
+    pieces = np.maximum(1, -(-totals // U32_SPLIT))
+    if int(pieces.max(initial=1)) > n_files:
+        raise ValueError("a key holds more than n_files * 2^31 samples")
+    rk = np.repeat(np.arange(len(gkeys)), pieces)
+    sub = np.arange(len(rk)) - np.repeat(np.cumsum(pieces) - pieces, pieces)
+    size = np.minimum(totals[rk] - sub * U32_SPLIT, U32_SPLIT)
+    krows = np.zeros((len(rk), 4), np.uint32)
+    krows[:, 0] = gkeys[rk].astype(np.uint32)
+    krows[:, 1] = sub
+    krows[:, 2] = size
+    krows[:, 3] = 1
+    d_krows = torch.from_numpy(krows.view(np.int32)).to(dev)
+    sp = C.c_void_p(_lib.stream_ptr(stream))
+    out = C.c_void_p()
+    _lib.check(L.mx_index_build_owner(local.handle, d_krows.data_ptr(), len(krows), n_files, _lib.ptr(file_ds),
+                                      _lib.ptr(file_ids), sp, C.byref(out)))
+    idx = ChunkerIndex(out.value, local_catalog, stream)
+    d_gkeys = torch.from_numpy(gkeys).to(dev)
+    key_g = torch.searchsorted(d_gkeys, torch.from_numpy(packed.astype(np.int64)).to(dev)).to(torch.int32)
+    rows = torch.empty((max(local.n_blocks, 1), 4), dtype=torch.int32, device=dev)
+    if local.n_blocks:
+        _lib.check(L.mx_index_block_table(local.handle, int(file_lo), rows.data_ptr(), sp))
+    rows = rows[: local.n_blocks]
+    key_g_rows = torch.searchsorted(d_gkeys, rows[:, 0].to(torch.int64) & 0xFFFFFFFF)
+    idx.partition = PartitionInfo(world, rank, group, int(file_lo), int(file_lo) + local_catalog.host.n_files,
+                                  file_ds, file_ids, local, rows, key_g, key_g_rows)
+    return idx
+
+
+def attach_partition(gen):
+    """Collective (ChunkGenerator on a partitioned index): send every block
+    row to its key's owner, let the owners lay out their keys' cursor streams
+    (generator seed = gen.seed) and return the block offsets, then point the
+    generator's emission at this rank's intervals."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from .seeding import derive_seed, hash_message
+
+    pi = gen.index.partition
+    L = _lib.lib()
+    dev = gen.index.catalog.device
+    sp = C.c_void_p(_lib.stream_ptr(gen.stream))
+    owner = pi.key_g_rows % pi.world
+    perm = torch.argsort(owner, stable=True)
+    splits = torch.bincount(owner, minlength=pi.world).tolist() if len(owner) else [0] * pi.world
+    recv, in_splits = _all_to_all_rows(pi.rows[perm].contiguous(), splits, pi.group)
+    n = int(recv.shape[0])
+    oix = C.c_void_p()
+    _lib.check(L.mx_index_build_owner(pi.local.handle, recv.data_ptr() if n else None, n, len(pi.file_ids),
+                                      _lib.ptr(pi.file_ds), _lib.ptr(pi.file_ids), sp, C.byref(oix)))
+    off = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
+    og = C.c_void_p()
+    try:
+        cur = hash_message(gen.seed, "cursor")
+        chk = hash_message(gen.seed, "chunk")
+        _lib.check(L.mx_gen_create(oix, cur, len(cur), chk, len(chk), derive_seed(gen.seed, "component-order"), sp,
+                                   C.byref(og)))
+        try:
+            if n:
+                _lib.check(L.mx_gen_block_offsets(og, off.data_ptr(), sp))
+        finally:
+            L.mx_gen_free(og)
+    finally:
+        L.mx_index_free(oix)
+    back, _ = _all_to_all_rows(off[:n], in_splits, pi.group)
+    blk_off = torch.empty_like(back)
+    blk_off[perm] = back
+    gen._partition_bufs = (blk_off, pi.key_g)
+    _lib.check(L.mx_gen_set_local(gen._h, pi.local.handle, blk_off.data_ptr() if len(blk_off) else None,
+                                  pi.key_g.data_ptr() if len(pi.key_g) else None, pi.file_lo))

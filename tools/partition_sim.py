@@ -1,0 +1,196 @@
+"""Per-rank device cost of the KEY-PARTITIONED pipeline at N ranks, on ONE GPU.
+
+Builds the N ranks' local indexes (bench workload; --scale 1 = 100M samples
+per rank), then replays, with CUDA events: the replicated key-level index
+(parallel.build_partitioned_index), every key OWNER's block layout (owner
+index + generator + block offsets over the rows all ranks send it), every
+rank's plan + local emission (csrc/stage2.cu emit_local), and the root merge.
+Collectives are replaced by in-memory concatenation; their bytes are printed
+so the NVLink cost can be estimated. Usage:
+python tools/partition_sim.py --world 8 --scale 1.25   (1B samples total)
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import bench  # noqa: E402
+from paper_2502_19790_b200 import ChunkGenerator, _lib, build_index_from_catalog, synth  # noqa: E402
+from paper_2502_19790_b200.catalog import ColumnarCatalog  # noqa: E402
+from paper_2502_19790_b200.index import ChunkerIndex  # noqa: E402
+from paper_2502_19790_b200.parallel import U32_SPLIT  # noqa: E402
+from paper_2502_19790_b200.seeding import derive_seed, hash_message  # noqa: E402
+
+
+def timed(fn):
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    out = fn()
+    b.record()
+    torch.cuda.synchronize()
+    return out, a.elapsed_time(b)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--world", type=int, default=8)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    W = args.world
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    L = _lib.lib()
+    sp = C.c_void_p(_lib.stream_ptr())
+    spec = synth.cfg2_mixture(bench.CFG["chunk_size"])
+    seed = bench.CFG["job_seed"]
+    locs = []
+    for q in range(W):
+        rt = bench.make_workload(q, args.scale)
+        meta = ColumnarCatalog.meta_only(rt.vocab, rt.file_sizes)
+        codes, table = bench.run_level_tuples(rt, dev)
+        dcat = bench.device_catalog(meta, {"tuples": codes}, table)
+        idx, ms = timed(lambda: build_index_from_catalog(dcat, []))
+        nf = len(rt.file_sizes)
+        packed, samples = idx.packed_keys()
+        rows = torch.empty((max(idx.n_blocks, 1), 4), dtype=torch.int32, device=dev)
+        _lib.check(L.mx_index_block_table(idx.handle, q * nf, rows.data_ptr(), sp))
+        dcat.tuple_codes = dcat.tuple_codes[:0]
+        del codes
+        locs.append(dict(idx=idx, dcat=dcat, rows=rows[: idx.n_blocks], packed=packed, samples=samples, nf=nf,
+                         stage1_ms=ms, n_samples=rt.n_samples))
+        torch.cuda.empty_cache()
+    nf = locs[0]["nf"]
+    F = W * nf
+    file_ds, file_ids = np.zeros(F, np.int32), np.arange(1, F + 1, dtype=np.int64)
+    # ---- replicated key-level index (host part: union of the gathered key lists)
+    cat = np.concatenate([np.stack([x["packed"].astype(np.int64), x["samples"]], 1) for x in locs])
+    t0 = time.perf_counter()
+    gkeys, inv = np.unique(cat[:, 0], return_inverse=True)
+    totals = np.zeros(len(gkeys), np.int64)
+    np.add.at(totals, inv, cat[:, 1])
+    pieces = np.maximum(1, -(-totals // U32_SPLIT))
+    rk = np.repeat(np.arange(len(gkeys)), pieces)
+    sub = np.arange(len(rk)) - np.repeat(np.cumsum(pieces) - pieces, pieces)
+    krows = np.zeros((len(rk), 4), np.uint32)
+    krows[:, 0], krows[:, 1] = gkeys[rk].astype(np.uint32), sub
+    krows[:, 2], krows[:, 3] = np.minimum(totals[rk] - sub * U32_SPLIT, U32_SPLIT), 1
+    host_keys_ms = (time.perf_counter() - t0) * 1e3
+    d_krows = torch.from_numpy(krows.view(np.int32)).to(dev)
+    d_gkeys = torch.from_numpy(gkeys).to(dev)
+
+    def key_index():
+        out = C.c_void_p()
+        _lib.check(L.mx_index_build_owner(locs[0]["idx"].handle, d_krows.data_ptr(), len(krows), F,
+                                          _lib.ptr(file_ds), _lib.ptr(file_ids), sp, C.byref(out)))
+        return ChunkerIndex(out.value, locs[0]["dcat"])
+
+    # ---- owner work: rows sent to owner o = rows whose key rank % W == o
+    for x in locs:
+        x["kg_rows"] = torch.searchsorted(d_gkeys, x["rows"][:, 0].to(torch.int64) & 0xFFFFFFFF)
+        x["key_g"] = torch.searchsorted(d_gkeys, torch.from_numpy(x["packed"].astype(np.int64)).to(dev)).to(
+            torch.int32)
+    recv = []
+    for o in range(W):
+        parts = [x["rows"][x["kg_rows"] % W == o] for x in locs]
+        recv.append((torch.cat(parts).contiguous(), [len(p) for p in parts]))
+    cur, chk = hash_message(seed, "cursor"), hash_message(seed, "chunk")
+    oseed = derive_seed(seed, "component-order")
+
+    def owner(o):
+        rows, _ = recv[o]
+        n = len(rows)
+        oix, og = C.c_void_p(), C.c_void_p()
+        off = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        _lib.check(L.mx_index_build_owner(locs[0]["idx"].handle, rows.data_ptr(), n, F, _lib.ptr(file_ds),
+                                          _lib.ptr(file_ids), sp, C.byref(oix)))
+        _lib.check(L.mx_gen_create(oix, cur, len(cur), chk, len(chk), oseed, sp, C.byref(og)))
+        _lib.check(L.mx_gen_block_offsets(og, off.data_ptr(), sp))
+        L.mx_gen_free(og)
+        L.mx_index_free(oix)
+        return off[:n]
+
+    offs = [owner(o) for o in range(W)]  # warm
+    own_ms = []
+    for o in range(W):
+        best = min(timed(lambda: owner(o))[1] for _ in range(args.reps))
+        own_ms.append(round(best, 3))
+    # offsets back to the file owners
+    for q, x in enumerate(locs):
+        perm = torch.argsort(x["kg_rows"] % W, stable=True)
+        back = []
+        for o in range(W):
+            lo = sum(recv[o][1][:q])
+            back.append(offs[o][lo: lo + recv[o][1][q]])
+        blk = torch.empty(len(perm), dtype=torch.int64, device=dev)
+        blk[perm] = torch.cat(back)
+        x["blk_off"] = blk
+
+    # ---- per rank: key-level index + generator + plan + local emission
+    def rank_job(x):
+        kix = key_index()
+        gen = ChunkGenerator(kix, seed)
+        _lib.check(L.mx_gen_set_local(gen._h, x["idx"].handle, x["blk_off"].data_ptr(), x["key_g"].data_ptr(),
+                                      locs.index(x) * nf))
+        batch = gen.plan_batch(spec, 1 << 40)
+        return kix, gen, batch
+
+    rank_job(locs[0])
+    results, rank_ms = [], []
+    for q, x in enumerate(locs):
+        best = None
+        for _ in range(args.reps):
+            (kix, gen, batch), t = timed(lambda: rank_job(x))
+            best = t if best is None else min(best, t)
+        n, rr = batch.n_chunks, batch.n_ranges
+        off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        cols4 = torch.empty((4, max(rr, 1)), dtype=torch.int32, device=dev)
+        _lib.check(L.mx_gen_result_export(gen._h, off.data_ptr(), *(cols4[f].data_ptr() for f in range(4)), sp))
+        results.append((off, cols4[:, :rr], rr))
+        rank_ms.append(round(best, 3))
+        del kix, gen, batch
+    # ---- root merge
+    n = results[0][0].numel() - 1
+    capr = max(max(x[2] for x in results), 1)
+    o_all = torch.stack([x[0] for x in results]).contiguous()
+    g4 = torch.zeros((4, W, capr), dtype=torch.int32, device=dev)
+    for q, (_, c4, rr) in enumerate(results):
+        g4[:, q, :rr] = c4
+    total = sum(x[2] for x in results)
+    out_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    out = torch.empty((4, max(total, 1)), dtype=torch.int32, device=dev)
+
+    def merge():
+        _lib.check(L.mx_chunks_merge(W, n, capr, o_all.data_ptr(), *(g4[f].data_ptr() for f in range(4)),
+                                     out_off.data_ptr(), *(out[f].data_ptr() for f in range(4)), sp))
+
+    merge()
+    _, t_m = timed(merge)
+    rows_total = sum(len(x["rows"]) for x in locs)
+    stage1 = [round(x["stage1_ms"], 3) for x in locs]
+    report = {
+        "world": W, "samples_per_rank": int(locs[0]["n_samples"]), "global_keys": int(len(gkeys)),
+        "stage1_ms": stage1, "host_key_union_ms": round(host_keys_ms, 3),
+        "owner_ms": own_ms, "rank_plan_emit_ms": rank_ms, "merge_ms": round(t_m, 3),
+        "global_chunks": int(n), "global_pieces": int(total),
+        "bytes": {"keys_allgather": int(W * len(cat) * 16), "rows_alltoall": int(rows_total * 16),
+                  "offsets_alltoall": int(rows_total * 8), "pieces_allgather": int(W * capr * 16)},
+        "device_step_ms_est": round(max(stage1) + max(own_ms) + max(rank_ms) + t_m, 3),
+    }
+    print(json.dumps(report))
+
+
+if __name__ == "__main__":
+    main()
