@@ -282,9 +282,14 @@ int mx_chunks_merge(int32_t world, int64_t n_chunks, int64_t cap, const int64_t*
  * gives each block's offset in its key's cursor stream (device uint64[n_rows],
  * in the order of the rows given to mx_index_build_owner). The same call on
  * rows (packed key, 0, total samples) gives the key-level index every rank
- * plans on (global per-key totals; chunks.py:188-259 only needs those). */
+ * plans on (global per-key totals; chunks.py:188-259 only needs those).
+ * dense_key_bits > 0: the rows are already file-ordered within each key
+ * (every source's (key, file)-sorted rows concatenated in rank order) and
+ * row[3] holds a dense key rank increasing with the packed key, < 2^bits:
+ * one stable sort pass per 8 bits instead of a (file, key) sort. */
 int mx_index_build_owner(const mx_index* like, const uint32_t* rows, int64_t n_rows, int32_t n_files,
-                         const int32_t* file_ds, const int64_t* file_ids, void* stream, mx_index** out);
+                         const int32_t* file_ds, const int64_t* file_ids, int32_t dense_key_bits, void* stream,
+                         mx_index** out);
 int mx_gen_block_offsets(mx_gen* gen, uint64_t* offsets, void* stream);
 /* Plans of `gen` (on a key-level index) then emit only `local`'s pieces:
  * block b of local key k is the key's cursor stream at blk_off[b] (device
@@ -294,6 +299,21 @@ int mx_gen_block_offsets(mx_gen* gen, uint64_t* offsets, void* stream);
  * MX_ERR_UNSUPPORTED); pass local == NULL to detach. */
 int mx_gen_set_local(mx_gen* gen, const mx_index* local, const uint64_t* blk_off, const uint32_t* key_g,
                      int64_t file_lo);
+/* Chunk-owner output (no rank gathers every piece). With
+ * handoff on, a plan of a partitioned generator stops after the cut: its
+ * pieces, grouped by global chunk, stay in the generator (mx_gen_handoff:
+ * device offsets int64[n_chunks + 1], pieces uint32[n_pieces][4] = (mixture
+ * key, global file index, start, end)). The caller sends each chunk owner the
+ * pieces of its chunks (one all-to-all; rank r owns a contiguous chunk range)
+ * with their per-chunk counts, and the owner finishes ITS chunks:
+ * counts device int32[world][n_own], pieces device uint32[n_pieces][4]
+ * source-major then chunk-major. The result (mx_gen_result_*) then holds the
+ * owned chunks (ids chunk_lo..), normalised as the single-GPU path does. */
+int mx_gen_set_handoff(mx_gen* gen, int32_t on);
+int mx_gen_handoff(const mx_gen* gen, int64_t* n_chunks, int64_t* n_pieces, const int64_t** chunk_offsets,
+                   const uint32_t** pieces);
+int mx_gen_finish_owned(mx_gen* gen, int32_t world, int64_t chunk_lo, int64_t n_own, int64_t n_global,
+                        const int32_t* counts, const uint32_t* pieces, int64_t n_pieces, void* stream);
 
 /* ------------------------------------------------------------ registration
  * Metadata registration from JSON-lines bytes in HBM [MetadataCatalog.

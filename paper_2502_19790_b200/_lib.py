@@ -160,9 +160,12 @@ _SIGS = {
     "mx_index_build_sharded": (C.c_int, [vp, P(ShardDesc), vp, P(vp)]),
     "mx_gen_cursor_to_consumed": (C.c_int, [vp, vp, vp, vp]),
     "mx_gen_set_consumed": (C.c_int, [vp, vp]),
-    "mx_index_build_owner": (C.c_int, [vp, vp, i64, i32, vp, vp, vp, P(vp)]),
+    "mx_index_build_owner": (C.c_int, [vp, vp, i64, i32, vp, vp, i32, vp, P(vp)]),
     "mx_gen_block_offsets": (C.c_int, [vp, vp, vp]),
     "mx_gen_set_local": (C.c_int, [vp, vp, vp, vp, i64]),
+    "mx_gen_set_handoff": (C.c_int, [vp, i32]),
+    "mx_gen_handoff": (C.c_int, [vp, P(i64), P(i64), P(vp), P(vp)]),
+    "mx_gen_finish_owned": (C.c_int, [vp, i32, i64, i64, i64, vp, vp, i64, vp]),
     "mx_chunks_merge": (C.c_int, [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "mx_domain_loss": (C.c_int, [vp, vp, i64, i32, vp, vp, vp]),
     "mx_fit_power_law": (C.c_int, [i32, vp, vp, vp, vp, vp, vp]),

@@ -632,7 +632,8 @@ int mx_index_build_sharded(const mx_index* local, const mx_shard_desc* desc, voi
 }
 
 int mx_index_build_owner(const mx_index* like, const uint32_t* rows, int64_t n_rows, int32_t n_files,
-                         const int32_t* file_ds, const int64_t* file_ids, void* stream, mx_index** out) {
+                         const int32_t* file_ds, const int64_t* file_ids, int32_t dense_key_bits, void* stream,
+                         mx_index** out) {
   if (like)
     if (int rc = ix_resolve(const_cast<IndexData*>(&like->d))) return rc;
   MX_CHECK_ARG(like && out && (rows || n_rows == 0), "null argument");
@@ -641,7 +642,9 @@ int mx_index_build_owner(const mx_index* like, const uint32_t* rows, int64_t n_r
   g_err.clear();
   keep_pool_warm();
   mx_index* ix = new mx_index();
-  int rc = owner_index_build(&like->d, rows, n_rows, n_files, file_ds, file_ids, (cudaStream_t)stream, &ix->d);
+  MX_CHECK_ARG(dense_key_bits >= 0 && dense_key_bits <= 32, "bad dense key bits");
+  int rc = owner_index_build(&like->d, rows, n_rows, n_files, file_ds, file_ids, dense_key_bits, (cudaStream_t)stream,
+                             &ix->d);
   if (rc < 0) {
     delete ix;
     return rc;
@@ -678,6 +681,39 @@ int mx_gen_set_local(mx_gen* gen, const mx_index* local, const uint64_t* blk_off
   MX_CHECK_ARG(file_lo >= 0 && file_lo + local->d.n_files <= gen->d.ix->n_files, "local files outside the file table");
   gen->d.local = LocalSrc{&local->d, reinterpret_cast<const u64*>(blk_off), key_g, (long long)file_lo};
   return MX_OK;
+}
+
+int mx_gen_set_handoff(mx_gen* gen, int32_t on) {
+  MX_CHECK_ARG(gen, "null argument");
+  MX_CHECK_ARG(!on || gen->d.local.loc, "handoff needs a partitioned generator (mx_gen_set_local)");
+  g_err.clear();
+  gen->d.local.handoff = on != 0;
+  gen->d.handoff.n_chunks = -1;
+  return MX_OK;
+}
+
+int mx_gen_handoff(const mx_gen* gen, int64_t* n_chunks, int64_t* n_pieces, const int64_t** chunk_offsets,
+                   const uint32_t** pieces) {
+  MX_CHECK_ARG(gen && n_chunks && n_pieces && chunk_offsets && pieces, "null argument");
+  const Handoff& h = gen->d.handoff;
+  if (h.n_chunks < 0) return mx_fail(MX_ERR_INVALID, "no partitioned plan pending");
+  long long np = 0;
+  cudaError_t e = cudaMemcpy(&np, h.off.p + h.n_chunks, sizeof(long long), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return mx_fail_cuda(e, "handoff size", __FILE__, __LINE__);
+  *n_chunks = h.n_chunks;
+  *n_pieces = np;
+  *chunk_offsets = reinterpret_cast<const int64_t*>(h.off.p);
+  *pieces = reinterpret_cast<const uint32_t*>(h.pieces.p);
+  return MX_OK;
+}
+
+int mx_gen_finish_owned(mx_gen* gen, int32_t world, int64_t chunk_lo, int64_t n_own, int64_t n_global,
+                        const int32_t* counts, const uint32_t* pieces, int64_t n_pieces, void* stream) {
+  MX_CHECK_ARG(gen && world >= 1 && n_own >= 0 && n_pieces >= 0, "bad argument");
+  MX_CHECK_ARG((counts || n_own == 0) && (pieces || n_pieces == 0), "null counts / pieces");
+  g_err.clear();
+  return gen_finish_owned(&gen->d, world, chunk_lo, n_own, n_global, counts, reinterpret_cast<const uint4*>(pieces),
+                          n_pieces, (cudaStream_t)stream);
 }
 
 int mx_chunks_merge(int32_t world, int64_t n_chunks, int64_t cap, const int64_t* offs, const uint32_t* mkey,

@@ -85,6 +85,10 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
   for (long long k = blockIdx.x * (long long)wpc + w; k < K; k += (long long)gridDim.x * wpc) {
     const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
     const int nb = (int)(b1 - b0);
+    if (nb <= 1) {  // shuffling one block draws nothing: skip the MT seeding
+      if (lane == 0 && nb == 1) cur_blk[b0] = b0;
+      continue;
+    }
     const bool in_smem = nb <= list_cap;
     // dataset groups (blocks are file-sorted and ds is nondecreasing in file
     // order): one group when first and last block share a dataset, else a

@@ -160,6 +160,16 @@ struct LocalSrc {
   const u64* blk_off = nullptr;    // device [loc->n_blocks]: block offset in its key's global cursor stream
   const u32* key_g = nullptr;      // device [loc->n_keys]: global component rank of each local key
   long long file_lo = 0;           // global index of local file 0
+  bool handoff = false;            // stop after the cut: chunk-grouped pieces for the chunk owners (handoff)
+};
+
+// Cut pieces of a partitioned plan, grouped by chunk, before the exchange to
+// the chunk owners (mx_gen_handoff / mx_gen_finish_owned).
+struct Handoff {
+  DevBuf<long long> off;   // [n_chunks + 1] piece offsets per chunk
+  DevBuf<uint4> pieces;    // (mixture key, global file, start, end)
+  long long n_chunks = -1; // -1: none pending
+  long long first_id = 0;  // chunk id of global chunk 0 of the plan
 };
 
 struct GenData {
@@ -228,6 +238,7 @@ struct GenData {
   cudaEvent_t ev_plan = nullptr, ev_seg = nullptr, ev_seed_fork = nullptr, ev_seed = nullptr;
   bool fresh_layout = false;  // no work on `stream` since cursor_build except the layout itself
   LocalSrc local;             // set: plans emit this rank's pieces of the global chunks (emit_local)
+  Handoff handoff;
   int aux_dev = -1;
   cudaError_t aux_init() {  // streams shared per device, events pooled (capi.cu)
     if (ostream) return cudaSuccess;
@@ -266,8 +277,10 @@ int index_build_sharded(const IndexData* loc, const mx_shard_desc* d, cudaStream
 int gen_local_lists(GenData* g, cudaStream_t s);
 int gen_host_mirrors(GenData* g);
 int gen_block_offsets(GenData* g, u64* out, cudaStream_t s);
+int gen_finish_owned(GenData* g, int world, long long chunk_lo, long long n_own, long long n_global,
+                     const int32_t* counts, const uint4* pieces, long long n_pieces, cudaStream_t s);
 int owner_index_build(const IndexData* src, const u32* rows, long long n, int n_files, const int32_t* file_ds,
-                      const int64_t* file_ids, cudaStream_t s, IndexData* out);
+                      const int64_t* file_ids, int dense_bits, cudaStream_t s, IndexData* out);
 int excl_scan_ll(const u64* in, long long n, long long* out, cudaStream_t s);
 int gen_result_json(GenData* g, const mx_json_desc* d, cudaStream_t s);
 int chunks_merge(int W, long long C, long long cap, const long long* offs, const u32* mkey, const u32* file,

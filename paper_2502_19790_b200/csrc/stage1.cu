@@ -902,18 +902,24 @@ int rows_build(const mx_rows_desc* d, cudaStream_t s, IndexData* out) {
 // generator's RangeCursor shuffles are the reference's over the key's files
 // of the WHOLE catalog (index.py:134-144), and its cursor prefix sums give
 // every block's offset in its key's cursor stream.
-__global__ void owner_rows_kernel(long long n, const uint4* rows, u32* key, u32* file, u32* start, u32* end) {
+__global__ void owner_rows_kernel(long long n, const uint4* rows, int dense, u32* key, u32* file, u32* start,
+                                  u32* end) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint4 r = rows[i];
-  key[i] = r.x;
+  key[i] = dense ? r.w : r.x;
   file[i] = r.y;
   start[i] = (u32)i;  // row id through the sort (owner_row); the pseudo-interval starts at 0
   end[i] = r.z;
 }
 
+__global__ void owner_keys_kernel(long long n, const uint4* rows, const u32* row, u32* key) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) key[i] = rows[row[i]].x;
+}
+
 int owner_index_build(const IndexData* src, const u32* rows, long long n, int n_files, const int32_t* file_ds,
-                      const int64_t* file_ids, cudaStream_t s, IndexData* out) {
+                      const int64_t* file_ids, int dense_bits, cudaStream_t s, IndexData* out) {
   IndexData& ix = *out;
   ix.stream = s;
   ix.n_files = n_files;
@@ -946,8 +952,8 @@ int owner_index_build(const IndexData* src, const u32* rows, long long n, int n_
     MX_CUDA_TRY(a[j].alloc(n, s));
     MX_CUDA_TRY(b[j].alloc(n, s));
   }
-  owner_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, reinterpret_cast<const uint4*>(rows), a[0].p,
-                                                               a[1].p, a[2].p, a[3].p);
+  owner_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, reinterpret_cast<const uint4*>(rows),
+                                                               dense_bits > 0, a[0].p, a[1].p, a[2].p, a[3].p);
   mx_count_launch();
   const int tiles = (int)((n + RS_THREADS * 8 - 1) / (RS_THREADS * 8));
   MX_CUDA_TRY(hist.alloc((long long)256 * tiles, s));
@@ -956,10 +962,19 @@ int owner_index_build(const IndexData* src, const u32* rows, long long n, int n_
                                    (int)(4 * RS_THREADS * 8 * sizeof(u32))));
   u32 *k = a[0].p, *f = a[1].p, *st = a[2].p, *en = a[3].p;
   u32 *k2 = b[0].p, *f2 = b[1].p, *st2 = b[2].p, *en2 = b[3].p;
-  if (int rc = radix_sort_by(f, k, st, en, f2, k2, st2, en2, n, bits_of((u32)std::max(0, n_files - 1)), hist.p,
-                             dtot.p, s))
-    return rc;
-  if (int rc = radix_sort_by(k, f, st, en, k2, f2, st2, en2, n, (int)ix.key_bits, hist.p, dtot.p, s)) return rc;
+  if (dense_bits > 0) {
+    // rows file-ordered within each key (sources concatenated in rank order)
+    // with a dense key rank in .w: one stable sort by that rank, then the
+    // packed keys gathered back through the row ids
+    if (int rc = radix_sort_by(k, f, st, en, k2, f2, st2, en2, n, dense_bits, hist.p, dtot.p, s)) return rc;
+    owner_keys_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, reinterpret_cast<const uint4*>(rows), st, k);
+    mx_count_launch();
+  } else {
+    if (int rc = radix_sort_by(f, k, st, en, f2, k2, st2, en2, n, bits_of((u32)std::max(0, n_files - 1)), hist.p,
+                               dtot.p, s))
+      return rc;
+    if (int rc = radix_sort_by(k, f, st, en, k2, f2, st2, en2, n, (int)ix.key_bits, hist.p, dtot.p, s)) return rc;
+  }
   MX_CUDA_TRY(ix.iv_key.alloc(n, s));
   MX_CUDA_TRY(ix.iv_file.alloc(n, s));
   MX_CUDA_TRY(ix.iv_start.alloc(n, s));

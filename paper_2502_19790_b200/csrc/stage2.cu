@@ -2542,6 +2542,11 @@ __global__ void local_cut_kernel(LocalCut a, u64* cnt, const u64* off, u32* pc, 
 }
 
 // pieces -> chunk CSR (order inside a chunk is settled by the normalisation)
+__global__ void widen_kernel(long long n, const int32_t* in, u64* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (u64)in[i];
+}
+
 __global__ void chunk_hist_kernel(long long n, const u32* pc, u64* cc) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) atomicAdd(reinterpret_cast<unsigned long long*>(cc + pc[i]), 1ull);
@@ -2560,6 +2565,106 @@ __global__ void chunk_scatter_kernel(long long n, const u32* pc, const u32* pm, 
   qe[q] = pe[i];
 }
 
+__global__ void chunk_scatter_aos_kernel(long long n, const u32* pc, const u32* pm, const u32* pf, const u32* ps,
+                                         const u32* pe, const u64* cpo, unsigned long long* fill, uint4* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u32 c = pc[i];
+  out[cpo[c] + atomicAdd(fill + c, 1ull)] = make_uint4(pm[i], pf[i], ps[i], pe[i]);
+}
+
+// Chunk owner: the pieces of its chunks [chunk_lo, chunk_lo + n_own) from
+// every rank (received source-major, chunk-major inside a source; counts
+// [world][n_own]) into one chunk CSR, then the normal per-chunk
+// normalisation. Pieces of one chunk never merge across ranks (a file lives
+// on one rank), so the result equals the single-GPU chunk.
+__global__ void owned_totals_kernel(int world, long long n_own, const int32_t* counts, u64* tot) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= n_own) return;
+  u64 t = 0;
+  for (int q = 0; q < world; ++q) t += (u64)counts[(long long)q * n_own + c];
+  tot[c] = t;
+}
+
+__global__ void owned_gather_kernel(int world, long long n_own, const int32_t* counts, const u64* src_off,
+                                    const u64* cpo, const uint4* in, u32* pm, u32* pf, u32* ps, u32* pe) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= n_own) return;
+  u64 d = cpo[c];
+  for (int q = 0; q < world; ++q) {
+    const long long qc = (long long)q * n_own + c;
+    const u64 so = src_off[qc];
+    for (int32_t i = 0; i < counts[qc]; ++i, ++d) {
+      const uint4 r = in[so + i];
+      pm[d] = r.x;
+      pf[d] = r.y;
+      ps[d] = r.z;
+      pe[d] = r.w;
+    }
+  }
+}
+
+int gen_finish_owned(GenData* g, int world, long long chunk_lo, long long n_own, long long n_global,
+                     const int32_t* counts, const uint4* pieces, long long n_pieces, cudaStream_t s) {
+  if (g->handoff.n_chunks < 0) return mx_fail(MX_ERR_INVALID, "no partitioned plan pending (mx_gen_handoff)");
+  if (n_global != g->handoff.n_chunks || chunk_lo < 0 || n_own < 0 || chunk_lo + n_own > n_global)
+    return mx_fail(MX_ERR_INVALID, "owned chunk range outside the pending plan");
+  const long long base_id = g->handoff.first_id;
+  g->handoff.n_chunks = -1;
+  MxPhase ph("emit", s);
+  g->h_small_valid = 0;
+  g->res_chunks = n_own;
+  g->res_ranges = 0;
+  MX_CUDA_TRY(g->res_off.reserve(n_own + 1, s));
+  MX_CUDA_TRY(g->res_seed.reserve(n_own > 0 ? n_own : 1, s));
+  MX_CUDA_TRY(g->res_id.reserve(n_own > 0 ? n_own : 1, s));
+  MX_CUDA_TRY(g->aux_init());
+  if (n_own == 0) {
+    const long long z = 0;
+    MX_CUDA_TRY(mx_h2d(g->res_off.p, &z, sizeof(z), s));
+    MX_CUDA_TRY(cudaStreamSynchronize(s));
+    g->next_chunk_id = base_id + n_global;
+    return MX_OK;
+  }
+  // chunk seeds of the owned ids on the side stream
+  MX_CUDA_TRY(cudaEventRecord(g->ev_seed_fork, s));
+  MX_CUDA_TRY(cudaStreamWaitEvent(g->sstream, g->ev_seed_fork, 0));
+  chunk_seed_kernel<<<(unsigned)((n_own + 127) / 128), 128, 0, g->sstream>>>(
+      n_own, base_id + chunk_lo, g->chunk_prefix.p, g->chunk_prefix_len, g->res_seed.p, g->res_id.p);
+  mx_count_launch();
+  MX_CUDA_TRY(cudaEventRecord(g->ev_seed, g->sstream));
+  const long long cap = n_pieces + 1;
+  DevBuf<u64> tot, cpo, mcnt, src_off;
+  DevBuf<u32> big, pm, pf, ps, pe;
+  MX_CUDA_TRY(tot.alloc(n_own, s));
+  MX_CUDA_TRY(cpo.alloc(n_own + 1, s));
+  MX_CUDA_TRY(mcnt.alloc(n_own, s));
+  MX_CUDA_TRY(src_off.alloc((long long)world * n_own + 1, s));
+  MX_CUDA_TRY(big.alloc(1, s));
+  MX_CUDA_TRY(cudaMemsetAsync(big.p, 0, sizeof(u32), s));
+  for (DevBuf<u32>* x : {&pm, &pf, &ps, &pe}) MX_CUDA_TRY(x->alloc(cap, s));
+  const unsigned gb = (unsigned)((n_own + 255) / 256);
+  owned_totals_kernel<<<gb, 256, 0, s>>>(world, n_own, counts, tot.p);
+  mx_count_launch();
+  if (int rc = excl_scan<u64>(tot.p, n_own, cpo.p, s)) return rc;
+  DevBuf<u64> cnt64;  // counts widened for the source-offset scan
+  MX_CUDA_TRY(cnt64.alloc((long long)world * n_own, s));
+  widen_kernel<<<(unsigned)(((long long)world * n_own + 255) / 256), 256, 0, s>>>((long long)world * n_own, counts,
+                                                                                   cnt64.p);
+  mx_count_launch();
+  if (int rc = excl_scan<u64>(cnt64.p, (long long)world * n_own, src_off.p, s)) return rc;
+  owned_gather_kernel<<<gb, 256, 0, s>>>(world, n_own, counts, src_off.p, cpo.p, pieces, pm.p, pf.p, ps.p, pe.p);
+  mx_count_launch();
+  IndexData* ix = g->ix;
+  int fbits = 1, mbits = 1;
+  while ((1ll << fbits) < (long long)ix->n_files + 1) ++fbits;
+  while ((1ll << mbits) < (long long)std::max<long long>(g->last_mkeys, g->K) + 1) ++mbits;
+  const bool pack = fbits + mbits <= 31;
+  int rc = normalize_tail(g, n_own, cpo, mcnt, big, pm, pf, ps, pe, cap, pack, fbits, g->ev_seed, s);
+  g->next_chunk_id = base_id + n_global;
+  return rc;
+}
+
 static int emit_local(GenData* g, const PlanWork& w, const Phase* h_phases, const Term* terms, long long n_chunks,
                       long long n_phases, cudaStream_t s) {
   const int Km = w.n_streams;
@@ -2574,7 +2679,9 @@ static int emit_local(GenData* g, const PlanWork& w, const Phase* h_phases, cons
   MX_CUDA_TRY(g->res_id.reserve(n_chunks > 0 ? n_chunks : 1, s));
   MX_CUDA_TRY(g->aux_init());
   cudaEvent_t seed_join = g->ev_seed;
-  if (n_chunks > 0) {
+  const bool handoff = L.handoff;
+  g->handoff.n_chunks = -1;
+  if (n_chunks > 0 && !handoff) {
     MX_CUDA_TRY(cudaEventRecord(g->ev_seed_fork, s));
     MX_CUDA_TRY(cudaStreamWaitEvent(g->sstream, g->ev_seed_fork, 0));
     chunk_seed_kernel<<<(unsigned)((n_chunks + 127) / 128), 128, 0, g->sstream>>>(
@@ -2582,9 +2689,19 @@ static int emit_local(GenData* g, const PlanWork& w, const Phase* h_phases, cons
     mx_count_launch();
     MX_CUDA_TRY(cudaEventRecord(seed_join, g->sstream));
   }
-  if (n_chunks == 0) {
+  if (n_chunks == 0 && !handoff) {
     const long long z = 0;
     MX_CUDA_TRY(mx_h2d(g->res_off.p, &z, sizeof(z), s));
+    MX_CUDA_TRY(cudaStreamSynchronize(s));
+    return MX_OK;
+  }
+  if (n_chunks == 0) {
+    MX_CUDA_TRY(g->handoff.off.reserve(1, s));
+    MX_CUDA_TRY(cudaMemsetAsync(g->handoff.off.p, 0, sizeof(long long), s));
+    MX_CUDA_TRY(g->handoff.pieces.reserve(1, s));
+    g->handoff.n_chunks = 0;
+    g->handoff.first_id = g->next_chunk_id;
+    g->res_chunks = 0;
     MX_CUDA_TRY(cudaStreamSynchronize(s));
     return MX_OK;
   }
@@ -2684,6 +2801,23 @@ static int emit_local(GenData* g, const PlanWork& w, const Phase* h_phases, cons
     mx_count_launch();
   }
   if (int rc = excl_scan<u64>(cc.p, n_chunks, cpo.p, s)) return rc;
+  if (handoff) {  // pieces grouped by chunk for the chunk owners; the owners normalise
+    MX_CUDA_TRY(g->handoff.off.reserve(n_chunks + 1, s));
+    MX_CUDA_TRY(g->handoff.pieces.reserve(cap, s));
+    MX_CUDA_TRY(cudaMemcpyAsync(g->handoff.off.p, cpo.p, sizeof(long long) * (n_chunks + 1),
+                                cudaMemcpyDeviceToDevice, s));
+    if (np > 0) {
+      chunk_scatter_aos_kernel<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(np, pc.p, pm.p, pf.p, ps.p, pe.p, cpo.p,
+                                                                            fill.p, g->handoff.pieces.p);
+      mx_count_launch();
+    }
+    MX_CUDA_TRY(cudaGetLastError());
+    MX_CUDA_TRY(cudaStreamSynchronize(s));  // the buffers above are freed with this scope
+    g->handoff.n_chunks = n_chunks;
+    g->handoff.first_id = g->next_chunk_id;
+    g->res_chunks = 0;  // the owners' results come from gen_finish_owned
+    return MX_OK;
+  }
   if (np > 0) {
     chunk_scatter_kernel<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(np, pc.p, pm.p, pf.p, ps.p, pe.p, cpo.p,
                                                                       fill.p, qm.p, qf.p, qs.p, qe.p);

@@ -398,12 +398,12 @@ def build_partitioned_index(local_catalog, predicates=(), file_lo: int = 0, file
     krows[:, 0] = gkeys[rk].astype(np.uint32)
     krows[:, 1] = sub
     krows[:, 2] = size
-    krows[:, 3] = 1
+    krows[:, 3] = rk  # dense key rank: the rows are already in (key, pseudo file) order
     d_krows = torch.from_numpy(krows.view(np.int32)).to(dev)
     sp = C.c_void_p(_lib.stream_ptr(stream))
     out = C.c_void_p()
     _lib.check(L.mx_index_build_owner(local.handle, d_krows.data_ptr(), len(krows), n_files, _lib.ptr(file_ds),
-                                      _lib.ptr(file_ids), sp, C.byref(out)))
+                                      _lib.ptr(file_ids), _bits(len(gkeys) - 1), sp, C.byref(out)))
     idx = ChunkerIndex(out.value, local_catalog, stream)
     d_gkeys = torch.from_numpy(gkeys).to(dev)
     key_g = torch.searchsorted(d_gkeys, torch.from_numpy(packed.astype(np.int64)).to(dev)).to(torch.int32)
@@ -412,9 +412,19 @@ def build_partitioned_index(local_catalog, predicates=(), file_lo: int = 0, file
         _lib.check(L.mx_index_block_table(local.handle, int(file_lo), rows.data_ptr(), sp))
     rows = rows[: local.n_blocks]
     key_g_rows = torch.searchsorted(d_gkeys, rows[:, 0].to(torch.int64) & 0xFFFFFFFF)
-    idx.partition = PartitionInfo(world, rank, group, int(file_lo), int(file_lo) + local_catalog.host.n_files,
-                                  file_ds, file_ids, local, rows, key_g, key_g_rows)
+    file_hi = int(file_lo) + local_catalog.host.n_files
+    ranges, _ = all_gather_rows(torch.tensor([[int(file_lo), file_hi]], dtype=torch.int64), group)
+    ranges = ranges[:, 0].numpy()
+    idx.partition = PartitionInfo(world, rank, group, int(file_lo), file_hi, file_ds, file_ids, local, rows, key_g,
+                                  key_g_rows)
+    # owners can skip the (file, key) sort when rank order is file order
+    idx.partition.rank_file_ordered = bool((ranges[1:, 0] >= ranges[:-1, 1]).all())
+    idx.partition.n_global_keys = len(gkeys)
     return idx
+
+
+def _bits(v: int) -> int:
+    return max(1, int(v).bit_length())
 
 
 def attach_partition(gen):
@@ -436,11 +446,16 @@ def attach_partition(gen):
     owner = pi.key_g_rows % pi.world
     perm = torch.argsort(owner, stable=True)
     splits = torch.bincount(owner, minlength=pi.world).tolist() if len(owner) else [0] * pi.world
-    recv, in_splits = _all_to_all_rows(pi.rows[perm].contiguous(), splits, pi.group)
+    send = pi.rows[perm].contiguous()
+    dense = 0
+    if pi.rank_file_ordered:  # row[3] := the key's rank among the owner's keys
+        send[:, 3] = (pi.key_g_rows[perm] // pi.world).to(torch.int32)
+        dense = _bits((pi.n_global_keys - 1) // pi.world)
+    recv, in_splits = _all_to_all_rows(send, splits, pi.group)
     n = int(recv.shape[0])
     oix = C.c_void_p()
     _lib.check(L.mx_index_build_owner(pi.local.handle, recv.data_ptr() if n else None, n, len(pi.file_ids),
-                                      _lib.ptr(pi.file_ds), _lib.ptr(pi.file_ids), sp, C.byref(oix)))
+                                      _lib.ptr(pi.file_ds), _lib.ptr(pi.file_ids), dense, sp, C.byref(oix)))
     off = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
     og = C.c_void_p()
     try:
@@ -461,3 +476,67 @@ def attach_partition(gen):
     gen._partition_bufs = (blk_off, pi.key_g)
     _lib.check(L.mx_gen_set_local(gen._h, pi.local.handle, blk_off.data_ptr() if len(blk_off) else None,
                                   pi.key_g.data_ptr() if len(pi.key_g) else None, pi.file_lo))
+
+
+def chunk_range(n_chunks: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced range [c0, c1) of the plan's chunks owned by ``rank``."""
+    return file_shard(n_chunks, world, rank)
+
+
+class _DevPtr:
+    """Zero-copy view of library-owned device memory (valid until the next plan)."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (int(ptr or 0), False),
+                                         "version": 3}
+
+
+def plan_owned(gen, spec, max_chunks: int, arbitrary_size: int | None = None):
+    """Collective bulk plan of a partitioned generator, chunk-owner output
+    (SURVEY.md §8(e)): every rank cuts its pieces of every planned chunk; one
+    all-to-all sends each contiguous chunk range's pieces (and per-chunk
+    counts) to its owner, which normalises only its chunks. Returns this
+    rank's ``ChunkBatch`` (global chunks ``batch.chunk_lo`` ..
+    ``batch.chunk_lo + batch.n_chunks`` of ``batch.global_chunks``); the
+    generator state advances past all of them on every rank. Equivalent to
+    ``plan_batch`` whose result is split by chunk over the ranks."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from .chunks import ChunkBatch
+
+    pi = gen.index.partition
+    L = _lib.lib()
+    sp = C.c_void_p(_lib.stream_ptr(gen.stream))
+    dev = gen.index.catalog.device
+    gen._rewind()
+    _lib.check(L.mx_gen_set_handoff(gen._h, 1))
+    try:
+        n, exhausted, (mkeys, report) = gen._plan(spec, max_chunks, arbitrary_size)
+        nc, npc, offp, pp = C.c_int64(), C.c_int64(), C.c_void_p(), C.c_void_p()
+        _lib.check(L.mx_gen_handoff(gen._h, C.byref(nc), C.byref(npc), C.byref(offp), C.byref(pp)))
+        off = torch.as_tensor(_DevPtr(offp.value, (n + 1,), "<i8"), device=dev)
+        pieces = torch.as_tensor(_DevPtr(pp.value, (npc.value, 4), "<i4"), device=dev) if npc.value else \
+            torch.zeros((0, 4), dtype=torch.int32, device=dev)
+        bounds = [chunk_range(n, pi.world, r) for r in range(pi.world)]
+        cut = off[torch.tensor([b[0] for b in bounds] + [n], device=dev)].cpu().tolist()
+        splits = [cut[r + 1] - cut[r] for r in range(pi.world)]
+        recv, _ = _all_to_all_rows(pieces, splits, pi.group)
+        counts = (off[1:] - off[:-1]).to(torch.int32)
+        rcounts, _ = _all_to_all_rows(counts, [b - a for a, b in bounds], pi.group)
+        lo, hi = bounds[pi.rank]
+        _lib.check(L.mx_gen_finish_owned(gen._h, pi.world, lo, hi - lo, n, rcounts.data_ptr() if len(rcounts) else None,
+                                         recv.data_ptr() if len(recv) else None, len(recv), sp))
+    finally:
+        L.mx_gen_set_handoff(gen._h, 0)
+    gen._next_id += n
+    cn, cr = C.c_int64(), C.c_int64()
+    _lib.check(L.mx_gen_result_sizes(gen._h, C.byref(cn), C.byref(cr)))
+    batch = ChunkBatch(gen, cn.value, cr.value, mkeys, spec, arbitrary_size)
+    batch.exhausted, batch.report = exhausted, report
+    batch.chunk_lo, batch.global_chunks = lo, n
+    if exhausted:
+        gen.last_report = report
+    return batch

@@ -7,7 +7,9 @@ block offsets; every rank plans on the key-level index and cuts only its own
 intervals; the merged chunks must be the REFERENCE's chunk bytes and
 shortfall reports (tests/golden, produced by the reference itself).
 Every plan mode is covered: disjoint mixtures (fused and general planner),
-keys sharing components, arbitrary chunks. Cursor checkpoints (reference
+keys sharing components, arbitrary chunks. The chunk-owner output
+(parallel.plan_owned: pieces all-to-all'd to the owner of each contiguous
+chunk range, normalised there) must tile the same plan. Cursor checkpoints (reference
 format) are refused with NotImplementedError."""
 
 from __future__ import annotations
@@ -44,7 +46,8 @@ def _run_case(rank, world, case):
     from conftest import golden_predicates, load_golden, spec_from_json
 
     from paper_2502_19790_b200 import ChunkGenerator, DeviceCatalog
-    from paper_2502_19790_b200.parallel import build_partitioned_index, file_shard, global_nullable, shard
+    from paper_2502_19790_b200.parallel import (build_partitioned_index, file_shard, global_nullable, plan_owned,
+                                                shard)
 
     cc, g = load_golden(case)
     f0, _ = file_shard(cc.n_files, world, rank)
@@ -72,7 +75,21 @@ def _run_case(rank, world, case):
             if spec is not None:
                 c.mixture = spec
             bulk.append(c.serialize().decode("ascii"))
-        res["runs"][name] = {"chunks": got, "report": report, "bulk": bulk}
+        # chunk-owner output: this rank's contiguous range of the same plan
+        gen = ChunkGenerator(idx, g["job_seed"])
+        ob = plan_owned(gen, spec, 10_000, arbitrary_size=arb)
+        owned = []
+        for i in range(ob.n_chunks):
+            c = ob.chunk(i)
+            if spec is not None:
+                c.mixture = spec
+            owned.append(c.serialize().decode("ascii"))
+        blob, offs = ob.serialize_all() if ob.n_chunks else (b"", [0])
+        dev_json = [blob[offs[i]:offs[i + 1]].decode("ascii") for i in range(ob.n_chunks)]
+        after = gen.generate_arbitrary(arb) if arb else gen.generate(spec)  # state moved past every chunk
+        res["runs"][name] = {"chunks": got, "report": report, "bulk": bulk, "owned": owned, "owned_json": dev_json,
+                             "owned_lo": ob.chunk_lo, "owned_of": ob.global_chunks,
+                             "after": None if after is None else after.serialize().decode("ascii")}
     try:
         ChunkGenerator(idx, g["job_seed"]).state_dict()
     except NotImplementedError:
@@ -107,6 +124,16 @@ def _check(case, world):
             if run.get("exhausted", True):
                 assert len(mine["bulk"]) == n
     assert n_ok > 0
+    for name, run in g["runs"].items():  # chunk-owner output: the ranks' ranges tile the bulk plan
+        parts = sorted((r["runs"][name]["owned_lo"], r["runs"][name]["owned"]) for r in res.values())
+        joined = [c for _, cs in parts for c in cs]
+        bulk = res[0]["runs"][name]["bulk"]
+        assert joined == bulk, f"{case}/{name} owned chunks"
+        for rank, r in res.items():
+            mine = r["runs"][name]
+            assert mine["owned_json"] == mine["owned"], f"{case}/{name} owned device JSON rank {rank}"
+            assert mine["owned_of"] == len(bulk)
+            assert mine["after"] is None  # plan_owned consumed the whole plan (bulk = to exhaustion here)
     return res
 
 

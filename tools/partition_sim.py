@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--world", type=int, default=8)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--trace", type=int, default=None, help="profile this rank's plan + emission")
     args = ap.parse_args()
     W = args.world
     dev = torch.device("cuda", 0)
@@ -63,6 +64,10 @@ def main():
         codes, table = bench.run_level_tuples(rt, dev)
         dcat = bench.device_catalog(meta, {"tuples": codes}, table)
         idx, ms = timed(lambda: build_index_from_catalog(dcat, []))
+        for _ in range(2):  # warm: first-call costs (pool growth, module load) are not the step
+            del idx
+            idx, t = timed(lambda: build_index_from_catalog(dcat, []))
+            ms = min(ms, t)
         nf = len(rt.file_sizes)
         packed, samples = idx.packed_keys()
         rows = torch.empty((max(idx.n_blocks, 1), 4), dtype=torch.int32, device=dev)
@@ -86,15 +91,17 @@ def main():
     sub = np.arange(len(rk)) - np.repeat(np.cumsum(pieces) - pieces, pieces)
     krows = np.zeros((len(rk), 4), np.uint32)
     krows[:, 0], krows[:, 1] = gkeys[rk].astype(np.uint32), sub
-    krows[:, 2], krows[:, 3] = np.minimum(totals[rk] - sub * U32_SPLIT, U32_SPLIT), 1
+    krows[:, 2], krows[:, 3] = np.minimum(totals[rk] - sub * U32_SPLIT, U32_SPLIT), rk
     host_keys_ms = (time.perf_counter() - t0) * 1e3
     d_krows = torch.from_numpy(krows.view(np.int32)).to(dev)
     d_gkeys = torch.from_numpy(gkeys).to(dev)
+    dense_k = max(1, (len(gkeys) - 1).bit_length())
+    dense_o = max(1, ((len(gkeys) - 1) // W).bit_length())
 
     def key_index():
         out = C.c_void_p()
         _lib.check(L.mx_index_build_owner(locs[0]["idx"].handle, d_krows.data_ptr(), len(krows), F,
-                                          _lib.ptr(file_ds), _lib.ptr(file_ids), sp, C.byref(out)))
+                                          _lib.ptr(file_ds), _lib.ptr(file_ids), dense_k, sp, C.byref(out)))
         return ChunkerIndex(out.value, locs[0]["dcat"])
 
     # ---- owner work: rows sent to owner o = rows whose key rank % W == o
@@ -104,7 +111,12 @@ def main():
             torch.int32)
     recv = []
     for o in range(W):
-        parts = [x["rows"][x["kg_rows"] % W == o] for x in locs]
+        parts = []
+        for x in locs:
+            sel = x["kg_rows"] % W == o
+            r = x["rows"][sel].clone()
+            r[:, 3] = (x["kg_rows"][sel] // W).to(torch.int32)
+            parts.append(r)
         recv.append((torch.cat(parts).contiguous(), [len(p) for p in parts]))
     cur, chk = hash_message(seed, "cursor"), hash_message(seed, "chunk")
     oseed = derive_seed(seed, "component-order")
@@ -115,7 +127,7 @@ def main():
         oix, og = C.c_void_p(), C.c_void_p()
         off = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
         _lib.check(L.mx_index_build_owner(locs[0]["idx"].handle, rows.data_ptr(), n, F, _lib.ptr(file_ds),
-                                          _lib.ptr(file_ids), sp, C.byref(oix)))
+                                          _lib.ptr(file_ids), dense_o, sp, C.byref(oix)))
         _lib.check(L.mx_gen_create(oix, cur, len(cur), chk, len(chk), oseed, sp, C.byref(og)))
         _lib.check(L.mx_gen_block_offsets(og, off.data_ptr(), sp))
         L.mx_gen_free(og)
@@ -123,6 +135,14 @@ def main():
         return off[:n]
 
     offs = [owner(o) for o in range(W)]  # warm
+    if args.trace is not None:
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as pr:
+            owner(args.trace)
+            torch.cuda.synchronize()
+        print("OWNER", file=sys.stderr)
+        print(pr.key_averages().table(sort_by="self_cuda_time_total", row_limit=20), file=sys.stderr)
     own_ms = []
     for o in range(W):
         best = min(timed(lambda: owner(o))[1] for _ in range(args.reps))
@@ -139,20 +159,33 @@ def main():
         x["blk_off"] = blk
 
     # ---- per rank: key-level index + generator + plan + local emission
-    def rank_job(x):
+    def rank_job(q):
+        x = locs[q]
         kix = key_index()
         gen = ChunkGenerator(kix, seed)
         _lib.check(L.mx_gen_set_local(gen._h, x["idx"].handle, x["blk_off"].data_ptr(), x["key_g"].data_ptr(),
-                                      locs.index(x) * nf))
+                                      q * nf))
         batch = gen.plan_batch(spec, 1 << 40)
         return kix, gen, batch
 
-    rank_job(locs[0])
-    results, rank_ms = [], []
+    rank_job(0)
+    if args.trace is not None:
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as pr:
+            rank_job(args.trace)
+            torch.cuda.synchronize()
+        print("RANK", file=sys.stderr)
+        print(pr.key_averages().table(sort_by="self_cuda_time_total", row_limit=30), file=sys.stderr)
+        pr.export_chrome_trace("gpurun_out/psim_rank_trace.json")
+        print(pr.key_averages().table(sort_by="self_cpu_time_total", row_limit=15), file=sys.stderr)
+    results, rank_ms, host_ms = [], [], []
     for q, x in enumerate(locs):
         best = None
         for _ in range(args.reps):
-            (kix, gen, batch), t = timed(lambda: rank_job(x))
+            h0 = time.perf_counter()
+            (kix, gen, batch), t = timed(lambda: rank_job(q))
+            host_ms.append(round((time.perf_counter() - h0) * 1e3, 3))
             best = t if best is None else min(best, t)
         n, rr = batch.n_chunks, batch.n_ranges
         off = torch.empty(n + 1, dtype=torch.int64, device=dev)
@@ -183,7 +216,7 @@ def main():
     report = {
         "world": W, "samples_per_rank": int(locs[0]["n_samples"]), "global_keys": int(len(gkeys)),
         "stage1_ms": stage1, "host_key_union_ms": round(host_keys_ms, 3),
-        "owner_ms": own_ms, "rank_plan_emit_ms": rank_ms, "merge_ms": round(t_m, 3),
+        "owner_ms": own_ms, "rank_plan_emit_ms": rank_ms, "rank_host_ms": host_ms, "merge_ms": round(t_m, 3),
         "global_chunks": int(n), "global_pieces": int(total),
         "bytes": {"keys_allgather": int(W * len(cat) * 16), "rows_alltoall": int(rows_total * 16),
                   "offsets_alltoall": int(rows_total * 8), "pieces_allgather": int(W * capr * 16)},
