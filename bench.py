@@ -27,11 +27,13 @@ the same workload on the host cores; without baseline/_ref the CPU oracle port
 (oracle/oracle.py) stands in and the line says kind "port".
 
 Under torchrun with N > 1 rank r owns its own 100M-sample shard = global files [r*F, (r+1)*F) of ONE N x 100M-sample catalog
-(weak scaling, cfg 3 shape) and the step is the file-sharded pipeline: local
-stage 1, NCCL all-gather of the per-(key, file) block tables, hybrid index +
-global cursor layout + plan (replicated), local emission, NCCL all-gather of
-every rank's pieces and the device merge into the global chunks. Step time =
-max over ranks.
+(weak scaling, cfg 3 shape; --scaling strong splits a fixed total, default
+1B) and the step is the key-partitioned pipeline (run_step): local stage 1,
+NCCL all-gather of per-key totals, all-to-all of block rows to the key
+owners and of block offsets back, replicated key-level plan, local cut, and
+an all-to-all of each chunk range's pieces to its owner rank, which
+normalises its chunks; every rank reads its own chunks back (e2e). Step
+time = max over ranks.
 """
 
 from __future__ import annotations
@@ -162,18 +164,26 @@ def layout_columns(rt, cols, layout):
 
 def run_step(dcat, spec, stream=None, shard=None):
     """One job on the device: index + cursor layout + every chunk. Returns
-    (index, batch) so callers can read sizes. With `shard` = (file_lo,
-    file_ds, file_ids) of the global catalog (N > 1): the file-sharded
-    pipeline -- local stage 1, all-gather of block tables, hybrid index,
-    global cursor layout + plan, local emission, all-gather + device merge
-    of every rank's pieces into the global chunks (paralle.py, shard.cu)."""
+    (index, gen, batch) so callers can read sizes. With `shard` = (file_lo,
+    file_ds, file_ids) of the global catalog (N > 1): the key-partitioned
+    pipeline (parallel.py) -- local stage 1, all-gather of per-key totals,
+    all-to-all of (key, file) block rows to the key owners, which lay out
+    their keys' cursor streams and return block offsets (all-to-all), plan
+    on the key-level index, local cut of every chunk, all-to-all of each
+    chunk range's pieces to its owner, which normalises its chunks
+    (parallel.plan_owned). MX_BENCH_MULTI=hybrid selects the file-sharded
+    hybrid index + full-piece all-gather of round 1 instead."""
     from paper_2502_19790_b200 import ChunkGenerator, build_index_from_catalog
-    from paper_2502_19790_b200.parallel import build_sharded_index
+    from paper_2502_19790_b200.parallel import build_partitioned_index, build_sharded_index, plan_owned
 
     if shard is None:
         idx = build_index_from_catalog(dcat, [], stream=stream)
-    else:
+    elif os.environ.get("MX_BENCH_MULTI") == "hybrid":
         idx = build_sharded_index(dcat, [], *shard, stream=stream)
+    else:
+        idx = build_partitioned_index(dcat, [], *shard, stream=stream)
+        gen = ChunkGenerator(idx, CFG["job_seed"], stream=stream)
+        return idx, gen, plan_owned(gen, spec, 1 << 40)
     gen = ChunkGenerator(idx, CFG["job_seed"], stream=stream)
     batch = gen.plan_batch(spec, 1 << 40)
     return idx, gen, batch
@@ -325,7 +335,8 @@ def arm_config(world: int, layout: str) -> dict:
     """The workload description both arms print (identical dicts)."""
     code_bytes, n_cols = (2, 1) if layout == "tuples" else (4, CFG["props"])
     n = CFG["n_samples"] * world
-    return dict(CFG, parallelism=f"file-sharded x{world}" if world > 1 else "single GPU",
+    multi = ("file-sharded hybrid" if os.environ.get("MX_BENCH_MULTI") == "hybrid" else "key-partitioned")
+    return dict(CFG, parallelism=f"{multi} x{world}" if world > 1 else "single GPU",
                 layout=LAYOUT_NOTE[layout],
                 l2=f"inputs ({n * code_bytes * n_cols / 1e9:.1f} GB of code columns) exceed the 126 MB L2; "
                    "no flush needed")
@@ -427,8 +438,10 @@ def our_arm(args):
     n_chunks = n_ranges = n_iv = 0
     for _ in range(args.steps):
         idx, gen, batch = run_step(dcat, spec, shard=shard)
-        n_chunks, n_ranges = batch.n_chunks, batch.n_ranges  # global chunks (merged when sharded)
-        n_iv = getattr(idx, "local_index", idx).n_intervals  # intervals this rank's scan wrote
+        # global chunks (this rank's owned range under the partitioned path)
+        n_chunks, n_ranges = getattr(batch, "global_chunks", batch.n_chunks), batch.n_ranges
+        part = getattr(idx, "partition", None)
+        n_iv = (part.local if part is not None else getattr(idx, "local_index", idx)).n_intervals
         n_keys, n_blocks = idx.n_keys, idx.n_blocks
         del idx, gen, batch
     ev1.record(stream)
@@ -495,9 +508,9 @@ def our_arm(args):
         for p, x in pinned.items():
             dbufs[p].copy_(x, non_blocking=True)
         idx, gen, batch = run_step(dcat_e2e, spec, shard=shard)
-        if rank != 0:  # the merged global chunks are read back on the root
+        if rank != 0 and not hasattr(batch, "chunk_lo"):  # hybrid: the merged global chunks are read on the root
             return 0
-        h = batch.to_host()
+        h = batch.to_host()  # partitioned: every rank reads back its own chunk range
         return sum(v.nbytes for k, v in h.items() if k in ("off", "ids", "seeds")) + 16 * batch.n_ranges
 
     for _ in range(max(1, args.warmup)):

@@ -1,6 +1,7 @@
-"""bench.py end to end at a small scale: the single-GPU line and the
-file-sharded N = 2 pipeline (two ranks sharing the GPU over gloo) both produce
-a well-formed JSON line with the contract's keys."""
+"""bench.py end to end at a small scale: the single-GPU line and the N = 2
+pipelines (key-partitioned, and the file-sharded hybrid; two ranks sharing
+the GPU over gloo) all produce a well-formed JSON line with the contract's
+keys."""
 
 from __future__ import annotations
 
@@ -40,11 +41,12 @@ def test_bench_single_gpu_small():
     _check(_line(r.stdout), 1)
 
 
-def test_bench_sharded_two_ranks_small():
+@pytest.mark.parametrize("multi", ["partitioned", "hybrid"])
+def test_bench_sharded_two_ranks_small(multi):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    env = dict(os.environ, MX_BENCH_BACKEND="gloo")
+    env = dict(os.environ, MX_BENCH_BACKEND="gloo", MX_BENCH_MULTI=multi)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
                         "--steps", "2", "--warmup", "1", "--scale", "0.05"], cwd=ROOT, capture_output=True,
@@ -52,4 +54,5 @@ def test_bench_sharded_two_ranks_small():
     assert r.returncode == 0, r.stderr[-3000:]
     d = _line(r.stdout)
     _check(d, 2)
-    assert d["config"]["parallelism"] == "file-sharded x2"
+    assert d["config"]["parallelism"] == ("file-sharded hybrid x2" if multi == "hybrid" else "key-partitioned x2")
+    assert d["job"]["chunks"] > 0

@@ -158,15 +158,26 @@ def main():
         blk[perm] = torch.cat(back)
         x["blk_off"] = blk
 
-    # ---- per rank: key-level index + generator + plan + local emission
-    def rank_job(q):
+    # ---- per rank: key-level index + generator + plan + cut (handoff); then
+    # every chunk owner finishes its contiguous chunk range
+    from paper_2502_19790_b200.parallel import _DevPtr, chunk_range
+
+    def rank_job(q, finish=None):
         x = locs[q]
         kix = key_index()
         gen = ChunkGenerator(kix, seed)
         _lib.check(L.mx_gen_set_local(gen._h, x["idx"].handle, x["blk_off"].data_ptr(), x["key_g"].data_ptr(),
                                       q * nf))
-        batch = gen.plan_batch(spec, 1 << 40)
-        return kix, gen, batch
+        _lib.check(L.mx_gen_set_handoff(gen._h, 1))
+        n, _, _ = gen._plan(spec, 1 << 40)
+        return kix, gen, n
+
+    def handoff(gen, n):
+        nc, npc, offp, pp = C.c_int64(), C.c_int64(), C.c_void_p(), C.c_void_p()
+        _lib.check(L.mx_gen_handoff(gen._h, C.byref(nc), C.byref(npc), C.byref(offp), C.byref(pp)))
+        off = torch.as_tensor(_DevPtr(offp.value, (n + 1,), "<i8"), device=dev).clone()
+        pieces = torch.as_tensor(_DevPtr(pp.value, (npc.value, 4), "<i4"), device=dev).clone()
+        return off, pieces
 
     rank_job(0)
     if args.trace is not None:
@@ -177,50 +188,47 @@ def main():
             torch.cuda.synchronize()
         print("RANK", file=sys.stderr)
         print(pr.key_averages().table(sort_by="self_cuda_time_total", row_limit=30), file=sys.stderr)
-        pr.export_chrome_trace("gpurun_out/psim_rank_trace.json")
-        print(pr.key_averages().table(sort_by="self_cpu_time_total", row_limit=15), file=sys.stderr)
-    results, rank_ms, host_ms = [], [], []
-    for q, x in enumerate(locs):
+    cut_ms, host_ms, hand = [], [], []
+    for q in range(W):
         best = None
         for _ in range(args.reps):
             h0 = time.perf_counter()
-            (kix, gen, batch), t = timed(lambda: rank_job(q))
+            (kix, gen, n), t = timed(lambda: rank_job(q))
             host_ms.append(round((time.perf_counter() - h0) * 1e3, 3))
             best = t if best is None else min(best, t)
-        n, rr = batch.n_chunks, batch.n_ranges
-        off = torch.empty(n + 1, dtype=torch.int64, device=dev)
-        cols4 = torch.empty((4, max(rr, 1)), dtype=torch.int32, device=dev)
-        _lib.check(L.mx_gen_result_export(gen._h, off.data_ptr(), *(cols4[f].data_ptr() for f in range(4)), sp))
-        results.append((off, cols4[:, :rr], rr))
-        rank_ms.append(round(best, 3))
-        del kix, gen, batch
-    # ---- root merge
-    n = results[0][0].numel() - 1
-    capr = max(max(x[2] for x in results), 1)
-    o_all = torch.stack([x[0] for x in results]).contiguous()
-    g4 = torch.zeros((4, W, capr), dtype=torch.int32, device=dev)
-    for q, (_, c4, rr) in enumerate(results):
-        g4[:, q, :rr] = c4
-    total = sum(x[2] for x in results)
-    out_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
-    out = torch.empty((4, max(total, 1)), dtype=torch.int32, device=dev)
+        cut_ms.append(round(best, 3))
+        hand.append(handoff(gen, n))
+        del kix, gen
+    # owner r: counts [W][n_own] and pieces (source-major) of its range
+    bounds = [chunk_range(n, W, r) for r in range(W)]
+    fin_ms = []
+    pieces_moved = 0
+    for r, (lo, hi) in enumerate(bounds):
+        cnt = torch.stack([(o[lo + 1: hi + 1] - o[lo:hi]).to(torch.int32) for o, _ in hand]).contiguous()
+        parts = [p[int(o[lo]): int(o[hi])] for o, p in hand]
+        pieces_moved += sum(len(p) for q_, p in enumerate(parts) if q_ != r)
+        rp = torch.cat(parts).contiguous()
+        fg_kix, fg, fn = rank_job(r)
 
-    def merge():
-        _lib.check(L.mx_chunks_merge(W, n, capr, o_all.data_ptr(), *(g4[f].data_ptr() for f in range(4)),
-                                     out_off.data_ptr(), *(out[f].data_ptr() for f in range(4)), sp))
+        def fin():
+            _lib.check(L.mx_gen_finish_owned(fg._h, W, lo, hi - lo, n, cnt.data_ptr(), rp.data_ptr(), len(rp), sp))
 
-    merge()
-    _, t_m = timed(merge)
+        _, t = timed(fin)
+        fin_ms.append(round(t, 3))
+        del fg, fg_kix
+    total = sum(len(p) for _, p in hand)
+    t_m = 0.0
     rows_total = sum(len(x["rows"]) for x in locs)
     stage1 = [round(x["stage1_ms"], 3) for x in locs]
     report = {
         "world": W, "samples_per_rank": int(locs[0]["n_samples"]), "global_keys": int(len(gkeys)),
         "stage1_ms": stage1, "host_key_union_ms": round(host_keys_ms, 3),
-        "owner_ms": own_ms, "rank_plan_emit_ms": rank_ms, "rank_host_ms": host_ms, "merge_ms": round(t_m, 3),
-        "global_chunks": int(n), "global_pieces": int(total),
+        "owner_ms": own_ms, "rank_plan_cut_ms": cut_ms, "rank_host_ms": host_ms, "chunk_owner_finish_ms": fin_ms,
+        "global_chunks": int(n), "global_pieces_before_merge": int(total),
         "bytes": {"keys_allgather": int(W * len(cat) * 16), "rows_alltoall": int(rows_total * 16),
-                  "offsets_alltoall": int(rows_total * 8), "pieces_allgather": int(W * capr * 16)},
-        "device_step_ms_est": round(max(stage1) + max(own_ms) + max(rank_ms) + t_m, 3),
+                  "offsets_alltoall": int(rows_total * 8), "pieces_alltoall": int(pieces_moved * 16),
+                  "counts_alltoall": int(W * n * 4)},
+        "device_step_ms_est": round(max(stage1) + max(own_ms) + max(cut_ms) + max(fin_ms), 3),
     }
     print(json.dumps(report))
 
