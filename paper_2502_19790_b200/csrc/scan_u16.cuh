@@ -43,8 +43,8 @@ constexpr int U16_SMEM_LUT_MAX = 16384;
 
 struct U16Warp {                     // per-warp shared scratch
   uint16_t codes[SEG_LEN];           // the segment's codes, 16-byte chunks swizzled (u16_chunk)
-  uint16_t ev[SEG_LEN];              // candidate boundaries (segment offsets), sample order
-  uint8_t flag[SEG_LEN];             // bit 0 real boundary, bit 1 starts a record
+  uint16_t ev[SEG_LEN];              // candidate boundaries (segment offsets < 2048), sample order;
+                                     // pass 1 adds bit 14 (real boundary), bit 15 (starts a record)
   u32 fsm[SEG_LEN / 32];             // file starts inside the segment (bit = offset)
 };
 
@@ -131,7 +131,7 @@ __device__ __forceinline__ u32 change32(u32 prev, const uint4* w) {
 }
 
 template <bool SLUT>
-__global__ void __launch_bounds__(U16_WARPS * 32, 4)
+__global__ void __launch_bounds__(U16_WARPS * 32, 5)
 scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
   extern __shared__ __align__(16) unsigned char u16_dyn[];
   U16Warp* wsm = reinterpret_cast<U16Warp*>(u16_dyn);
@@ -242,7 +242,7 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
           real = (pc || kp < lim) && (fs || kc != kp);
         }
         rec = real && pc;
-        W.flag[e] = (uint8_t)((real ? 1u : 0u) | (rec ? 2u : 0u));
+        W.ev[e] = (uint16_t)(idx | (real ? 0x4000 : 0) | (rec ? 0x8000 : 0));
       }
       rtot += (u32)__popc(__ballot_sync(MX_FULL, rec));
     }
@@ -268,8 +268,9 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
     for (int b = (nev - 1) & ~31; b >= 0; b -= 32) {
       const int e = b + lane;
       const bool ok = e < nev;
-      const u32 fl = ok ? (u32)W.flag[e] : 0u;
-      const int idx = ok ? (int)W.ev[e] : 0;
+      const u32 ev = ok ? (u32)W.ev[e] : 0u;
+      const u32 fl = ev >> 14;
+      const int idx = (int)(ev & 0x3fffu);
       const u32 realb = __ballot_sync(MX_FULL, fl & 1u);
       const u32 recb = __ballot_sync(MX_FULL, fl & 2u);
       const u32 above = ~((2u << lane) - 1u);  // lanes > this one
@@ -302,7 +303,7 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
     }
     if (lane == 0) {
       a.tile_cnt[seg] = rtot;
-      const bool open = last_real_e >= 0 && (W.flag[last_real_e] & 2u) && !end_real;
+      const bool open = last_real_e >= 0 && (W.ev[last_real_e] & 0x8000u) && !end_real;
       a.tile_open[seg] = open ? 1u : 0u;
       // where the run continuing into this segment ends: the first real
       // boundary; the data end for the last segment; else "passes through"
