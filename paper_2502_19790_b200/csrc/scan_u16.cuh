@@ -224,29 +224,20 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
       for (u32 c = m1; c; c &= c - 1) W.ev[p++] = (uint16_t)(64 * lane + 32 + __ffs(c) - 1);
     }
     __syncwarp();
-    // ---- pass 1 (forward): real boundaries and records
-    u32 rtot = 0;
-    for (int b = 0; b < nev; b += 32) {
-      const int e = b + lane;
-      bool real = false, rec = false;
-      if (e < nev) {
-        const int idx = W.ev[e];
-        const u32 kc = u16_key<SLUT>(s_lut, g_lut, u16_code(W, idx));
-        const bool pc = kc < lim;
-        if (s0 + idx == 0) {
-          real = pc;
-        } else {
-          const u32 pre = idx > 0 ? u16_code(W, idx - 1) : hprev;
-          const u32 kp = u16_key<SLUT>(s_lut, g_lut, pre);
-          const bool fs = idx == 0 ? fs0 : ((W.fsm[idx >> 5] >> (idx & 31)) & 1u) != 0;
-          real = (pc || kp < lim) && (fs || kc != kp);
-        }
-        rec = real && pc;
-        W.ev[e] = (uint16_t)(idx | (real ? 0x4000 : 0) | (rec ? 0x8000 : 0));
+    // ---- candidate -> (real boundary, starts a record)
+    auto classify = [&](int idx, bool& real, bool& rec) {
+      const u32 kc = u16_key<SLUT>(s_lut, g_lut, u16_code(W, idx));
+      const bool pc = kc < lim;
+      if (s0 + idx == 0) {
+        real = pc;
+      } else {
+        const u32 pre = idx > 0 ? u16_code(W, idx - 1) : hprev;
+        const u32 kp = u16_key<SLUT>(s_lut, g_lut, pre);
+        const bool fs = idx == 0 ? fs0 : ((W.fsm[idx >> 5] >> (idx & 31)) & 1u) != 0;
+        real = (pc || kp < lim) && (fs || kc != kp);
       }
-      rtot += (u32)__popc(__ballot_sync(MX_FULL, rec));
-    }
-    __syncwarp();
+      rec = real && pc;
+    };
     // ---- segment end: is sample s0 + len a boundary of the run holding s0 + len - 1?
     bool end_real = true;
     {
@@ -259,51 +250,95 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
         end_real = fs_end || kl != kn;
       }
     }
-    // ---- pass 2 (backward): each record ends at the next real boundary; its
-    // slot = records before it (rtot minus the records at or after it)
+    // ---- a record [idx, end) in slot r (end < 0: continues past the segment)
     const u64 sbase = (u64)seg * SEG_LEN;
-    int next_real = end_real ? len : -1;  // -1: the run continues past the segment
-    int first_real = -1, last_real_e = -1;
-    u32 rsuf = 0;  // records in the batches after this one
-    for (int b = (nev - 1) & ~31; b >= 0; b -= 32) {
-      const int e = b + lane;
-      const bool ok = e < nev;
-      const u32 ev = ok ? (u32)W.ev[e] : 0u;
-      const u32 fl = ev >> 14;
-      const int idx = (int)(ev & 0x3fffu);
-      const u32 realb = __ballot_sync(MX_FULL, fl & 1u);
-      const u32 recb = __ballot_sync(MX_FULL, fl & 2u);
-      const u32 above = ~((2u << lane) - 1u);  // lanes > this one
-      const u32 after = realb & above;
-      const int nidx = __shfl_sync(MX_FULL, idx, after ? __ffs(after) - 1 : lane);
-      if (realb) {
-        if (last_real_e < 0) last_real_e = b + 31 - __clz(realb);
-        first_real = __shfl_sync(MX_FULL, idx, __ffs(realb) - 1);
+    auto store = [&](int idx, int end, u32 r) {
+      // file of the run: fa + the segment's file starts at or before it
+      int lo = 0, hi = nf;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(a.file_off + cfa + mid) <= s0 + idx) lo = mid; else hi = mid - 1;
       }
-      if (fl & 2u) {
-        const int end = after ? nidx : next_real;
-        const u32 r = rtot - 1u - rsuf - (u32)__popc(recb & above);
-        // file of the run: fa + the segment's file starts at or before it
-        int lo = 0, hi = nf;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (__ldg(a.file_off + cfa + mid) <= s0 + idx) lo = mid; else hi = mid - 1;
+      const long long fstart = lo ? __ldg(a.file_off + cfa + lo) : fbase;
+      const u32 key = u16_key<SLUT>(s_lut, g_lut, u16_code(W, idx));
+      const u32 off = (u32)(s0 - fstart);
+      a.rec_key[sbase + r] = key;
+      a.rec_file[sbase + r] = (u32)(cfa + lo);
+      a.rec_start[sbase + r] = off + (u32)idx;
+      if (end >= 0) a.rec_end[sbase + r] = off + (u32)end;
+      if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)(s0 + idx));
+    };
+    const int seg_end = end_real ? len : -1;  // -1: the run continues past the segment
+    const u32 above = ~((2u << lane) - 1u), below = (1u << lane) - 1u;
+    u32 rtot = 0;
+    int first_real = -1;
+    bool open = false;
+    if (nev <= 64) {
+      // ---- common case: every candidate in registers (two per lane), no
+      // shared flags, one pass
+      const bool ok0 = lane < nev, ok1 = 32 + lane < nev;
+      const int idx0 = ok0 ? (int)W.ev[lane] : 0, idx1 = ok1 ? (int)W.ev[32 + lane] : 0;
+      bool real0 = false, rec0 = false, real1 = false, rec1 = false;
+      if (ok0) classify(idx0, real0, rec0);
+      if (ok1) classify(idx1, real1, rec1);
+      const u32 realb0 = __ballot_sync(MX_FULL, real0), recb0 = __ballot_sync(MX_FULL, rec0);
+      const u32 realb1 = __ballot_sync(MX_FULL, real1), recb1 = __ballot_sync(MX_FULL, rec1);
+      const int r0 = __ffs(realb0) - 1, r1 = __ffs(realb1) - 1;
+      const int after0 = __ffs(realb0 & above) - 1, after1 = __ffs(realb1 & above) - 1;
+      const int nx0 = __shfl_sync(MX_FULL, idx0, after0 >= 0 ? after0 : lane);
+      const int nx1 = __shfl_sync(MX_FULL, idx1, after1 >= 0 ? after1 : lane);
+      const int fr0 = __shfl_sync(MX_FULL, idx0, r0 >= 0 ? r0 : 0);
+      const int fr1 = __shfl_sync(MX_FULL, idx1, r1 >= 0 ? r1 : 0);
+      const int next1 = seg_end;                     // after the last candidate
+      const int next0 = r1 >= 0 ? fr1 : seg_end;     // after half 0
+      if (rec0) store(idx0, after0 >= 0 ? nx0 : next0, (u32)__popc(recb0 & below));
+      if (rec1) store(idx1, after1 >= 0 ? nx1 : next1, (u32)(__popc(recb0) + __popc(recb1 & below)));
+      rtot = (u32)(__popc(recb0) + __popc(recb1));
+      first_real = r0 >= 0 ? fr0 : (r1 >= 0 ? fr1 : -1);
+      // the last real boundary starts a record that runs past the segment end
+      if (realb1) open = ((recb1 >> (31 - __clz(realb1))) & 1u) != 0;
+      else if (realb0) open = ((recb0 >> (31 - __clz(realb0))) & 1u) != 0;
+      open = open && !end_real;
+    } else {
+      // ---- pass 1 (forward): real boundaries and records, flags into the list
+      for (int b = 0; b < nev; b += 32) {
+        const int e = b + lane;
+        bool real = false, rec = false;
+        if (e < nev) {
+          const int idx = W.ev[e];
+          classify(idx, real, rec);
+          W.ev[e] = (uint16_t)(idx | (real ? 0x4000 : 0) | (rec ? 0x8000 : 0));
         }
-        const long long fstart = lo ? __ldg(a.file_off + cfa + lo) : fbase;
-        const u32 key = u16_key<SLUT>(s_lut, g_lut, u16_code(W, idx));
-        const u32 off = (u32)(s0 - fstart);
-        a.rec_key[sbase + r] = key;
-        a.rec_file[sbase + r] = (u32)(cfa + lo);
-        a.rec_start[sbase + r] = off + (u32)idx;
-        if (end >= 0) a.rec_end[sbase + r] = off + (u32)end;
-        if ((key & a.rank_mask) == 0) atomicMin(&a.err->null_key_sample, (u64)(s0 + idx));
+        rtot += (u32)__popc(__ballot_sync(MX_FULL, rec));
       }
-      rsuf += (u32)__popc(recb);
-      if (realb) next_real = first_real;
+      __syncwarp();
+      // ---- pass 2 (backward): each record ends at the next real boundary;
+      // its slot = records before it (rtot minus the records at or after it)
+      int next_real = seg_end;
+      int last_real_e = -1;
+      u32 rsuf = 0;  // records in the batches after this one
+      for (int b = (nev - 1) & ~31; b >= 0; b -= 32) {
+        const int e = b + lane;
+        const bool ok = e < nev;
+        const u32 ev = ok ? (u32)W.ev[e] : 0u;
+        const u32 fl = ev >> 14;
+        const int idx = (int)(ev & 0x3fffu);
+        const u32 realb = __ballot_sync(MX_FULL, fl & 1u);
+        const u32 recb = __ballot_sync(MX_FULL, fl & 2u);
+        const u32 after = realb & above;
+        const int nidx = __shfl_sync(MX_FULL, idx, after ? __ffs(after) - 1 : lane);
+        if (realb) {
+          if (last_real_e < 0) last_real_e = b + 31 - __clz(realb);
+          first_real = __shfl_sync(MX_FULL, idx, __ffs(realb) - 1);
+        }
+        if (fl & 2u) store(idx, after ? nidx : next_real, rtot - 1u - rsuf - (u32)__popc(recb & above));
+        rsuf += (u32)__popc(recb);
+        if (realb) next_real = first_real;
+      }
+      open = last_real_e >= 0 && (W.ev[last_real_e] & 0x8000u) && !end_real;
     }
     if (lane == 0) {
       a.tile_cnt[seg] = rtot;
-      const bool open = last_real_e >= 0 && (W.ev[last_real_e] & 0x8000u) && !end_real;
       a.tile_open[seg] = open ? 1u : 0u;
       // where the run continuing into this segment ends: the first real
       // boundary; the data end for the last segment; else "passes through"
