@@ -544,8 +544,8 @@ def our_arm(args):
     if tf.exists():
         prof = json.loads(tf.read_text()).get(args.layout, {})
         traffic = prof.get("bytes_per_launch")
-    # the u16 single-column scan is instruction-issue bound (ncu issue-active),
-    # not HBM bound: say so next to its HBM fraction
+    # the u16 single-column scan is issue / latency bound (ncu issue-active,
+    # warps active), not HBM bound: say so next to its HBM fraction
     issue = prof.get("issue_active_pct")
     line = {
         "metric": METRIC, "value": world * n / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
@@ -566,9 +566,11 @@ def our_arm(args):
                                 "deferred-tile scan_list + tail scan_direct)"),
                      "bytes_per_launch": scan_bytes, "peak_kind": peak_kind,
                      "note": "algorithmic bytes = N*b*C code-column reads (C = 1 row-tuple column of b = 2-byte codes, or P per-property int32 columns) + 16 B per interval record"
-                             + (f"; at {b_per_sample} B/sample this kernel is instruction-issue bound "
-                                f"(ncu: {issue:.0f}% issue-active, {prof.get('inst_executed', 0) / n:.2f} warp "
-                                f"instructions per sample), not HBM bound" if issue and code_bytes * n_cols <= 2 else "")},
+                             + (f"; at {b_per_sample} B/sample this kernel is bound by instruction issue and "
+                                f"latency, not HBM (ncu: {issue:.0f}% issue-active at "
+                                f"{prof.get('warps_active_pct', 0):.0f}% warps active, "
+                                f"{prof.get('inst_executed', 0) / n:.2f} warp instructions per sample)"
+                                if issue and code_bytes * n_cols <= 2 else "")},
         # the whole job against the same peak (B1 + B2 per step)
         "roofline_step": {
             "bytes": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
