@@ -89,8 +89,32 @@ class DeviceCatalog:
         return inv.to(torch.int32), table
 
     @staticmethod
-    def from_reference(cat, device=None) -> "DeviceCatalog":
-        return DeviceCatalog(ColumnarCatalog.from_reference(cat), device=device)
+    def from_reference(cat, device=None, layout: str = "tuples") -> "DeviceCatalog":
+        """A reference ``MetadataCatalog`` in HBM. ``layout="tuples"`` (the
+        drop-in's default) dictionary-encodes the rows once into one u16 (or
+        int32) row-tuple column, the layout stage 1 scans fastest;
+        ``"columns"`` keeps one int32 column per property."""
+        host = ColumnarCatalog.from_reference(cat)
+        if layout == "tuples":
+            return DeviceCatalog.with_row_tuples(host, device)
+        return DeviceCatalog(host, device=device)
+
+    @staticmethod
+    def with_row_tuples(host: ColumnarCatalog, device=None) -> "DeviceCatalog":
+        """Upload ``host`` and encode its rows into one row-tuple column on
+        the device (``encode_row_tuples_device``); the per-property columns
+        are dropped after the encoding."""
+        import torch
+
+        dev = torch.device(device or "cuda")
+        props = sorted(host.vocab)
+        if host.n_samples == 0 or not props:
+            return DeviceCatalog(host, device=dev)
+        cols = {p: torch.from_numpy(np.ascontiguousarray(host.columns[p], dtype=np.int32)).to(dev) for p in props}
+        nullable = {p: bool((cols[p] < 0).any().item()) for p in props}
+        codes, table = DeviceCatalog.encode_row_tuples_device(cols, [len(host.vocab[p]) for p in props])
+        del cols
+        return DeviceCatalog(host, nullable=nullable, device=dev, tuples=(codes, table))
 
     @property
     def n_samples(self) -> int:
