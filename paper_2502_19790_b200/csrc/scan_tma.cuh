@@ -521,7 +521,8 @@ __global__ void slot_compact_kernel(long long ntiles, long long tile_len, const 
                                     const u32* k, const u32* f, const u32* s, const u32* e, u32* k2, u32* f2, u32* s2,
                                     u32* e2) {
   // four tiles per warp in flight: their counts / offsets, then their first
-  // 32 records each, are loaded before anything is stored
+  // 64 records each (two per lane: a 2048-sample segment at R = 64 holds ~32),
+  // are loaded before anything is stored
   constexpr int U = 4;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   const u32 lane = threadIdx.x & 31;
@@ -534,21 +535,27 @@ __global__ void slot_compact_kernel(long long ntiles, long long tile_len, const 
       c[u] = t < ntiles ? cnt[t] : 0;
       dst[u] = t < ntiles ? off[t] : 0;
     }
-    u32 vk[U], vf[U], vs[U], ve[U];
+    u32 vk[U][2], vf[U][2], vs[U][2], ve[U][2];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const u64 src = (u64)(t0 + u * warps) * tile_len + lane;
-      if (lane < c[u]) {
-        vk[u] = k[src]; vf[u] = f[src]; vs[u] = s[src]; ve[u] = e[src];
-      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (lane + 32 * h < c[u]) {
+          vk[u][h] = k[src + 32 * h]; vf[u][h] = f[src + 32 * h]; vs[u][h] = s[src + 32 * h];
+          ve[u][h] = e[src + 32 * h];
+        }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (lane < c[u]) {
-        k2[dst[u] + lane] = vk[u]; f2[dst[u] + lane] = vf[u]; s2[dst[u] + lane] = vs[u]; e2[dst[u] + lane] = ve[u];
-      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (lane + 32 * h < c[u]) {
+          const u64 d = dst[u] + lane + 32 * h;
+          k2[d] = vk[u][h]; f2[d] = vf[u][h]; s2[d] = vs[u][h]; e2[d] = ve[u][h];
+        }
       const u64 src = (u64)(t0 + u * warps) * tile_len;
-      for (u32 i = lane + 32; i < c[u]; i += 32) {  // tiles with more than 32 runs
+      for (u32 i = lane + 64; i < c[u]; i += 32) {  // tiles with more than 64 runs
         k2[dst[u] + i] = k[src + i];
         f2[dst[u] + i] = f[src + i];
         s2[dst[u] + i] = s[src + i];
