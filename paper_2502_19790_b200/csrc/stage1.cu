@@ -184,7 +184,7 @@ radix_upsweep2(const u32* keys, long long n, int shift, u32* hist, int ntiles) {
 }
 
 template <int RS2_ITEMS>
-__global__ void __launch_bounds__(RS_THREADS)
+__global__ void __launch_bounds__(RS_THREADS, 4)
 radix_downsweep2(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2in, u32* kout, u32* p0out,
                  u32* p1out, u32* p2out, long long n, int shift, const u32* hist, const u32* digit_tot,
                  int ntiles) {
@@ -214,11 +214,24 @@ radix_downsweep2(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2
   const long long t0 = (long long)blockIdx.x * RS2_TILE;
   const long long base = t0 + warp * (32 * RS2_ITEMS);
   u32 dig[RS2_ITEMS], rank[RS2_ITEMS];
+  // every record's four words are loaded up front (one round of global
+  // latency per tile; the ranking below only needs the keys)
+  u32 vk[RS2_ITEMS], va[RS2_ITEMS], vb[RS2_ITEMS], vc[RS2_ITEMS];
+#pragma unroll
+  for (int k = 0; k < RS2_ITEMS; ++k) {
+    const long long i = base + k * 32 + lane;
+    if (i < n) {
+      vk[k] = kin[i];
+      va[k] = p0in[i];
+      vb[k] = p1in[i];
+      vc[k] = p2in[i];
+    }
+  }
 #pragma unroll
   for (int k = 0; k < RS2_ITEMS; ++k) {
     const long long i = base + k * 32 + lane;
     const bool ok = i < n;
-    const u32 d = ok ? (kin[i] >> shift) & 0xff : 0x100u;
+    const u32 d = ok ? (vk[k] >> shift) & 0xff : 0x100u;
     const u32 peers = __match_any_sync(MX_FULL, d);
     const u32 before = __popc(peers & ((1u << lane) - 1));
     const u32 cur = s_wcnt[warp][d & 0xff];
@@ -258,14 +271,13 @@ radix_downsweep2(const u32* kin, const u32* p0in, const u32* p1in, const u32* p2
   u32* sc = s_stage + 3 * RS2_TILE;
 #pragma unroll
   for (int k = 0; k < RS2_ITEMS; ++k) {
-    const long long i = base + k * 32 + lane;
     if (dig[k] < 0x100u) {
       const u32 d = dig[k];
       const u32 pos = s_loc[d] + s_wcnt[warp][d] + rank[k];
-      sk[pos] = kin[i];
-      sa[pos] = p0in[i];
-      sb[pos] = p1in[i];
-      sc[pos] = p2in[i];
+      sk[pos] = vk[k];
+      sa[pos] = va[k];
+      sb[pos] = vb[k];
+      sc[pos] = vc[k];
     }
   }
   __syncthreads();
