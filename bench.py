@@ -663,8 +663,8 @@ def extra_measurements(args, rt, meta, spec, device) -> dict:
     out["columns_layout"] = {
         "ms_per_step": ms, "value": n / (ms * 1e-3), "unit": UNIT,
         "scan_ms": scan_avg, "scan_roofline_frac": scan_bytes / (scan_avg * 1e-3) / 1e9 / peak,
-        "note": "one int32 code column per property (2 GB at cfg2), the layout of a catalog adopted from the "
-                "reference (DeviceCatalog.from_reference)"}
+        "note": "one int32 code column per property (2 GB at cfg2): DeviceCatalog.from_reference(cat, "
+                "layout='columns'); drop-in catalogs default to the row-tuple layout"}
     cards = [len(rt.vocab[p]) for p in sorted(rt.vocab)]
     enc_ms = _timed_steps(lambda: DeviceCatalog.encode_row_tuples_device(cols, cards), 3, 1)
     out["registration"] = {
