@@ -351,6 +351,38 @@ def _all_to_all_rows(send, splits, group):
     return recv.to(send.device), in_splits
 
 
+def key_level_rows(gkeys: np.ndarray, totals: np.ndarray, n_files: int) -> np.ndarray:
+    """Rows (packed key, pseudo file, samples, dense key rank) uint32[R, 4] of
+    the key-level index: one pseudo-interval per key, totals above 2^31 split
+    over consecutive pseudo files (u32 interval ends); already in (key, file)
+    order."""
+    gkeys = np.asarray(gkeys)
+    totals = np.asarray(totals, dtype=np.int64)
+    pieces = np.maximum(1, -(-totals // U32_SPLIT))
+    if int(pieces.max(initial=1)) > n_files:
+        raise ValueError("a key holds more than n_files * 2^31 samples")
+    rk = np.repeat(np.arange(len(gkeys)), pieces)
+    sub = np.arange(len(rk)) - np.repeat(np.cumsum(pieces) - pieces, pieces)
+    krows = np.zeros((len(rk), 4), np.uint32)
+    krows[:, 0] = gkeys[rk].astype(np.uint32)
+    krows[:, 1] = sub
+    krows[:, 2] = np.minimum(totals[rk] - sub * U32_SPLIT, U32_SPLIT)
+    krows[:, 3] = rk
+    return krows
+
+
+def route_to_owners(key_rank, world: int):
+    """Rows grouped by owner rank (key rank mod world), stable: (permutation
+    of the rows, rows per owner). The owner's reply comes back in the same
+    grouped order: ``reply_in_row_order[perm] = reply``."""
+    import torch
+
+    owner = key_rank % world
+    perm = torch.argsort(owner, stable=True)
+    splits = torch.bincount(owner, minlength=world).tolist() if len(owner) else [0] * world
+    return perm, splits
+
+
 def build_partitioned_index(local_catalog, predicates=(), file_lo: int = 0, file_ds=None, file_ids=None,
                             group=None, stream=None):
     """Collective: the key-level ChunkerIndex every rank plans on (global
@@ -387,18 +419,7 @@ def build_partitioned_index(local_catalog, predicates=(), file_lo: int = 0, file
     file_ds = np.ascontiguousarray(file_ds, dtype=np.int32)
     file_ids = np.ascontiguousarray(file_ids, dtype=np.int64)
     n_files = len(file_ids)
-    # key-level rows (packed key, pseudo file, samples): totals above 2^31 split
-    pieces = np.maximum(1, -(-totals // U32_SPLIT))
-    if int(pieces.max(initial=1)) > n_files:
-        raise ValueError("a key holds more than n_files * 2^31 samples")
-    rk = np.repeat(np.arange(len(gkeys)), pieces)
-    sub = np.arange(len(rk)) - np.repeat(np.cumsum(pieces) - pieces, pieces)
-    size = np.minimum(totals[rk] - sub * U32_SPLIT, U32_SPLIT)
-    krows = np.zeros((len(rk), 4), np.uint32)
-    krows[:, 0] = gkeys[rk].astype(np.uint32)
-    krows[:, 1] = sub
-    krows[:, 2] = size
-    krows[:, 3] = rk  # dense key rank: the rows are already in (key, pseudo file) order
+    krows = key_level_rows(gkeys, totals, n_files)
     d_krows = torch.from_numpy(krows.view(np.int32)).to(dev)
     sp = C.c_void_p(_lib.stream_ptr(stream))
     out = C.c_void_p()
@@ -443,9 +464,7 @@ def attach_partition(gen):
     L = _lib.lib()
     dev = gen.index.catalog.device
     sp = C.c_void_p(_lib.stream_ptr(gen.stream))
-    owner = pi.key_g_rows % pi.world
-    perm = torch.argsort(owner, stable=True)
-    splits = torch.bincount(owner, minlength=pi.world).tolist() if len(owner) else [0] * pi.world
+    perm, splits = route_to_owners(pi.key_g_rows, pi.world)
     send = pi.rows[perm].contiguous()
     dense = 0
     if pi.rank_file_ordered:  # row[3] := the key's rank among the owner's keys

@@ -1,6 +1,8 @@
 """Multi-process (gloo, world_size 2, CPU) tests of the N>1 host paths:
-file sharding, the block-table all-gather for the global cursor merge, and
-the data-parallel per-domain loss all-reduce (stage 3)."""
+file sharding, the block-table all-gather for the global cursor merge, the
+key-partitioned exchanges (block rows to the key owners and their replies
+back, chunk ranges to their owners), and the data-parallel per-domain loss
+all-reduce (stage 3)."""
 
 from __future__ import annotations
 
@@ -118,3 +120,57 @@ def test_domain_loss_allreduce_sums_ranks():
     for r in range(2):
         np.testing.assert_allclose(got[r][0], exp_s, rtol=1e-12)
         assert got[r][1] == exp_c.tolist()
+
+
+def owners_job(rank, world):
+    """Every rank routes its (key rank, payload) rows to the key owners; each
+    owner answers f(row) and the replies come back in the sender's row order."""
+    import torch
+
+    from paper_2502_19790_b200.parallel import _all_to_all_rows, route_to_owners
+
+    rng = np.random.default_rng(100 + rank)
+    n = int(rng.integers(0, 50))
+    key_rank = torch.from_numpy(rng.integers(0, 7, n).astype(np.int64))
+    rows = torch.stack([key_rank.to(torch.int32), torch.from_numpy(rng.integers(0, 1000, n).astype(np.int32)),
+                        torch.full((n,), rank, dtype=torch.int32)], 1) if n else torch.zeros((0, 3), dtype=torch.int32)
+    perm, splits = route_to_owners(key_rank, world)
+    recv, in_splits = _all_to_all_rows(rows[perm].contiguous(), splits, None)
+    assert bool((recv[:, 0].to(torch.int64) % world == rank).all())  # only this owner's keys arrive
+    reply = (recv[:, 0].to(torch.int64) * 100000 + recv[:, 1].to(torch.int64) * 10 + recv[:, 2].to(torch.int64))
+    back, _ = _all_to_all_rows(reply.contiguous(), in_splits, None)
+    out = torch.empty_like(back)
+    out[perm] = back
+    want = rows[:, 0].to(torch.int64) * 100000 + rows[:, 1].to(torch.int64) * 10 + rank
+    return bool(torch.equal(out, want)), n, sum(in_splits)
+
+
+def test_key_owner_routing_round_trip():
+    got = _run("owners_job")
+    assert all(ok for ok, _, _ in got.values())
+    assert sum(n for _, n, _ in got.values()) == sum(m for _, _, m in got.values())
+
+
+def test_key_level_rows_split_large_totals():
+    from paper_2502_19790_b200.parallel import U32_SPLIT, key_level_rows
+
+    gkeys = np.array([3, 9, 40], dtype=np.uint32)
+    totals = np.array([5, 2 * U32_SPLIT + 7, U32_SPLIT], dtype=np.int64)
+    rows = key_level_rows(gkeys, totals, n_files=4)
+    assert rows[:, 0].tolist() == [3, 9, 9, 9, 40]
+    assert rows[:, 1].tolist() == [0, 0, 1, 2, 0]
+    assert rows[:, 3].tolist() == [0, 1, 1, 1, 2]
+    for k, t in zip(gkeys, totals):
+        assert int(rows[rows[:, 0] == k, 2].astype(np.int64).sum()) == int(t)
+    with pytest.raises(ValueError):
+        key_level_rows(gkeys, totals, n_files=2)
+
+
+def test_chunk_ranges_tile_the_plan():
+    from paper_2502_19790_b200.parallel import chunk_range
+
+    for n in (0, 1, 5, 83_006):
+        for world in (1, 2, 3, 8):
+            spans = [chunk_range(n, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
