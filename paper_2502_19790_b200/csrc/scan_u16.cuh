@@ -44,9 +44,11 @@ constexpr int U16_SMEM_LUT_MAX = 16384;
 struct U16Warp {                     // per-warp shared scratch
   uint16_t codes[SEG_LEN];           // the segment's codes, 16-byte chunks swizzled (u16_chunk)
   uint16_t ev[SEG_LEN];              // candidate boundaries (segment offsets < 2048), sample order;
-                                     // pass 1 adds bit 14 (real boundary), bit 15 (starts a record)
-  u32 fsm[SEG_LEN / 32];             // file starts inside the segment (bit = offset)
+                                     // bit 11: a file starts there; pass 1 adds bit 14 (real
+                                     // boundary), bit 15 (starts a record)
 };
+
+constexpr u32 EV_IDX = 0x7ffu, EV_FS = 0x800u;
 
 // physical 16-byte chunk of logical chunk c (8 codes) in U16Warp::codes
 __device__ __forceinline__ int u16_chunk(int c) { return c ^ ((c >> 3) & 7); }
@@ -81,9 +83,15 @@ __global__ void seg_file_kernel(const long long* file_off, int n_files, long lon
   seg_fa[s] = (int)lo;
 }
 
-template <bool SLUT>
-__device__ __forceinline__ u32 u16_key(const u32* s_lut, const u32* g_lut, u32 code) {
-  return SLUT ? s_lut[code] : __ldg(g_lut + code);
+// key of a tuple code: LUT 0 = global u32, 1 = shared u32, 2 = shared u16
+// (packed keys < 2^15: a failing tuple is clamped to 0xffff >= fail_limit --
+// two failing neighbours then compare equal, which never makes a boundary
+// real since neither side passes)
+template <int LUT>
+__device__ __forceinline__ u32 u16_key(const void* s_lut, const u32* g_lut, u32 code) {
+  if (LUT == 2) return reinterpret_cast<const uint16_t*>(s_lut)[code];
+  if (LUT == 1) return reinterpret_cast<const u32*>(s_lut)[code];
+  return __ldg(g_lut + code);
 }
 
 template <int LUT>
@@ -130,20 +138,23 @@ __device__ __forceinline__ u32 change32(u32 prev, const uint4* w) {
   return m;
 }
 
-template <bool SLUT>
+template <int SLUT>
 __global__ void __launch_bounds__(U16_WARPS * 32, 5)
 scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
   extern __shared__ __align__(16) unsigned char u16_dyn[];
   U16Warp* wsm = reinterpret_cast<U16Warp*>(u16_dyn);
-  u32* s_lut = reinterpret_cast<u32*>(u16_dyn + sizeof(U16Warp) * U16_WARPS);
+  void* s_lut = u16_dyn + sizeof(U16Warp) * U16_WARPS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   U16Warp& W = wsm[warp];
   const uint16_t* __restrict__ col = reinterpret_cast<const uint16_t*>(a.cols[0]);
   const u32* __restrict__ g_lut = a.lut_sum + 1;  // entry of code c at c (a tuple column has no null code)
   const u32 lim = a.fail_limit;
   const long long n = a.n;
-  if (SLUT)
-    for (int i = threadIdx.x; i < a.lut_off[1] - 1; i += U16_WARPS * 32) s_lut[i] = g_lut[i];
+  if (SLUT == 1)
+    for (int i = threadIdx.x; i < a.lut_off[1] - 1; i += U16_WARPS * 32) reinterpret_cast<u32*>(s_lut)[i] = g_lut[i];
+  if (SLUT == 2)
+    for (int i = threadIdx.x; i < a.lut_off[1] - 1; i += U16_WARPS * 32)
+      reinterpret_cast<uint16_t*>(s_lut)[i] = (uint16_t)min(g_lut[i], 0xffffu);
   __syncthreads();  // the only CTA barrier: LUT staged
   const long long wstride = (long long)gridDim.x * U16_WARPS;
   long long seg = (long long)blockIdx.x * U16_WARPS + warp;
@@ -189,8 +200,6 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
     const int nf = fa_next - fa;  // file starts in (s0, s0 + 2048] ((s0, n) for the last segment)
     const long long nxt = seg + wstride;
     if (nxt < nseg) fetch(nxt);
-    W.fsm[2 * lane] = 0;
-    W.fsm[2 * lane + 1] = 0;
     __syncwarp();
     // ---- this lane's 64 contiguous samples [64 lane, 64 lane + 64)
     uint4 x[8];
@@ -201,31 +210,44 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
     u32 m0 = change32(lane > 0 ? up : hprev << 16, x);
     u32 m1 = change32(x[3].w, x + 4);
     if (s0 == 0 && lane == 0) m0 |= 1u;  // sample 0: no predecessor
-    // ---- file starts in (s0, s0 + len): bitmask by segment offset
+    // ---- file starts in (s0, s0 + len): this lane's 64-bit mask, 32 starts
+    // per round (one per lane, then broadcast)
     const long long fbase = __ldg(a.file_off + cfa);  // start of the file holding s0
-    if (nf > 0) {
-      for (int k = 1 + lane; k <= nf; k += 32) {
-        const long long p = __ldg(a.file_off + cfa + k) - s0;
-        if (p > 0 && p < len) atomicOr(&W.fsm[p >> 5], 1u << (p & 31));
+    u32 f0 = 0, f1 = 0;
+    for (int k0 = 1; k0 <= nf; k0 += 32) {
+      const int k = k0 + lane;
+      const long long p = k <= nf ? __ldg(a.file_off + cfa + k) - s0 : -1;
+      const int pi = p > 0 && p < len ? (int)p : -1;
+      const int cnt = nf - k0 + 1 < 32 ? nf - k0 + 1 : 32;
+      for (int t = 0; t < cnt; ++t) {
+        const int q = __shfl_sync(MX_FULL, pi, t) - 64 * lane;
+        if (q >= 0 && q < 32) f0 |= 1u << q;
+        else if (q >= 32 && q < 64) f1 |= 1u << (q - 32);
       }
-      __syncwarp();
-      m0 |= W.fsm[2 * lane];
-      m1 |= W.fsm[2 * lane + 1];
     }
     const bool fs0 = s0 > 0 && fbase == s0;  // a file starts at the segment's first sample
-    if (fs0 && lane == 0) m0 |= 1u;
+    if (fs0 && lane == 0) f0 |= 1u;
+    m0 |= f0;
+    m1 |= f1;
     // ---- candidates in sample order (lane-major): one warp scan of the counts
     const u32 cnt = (u32)(__popc(m0) + __popc(m1));
     const u32 incl = warp_incl_scan(cnt);
     const int nev = (int)__shfl_sync(MX_FULL, incl, 31);
     {
       u32 p = incl - cnt;
-      for (u32 c = m0; c; c &= c - 1) W.ev[p++] = (uint16_t)(64 * lane + __ffs(c) - 1);
-      for (u32 c = m1; c; c &= c - 1) W.ev[p++] = (uint16_t)(64 * lane + 32 + __ffs(c) - 1);
+      for (u32 c = m0; c; c &= c - 1) {
+        const int b = __ffs(c) - 1;
+        W.ev[p++] = (uint16_t)(64 * lane + b + (((f0 >> b) & 1u) ? EV_FS : 0u));
+      }
+      for (u32 c = m1; c; c &= c - 1) {
+        const int b = __ffs(c) - 1;
+        W.ev[p++] = (uint16_t)(64 * lane + 32 + b + (((f1 >> b) & 1u) ? EV_FS : 0u));
+      }
     }
     __syncwarp();
     // ---- candidate -> (real boundary, starts a record)
-    auto classify = [&](int idx, bool& real, bool& rec) {
+    auto classify = [&](u32 ev, bool& real, bool& rec) {
+      const int idx = (int)(ev & EV_IDX);
       const u32 kc = u16_key<SLUT>(s_lut, g_lut, u16_code(W, idx));
       const bool pc = kc < lim;
       if (s0 + idx == 0) {
@@ -233,7 +255,7 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
       } else {
         const u32 pre = idx > 0 ? u16_code(W, idx - 1) : hprev;
         const u32 kp = u16_key<SLUT>(s_lut, g_lut, pre);
-        const bool fs = idx == 0 ? fs0 : ((W.fsm[idx >> 5] >> (idx & 31)) & 1u) != 0;
+        const bool fs = (ev & EV_FS) != 0;
         real = (pc || kp < lim) && (fs || kc != kp);
       }
       rec = real && pc;
@@ -277,10 +299,11 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
       // ---- common case: every candidate in registers (two per lane), no
       // shared flags, one pass
       const bool ok0 = lane < nev, ok1 = 32 + lane < nev;
-      const int idx0 = ok0 ? (int)W.ev[lane] : 0, idx1 = ok1 ? (int)W.ev[32 + lane] : 0;
+      const u32 ev0 = ok0 ? (u32)W.ev[lane] : 0u, ev1 = ok1 ? (u32)W.ev[32 + lane] : 0u;
+      const int idx0 = (int)(ev0 & EV_IDX), idx1 = (int)(ev1 & EV_IDX);
       bool real0 = false, rec0 = false, real1 = false, rec1 = false;
-      if (ok0) classify(idx0, real0, rec0);
-      if (ok1) classify(idx1, real1, rec1);
+      if (ok0) classify(ev0, real0, rec0);
+      if (ok1) classify(ev1, real1, rec1);
       const u32 realb0 = __ballot_sync(MX_FULL, real0), recb0 = __ballot_sync(MX_FULL, rec0);
       const u32 realb1 = __ballot_sync(MX_FULL, real1), recb1 = __ballot_sync(MX_FULL, rec1);
       const int r0 = __ffs(realb0) - 1, r1 = __ffs(realb1) - 1;
@@ -305,9 +328,9 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
         const int e = b + lane;
         bool real = false, rec = false;
         if (e < nev) {
-          const int idx = W.ev[e];
-          classify(idx, real, rec);
-          W.ev[e] = (uint16_t)(idx | (real ? 0x4000 : 0) | (rec ? 0x8000 : 0));
+          const u32 ev = W.ev[e];
+          classify(ev, real, rec);
+          W.ev[e] = (uint16_t)(ev | (real ? 0x4000u : 0u) | (rec ? 0x8000u : 0u));
         }
         rtot += (u32)__popc(__ballot_sync(MX_FULL, rec));
       }
@@ -322,7 +345,7 @@ scan_u16_kernel(S1Args a, const int* __restrict__ seg_fa, long long nseg) {
         const bool ok = e < nev;
         const u32 ev = ok ? (u32)W.ev[e] : 0u;
         const u32 fl = ev >> 14;
-        const int idx = (int)(ev & 0x3fffu);
+        const int idx = (int)(ev & EV_IDX);
         const u32 realb = __ballot_sync(MX_FULL, fl & 1u);
         const u32 recb = __ballot_sync(MX_FULL, fl & 2u);
         const u32 after = realb & above;

@@ -496,26 +496,32 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     {
       MxPhase ph("scan_runs", s);
       const int entries = lut_total - 1;
-      const bool slut = entries <= U16_SMEM_LUT_MAX;
-      const size_t dyn = sizeof(U16Warp) * U16_WARPS + (slut ? sizeof(u32) * (size_t)entries : 0);
+      // LUT placement: shared u16 when packed keys fit 15 bits (6 CTAs/SM),
+      // shared u32, or global
+      const int mode = entries > U16_SMEM_LUT_MAX ? 0 : (d->key_bits <= 15 ? 2 : 1);
+      const size_t dyn = sizeof(U16Warp) * U16_WARPS + (mode == 2 ? 2 : mode == 1 ? 4 : 0) * (size_t)entries;
       // attribute + occupancy per (LUT placement, shared bytes), queried once
-      static thread_local size_t q_dyn[2] = {0, 0};
-      static thread_local int q_per_sm[2] = {1, 1};
-      int& per_sm = q_per_sm[slut ? 1 : 0];
-      if (q_dyn[slut ? 1 : 0] != dyn) {
-        if (slut) {
-          MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-          MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<true>, U16_WARPS * 32, dyn));
+      static thread_local size_t q_dyn[3] = {0, 0, 0};
+      static thread_local int q_per_sm[3] = {1, 1, 1};
+      int& per_sm = q_per_sm[mode];
+      if (q_dyn[mode] != dyn) {
+        if (mode == 2) {
+          MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+          MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<2>, U16_WARPS * 32, dyn));
+        } else if (mode == 1) {
+          MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+          MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<1>, U16_WARPS * 32, dyn));
         } else {
-          MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-          MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<false>, U16_WARPS * 32, dyn));
+          MX_CUDA_TRY(cudaFuncSetAttribute(scan_u16_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+          MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_u16_kernel<0>, U16_WARPS * 32, dyn));
         }
-        q_dyn[slut ? 1 : 0] = dyn;
+        q_dyn[mode] = dyn;
       }
       const long long want = (ntiles + U16_WARPS - 1) / U16_WARPS;
       const unsigned grid = (unsigned)std::min<long long>(want, (long long)n_sm * std::max(1, per_sm));
-      if (slut) scan_u16_kernel<true><<<grid, U16_WARPS * 32, dyn, s>>>(a, seg_fa.p, ntiles);
-      else scan_u16_kernel<false><<<grid, U16_WARPS * 32, dyn, s>>>(a, seg_fa.p, ntiles);
+      if (mode == 2) scan_u16_kernel<2><<<grid, U16_WARPS * 32, dyn, s>>>(a, seg_fa.p, ntiles);
+      else if (mode == 1) scan_u16_kernel<1><<<grid, U16_WARPS * 32, dyn, s>>>(a, seg_fa.p, ntiles);
+      else scan_u16_kernel<0><<<grid, U16_WARPS * 32, dyn, s>>>(a, seg_fa.p, ntiles);
       mx_count_launch();
       MX_CUDA_TRY(cudaGetLastError());
     }
