@@ -33,111 +33,143 @@ struct KeyStrView {
   const long long* off;
 };
 
-__global__ void key_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix, int prefix_len, u64* seeds) {
-  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  const u32 packed = v.key_packed[k];
-  long long len = 0;
-  int present = 0;
-  for (int p = 0; p < v.n_props; ++p) {
-    u32 r = (packed >> v.shift[p]) & ((1u << v.width[p]) - 1u);
-    if (r) {
-      long long pc = v.base[p] + r - 1;
-      len += v.off[pc + 1] - v.off[pc] + (present ? 1 : 0);
-      ++present;
+// One THREAD per key (k < K: derive_seed(seed, "cursor", key string) by
+// device BLAKE2b; k == K: the component-order seed from the host), then the
+// key's MT19937 init_by_array chain in shared memory (lane-interleaved rows of
+// 33 words, conflict-free), copied out 32 keys interleaved (mt_state_of).
+constexpr int SEED_THREADS = 32;
+constexpr int SEED_ROW = SEED_THREADS + 1;
+
+__global__ void __launch_bounds__(SEED_THREADS)
+key_mt_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix, int prefix_len, u64 order_seed,
+                   u32* states) {
+  extern __shared__ u32 ks_dyn[];  // [MT_N][SEED_ROW]
+  const int lane = threadIdx.x;
+  const long long k0 = blockIdx.x * (long long)SEED_THREADS, k = k0 + lane;
+  if (k <= K) {
+    u64 seed = order_seed;
+    if (k < K) {
+      const u32 packed = v.key_packed[k];
+      long long len = 0;
+      int present = 0;
+      for (int p = 0; p < v.n_props; ++p) {
+        u32 r = (packed >> v.shift[p]) & ((1u << v.width[p]) - 1u);
+        if (r) {
+          long long pc = v.base[p] + r - 1;
+          len += v.off[pc + 1] - v.off[pc] + (present ? 1 : 0);
+          ++present;
+        }
+      }
+      Blake2b b;
+      b.init();
+      b.bytes(prefix, prefix_len);
+      b.len8((u64)len);
+      present = 0;
+      for (int p = 0; p < v.n_props; ++p) {
+        u32 r = (packed >> v.shift[p]) & ((1u << v.width[p]) - 1u);
+        if (r) {
+          if (present) b.byte(';');
+          long long pc = v.base[p] + r - 1;
+          b.bytes(v.bytes + v.off[pc], v.off[pc + 1] - v.off[pc]);
+          ++present;
+        }
+      }
+      seed = b.seed63();
     }
+    mt_init_by_array(seed, [&](int a) -> u32& { return ks_dyn[a * SEED_ROW + lane]; });
   }
-  Blake2b b;
-  b.init();
-  b.bytes(prefix, prefix_len);
-  b.len8((u64)len);
-  present = 0;
-  for (int p = 0; p < v.n_props; ++p) {
-    u32 r = (packed >> v.shift[p]) & ((1u << v.width[p]) - 1u);
-    if (r) {
-      if (present) b.byte(';');
-      long long pc = v.base[p] + r - 1;
-      b.bytes(v.bytes + v.off[pc], v.off[pc + 1] - v.off[pc]);
-      ++present;
-    }
-  }
-  seeds[k] = b.seed63();
+  __syncwarp();
+  // states of 32 consecutive keys interleaved: word a of key k at
+  // states[((k / 32) * MT_N + a) * 32 + k % 32] (coalesced here)
+  u32* dst = states + (size_t)blockIdx.x * MT_N * SEED_THREADS + lane;
+#pragma unroll 8
+  for (int a = 0; a < MT_N; ++a) dst[(size_t)a * SEED_THREADS] = ks_dyn[a * SEED_ROW + lane];
 }
 
-// Per-warp shared memory: MT state + outputs + window pairs + the key's block
-// list (list_cap entries; a key with more blocks shuffles in global memory).
-// Per-warp shared memory: MT state + outputs + window pairs (CS_FIXED words)
-// and the key's block list as 16-bit offsets from the key's first block
-// (list_cap entries; a key with more blocks shuffles its u32 list in global
-// memory). Half-width entries double the keys resident per SM.
-constexpr int CS_FIXED = 2 * MT_N + 64;
+__device__ __forceinline__ const u32* mt_state_of(const u32* states, long long k) {
+  return states + (size_t)(k / SEED_THREADS) * MT_N * SEED_THREADS + k % SEED_THREADS;
+}
 
-__global__ void __launch_bounds__(128)
+// One WARP per key (grid-stride over warps): the key's seeded MT state loaded
+// from key_mt_seed_kernel into shared memory, the dataset-order shuffle and
+// then every dataset's block shuffle drawn from the same stream
+// (WarpMT::draws, no swaps) and applied in parallel (fy_apply). The draw /
+// bucket scratch of a key with <= cap blocks lives in the warp's shared memory
+// as 16-bit entries (6 B per block); larger keys use the u32 global scratch
+// at the key's block offset (g_*: B entries each).
+constexpr int CS_WARPS = 2;
+constexpr int CS_MT_WORDS = 2 * MT_N;
+constexpr int CS_SMEM_CAP = 16000;
+
+template <typename IT>
+__device__ void cursor_key_shuffle(WarpMT& mt, u32 b0, int nb, int G, const u32* grp, u32* gid, u32* cur_blk, IT* j,
+                                   IT* top, IT* link) {
+  if (G > 1) {  // dataset order (one stream for the whole key)
+    mt.draws(G, j);
+    fy_apply(G, j, top, link, [&](int i, u32 v) { gid[b0 + i] = v; });
+  }
+  // every dataset's draws in the shuffled dataset order, then one apply each
+  int pos = 0;
+  for (int g = 0; g < G; ++g) {
+    const u32 gi = G > 1 ? gid[b0 + g] : 0u;
+    const int s = G > 1 ? (int)grp[b0 + gi] : 0;
+    const int e = G > 1 && gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
+    mt.draws(e - s, j + pos);
+    pos += e - s;
+  }
+  pos = 0;
+  for (int g = 0; g < G; ++g) {
+    const u32 gi = G > 1 ? gid[b0 + g] : 0u;
+    const int s = G > 1 ? (int)grp[b0 + gi] : 0;
+    const int e = G > 1 && gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
+    u32* dst = cur_blk + b0 + pos;
+    const u32 base = b0 + (u32)s;
+    fy_apply(e - s, j + pos, top + pos, link + pos, [&](int i, u32 v) { dst[i] = base + v; });
+    pos += e - s;
+  }
+}
+
+__global__ void __launch_bounds__(CS_WARPS * 32)
 cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file, const int32_t* file_ds,
-                      const u64* seeds, const u32* mt_base, u32* grp, u32* gid, u32* cur_blk, int list_cap) {
+                      const u32* states, u32* grp, u32* gid, u32* cur_blk, int cap, u32* g_j, u32* g_top,
+                      u32* g_link) {
   extern __shared__ __align__(16) u32 cs_dyn[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpc = blockDim.x >> 5;
-  u32* mine = cs_dyn + (size_t)w * (CS_FIXED + list_cap / 2);
-  u32* s_mt = mine;
-  u32* s_out = mine + MT_N;
-  uint2* s_pairs = reinterpret_cast<uint2*>(mine + 2 * MT_N);
-  unsigned short* s_list = reinterpret_cast<unsigned short*>(mine + CS_FIXED);
-  for (long long k = blockIdx.x * (long long)wpc + w; k < K; k += (long long)gridDim.x * wpc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  u32* mine = cs_dyn + (size_t)w * (CS_MT_WORDS + (size_t)cap * 6 / 4);
+  unsigned short* s_j = reinterpret_cast<unsigned short*>(mine + CS_MT_WORDS);
+  unsigned short* s_top = s_j + cap;
+  unsigned short* s_link = s_top + cap;
+  for (long long k = blockIdx.x * (long long)CS_WARPS + w; k < K; k += (long long)gridDim.x * CS_WARPS) {
     const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
     const int nb = (int)(b1 - b0);
-    if (nb <= 1) {  // shuffling one block draws nothing: skip the MT seeding
+    if (nb <= 1) {  // shuffling one block draws nothing
       if (lane == 0 && nb == 1) cur_blk[b0] = b0;
       continue;
     }
-    const bool in_smem = nb <= list_cap;
     // dataset groups (blocks are file-sorted and ds is nondecreasing in file
     // order): one group when first and last block share a dataset, else a
     // warp-parallel scan of dataset changes
-    const bool one_ds = nb == 0 || file_ds[blk_file[b0]] == file_ds[blk_file[b1 - 1]];
     int G = 1;
-    if (!one_ds) {
+    if (file_ds[blk_file[b0]] != file_ds[blk_file[b1 - 1]]) {
       G = 0;
       for (int b = 0; b < nb; b += 32) {
         const int i = b + lane;
-        bool head = false;
-        if (i < nb) head = i == 0 || file_ds[blk_file[b0 + i]] != file_ds[blk_file[b0 + i - 1]];
-        const u32 hm = __ballot_sync(MX_FULL, head);
-        if (head) {
-          const int gi = G + __popc(hm & ((1u << lane) - 1));
-          grp[b0 + gi] = (u32)i;
-          gid[b0 + gi] = (u32)gi;
-        }
+        bool hd = false;
+        if (i < nb) hd = i == 0 || file_ds[blk_file[b0 + i]] != file_ds[blk_file[b0 + i - 1]];
+        const u32 hm = __ballot_sync(MX_FULL, hd);
+        if (hd) grp[b0 + G + __popc(hm & ((1u << lane) - 1))] = (u32)i;
         G += __popc(hm);
       }
-    } else if (lane == 0) {
-      grp[b0] = 0;
-      gid[b0] = 0;
     }
+    WarpMT mt{mine, mine + MT_N, MT_N};
+    const u32* st = mt_state_of(states, k);
+#pragma unroll 4
+    for (int a = lane; a < MT_N; a += 32) mine[a] = st[(size_t)a * SEED_THREADS];
     __syncwarp();
-    WarpMT mt{s_mt, s_out, s_pairs, MT_N};
-    mt.seed(mt_base, seeds[k]);
-    mt.shuffle(gid + b0, G);  // dataset order (one stream for the whole key)
-    int pos = 0;
-    for (int g = 0; g < G; ++g) {
-      const u32 gi = gid[b0 + g];
-      const int s = (int)grp[b0 + gi];
-      const int e = gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
-      // the dataset's blocks in file order, then shuffled (file order within
-      // the dataset, index.py:140-143)
-      if (in_smem) {
-        for (int b = s + lane; b < e; b += 32) s_list[pos + b - s] = (unsigned short)b;
-        __syncwarp();
-        mt.shuffle(s_list + pos, e - s);
-      } else {
-        for (int b = s + lane; b < e; b += 32) cur_blk[b0 + pos + b - s] = b0 + (u32)b;
-        __syncwarp();
-        mt.shuffle(cur_blk + b0 + pos, e - s);
-      }
-      pos += e - s;
-    }
-    __syncwarp();
-    if (in_smem)
-      for (int i = lane; i < nb; i += 32) cur_blk[b0 + i] = b0 + s_list[i];
+    if (nb <= cap)
+      cursor_key_shuffle<unsigned short>(mt, b0, nb, G, grp, gid, cur_blk, s_j, s_top, s_link);
+    else
+      cursor_key_shuffle<u32>(mt, b0, nb, G, grp, gid, cur_blk, g_j + b0, g_top + b0, g_link + b0);
     __syncwarp();
   }
 }
@@ -184,6 +216,44 @@ struct CumPermF {
   __device__ void total(u64) const {}
 };
 
+// Both layouts in ONE scan over the cursor's blocks when the index holds
+// < 2^32 samples: the value of block position p packs (intervals << 32 |
+// samples) of block cur_blk[p], so the exclusive prefix gives the block's
+// first cursor position and its sample offset at once (sums never carry).
+struct CursorF {
+  const u32* cur_blk;
+  const u32* blk_first;
+  const u64* iv_cum;
+  const u32* start;
+  const u32* end;
+  const u32* file;
+  u32* civ;
+  u64* cum;
+  u32* cfile;
+  u32* cstart;
+  __device__ u64 value(long long p) const {
+    const u32 b = cur_blk[p];
+    const u32 f0 = blk_first[b], f1 = blk_first[b + 1];
+    return ((u64)(f1 - f0) << 32) | (iv_cum[f1] - iv_cum[f0]);
+  }
+  __device__ void apply(long long p, u64 ex, u64) const {
+    const u32 b = cur_blk[p];
+    const u32 f0 = blk_first[b], f1 = blk_first[b + 1];
+    const u64 pos = ex >> 32;
+    u64 samp = ex & 0xffffffffull;
+    if (p == 0) cum[0] = 0;
+    for (u32 t = 0; t < f1 - f0; ++t) {
+      const u32 iv = f0 + t, a = start[iv];
+      civ[pos + t] = iv;
+      cfile[pos + t] = file[iv];
+      cstart[pos + t] = a;
+      samp += end[iv] - a;
+      cum[pos + t + 1] = samp;
+    }
+  }
+  __device__ void total(u64) const {}
+};
+
 __global__ void comp_total_kernel(long long K, const u32* key_blk_first, const u32* blk_first, const u64* iv_cum,
                                   u64* total) {
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -191,27 +261,28 @@ __global__ void comp_total_kernel(long long K, const u32* key_blk_first, const u
   total[k] = iv_cum[blk_first[key_blk_first[k + 1]]] - iv_cum[blk_first[key_blk_first[k]]];
 }
 
-constexpr int CO_SMEM = 8192;
+// one warp: the shuffle of the K component ranks (chunks.py:139-141) from the
+// seeded state key_mt_seed_kernel wrote at entry K; 16-bit scratch in shared
+// memory up to CO_SMEM ranks, else u32 global scratch
+constexpr int CO_SMEM = 16384;
 
-// one warp: shuffle of the K component ranks (chunks.py:139-141)
-__global__ void __launch_bounds__(32) component_order_kernel(long long K, u64 seed, const u32* mt_base, u32* order) {
-  __shared__ u32 s_mt[MT_N], s_out[MT_N];
-  __shared__ uint2 s_pairs[32];
-  __shared__ u32 s_ord[CO_SMEM];
-  const int lane = threadIdx.x;
-  const bool in_smem = K <= CO_SMEM;
-  for (long long i = lane; i < K; i += 32) {
-    if (in_smem) s_ord[i] = (u32)i;
-    else order[i] = (u32)i;
-  }
+__global__ void __launch_bounds__(32) component_order_kernel(long long K, const u32* states, u32* order, u32* g_j,
+                                                           u32* g_top, u32* g_link) {
+  extern __shared__ __align__(16) u32 co_dyn[];
+  const int n = (int)K, lane = threadIdx.x;
+  WarpMT mt{co_dyn, co_dyn + MT_N, MT_N};
+  const u32* st = mt_state_of(states, K);
+#pragma unroll 4
+  for (int a = lane; a < MT_N; a += 32) co_dyn[a] = st[(size_t)a * SEED_THREADS];
   __syncwarp();
-  WarpMT mt{s_mt, s_out, s_pairs, MT_N};
-  mt.seed(mt_base, seed);
-  if (in_smem) {
-    mt.shuffle(s_ord, (int)K);
-    for (long long i = lane; i < K; i += 32) order[i] = s_ord[i];
+  auto out = [&](int i, u32 v) { order[i] = v; };
+  if (n <= CO_SMEM) {
+    unsigned short* s_j = reinterpret_cast<unsigned short*>(co_dyn + CS_MT_WORDS);
+    mt.draws(n, s_j);
+    fy_apply(n, s_j, s_j + n, s_j + 2 * n, out);
   } else {
-    mt.shuffle(order, (int)K);
+    mt.draws(n, g_j);
+    fy_apply(n, g_j, g_top, g_link, out);
   }
 }
 
@@ -234,30 +305,16 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   mx_count_launch();
   // the component-order shuffle (one sequential Fisher-Yates over K ranks)
   // runs on a side stream, overlapped with the per-key cursor shuffles
-  static thread_local uint32_t h_base[MT_N];
-  if (h_base[0] != 19650218u) mt_base_table(h_base);
-  DevBuf<u32> mt_base;  // constant table: uploaded into the stream's workspace once
-  {
-    static thread_local std::map<cudaStream_t, u32*> uploaded;
-    MX_CUDA_TRY(ws_borrow(mt_base, s, WS_MTBASE, MT_N));
-    if (uploaded[s] != mt_base.p) {
-      MX_CUDA_TRY(mx_h2d(mt_base.p, h_base, sizeof(h_base), s));
-      uploaded[s] = mt_base.p;
-    }
-  }
   MX_CUDA_TRY(g->comp_order.alloc(K, s));
   MX_CUDA_TRY(cudaEventRecord(g->ev_tot, s));
-  MX_CUDA_TRY(cudaStreamWaitEvent(g->ostream, g->ev_tot, 0));
   mx_host_mark("cursor prologue");
-  component_order_kernel<<<1, 32, 0, g->ostream>>>(K, order_seed, mt_base.p, g->comp_order.p);
-  mx_count_launch();
-  MX_CUDA_TRY(cudaEventRecord(g->ev_order, g->ostream));
+  // every key's cursor seed + seeded MT state, and the component order's (K)
   DevBuf<uint8_t> pre;
-  DevBuf<u64> seeds;
+  DevBuf<u32> states;
   MX_CUDA_TRY(ws_borrow(pre, s, WS_CPRE, prefix_len > 0 ? prefix_len : 1));
   if (prefix_len > 0)
     MX_CUDA_TRY(mx_h2d(pre.p, cursor_prefix, prefix_len, s));
-  MX_CUDA_TRY(ws_borrow(seeds, s, WS_CSEED, K));
+  MX_CUDA_TRY(ws_borrow(states, s, WS_CSEED, (K + 1 + SEED_THREADS) / SEED_THREADS * SEED_THREADS * MT_N));
   KeyStrView v{};
   v.key_packed = ix->key_packed.p;
   v.n_props = ix->n_props;
@@ -268,35 +325,76 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   }
   v.bytes = ix->str_bytes.p;
   v.off = ix->str_off.p;
-  key_seed_kernel<<<(unsigned)((K + 127) / 128), 128, 0, s>>>(v, K, pre.p, prefix_len, seeds.p);
-  mx_count_launch();
+  {
+    const size_t dyn = sizeof(u32) * MT_N * SEED_ROW;
+    MX_CUDA_TRY(cudaFuncSetAttribute(key_mt_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    key_mt_seed_kernel<<<(unsigned)((K + 1 + SEED_THREADS - 1) / SEED_THREADS), SEED_THREADS, dyn, s>>>(
+        v, K, pre.p, prefix_len, order_seed, states.p);
+    mx_count_launch();
+  }
+  // the component-order shuffle runs on a side stream, overlapped with the
+  // per-key cursor shuffles
+  MX_CUDA_TRY(cudaEventRecord(g->ev_fork, s));
+  MX_CUDA_TRY(cudaStreamWaitEvent(g->ostream, g->ev_fork, 0));
+  {
+    DevBuf<u32> fj, ft, fl;  // global scratch only beyond CO_SMEM ranks
+    const long long gn = K > CO_SMEM ? K : 1;
+    MX_CUDA_TRY(ws_borrow(fj, g->ostream, WS_FYJ, gn));
+    MX_CUDA_TRY(ws_borrow(ft, g->ostream, WS_FYTOP, gn));
+    MX_CUDA_TRY(ws_borrow(fl, g->ostream, WS_FYLINK, gn));
+    const size_t dyn = sizeof(u32) * CS_MT_WORDS + (K <= CO_SMEM ? 6 * (size_t)K : 0);
+    MX_CUDA_TRY(cudaFuncSetAttribute(component_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    component_order_kernel<<<1, 32, dyn, g->ostream>>>(K, states.p, g->comp_order.p, fj.p, ft.p, fl.p);
+    mx_count_launch();
+  }
+  MX_CUDA_TRY(cudaEventRecord(g->ev_order, g->ostream));
   DevBuf<u32> grp, gid;
   MX_CUDA_TRY(ws_borrow(grp, s, WS_CGRP, B));
   MX_CUDA_TRY(ws_borrow(gid, s, WS_CGID, B));
   MX_CUDA_TRY(g->cur_blk.alloc(B, s));
   {
     MxPhase ph2("cursor_shuffle", s);
-    // list capacity = the largest key's block count (up to 16K entries, 64 KB)
-    const int cap = (int)std::min<long long>((ix->max_key_blocks + 63) / 64 * 64, 32768);
-    const size_t per_warp = sizeof(u32) * CS_FIXED + sizeof(unsigned short) * cap;
-    const int wpc = per_warp <= 12 * 1024 ? 4 : 1;
-    const size_t dyn = per_warp * wpc;
+    // keys with <= cap blocks keep their scratch in shared memory (6 B per
+    // block); larger keys use the u32 global scratch
+    const long long mkb = ix->max_key_blocks;
+    const int cap = (int)std::min<long long>((mkb + 63) / 64 * 64, CS_SMEM_CAP);
+    DevBuf<u32> fj, ft, fl;
+    const long long gn = mkb > cap ? B : 1;
+    MX_CUDA_TRY(ws_borrow(fj, s, WS_FYJ, gn));
+    MX_CUDA_TRY(ws_borrow(ft, s, WS_FYTOP, gn));
+    MX_CUDA_TRY(ws_borrow(fl, s, WS_FYLINK, gn));
+    const size_t dyn = ((size_t)CS_MT_WORDS * 4 + (size_t)cap * 6) * CS_WARPS;
     MX_CUDA_TRY(cudaFuncSetAttribute(cursor_shuffle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    long long blocks = (K + wpc - 1) / wpc;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    cursor_shuffle_kernel<<<(unsigned)blocks, wpc * 32, dyn, s>>>(K, ix->key_blk_first.p, ix->blk_file.p,
-                                                                ix->file_ds.p, seeds.p, mt_base.p, grp.p, gid.p,
-                                                                g->cur_blk.p, cap);
+    static thread_local std::map<size_t, int> occ;  // smem -> resident CTAs per SM
+    static thread_local int n_sm = 0;
+    if (!n_sm) {
+      int dev = 0;
+      MX_CUDA_TRY(cudaGetDevice(&dev));
+      MX_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    int& per_sm = occ[dyn];
+    if (!per_sm)
+      MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cursor_shuffle_kernel, CS_WARPS * 32, dyn));
+    const long long blocks = std::min<long long>((K + CS_WARPS - 1) / CS_WARPS, (long long)std::max(per_sm, 1) * n_sm);
+    cursor_shuffle_kernel<<<(unsigned)blocks, CS_WARPS * 32, dyn, s>>>(K, ix->key_blk_first.p, ix->blk_file.p,
+                                                                     ix->file_ds.p, states.p, grp.p, gid.p,
+                                                                     g->cur_blk.p, cap, fj.p, ft.p, fl.p);
     mx_count_launch();
   }
   MX_CUDA_TRY(g->civ.alloc(I, s));
-  if (int rc = gs_run(B, CursorIvF{g->cur_blk.p, ix->blk_first.p, g->civ.p}, s)) return rc;
   MX_CUDA_TRY(g->ccum.alloc(I + 1, s));
   MX_CUDA_TRY(g->cfile.alloc(I, s));
   MX_CUDA_TRY(g->cstart.alloc(I, s));
-  if (int rc = gs_run(I, CumPermF{g->civ.p, ix->iv_start.p, ix->iv_end.p, g->ccum.p, ix->iv_file.p, g->cfile.p,
-                                   g->cstart.p}, s))
-    return rc;
+  if (ix->indexed_samples < (1ll << 32) && I < (1ll << 31)) {  // resolved sizes (ix_resolve)
+    if (int rc = gs_run(B, CursorF{g->cur_blk.p, ix->blk_first.p, ix->iv_cum.p, ix->iv_start.p, ix->iv_end.p,
+                                   ix->iv_file.p, g->civ.p, g->ccum.p, g->cfile.p, g->cstart.p}, s))
+      return rc;
+  } else {  // >= 2^32 samples: positions first, then the 64-bit sample prefix
+    if (int rc = gs_run(B, CursorIvF{g->cur_blk.p, ix->blk_first.p, g->civ.p}, s)) return rc;
+    if (int rc = gs_run(I, CumPermF{g->civ.p, ix->iv_start.p, ix->iv_end.p, g->ccum.p, ix->iv_file.p, g->cfile.p,
+                                     g->cstart.p}, s))
+      return rc;
+  }
   if (int rc = gen_local_lists(g, s)) return rc;  // sharded index: this rank's cursor positions
   MX_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_order, 0));
   g->fresh_layout = true;

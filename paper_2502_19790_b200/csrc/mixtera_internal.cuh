@@ -77,7 +77,8 @@ struct DevBuf {
 // critical path before the first kernel. Buffers are reused in stream order;
 // a view must never outlive the call that borrowed it.
 enum WsSlot { WS_TCNT, WS_TOPEN, WS_THEAD, WS_DEFER, WS_RK, WS_RF, WS_RS, WS_RE, WS_SEGFA, WS_SCR64, WS_ERR,
-              WS_HIST, WS_DTOT, WS_TOFF, WS_GSAGG, WS_CPRE, WS_CSEED, WS_CGRP, WS_CGID, WS_MTBASE,
+              WS_HIST, WS_DTOT, WS_TOFF, WS_GSAGG, WS_CPRE, WS_CSEED, WS_CGRP, WS_CGID,
+              WS_FYJ, WS_FYTOP, WS_FYLINK,  // cursor / component-order shuffle scratch
               WS_GEN,            // + GenData scratch slot (24 of them)
               WS_N = WS_GEN + 24 };
 // `s` keys the workspace (a call's stream: work on it is ordered); growth
