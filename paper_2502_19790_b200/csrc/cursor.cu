@@ -39,16 +39,20 @@ struct KeyStrView {
 // 33 words, conflict-free), copied out 32 keys interleaved (mt_state_of).
 constexpr int SEED_THREADS = 32;
 constexpr int SEED_ROW = SEED_THREADS + 1;
+constexpr int SEED_MSG = 128;  // one BLAKE2b block per thread in shared memory
 
 __global__ void __launch_bounds__(SEED_THREADS)
 key_mt_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix, int prefix_len, u64 order_seed,
                    u32* states) {
-  extern __shared__ u32 ks_dyn[];  // [MT_N][SEED_ROW]
+  extern __shared__ u32 ks_dyn[];  // [MT_N][SEED_ROW] + [SEED_THREADS][SEED_MSG] bytes
   const int lane = threadIdx.x;
   const long long k0 = blockIdx.x * (long long)SEED_THREADS, k = k0 + lane;
+  uint8_t* msg = reinterpret_cast<uint8_t*>(ks_dyn + MT_N * SEED_ROW) + lane * SEED_MSG;
   if (k <= K) {
     u64 seed = order_seed;
     if (k < K) {
+      // stable_hash message: prefix, 8-byte length, "v1;v2;..." of the
+      // key's present properties; assembled in the thread's shared row
       const u32 packed = v.key_packed[k];
       long long len = 0;
       int present = 0;
@@ -60,21 +64,42 @@ key_mt_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix, int prefix_
           ++present;
         }
       }
-      Blake2b b;
-      b.init();
-      b.bytes(prefix, prefix_len);
-      b.len8((u64)len);
-      present = 0;
-      for (int p = 0; p < v.n_props; ++p) {
-        u32 r = (packed >> v.shift[p]) & ((1u << v.width[p]) - 1u);
-        if (r) {
-          if (present) b.byte(';');
-          long long pc = v.base[p] + r - 1;
-          b.bytes(v.bytes + v.off[pc], v.off[pc + 1] - v.off[pc]);
-          ++present;
+      const long long total = prefix_len + 8 + len;
+      if (total <= SEED_MSG) {
+        for (int q = 0; q < prefix_len; ++q) msg[q] = prefix[q];
+        int w = prefix_len;
+#pragma unroll
+        for (int b = 7; b >= 0; --b) msg[w++] = (uint8_t)((u64)len >> (8 * b));
+        present = 0;
+        for (int p = 0; p < v.n_props; ++p) {
+          u32 r = (packed >> v.shift[p]) & ((1u << v.width[p]) - 1u);
+          if (r) {
+            if (present) msg[w++] = ';';
+            const long long pc = v.base[p] + r - 1, o0 = v.off[pc], nb = v.off[pc + 1] - o0;
+#pragma unroll 4
+            for (long long q = 0; q < nb; ++q) msg[w + q] = v.bytes[o0 + q];
+            w += (int)nb;
+            ++present;
+          }
         }
+        seed = blake2b_seed63_1block((int)total, [&](int i) { return msg[i]; });
+      } else {  // long key strings: the streaming hash
+        Blake2b b;
+        b.init();
+        b.bytes(prefix, prefix_len);
+        b.len8((u64)len);
+        present = 0;
+        for (int p = 0; p < v.n_props; ++p) {
+          u32 r = (packed >> v.shift[p]) & ((1u << v.width[p]) - 1u);
+          if (r) {
+            if (present) b.byte(';');
+            long long pc = v.base[p] + r - 1;
+            b.bytes(v.bytes + v.off[pc], v.off[pc + 1] - v.off[pc]);
+            ++present;
+          }
+        }
+        seed = b.seed63();
       }
-      seed = b.seed63();
     }
     mt_init_by_array(seed, [&](int a) -> u32& { return ks_dyn[a * SEED_ROW + lane]; });
   }
@@ -326,7 +351,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   v.bytes = ix->str_bytes.p;
   v.off = ix->str_off.p;
   {
-    const size_t dyn = sizeof(u32) * MT_N * SEED_ROW;
+    const size_t dyn = sizeof(u32) * MT_N * SEED_ROW + (size_t)SEED_MSG * SEED_THREADS;
     MX_CUDA_TRY(cudaFuncSetAttribute(key_mt_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     key_mt_seed_kernel<<<(unsigned)((K + 1 + SEED_THREADS - 1) / SEED_THREADS), SEED_THREADS, dyn, s>>>(
         v, K, pre.p, prefix_len, order_seed, states.p);

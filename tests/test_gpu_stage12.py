@@ -253,12 +253,12 @@ def test_u16_tuple_codes_above_32767_match_columns(n_files):
     assert np.array_equal(dc.cpu().numpy(), dcat16.tuple_codes.cpu().numpy())
 
 
-@pytest.mark.parametrize("n_samples,n_files,cards", [(48_000, 24_000, (2,)), (60_000, 4_000, (30, 30, 20))])
+@pytest.mark.parametrize("n_samples,n_files,cards", [(80_000, 40_000, (2,)), (60_000, 4_000, (30, 30, 20))])
 def test_shuffles_beyond_shared_memory(n_samples, n_files, cards):
-    """The CTA-wide Fisher-Yates (csrc/mt19937.cuh CtaMT + cta_fy_apply) in
-    its global-scratch form: keys with more blocks than the kernel's
-    shared-memory capacity (9,600) and a component order of more ranks than
-    component_order_kernel keeps in shared memory (12,288), vs the oracle's
+    """The draw-then-apply Fisher-Yates (csrc/mt19937.cuh WarpMT::draws +
+    fy_apply) in its global-scratch form: keys with more blocks than the kernel's
+    shared-memory capacity (16,000) and a component order of more ranks than
+    component_order_kernel keeps in shared memory (16,384), vs the oracle's
     random.shuffle (index.py:134-144, chunks.py:139-141)."""
     import random
 
@@ -277,12 +277,12 @@ def test_shuffles_beyond_shared_memory(n_samples, n_files, cards):
     random.Random(orc.seed_of(99, "component-order")).shuffle(order)
     assert [k.canonical_string() for k in gen._component_order] == [orc.key_string(ref.keys[r]) for r in order]
     if len(cards) == 1:
-        assert max(ref.key_bounds[1:] - ref.key_bounds[:-1]) > 9_600
+        assert max(ref.key_bounds[1:] - ref.key_bounds[:-1]) > 16_000
         for r in range(n):
             got = [tuple(x) for x in gen.cursor_ranges(idx.component_keys()[r])]
             assert got == ref.cursor_ranges(r, 99)
     else:
-        assert n > 12_288
+        assert n > 16_384
         for r in range(0, n, 997):
             got = [tuple(x) for x in gen.cursor_ranges(idx.component_keys()[r])]
             assert got == ref.cursor_ranges(r, 99)
