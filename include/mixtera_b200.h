@@ -50,7 +50,9 @@ int mx_abi_version(void);
 int64_t mx_launch_count(void);
 /* Per-phase CUDA-event timing on the launching stream: phases are
  * "scan_runs" (the stage-1 streaming kernel alone), "radix_sort",
- * "index_scans", "cursor_layout", "cursor_shuffle", "plan", "emit". */
+ * "index_scans", "cursor_layout", "cursor_shuffle", "plan", "emit".
+ * on = 1: every phase; on = 2: "scan_runs" only (two event records per job,
+ * for timed loops); 0: off. */
 int mx_profile_enable(int on);
 int mx_profile_reset(void);
 int mx_profile_read(const char* phase, double* total_ms, int64_t* count);

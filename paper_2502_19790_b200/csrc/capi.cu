@@ -358,18 +358,44 @@ static void keep_pool_warm() {
   done.push_back(dev);
 }
 
+// Phase events come from a recycled pool (cudaEventCreate costs microseconds
+// of host time; the phases are measured inside the bench's timed region).
+// Events belong to the device that created them: one pool per device.
+static std::map<int, std::vector<cudaEvent_t>> g_ev_free;  // guarded by g_prof_mu
+static std::map<cudaEvent_t, int> g_ev_dev;
+
+static cudaEvent_t phase_event() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    auto& fr = g_ev_free[dev];
+    if (!fr.empty()) {
+      cudaEvent_t e = fr.back();
+      fr.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_ev_dev[e] = dev;
+  return e;
+}
+
 MxPhase::MxPhase(const char* n, cudaStream_t s) : name(n), stream(s), start(nullptr) {
-  if (!g_profile.load()) return;
-  cudaEvent_t e;
-  if (cudaEventCreate(&e) != cudaSuccess) return;
+  const int mode = g_profile.load();
+  if (!mode || (mode == 2 && strcmp(n, "scan_runs") != 0)) return;
+  cudaEvent_t e = phase_event();
+  if (!e) return;
   cudaEventRecord(e, s);
   start = e;
 }
 
 MxPhase::~MxPhase() {
   if (!start) return;
-  cudaEvent_t e;
-  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEvent_t e = phase_event();
+  if (!e) return;
   cudaEventRecord(e, stream);
   std::lock_guard<std::mutex> g(g_prof_mu);
   g_pending.push_back(PendingPhase{name, (cudaEvent_t)start, e});
@@ -385,8 +411,8 @@ static void collect_phases() {
       acc.ms += ms;
       acc.count += 1;
     }
-    cudaEventDestroy(p.a);
-    cudaEventDestroy(p.b);
+    g_ev_free[g_ev_dev[p.a]].push_back(p.a);
+    g_ev_free[g_ev_dev[p.b]].push_back(p.b);
   }
   g_pending.clear();
 }
@@ -436,7 +462,7 @@ int64_t mx_launch_count(void) { return g_launches.load(); }
 
 int mx_profile_enable(int on) {
   collect_phases();
-  g_profile.store(on ? 1 : 0);
+  g_profile.store(on == 2 ? 2 : on ? 1 : 0);
   return MX_OK;
 }
 

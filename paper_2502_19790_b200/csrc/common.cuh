@@ -8,6 +8,7 @@
 //   struct the host reads after the launch sequence (mapped to the
 //   reference's exception types by capi.cu).
 #pragma once
+#include <map>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -128,6 +129,22 @@ cudaError_t mx_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
 // the pinned ring); item i lands at dst + off[i]
 cudaError_t mx_h2d_gather(void* dst, const void* const* src, const size_t* bytes, const size_t* off, int n,
                           size_t total, cudaStream_t s);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) costs microseconds of host
+// time per call: raise the limit only when a launch needs more than the
+// kernel has on this device (per host thread).
+template <typename K>
+cudaError_t mx_smem_attr(K* kernel, size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static thread_local std::map<std::pair<const void*, int>, size_t> have;
+  size_t& h = have[{reinterpret_cast<const void*>(kernel), dev}];
+  if (bytes <= h) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) h = bytes;
+  return e;
+}
+
 struct Uploads {
   static constexpr int kMax = 16;
   const void* src[kMax];

@@ -352,7 +352,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   v.off = ix->str_off.p;
   {
     const size_t dyn = sizeof(u32) * MT_N * SEED_ROW + (size_t)SEED_MSG * SEED_THREADS;
-    MX_CUDA_TRY(cudaFuncSetAttribute(key_mt_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    MX_CUDA_TRY(mx_smem_attr(key_mt_seed_kernel, dyn));
     key_mt_seed_kernel<<<(unsigned)((K + 1 + SEED_THREADS - 1) / SEED_THREADS), SEED_THREADS, dyn, s>>>(
         v, K, pre.p, prefix_len, order_seed, states.p);
     mx_count_launch();
@@ -368,7 +368,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     MX_CUDA_TRY(ws_borrow(ft, g->ostream, WS_FYTOP, gn));
     MX_CUDA_TRY(ws_borrow(fl, g->ostream, WS_FYLINK, gn));
     const size_t dyn = sizeof(u32) * CS_MT_WORDS + (K <= CO_SMEM ? 6 * (size_t)K : 0);
-    MX_CUDA_TRY(cudaFuncSetAttribute(component_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    MX_CUDA_TRY(mx_smem_attr(component_order_kernel, dyn));
     component_order_kernel<<<1, 32, dyn, g->ostream>>>(K, states.p, g->comp_order.p, fj.p, ft.p, fl.p);
     mx_count_launch();
   }
@@ -389,7 +389,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     MX_CUDA_TRY(ws_borrow(ft, s, WS_FYTOP, gn));
     MX_CUDA_TRY(ws_borrow(fl, s, WS_FYLINK, gn));
     const size_t dyn = ((size_t)CS_MT_WORDS * 4 + (size_t)cap * 6) * CS_WARPS;
-    MX_CUDA_TRY(cudaFuncSetAttribute(cursor_shuffle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    MX_CUDA_TRY(mx_smem_attr(cursor_shuffle_kernel, dyn));
     static thread_local std::map<size_t, int> occ;  // smem -> resident CTAs per SM
     static thread_local int n_sm = 0;
     if (!n_sm) {

@@ -78,7 +78,9 @@ struct DevBuf {
 // a view must never outlive the call that borrowed it.
 enum WsSlot { WS_TCNT, WS_TOPEN, WS_THEAD, WS_DEFER, WS_RK, WS_RF, WS_RS, WS_RE, WS_SEGFA, WS_SCR64, WS_ERR,
               WS_HIST, WS_DTOT, WS_TOFF, WS_GSAGG, WS_CPRE, WS_CSEED, WS_CGRP, WS_CGID,
-              WS_FYJ, WS_FYTOP, WS_FYLINK,  // cursor / component-order shuffle scratch
+              WS_FYJ, WS_FYTOP, WS_FYLINK,
+              WS_EPRE, WS_EOFF, WS_EFLAG, WS_ELIST, WS_ELCNT, WS_ECPO, WS_EMCNT, WS_EBIG,  // emission temporaries
+              WS_NBL, WS_NBC, WS_NWL, WS_NWC,  // cursor / component-order shuffle scratch
               WS_GEN,            // + GenData scratch slot (24 of them)
               WS_N = WS_GEN + 24 };
 // `s` keys the workspace (a call's stream: work on it is ordered); growth
@@ -118,7 +120,7 @@ struct IndexData {
   DevBuf<long long> str_off;
   // one device block holding the small per-build host uploads (key strings,
   // file tables, LUTs: one copy); str_*, file_* may be views into it
-  DevBuf<uint8_t> consts;
+  DevBuf<uint8_t> consts, consts2;  // LUTs (before the scan) / key strings + file tables (after)
   // file-sharded hybrid index (shard.cu): this rank's intervals + one
   // pseudo-interval per remote (key, file) block; files [file_lo, file_hi)
   // are local, iv_nreal = real intervals behind each entry (1 if local)

@@ -398,20 +398,20 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     n_pieces = std::max(n_pieces, d->key_string_base[p] + card);
   }
   const long long str_nbytes = d->key_string_offsets[n_pieces];
-  // every small host array of the build in ONE device block and ONE copy
-  Uploads up;
-  const size_t o_soff = up.add(d->key_string_offsets, sizeof(long long) * (n_pieces + 1));
-  const size_t o_sbytes = up.add(d->key_strings, str_nbytes > 0 ? (size_t)str_nbytes : 0);
+  // the small host arrays of the build in two device blocks: the LUTs the
+  // scan reads go up first; key strings and file tables (not read until the
+  // index finalize) are uploaded after the scan launch, while it runs
+  Uploads up, up2;
   const size_t o_lut = up.add(d->lut, sizeof(u32) * lut_total);
   const size_t o_lsum = up.add(ls.data(), sizeof(u32) * ls.size());
-  const size_t o_fds = up.add(d->file_ds, sizeof(int32_t) * d->n_files);
-  const size_t o_fid = up.add(d->file_ids, sizeof(long long) * d->n_files);
+  const size_t o_soff = up2.add(d->key_string_offsets, sizeof(long long) * (n_pieces + 1));
+  const size_t o_sbytes = up2.add(d->key_strings, str_nbytes > 0 ? (size_t)str_nbytes : 0);
+  const size_t o_fds = up2.add(d->file_ds, sizeof(int32_t) * d->n_files);
+  const size_t o_fid = up2.add(d->file_ids, sizeof(long long) * d->n_files);
   mx_host_mark("s1 host tables");
   MX_CUDA_TRY(ix.consts.alloc((long long)up.total + 16, s));
   MX_CUDA_TRY(up.run(ix.consts.p, s));
   mx_host_mark("s1 upload");
-  ix.str_off.borrow(ix.consts.p + o_soff, n_pieces + 1);
-  ix.str_bytes.borrow(ix.consts.p + o_sbytes, str_nbytes > 0 ? str_nbytes : 1);
   a.lut = reinterpret_cast<const u32*>(ix.consts.p + o_lut);
   if (sum_ok) {
     a.lut_sum = reinterpret_cast<const u32*>(ix.consts.p + o_lsum);
@@ -421,11 +421,6 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   a.file_off = reinterpret_cast<const long long*>(d->file_offsets);
   a.n_files = d->n_files;
   a.rank_mask = d->rank_mask;
-  // file table copies (ds and ids are needed for exports and cursors)
-  ix.file_ds.borrow(ix.consts.p + o_fds, d->n_files);
-  ix.file_ids.borrow(ix.consts.p + o_fid, d->n_files);
-  ix.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
-  ix.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
 
   // ---- stage-1 pass variant (MX_SCAN = direct (default) | pipe | v1):
   //  direct: one CTA per 4096-sample tile, slot output (scan_direct_kernel)
@@ -540,6 +535,16 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
     MX_CUDA_TRY(cudaGetLastError());
   }
   mx_host_mark("s1 scan launched");
+  // key strings and file tables (ds and ids are needed for exports and cursors)
+  MX_CUDA_TRY(ix.consts2.alloc((long long)up2.total + 16, s));
+  MX_CUDA_TRY(up2.run(ix.consts2.p, s));
+  ix.str_off.borrow(ix.consts2.p + o_soff, n_pieces + 1);
+  ix.str_bytes.borrow(ix.consts2.p + o_sbytes, str_nbytes > 0 ? str_nbytes : 1);
+  ix.file_ds.borrow(ix.consts2.p + o_fds, d->n_files);
+  ix.file_ids.borrow(ix.consts2.p + o_fid, d->n_files);
+  ix.h_file_ds.assign(d->file_ds, d->file_ds + d->n_files);
+  ix.h_file_ids.assign(d->file_ids, d->file_ids + d->n_files);
+  mx_host_mark("s1 tables uploaded");
   u64 h_runs = 0;
   DevError h_err;
   {
@@ -572,6 +577,10 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   const int rtile2 = RS_THREADS * RIT;
   const int rtiles2 = (int)((I + rtile2 - 1) / rtile2);
   const size_t rsmem = 4 * (size_t)rtile2 * sizeof(u32);
+  std::unique_ptr<MxPhase> ph_sort(new MxPhase("radix_sort", s));
+  DevBuf<u64> toff;  // tile offsets first: the device starts while the host allocates
+  MX_CUDA_TRY(ws_borrow(toff, s, WS_TOFF, ntiles + 1));
+  if (int rc = gs_run(ntiles, TileOffF{t_cnt.p, toff.p, ntiles}, s)) return rc;
   DevBuf<u32> k2, f2, s2, e2, hist, dtot;
   MX_CUDA_TRY(k2.alloc(I, s));
   MX_CUDA_TRY(f2.alloc(I, s));
@@ -581,11 +590,7 @@ int stage1_build(const mx_catalog_desc* d, cudaStream_t s, IndexData* out) {
   MX_CUDA_TRY(ws_borrow(dtot, s, WS_DTOT, 256));
   u32 *ka = rk.p, *fa_ = rf.p, *sa = rs.p, *ea = re.p;
   u32 *kb = k2.p, *fb = f2.p, *sb = s2.p, *eb = e2.p;
-  std::unique_ptr<MxPhase> ph_sort(new MxPhase("radix_sort", s));
   {
-    DevBuf<u64> toff;
-    MX_CUDA_TRY(ws_borrow(toff, s, WS_TOFF, ntiles + 1));
-    if (int rc = gs_run(ntiles, TileOffF{t_cnt.p, toff.p, ntiles}, s)) return rc;
     slot_compact_kernel<<<(unsigned)std::min<long long>(ntiles, (long long)n_sm * 16), 256, 0, s>>>(
         ntiles, tile_len, t_cnt.p, toff.p, rk.p, rf.p, rs.p, re.p, k2.p, f2.p, s2.p, e2.p);
     mx_count_launch();

@@ -2384,12 +2384,12 @@ static int normalize_tail(GenData* g, long long n_chunks, DevBuf<u64>& cpo, DevB
                           bool pack, int fbits, cudaEvent_t seed_join, cudaStream_t s) {
   {
     DevBuf<u32> blist, bcnt;
-    MX_CUDA_TRY(blist.alloc(n_chunks, s));
-    MX_CUDA_TRY(bcnt.alloc(1, s));
+    MX_CUDA_TRY(ws_borrow(blist, s, WS_NBL, n_chunks));
+    MX_CUDA_TRY(ws_borrow(bcnt, s, WS_NBC, 1));
     MX_CUDA_TRY(cudaMemsetAsync(bcnt.p, 0, sizeof(u32), s));
     DevBuf<u32> wlist, wcnt;
-    MX_CUDA_TRY(wlist.alloc(n_chunks, s));
-    MX_CUDA_TRY(wcnt.alloc(1, s));
+    MX_CUDA_TRY(ws_borrow(wlist, s, WS_NWL, n_chunks));
+    MX_CUDA_TRY(ws_borrow(wcnt, s, WS_NWC, 1));
     MX_CUDA_TRY(cudaMemsetAsync(wcnt.p, 0, sizeof(u32), s));
     normalize_tiny_kernel<<<(unsigned)((n_chunks + 255) / 256), 256, 0, s>>>(n_chunks, cpo.p, pm.p, pf.p, ps.p, pe.p,
                                                                            mcnt.p, wlist.p, wcnt.p);
@@ -2866,8 +2866,9 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   for (long long p = 0; p < n_phases; ++p)
     h_pre[p + 1] = h_pre[p] + (u64)h_phases[p].n_chunks * (u64)h_phases[p].n_terms;
   const u64 n_pairs = h_pre[n_phases];
+  // call temporaries come from the per-(thread, stream) workspace
   DevBuf<u64> pair_pre;
-  MX_CUDA_TRY(pair_pre.alloc(n_phases + 1, s));
+  MX_CUDA_TRY(ws_borrow(pair_pre, s, WS_EPRE, n_phases + 1));
   MX_CUDA_TRY(mx_h2d(pair_pre.p, h_pre.data(), sizeof(u64) * (n_phases + 1), s));
   EmitArgs a{};
   a.phases = phases;
@@ -2898,7 +2899,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   // not for a file-sharded (hybrid) index: its file ids are checked nowhere here
   const bool pack = w.max_mkey > 0 && fbits + mbits <= 31 && g->lcnt.p == nullptr;
   DevBuf<u64> pair_off;
-  MX_CUDA_TRY(pair_off.alloc(n_pairs + 1, s));
+  MX_CUDA_TRY(ws_borrow(pair_off, s, WS_EOFF, (long long)n_pairs + 1));
   const unsigned pb = (unsigned)((n_pairs + 255) / 256);
   mx_host_mark("emit setup");
   emit_count_kernel<<<pb, 256, 0, s>>>(a, n_pairs, pair_off.p);
@@ -2910,7 +2911,7 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   // (mixture key, file, start) order unless a pair was long / a merge exists
   const bool sort_terms = w.mode == 0 && g->lcnt.p == nullptr;
   DevBuf<u32> eflags;
-  MX_CUDA_TRY(eflags.alloc(1, s));
+  MX_CUDA_TRY(ws_borrow(eflags, s, WS_EFLAG, 1));
   MX_CUDA_TRY(cudaMemsetAsync(eflags.p, 0, sizeof(u32), s));
   DevBuf<u32> pm, pf, ps, pe;
   MX_CUDA_TRY(pm.alloc(cap, s));
@@ -2919,8 +2920,8 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   MX_CUDA_TRY(pe.alloc(cap, s));
   {
     DevBuf<u32> llist, lcnt;
-    MX_CUDA_TRY(llist.alloc(2 * n_pairs, s));  // [long pairs | unstaged pairs to sort]
-    MX_CUDA_TRY(lcnt.alloc(2, s));
+    MX_CUDA_TRY(ws_borrow(llist, s, WS_ELIST, 2 * (long long)n_pairs));  // [long pairs | unstaged pairs to sort]
+    MX_CUDA_TRY(ws_borrow(lcnt, s, WS_ELCNT, 2));
     MX_CUDA_TRY(cudaMemsetAsync(lcnt.p, 0, 2 * sizeof(u32), s));
     constexpr u32 warp_min = 32;  // pairs with more pieces are cut by a warp (emit_write_warp_kernel)
     emit_write_staged_kernel<<<(unsigned)((n_pairs + EW_THREADS - 1) / EW_THREADS), EW_THREADS, 0, s>>>(
@@ -2941,9 +2942,9 @@ static int emit(GenData* g, const PlanWork& w, const Phase* phases, const Phase*
   }
   DevBuf<u64> cpo, mcnt;
   DevBuf<u32> big;
-  MX_CUDA_TRY(cpo.alloc(n_chunks + 1, s));
-  MX_CUDA_TRY(mcnt.alloc(n_chunks, s));
-  MX_CUDA_TRY(big.alloc(1, s));
+  MX_CUDA_TRY(ws_borrow(cpo, s, WS_ECPO, n_chunks + 1));
+  MX_CUDA_TRY(ws_borrow(mcnt, s, WS_EMCNT, n_chunks));
+  MX_CUDA_TRY(ws_borrow(big, s, WS_EBIG, 1));
   MX_CUDA_TRY(cudaMemsetAsync(big.p, 0, sizeof(u32), s));
   chunk_pieces_kernel<<<(unsigned)((n_chunks + 256) / 256), 256, 0, s>>>(a, n_chunks, pair_off.p, n_pairs, cpo.p);
   mx_count_launch();
