@@ -7,13 +7,12 @@
 // ChunkGenerator.__init__ (chunks.py:139-141) -- component keys in sort order
 //   shuffled by Random(derive_seed(seed, "component-order")).
 //
-// Kernels: key_seed_kernel (device BLAKE2b of each key's canonical string),
-// cursor_shuffle_kernel (one warp per key; MT19937 state and the key's block
-// list (16-bit offsets) in shared memory; warp-parallel rejection sampling and
-// conflict-free swap rounds, csrc/mt19937.cuh), CursorIvF (shuffled blocks ->
-// interval ids, one reduce-then-scan over all keys),
-// cum_len_kernel (u64 look-back scan of lengths in cursor order),
-// component_order_kernel (one shuffle of K ranks).
+// Kernels: key_mt_seed_kernel (one thread per key: device BLAKE2b of the
+// key's canonical string, then the MT19937 init_by_array chain),
+// cursor_shuffle_kernel (one CTA per key: the dataset / file shuffles drawn
+// 32 outputs at a time, applied in parallel (csrc/mt19937.cuh), then the
+// key's interval-level layout by a CTA scan: civ / ccum / cfile / cstart),
+// component_order_kernel (one warp: the shuffle of K ranks).
 #include <map>
 #include "blake2b.cuh"
 #include "common.cuh"
@@ -33,8 +32,8 @@ struct KeyStrView {
   const long long* off;
 };
 
-// One THREAD per key (k < K: derive_seed(seed, "cursor", key string) by
-// device BLAKE2b; k == K: the component-order seed from the host), then the
+// One THREAD per key (derive_seed(seed, "cursor", key string) by device
+// BLAKE2b), then the
 // key's MT19937 init_by_array chain in shared memory (lane-interleaved rows of
 // 33 words, conflict-free), copied out 32 keys interleaved (mt_state_of).
 constexpr int SEED_THREADS = 32;
@@ -42,15 +41,14 @@ constexpr int SEED_ROW = SEED_THREADS + 1;
 constexpr int SEED_MSG = 128;  // one BLAKE2b block per thread in shared memory
 
 __global__ void __launch_bounds__(SEED_THREADS)
-key_mt_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix, int prefix_len, u64 order_seed,
-                   u32* states) {
+key_mt_seed_kernel(KeyStrView v, long long K, const uint8_t* prefix, int prefix_len, u32* states) {
   extern __shared__ u32 ks_dyn[];  // [MT_N][SEED_ROW] + [SEED_THREADS][SEED_MSG] bytes
   const int lane = threadIdx.x;
   const long long k0 = blockIdx.x * (long long)SEED_THREADS, k = k0 + lane;
   uint8_t* msg = reinterpret_cast<uint8_t*>(ks_dyn + MT_N * SEED_ROW) + lane * SEED_MSG;
-  if (k <= K) {
-    u64 seed = order_seed;
-    if (k < K) {
+  if (k < K) {
+    u64 seed = 0;
+    {
       // stable_hash message: prefix, 8-byte length, "v1;v2;..." of the
       // key's present properties; assembled in the thread's shared row
       const u32 packed = v.key_packed[k];
@@ -115,38 +113,39 @@ __device__ __forceinline__ const u32* mt_state_of(const u32* states, long long k
   return states + (size_t)(k / SEED_THREADS) * MT_N * SEED_THREADS + k % SEED_THREADS;
 }
 
-// One WARP per key (grid-stride over warps): the key's seeded MT state loaded
-// from key_mt_seed_kernel into shared memory, the dataset-order shuffle and
-// then every dataset's block shuffle drawn from the same stream
-// (WarpMT::draws, no swaps) and applied in parallel (fy_apply). The draw /
-// bucket scratch of a key with <= cap blocks lives in the warp's shared memory
-// as 16-bit entries (6 B per block); larger keys use the u32 global scratch
-// at the key's block offset (g_*: B entries each).
-constexpr int CS_WARPS = 2;
+// One CTA (CS_THREADS) per key, grid-stride: the key's seeded MT state
+// (key_mt_seed_kernel) in shared memory; warp 0 draws the shuffle (WarpMT::
+// draws, 32 outputs at a time) and builds the ascending bucket lists
+// (fy_lists), then the whole CTA resolves the positions (fy_resolve) and
+// writes the interval-level layout (key_layout). Keys with several datasets
+// (the dataset-order shuffle first, then every dataset's blocks from the
+// same stream) run the warp form (cursor_key_shuffle) on warp 0. Draw /
+// bucket scratch: 16-bit entries in shared memory (6 B per block) for keys
+// with <= cap blocks, else u32 global scratch at the key's block offset.
+constexpr int CS_THREADS = 128;
 constexpr int CS_MT_WORDS = 2 * MT_N;
 constexpr int CS_SMEM_CAP = 16000;
 
 template <typename IT>
 __device__ void cursor_key_shuffle(WarpMT& mt, u32 b0, int nb, int G, const u32* grp, u32* gid, u32* cur_blk, IT* j,
                                    IT* top, IT* link) {
-  if (G > 1) {  // dataset order (one stream for the whole key)
-    mt.draws(G, j);
-    fy_apply(G, j, top, link, [&](int i, u32 v) { gid[b0 + i] = v; });
-  }
+  // dataset order (one stream for the whole key)
+  mt.draws(G, j);
+  fy_apply(G, j, top, link, [&](int i, u32 v) { gid[b0 + i] = v; });
   // every dataset's draws in the shuffled dataset order, then one apply each
   int pos = 0;
   for (int g = 0; g < G; ++g) {
-    const u32 gi = G > 1 ? gid[b0 + g] : 0u;
-    const int s = G > 1 ? (int)grp[b0 + gi] : 0;
-    const int e = G > 1 && gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
+    const u32 gi = gid[b0 + g];
+    const int s = (int)grp[b0 + gi];
+    const int e = gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
     mt.draws(e - s, j + pos);
     pos += e - s;
   }
   pos = 0;
   for (int g = 0; g < G; ++g) {
-    const u32 gi = G > 1 ? gid[b0 + g] : 0u;
-    const int s = G > 1 ? (int)grp[b0 + gi] : 0;
-    const int e = G > 1 && gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
+    const u32 gi = gid[b0 + g];
+    const int s = (int)grp[b0 + gi];
+    const int e = gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
     u32* dst = cur_blk + b0 + pos;
     const u32 base = b0 + (u32)s;
     fy_apply(e - s, j + pos, top + pos, link + pos, [&](int i, u32 v) { dst[i] = base + v; });
@@ -154,130 +153,144 @@ __device__ void cursor_key_shuffle(WarpMT& mt, u32 b0, int nb, int G, const u32*
   }
 }
 
-__global__ void __launch_bounds__(CS_WARPS * 32)
-cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file, const int32_t* file_ds,
-                      const u32* states, u32* grp, u32* gid, u32* cur_blk, int cap, u32* g_j, u32* g_top,
-                      u32* g_link) {
-  extern __shared__ __align__(16) u32 cs_dyn[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  u32* mine = cs_dyn + (size_t)w * (CS_MT_WORDS + (size_t)cap * 6 / 4);
-  unsigned short* s_j = reinterpret_cast<unsigned short*>(mine + CS_MT_WORDS);
-  unsigned short* s_top = s_j + cap;
-  unsigned short* s_link = s_top + cap;
-  for (long long k = blockIdx.x * (long long)CS_WARPS + w; k < K; k += (long long)gridDim.x * CS_WARPS) {
-    const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
-    const int nb = (int)(b1 - b0);
-    if (nb <= 1) {  // shuffling one block draws nothing
-      if (lane == 0 && nb == 1) cur_blk[b0] = b0;
-      continue;
-    }
-    // dataset groups (blocks are file-sorted and ds is nondecreasing in file
-    // order): one group when first and last block share a dataset, else a
-    // warp-parallel scan of dataset changes
-    int G = 1;
-    if (file_ds[blk_file[b0]] != file_ds[blk_file[b1 - 1]]) {
-      G = 0;
-      for (int b = 0; b < nb; b += 32) {
-        const int i = b + lane;
-        bool hd = false;
-        if (i < nb) hd = i == 0 || file_ds[blk_file[b0 + i]] != file_ds[blk_file[b0 + i - 1]];
-        const u32 hm = __ballot_sync(MX_FULL, hd);
-        if (hd) grp[b0 + G + __popc(hm & ((1u << lane) - 1))] = (u32)i;
-        G += __popc(hm);
-      }
-    }
-    WarpMT mt{mine, mine + MT_N, MT_N};
-    const u32* st = mt_state_of(states, k);
-#pragma unroll 4
-    for (int a = lane; a < MT_N; a += 32) mine[a] = st[(size_t)a * SEED_THREADS];
-    __syncwarp();
-    if (nb <= cap)
-      cursor_key_shuffle<unsigned short>(mt, b0, nb, G, grp, gid, cur_blk, s_j, s_top, s_link);
-    else
-      cursor_key_shuffle<u32>(mt, b0, nb, G, grp, gid, cur_blk, g_j + b0, g_top + b0, g_link + b0);
-    __syncwarp();
-  }
-}
-
-// civ: interval ids in cursor order. Cursor positions of key k occupy the
-// same index range as its intervals in sorted order, and keys are stored
-// consecutively, so the output position of block p (in cursor order, keys
-// concatenated) is the exclusive prefix of interval counts over [0, p).
-struct CursorIvF {
-  const u32* cur_blk;
-  const u32* blk_first;
-  u32* civ;
-  __device__ u64 value(long long p) const {
-    const u32 b = cur_blk[p];
-    return blk_first[b + 1] - blk_first[b];
-  }
-  __device__ void apply(long long p, u64 ex, u64 v) const {
-    const u32 f = blk_first[cur_blk[p]];
-    for (u32 t = 0; t < (u32)v; ++t) civ[ex + t] = f + t;
-  }
-  __device__ void total(u64) const {}
-};
-
-// ccum[j + 1] = samples of cursor positions [0, j] (interval perm[j])
-struct CumPermF {
-  const u32* perm;
-  const u32* start;
-  const u32* end;
-  u64* cum;
-  const u32* file;
-  u32* cfile;   // file / start of cursor position j (the emission's gathers, done once here)
-  u32* cstart;
-  __device__ u64 value(long long j) const {
-    const u32 iv = perm[j];
-    return end[iv] - start[iv];
-  }
-  __device__ void apply(long long j, u64 ex, u64 v) const {
-    if (j == 0) cum[0] = 0;
-    cum[j + 1] = ex + v;
-    const u32 iv = perm[j];
-    cfile[j] = file[iv];
-    cstart[j] = start[iv];
-  }
-  __device__ void total(u64) const {}
-};
-
-// Both layouts in ONE scan over the cursor's blocks when the index holds
-// < 2^32 samples: the value of block position p packs (intervals << 32 |
-// samples) of block cur_blk[p], so the exclusive prefix gives the block's
-// first cursor position and its sample offset at once (sums never carry).
-struct CursorF {
-  const u32* cur_blk;
+// The key's interval-level cursor layout (whole CTA): cursor positions of
+// key k occupy the same index range as its intervals in index order,
+// [blk_first[b0], blk_first[b1]), with sample offsets from
+// iv_cum[blk_first[b0]]; a CTA scan over the shuffled blocks' (interval,
+// sample) counts places each block's intervals. civ[j] = interval at cursor
+// position j, ccum[j + 1] = samples of positions [0, j], cfile / cstart =
+// its file / start (the emission's gathers, done once here).
+struct LayoutOut {
   const u32* blk_first;
   const u64* iv_cum;
   const u32* start;
   const u32* end;
   const u32* file;
   u32* civ;
-  u64* cum;
+  u64* ccum;
   u32* cfile;
   u32* cstart;
-  __device__ u64 value(long long p) const {
-    const u32 b = cur_blk[p];
-    const u32 f0 = blk_first[b], f1 = blk_first[b + 1];
-    return ((u64)(f1 - f0) << 32) | (iv_cum[f1] - iv_cum[f0]);
-  }
-  __device__ void apply(long long p, u64 ex, u64) const {
-    const u32 b = cur_blk[p];
-    const u32 f0 = blk_first[b], f1 = blk_first[b + 1];
-    const u64 pos = ex >> 32;
-    u64 samp = ex & 0xffffffffull;
-    if (p == 0) cum[0] = 0;
-    for (u32 t = 0; t < f1 - f0; ++t) {
-      const u32 iv = f0 + t, a = start[iv];
-      civ[pos + t] = iv;
-      cfile[pos + t] = file[iv];
-      cstart[pos + t] = a;
-      samp += end[iv] - a;
-      cum[pos + t + 1] = samp;
-    }
-  }
-  __device__ void total(u64) const {}
 };
+
+__device__ void key_layout(const LayoutOut& o, u32 b0, u32 b1, const u32* cur_blk, u64* s_red) {
+  constexpr int NW = CS_THREADS / 32;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  u32 pos = o.blk_first[b0];
+  u64 samp = o.iv_cum[pos];
+  if (tid == 0 && pos == 0) o.ccum[0] = 0;
+  for (u32 q = b0; q < b1; q += CS_THREADS) {
+    const u32 p = q + tid;
+    u32 f0 = 0, f1 = 0;
+    u64 sm = 0;
+    if (p < b1) {
+      const u32 b = cur_blk[p];
+      f0 = o.blk_first[b];
+      f1 = o.blk_first[b + 1];
+      sm = o.iv_cum[f1] - o.iv_cum[f0];
+    }
+    const u32 c = f1 - f0;
+    const u64 ic = warp_incl_scan((u64)c), is = warp_incl_scan(sm);
+    if (lane == 31) {
+      s_red[w] = ic;
+      s_red[NW + w] = is;
+    }
+    __syncthreads();
+    u64 bc = 0, bs = 0, tc = 0, ts = 0;
+#pragma unroll
+    for (int x = 0; x < NW; ++x) {
+      const u64 xc = s_red[x], xs = s_red[NW + x];
+      bc += x < w ? xc : 0;
+      bs += x < w ? xs : 0;
+      tc += xc;
+      ts += xs;
+    }
+    __syncthreads();
+    const u32 my = pos + (u32)(bc + ic - c);
+    u64 run = samp + bs + is - sm;
+    for (u32 t = 0; t < c; ++t) {
+      const u32 iv = f0 + t, a = o.start[iv];
+      o.civ[my + t] = iv;
+      o.cfile[my + t] = o.file[iv];
+      o.cstart[my + t] = a;
+      run += o.end[iv] - a;
+      o.ccum[my + t + 1] = run;
+    }
+    pos += (u32)tc;
+    samp += ts;
+  }
+}
+
+__global__ void __launch_bounds__(CS_THREADS)
+cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file, const int32_t* file_ds,
+                      const u32* states, u32* grp, u32* gid, u32* cur_blk, int cap, u32* g_j, u32* g_top,
+                      u32* g_link, LayoutOut lo) {
+  extern __shared__ __align__(16) u32 cs_dyn[];
+  __shared__ u64 s_red[2 * (CS_THREADS / 32)];
+  __shared__ int s_G;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  u32* mt_s = cs_dyn;
+  unsigned short* s_j = reinterpret_cast<unsigned short*>(cs_dyn + CS_MT_WORDS);
+  unsigned short* s_top = s_j + cap;
+  unsigned short* s_link = s_top + cap;
+  for (long long k = blockIdx.x; k < K; k += gridDim.x) {
+    const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
+    const int nb = (int)(b1 - b0);
+    if (nb == 0) continue;
+    if (nb == 1) {  // shuffling one block draws nothing
+      if (tid == 0) cur_blk[b0] = b0;
+      __syncthreads();
+      key_layout(lo, b0, b1, cur_blk, s_red);
+      continue;
+    }
+    const u32* st = mt_state_of(states, k);
+    for (int a = tid; a < MT_N; a += CS_THREADS) mt_s[a] = st[(size_t)a * SEED_THREADS];
+    // dataset groups (blocks are file-sorted and ds is nondecreasing in file
+    // order): one group when first and last block share a dataset, else a
+    // warp-parallel scan of dataset changes
+    if (w == 0) {
+      int G = 1;
+      if (file_ds[blk_file[b0]] != file_ds[blk_file[b1 - 1]]) {
+        G = 0;
+        for (int b = 0; b < nb; b += 32) {
+          const int i = b + lane;
+          bool hd = false;
+          if (i < nb) hd = i == 0 || file_ds[blk_file[b0 + i]] != file_ds[blk_file[b0 + i - 1]];
+          const u32 hm = __ballot_sync(MX_FULL, hd);
+          if (hd) grp[b0 + G + __popc(hm & ((1u << lane) - 1))] = (u32)i;
+          G += __popc(hm);
+        }
+      }
+      if (lane == 0) s_G = G;
+    }
+    __syncthreads();
+    const int G = s_G;
+    const bool in_smem = nb <= cap;
+    if (w == 0) {
+      WarpMT mt{mt_s, mt_s + MT_N, MT_N};
+      if (G == 1) {
+        if (in_smem) {
+          mt.draws(nb, s_j);
+          fy_lists(nb, s_j, s_top, s_link);
+        } else {
+          mt.draws(nb, g_j + b0);
+          fy_lists(nb, g_j + b0, g_top + b0, g_link + b0);
+        }
+      } else if (in_smem) {
+        cursor_key_shuffle<unsigned short>(mt, b0, nb, G, grp, gid, cur_blk, s_j, s_top, s_link);
+      } else {
+        cursor_key_shuffle<u32>(mt, b0, nb, G, grp, gid, cur_blk, g_j + b0, g_top + b0, g_link + b0);
+      }
+    }
+    __syncthreads();
+    if (G == 1) {
+      auto out = [&](int i, u32 v) { cur_blk[b0 + i] = b0 + v; };
+      if (in_smem) fy_resolve(nb, s_j, s_top, s_link, tid, CS_THREADS, out);
+      else fy_resolve(nb, g_j + b0, g_top + b0, g_link + b0, tid, CS_THREADS, out);
+      __syncthreads();
+    }
+    key_layout(lo, b0, b1, cur_blk, s_red);
+  }
+}
 
 __global__ void comp_total_kernel(long long K, const u32* key_blk_first, const u32* blk_first, const u64* iv_cum,
                                   u64* total) {
@@ -286,19 +299,18 @@ __global__ void comp_total_kernel(long long K, const u32* key_blk_first, const u
   total[k] = iv_cum[blk_first[key_blk_first[k + 1]]] - iv_cum[blk_first[key_blk_first[k]]];
 }
 
-// one warp: the shuffle of the K component ranks (chunks.py:139-141) from the
-// seeded state key_mt_seed_kernel wrote at entry K; 16-bit scratch in shared
-// memory up to CO_SMEM ranks, else u32 global scratch
+// one warp: the shuffle of the K component ranks (chunks.py:139-141); 16-bit
+// scratch in shared memory up to CO_SMEM ranks, else u32 global scratch
 constexpr int CO_SMEM = 16384;
 
-__global__ void __launch_bounds__(32) component_order_kernel(long long K, const u32* states, u32* order, u32* g_j,
-                                                           u32* g_top, u32* g_link) {
+__global__ void __launch_bounds__(32) component_order_kernel(long long K, u64 seed, u32* order, u32* g_j, u32* g_top,
+                                                           u32* g_link) {
   extern __shared__ __align__(16) u32 co_dyn[];
   const int n = (int)K, lane = threadIdx.x;
   WarpMT mt{co_dyn, co_dyn + MT_N, MT_N};
-  const u32* st = mt_state_of(states, K);
-#pragma unroll 4
-  for (int a = lane; a < MT_N; a += 32) co_dyn[a] = st[(size_t)a * SEED_THREADS];
+  // the component-order seed comes from the host: seeded here (lane 0) so
+  // the shuffle does not wait for the per-key seed kernel
+  if (lane == 0) mt_init_by_array(seed, [&](int a) -> u32& { return co_dyn[a]; });
   __syncwarp();
   auto out = [&](int i, u32 v) { order[i] = v; };
   if (n <= CO_SMEM) {
@@ -328,18 +340,31 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   comp_total_kernel<<<(unsigned)((K + 255) / 256), 256, 0, s>>>(K, ix->key_blk_first.p, ix->blk_first.p,
                                                                ix->iv_cum.p, g->comp_total.p);
   mx_count_launch();
-  // the component-order shuffle (one sequential Fisher-Yates over K ranks)
-  // runs on a side stream, overlapped with the per-key cursor shuffles
   MX_CUDA_TRY(g->comp_order.alloc(K, s));
   MX_CUDA_TRY(cudaEventRecord(g->ev_tot, s));
   mx_host_mark("cursor prologue");
-  // every key's cursor seed + seeded MT state, and the component order's (K)
+  // the component-order shuffle runs on a side stream, overlapped with the
+  // per-key seeds and cursor shuffles
+  MX_CUDA_TRY(cudaStreamWaitEvent(g->ostream, g->ev_tot, 0));
+  {
+    DevBuf<u32> fj, ft, fl;  // global scratch only beyond CO_SMEM ranks
+    const long long gn = K > CO_SMEM ? K : 1;
+    MX_CUDA_TRY(ws_borrow(fj, g->ostream, WS_FYJ, gn));
+    MX_CUDA_TRY(ws_borrow(ft, g->ostream, WS_FYTOP, gn));
+    MX_CUDA_TRY(ws_borrow(fl, g->ostream, WS_FYLINK, gn));
+    const size_t dyn = sizeof(u32) * CS_MT_WORDS + (K <= CO_SMEM ? 6 * (size_t)K : 0);
+    MX_CUDA_TRY(mx_smem_attr(component_order_kernel, dyn));
+    component_order_kernel<<<1, 32, dyn, g->ostream>>>(K, order_seed, g->comp_order.p, fj.p, ft.p, fl.p);
+    mx_count_launch();
+  }
+  MX_CUDA_TRY(cudaEventRecord(g->ev_order, g->ostream));
+  // every key's cursor seed + seeded MT state
   DevBuf<uint8_t> pre;
   DevBuf<u32> states;
   MX_CUDA_TRY(ws_borrow(pre, s, WS_CPRE, prefix_len > 0 ? prefix_len : 1));
   if (prefix_len > 0)
     MX_CUDA_TRY(mx_h2d(pre.p, cursor_prefix, prefix_len, s));
-  MX_CUDA_TRY(ws_borrow(states, s, WS_CSEED, (K + 1 + SEED_THREADS) / SEED_THREADS * SEED_THREADS * MT_N));
+  MX_CUDA_TRY(ws_borrow(states, s, WS_CSEED, (K + SEED_THREADS - 1) / SEED_THREADS * SEED_THREADS * MT_N));
   KeyStrView v{};
   v.key_packed = ix->key_packed.p;
   v.n_props = ix->n_props;
@@ -353,30 +378,18 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   {
     const size_t dyn = sizeof(u32) * MT_N * SEED_ROW + (size_t)SEED_MSG * SEED_THREADS;
     MX_CUDA_TRY(mx_smem_attr(key_mt_seed_kernel, dyn));
-    key_mt_seed_kernel<<<(unsigned)((K + 1 + SEED_THREADS - 1) / SEED_THREADS), SEED_THREADS, dyn, s>>>(
-        v, K, pre.p, prefix_len, order_seed, states.p);
+    key_mt_seed_kernel<<<(unsigned)((K + SEED_THREADS - 1) / SEED_THREADS), SEED_THREADS, dyn, s>>>(
+        v, K, pre.p, prefix_len, states.p);
     mx_count_launch();
   }
-  // the component-order shuffle runs on a side stream, overlapped with the
-  // per-key cursor shuffles
-  MX_CUDA_TRY(cudaEventRecord(g->ev_fork, s));
-  MX_CUDA_TRY(cudaStreamWaitEvent(g->ostream, g->ev_fork, 0));
-  {
-    DevBuf<u32> fj, ft, fl;  // global scratch only beyond CO_SMEM ranks
-    const long long gn = K > CO_SMEM ? K : 1;
-    MX_CUDA_TRY(ws_borrow(fj, g->ostream, WS_FYJ, gn));
-    MX_CUDA_TRY(ws_borrow(ft, g->ostream, WS_FYTOP, gn));
-    MX_CUDA_TRY(ws_borrow(fl, g->ostream, WS_FYLINK, gn));
-    const size_t dyn = sizeof(u32) * CS_MT_WORDS + (K <= CO_SMEM ? 6 * (size_t)K : 0);
-    MX_CUDA_TRY(mx_smem_attr(component_order_kernel, dyn));
-    component_order_kernel<<<1, 32, dyn, g->ostream>>>(K, states.p, g->comp_order.p, fj.p, ft.p, fl.p);
-    mx_count_launch();
-  }
-  MX_CUDA_TRY(cudaEventRecord(g->ev_order, g->ostream));
   DevBuf<u32> grp, gid;
   MX_CUDA_TRY(ws_borrow(grp, s, WS_CGRP, B));
   MX_CUDA_TRY(ws_borrow(gid, s, WS_CGID, B));
   MX_CUDA_TRY(g->cur_blk.alloc(B, s));
+  MX_CUDA_TRY(g->civ.alloc(I, s));
+  MX_CUDA_TRY(g->ccum.alloc(I + 1, s));
+  MX_CUDA_TRY(g->cfile.alloc(I, s));
+  MX_CUDA_TRY(g->cstart.alloc(I, s));
   {
     MxPhase ph2("cursor_shuffle", s);
     // keys with <= cap blocks keep their scratch in shared memory (6 B per
@@ -388,7 +401,7 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     MX_CUDA_TRY(ws_borrow(fj, s, WS_FYJ, gn));
     MX_CUDA_TRY(ws_borrow(ft, s, WS_FYTOP, gn));
     MX_CUDA_TRY(ws_borrow(fl, s, WS_FYLINK, gn));
-    const size_t dyn = ((size_t)CS_MT_WORDS * 4 + (size_t)cap * 6) * CS_WARPS;
+    const size_t dyn = (size_t)CS_MT_WORDS * 4 + (size_t)cap * 6;
     MX_CUDA_TRY(mx_smem_attr(cursor_shuffle_kernel, dyn));
     static thread_local std::map<size_t, int> occ;  // smem -> resident CTAs per SM
     static thread_local int n_sm = 0;
@@ -399,26 +412,14 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     }
     int& per_sm = occ[dyn];
     if (!per_sm)
-      MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cursor_shuffle_kernel, CS_WARPS * 32, dyn));
-    const long long blocks = std::min<long long>((K + CS_WARPS - 1) / CS_WARPS, (long long)std::max(per_sm, 1) * n_sm);
-    cursor_shuffle_kernel<<<(unsigned)blocks, CS_WARPS * 32, dyn, s>>>(K, ix->key_blk_first.p, ix->blk_file.p,
-                                                                     ix->file_ds.p, states.p, grp.p, gid.p,
-                                                                     g->cur_blk.p, cap, fj.p, ft.p, fl.p);
+      MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cursor_shuffle_kernel, CS_THREADS, dyn));
+    const long long blocks = std::min<long long>(K, (long long)std::max(per_sm, 1) * n_sm);
+    cursor_shuffle_kernel<<<(unsigned)blocks, CS_THREADS, dyn, s>>>(
+        K, ix->key_blk_first.p, ix->blk_file.p, ix->file_ds.p, states.p, grp.p, gid.p, g->cur_blk.p, cap, fj.p, ft.p,
+        fl.p,
+        LayoutOut{ix->blk_first.p, ix->iv_cum.p, ix->iv_start.p, ix->iv_end.p, ix->iv_file.p, g->civ.p, g->ccum.p,
+                  g->cfile.p, g->cstart.p});
     mx_count_launch();
-  }
-  MX_CUDA_TRY(g->civ.alloc(I, s));
-  MX_CUDA_TRY(g->ccum.alloc(I + 1, s));
-  MX_CUDA_TRY(g->cfile.alloc(I, s));
-  MX_CUDA_TRY(g->cstart.alloc(I, s));
-  if (ix->indexed_samples < (1ll << 32) && I < (1ll << 31)) {  // resolved sizes (ix_resolve)
-    if (int rc = gs_run(B, CursorF{g->cur_blk.p, ix->blk_first.p, ix->iv_cum.p, ix->iv_start.p, ix->iv_end.p,
-                                   ix->iv_file.p, g->civ.p, g->ccum.p, g->cfile.p, g->cstart.p}, s))
-      return rc;
-  } else {  // >= 2^32 samples: positions first, then the 64-bit sample prefix
-    if (int rc = gs_run(B, CursorIvF{g->cur_blk.p, ix->blk_first.p, g->civ.p}, s)) return rc;
-    if (int rc = gs_run(I, CumPermF{g->civ.p, ix->iv_start.p, ix->iv_end.p, g->ccum.p, ix->iv_file.p, g->cfile.p,
-                                     g->cstart.p}, s))
-      return rc;
   }
   if (int rc = gen_local_lists(g, s)) return rc;  // sharded index: this rank's cursor positions
   MX_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_order, 0));

@@ -65,11 +65,10 @@ __device__ __forceinline__ void mt_init_by_array(unsigned long long seed_v, S st
 //    ([0,227) reads only old words, [227,454) reads words of the first range,
 //    [454,623) of the second, then word 623) and tempered into `out`;
 //  * draws: the _randbelow(i + 1) results j_i of a shuffle (i = n-1..1) are
-//    resolved 32 outputs at a time: lane l takes output pos+l and the number
-//    A_l of accepted draws before it (which fixes the bound i - A_l + 1 it is
-//    tested against) is found by fixed-point iteration of
-//    A = prefix_popcount(accept(A)) -- after s rounds lanes 0..s are exact,
-//    and a fixed point IS the sequential answer. No swaps while drawing.
+//    resolved a 128-output window at a time: the number of accepted draws
+//    before an output fixes the bound i - A + 1 it is tested against, and
+//    A is found by fixed-point iteration (see draws()). No swaps while
+//    drawing.
 struct WarpMT {
   uint32_t* s;    // state [624]
   uint32_t* out;  // tempered outputs [624]
@@ -114,34 +113,71 @@ struct WarpMT {
     __syncwarp();
   }
 
-  // j[i] = _randbelow(i + 1) for i = n-1..1, in stream order (whole warp)
+  // j[i] = _randbelow(i + 1) for i = n-1..1, in stream order (whole warp).
+  // DU consecutive outputs per lane (a window of up to 32 * DU outputs, never
+  // across a refill): given the accepted count `base` of the earlier lanes,
+  // a lane resolves its own outputs in order; `base` is iterated to the fixed
+  // point of base = prefix over lanes of their accepted counts (counts < 8:
+  // three ballots). A fixed point is the sequential answer (induction over
+  // the outputs), and every round makes at least one more lane exact.
   template <typename IT>
   __device__ void draws(int n, IT* j) {
+    constexpr int DU = 4;
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     int i = n - 1;
     while (i >= 1) {
       if (pos >= MT_N) refill();
-      const bool valid = pos + lane < MT_N;
-      const uint32_t u = valid ? out[pos + lane] : 0u;
-      uint32_t A = 0, acc_mask, r = 0;
-      bool acc;
-      for (;;) {
-        const int ii = i - (int)A;
-        acc = false;
-        if (valid && ii >= 1) {
-          const uint32_t bound = (uint32_t)ii + 1u;
-          r = u >> __clz(bound);  // getrandbits(bound.bit_length())
-          acc = r < bound;
-        }
-        acc_mask = __ballot_sync(0xffffffffu, acc);
-        const uint32_t A2 = __popc(acc_mask & lt);
-        if (__all_sync(0xffffffffu, A2 == A)) break;
-        A = A2;
+      uint32_t u[DU];
+#pragma unroll
+      for (int t = 0; t < DU; ++t) {
+        const int o = pos + DU * lane + t;
+        u[t] = o < MT_N ? out[o] : 0u;
       }
-      if (acc) j[i - (int)A] = (IT)r;
-      pos += __popc(__ballot_sync(0xffffffffu, valid && i - (int)A >= 1));
-      i -= __popc(acc_mask);
+      const int lim = MT_N - pos - DU * lane;  // valid outputs of this lane (may be <= 0)
+      int base = 0, cnt = 0, act = 0;
+      uint32_t accm = 0, r[DU];
+      for (;;) {
+        int A = base;
+        cnt = 0;
+        act = 0;
+        accm = 0;
+#pragma unroll
+        for (int t = 0; t < DU; ++t) {
+          const int ii = i - A;
+          r[t] = 0;
+          if (t < lim && ii >= 1) {
+            ++act;
+            const uint32_t bound = (uint32_t)ii + 1u;
+            r[t] = u[t] >> __clz(bound);  // getrandbits(bound.bit_length())
+            if (r[t] < bound) {
+              accm |= 1u << t;
+              ++A;
+              ++cnt;
+            }
+          }
+        }
+        const uint32_t m0 = __ballot_sync(0xffffffffu, cnt & 1), m1 = __ballot_sync(0xffffffffu, cnt & 2),
+                       m2 = __ballot_sync(0xffffffffu, cnt & 4);
+        const int nb = __popc(m0 & lt) + 2 * __popc(m1 & lt) + 4 * __popc(m2 & lt);
+        if (__all_sync(0xffffffffu, nb == base)) break;
+        base = nb;
+      }
+      // accepted outputs: step i - (accepted before it) draws r
+      int A = base;
+#pragma unroll
+      for (int t = 0; t < DU; ++t) {
+        if (accm >> t & 1u) {
+          j[i - A] = (IT)r[t];
+          ++A;
+        }
+      }
+      const uint32_t a0 = __ballot_sync(0xffffffffu, act & 1), a1 = __ballot_sync(0xffffffffu, act & 2),
+                     a2 = __ballot_sync(0xffffffffu, act & 4);
+      const uint32_t c0 = __ballot_sync(0xffffffffu, cnt & 1), c1 = __ballot_sync(0xffffffffu, cnt & 2),
+                     c2 = __ballot_sync(0xffffffffu, cnt & 4);
+      pos += __popc(a0) + 2 * __popc(a1) + 4 * __popc(a2);
+      i -= __popc(c0) + 2 * __popc(c1) + 4 * __popc(c2);
     }
     __syncwarp();
   }
@@ -164,8 +200,9 @@ struct WarpMT {
 // link[p] when top[p] == p; every element's chain is followed independently
 // (mean length ~1, max ~log n). IT = u16 in the shared-memory form
 // (n < 65535), u32 otherwise; the all-ones IT marks "none".
-template <typename IT, typename F>
-__device__ void fy_apply(int n, const IT* j, IT* top, IT* link, F out) {
+// phase 1 (one warp): the ascending bucket lists of steps 1..n-1
+template <typename IT>
+__device__ void fy_lists(int n, const IT* j, IT* top, IT* link) {
   const int lane = threadIdx.x & 31;
   const uint32_t none = (uint32_t)(IT)~0u;
   for (int p = lane; p < n; p += 32) top[p] = (IT)none;
@@ -184,11 +221,17 @@ __device__ void fy_apply(int n, const IT* j, IT* top, IT* link, F out) {
     }
     __syncwarp();
   }
+}
+
+// phase 2 (any number of threads, element-parallel): every output position
+template <typename IT, typename F>
+__device__ void fy_resolve(int n, const IT* j, const IT* top, const IT* link, int tid, int stride, F out) {
+  const uint32_t none = (uint32_t)(IT)~0u;
   auto head = [&](uint32_t p) -> uint32_t {
     const uint32_t t = top[p];
     return t == p ? (uint32_t)link[p] : t;
   };
-  for (int i = lane; i < n; i += 32) {
+  for (int i = tid; i < n; i += stride) {
     uint32_t h, last;
     if (i == 0) {
       h = head(0);
@@ -203,6 +246,14 @@ __device__ void fy_apply(int n, const IT* j, IT* top, IT* link, F out) {
     }
     out(i, last);
   }
+}
+
+// the whole apply by one warp
+template <typename IT, typename F>
+__device__ void fy_apply(int n, const IT* j, IT* top, IT* link, F out) {
+  fy_lists(n, j, top, link);
+  __syncwarp();
+  fy_resolve(n, j, top, link, threadIdx.x & 31, 32, out);
   __syncwarp();
 }
 
