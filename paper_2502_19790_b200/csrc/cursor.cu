@@ -10,8 +10,9 @@
 // Kernels: key_mt_seed_kernel (one thread per key: device BLAKE2b of the
 // key's canonical string, then the MT19937 init_by_array chain),
 // cursor_shuffle_kernel (one CTA per key: the dataset / file shuffles drawn
-// 32 outputs at a time, applied in parallel (csrc/mt19937.cuh), then the
-// key's interval-level layout by a CTA scan: civ / ccum / cfile / cstart),
+// 128 outputs per window, applied in parallel (csrc/mt19937.cuh)), the
+// interval-level layout civ / ccum / cfile / cstart by one reduce-then-scan
+// over the shuffled blocks (CursorF),
 // component_order_kernel (one warp: the shuffle of K ranks).
 #include <map>
 #include "blake2b.cuh"
@@ -115,14 +116,16 @@ __device__ __forceinline__ const u32* mt_state_of(const u32* states, long long k
 
 // One CTA (CS_THREADS) per key, grid-stride: the key's seeded MT state
 // (key_mt_seed_kernel) in shared memory; warp 0 draws the shuffle (WarpMT::
-// draws, 32 outputs at a time) and builds the ascending bucket lists
-// (fy_lists), then the whole CTA resolves the positions (fy_resolve) and
-// writes the interval-level layout (key_layout). Keys with several datasets
+// draws, 128 outputs per window) and builds the ascending bucket lists
+// (fy_lists), then the whole CTA resolves the positions (fy_resolve). The
+// interval-level layout is one device-wide scan afterwards (CursorF): per key
+// it is a chain of dependent gathers that leaves the device idle at 1B
+// samples (measured 0.4 ms per key there, clock64). Keys with several datasets
 // (the dataset-order shuffle first, then every dataset's blocks from the
 // same stream) run the warp form (cursor_key_shuffle) on warp 0. Draw /
 // bucket scratch: 16-bit entries in shared memory (6 B per block) for keys
 // with <= cap blocks, else u32 global scratch at the key's block offset.
-constexpr int CS_THREADS = 128;
+constexpr int CS_THREADS = 64;  // 16 CTAs per SM: every cfg2 key resident at once
 constexpr int CS_MT_WORDS = 2 * MT_N;
 constexpr int CS_SMEM_CAP = 16000;
 
@@ -153,79 +156,11 @@ __device__ void cursor_key_shuffle(WarpMT& mt, u32 b0, int nb, int G, const u32*
   }
 }
 
-// The key's interval-level cursor layout (whole CTA): cursor positions of
-// key k occupy the same index range as its intervals in index order,
-// [blk_first[b0], blk_first[b1]), with sample offsets from
-// iv_cum[blk_first[b0]]; a CTA scan over the shuffled blocks' (interval,
-// sample) counts places each block's intervals. civ[j] = interval at cursor
-// position j, ccum[j + 1] = samples of positions [0, j], cfile / cstart =
-// its file / start (the emission's gathers, done once here).
-struct LayoutOut {
-  const u32* blk_first;
-  const u64* iv_cum;
-  const u32* start;
-  const u32* end;
-  const u32* file;
-  u32* civ;
-  u64* ccum;
-  u32* cfile;
-  u32* cstart;
-};
-
-__device__ void key_layout(const LayoutOut& o, u32 b0, u32 b1, const u32* cur_blk, u64* s_red) {
-  constexpr int NW = CS_THREADS / 32;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  u32 pos = o.blk_first[b0];
-  u64 samp = o.iv_cum[pos];
-  if (tid == 0 && pos == 0) o.ccum[0] = 0;
-  for (u32 q = b0; q < b1; q += CS_THREADS) {
-    const u32 p = q + tid;
-    u32 f0 = 0, f1 = 0;
-    u64 sm = 0;
-    if (p < b1) {
-      const u32 b = cur_blk[p];
-      f0 = o.blk_first[b];
-      f1 = o.blk_first[b + 1];
-      sm = o.iv_cum[f1] - o.iv_cum[f0];
-    }
-    const u32 c = f1 - f0;
-    const u64 ic = warp_incl_scan((u64)c), is = warp_incl_scan(sm);
-    if (lane == 31) {
-      s_red[w] = ic;
-      s_red[NW + w] = is;
-    }
-    __syncthreads();
-    u64 bc = 0, bs = 0, tc = 0, ts = 0;
-#pragma unroll
-    for (int x = 0; x < NW; ++x) {
-      const u64 xc = s_red[x], xs = s_red[NW + x];
-      bc += x < w ? xc : 0;
-      bs += x < w ? xs : 0;
-      tc += xc;
-      ts += xs;
-    }
-    __syncthreads();
-    const u32 my = pos + (u32)(bc + ic - c);
-    u64 run = samp + bs + is - sm;
-    for (u32 t = 0; t < c; ++t) {
-      const u32 iv = f0 + t, a = o.start[iv];
-      o.civ[my + t] = iv;
-      o.cfile[my + t] = o.file[iv];
-      o.cstart[my + t] = a;
-      run += o.end[iv] - a;
-      o.ccum[my + t + 1] = run;
-    }
-    pos += (u32)tc;
-    samp += ts;
-  }
-}
-
 __global__ void __launch_bounds__(CS_THREADS)
 cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file, const int32_t* file_ds,
                       const u32* states, u32* grp, u32* gid, u32* cur_blk, int cap, u32* g_j, u32* g_top,
-                      u32* g_link, LayoutOut lo) {
+                      u32* g_link) {
   extern __shared__ __align__(16) u32 cs_dyn[];
-  __shared__ u64 s_red[2 * (CS_THREADS / 32)];
   __shared__ int s_G;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   u32* mt_s = cs_dyn;
@@ -238,8 +173,6 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
     if (nb == 0) continue;
     if (nb == 1) {  // shuffling one block draws nothing
       if (tid == 0) cur_blk[b0] = b0;
-      __syncthreads();
-      key_layout(lo, b0, b1, cur_blk, s_red);
       continue;
     }
     const u32* st = mt_state_of(states, k);
@@ -286,11 +219,90 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
       auto out = [&](int i, u32 v) { cur_blk[b0 + i] = b0 + v; };
       if (in_smem) fy_resolve(nb, s_j, s_top, s_link, tid, CS_THREADS, out);
       else fy_resolve(nb, g_j + b0, g_top + b0, g_link + b0, tid, CS_THREADS, out);
-      __syncthreads();
     }
-    key_layout(lo, b0, b1, cur_blk, s_red);
+    __syncthreads();
   }
 }
+
+// civ: interval ids in cursor order. Cursor positions of key k occupy the
+// same index range as its intervals in sorted order, and keys are stored
+// consecutively, so the output position of block p (in cursor order, keys
+// concatenated) is the exclusive prefix of interval counts over [0, p).
+struct CursorIvF {
+  const u32* cur_blk;
+  const u32* blk_first;
+  u32* civ;
+  __device__ u64 value(long long p) const {
+    const u32 b = cur_blk[p];
+    return blk_first[b + 1] - blk_first[b];
+  }
+  __device__ void apply(long long p, u64 ex, u64 v) const {
+    const u32 f = blk_first[cur_blk[p]];
+    for (u32 t = 0; t < (u32)v; ++t) civ[ex + t] = f + t;
+  }
+  __device__ void total(u64) const {}
+};
+
+// ccum[j + 1] = samples of cursor positions [0, j] (interval perm[j])
+struct CumPermF {
+  const u32* perm;
+  const u32* start;
+  const u32* end;
+  u64* cum;
+  const u32* file;
+  u32* cfile;   // file / start of cursor position j (the emission's gathers, done once here)
+  u32* cstart;
+  __device__ u64 value(long long j) const {
+    const u32 iv = perm[j];
+    return end[iv] - start[iv];
+  }
+  __device__ void apply(long long j, u64 ex, u64 v) const {
+    if (j == 0) cum[0] = 0;
+    cum[j + 1] = ex + v;
+    const u32 iv = perm[j];
+    cfile[j] = file[iv];
+    cstart[j] = start[iv];
+  }
+  __device__ void total(u64) const {}
+};
+
+// Both layouts in ONE scan over the cursor's blocks when the index holds
+// < 2^32 samples: the value of block position p packs (intervals << 32 |
+// samples) of block cur_blk[p], so the exclusive prefix gives the block's
+// first cursor position and its sample offset at once (sums never carry).
+struct CursorF {
+  const u32* cur_blk;
+  const u32* blk_first;
+  const u64* iv_cum;
+  const u32* start;
+  const u32* end;
+  const u32* file;
+  u32* civ;
+  u64* cum;
+  u32* cfile;
+  u32* cstart;
+  __device__ u64 value(long long p) const {
+    const u32 b = cur_blk[p];
+    const u32 f0 = blk_first[b], f1 = blk_first[b + 1];
+    return ((u64)(f1 - f0) << 32) | (iv_cum[f1] - iv_cum[f0]);
+  }
+  __device__ void apply(long long p, u64 ex, u64) const {
+    const u32 b = cur_blk[p];
+    const u32 f0 = blk_first[b], f1 = blk_first[b + 1];
+    const u64 pos = ex >> 32;
+    u64 samp = ex & 0xffffffffull;
+    if (p == 0) cum[0] = 0;
+    for (u32 t = 0; t < f1 - f0; ++t) {
+      const u32 iv = f0 + t, a = start[iv];
+      civ[pos + t] = iv;
+      cfile[pos + t] = file[iv];
+      cstart[pos + t] = a;
+      samp += end[iv] - a;
+      cum[pos + t + 1] = samp;
+    }
+  }
+  __device__ void total(u64) const {}
+};
 
 __global__ void comp_total_kernel(long long K, const u32* key_blk_first, const u32* blk_first, const u64* iv_cum,
                                   u64* total) {
@@ -386,23 +398,13 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   MX_CUDA_TRY(ws_borrow(grp, s, WS_CGRP, B));
   MX_CUDA_TRY(ws_borrow(gid, s, WS_CGID, B));
   MX_CUDA_TRY(g->cur_blk.alloc(B, s));
-  MX_CUDA_TRY(g->civ.alloc(I, s));
-  MX_CUDA_TRY(g->ccum.alloc(I + 1, s));
-  MX_CUDA_TRY(g->cfile.alloc(I, s));
-  MX_CUDA_TRY(g->cstart.alloc(I, s));
   {
     MxPhase ph2("cursor_shuffle", s);
     // keys with <= cap blocks keep their scratch in shared memory (6 B per
-    // block); larger keys use the u32 global scratch
-    const long long mkb = ix->max_key_blocks;
-    const int cap = (int)std::min<long long>((mkb + 63) / 64 * 64, CS_SMEM_CAP);
-    DevBuf<u32> fj, ft, fl;
-    const long long gn = mkb > cap ? B : 1;
-    MX_CUDA_TRY(ws_borrow(fj, s, WS_FYJ, gn));
-    MX_CUDA_TRY(ws_borrow(ft, s, WS_FYTOP, gn));
-    MX_CUDA_TRY(ws_borrow(fl, s, WS_FYLINK, gn));
-    const size_t dyn = (size_t)CS_MT_WORDS * 4 + (size_t)cap * 6;
-    MX_CUDA_TRY(mx_smem_attr(cursor_shuffle_kernel, dyn));
+    // block); larger keys use the u32 global scratch. cap is also bounded so
+    // that every key's CTA can be resident at once (at 1B samples a key has
+    // ~7,500 blocks: shared scratch for all of them would leave 4 CTAs per
+    // SM and ~3.4 waves of serial per-key draws; global scratch keeps one)
     static thread_local std::map<size_t, int> occ;  // smem -> resident CTAs per SM
     static thread_local int n_sm = 0;
     if (!n_sm) {
@@ -410,16 +412,40 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
       MX_CUDA_TRY(cudaGetDevice(&dev));
       MX_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
     }
+    const long long mkb = ix->max_key_blocks;
+    const long long need = std::min<long long>(16, (K + n_sm - 1) / n_sm);  // CTAs per SM for one wave
+    const long long budget = 227 * 1024 / std::max(need, 1ll) - 1024 - 4 * CS_MT_WORDS;
+    const int cap_fit = (int)std::max<long long>(64, budget / 6 / 64 * 64);
+    const int cap = (int)std::min<long long>(std::min<long long>((mkb + 63) / 64 * 64, CS_SMEM_CAP), cap_fit);
+    DevBuf<u32> fj, ft, fl;
+    const long long gn = mkb > cap ? B : 1;
+    MX_CUDA_TRY(ws_borrow(fj, s, WS_FYJ, gn));
+    MX_CUDA_TRY(ws_borrow(ft, s, WS_FYTOP, gn));
+    MX_CUDA_TRY(ws_borrow(fl, s, WS_FYLINK, gn));
+    const size_t dyn = (size_t)CS_MT_WORDS * 4 + (size_t)cap * 6;
+    MX_CUDA_TRY(mx_smem_attr(cursor_shuffle_kernel, dyn));
     int& per_sm = occ[dyn];
     if (!per_sm)
       MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cursor_shuffle_kernel, CS_THREADS, dyn));
     const long long blocks = std::min<long long>(K, (long long)std::max(per_sm, 1) * n_sm);
     cursor_shuffle_kernel<<<(unsigned)blocks, CS_THREADS, dyn, s>>>(
         K, ix->key_blk_first.p, ix->blk_file.p, ix->file_ds.p, states.p, grp.p, gid.p, g->cur_blk.p, cap, fj.p, ft.p,
-        fl.p,
-        LayoutOut{ix->blk_first.p, ix->iv_cum.p, ix->iv_start.p, ix->iv_end.p, ix->iv_file.p, g->civ.p, g->ccum.p,
-                  g->cfile.p, g->cstart.p});
+        fl.p);
     mx_count_launch();
+  }
+  MX_CUDA_TRY(g->civ.alloc(I, s));
+  MX_CUDA_TRY(g->ccum.alloc(I + 1, s));
+  MX_CUDA_TRY(g->cfile.alloc(I, s));
+  MX_CUDA_TRY(g->cstart.alloc(I, s));
+  if (ix->indexed_samples < (1ll << 32) && I < (1ll << 31)) {  // resolved sizes (ix_resolve)
+    if (int rc = gs_run(B, CursorF{g->cur_blk.p, ix->blk_first.p, ix->iv_cum.p, ix->iv_start.p, ix->iv_end.p,
+                                   ix->iv_file.p, g->civ.p, g->ccum.p, g->cfile.p, g->cstart.p}, s))
+      return rc;
+  } else {  // >= 2^32 samples: positions first, then the 64-bit sample prefix
+    if (int rc = gs_run(B, CursorIvF{g->cur_blk.p, ix->blk_first.p, g->civ.p}, s)) return rc;
+    if (int rc = gs_run(I, CumPermF{g->civ.p, ix->iv_start.p, ix->iv_end.p, g->ccum.p, ix->iv_file.p, g->cfile.p,
+                                     g->cstart.p}, s))
+      return rc;
   }
   if (int rc = gen_local_lists(g, s)) return rc;  // sharded index: this rank's cursor positions
   MX_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_order, 0));
