@@ -123,7 +123,7 @@ __device__ __forceinline__ const u32* mt_state_of(const u32* states, long long k
 // samples (measured 0.4 ms per key there, clock64). Keys with several datasets
 // (the dataset-order shuffle first, then every dataset's blocks from the
 // same stream) run the warp form (cursor_key_shuffle) on warp 0. Draw /
-// bucket scratch: 16-bit entries in shared memory (6 B per block) for keys
+// bucket scratch: 16-bit entries in shared memory (4 B per block) for keys
 // with <= cap blocks, else u32 global scratch at the key's block offset.
 constexpr int CS_THREADS = 64;  // 16 CTAs per SM: every cfg2 key resident at once
 constexpr int CS_MT_WORDS = 2 * MT_N;
@@ -131,10 +131,10 @@ constexpr int CS_SMEM_CAP = 16000;
 
 template <typename IT>
 __device__ void cursor_key_shuffle(WarpMT& mt, u32 b0, int nb, int G, const u32* grp, u32* gid, u32* cur_blk, IT* j,
-                                   IT* top, IT* link) {
+                                   IT* top) {
   // dataset order (one stream for the whole key)
   mt.draws(G, j);
-  fy_apply(G, j, top, link, [&](int i, u32 v) { gid[b0 + i] = v; });
+  fy_apply(G, j, top, [&](int i, u32 v) { gid[b0 + i] = v; });
   // every dataset's draws in the shuffled dataset order, then one apply each
   int pos = 0;
   for (int g = 0; g < G; ++g) {
@@ -151,22 +151,20 @@ __device__ void cursor_key_shuffle(WarpMT& mt, u32 b0, int nb, int G, const u32*
     const int e = gi + 1 < (u32)G ? (int)grp[b0 + gi + 1] : nb;
     u32* dst = cur_blk + b0 + pos;
     const u32 base = b0 + (u32)s;
-    fy_apply(e - s, j + pos, top + pos, link + pos, [&](int i, u32 v) { dst[i] = base + v; });
+    fy_apply(e - s, j + pos, top + pos, [&](int i, u32 v) { dst[i] = base + v; });
     pos += e - s;
   }
 }
 
 __global__ void __launch_bounds__(CS_THREADS)
 cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file, const int32_t* file_ds,
-                      const u32* states, u32* grp, u32* gid, u32* cur_blk, int cap, u32* g_j, u32* g_top,
-                      u32* g_link) {
+                      const u32* states, u32* grp, u32* gid, u32* cur_blk, int cap, u32* g_j, u32* g_top) {
   extern __shared__ __align__(16) u32 cs_dyn[];
   __shared__ int s_G;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   u32* mt_s = cs_dyn;
   unsigned short* s_j = reinterpret_cast<unsigned short*>(cs_dyn + CS_MT_WORDS);
   unsigned short* s_top = s_j + cap;
-  unsigned short* s_link = s_top + cap;
   for (long long k = blockIdx.x; k < K; k += gridDim.x) {
     const u32 b0 = key_blk_first[k], b1 = key_blk_first[k + 1];
     const int nb = (int)(b1 - b0);
@@ -203,22 +201,22 @@ cursor_shuffle_kernel(long long K, const u32* key_blk_first, const u32* blk_file
       if (G == 1) {
         if (in_smem) {
           mt.draws(nb, s_j);
-          fy_lists(nb, s_j, s_top, s_link);
+          fy_lists(nb, s_j, s_top);
         } else {
           mt.draws(nb, g_j + b0);
-          fy_lists(nb, g_j + b0, g_top + b0, g_link + b0);
+          fy_lists(nb, g_j + b0, g_top + b0);
         }
       } else if (in_smem) {
-        cursor_key_shuffle<unsigned short>(mt, b0, nb, G, grp, gid, cur_blk, s_j, s_top, s_link);
+        cursor_key_shuffle<unsigned short>(mt, b0, nb, G, grp, gid, cur_blk, s_j, s_top);
       } else {
-        cursor_key_shuffle<u32>(mt, b0, nb, G, grp, gid, cur_blk, g_j + b0, g_top + b0, g_link + b0);
+        cursor_key_shuffle<u32>(mt, b0, nb, G, grp, gid, cur_blk, g_j + b0, g_top + b0);
       }
     }
     __syncthreads();
     if (G == 1) {
       auto out = [&](int i, u32 v) { cur_blk[b0 + i] = b0 + v; };
-      if (in_smem) fy_resolve(nb, s_j, s_top, s_link, tid, CS_THREADS, out);
-      else fy_resolve(nb, g_j + b0, g_top + b0, g_link + b0, tid, CS_THREADS, out);
+      if (in_smem) fy_resolve(nb, s_j, s_top, tid, CS_THREADS, out);
+      else fy_resolve(nb, g_j + b0, g_top + b0, tid, CS_THREADS, out);
     }
     __syncthreads();
   }
@@ -315,8 +313,8 @@ __global__ void comp_total_kernel(long long K, const u32* key_blk_first, const u
 // scratch in shared memory up to CO_SMEM ranks, else u32 global scratch
 constexpr int CO_SMEM = 16384;
 
-__global__ void __launch_bounds__(32) component_order_kernel(long long K, u64 seed, u32* order, u32* g_j, u32* g_top,
-                                                           u32* g_link) {
+__global__ void __launch_bounds__(32) component_order_kernel(long long K, u64 seed, u32* order, u32* g_j,
+                                                           u32* g_top) {
   extern __shared__ __align__(16) u32 co_dyn[];
   const int n = (int)K, lane = threadIdx.x;
   WarpMT mt{co_dyn, co_dyn + MT_N, MT_N};
@@ -328,10 +326,10 @@ __global__ void __launch_bounds__(32) component_order_kernel(long long K, u64 se
   if (n <= CO_SMEM) {
     unsigned short* s_j = reinterpret_cast<unsigned short*>(co_dyn + CS_MT_WORDS);
     mt.draws(n, s_j);
-    fy_apply(n, s_j, s_j + n, s_j + 2 * n, out);
+    fy_apply(n, s_j, s_j + n, out);
   } else {
     mt.draws(n, g_j);
-    fy_apply(n, g_j, g_top, g_link, out);
+    fy_apply(n, g_j, g_top, out);
   }
 }
 
@@ -359,14 +357,13 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   // per-key seeds and cursor shuffles
   MX_CUDA_TRY(cudaStreamWaitEvent(g->ostream, g->ev_tot, 0));
   {
-    DevBuf<u32> fj, ft, fl;  // global scratch only beyond CO_SMEM ranks
+    DevBuf<u32> fj, ft;  // global scratch only beyond CO_SMEM ranks
     const long long gn = K > CO_SMEM ? K : 1;
     MX_CUDA_TRY(ws_borrow(fj, g->ostream, WS_FYJ, gn));
     MX_CUDA_TRY(ws_borrow(ft, g->ostream, WS_FYTOP, gn));
-    MX_CUDA_TRY(ws_borrow(fl, g->ostream, WS_FYLINK, gn));
-    const size_t dyn = sizeof(u32) * CS_MT_WORDS + (K <= CO_SMEM ? 6 * (size_t)K : 0);
+    const size_t dyn = sizeof(u32) * CS_MT_WORDS + (K <= CO_SMEM ? 4 * (size_t)K : 0);
     MX_CUDA_TRY(mx_smem_attr(component_order_kernel, dyn));
-    component_order_kernel<<<1, 32, dyn, g->ostream>>>(K, order_seed, g->comp_order.p, fj.p, ft.p, fl.p);
+    component_order_kernel<<<1, 32, dyn, g->ostream>>>(K, order_seed, g->comp_order.p, fj.p, ft.p);
     mx_count_launch();
   }
   MX_CUDA_TRY(cudaEventRecord(g->ev_order, g->ostream));
@@ -400,11 +397,8 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
   MX_CUDA_TRY(g->cur_blk.alloc(B, s));
   {
     MxPhase ph2("cursor_shuffle", s);
-    // keys with <= cap blocks keep their scratch in shared memory (6 B per
-    // block); larger keys use the u32 global scratch. cap is also bounded so
-    // that every key's CTA can be resident at once (at 1B samples a key has
-    // ~7,500 blocks: shared scratch for all of them would leave 4 CTAs per
-    // SM and ~3.4 waves of serial per-key draws; global scratch keeps one)
+    // keys with <= cap blocks keep their scratch in shared memory (4 B per
+    // block); larger keys use the u32 global scratch
     static thread_local std::map<size_t, int> occ;  // smem -> resident CTAs per SM
     static thread_local int n_sm = 0;
     if (!n_sm) {
@@ -415,22 +409,26 @@ int cursor_build(IndexData* ix, const uint8_t* cursor_prefix, int prefix_len, un
     const long long mkb = ix->max_key_blocks;
     const long long need = std::min<long long>(16, (K + n_sm - 1) / n_sm);  // CTAs per SM for one wave
     const long long budget = 227 * 1024 / std::max(need, 1ll) - 1024 - 4 * CS_MT_WORDS;
-    const int cap_fit = (int)std::max<long long>(64, budget / 6 / 64 * 64);
-    const int cap = (int)std::min<long long>(std::min<long long>((mkb + 63) / 64 * 64, CS_SMEM_CAP), cap_fit);
-    DevBuf<u32> fj, ft, fl;
+    const int cap_fit = (int)std::max<long long>(64, budget / 4 / 64 * 64);
+    // shared scratch for every key unless that needs more than 3 waves of
+    // keys (a key in global scratch runs ~3.5x longer: 1B, clock64)
+    const int cap_full = (int)std::min<long long>((mkb + 63) / 64 * 64, CS_SMEM_CAP);
+    const long long per_sm_full =
+        std::max<long long>(1, std::min<long long>(16, 227 * 1024 / ((long long)CS_MT_WORDS * 4 + 4ll * cap_full + 1024)));
+    const long long waves = (K + per_sm_full * n_sm - 1) / (per_sm_full * n_sm);
+    const int cap = waves <= 3 ? cap_full : std::min(cap_full, cap_fit);
+    DevBuf<u32> fj, ft;
     const long long gn = mkb > cap ? B : 1;
     MX_CUDA_TRY(ws_borrow(fj, s, WS_FYJ, gn));
     MX_CUDA_TRY(ws_borrow(ft, s, WS_FYTOP, gn));
-    MX_CUDA_TRY(ws_borrow(fl, s, WS_FYLINK, gn));
-    const size_t dyn = (size_t)CS_MT_WORDS * 4 + (size_t)cap * 6;
+    const size_t dyn = (size_t)CS_MT_WORDS * 4 + (size_t)cap * 4;
     MX_CUDA_TRY(mx_smem_attr(cursor_shuffle_kernel, dyn));
     int& per_sm = occ[dyn];
     if (!per_sm)
       MX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cursor_shuffle_kernel, CS_THREADS, dyn));
     const long long blocks = std::min<long long>(K, (long long)std::max(per_sm, 1) * n_sm);
     cursor_shuffle_kernel<<<(unsigned)blocks, CS_THREADS, dyn, s>>>(
-        K, ix->key_blk_first.p, ix->blk_file.p, ix->file_ds.p, states.p, grp.p, gid.p, g->cur_blk.p, cap, fj.p, ft.p,
-        fl.p);
+        K, ix->key_blk_first.p, ix->blk_file.p, ix->file_ds.p, states.p, grp.p, gid.p, g->cur_blk.p, cap, fj.p, ft.p);
     mx_count_launch();
   }
   MX_CUDA_TRY(g->civ.alloc(I, s));

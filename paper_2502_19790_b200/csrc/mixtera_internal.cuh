@@ -78,7 +78,7 @@ struct DevBuf {
 // a view must never outlive the call that borrowed it.
 enum WsSlot { WS_TCNT, WS_TOPEN, WS_THEAD, WS_DEFER, WS_RK, WS_RF, WS_RS, WS_RE, WS_SEGFA, WS_SCR64, WS_ERR,
               WS_HIST, WS_DTOT, WS_TOFF, WS_GSAGG, WS_CPRE, WS_CSEED, WS_CGRP, WS_CGID,
-              WS_FYJ, WS_FYTOP, WS_FYLINK,
+              WS_FYJ, WS_FYTOP,
               WS_EPRE, WS_EOFF, WS_EFLAG, WS_ELIST, WS_ELCNT, WS_ECPO, WS_EMCNT, WS_EBIG,  // emission temporaries
               WS_NBL, WS_NBC, WS_NWL, WS_NWC,  // cursor / component-order shuffle scratch
               WS_GEN,            // + GenData scratch slot (24 of them)

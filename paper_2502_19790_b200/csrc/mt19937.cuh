@@ -194,29 +194,35 @@ struct WarpMT {
 //   out[i] = nxt_i exists ? V(nxt_i) : j_i,  nxt_i = min{s > i : j_s = j_i}
 //   out[0] = head(0) exists ? V(head(0)) : 0
 // Every bucket is built as an ASCENDING linked list (top[p] = its smallest
-// step, link[s] = the next larger step of s's bucket) by inserting the steps
-// from n-1 down, 32 at a time; steps of one batch that share a bucket are
-// ordered by __match_any_sync. Then nxt_i = link[i] and head(p) = top[p], or
-// link[p] when top[p] == p; every element's chain is followed independently
-// (mean length ~1, max ~log n). IT = u16 in the shared-memory form
-// (n < 65535), u32 otherwise; the all-ones IT marks "none".
-// phase 1 (one warp): the ascending bucket lists of steps 1..n-1
+// step, link(s) = the next larger step of s's bucket, stored over the draw
+// j_s) by inserting the steps from n-1 down, 32 at a time; steps of one batch
+// that share a bucket are ordered by __match_any_sync. Then nxt_i = link(i)
+// and head(p) = top[p], or link(p) when top[p] == p; every element's chain
+// is followed independently (mean length ~1, max ~log n). 4 B of scratch per
+// element as u16 (n <= 2^15, shared memory), u32 otherwise; the all-ones IT
+// marks "none".
+// phase 1 (one warp): the ascending bucket lists of steps 1..n-1, built in
+// place of the draws: jl[s] holds j_s on entry and, on exit, the next larger
+// step of s's bucket, or FLAG | j_s when s is its bucket's largest step (the
+// top bit of IT is free: n <= 2^15 for u16, 2^31 for u32). Each batch reads
+// its 32 draws before it overwrites them; later batches read smaller steps.
 template <typename IT>
-__device__ void fy_lists(int n, const IT* j, IT* top, IT* link) {
+__device__ void fy_lists(int n, IT* jl, IT* top) {
   const int lane = threadIdx.x & 31;
-  const uint32_t none = (uint32_t)(IT)~0u;
+  const uint32_t none = (uint32_t)(IT)~0u, flag = (none >> 1) + 1u;
   for (int p = lane; p < n; p += 32) top[p] = (IT)none;
   __syncwarp();
   for (int hi = n - 1; hi >= 1; hi -= 32) {
     const int s = hi - lane;  // descending with the lane
     const bool ok = s >= 1;
-    const uint32_t js = ok ? (uint32_t)j[s] : 0u;
+    const uint32_t js = ok ? (uint32_t)jl[s] : 0u;
     const uint32_t m = __match_any_sync(0xffffffffu, ok ? js : 0x80000000u | (uint32_t)lane);
     const uint32_t old = ok ? (uint32_t)top[js] : none;
     __syncwarp();
     if (ok) {
       const uint32_t lower = m & ((1u << lane) - 1u);  // same bucket, larger steps
-      link[s] = (IT)(lower ? (uint32_t)(hi - (31 - __clz(lower))) : old);
+      const uint32_t nx = lower ? (uint32_t)(hi - (31 - __clz(lower))) : old;
+      jl[s] = (IT)(nx != none ? nx : (flag | js));
       if ((m >> lane) == 1u) top[js] = (IT)s;  // highest lane = smallest step
     }
     __syncwarp();
@@ -225,20 +231,28 @@ __device__ void fy_lists(int n, const IT* j, IT* top, IT* link) {
 
 // phase 2 (any number of threads, element-parallel): every output position
 template <typename IT, typename F>
-__device__ void fy_resolve(int n, const IT* j, const IT* top, const IT* link, int tid, int stride, F out) {
-  const uint32_t none = (uint32_t)(IT)~0u;
+__device__ void fy_resolve(int n, const IT* jl, const IT* top, int tid, int stride, F out) {
+  const uint32_t none = (uint32_t)(IT)~0u, flag = (none >> 1) + 1u;
+  auto nxt = [&](uint32_t s) -> uint32_t {
+    const uint32_t v = jl[s];
+    return (v & flag) ? none : v;
+  };
   auto head = [&](uint32_t p) -> uint32_t {
     const uint32_t t = top[p];
-    return t == p ? (uint32_t)link[p] : t;
+    return t == p ? nxt(p) : t;
   };
   for (int i = tid; i < n; i += stride) {
-    uint32_t h, last;
+    uint32_t h, last = 0;
     if (i == 0) {
       h = head(0);
-      last = 0;
     } else {
-      h = link[i];
-      last = j[i];
+      const uint32_t v = jl[i];
+      if (v & flag) {
+        h = none;
+        last = v & ~flag;  // no later step wrote position j_i: its original value
+      } else {
+        h = v;
+      }
     }
     while (h != none) {
       last = h;
@@ -250,10 +264,10 @@ __device__ void fy_resolve(int n, const IT* j, const IT* top, const IT* link, in
 
 // the whole apply by one warp
 template <typename IT, typename F>
-__device__ void fy_apply(int n, const IT* j, IT* top, IT* link, F out) {
-  fy_lists(n, j, top, link);
+__device__ void fy_apply(int n, IT* jl, IT* top, F out) {
+  fy_lists(n, jl, top);
   __syncwarp();
-  fy_resolve(n, j, top, link, threadIdx.x & 31, 32, out);
+  fy_resolve(n, jl, top, threadIdx.x & 31, 32, out);
   __syncwarp();
 }
 
